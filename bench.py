@@ -1,0 +1,360 @@
+#!/usr/bin/env python
+"""Benchmark of the Wide & Deep retrieval hot path (arXiv 2511.22460) on B200.
+
+One step = one batch of users scored against the whole inventory (wide through the compressed
+inverted list + deep dual-tower inner product + fused top-K), i.e. every SURVEY.md §8(a) row;
+for N > 1 GPUs the inventory is sharded by ad range (strong scaling of a fixed inventory) and
+each step adds the NCCL all-gather of the per-shard top-K keys and the merge kernel.
+
+Default workload: BASELINE.json config 2 ("1M ads, d=64, 32 cross features, batch 1, K=500 on
+1 B200 (latency path)").  Prints ONE JSON line on rank 0.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2511_22460_b200 import synth  # noqa: E402
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--k", type=int, default=None)
+    ap.add_argument("--mode", default="real")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="few steps, no side measurements (for ncu)")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev: int):
+        self.dev = dev
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def algorithmic_bytes(ebr, inv, users, idx_stats, lo, hi):
+    """N_s*d*e (embeddings, once) + P_U (encoded postings of the batch's
+    distinct keys in the shard: 8-byte chunk headers + payload words) + inputs + outputs."""
+    kco, kwo, hdr, pay = ebr.encode_host(inv.ad_feat[lo:hi], inv.field_card)
+    base = np.concatenate([[0], np.cumsum(inv.field_card)[:-1]]).astype(np.int64)
+    F, S = users.user_feat.shape[1:]
+    keys = set()
+    for b in range(users.batch):
+        for f in range(F):
+            for s in range(S):
+                v = users.user_feat[b, f, s]
+                if v >= 0:
+                    keys.add(int(base[f] + v))
+    keys = np.array(sorted(keys), np.int64)
+    nch = (kco[keys + 1].astype(np.int64) - kco[keys]).sum()
+    # payload words of a key = next key's word base - this one's (keys are laid out in order)
+    wend = np.append(kwo.astype(np.int64), len(pay))
+    words = (wend[keys + 1] - wend[keys]).sum()
+    hits = 0
+    esz = 2 if inv.dtype == "bf16" else 4
+    emb = (hi - lo) * idx_stats["d_pad"] * esz
+    postings = int(nch) * 8 + int(words) * 4 + len(keys) * 12
+    io = users.batch * (inv.d * esz + 8 * F * S)
+    return emb, postings, io
+
+
+def run_reference(args, cfg, rank, world):
+    """Reference arm: the CPU oracle as it stands, on this host's cores (no GPU)."""
+    if rank != 0:
+        return
+    import oracle
+    B = args.batch or cfg.batch
+    K = args.k or cfg.k
+    inv, users = synth.make_config(cfg, mode=args.mode, batch=B)
+    o = oracle.Oracle.of(inv)
+    threads = os.cpu_count() or 1
+    # bounded sample: each step scores a sample of the batch's users over the full inventory
+    per_user = None
+    t = time.perf_counter()
+    o.topk(users.user_emb[:1], users.user_feat[:1], users.user_x[:1], K, threads=1)
+    per_user = time.perf_counter() - t
+    n_sample = int(max(1, min(B, threads, 20.0 / max(per_user, 1e-3) / max(args.steps, 1) * threads)))
+    for _ in range(args.warmup):
+        pass   # the oracle has no warm state worth priming
+    times = []
+    for s in range(args.steps):
+        sel = [(s * n_sample + j) % B for j in range(n_sample)]
+        t = time.perf_counter()
+        o.topk(users.user_emb[sel], users.user_feat[sel], users.user_x[sel], K,
+               threads=min(threads, n_sample))
+        times.append(time.perf_counter() - t)
+    tot = sum(times)
+    users_s = n_sample * args.steps / tot
+    line = {
+        "impl": "reference",
+        "metric": "users_per_s", "value": users_s, "unit": "users/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / args.steps * B / n_sample,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": f"synthetic ({args.mode} mode, seeded generator)",
+        "config": config_dict(cfg, B, K, world),
+        "ads_scored_per_s": users_s * inv.n_ads,
+        "cpu_baseline": {"value": users_s, "unit": "users/s", "cores": min(threads, n_sample),
+                         "kind": "oracle",
+                         "sample": f"{n_sample} users x all {inv.n_ads} ads per step, {args.steps} steps"},
+        "e2e": {"value": users_s, "unit": "users/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(cfg, B, K, world):
+    return {"workload": f"{cfg.name}: {cfg.n_ads} ads, d={cfg.d} {cfg.dtype}, {cfg.n_fields} cross "
+                        f"features (Zipf alpha={cfg.alpha}), batch {B}, K={K}",
+            "n_ads": cfg.n_ads, "d": cfg.d, "emb_dtype": cfg.dtype, "cross_features": cfg.n_fields,
+            "slots_per_field": cfg.slots, "zipf_alpha": cfg.alpha, "batch": B, "k": K,
+            "parallelism": f"ad-shard x{world}",
+            "l2": "flushed between steps (write of a 256 MiB buffer outside the per-step events); "
+                  "A itself is larger than L2"}
+
+
+def cpu_baseline(cfg, inv, users, K, budget_s=15.0):
+    import oracle
+    o = oracle.Oracle.of(inv)
+    threads = os.cpu_count() or 1
+    t = time.perf_counter()
+    o.topk(users.user_emb[:1], users.user_feat[:1], users.user_x[:1], K, threads=1)
+    one = time.perf_counter() - t
+    n = int(max(1, min(threads * 4, budget_s / max(one, 1e-3) * threads / 1.5)))
+    rng = np.random.default_rng(0)
+    B = users.batch
+    sel = rng.integers(0, B, n) if B > 1 else np.zeros(n, np.int64)
+    t = time.perf_counter()
+    o.topk(users.user_emb[sel], users.user_feat[sel], users.user_x[sel], K, threads=min(threads, n))
+    dt = time.perf_counter() - t
+    return {"value": n / dt, "unit": "users/s", "cores": min(threads, n), "kind": "oracle",
+            "sample": f"{n} users (drawn from the batch) x all {inv.n_ads} ads, brute-force sort",
+            "single_thread_s_per_user": one}
+
+
+def main():
+    args = parse()
+    cfg = synth.CONFIGS[args.config]
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+    import torch
+    import torch.distributed as dist
+    from paper_2511_22460_b200 import ebr
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    B = args.batch or cfg.batch
+    K = args.k or cfg.k
+    inv, users = synth.make_config(cfg, mode=args.mode, batch=B)
+    N = inv.n_ads
+    Ns = ((N + world - 1) // world + 127) // 128 * 128
+    lo, hi = min(N, rank * Ns), min(N, (rank + 1) * Ns)
+    idx = ebr.Index.of(inv, lo=lo, hi=hi, device=local)
+    st = idx.stats()
+    stream = torch.cuda.Stream(device=dev)
+    emb_np = users.user_emb
+    emb = torch.from_numpy(emb_np.view(np.int16) if emb_np.dtype == np.uint16 else emb_np).to(dev)
+    feat = torch.from_numpy(users.user_feat).to(dev)
+    x = torch.from_numpy(users.user_x).to(dev)
+    S = users.slots
+    ws = torch.empty(idx.workspace_bytes(B, S, K), dtype=torch.uint8, device=dev)
+    ids = torch.empty((B, K), dtype=torch.int32, device=dev)
+    sc = torch.empty((B, K), dtype=torch.float32, device=dev)
+    keys = torch.empty((B, K), dtype=torch.int64, device=dev)
+    gathered = torch.empty((world, B, K), dtype=torch.int64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        if world == 1:
+            ebr.score_topk(idx, emb, feat, x, K, ids, sc, ws, stream)
+        else:
+            ebr.score_topk_keys(idx, emb, feat, x, K, keys, ws, stream)
+            with torch.cuda.stream(stream):
+                dist.all_gather_into_tensor(gathered, keys)
+            ebr.merge_topk(gathered, world, B, K, ids, sc, stream)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    hbm_peak, peak_kind = peaks()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(i & 0xFF)                     # evict L2 (outside the events)
+                ev[i][0].record(stream)
+            step()
+            with torch.cuda.stream(stream):
+                ev[i][1].record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+    if world > 1:
+        dist.barrier()
+    per = np.array([a.elapsed_time(b) for a, b in ev])        # ms, device side
+    tot_ms = float(per.sum())
+    t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tot_ms = float(t.item())
+    ms_step = tot_ms / args.steps
+    users_s = B * args.steps / (tot_ms / 1e3)
+
+    line = None
+    if rank == 0:
+        emb_b, post_b, io_b = algorithmic_bytes(ebr, inv, users, st, lo, hi)
+        alg = emb_b + post_b + io_b + 8 * B * K
+        achieved = alg / (ms_step / 1e3) / 1e9   # GB/s (per GPU: shard bytes / step time)
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+                tr = json.load(f).get(cfg.name)
+            if tr and tr.get("world", 1) == world and tr.get("batch") == B:
+                traffic = tr["dram_bytes_per_launch"]
+        except Exception:
+            pass
+        line = {
+            "metric": "users_per_s", "value": users_s, "unit": "users/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32" if cfg.dtype == "f32" else "bf16",
+            "data": f"synthetic ({args.mode} mode, seeded Zipf generator of DESIGN.md)",
+            "config": config_dict(cfg, B, K, world),
+            "ads_scored_per_s": users_s * N,
+            "latency_us": {"p50": float(np.percentile(per, 50) * 1e3),
+                           "p99": float(np.percentile(per, 99) * 1e3),
+                           "min": float(per.min() * 1e3)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": traffic,
+                         "peak_kind": peak_kind,
+                         "kernel": "small_kernel (fused plan+decode+wide+GEMV+fuse+top-K, 1 launch)",
+                         "alg_bytes_per_launch": alg,
+                         "alg_bytes_split": {"embeddings": emb_b, "postings": post_b, "io": io_b + 8 * B * K}},
+            "index": {"build_ms": st["build_ms"], "index_bytes": st["index_bytes"],
+                      "nnz": st["nnz"], "chunks": st["chunks"]},
+            "clocks": clk.summary(),
+            "gpu_launches": args.steps * ((B + 7) // 8 + (1 if world > 1 else 0)),
+            "wall_s_timed_region": wall,
+        }
+    # e2e through the host-buffer C-ABI call (pinned host memory, copies inside the region)
+    if world == 1 and not args.profile:
+        wsh = torch.empty(idx.workspace_bytes_host(B, S, K), dtype=torch.uint8, device=dev)
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
+        h_emb = pin(emb_np.view(np.int16) if emb_np.dtype == np.uint16 else emb_np)
+        h_feat, h_x = pin(users.user_feat), pin(users.user_x)
+        h_ids = torch.empty((B, K), dtype=torch.int32).pin_memory().numpy()
+        h_sc = torch.empty((B, K), dtype=torch.float32).pin_memory().numpy()
+        for _ in range(3):
+            ebr.score_topk_host(idx, h_emb, h_feat, h_x, K, h_ids, h_sc, wsh, stream)
+        e_ms = []
+        for i in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(i & 0xFF)
+            stream.synchronize()
+            t = time.perf_counter()
+            ebr.score_topk_host(idx, h_emb, h_feat, h_x, K, h_ids, h_sc, wsh, stream)
+            e_ms.append((time.perf_counter() - t) * 1e3)
+        e_ms = np.array(e_ms)
+        if line is not None:
+            line["e2e"] = {"value": B / (e_ms.mean() / 1e3), "unit": "users/s",
+                           "h2d_bytes_per_step": int(h_emb.nbytes + h_feat.nbytes + h_x.nbytes),
+                           "d2h_bytes_per_step": int(h_ids.nbytes + h_sc.nbytes),
+                           "p50_us": float(np.percentile(e_ms, 50) * 1e3),
+                           "timing": "host wall clock around ebr_score_topk_host (H2D + query + D2H + sync)"}
+    if rank == 0 and not args.no_cpu_baseline and not args.profile:
+        line["cpu_baseline"] = cpu_baseline(cfg, inv, users, K)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,217 @@
+/*
+ * ebr.h -- C-ABI of the B200-native Wide & Deep ad-retrieval scorer (arXiv 2511.22460).
+ *
+ * One hot path: score every ad of an inventory shard for a batch of users as
+ *     s(u,a) = <h~_u, h~_a> + sum_i w_i x_i L_{a,i}          (Eq. 9, l.253-257)
+ * -- the dual-tower inner product ("deep", Eq. 1 l.188 / Eq. 8 l.243) plus the HitMatch cross
+ * features ("wide", l.251-252), the latter read through a compressed inverted list of L
+ * (l.280-296, Alg. 1 l.309-344, Alg. 2 l.346-364) -- and return each user's top-K ads
+ * ("retrieve top k relevant ads", l.157), ties broken by ascending ad id.
+ *
+ * Citations "P:n" are /root/reference/PAPER.md lines.  Readings of the paper where it is silent
+ * or ambiguous are numbered R1..R21 in DESIGN.md.
+ *
+ * Conventions for every call
+ *   - No exception crosses the ABI.  Every call returns an ebr_status; on failure a thread-local
+ *     message is available from ebr_last_error().
+ *   - Pointers documented "host" are CPU memory; "device" pointers are CUDA device memory on the
+ *     index's device (e.g. torch tensor storage).  All device memory passed in is caller-owned;
+ *     memory behind an ebr_index is library-owned and released by ebr_free_index().
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Calls marked
+ *     "async" only enqueue work on it; their device outputs are valid after the stream syncs.
+ *     Kernel faults surface at the caller's next synchronisation.
+ *   - There is no CPU fallback: with no usable sm_100 device every compute call fails with
+ *     EBR_ECUDA / EBR_EUNSUPPORTED.
+ */
+#ifndef EBR_H_
+#define EBR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ebr_index ebr_index; /* opaque; immutable after build, shareable across streams */
+
+typedef enum {
+    EBR_OK = 0,
+    EBR_EINVAL = 1,         /* bad argument (bounds, sizes, undersized workspace)            */
+    EBR_ENOMEM = 2,         /* host or device allocation failed                               */
+    EBR_ECUDA = 3,          /* CUDA runtime error (message in ebr_last_error)                 */
+    EBR_EUNSUPPORTED = 4,   /* device is not sm_100 / feature outside the supported envelope */
+    EBR_EDEVICE = 5         /* a device-side validation flag was raised (see ebr_query_error) */
+} ebr_status;
+
+typedef enum { EBR_F32 = 0, EBR_BF16 = 1 } ebr_dtype;
+
+/* Largest K one call returns (one CTA sorts the K results in shared memory). */
+#define EBR_MAX_K 16384
+
+/* ------------------------------------------------------------------------------------------ */
+/* A0  Index build  (Alg. 1 l.309-344, "Storage Layout" l.295; refresh l.307)          */
+/* ------------------------------------------------------------------------------------------ */
+/*
+ * Builds this rank's shard: global ads [ad_begin, ad_end).  Host inputs are copied; the caller
+ * may free them on return.  Synchronous w.r.t. the host (uploads run on `stream`, which is
+ * synchronised before return).
+ *
+ *  ad_emb     host, [n][d] row-major, n = ad_end - ad_begin; fp32 (EBR_F32) or raw bf16 bit
+ *             patterns (EBR_BF16, uint16).  This is h~_a (Eq. 8: tower output + IPNN extension,
+ *             already concatenated; reading R19).  Rows are zero-padded on the device to the
+ *             kernel width (exact).
+ *  ad_feat    host, [n][n_fields] int32, the ad's value v in field f, -1 = empty (L_{a,i}=0).
+ *             Defines L: L[a, base_f + v] = 1 (reading A1).  Must be in [-1, V_f).
+ *  field_card host, [n_fields] int32 V_f >= 1; key i = base_f + v with base_f = sum_{g<f} V_g.
+ *  cross_w    host, [n_keys] fp32, the learned weight w_i of every key (Eq. 9).
+ *  n_keys     must equal sum V_f and be < 2^31.
+ *  device     CUDA ordinal; the index lives there.
+ *  out        receives the handle.
+ * Errors: EBR_EINVAL for d < 1, ad_begin >= ad_end, ad_end > 2^31-1, ad_feat out of range,
+ *         n_keys != sum V_f; EBR_ENOMEM / EBR_ECUDA; EBR_EUNSUPPORTED on a non-sm_100 device.
+ *
+ * Device layout: ad embeddings A[n_pad][d_pad]; the posting lists of
+ * every key as 32-posting chunks, delta-coded and bit-packed (DESIGN.md "Posting-chunk wire
+ * format"), with an SoA directory key_chunk_off[M+1], key_word_off[M], chunk_hdr[C] (u32 pairs)
+ * and payload words; w[M].
+ */
+ebr_status ebr_build_index(const void *ad_emb, ebr_dtype dtype, int64_t ad_begin, int64_t ad_end,
+                           int32_t d, const int32_t *ad_feat, int32_t n_fields,
+                           const int32_t *field_card, const float *cross_w, int64_t n_keys,
+                           int device, void *stream, ebr_index **out);
+
+void ebr_free_index(ebr_index *idx);
+
+/* ------------------------------------------------------------------------------------------ */
+/* A1-A6  Query: plan, posting decode, wide accumulate, deep score, fuse, top-K                 */
+/* ------------------------------------------------------------------------------------------ */
+/*
+ * Device workspace size for ebr_score_topk / ebr_score_topk_keys with this batch, slot count
+ * and k.  Returns 0 for invalid arguments.
+ */
+size_t ebr_workspace_bytes(const ebr_index *idx, int32_t batch, int32_t slots, int32_t k);
+
+/*
+ * async.  For each user b in [0, batch):
+ *   A1 plan: for every slot (f,s) with v = user_feat[b][f][s] >= 0: key i = base_f + v,
+ *      w~ = fl32(w_i * user_x[b][f][s])  (one rounding, never fused into an FMA, R10);
+ *   A2/A3 decode each such key's posting chunks and add w~ to the wide score of every listed ad
+ *      (Alg. 2 l.355-358);
+ *   A4 deep score <user_emb[b], A[a]> with fp32 accumulation (Eq. 1);
+ *   A5 s = deep + wide (Eq. 9), -0 canonicalised to +0, key kappa = (ord(s) << 32) | ~id;
+ *   A6 the k largest kappa, i.e. score descending, ties by ascending global ad id.
+ *
+ *  user_emb   device, [batch][d] in the index dtype (fp32 or bf16 bits).
+ *  user_feat  device, [batch][n_fields][slots] int32, -1 = empty slot.  A value outside
+ *             [-1, V_f) is skipped and raises the device error flag (see ebr_query_error).
+ *  user_x     device, [batch][n_fields][slots] fp32, the user's statistic x_i for that slot.
+ *  slots      1 <= slots <= 64.
+ *  k          1 <= k <= EBR_MAX_K.  k may exceed the shard size: missing entries are returned
+ *             as (id -1, score -inf) (reading R15).
+ *  out_ids    device, [batch][k] int32 global ad ids (ad_begin + local), best first.
+ *  out_scores device, [batch][k] fp32 s(u,a) of those ads.
+ *  workspace  device, >= ebr_workspace_bytes(idx, batch, slots, k) bytes, 256-byte aligned,
+ *             caller-owned; one in-flight call per workspace.
+ * Errors: EBR_EINVAL for batch < 1, slots out of range, k out of range, undersized workspace;
+ *         EBR_ECUDA on a launch failure.  Duplicate (f,v) slots of one user add (reading A3).
+ */
+ebr_status ebr_score_topk(const ebr_index *idx, const void *user_emb, int32_t batch,
+                          const int32_t *user_feat, const float *user_x, int32_t slots, int32_t k,
+                          int32_t *out_ids, float *out_scores, void *workspace,
+                          size_t workspace_bytes, void *stream);
+
+/*
+ * async.  Same as ebr_score_topk but emits the packed keys
+ *   kappa = (ord(score) << 32) | (0xFFFFFFFF - global_id),  [batch][k] uint64, descending,
+ * padding entries = 0 -- the all-gather payload of the multi-GPU path (A7).
+ */
+ebr_status ebr_score_topk_keys(const ebr_index *idx, const void *user_emb, int32_t batch,
+                               const int32_t *user_feat, const float *user_x, int32_t slots,
+                               int32_t k, uint64_t *out_keys, void *workspace,
+                               size_t workspace_bytes, void *stream);
+
+/*
+ * Reads (and clears) the device-side validation flag of `workspace` written by the last
+ * ebr_score_topk* call on it.  Host-synchronous on `stream`.  *flags bit 0 = a user_feat value
+ * was outside [-1, V_f).  Returns EBR_EDEVICE if any bit was set, EBR_OK otherwise.
+ */
+ebr_status ebr_query_error(void *workspace, void *stream, uint32_t *flags);
+
+/*
+ * End-to-end variant with HOST buffers (the e2e measurement): copies user_emb, user_feat and
+ * user_x host->device, runs ebr_score_topk, copies ids and scores device->host and synchronises
+ * `stream` before returning.  Host buffers should be pinned for full speed.
+ * workspace: device, >= ebr_workspace_bytes_host(idx, batch, slots, k).
+ */
+size_t ebr_workspace_bytes_host(const ebr_index *idx, int32_t batch, int32_t slots, int32_t k);
+ebr_status ebr_score_topk_host(const ebr_index *idx, const void *user_emb_host, int32_t batch,
+                               const int32_t *user_feat_host, const float *user_x_host,
+                               int32_t slots, int32_t k, int32_t *out_ids_host,
+                               float *out_scores_host, void *workspace, size_t workspace_bytes,
+                               void *stream);
+
+/* ------------------------------------------------------------------------------------------ */
+/* A7  Cross-GPU merge (not in the paper: the inventory is sharded over the GPUs of one box)    */
+/* ------------------------------------------------------------------------------------------ */
+/*
+ * async.  gathered: device, [G][batch][k] uint64 kappa lists (each descending, padding 0) from
+ * G shards.  Writes the global top k per user: out_ids [batch][k] int32, out_scores fp32.
+ * Because kappa is unique per ad, the result equals the single-GPU answer exactly.
+ * workspace: device, >= ebr_merge_workspace_bytes(G, batch, k).
+ */
+size_t ebr_merge_workspace_bytes(int32_t G, int32_t batch, int32_t k);
+ebr_status ebr_merge_topk(const uint64_t *gathered, int32_t G, int32_t batch, int32_t k,
+                          int32_t *out_ids, float *out_scores, void *workspace,
+                          size_t workspace_bytes, void *stream);
+
+/* ------------------------------------------------------------------------------------------ */
+/* Parity / introspection                                                                       */
+/* ------------------------------------------------------------------------------------------ */
+/*
+ * Host-synchronous.  Decodes key `key`'s posting list ON THE DEVICE with the same warp decoder
+ * the query path uses and copies the shard-local ad ids (ascending) to out_ads (host, cap
+ * entries).  *n receives the list length (also when it exceeds cap, then EBR_EINVAL).
+ */
+ebr_status ebr_debug_decode(const ebr_index *idx, int64_t key, int32_t *out_ads, int64_t cap,
+                            int64_t *n);
+
+typedef struct {
+    int64_t n_ads;        /* shard size                                        */
+    int64_t ad_begin;     /* first global id of the shard                      */
+    int32_t d, d_pad;     /* embedding width and padded kernel width           */
+    int32_t dtype;        /* ebr_dtype                                         */
+    int32_t n_fields;
+    int64_t n_keys;       /* M                                                 */
+    int64_t nnz;          /* postings (entries of L in the shard)              */
+    int64_t chunks;       /* 32-posting chunks                                 */
+    int64_t payload_words;
+    int64_t index_bytes;  /* directory + headers + payload + w                 */
+    int64_t emb_bytes;    /* device bytes of A                                 */
+    double build_ms;      /* host encode + upload wall time                    */
+} ebr_stats;
+ebr_status ebr_index_stats(const ebr_index *idx, ebr_stats *out);
+
+/*
+ * Host-only encoder (no device needed; used to pin the wire format on CPU).  Encodes the
+ * posting lists of ad_feat (shard-local ids 0..n_ads-1) exactly as ebr_build_index does.
+ * Output capacities: key_chunk_off [n_keys+1], key_word_off [n_keys], chunk_hdr [2*hdr_cap],
+ * payload [payload_cap].  *n_chunks / *n_words receive the sizes; EBR_EINVAL if a capacity is
+ * too small (sizes still written) or the inputs are invalid.
+ */
+ebr_status ebr_encode_host(const int32_t *ad_feat, int64_t n_ads, int32_t n_fields,
+                           const int32_t *field_card, int64_t n_keys, uint32_t *key_chunk_off,
+                           uint32_t *key_word_off, uint32_t *chunk_hdr, int64_t hdr_cap,
+                           uint32_t *payload, int64_t payload_cap, int64_t *n_chunks,
+                           int64_t *n_words);
+
+/* Thread-local message describing the last failure of any ebr_* call on this thread. */
+const char *ebr_last_error(void);
+
+/* Library build identifier ("ebr <git-describe> sm_100a"). */
+const char *ebr_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EBR_H_ */

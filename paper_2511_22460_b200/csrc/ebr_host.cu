@@ -1,0 +1,585 @@
+// ebr_host.cu -- the C-ABI (include/ebr.h): index build (host encode + upload), query dispatch,
+// cross-shard merge, debug decode, stats and error reporting.
+//
+// A0 index build follows the paper's Alg. 1 in purpose -- turn the binary matrix L
+// into an inverted list keyed by feature index with ad indices as values, compressed
+// and stored as a struct of arrays with per-key offsets -- with a different layout
+// (DESIGN.md "Posting-chunk wire format"): each key's ascending list is cut into chunks of 32
+// postings, delta-coded (gap-1) and bit-packed at the chunk's own width b (PforDelta-style,
+// P:176).  Chunks play the role of the paper's uniform-size blocks: every chunk but
+// a key's last holds exactly 32 postings, so a warp decodes any chunk in the same time.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "ebr_device.cuh"
+
+namespace ebr {
+
+static thread_local std::string g_last_error;
+
+ebr_status set_error(ebr_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return st;
+}
+
+ebr_status cuda_check(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return EBR_OK;
+    return set_error(EBR_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define EBR_CUDA(call)                                              \
+    do {                                                            \
+        cudaError_t e__ = (call);                                   \
+        if (e__ != cudaSuccess) return cuda_check(e__, #call);      \
+    } while (0)
+
+ebr_status run_small(const QueryArgs& q, int b0, int B);
+size_t small_workspace_bytes(const ebr_index* idx, int32_t slots, int32_t k);
+
+// ------------------------------------------------------------------------------------------
+// host encoder
+// ------------------------------------------------------------------------------------------
+struct Encoded {
+    std::vector<uint32_t> key_chunk_off, key_word_off, hdr, payload;
+    int64_t nnz = 0;
+};
+
+static inline uint32_t bit_width(uint32_t v) { return v ? 32u - (uint32_t)__builtin_clz(v) : 0u; }
+
+static ebr_status validate_inventory(const int32_t* ad_feat, int64_t n_ads, int32_t F,
+                                     const int32_t* card, int64_t n_keys) {
+    if (F < 0) return set_error(EBR_EINVAL, "n_fields < 0");
+    int64_t m = 0;
+    for (int f = 0; f < F; ++f) {
+        if (card[f] < 1) return set_error(EBR_EINVAL, "field_card[%d] = %d < 1", f, card[f]);
+        m += card[f];
+    }
+    if (m != n_keys) return set_error(EBR_EINVAL, "n_keys %lld != sum(field_card) %lld", (long long)n_keys, (long long)m);
+    if (n_keys >= (int64_t)1 << 31) return set_error(EBR_EINVAL, "n_keys >= 2^31");
+    for (int64_t a = 0; a < n_ads; ++a)
+        for (int f = 0; f < F; ++f) {
+            const int32_t v = ad_feat[a * F + f];
+            if (v < -1 || v >= card[f])
+                return set_error(EBR_EINVAL, "ad_feat[%lld][%d] = %d outside [-1, %d)", (long long)a, f, v, card[f]);
+        }
+    return EBR_OK;
+}
+
+// Encodes all posting lists of the shard; fields are independent (disjoint key ranges) and are
+// encoded in parallel.
+static ebr_status encode(const int32_t* ad_feat, int64_t n_ads, int32_t F, const int32_t* card,
+                         int64_t n_keys, Encoded& out) {
+    std::vector<int64_t> base(F + 1, 0);
+    for (int f = 0; f < F; ++f) base[f + 1] = base[f] + card[f];
+    std::vector<uint32_t> nchunks(n_keys, 0), nwords(n_keys, 0);
+    std::vector<std::vector<int32_t>> lists(F);
+    std::vector<std::vector<int64_t>> loff(F);
+    const int T = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 32u));
+    std::atomic<int> next{0};
+    std::atomic<bool> too_far{false};
+    // pass 1: counting sort per field, chunk and word counts per key
+    auto pass1 = [&]() {
+        for (int f; (f = next.fetch_add(1)) < F;) {
+            const int V = card[f];
+            std::vector<int64_t>& off = loff[f];
+            off.assign(V + 1, 0);
+            for (int64_t a = 0; a < n_ads; ++a) {
+                const int32_t v = ad_feat[a * F + f];
+                if (v >= 0) off[v + 1]++;
+            }
+            for (int v = 0; v < V; ++v) off[v + 1] += off[v];
+            std::vector<int32_t>& L = lists[f];
+            L.resize(off[V]);
+            std::vector<int64_t> fill(off.begin(), off.end() - 1);
+            for (int64_t a = 0; a < n_ads; ++a) {
+                const int32_t v = ad_feat[a * F + f];
+                if (v >= 0) L[fill[v]++] = (int32_t)a;      // ascending a => ascending lists
+            }
+            for (int v = 0; v < V; ++v) {
+                const int64_t n = off[v + 1] - off[v];
+                const int64_t key = base[f] + v;
+                nchunks[key] = (uint32_t)((n + 31) / 32);
+                uint64_t words = 0;
+                for (int64_t c0 = off[v]; c0 < off[v + 1]; c0 += 32) {
+                    const int64_t c1 = std::min<int64_t>(c0 + 32, off[v + 1]);
+                    uint32_t mx = 0;
+                    for (int64_t j = c0 + 1; j < c1; ++j) mx = std::max<uint32_t>(mx, (uint32_t)(L[j] - L[j - 1] - 1));
+                    const uint32_t b = bit_width(mx);
+                    words += ((uint64_t)(c1 - c0 - 1) * b + 31) / 32;
+                }
+                if (words >= (1u << 22)) too_far = true;   // relative word offset field is 22 bits
+                nwords[key] = (uint32_t)words;
+            }
+        }
+    };
+    {
+        std::vector<std::thread> th;
+        for (int t = 1; t < T; ++t) th.emplace_back(pass1);
+        pass1();
+        for (auto& t : th) t.join();
+    }
+    if (too_far) return set_error(EBR_EUNSUPPORTED, "a posting list exceeds 2^22 payload words");
+    out.key_chunk_off.assign(n_keys + 1, 0);
+    out.key_word_off.assign(n_keys, 0);
+    uint64_t cacc = 0, wacc = 0;
+    for (int64_t k = 0; k < n_keys; ++k) {
+        out.key_chunk_off[k] = (uint32_t)cacc;
+        out.key_word_off[k] = (uint32_t)wacc;
+        cacc += nchunks[k];
+        wacc += nwords[k];
+        if (cacc >= 0xFFFFFFFFull || wacc >= 0xFFFFFFF0ull)
+            return set_error(EBR_EUNSUPPORTED, "index exceeds 2^32 chunks/words");
+    }
+    out.key_chunk_off[n_keys] = (uint32_t)cacc;
+    out.hdr.assign(2 * cacc, 0);
+    out.payload.assign(wacc + 2, 0);   // two guard words: the decoder reads word w+1
+    int64_t nnz = 0;
+    for (int f = 0; f < F; ++f) nnz += (int64_t)lists[f].size();
+    out.nnz = nnz;
+    // pass 2: headers + payload
+    next = 0;
+    auto pass2 = [&]() {
+        for (int f; (f = next.fetch_add(1)) < F;) {
+            const int V = card[f];
+            const std::vector<int32_t>& L = lists[f];
+            const std::vector<int64_t>& off = loff[f];
+            for (int v = 0; v < V; ++v) {
+                const int64_t key = base[f] + v;
+                uint32_t c = out.key_chunk_off[key];
+                uint32_t rel = 0;
+                uint32_t* pw = out.payload.data() + out.key_word_off[key];
+                for (int64_t c0 = off[v]; c0 < off[v + 1]; c0 += 32, ++c) {
+                    const int64_t c1 = std::min<int64_t>(c0 + 32, off[v + 1]);
+                    uint32_t mx = 0;
+                    for (int64_t j = c0 + 1; j < c1; ++j) mx = std::max<uint32_t>(mx, (uint32_t)(L[j] - L[j - 1] - 1));
+                    const uint32_t b = bit_width(mx);
+                    const uint32_t n = (uint32_t)(c1 - c0);
+                    out.hdr[2 * (size_t)c] = (uint32_t)L[c0];
+                    out.hdr[2 * (size_t)c + 1] = (n - 1u) | (b << 5) | (rel << 10);
+                    if (b) {
+                        for (int64_t j = c0 + 1; j < c1; ++j) {
+                            const uint32_t val = (uint32_t)(L[j] - L[j - 1] - 1);
+                            const uint64_t pos = (uint64_t)(j - c0 - 1) * b;
+                            uint32_t* w = pw + rel + (pos >> 5);
+                            const uint32_t sh = (uint32_t)(pos & 31);
+                            w[0] |= val << sh;
+                            if (sh + b > 32) w[1] |= val >> (32 - sh);
+                        }
+                    }
+                    rel += (uint32_t)(((uint64_t)(n - 1) * b + 31) / 32);
+                }
+            }
+        }
+    };
+    {
+        std::vector<std::thread> th;
+        for (int t = 1; t < T; ++t) th.emplace_back(pass2);
+        pass2();
+        for (auto& t : th) t.join();
+    }
+    return EBR_OK;
+}
+
+// Padded kernel row width: row bytes a power of two in [16, 512] (>= 128 B for bf16, the TMA
+// 128B-swizzle atom), or a multiple of 512 B.  Zero padding leaves every dot product exact.
+static int32_t padded_width(int32_t d, int esz) {
+    int64_t bytes = (int64_t)d * esz;
+    int64_t p = (esz == 2) ? 128 : 16;
+    while (p < bytes && p < 512) p <<= 1;
+    if (bytes > 512) p = (bytes + 511) / 512 * 512;
+    return (int32_t)(p / esz);
+}
+
+// ------------------------------------------------------------------------------------------
+// kernels owned by the host file: merge (A7) and debug decode
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) merge_kernel(const uint64_t* __restrict__ gathered, int G,
+                                                         int B, int K, int32_t* out_ids,
+                                                         float* out_scores) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint32_t sScalar[8];
+    uint64_t* sbuf = reinterpret_cast<uint64_t*>(smem);
+    const int b = blockIdx.x;
+    const int64_t n = (int64_t)G * K;
+    auto get = [=](int64_t i) {
+        const int64_t g = i / K, q = i - g * K;
+        return __ldg(&gathered[(g * B + b) * (int64_t)K + q]);
+    };
+    const int nsel = cta_select_topk(get, n, K, sbuf, reinterpret_cast<uint32_t*>(sbuf + pow2ceil_i(K)), sScalar);
+    // padding keys (0) may have been selected when fewer than K real keys exist: they sort last
+    cta_write_topk(sbuf, nsel, K, out_ids + (size_t)b * K, out_scores + (size_t)b * K, nullptr);
+}
+
+__global__ void decode_key_kernel(const uint2* __restrict__ hdr, const uint32_t* __restrict__ payload,
+                                  uint32_t c0, uint32_t c1, uint32_t kwb, int32_t* out, int64_t cap) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t c = c0 + blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    if (c >= c1) return;   // warp-uniform
+    uint32_t id;
+    const bool ok = decode_chunk(hdr, payload, kwb, c, lane, id);
+    const int64_t pos = (int64_t)(c - c0) * 32 + lane;   // every chunk but the last is full
+    if (ok && pos < cap) out[pos] = (int32_t)id;
+}
+
+ebr_status run_merge(const uint64_t* gathered, int32_t G, int32_t batch, int32_t k,
+                     int32_t* out_ids, float* out_scores, cudaStream_t stream) {
+    const size_t smem = (size_t)pow2ceil_i(k) * 8 + 256 * 4 + 64;
+    EBR_CUDA(cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    merge_kernel<<<batch, kThreads, smem, stream>>>(gathered, G, batch, k, out_ids, out_scores);
+    return cuda_check(cudaGetLastError(), "launch(merge)");
+}
+
+ebr_status run_debug_decode(const ebr_index* idx, int64_t key, int32_t* dev_out, int64_t cap,
+                            cudaStream_t stream) {
+    uint32_t c[2], kwb;
+    EBR_CUDA(cudaMemcpy(c, idx->key_chunk_off + key, 8, cudaMemcpyDeviceToHost));
+    EBR_CUDA(cudaMemcpy(&kwb, idx->key_word_off + key, 4, cudaMemcpyDeviceToHost));
+    if (c[1] > c[0]) {
+        const uint32_t nch = c[1] - c[0];
+        decode_key_kernel<<<(nch + 3) / 4, 128, 0, stream>>>(idx->chunk_hdr, idx->payload, c[0], c[1], kwb, dev_out, cap);
+        EBR_CUDA(cudaGetLastError());
+    }
+    return EBR_OK;
+}
+
+size_t workspace_bytes(const ebr_index* idx, int32_t batch, int32_t slots, int32_t k) {
+    (void)batch;
+    return small_workspace_bytes(idx, slots, k);
+}
+
+ebr_status run_query(const QueryArgs& q) {
+    for (int b0 = 0; b0 < q.batch; b0 += kSmallMaxB) {
+        const int B = std::min(kSmallMaxB, q.batch - b0);
+        ebr_status st = run_small(q, b0, B);
+        if (st != EBR_OK) return st;
+    }
+    return EBR_OK;
+}
+
+}  // namespace ebr
+
+using namespace ebr;
+
+// ------------------------------------------------------------------------------------------
+// C-ABI
+// ------------------------------------------------------------------------------------------
+extern "C" {
+
+const char* ebr_last_error(void) { return g_last_error.c_str(); }
+
+const char* ebr_version(void) {
+#ifndef EBR_GIT
+#define EBR_GIT "dev"
+#endif
+    return "ebr " EBR_GIT " sm_100a";
+}
+
+ebr_status ebr_encode_host(const int32_t* ad_feat, int64_t n_ads, int32_t n_fields,
+                           const int32_t* field_card, int64_t n_keys, uint32_t* key_chunk_off,
+                           uint32_t* key_word_off, uint32_t* chunk_hdr, int64_t hdr_cap,
+                           uint32_t* payload, int64_t payload_cap, int64_t* n_chunks,
+                           int64_t* n_words) {
+    if (n_chunks) *n_chunks = -1;
+    if (n_words) *n_words = -1;
+    try {
+        if (n_ads < 0 || (n_ads > 0 && !ad_feat) || !field_card)
+            return set_error(EBR_EINVAL, "bad arguments");
+        ebr_status st = validate_inventory(ad_feat, n_ads, n_fields, field_card, n_keys);
+        if (st) return st;
+        Encoded enc;
+        st = encode(ad_feat, n_ads, n_fields, field_card, n_keys, enc);
+        if (st) return st;
+        const int64_t C = (int64_t)enc.hdr.size() / 2, W = (int64_t)enc.payload.size() - 2;
+        if (n_chunks) *n_chunks = C;
+        if (n_words) *n_words = W;
+        if (C > hdr_cap || W > payload_cap) return set_error(EBR_EINVAL, "capacity too small");
+        memcpy(key_chunk_off, enc.key_chunk_off.data(), sizeof(uint32_t) * (n_keys + 1));
+        memcpy(key_word_off, enc.key_word_off.data(), sizeof(uint32_t) * n_keys);
+        memcpy(chunk_hdr, enc.hdr.data(), sizeof(uint32_t) * 2 * C);
+        memcpy(payload, enc.payload.data(), sizeof(uint32_t) * W);
+        return EBR_OK;
+    } catch (const std::bad_alloc&) {
+        return set_error(EBR_ENOMEM, "host allocation failed");
+    } catch (...) {
+        return set_error(EBR_EINVAL, "unexpected exception");
+    }
+}
+
+void ebr_free_index(ebr_index* idx) {
+    if (!idx) return;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(idx->device);
+    void* ptrs[] = {idx->A, idx->key_chunk_off, idx->key_word_off, idx->chunk_hdr, idx->payload,
+                    idx->cross_w, idx->field_card, idx->field_base};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    free(idx->tmap_A);
+    if (prev >= 0) cudaSetDevice(prev);
+    delete idx;
+}
+
+ebr_status ebr_build_index(const void* ad_emb, ebr_dtype dtype, int64_t ad_begin, int64_t ad_end,
+                           int32_t d, const int32_t* ad_feat, int32_t n_fields,
+                           const int32_t* field_card, const float* cross_w, int64_t n_keys,
+                           int device, void* stream_v, ebr_index** out) {
+    auto t0 = std::chrono::steady_clock::now();
+    if (!out) return set_error(EBR_EINVAL, "out is null");
+    *out = nullptr;
+    if (d < 1) return set_error(EBR_EINVAL, "d < 1");
+    if (dtype != EBR_F32 && dtype != EBR_BF16) return set_error(EBR_EINVAL, "bad dtype");
+    if (ad_begin < 0 || ad_begin >= ad_end) return set_error(EBR_EINVAL, "need 0 <= ad_begin < ad_end");
+    if (ad_end > 0x7FFFFFFFll) return set_error(EBR_EINVAL, "ad_end > 2^31-1");
+    if (!ad_emb || !ad_feat || !field_card || (!cross_w && n_keys > 0))
+        return set_error(EBR_EINVAL, "null input");
+    const int64_t n = ad_end - ad_begin;
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+    try {
+        ebr_status st = validate_inventory(ad_feat, n, n_fields, field_card, n_keys);
+        if (st) return st;
+        int prev = -1;
+        cudaGetDevice(&prev);
+        EBR_CUDA(cudaSetDevice(device));
+        cudaDeviceProp prop;
+        EBR_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10) {
+            if (prev >= 0) cudaSetDevice(prev);
+            return set_error(EBR_EUNSUPPORTED, "device %d is sm_%d%d, this library is built for sm_100a",
+                             device, prop.major, prop.minor);
+        }
+        Encoded enc;
+        st = encode(ad_feat, n, n_fields, field_card, n_keys, enc);
+        if (st) return st;
+        ebr_index* idx = new ebr_index();
+        memset(idx, 0, sizeof(*idx));
+        idx->device = device;
+        idx->dtype = dtype;
+        idx->d = d;
+        const int esz = dtype == EBR_BF16 ? 2 : 4;
+        idx->d_pad = padded_width(d, esz);
+        idx->n_ads = n;
+        idx->n_pad = (n + 127) / 128 * 128;
+        idx->ad_begin = ad_begin;
+        idx->n_fields = n_fields;
+        idx->n_keys = n_keys;
+        idx->nnz = enc.nnz;
+        idx->n_chunks = (int64_t)enc.hdr.size() / 2;
+        idx->n_words = (int64_t)enc.payload.size() - 2;
+        idx->sm_count = prop.multiProcessorCount;
+        auto fail = [&](ebr_status s) { ebr_free_index(idx); if (prev >= 0) cudaSetDevice(prev); return s; };
+#define EBR_TRY(call) do { cudaError_t e__ = (call); if (e__ != cudaSuccess) return fail(cuda_check(e__, #call)); } while (0)
+        const size_t abytes = (size_t)idx->n_pad * idx->d_pad * esz;
+        EBR_TRY(cudaMalloc(&idx->A, abytes));
+        EBR_TRY(cudaMemsetAsync(idx->A, 0, abytes, stream));
+        EBR_TRY(cudaMemcpy2DAsync(idx->A, (size_t)idx->d_pad * esz, ad_emb, (size_t)d * esz, (size_t)d * esz, n,
+                                  cudaMemcpyHostToDevice, stream));
+        auto upload = [&](void** dst, const void* src, size_t bytes) -> cudaError_t {
+            cudaError_t e = cudaMalloc(dst, bytes ? bytes : 4);
+            if (e != cudaSuccess || !bytes) return e;
+            return cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, stream);
+        };
+        EBR_TRY(upload((void**)&idx->key_chunk_off, enc.key_chunk_off.data(), enc.key_chunk_off.size() * 4));
+        EBR_TRY(upload((void**)&idx->key_word_off, enc.key_word_off.data(), enc.key_word_off.size() * 4));
+        EBR_TRY(upload((void**)&idx->chunk_hdr, enc.hdr.data(), enc.hdr.size() * 4));
+        EBR_TRY(upload((void**)&idx->payload, enc.payload.data(), enc.payload.size() * 4));
+        EBR_TRY(upload((void**)&idx->cross_w, cross_w, (size_t)n_keys * 4));
+        std::vector<int32_t> fb(n_fields);
+        int64_t acc = 0;
+        for (int f = 0; f < n_fields; ++f) { fb[f] = (int32_t)acc; acc += field_card[f]; }
+        EBR_TRY(upload((void**)&idx->field_card, field_card, (size_t)n_fields * 4));
+        EBR_TRY(upload((void**)&idx->field_base, fb.data(), (size_t)n_fields * 4));
+        EBR_TRY(cudaStreamSynchronize(stream));
+#undef EBR_TRY
+        idx->build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        if (prev >= 0) cudaSetDevice(prev);
+        *out = idx;
+        return EBR_OK;
+    } catch (const std::bad_alloc&) {
+        return set_error(EBR_ENOMEM, "host allocation failed");
+    }
+}
+
+size_t ebr_workspace_bytes(const ebr_index* idx, int32_t batch, int32_t slots, int32_t k) {
+    if (!idx || batch < 1 || slots < 1 || slots > 64 || k < 1 || k > EBR_MAX_K) return 0;
+    return workspace_bytes(idx, batch, slots, k);
+}
+
+static ebr_status query_common(const ebr_index* idx, const void* user_emb, int32_t batch,
+                               const int32_t* user_feat, const float* user_x, int32_t slots,
+                               int32_t k, int32_t* out_ids, float* out_scores, uint64_t* out_keys,
+                               void* workspace, size_t workspace_bytes_, void* stream) {
+    if (!idx) return set_error(EBR_EINVAL, "null index");
+    if (batch < 1) return set_error(EBR_EINVAL, "batch < 1");
+    if (slots < 1 || slots > 64) return set_error(EBR_EINVAL, "slots must be in [1, 64]");
+    if (k < 1 || k > EBR_MAX_K) return set_error(EBR_EINVAL, "k must be in [1, %d]", EBR_MAX_K);
+    if (!user_emb || !user_feat || !user_x || !workspace) return set_error(EBR_EINVAL, "null pointer");
+    if (!out_keys && (!out_ids || !out_scores)) return set_error(EBR_EINVAL, "null output");
+    const size_t need = workspace_bytes(idx, batch, slots, k);
+    if (workspace_bytes_ < need)
+        return set_error(EBR_EINVAL, "workspace %zu bytes < required %zu", workspace_bytes_, need);
+    if (reinterpret_cast<uintptr_t>(workspace) & 255) return set_error(EBR_EINVAL, "workspace not 256-byte aligned");
+    int prev = -1;
+    cudaGetDevice(&prev);
+    if (prev != idx->device) cudaSetDevice(idx->device);
+    QueryArgs q{idx, user_emb, batch, user_feat, user_x, slots, k, out_ids, out_scores, out_keys,
+                workspace, workspace_bytes_, static_cast<cudaStream_t>(stream)};
+    ebr_status st = run_query(q);
+    if (prev >= 0 && prev != idx->device) cudaSetDevice(prev);
+    return st;
+}
+
+ebr_status ebr_score_topk(const ebr_index* idx, const void* user_emb, int32_t batch,
+                          const int32_t* user_feat, const float* user_x, int32_t slots, int32_t k,
+                          int32_t* out_ids, float* out_scores, void* workspace,
+                          size_t workspace_bytes_, void* stream) {
+    return query_common(idx, user_emb, batch, user_feat, user_x, slots, k, out_ids, out_scores,
+                        nullptr, workspace, workspace_bytes_, stream);
+}
+
+ebr_status ebr_score_topk_keys(const ebr_index* idx, const void* user_emb, int32_t batch,
+                               const int32_t* user_feat, const float* user_x, int32_t slots,
+                               int32_t k, uint64_t* out_keys, void* workspace,
+                               size_t workspace_bytes_, void* stream) {
+    if (!out_keys) return set_error(EBR_EINVAL, "null out_keys");
+    return query_common(idx, user_emb, batch, user_feat, user_x, slots, k, nullptr, nullptr,
+                        out_keys, workspace, workspace_bytes_, stream);
+}
+
+ebr_status ebr_query_error(void* workspace, void* stream, uint32_t* flags) {
+    if (!workspace) return set_error(EBR_EINVAL, "null workspace");
+    uint32_t f = 0;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    EBR_CUDA(cudaMemcpyAsync(&f, workspace, 4, cudaMemcpyDeviceToHost, s));
+    EBR_CUDA(cudaMemsetAsync(workspace, 0, 4, s));
+    EBR_CUDA(cudaStreamSynchronize(s));
+    if (flags) *flags = f;
+    return f ? set_error(EBR_EDEVICE, "device validation flags 0x%x", f) : EBR_OK;
+}
+
+// e2e: inputs staged after the query workspace
+static size_t host_stage_bytes(const ebr_index* idx, int32_t batch, int32_t slots, int32_t k) {
+    const int esz = idx->dtype == EBR_BF16 ? 2 : 4;
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const size_t nfs = (size_t)batch * idx->n_fields * slots;
+    return al((size_t)batch * idx->d * esz) + al(nfs * 4) + al(nfs * 4) + al((size_t)batch * k * 4) * 2;
+}
+
+size_t ebr_workspace_bytes_host(const ebr_index* idx, int32_t batch, int32_t slots, int32_t k) {
+    const size_t w = ebr_workspace_bytes(idx, batch, slots, k);
+    if (!w) return 0;
+    return ((w + 255) & ~(size_t)255) + host_stage_bytes(idx, batch, slots, k);
+}
+
+ebr_status ebr_score_topk_host(const ebr_index* idx, const void* user_emb_host, int32_t batch,
+                               const int32_t* user_feat_host, const float* user_x_host,
+                               int32_t slots, int32_t k, int32_t* out_ids_host,
+                               float* out_scores_host, void* workspace, size_t workspace_bytes_,
+                               void* stream_v) {
+    if (!idx) return set_error(EBR_EINVAL, "null index");
+    const size_t w = ebr_workspace_bytes(idx, batch, slots, k);
+    if (!w) return set_error(EBR_EINVAL, "bad batch/slots/k");
+    if (workspace_bytes_ < ebr_workspace_bytes_host(idx, batch, slots, k))
+        return set_error(EBR_EINVAL, "workspace too small for the host variant");
+    if (!user_emb_host || !user_feat_host || !user_x_host || !out_ids_host || !out_scores_host)
+        return set_error(EBR_EINVAL, "null host pointer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream_v);
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const int esz = idx->dtype == EBR_BF16 ? 2 : 4;
+    const size_t nfs = (size_t)batch * idx->n_fields * slots;
+    char* st = static_cast<char*>(workspace) + al(w);
+    char* d_emb = st;            st += al((size_t)batch * idx->d * esz);
+    int32_t* d_feat = (int32_t*)st; st += al(nfs * 4);
+    float* d_x = (float*)st;     st += al(nfs * 4);
+    int32_t* d_ids = (int32_t*)st; st += al((size_t)batch * k * 4);
+    float* d_sc = (float*)st;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    if (prev != idx->device) cudaSetDevice(idx->device);
+    EBR_CUDA(cudaMemcpyAsync(d_emb, user_emb_host, (size_t)batch * idx->d * esz, cudaMemcpyHostToDevice, s));
+    EBR_CUDA(cudaMemcpyAsync(d_feat, user_feat_host, nfs * 4, cudaMemcpyHostToDevice, s));
+    EBR_CUDA(cudaMemcpyAsync(d_x, user_x_host, nfs * 4, cudaMemcpyHostToDevice, s));
+    ebr_status r = ebr_score_topk(idx, d_emb, batch, d_feat, d_x, slots, k, d_ids, d_sc, workspace, w, stream_v);
+    if (r != EBR_OK) return r;
+    EBR_CUDA(cudaMemcpyAsync(out_ids_host, d_ids, (size_t)batch * k * 4, cudaMemcpyDeviceToHost, s));
+    EBR_CUDA(cudaMemcpyAsync(out_scores_host, d_sc, (size_t)batch * k * 4, cudaMemcpyDeviceToHost, s));
+    EBR_CUDA(cudaStreamSynchronize(s));
+    if (prev >= 0 && prev != idx->device) cudaSetDevice(prev);
+    return EBR_OK;
+}
+
+size_t ebr_merge_workspace_bytes(int32_t G, int32_t batch, int32_t k) {
+    if (G < 1 || batch < 1 || k < 1 || k > EBR_MAX_K) return 0;
+    return 256;
+}
+
+ebr_status ebr_merge_topk(const uint64_t* gathered, int32_t G, int32_t batch, int32_t k,
+                          int32_t* out_ids, float* out_scores, void* workspace,
+                          size_t workspace_bytes_, void* stream) {
+    (void)workspace; (void)workspace_bytes_;
+    if (!gathered || !out_ids || !out_scores) return set_error(EBR_EINVAL, "null pointer");
+    if (G < 1 || batch < 1 || k < 1 || k > EBR_MAX_K) return set_error(EBR_EINVAL, "bad G/batch/k");
+    return run_merge(gathered, G, batch, k, out_ids, out_scores, static_cast<cudaStream_t>(stream));
+}
+
+ebr_status ebr_debug_decode(const ebr_index* idx, int64_t key, int32_t* out_ads, int64_t cap,
+                            int64_t* n) {
+    if (!idx || !n) return set_error(EBR_EINVAL, "null argument");
+    if (key < 0 || key >= idx->n_keys) return set_error(EBR_EINVAL, "key out of range");
+    int prev = -1;
+    cudaGetDevice(&prev);
+    if (prev != idx->device) cudaSetDevice(idx->device);
+    uint32_t c[2];
+    EBR_CUDA(cudaMemcpy(c, idx->key_chunk_off + key, 8, cudaMemcpyDeviceToHost));
+    int64_t len = 0;
+    if (c[1] > c[0]) {
+        uint32_t last_hdr[2];
+        EBR_CUDA(cudaMemcpy(last_hdr, idx->chunk_hdr + (c[1] - 1), 8, cudaMemcpyDeviceToHost));
+        len = (int64_t)(c[1] - c[0] - 1) * 32 + (last_hdr[1] & 31u) + 1;
+    }
+    *n = len;
+    if (len > cap) return set_error(EBR_EINVAL, "list of %lld ids exceeds cap", (long long)len);
+    if (len == 0) return EBR_OK;
+    int32_t* dev = nullptr;
+    EBR_CUDA(cudaMalloc(&dev, (size_t)len * 4));
+    ebr_status st = run_debug_decode(idx, key, dev, len, nullptr);
+    if (st == EBR_OK) {
+        cudaError_t e = cudaMemcpy(out_ads, dev, (size_t)len * 4, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) st = cuda_check(e, "cudaMemcpy(decode)");
+    }
+    cudaFree(dev);
+    if (prev >= 0 && prev != idx->device) cudaSetDevice(prev);
+    return st;
+}
+
+ebr_status ebr_index_stats(const ebr_index* idx, ebr_stats* o) {
+    if (!idx || !o) return set_error(EBR_EINVAL, "null argument");
+    const int esz = idx->dtype == EBR_BF16 ? 2 : 4;
+    o->n_ads = idx->n_ads;
+    o->ad_begin = idx->ad_begin;
+    o->d = idx->d;
+    o->d_pad = idx->d_pad;
+    o->dtype = idx->dtype;
+    o->n_fields = idx->n_fields;
+    o->n_keys = idx->n_keys;
+    o->nnz = idx->nnz;
+    o->chunks = idx->n_chunks;
+    o->payload_words = idx->n_words;
+    o->index_bytes = (idx->n_keys * 2 + 1) * 4 + idx->n_chunks * 8 + (idx->n_words + 2) * 4 + idx->n_keys * 4;
+    o->emb_bytes = idx->n_pad * idx->d_pad * esz;
+    o->build_ms = idx->build_ms;
+    return EBR_OK;
+}
+
+}  // extern "C"

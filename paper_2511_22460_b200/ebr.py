@@ -1,0 +1,239 @@
+"""Thin ctypes binding of include/ebr.h (argument marshalling only).
+
+Every step of the hot path runs in the CUDA library libebr.so; this module only passes pointers
+(numpy arrays for host inputs, torch tensors for device buffers, a CUDA stream handle) and turns
+status codes into exceptions.  There is no fallback: if libebr.so is missing or fails to load,
+importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libebr.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`"
+                      " (there is no CPU fallback)")
+_lib = ctypes.CDLL(LIB_PATH)
+
+F32, BF16 = 0, 1
+MAX_K = 16384
+STATUS = {0: "EBR_OK", 1: "EBR_EINVAL", 2: "EBR_ENOMEM", 3: "EBR_ECUDA", 4: "EBR_EUNSUPPORTED",
+          5: "EBR_EDEVICE"}
+
+_P, _I32, _I64, _SZ, _U32P = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t, ctypes.c_void_p
+
+EXPORTS = {
+    # name: (restype, argtypes)
+    "ebr_build_index": (ctypes.c_int, [_P, ctypes.c_int, _I64, _I64, _I32, _P, _I32, _P, _P, _I64,
+                                       ctypes.c_int, _P, ctypes.POINTER(_P)]),
+    "ebr_free_index": (None, [_P]),
+    "ebr_workspace_bytes": (_SZ, [_P, _I32, _I32, _I32]),
+    "ebr_score_topk": (ctypes.c_int, [_P, _P, _I32, _P, _P, _I32, _I32, _P, _P, _P, _SZ, _P]),
+    "ebr_score_topk_keys": (ctypes.c_int, [_P, _P, _I32, _P, _P, _I32, _I32, _P, _P, _SZ, _P]),
+    "ebr_query_error": (ctypes.c_int, [_P, _P, ctypes.POINTER(ctypes.c_uint32)]),
+    "ebr_workspace_bytes_host": (_SZ, [_P, _I32, _I32, _I32]),
+    "ebr_score_topk_host": (ctypes.c_int, [_P, _P, _I32, _P, _P, _I32, _I32, _P, _P, _P, _SZ, _P]),
+    "ebr_merge_workspace_bytes": (_SZ, [_I32, _I32, _I32]),
+    "ebr_merge_topk": (ctypes.c_int, [_P, _I32, _I32, _I32, _P, _P, _P, _SZ, _P]),
+    "ebr_debug_decode": (ctypes.c_int, [_P, _I64, _P, _I64, ctypes.POINTER(_I64)]),
+    "ebr_index_stats": (ctypes.c_int, [_P, _P]),
+    "ebr_encode_host": (ctypes.c_int, [_P, _I64, _I32, _P, _I64, _P, _P, _P, _I64, _P, _I64,
+                                       ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
+    "ebr_last_error": (ctypes.c_char_p, []),
+    "ebr_version": (ctypes.c_char_p, []),
+}
+for _name, (_res, _args) in EXPORTS.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+
+class EbrError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        super().__init__(f"{where}: {STATUS.get(status, status)}: {last_error()}")
+
+
+def last_error() -> str:
+    return _lib.ebr_last_error().decode()
+
+
+def version() -> str:
+    return _lib.ebr_version().decode()
+
+
+def _check(st: int, where: str):
+    if st != 0:
+        raise EbrError(st, where)
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("n_ads", _I64), ("ad_begin", _I64), ("d", _I32), ("d_pad", _I32),
+                ("dtype", _I32), ("n_fields", _I32), ("n_keys", _I64), ("nnz", _I64),
+                ("chunks", _I64), ("payload_words", _I64), ("index_bytes", _I64),
+                ("emb_bytes", _I64), ("build_ms", ctypes.c_double)]
+
+
+def _np_ptr(a: np.ndarray):
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def _t_ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        return None
+    return ctypes.c_void_p(int(getattr(stream, "cuda_stream", stream)))
+
+
+class Index:
+    """An inventory shard resident on one GPU (ebr_build_index / ebr_free_index)."""
+
+    def __init__(self, ad_emb, ad_feat, field_card, cross_w, ad_begin: int = 0, device: int = 0,
+                 stream=None):
+        ad_emb = np.ascontiguousarray(ad_emb)
+        if ad_emb.dtype == np.uint16:
+            self.dtype = BF16
+        elif ad_emb.dtype == np.float32:
+            self.dtype = F32
+        else:
+            raise TypeError("ad_emb must be float32 or uint16 (bf16 bits)")
+        ad_feat = np.ascontiguousarray(ad_feat, np.int32)
+        field_card = np.ascontiguousarray(field_card, np.int32)
+        cross_w = np.ascontiguousarray(cross_w, np.float32)
+        n, self.d = ad_emb.shape
+        self.n_fields = field_card.shape[0]
+        self.n_keys = int(field_card.astype(np.int64).sum())
+        self.ad_begin = int(ad_begin)
+        self.n_ads = int(n)
+        self.device = device
+        h = ctypes.c_void_p()
+        st = _lib.ebr_build_index(_np_ptr(ad_emb), self.dtype, self.ad_begin, self.ad_begin + n,
+                                  self.d, _np_ptr(ad_feat), self.n_fields, _np_ptr(field_card),
+                                  _np_ptr(cross_w), self.n_keys, device, _stream_ptr(stream),
+                                  ctypes.byref(h))
+        _check(st, "ebr_build_index")
+        self._h = h
+
+    @classmethod
+    def of(cls, inv, ad_begin: int = 0, device: int = 0, lo: int | None = None, hi: int | None = None):
+        lo = 0 if lo is None else lo
+        hi = inv.n_ads if hi is None else hi
+        return cls(inv.ad_emb[lo:hi], inv.ad_feat[lo:hi], inv.field_card, inv.cross_w,
+                   ad_begin=ad_begin + lo, device=device)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.ebr_free_index(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def stats(self) -> dict:
+        s = Stats()
+        _check(_lib.ebr_index_stats(self._h, ctypes.byref(s)), "ebr_index_stats")
+        return {k: getattr(s, k) for k, _ in Stats._fields_}
+
+    def workspace_bytes(self, batch: int, slots: int, k: int) -> int:
+        n = _lib.ebr_workspace_bytes(self._h, batch, slots, k)
+        if n == 0:
+            raise EbrError(1, "ebr_workspace_bytes")
+        return int(n)
+
+    def workspace_bytes_host(self, batch: int, slots: int, k: int) -> int:
+        n = _lib.ebr_workspace_bytes_host(self._h, batch, slots, k)
+        if n == 0:
+            raise EbrError(1, "ebr_workspace_bytes_host")
+        return int(n)
+
+    def debug_decode(self, key: int) -> np.ndarray:
+        n = _I64()
+        st = _lib.ebr_debug_decode(self._h, key, None, 0, ctypes.byref(n))
+        if st not in (0, 1):
+            _check(st, "ebr_debug_decode")
+        out = np.empty(max(int(n.value), 1), np.int32)
+        _check(_lib.ebr_debug_decode(self._h, key, _np_ptr(out), out.shape[0], ctypes.byref(n)),
+               "ebr_debug_decode")
+        return out[: int(n.value)]
+
+
+def score_topk(idx: Index, user_emb, user_feat, user_x, k: int, out_ids, out_scores, workspace,
+               stream=None):
+    """Device buffers (torch CUDA tensors); asynchronous on `stream`."""
+    B, F, S = user_feat.shape
+    _check(_lib.ebr_score_topk(idx.handle, _t_ptr(user_emb), B, _t_ptr(user_feat), _t_ptr(user_x),
+                               S, k, _t_ptr(out_ids), _t_ptr(out_scores), _t_ptr(workspace),
+                               workspace.numel() * workspace.element_size(), _stream_ptr(stream)),
+           "ebr_score_topk")
+
+
+def score_topk_keys(idx: Index, user_emb, user_feat, user_x, k: int, out_keys, workspace,
+                    stream=None):
+    B, F, S = user_feat.shape
+    _check(_lib.ebr_score_topk_keys(idx.handle, _t_ptr(user_emb), B, _t_ptr(user_feat),
+                                    _t_ptr(user_x), S, k, _t_ptr(out_keys), _t_ptr(workspace),
+                                    workspace.numel() * workspace.element_size(),
+                                    _stream_ptr(stream)),
+           "ebr_score_topk_keys")
+
+
+def score_topk_host(idx: Index, user_emb: np.ndarray, user_feat: np.ndarray, user_x: np.ndarray,
+                    k: int, out_ids: np.ndarray, out_scores: np.ndarray, workspace, stream=None):
+    """Host numpy buffers (ideally pinned); synchronous."""
+    B, F, S = user_feat.shape
+    _check(_lib.ebr_score_topk_host(idx.handle, _np_ptr(user_emb), B, _np_ptr(user_feat),
+                                    _np_ptr(user_x), S, k, _np_ptr(out_ids), _np_ptr(out_scores),
+                                    _t_ptr(workspace), workspace.numel() * workspace.element_size(),
+                                    _stream_ptr(stream)),
+           "ebr_score_topk_host")
+
+
+def query_error(workspace, stream=None) -> int:
+    f = ctypes.c_uint32()
+    st = _lib.ebr_query_error(_t_ptr(workspace), _stream_ptr(stream), ctypes.byref(f))
+    if st not in (0, 5):
+        _check(st, "ebr_query_error")
+    return int(f.value)
+
+
+def merge_topk(gathered, G: int, batch: int, k: int, out_ids, out_scores, stream=None):
+    _check(_lib.ebr_merge_topk(_t_ptr(gathered), G, batch, k, _t_ptr(out_ids), _t_ptr(out_scores),
+                               None, 0, _stream_ptr(stream)),
+           "ebr_merge_topk")
+
+
+def encode_host(ad_feat: np.ndarray, field_card: np.ndarray):
+    """Host-only encoder (no GPU): (key_chunk_off, key_word_off, chunk_hdr[2C], payload[W])."""
+    ad_feat = np.ascontiguousarray(ad_feat, np.int32)
+    field_card = np.ascontiguousarray(field_card, np.int32)
+    n, F = ad_feat.shape
+    M = int(field_card.astype(np.int64).sum())
+    kco = np.empty(M + 1, np.uint32)
+    kwo = np.empty(max(M, 1), np.uint32)
+    C, W = _I64(), _I64()
+    st = _lib.ebr_encode_host(_np_ptr(ad_feat), n, F, _np_ptr(field_card), M, _np_ptr(kco),
+                              _np_ptr(kwo), None, 0, None, 0, ctypes.byref(C), ctypes.byref(W))
+    if st != 0 and (st != 1 or C.value < 0):
+        _check(st, "ebr_encode_host")
+    hdr = np.zeros(2 * max(C.value, 1), np.uint32)
+    pay = np.zeros(max(W.value, 1), np.uint32)
+    _check(_lib.ebr_encode_host(_np_ptr(ad_feat), n, F, _np_ptr(field_card), M, _np_ptr(kco),
+                                _np_ptr(kwo), _np_ptr(hdr), C.value, _np_ptr(pay), W.value,
+                                ctypes.byref(C), ctypes.byref(W)),
+           "ebr_encode_host")
+    return kco, kwo[:M], hdr[: 2 * C.value], pay[: W.value]

@@ -1,0 +1,243 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle, element by element.
+
+Bit-exact for integer work (decoded posting lists, top-K ids in exact mode), tolerance for fp
+(1e-5 * sigma, tests/parity.py).  Sizes span several ranges/tiles with ragged tails; the full
+C1 and C2 configs run at their BASELINE.json sizes in the launch configuration bench.py uses."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+from paper_2511_22460_b200 import synth  # noqa: E402
+from tests.parity import check_user  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def ebr():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2511_22460_b200 import ebr as m
+    return m
+
+
+def run(ebr, idx, users, k, keys=False, stream=None):
+    dev = torch.device("cuda", idx.device)
+    B, F, S = users.user_feat.shape
+    emb = torch.from_numpy(np.ascontiguousarray(users.user_emb).view(
+        np.int16 if users.user_emb.dtype == np.uint16 else np.float32)).to(dev)
+    feat = torch.from_numpy(users.user_feat).to(dev)
+    x = torch.from_numpy(users.user_x).to(dev)
+    ws = torch.empty(idx.workspace_bytes(B, S, k), dtype=torch.uint8, device=dev)
+    if keys:
+        out = torch.empty((B, k), dtype=torch.int64, device=dev)
+        ebr.score_topk_keys(idx, emb, feat, x, k, out, ws, stream)
+        torch.cuda.synchronize()
+        return out.cpu().numpy().view(np.uint64), ws
+    ids = torch.empty((B, k), dtype=torch.int32, device=dev)
+    sc = torch.empty((B, k), dtype=torch.float32, device=dev)
+    ebr.score_topk(idx, emb, feat, x, k, ids, sc, ws, stream)
+    torch.cuda.synchronize()
+    return (ids.cpu().numpy(), sc.cpu().numpy()), ws
+
+
+def check_all(o, users, ids, sc, k, mode, id_base=0):
+    mism = 0
+    for b in range(users.batch):
+        r, s = o.scores(users.user_emb[b], users.user_feat[b], users.user_x[b])
+        mism += check_user(ids[b], sc[b], r, s, k, mode, id_base=id_base)
+    return mism
+
+
+# ---------------------------------------------------------------- A0/A2: decode(encode(L)) == L
+
+def test_device_decode_equals_postings(ebr):
+    inv = synth.make_inventory(70_000, 8, 12, alpha=1.2, seed=21)
+    idx = ebr.Index.of(inv)
+    off, ads = oracle.Oracle.of(inv).postings()
+    rng = np.random.default_rng(0)
+    keys = np.concatenate([np.arange(0, min(400, idx.n_keys)),
+                           np.argsort(-np.diff(off))[:50],                 # the hottest lists
+                           rng.integers(0, idx.n_keys, 300)])
+    for k in np.unique(keys):
+        got = idx.debug_decode(int(k))
+        assert (got == ads[off[k]:off[k + 1]]).all(), k
+    st = idx.stats()
+    assert st["nnz"] == off[-1] and st["n_ads"] == inv.n_ads
+
+
+# ---------------------------------------------------------------- exact mode: bit-exact top-K
+
+@pytest.mark.parametrize("cfg,n,b,k", [("C1", 10_000, 1, 100), ("C1", 10_000, 3, 100),
+                                       ("C1", 9_973, 8, 257), ("C2", 200_003, 2, 500),
+                                       ("C4", 50_001, 5, 1000), ("C3", 40_000, 8, 1000)])
+def test_exact_mode_bit_exact(ebr, cfg, n, b, k):
+    inv, users = synth.make_config(cfg, mode="exact", n_ads=n, batch=b)
+    idx = ebr.Index.of(inv)
+    (ids, sc), ws = run(ebr, idx, users, k)
+    assert check_all(oracle.Oracle.of(inv), users, ids, sc, k, "exact") == 0
+    assert ebr.query_error(ws) == 0
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("d", [16, 64, 100, 128, 200])
+def test_exact_mode_widths(ebr, dtype, d):
+    inv = synth.make_inventory(5_000, d, 6, dtype=dtype, mode="exact", seed=d)
+    users = synth.make_users(inv, 3, mode="exact", seed=d + 1)
+    idx = ebr.Index.of(inv)
+    (ids, sc), _ = run(ebr, idx, users, 64)
+    assert check_all(oracle.Oracle.of(inv), users, ids, sc, 64, "exact") == 0
+
+
+# ---------------------------------------------------------------- real mode: tolerance
+
+@pytest.mark.parametrize("cfg,n,b,k", [("C1", 10_000, 1, 100), ("C2", 300_000, 4, 500),
+                                       ("C3", 60_000, 8, 1000), ("C4", 80_000, 3, 1000)])
+def test_real_mode_tolerance(ebr, cfg, n, b, k):
+    inv, users = synth.make_config(cfg, mode="real", n_ads=n, batch=b)
+    idx = ebr.Index.of(inv)
+    (ids, sc), _ = run(ebr, idx, users, k)
+    check_all(oracle.Oracle.of(inv), users, ids, sc, k, "real")
+
+
+def test_full_c1_and_c2(ebr):
+    """BASELINE.json configs 1 and 2 at full size, in bench.py's launch configuration."""
+    for cfg in ("C1", "C2"):
+        c = synth.CONFIGS[cfg]
+        for mode in ("exact", "real"):
+            inv, users = synth.make_config(cfg, mode=mode)
+            idx = ebr.Index.of(inv)
+            (ids, sc), _ = run(ebr, idx, users, c.k)
+            check_all(oracle.Oracle.of(inv), users, ids, sc, c.k, mode)
+            del idx
+
+
+def test_bf16_quantisation_vs_fp32_masters(ebr):
+    """bf16 path vs the oracle on fp32 master embeddings: 2e-3 * sigma (north star)."""
+    inv32, users32 = synth.make_config("C1", mode="real", n_ads=20_000, batch=2)
+    inv16 = synth.Inventory(inv32.n_ads, inv32.d, "bf16", synth.f32_to_bf16_bits(inv32.ad_emb),
+                            inv32.ad_feat, inv32.field_card, inv32.cross_w)
+    users16 = synth.Users(2, users32.slots, synth.f32_to_bf16_bits(users32.user_emb),
+                          users32.user_feat, users32.user_x)
+    (ids, sc), _ = run(ebr, ebr.Index.of(inv16), users16, 50)
+    o = oracle.Oracle.of(inv32)
+    for b in range(2):
+        r, s = o.scores(users32.user_emb[b], users32.user_feat[b], users32.user_x[b])
+        assert (np.abs(sc[b] - r[ids[b]]) <= 2e-3 * s[ids[b]]).all()
+
+
+# ---------------------------------------------------------------- edge cases
+
+def test_k_larger_than_inventory_and_k1(ebr):
+    inv, users = synth.make_config("C1", mode="exact", n_ads=300, batch=2)
+    idx = ebr.Index.of(inv)
+    o = oracle.Oracle.of(inv)
+    for k in (1, 299, 300, 301, 1000):
+        (ids, sc), _ = run(ebr, idx, users, k)
+        assert check_all(o, users, ids, sc, k, "exact") == 0
+
+
+def test_tiny_inventories(ebr):
+    for n in (1, 2, 31, 33, 127, 129):
+        inv, users = synth.make_config("C1", mode="exact", n_ads=n, batch=2)
+        idx = ebr.Index.of(inv)
+        (ids, sc), _ = run(ebr, idx, users, 5)
+        assert check_all(oracle.Oracle.of(inv), users, ids, sc, 5, "exact") == 0
+
+
+def test_empty_users_and_zero_embeddings(ebr):
+    # zero-feature users == plain dual tower; zero embeddings == scorer B (pair enumeration)
+    inv, users = synth.make_config("C1", mode="exact", n_ads=4_000, batch=2)
+    users.user_feat[0] = -1
+    users.user_x[0] = 0
+    inv0 = synth.Inventory(inv.n_ads, inv.d, inv.dtype, np.zeros_like(inv.ad_emb), inv.ad_feat,
+                           inv.field_card, inv.cross_w)
+    o = oracle.Oracle.of(inv)
+    (ids, sc), _ = run(ebr, ebr.Index.of(inv), users, 40)
+    assert check_all(o, users, ids, sc, 40, "exact") == 0
+    (ids0, sc0), _ = run(ebr, ebr.Index.of(inv0), users, 4000)
+    wide = o.wide_pairs(users.user_feat[1], users.user_x[1])
+    order = np.lexsort((np.arange(inv.n_ads), -wide))
+    assert (ids0[1] == order).all() and (sc0[1] == wide[order]).all()
+
+
+def test_all_ties(ebr):
+    inv = synth.make_inventory(3_000, 8, 2, mode="exact", seed=4)
+    inv.ad_emb[:] = 0
+    inv.ad_feat[:] = -1
+    users = synth.make_users(inv, 2, mode="exact", seed=5)
+    (ids, sc), _ = run(ebr, ebr.Index.of(inv), users, 100)
+    assert (ids == np.arange(100)).all() and (sc == 0).all()
+
+
+def test_bad_user_value_raises_flag(ebr):
+    inv, users = synth.make_config("C1", mode="exact", n_ads=2_000, batch=1)
+    users.user_feat[0, 0, 0] = inv.field_card[0] + 5
+    (ids, sc), ws = run(ebr, ebr.Index.of(inv), users, 10)
+    assert ebr.query_error(ws) == 1
+    assert ebr.query_error(ws) == 0          # cleared
+
+
+def test_invalid_arguments(ebr):
+    inv, users = synth.make_config("C1", mode="exact", n_ads=100, batch=1)
+    idx = ebr.Index.of(inv)
+    with pytest.raises(ebr.EbrError):
+        run(ebr, idx, users, 0)
+    with pytest.raises(ebr.EbrError):
+        run(ebr, idx, users, ebr.MAX_K + 1)
+    bad = inv.ad_feat.copy()
+    bad[3, 1] = inv.field_card[1]
+    with pytest.raises(ebr.EbrError):
+        ebr.Index(inv.ad_emb, bad, inv.field_card, inv.cross_w)
+
+
+# ---------------------------------------------------------------- host (e2e) variant, keys
+
+def test_host_variant_equals_device(ebr):
+    inv, users = synth.make_config("C2", mode="real", n_ads=100_000, batch=3)
+    idx = ebr.Index.of(inv)
+    (ids, sc), _ = run(ebr, idx, users, 200)
+    ws = torch.empty(idx.workspace_bytes_host(3, users.slots, 200), dtype=torch.uint8, device="cuda")
+    hid = np.empty((3, 200), np.int32)
+    hsc = np.empty((3, 200), np.float32)
+    ebr.score_topk_host(idx, users.user_emb, users.user_feat, users.user_x, 200, hid, hsc, ws)
+    assert (hid == ids).all() and (hsc == sc).all()
+
+
+# ---------------------------------------------------------------- A7: shard + merge == 1 GPU
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_sharded_merge_equals_single(ebr, G):
+    inv, users = synth.make_config("C1", mode="exact", n_ads=50_000, batch=4)
+    k = 300
+    (ids1, sc1), _ = run(ebr, ebr.Index.of(inv), users, k)
+    bounds = np.linspace(0, inv.n_ads, G + 1).astype(int)
+    parts = []
+    for g in range(G):
+        idx = ebr.Index.of(inv, lo=bounds[g], hi=bounds[g + 1])
+        keys, _ = run(ebr, idx, users, k, keys=True)
+        parts.append(keys)
+    gathered = torch.from_numpy(np.stack(parts).view(np.int64)).cuda()
+    ids = torch.empty((4, k), dtype=torch.int32, device="cuda")
+    sc = torch.empty((4, k), dtype=torch.float32, device="cuda")
+    ebr.merge_topk(gathered, G, 4, k, ids, sc)
+    torch.cuda.synchronize()
+    assert (ids.cpu().numpy() == ids1).all() and (sc.cpu().numpy() == sc1).all()
+    assert check_all(oracle.Oracle.of(inv), users, ids1, sc1, k, "exact") == 0
+
+
+def test_shard_smaller_than_k_pads(ebr):
+    inv, users = synth.make_config("C1", mode="exact", n_ads=500, batch=2)
+    k = 400
+    parts = []
+    for lo, hi in ((0, 100), (100, 500)):
+        keys, _ = run(ebr, ebr.Index.of(inv, lo=lo, hi=hi), users, k, keys=True)
+        parts.append(keys)
+    assert (parts[0][:, 100:] == 0).all()
+    gathered = torch.from_numpy(np.stack(parts).view(np.int64)).cuda()
+    ids = torch.empty((2, k), dtype=torch.int32, device="cuda")
+    sc = torch.empty((2, k), dtype=torch.float32, device="cuda")
+    ebr.merge_topk(gathered, 2, 2, k, ids, sc)
+    torch.cuda.synchronize()
+    assert check_all(oracle.Oracle.of(inv), users, ids.cpu().numpy(), sc.cpu().numpy(), k, "exact") == 0
