@@ -32,7 +32,7 @@ from paper_2511_22460_b200 import synth  # noqa: E402
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C2")
     ap.add_argument("--batch", type=int, default=None)
@@ -72,6 +72,9 @@ class Clocks:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 5:   # first sample before timing starts
+                time.sleep(0.02)
         except Exception:
             self.proc = None
         return self
@@ -136,44 +139,49 @@ def algorithmic_bytes(ebr, inv, users, idx_stats, lo, hi):
 
 
 def run_reference(args, cfg, rank, world):
-    """Reference arm: the CPU oracle as it stands, on this host's cores (no GPU)."""
+    """Reference arm: the CPU oracle as it stands, on this host's cores (no GPU).  Each step is a
+    bounded sample of the workload -- min(B, cores) users of the batch scored against a seeded
+    prefix of the inventory sized so the whole run takes ~2 minutes -- and users/s is rescaled to
+    the full inventory by ads-scored/s (the oracle's cost is linear in N plus an N log N sort)."""
     if rank != 0:
         return
     import oracle
     B = args.batch or cfg.batch
     K = args.k or cfg.k
     inv, users = synth.make_config(cfg, mode=args.mode, batch=B)
-    o = oracle.Oracle.of(inv)
     threads = os.cpu_count() or 1
-    # bounded sample: each step scores a sample of the batch's users over the full inventory
-    per_user = None
+    nu = max(1, min(B, threads))
+    o_full = oracle.Oracle.of(inv)
     t = time.perf_counter()
-    o.topk(users.user_emb[:1], users.user_feat[:1], users.user_x[:1], K, threads=1)
-    per_user = time.perf_counter() - t
-    n_sample = int(max(1, min(B, threads, 20.0 / max(per_user, 1e-3) / max(args.steps, 1) * threads)))
-    for _ in range(args.warmup):
-        pass   # the oracle has no warm state worth priming
+    o_full.topk(users.user_emb[:1], users.user_feat[:1], users.user_x[:1], K, threads=1)
+    per_user_full = time.perf_counter() - t
+    budget = max(0.02, 120.0 / max(args.steps + args.warmup, 1))
+    n_sub = int(min(inv.n_ads, max(K, inv.n_ads * budget / max(per_user_full, 1e-6))))
+    o = oracle.Oracle(inv.ad_emb[:n_sub], inv.ad_feat[:n_sub], inv.field_card, inv.cross_w)
+    for s in range(args.warmup):
+        o.topk(users.user_emb[:1], users.user_feat[:1], users.user_x[:1], K, threads=1)
     times = []
     for s in range(args.steps):
-        sel = [(s * n_sample + j) % B for j in range(n_sample)]
+        sel = [(s * nu + j) % B for j in range(nu)]
         t = time.perf_counter()
-        o.topk(users.user_emb[sel], users.user_feat[sel], users.user_x[sel], K,
-               threads=min(threads, n_sample))
+        o.topk(users.user_emb[sel], users.user_feat[sel], users.user_x[sel], K, threads=nu)
         times.append(time.perf_counter() - t)
     tot = sum(times)
-    users_s = n_sample * args.steps / tot
+    ads_s = nu * n_sub * args.steps / tot
+    users_s = ads_s / inv.n_ads
     line = {
         "impl": "reference",
         "metric": "users_per_s", "value": users_s, "unit": "users/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * tot / args.steps * B / n_sample,
+        "ms_per_step": 1e3 * B / users_s,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": f"synthetic ({args.mode} mode, seeded generator)",
         "config": config_dict(cfg, B, K, world),
-        "ads_scored_per_s": users_s * inv.n_ads,
-        "cpu_baseline": {"value": users_s, "unit": "users/s", "cores": min(threads, n_sample),
-                         "kind": "oracle",
-                         "sample": f"{n_sample} users x all {inv.n_ads} ads per step, {args.steps} steps"},
+        "ads_scored_per_s": ads_s,
+        "cpu_baseline": {"value": users_s, "unit": "users/s", "cores": nu, "kind": "oracle",
+                         "sample": f"per step {nu} user(s) x the first {n_sub} of {inv.n_ads} ads "
+                                   f"(rescaled by ads-scored/s); full-inventory single-thread "
+                                   f"{per_user_full:.3f} s/user"},
         "e2e": {"value": users_s, "unit": "users/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }

@@ -133,7 +133,7 @@ ebr_status ebr_score_topk_keys(const ebr_index *idx, const void *user_emb, int32
 
 /*
  * Reads (and clears) the device-side validation flag of `workspace` written by the last
- * ebr_score_topk* call on it.  Host-synchronous on `stream`.  *flags bit 0 = a user_feat value
+ * ebr_score_topk* call on it (each call clears it when it starts).  Host-synchronous on `stream`.  *flags bit 0 = a user_feat value
  * was outside [-1, V_f).  Returns EBR_EDEVICE if any bit was set, EBR_OK otherwise.
  */
 ebr_status ebr_query_error(void *workspace, void *stream, uint32_t *flags);

@@ -28,6 +28,7 @@
 #include <cooperative_groups.h>
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "ebr_device.cuh"
 
@@ -64,6 +65,7 @@ struct SmallParams {
     const float* user_x;
     // workspace
     uint32_t* err;
+    unsigned long long* timers;  // optional phase stamps (EBR_PHASE_TIMERS=1), else null
     uint32_t* ghist;            // [B][kHistBins]
     uint32_t* cand_count;       // [B]
     float* scores;              // [B][n_pad]
@@ -115,6 +117,13 @@ __device__ __forceinline__ uint4 ldg_stream(const void* p) {
     return r;
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define EBR_STAMP(i) do { if (p.timers && (tid & 31) == 0) atomicMax(&p.timers[i], gtimer()); } while (0)
+
 __device__ __forceinline__ void wide_bar() {
     asm volatile("bar.sync 1, %0;" ::"n"(kWideWarps * 32));
 }
@@ -155,6 +164,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
     __shared__ uint32_t sBinStar[kSmallMaxB], sAbove[kSmallMaxB];
 
     // ---- phase 0: A1 plan (redundantly per CTA; B*F*S is small on this path) ----
+    if (p.timers && blockIdx.x == 0 && tid == 0) p.timers[0] = gtimer();
     if (tid == 0) sNItems = 0;
     for (int i = tid; i < B * kHistBins; i += kThreads) sHist[i] = 0;
     __syncthreads();
@@ -179,6 +189,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
     }
     __syncthreads();
     const int n_items = (int)sNItems;
+    EBR_STAMP(1);
 
     // user vectors -> registers (deep warps), zero-padded to d_pad
     using V = Vec<T>;
@@ -266,6 +277,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
                     }
                 }
             }
+            EBR_STAMP(2);
         } else {
             // ---------- deep: stream rows [r0, r1) ----------
             const int dw = warp - kWideWarps;
@@ -310,6 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
                     }
                 }
             }
+            EBR_STAMP(3);
         }
         __syncthreads();
         // ---------- A5 fuse + histogram ----------
@@ -328,8 +341,10 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
         const uint32_t c = sHist[i];
         if (c) atomicAdd(&p.ghist[i], c);
     }
+    EBR_STAMP(4);
 
     cg::this_grid().sync();
+    EBR_STAMP(5);
 
     // ---- phase 3: threshold bin per user (warp b handles user b) ----
     if (warp < B) {
@@ -383,7 +398,9 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
         }
     }
 
+    EBR_STAMP(6);
     cg::this_grid().sync();
+    EBR_STAMP(7);
 
     // ---- phase 5: exact selection, one CTA per user ----
     for (int b = blockIdx.x; b < B; b += gridDim.x) {
@@ -396,6 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
                        p.out_scores ? p.out_scores + (size_t)b * p.K : nullptr,
                        p.out_keys ? p.out_keys + (size_t)b * p.K : nullptr);
         __syncthreads();
+        EBR_STAMP(8);
     }
 }
 
@@ -422,7 +440,7 @@ SmallLayout small_layout(const ebr_index* idx, int B) {
     SmallLayout L;
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
     size_t o = 0;
-    L.off_err = o;    o = al(o + 16);
+    L.off_err = o;    o = al(o + 16 + 16 * 8);   // error word + 16 phase stamps
     L.off_hist = o;   o = al(o + (size_t)B * kHistBins * 4);
     L.off_count = o;  o = al(o + (size_t)B * 4);
     L.off_scores = o; o = al(o + (size_t)B * idx->n_pad * 4);
@@ -487,6 +505,8 @@ ebr_status run_small(const QueryArgs& q, int b0, int B) {
     p.user_feat = q.user_feat + (size_t)b0 * idx->n_fields * q.slots;
     p.user_x = q.user_x + (size_t)b0 * idx->n_fields * q.slots;
     p.err = reinterpret_cast<uint32_t*>(ws + L.off_err);
+    static const bool timers_on = getenv("EBR_PHASE_TIMERS") && getenv("EBR_PHASE_TIMERS")[0] == '1';
+    p.timers = timers_on ? reinterpret_cast<unsigned long long*>(ws + L.off_err + 16) : nullptr;
     p.ghist = reinterpret_cast<uint32_t*>(ws + L.off_hist);
     p.cand_count = reinterpret_cast<uint32_t*>(ws + L.off_count);
     p.scores = reinterpret_cast<float*>(ws + L.off_scores);
@@ -499,7 +519,9 @@ ebr_status run_small(const QueryArgs& q, int b0, int B) {
     p.items_cap = items_cap;
 
     // zero the per-call counters (histograms + candidate counts are contiguous)
-    e = cudaMemsetAsync(ws + L.off_hist, 0, L.off_scores - L.off_hist, q.stream);
+    // the first launch of a call also clears the device error word (flags of the last call)
+    const size_t z0 = (b0 == 0) ? L.off_err : L.off_hist;
+    e = cudaMemsetAsync(ws + z0, 0, L.off_scores - z0, q.stream);
     if (e != cudaSuccess) return cuda_check(e, "memset(small)");
     const int grid = std::max(1, std::min<int>(p.n_ranges, occ * sms));
     void* args[] = {&p};
