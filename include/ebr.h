@@ -112,7 +112,10 @@ size_t ebr_workspace_bytes(const ebr_index *idx, int32_t batch, int32_t slots, i
  *  out_ids    device, [batch][k] int32 global ad ids (ad_begin + local), best first.
  *  out_scores device, [batch][k] fp32 s(u,a) of those ads.
  *  workspace  device, >= ebr_workspace_bytes(idx, batch, slots, k) bytes, 256-byte aligned,
- *             caller-owned; one in-flight call per workspace.
+ *             caller-owned; one in-flight call per workspace.  Its contents are managed by the
+ *             library: the first call on a buffer (or after it was used with an index of another
+ *             size) initialises it inside the kernel and every call leaves it ready for the next,
+ *             so each query is a single kernel launch.  Do not modify it between calls.
  * Errors: EBR_EINVAL for batch < 1, slots out of range, k out of range, undersized workspace;
  *         EBR_ECUDA on a launch failure.  Duplicate (f,v) slots of one user add (reading A3).
  */

@@ -95,84 +95,221 @@ __device__ __forceinline__ uint32_t warp_upper_bound_first(const uint2* __restri
     return lo + __popc(__ballot_sync(FULL, pred));
 }
 
+// Decodes chunks [cb, ce) (ce - cb <= 16) of one key in two memory round trips: lanes fetch the
+// (up to) 16 chunk headers at once, then every lane issues its payload loads for all 16 chunks,
+// then each chunk is unpacked + warp-scanned.  f(id) is called on every lane holding a posting.
+template <typename F>
+__device__ __forceinline__ void decode_unit16(const uint2* __restrict__ hdr,
+                                              const uint32_t* __restrict__ payload, uint32_t kwb,
+                                              uint32_t cb, uint32_t ce, int lane, F f) {
+    const uint32_t nc = ce - cb;
+    uint2 h = make_uint2(0u, 0u);
+    if ((uint32_t)lane < nc) h = __ldg(&hdr[cb + lane]);
+    uint32_t lo[16], hi[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        const uint32_t meta = __shfl_sync(FULL, h.y, q);
+        lo[q] = 0u;
+        hi[q] = 0u;
+        const uint32_t n = (meta & 31u) + 1u, b = (meta >> 5) & 31u;
+        if ((uint32_t)q < nc && lane >= 1 && (uint32_t)lane < n && b) {
+            const uint32_t bit = (uint32_t)(lane - 1) * b;
+            const uint32_t w = kwb + (meta >> 10) + (bit >> 5);
+            lo[q] = __ldg(&payload[w]);
+            hi[q] = __ldg(&payload[w + 1]);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        if ((uint32_t)q >= nc) break;
+        const uint32_t meta = __shfl_sync(FULL, h.y, q);
+        const uint32_t first = __shfl_sync(FULL, h.x, q);
+        const uint32_t n = (meta & 31u) + 1u, b = (meta >> 5) & 31u;
+        uint32_t g;
+        if (lane == 0) {
+            g = first;
+        } else if ((uint32_t)lane < n) {
+            uint32_t v = 0u;
+            if (b) {
+                const uint32_t bit = (uint32_t)(lane - 1) * b;
+                v = (uint32_t)(((((uint64_t)hi[q]) << 32) | lo[q]) >> (bit & 31u)) & ((1u << b) - 1u);
+            }
+            g = v + 1u;
+        } else {
+            g = 0u;
+        }
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(FULL, g, o);
+            if (lane >= o) g += t;
+        }
+        if ((uint32_t)lane < n) f(g);
+    }
+}
+
+// Block-wide exclusive scan of one value per thread (blockDim.x <= 1024); returns the prefix and
+// writes the total to *total.  `scratch` holds >= 33 words.  Contains __syncthreads().
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* scratch, uint32_t* total) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = (blockDim.x + 31) >> 5;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) scratch[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = (lane < nw) ? scratch[lane] : 0u;
+        uint32_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(FULL, wi, o);
+            if (lane >= o) wi += t;
+        }
+        scratch[lane] = wi - w;
+        if (lane == 31) scratch[32] = wi;
+    }
+    __syncthreads();
+    const uint32_t r = scratch[warp] + incl - v;
+    *total = scratch[32];
+    __syncthreads();
+    return r;
+}
+
 // fp32 add into shared memory.  (red.shared.add.f32 is a CAS loop on sm_100a; callers use it
 // only where hits are few.)
 __device__ __forceinline__ void smem_add(float* p, float v) { atomicAdd(p, v); }
 
 // ------------------------------------------------------------------------------------------
+// mbarrier + bulk-copy (TMA engine) helpers, sm_90+ PTX
+// ------------------------------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+}
+// 1-D bulk copy global -> shared, completion counted on `bar` (bytes % 16 == 0, 16-B aligned)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// histogram increment aggregated over the lanes of a warp that hit the same bin
+__device__ __forceinline__ void warp_hist_add(uint32_t* hist, uint32_t bin, bool active) {
+    const unsigned act = __ballot_sync(FULL, active);
+    if (!active) return;
+    const unsigned peers = __match_any_sync(act, bin);
+    if ((threadIdx.x & 31) == (__ffs(peers) - 1)) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
+}
+
+
+// ------------------------------------------------------------------------------------------
 // A6: exact top-K of a set of unique 64-bit keys, by one CTA.
-//   1. radix select (8 passes of 8-bit digits) finds the K-th largest key exactly;
+//   1. radix select (8 passes of 8-bit digits, warp-aggregated shared histograms) finds the
+//      K-th largest key exactly;
 //   2. the keys >= it (exactly K, keys are unique) are gathered into shared memory;
 //   3. bitonic sort descending.
-// `get(i)` returns key i (global or shared memory).  sbuf holds >= pow2ceil(min(n,K)) keys.
+// `get(i)` returns key i (global memory).  If n <= scand_cap the keys are first staged in
+// scand (shared).  sbuf holds >= pow2ceil(min(n,K)) keys; shist 256 words; sscalar 4 words.
 // Returns the number of selected keys (min(n, K)) sorted descending in sbuf[0..).
 // ------------------------------------------------------------------------------------------
 template <typename Get>
-__device__ int cta_select_topk(Get get, int64_t n, int K, uint64_t* sbuf, uint32_t* shist,
-                               uint32_t* sscalar /* >= 4 words */) {
-    const int tid = threadIdx.x, nt = blockDim.x;
-    int nsel;
-    if (n <= (int64_t)K) {
-        nsel = (int)n;
-        for (int i = tid; i < nsel; i += nt) sbuf[i] = get(i);
-    } else {
-        uint64_t prefix = 0;
-        uint32_t need = (uint32_t)K;
-        for (int shift = 56; shift >= 0; shift -= 8) {
-            for (int i = tid; i < 256; i += nt) shist[i] = 0;
-            __syncthreads();
-            const uint64_t hmask = (shift == 56) ? 0ull : (~0ull << (shift + 8));
-            for (int64_t i = tid; i < n; i += nt) {
-                const uint64_t x = get(i);
-                if (((x ^ prefix) & hmask) == 0ull) atomicAdd(&shist[(x >> shift) & 255u], 1u);
-            }
-            __syncthreads();
-            if (tid < 32) {
-                // warp 0: find digit t with count(>t) < need <= count(>=t), scanning 255..0
-                uint32_t cnt[8];
-                uint32_t local = 0;
-#pragma unroll
-                for (int j = 0; j < 8; ++j) { cnt[j] = shist[255 - (tid * 8 + j)]; local += cnt[j]; }
-                uint32_t incl = local;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t t = __shfl_up_sync(FULL, incl, o);
-                    if (tid >= o) incl += t;
-                }
-                uint32_t c = incl - local;  // count of digits above this lane's group
-                int found = -1;
-                uint32_t above = 0;
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    if (found < 0 && c < need && c + cnt[j] >= need) { found = 255 - (tid * 8 + j); above = c; }
-                    c += cnt[j];
-                }
-                const unsigned m = __ballot_sync(FULL, found >= 0);
-                const int src = __ffs(m) - 1;
-                const int t = __shfl_sync(FULL, found, src);
-                const uint32_t ab = __shfl_sync(FULL, above, src);
-                if (tid == 0) { sscalar[0] = (uint32_t)t; sscalar[1] = ab; }
-            }
-            __syncthreads();
-            prefix |= (uint64_t)sscalar[0] << shift;
-            need -= sscalar[1];
-            __syncthreads();
-        }
-        // prefix == the K-th largest key; gather keys >= prefix (exactly K of them)
-        if (tid == 0) sscalar[2] = 0;
+__device__ int cta_radix_select(Get get, int64_t n, int K, uint64_t* sbuf, uint32_t* shist,
+                                uint32_t* sscalar) {
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
+    uint64_t prefix = 0;
+    uint32_t need = (uint32_t)K;
+    for (int shift = 56; shift >= 0; shift -= 8) {
+        for (int i = tid; i < 256; i += nt) shist[i] = 0;
         __syncthreads();
-        for (int64_t i = tid; i < n; i += nt) {
-            const uint64_t x = get(i);
-            if (x >= prefix) sbuf[atomicAdd(&sscalar[2], 1u)] = x;
+        const uint64_t hmask = (shift == 56) ? 0ull : (~0ull << (shift + 8));
+        for (int64_t base = 0; base < n; base += nt) {
+            const int64_t i = base + tid;
+            uint64_t x = 0;
+            bool act = false;
+            if (i < n) { x = get(i); act = ((x ^ prefix) & hmask) == 0ull; }
+            warp_hist_add(shist, (uint32_t)(x >> shift) & 255u, act);
         }
         __syncthreads();
-        nsel = K;
+        if (tid < 32) {
+            // warp 0: digit t with count(>t) < need <= count(>=t), scanning 255..0
+            uint32_t cnt[8];
+            uint32_t local = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) { cnt[j] = shist[255 - (tid * 8 + j)]; local += cnt[j]; }
+            uint32_t incl = local;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(FULL, incl, o);
+                if (tid >= o) incl += t;
+            }
+            uint32_t c = incl - local;
+            int found = -1;
+            uint32_t above = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (found < 0 && c < need && c + cnt[j] >= need) { found = 255 - (tid * 8 + j); above = c; }
+                c += cnt[j];
+            }
+            const unsigned m = __ballot_sync(FULL, found >= 0);
+            const int src = __ffs(m) - 1;
+            const int t = __shfl_sync(FULL, found, src);
+            const uint32_t ab = __shfl_sync(FULL, above, src);
+            if (tid == 0) { sscalar[0] = (uint32_t)t; sscalar[1] = ab; }
+        }
+        __syncthreads();
+        prefix |= (uint64_t)sscalar[0] << shift;
+        need -= sscalar[1];
+        __syncthreads();
     }
+    // prefix == the K-th largest key; gather the keys >= prefix (exactly K of them)
+    if (tid == 0) sscalar[2] = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < n; base += nt) {
+        const int64_t i = base + tid;
+        uint64_t x = 0;
+        bool take = false;
+        if (i < n) { x = get(i); take = x >= prefix; }
+        const unsigned m = __ballot_sync(FULL, take);
+        uint32_t pos = 0;
+        if (lane == 0 && m) pos = atomicAdd(&sscalar[2], (uint32_t)__popc(m));
+        pos = __shfl_sync(FULL, pos, 0);
+        if (take) sbuf[pos + __popc(m & ((1u << lane) - 1u))] = x;
+    }
+    __syncthreads();
+    return K;
+}
+
+__device__ __forceinline__ void cta_bitonic_desc(uint64_t* sbuf, int nsel) {
+    const int tid = threadIdx.x, nt = blockDim.x;
     int P = 1;
     while (P < nsel) P <<= 1;
     for (int i = nsel + tid; i < P; i += nt) sbuf[i] = 0ull;
     __syncthreads();
-    // bitonic sort, descending
     for (int size = 2; size <= P; size <<= 1) {
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
             for (int i = tid; i < (P >> 1); i += nt) {
@@ -185,6 +322,25 @@ __device__ int cta_select_topk(Get get, int64_t n, int K, uint64_t* sbuf, uint32
             __syncthreads();
         }
     }
+}
+
+template <typename Get>
+__device__ int cta_select_topk(Get get, int64_t n, int K, uint64_t* sbuf, uint64_t* scand,
+                               int64_t scand_cap, uint32_t* shist, uint32_t* sscalar) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    int nsel;
+    if (n <= (int64_t)K) {
+        nsel = (int)n;
+        for (int i = tid; i < nsel; i += nt) sbuf[i] = get(i);
+        __syncthreads();
+    } else if (scand && n <= scand_cap) {
+        for (int64_t i = tid; i < n; i += nt) scand[i] = get(i);
+        __syncthreads();
+        nsel = cta_radix_select([scand](int64_t i) { return scand[i]; }, n, K, sbuf, shist, sscalar);
+    } else {
+        nsel = cta_radix_select(get, n, K, sbuf, shist, sscalar);
+    }
+    cta_bitonic_desc(sbuf, nsel);
     return nsel;
 }
 

@@ -207,17 +207,20 @@ static int32_t padded_width(int32_t d, int esz) {
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads) merge_kernel(const uint64_t* __restrict__ gathered, int G,
                                                          int B, int K, int32_t* out_ids,
-                                                         float* out_scores) {
+                                                         float* out_scores, int64_t scand_cap) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint32_t sScalar[8];
+    const int P = pow2ceil_i(K);
     uint64_t* sbuf = reinterpret_cast<uint64_t*>(smem);
+    uint32_t* shist = reinterpret_cast<uint32_t*>(sbuf + P);
+    uint64_t* scand = reinterpret_cast<uint64_t*>(shist + 256);
     const int b = blockIdx.x;
     const int64_t n = (int64_t)G * K;
     auto get = [=](int64_t i) {
         const int64_t g = i / K, q = i - g * K;
         return __ldg(&gathered[(g * B + b) * (int64_t)K + q]);
     };
-    const int nsel = cta_select_topk(get, n, K, sbuf, reinterpret_cast<uint32_t*>(sbuf + pow2ceil_i(K)), sScalar);
+    const int nsel = cta_select_topk(get, n, K, sbuf, scand_cap > 0 ? scand : nullptr, scand_cap, shist, sScalar);
     // padding keys (0) may have been selected when fewer than K real keys exist: they sort last
     cta_write_topk(sbuf, nsel, K, out_ids + (size_t)b * K, out_scores + (size_t)b * K, nullptr);
 }
@@ -235,9 +238,13 @@ __global__ void decode_key_kernel(const uint2* __restrict__ hdr, const uint32_t*
 
 ebr_status run_merge(const uint64_t* gathered, int32_t G, int32_t batch, int32_t k,
                      int32_t* out_ids, float* out_scores, cudaStream_t stream) {
-    const size_t smem = (size_t)pow2ceil_i(k) * 8 + 256 * 4 + 64;
+    const size_t base = (size_t)pow2ceil_i(k) * 8 + 256 * 4;
+    const size_t cap_bytes = 200 * 1024 > base ? 200 * 1024 - base : 0;
+    int64_t scand_cap = std::min<int64_t>((int64_t)G * k, (int64_t)(cap_bytes / 8));
+    if (scand_cap < (int64_t)G * k) scand_cap = 0;   // too many: select straight from global
+    const size_t smem = base + (size_t)scand_cap * 8 + 64;
     EBR_CUDA(cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    merge_kernel<<<batch, kThreads, smem, stream>>>(gathered, G, batch, k, out_ids, out_scores);
+    merge_kernel<<<batch, kThreads, smem, stream>>>(gathered, G, batch, k, out_ids, out_scores, scand_cap);
     return cuda_check(cudaGetLastError(), "launch(merge)");
 }
 
@@ -461,8 +468,10 @@ ebr_status ebr_query_error(void* workspace, void* stream, uint32_t* flags) {
     if (!workspace) return set_error(EBR_EINVAL, "null workspace");
     uint32_t f = 0;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    EBR_CUDA(cudaMemcpyAsync(&f, workspace, 4, cudaMemcpyDeviceToHost, s));
-    EBR_CUDA(cudaMemsetAsync(workspace, 0, 4, s));
+    // workspace header: word 0 = state magic, word 1 = validation flags
+    uint32_t* flag_word = static_cast<uint32_t*>(workspace) + 1;
+    EBR_CUDA(cudaMemcpyAsync(&f, flag_word, 4, cudaMemcpyDeviceToHost, s));
+    EBR_CUDA(cudaMemsetAsync(flag_word, 0, 4, s));
     EBR_CUDA(cudaStreamSynchronize(s));
     if (flags) *flags = f;
     return f ? set_error(EBR_EDEVICE, "device validation flags 0x%x", f) : EBR_OK;

@@ -1,30 +1,32 @@
 // ebr_small.cu -- the latency path (small user batch, B <= 8 per launch): ONE cooperative,
-// persistent kernel per call that runs every step of the hot path:
+// persistent kernel per call (1 CTA per SM) runs every step of the hot path:
 //
-//   phase 0  A1 plan     : each CTA turns the batch's user slots into work items
-//                          (key i = base_f + v, w~ = w_i * x_i, the key's chunk span)  (P:277,
-//                          Alg. 2 l.352 "k_length")
-//   phase 1  per ad range [r0, r1) owned by the CTA, two warp roles run concurrently:
-//            wide warps  A2+A3: locate each item's chunks overlapping the range (interpolation
-//                          + 32-ary warp search), exclusive-scan the per-item piece counts and
-//                          hand 16-chunk pieces to warps from a shared counter (the paper's
-//                          ExclusiveScan + LoadBalance, Alg. 2 l.353-354), decode each
-//                          chunk warp-cooperatively and add w~ into a shared-memory fp32 array
-//                          (Alg. 2 l.358 AtomicAdd, but into SMEM instead of a global array)
-//            deep warps  A4: stream A's rows once from HBM with 16-byte non-allocating loads,
-//                          dot with the B user vectors held in registers (Eq. 1, fp32 FFMA)
-//            then A5 fuse s = deep + wide, write s to an L2-resident scratch and build a
-//            per-user 2048-bin histogram of ord(s)'s top 11 bits
-//   grid sync
-//   phase 3  A6a every CTA finds, per user, the histogram bin holding the K-th largest score
-//   phase 4  A6b compaction: every (user, ad) whose bin >= that bin is appended as a 64-bit key
-//   grid sync
-//   phase 5  A6c one CTA per user: exact radix select + bitonic sort of the candidates, write the
-//            sorted top-K (score desc, id asc; reading R13).
+//   A  plan     (every CTA, deterministic order): each valid user slot becomes a work item
+//               {key i = base_f + v, w~ = fl32(w_i x_i), the key's chunk span}, and an
+//               exclusive scan of the items' chunk counts gives a flat chunk space
+//               (Alg. 2 l.352-353 "k_length", "ExclusiveScan").
+//   B  three warp roles run concurrently:
+//       producer  (1 warp)  streams this CTA's contiguous rows of A into a 6-stage shared-memory
+//                 ring with bulk copies (TMA engine, cp.async.bulk + mbarrier complete_tx);
+//       deep      (8 warps) A4: dot of each staged row with the B user vectors held in registers
+//                 (Eq. 1, fp32 FFMA), written to an L2-resident score scratch;
+//       wide      (7 warps) A2+A3: every wide warp of the GPU takes an equal slice of the flat
+//                 chunk space (the paper's LoadBalance, Alg. 2 l.354, realised as a
+//                 static split of equal-cost 32-posting chunks), decodes 16 chunks per two memory
+//                 round trips and adds w~ with L2 reductions red.global.add.f32 into a per-(user,
+//                 ad) fp32 array (Alg. 2 l.358 "AtomicAdd(scores[..], w)").
+//   -- grid sync --
+//   C  A5 fuse: s = deep + wide (-0 -> +0), re-zero the wide array for the next call, per-user
+//      2048-bin histogram of ord(s)'s top 11 bits (warp-aggregated shared atomics).
+//   -- grid sync --
+//   D  A6a each CTA finds, per user, the bin holding the K-th largest score; A6b every (user, ad)
+//      in a bin >= it is appended as a 64-bit key kappa (warp-aggregated global atomics).
+//   -- grid sync --
+//   E  A6c one CTA per user: candidates staged in shared memory, exact radix select, bitonic sort,
+//      write the sorted top-K; re-zero the user's histogram and counter for the next call.
 //
-// The paper's design (T4: a global score array, 9 log2 groups, one global AtomicAdd per posting)
-// is prior art; here the whole query is one launch whose HBM traffic is A (read once) plus the
-// touched postings.
+// The workspace is self-maintaining: the first call on a workspace (magic word mismatch) zeroes
+// it inside the kernel; every call leaves it zeroed.  So a query is exactly one launch.
 #include <cooperative_groups.h>
 #include <algorithm>
 #include <cstdio>
@@ -37,17 +39,19 @@ namespace cg = cooperative_groups;
 namespace ebr {
 namespace {
 
-constexpr int kWideWarps = 8;
+constexpr int kProducerWarps = 1;
 constexpr int kDeepWarps = 8;
-static_assert((kWideWarps + kDeepWarps) * 32 == kThreads, "CTA layout");
-constexpr int kPiece = 16;     // chunks per load-balanced work unit
-constexpr int kDecodeU = 4;    // chunks decoded concurrently by one warp
-constexpr int kUnroll = 8;     // row-groups in flight per deep warp
+constexpr int kWideWarps = 7;
+static_assert((kProducerWarps + kDeepWarps + kWideWarps) * 32 == kThreads, "CTA layout");
+constexpr int kStages = 6;
+constexpr int kStageBytes = 16 * 1024;
+constexpr uint32_t kMagic = 0xEB200001u;
 
 struct SmallParams {
     // index
     const void* A;
     int32_t d, d_pad, lpr;      // lpr: lanes per row (row bytes = lpr * vpl * 16)
+    int32_t row_bytes, stage_rows;
     int64_t n_ads, n_pad;
     uint32_t ad_begin;
     const uint32_t* key_chunk_off;
@@ -64,11 +68,13 @@ struct SmallParams {
     const int32_t* user_feat;   // [B][F][S]
     const float* user_x;
     // workspace
-    uint32_t* err;
-    unsigned long long* timers;  // optional phase stamps (EBR_PHASE_TIMERS=1), else null
+    uint32_t* header;           // [0] magic, [1] error flags, then phase stamps
+    unsigned long long* timers; // optional phase stamps (EBR_PHASE_TIMERS=1), else null
+    uint32_t magic;
     uint32_t* ghist;            // [B][kHistBins]
     uint32_t* cand_count;       // [B]
-    float* scores;              // [B][n_pad]
+    float* scores;              // [B][n_pad]  deep, then fused score
+    float* wide;                // [B][n_pad]  wide accumulator (zero between calls)
     uint64_t* cand;             // [B][n_pad]
     // outputs
     int32_t* out_ids;           // [B][K] (already offset to this launch's first user)
@@ -78,10 +84,11 @@ struct SmallParams {
     int32_t R;                  // ads per range
     int32_t n_ranges;
     int32_t items_cap;          // >= B * F * S
+    int32_t smem_bytes;
 };
 
 struct Item {
-    uint32_t key, c0, c1, b;
+    uint32_t key, c0, c1, b, kwb;
     float w;
 };
 
@@ -109,14 +116,6 @@ template <> struct Vec<__nv_bfloat16> {
     }
 };
 
-__device__ __forceinline__ uint4 ldg_stream(const void* p) {
-    uint4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p));
-    return r;
-}
-
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -124,234 +123,252 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #define EBR_STAMP(i) do { if (p.timers && (tid & 31) == 0) atomicMax(&p.timers[i], gtimer()); } while (0)
 
-__device__ __forceinline__ void wide_bar() {
-    asm volatile("bar.sync 1, %0;" ::"n"(kWideWarps * 32));
-}
-
-// First chunk index in [c0, c1] whose first id is > x, guessing the position from x's relative
-// place in the shard (ad ids of a key are spread over the shard) and checking a 32-chunk window
-// before falling back to the 32-ary search.
-__device__ __forceinline__ uint32_t locate(const uint2* hdr, uint32_t c0, uint32_t c1, uint32_t x,
-                                          int64_t n_ads, int lane) {
-    if (c1 <= c0) return c0;
-    const uint32_t nch = c1 - c0;
-    uint32_t g = c0 + (uint32_t)(((double)x / (double)n_ads) * (double)nch);
-    g = min(g, c1 - 1u);
-    const uint32_t lo = (g >= c0 + 16u) ? g - 16u : c0;
-    const uint32_t hi = min(c1, lo + 32u);
-    const uint32_t p = lo + (uint32_t)lane;
-    const bool pred = (p < hi) && (__ldg(&hdr[p]).x <= x);
-    const uint32_t t = __popc(__ballot_sync(FULL, pred));
-    if ((t > 0u || lo == c0) && (t < hi - lo || hi == c1)) return lo + t;
-    if (t == 0u) return warp_upper_bound_first(hdr, c0, lo, x, lane);
-    return warp_upper_bound_first(hdr, hi, c1, x, lane);
-}
-
 template <typename T, int NB, int VPL>
 __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(1024) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int B = p.B, R = p.R;
-    // ---- shared-memory carve-up (phase 1) ----
-    float* sD = reinterpret_cast<float*>(smem);                         // [B][R] deep
-    float* sW = sD + (size_t)B * R;                                     // [B][R] wide
-    uint32_t* sHist = reinterpret_cast<uint32_t*>(sW + (size_t)B * R);  // [B][bins]
-    Item* sItems = reinterpret_cast<Item*>(sHist + (size_t)B * kHistBins);
-    uint32_t* sSpanLo = reinterpret_cast<uint32_t*>(sItems + p.items_cap);
-    uint32_t* sSpanHi = sSpanLo + p.items_cap;
-    uint32_t* sPieceOff = sSpanHi + p.items_cap;                        // [items_cap + 1]
-    __shared__ uint32_t sNItems, sPieceCounter, sScalar[8];
-    __shared__ uint32_t sBinStar[kSmallMaxB], sAbove[kSmallMaxB];
+    const cg::grid_group grid = cg::this_grid();
+    // ---- shared-memory carve-up ----
+    unsigned char* ring = smem;                                                   // [kStages][kStageBytes]
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + kStages * kStageBytes);   // [kStages]
+    uint64_t* empty = full + kStages;                                             // [kStages]
+    uint32_t* sHist = reinterpret_cast<uint32_t*>(empty + kStages);               // [B][bins]
+    Item* sItems = reinterpret_cast<Item*>(sHist + (size_t)B * kHistBins);        // [items_cap]
+    uint64_t* sChunkOff = reinterpret_cast<uint64_t*>(
+        (reinterpret_cast<uintptr_t>(sItems + p.items_cap) + 7) & ~(uintptr_t)7);  // [items_cap + 1]
+    __shared__ uint32_t sScan[40], sScalar[8], sNItems;
+    __shared__ uint32_t sBinStar[kSmallMaxB];
+    __shared__ int sInit;
 
-    // ---- phase 0: A1 plan (redundantly per CTA; B*F*S is small on this path) ----
     if (p.timers && blockIdx.x == 0 && tid == 0) p.timers[0] = gtimer();
-    if (tid == 0) sNItems = 0;
+    // ---- first use of this workspace: zero it (uniform decision across the grid) ----
+    if (tid == 0) {
+        sInit = (__ldcg(&p.header[0]) != p.magic);
+        for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kDeepWarps); }
+        fence_mbar_init();
+    }
     for (int i = tid; i < B * kHistBins; i += kThreads) sHist[i] = 0;
     __syncthreads();
-    const int nslot = B * p.n_fields * p.slots;
-    for (int i = tid; i < nslot; i += kThreads) {
-        const int b = i / (p.n_fields * p.slots);
-        const int f = (i / p.slots) % p.n_fields;
-        const int32_t v = p.user_feat[i];
-        if (v < 0) continue;
-        if (v >= p.field_card[f]) {            // bounds error: skip the slot, raise the flag
-            if (blockIdx.x == 0) atomicOr(p.err, 1u);
-            continue;
+    if (sInit) {
+        for (int range = blockIdx.x; range < p.n_ranges; range += gridDim.x) {
+            const int64_t r0 = (int64_t)range * R;
+            const int64_t r1 = (r0 + R < p.n_ads) ? r0 + R : p.n_ads;
+            for (int b = 0; b < kSmallMaxB; ++b)     // every user slot of the fixed layout
+                for (int64_t a = r0 + tid; a < r1; a += kThreads) p.wide[(size_t)b * p.n_pad + a] = 0.f;
         }
-        const uint32_t key = (uint32_t)(p.field_base[f] + v);
-        Item it;
-        it.key = key;
-        it.b = (uint32_t)b;
-        it.w = __fmul_rn(__ldg(&p.cross_w[key]), p.user_x[i]);   // w~ = fl32(w x)  (R10)
-        it.c0 = __ldg(&p.key_chunk_off[key]);
-        it.c1 = __ldg(&p.key_chunk_off[key + 1]);
-        if (it.c1 > it.c0) sItems[atomicAdd(&sNItems, 1u)] = it;
+        if (blockIdx.x == 0) {
+            for (int i = tid; i < kSmallMaxB * kHistBins; i += kThreads) p.ghist[i] = 0;
+            if (tid < kSmallMaxB) p.cand_count[tid] = 0;
+            if (tid == 0) p.header[1] = 0;
+        }
+        grid.sync();
     }
-    __syncthreads();
+
+    // ---- A: plan, deterministic item order ----
+    {
+        const int nslot = B * p.n_fields * p.slots;
+        const int per = (nslot + kThreads - 1) / kThreads;
+        const int s0 = min(nslot, tid * per), s1 = min(nslot, s0 + per);
+        uint32_t cnt = 0;
+        for (int i = s0; i < s1; ++i) {
+            const int f = (i / p.slots) % p.n_fields;
+            const int32_t v = p.user_feat[i];
+            if (v >= p.field_card[f]) {
+                if (blockIdx.x == 0) atomicOr(&p.header[1], 1u);   // bounds error: skip the slot
+                continue;
+            }
+            if (v < 0) continue;
+            const uint32_t key = (uint32_t)(p.field_base[f] + v);
+            if (__ldg(&p.key_chunk_off[key + 1]) > __ldg(&p.key_chunk_off[key])) ++cnt;
+        }
+        uint32_t total;
+        uint32_t pos = block_exclusive_scan(cnt, sScan, &total);
+        for (int i = s0; i < s1; ++i) {
+            const int b = i / (p.n_fields * p.slots);
+            const int f = (i / p.slots) % p.n_fields;
+            const int32_t v = p.user_feat[i];
+            if (v < 0 || v >= p.field_card[f]) continue;
+            const uint32_t key = (uint32_t)(p.field_base[f] + v);
+            Item it;
+            it.c0 = __ldg(&p.key_chunk_off[key]);
+            it.c1 = __ldg(&p.key_chunk_off[key + 1]);
+            if (it.c1 <= it.c0) continue;
+            it.key = key;
+            it.b = (uint32_t)b;
+            it.kwb = __ldg(&p.key_word_off[key]);
+            it.w = __fmul_rn(__ldg(&p.cross_w[key]), p.user_x[i]);   // w~ = fl32(w x), never an FMA (R10)
+            sItems[pos++] = it;
+        }
+        if (tid == 0) sNItems = total;
+        __syncthreads();
+        // exclusive scan of chunk counts over items
+        const int n_items = (int)sNItems;
+        const int per2 = (n_items + kThreads - 1) / kThreads;
+        const int i0 = min(n_items, tid * per2), i1 = min(n_items, i0 + per2);
+        uint32_t loc = 0;
+        for (int i = i0; i < i1; ++i) loc += sItems[i].c1 - sItems[i].c0;
+        uint32_t tot2;
+        uint64_t acc = block_exclusive_scan(loc, sScan, &tot2);
+        for (int i = i0; i < i1; ++i) { sChunkOff[i] = acc; acc += sItems[i].c1 - sItems[i].c0; }
+        if (tid == 0) sChunkOff[n_items] = tot2;
+        __syncthreads();
+    }
     const int n_items = (int)sNItems;
     EBR_STAMP(1);
 
-    // user vectors -> registers (deep warps), zero-padded to d_pad
-    using V = Vec<T>;
-    constexpr int E = V::E;
-    float u[NB][VPL][E];
-    const int lpr = p.lpr;
-    const int sub = lane / lpr, li = lane % lpr, rpw = 32 / lpr;
-#pragma unroll
-    for (int b = 0; b < NB; ++b)
-#pragma unroll
-        for (int v = 0; v < VPL; ++v)
-#pragma unroll
-            for (int e = 0; e < E; ++e) {
-                const int j = (li + v * lpr) * E + e;
-                u[b][v][e] = (b < B && j < p.d) ? V::elem(p.U, (int64_t)b * p.d + j) : 0.f;
-            }
-
-    // ---- phase 1: ranges ----
-    for (int range = blockIdx.x; range < p.n_ranges; range += gridDim.x) {
-        const int64_t r0 = (int64_t)range * R;
-        const int64_t r1 = ((r0 + R < p.n_ads) ? r0 + R : p.n_ads);
-        const int rn = (int)(r1 - r0);
-        for (int i = tid; i < B * R; i += kThreads) sW[i] = 0.f;
-        if (tid == 0) sPieceCounter = 0;
-        __syncthreads();
-        if (warp < kWideWarps) {
-            // ---------- wide: spans ----------
-            for (int it = warp; it < n_items; it += kWideWarps) {
-                const Item t = sItems[it];
-                uint32_t lo = locate(p.hdr, t.c0, t.c1, (uint32_t)r0, p.n_ads, lane);
-                if (lo > t.c0) lo -= 1u;                // chunk that may contain r0
-                const uint32_t hi = locate(p.hdr, lo, t.c1, (uint32_t)(r1 - 1), p.n_ads, lane);
-                if (lane == 0) { sSpanLo[it] = lo; sSpanHi[it] = hi; }
-            }
-            wide_bar();
-            // ---------- exclusive scan of piece counts (warp 0) ----------
-            if (warp == 0) {
-                uint32_t carry = 0;
-                for (int base = 0; base < n_items; base += 32) {
-                    const int it = base + lane;
-                    const uint32_t np = (it < n_items) ? (sSpanHi[it] - sSpanLo[it] + kPiece - 1) / kPiece : 0u;
-                    uint32_t incl = np;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const uint32_t x = __shfl_up_sync(FULL, incl, o);
-                        if (lane >= o) incl += x;
-                    }
-                    if (it < n_items) sPieceOff[it] = carry + incl - np;
-                    carry += __shfl_sync(FULL, incl, 31);
-                }
-                if (lane == 0) sPieceOff[n_items] = carry;
-            }
-            wide_bar();
-            const uint32_t total = sPieceOff[n_items];
-            // ---------- load-balanced decode + accumulate ----------
-            while (true) {
-                uint32_t unit = 0;
-                if (lane == 0) unit = atomicAdd(&sPieceCounter, 1u);
-                unit = __shfl_sync(FULL, unit, 0);
-                if (unit >= total) break;
-                // item = last it with sPieceOff[it] <= unit
-                int lo_i = 0, hi_i = n_items - 1;
-                while (lo_i < hi_i) {
-                    const int mid = (lo_i + hi_i + 1) >> 1;
-                    if (sPieceOff[mid] <= unit) lo_i = mid; else hi_i = mid - 1;
-                }
-                const Item t = sItems[lo_i];
-                const uint32_t cb = sSpanLo[lo_i] + (unit - sPieceOff[lo_i]) * kPiece;
-                const uint32_t ce = min(cb + (uint32_t)kPiece, sSpanHi[lo_i]);
-                const uint32_t kwb = __ldg(&p.key_word_off[t.key]);
-                float* wrow = sW + (size_t)t.b * R;
-                for (uint32_t c = cb; c < ce; c += kDecodeU) {
-                    uint32_t ids[kDecodeU];
-                    bool ok[kDecodeU];
-#pragma unroll
-                    for (int q = 0; q < kDecodeU; ++q) {
-                        ok[q] = false;
-                        ids[q] = 0;
-                        if (c + q < ce) ok[q] = decode_chunk(p.hdr, p.payload, kwb, c + q, lane, ids[q]);
-                    }
-#pragma unroll
-                    for (int q = 0; q < kDecodeU; ++q) {
-                        if (ok[q] && ids[q] >= (uint32_t)r0 && ids[q] < (uint32_t)r1)
-                            smem_add(&wrow[ids[q] - (uint32_t)r0], t.w);
-                    }
-                }
-            }
-            EBR_STAMP(2);
-        } else {
-            // ---------- deep: stream rows [r0, r1) ----------
-            const int dw = warp - kWideWarps;
+    // ---- B: producer / deep / wide ----
+    if (warp == 0) {
+        if (lane == 0) {
             const char* Abase = reinterpret_cast<const char*>(p.A);
-            const int64_t row_bytes = (int64_t)p.d_pad * sizeof(T);
-            const int64_t step = (int64_t)kDeepWarps * rpw * kUnroll;
-            for (int64_t base = r0 + (int64_t)dw * rpw * kUnroll; base < r1; base += step) {
-                uint4 av[kUnroll][VPL];
-#pragma unroll
-                for (int q = 0; q < kUnroll; ++q) {
-                    const int64_t row = base + q * rpw + sub;
-#pragma unroll
-                    for (int v = 0; v < VPL; ++v) {
-                        if (row < r1)
-                            av[q][v] = ldg_stream(Abase + row * row_bytes + (int64_t)(li + v * lpr) * 16);
-                        else
-                            av[q][v] = make_uint4(0, 0, 0, 0);
-                    }
+            uint32_t g = 0;
+            for (int range = blockIdx.x; range < p.n_ranges; range += gridDim.x) {
+                const int64_t r0 = (int64_t)range * R;
+                const int64_t r1 = (r0 + R < p.n_ads) ? r0 + R : p.n_ads;
+                for (int64_t s0 = r0; s0 < r1; s0 += p.stage_rows, ++g) {
+                    const int rows = (int)((r1 - s0 < p.stage_rows) ? (r1 - s0) : p.stage_rows);
+                    const int slot = g % kStages;
+                    const uint32_t round = g / kStages;
+                    if (round > 0) mbar_wait(&empty[slot], (round - 1) & 1);
+                    const uint32_t bytes = (uint32_t)rows * (uint32_t)p.row_bytes;
+                    mbar_arrive_expect_tx(&full[slot], bytes);
+                    bulk_g2s(ring + (size_t)slot * kStageBytes, Abase + s0 * p.row_bytes, bytes, &full[slot]);
                 }
+            }
+        }
+    } else if (warp <= kDeepWarps) {
+        using V = Vec<T>;
+        constexpr int E = V::E;
+        const int dw = warp - 1;
+        const int lpr = p.lpr;
+        const int sub = lane / lpr, li = lane % lpr, rpw = 32 / lpr;
+        float u[NB][VPL][E];
 #pragma unroll
-                for (int q = 0; q < kUnroll; ++q) {
+        for (int b = 0; b < NB; ++b)
+#pragma unroll
+            for (int v = 0; v < VPL; ++v)
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const int j = (li + v * lpr) * E + e;
+                    u[b][v][e] = (b < B && j < p.d) ? V::elem(p.U, (int64_t)b * p.d + j) : 0.f;
+                }
+        uint32_t g = 0;
+        for (int range = blockIdx.x; range < p.n_ranges; range += gridDim.x) {
+            const int64_t r0 = (int64_t)range * R;
+            const int64_t r1 = (r0 + R < p.n_ads) ? r0 + R : p.n_ads;
+            for (int64_t s0 = r0; s0 < r1; s0 += p.stage_rows, ++g) {
+                const int rows = (int)((r1 - s0 < p.stage_rows) ? (r1 - s0) : p.stage_rows);
+                const int slot = g % kStages;
+                mbar_wait(&full[slot], (g / kStages) & 1);
+                const unsigned char* st = ring + (size_t)slot * kStageBytes;
+                for (int jb = dw * rpw; jb < rows; jb += kDeepWarps * rpw) {
+                    const int j = jb + sub;
+                    const bool ok = j < rows;
                     float acc[NB];
 #pragma unroll
                     for (int b = 0; b < NB; ++b) acc[b] = 0.f;
 #pragma unroll
                     for (int v = 0; v < VPL; ++v) {
+                        uint4 raw = make_uint4(0, 0, 0, 0);
+                        if (ok) raw = *reinterpret_cast<const uint4*>(st + (size_t)j * p.row_bytes + (size_t)(li + v * lpr) * 16);
                         float a[E];
-                        V::unpack(av[q][v], a);
+                        V::unpack(raw, a);
 #pragma unroll
                         for (int b = 0; b < NB; ++b)
 #pragma unroll
                             for (int e = 0; e < E; ++e) acc[b] = fmaf(a[e], u[b][v][e], acc[b]);
                     }
 #pragma unroll
-                    for (int b = 0; b < NB; ++b)
-                        for (int o = lpr >> 1; o > 0; o >>= 1) acc[b] += __shfl_xor_sync(FULL, acc[b], o);
-                    const int64_t row = base + q * rpw + sub;
-                    if (li == 0 && row < r1) {
+                    for (int o = 16; o > 0; o >>= 1)
+                        if (o < lpr) {
+#pragma unroll
+                            for (int b = 0; b < NB; ++b) acc[b] += __shfl_xor_sync(FULL, acc[b], o);
+                        }
+                    if (ok && li == 0) {
 #pragma unroll
                         for (int b = 0; b < NB; ++b)
-                            if (b < B) sD[(size_t)b * R + (row - r0)] = acc[b];
+                            if (b < B) __stcg(&p.scores[(size_t)b * p.n_pad + s0 + j], acc[b]);
                     }
                 }
-            }
-            EBR_STAMP(3);
-        }
-        __syncthreads();
-        // ---------- A5 fuse + histogram ----------
-        for (int i = tid; i < B * R; i += kThreads) {
-            const int b = i / R, r = i - b * R;
-            if (r < rn) {
-                float s = sD[i] + sW[i];
-                if (s == 0.f) s = 0.f;                  // -0 -> +0 (R14)
-                __stcg(&p.scores[(size_t)b * p.n_pad + r0 + r], s);
-                atomicAdd(&sHist[b * kHistBins + (ord_of(s) >> (32 - kHistBits))], 1u);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[slot]);
             }
         }
-        __syncthreads();
+        EBR_STAMP(3);
+    } else {
+        // wide: equal slices of the flat chunk space over every wide warp of the grid
+        const uint64_t Ttot = sChunkOff[n_items];
+        const uint64_t nw = (uint64_t)gridDim.x * kWideWarps;
+        const uint64_t gw = (uint64_t)blockIdx.x * kWideWarps + (warp - 1 - kDeepWarps);
+        const uint64_t f0 = Ttot * gw / nw, f1 = Ttot * (gw + 1) / nw;
+        if (f0 < f1) {
+            int lo = 0, hi = n_items - 1;   // last item with sChunkOff <= f0
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (sChunkOff[mid] <= f0) lo = mid; else hi = mid - 1;
+            }
+            int it = lo;
+            uint64_t f = f0;
+            while (f < f1) {
+                while (sChunkOff[it + 1] <= f) ++it;
+                const Item t = sItems[it];
+                const uint32_t cb = t.c0 + (uint32_t)(f - sChunkOff[it]);
+                uint64_t nn = f1 - f;
+                if (nn > 16) nn = 16;
+                if (sChunkOff[it + 1] - f < nn) nn = sChunkOff[it + 1] - f;
+                const uint32_t n = (uint32_t)nn;
+                float* dst = p.wide + (size_t)t.b * p.n_pad;
+                const float w = t.w;
+                decode_unit16(p.hdr, p.payload, t.kwb, cb, cb + n, lane,
+                              [dst, w](uint32_t id) { atomicAdd(&dst[id], w); });
+                f += n;
+            }
+        }
+        EBR_STAMP(2);
     }
+    EBR_STAMP(4);
+    grid.sync();
+    EBR_STAMP(5);
+
+    // ---- C: fuse + histogram ----
+    for (int range = blockIdx.x; range < p.n_ranges; range += gridDim.x) {
+        const int64_t r0 = (int64_t)range * R;
+        const int64_t r1 = (r0 + R < p.n_ads) ? r0 + R : p.n_ads;
+        for (int b = 0; b < B; ++b) {
+            float* sc = p.scores + (size_t)b * p.n_pad;
+            float* wd = p.wide + (size_t)b * p.n_pad;
+            for (int64_t base = r0; base < r1; base += kThreads) {
+                const int64_t a = base + tid;
+                const bool ok = a < r1;
+                uint32_t bin = 0;
+                if (ok) {
+                    float s = __ldcg(&sc[a]) + __ldcg(&wd[a]);
+                    __stcg(&wd[a], 0.f);
+                    if (s == 0.f) s = 0.f;                      // -0 -> +0 (R14)
+                    __stcg(&sc[a], s);
+                    bin = ord_of(s) >> (32 - kHistBits);
+                }
+                warp_hist_add(sHist + b * kHistBins, bin, ok);
+            }
+        }
+    }
+    __syncthreads();
     for (int i = tid; i < B * kHistBins; i += kThreads) {
         const uint32_t c = sHist[i];
         if (c) atomicAdd(&p.ghist[i], c);
     }
-    EBR_STAMP(4);
+    EBR_STAMP(6);
+    grid.sync();
+    EBR_STAMP(7);
 
-    cg::this_grid().sync();
-    EBR_STAMP(5);
-
-    // ---- phase 3: threshold bin per user (warp b handles user b) ----
+    // ---- D: threshold bin per user (warp b), then compaction ----
     if (warp < B) {
         const uint32_t* h = p.ghist + (size_t)warp * kHistBins;
         constexpr int PER = kHistBins / 32;
+        uint32_t cnt[PER];
         uint32_t local = 0;
-        for (int j = 0; j < PER; ++j) local += __ldcg(&h[kHistBins - 1 - (lane * PER + j)]);
+#pragma unroll
+        for (int j = 0; j < PER; ++j) { cnt[j] = __ldcg(&h[kHistBins - 1 - (lane * PER + j)]); local += cnt[j]; }
         uint32_t incl = local;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -360,61 +377,65 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
         }
         uint32_t c = incl - local;
         int found = -1;
-        uint32_t above = 0;
         const uint32_t K = (uint32_t)p.K;
-        if (c < K && c + local >= K) {
-            for (int j = 0; j < PER; ++j) {
-                const int bin = kHistBins - 1 - (lane * PER + j);
-                const uint32_t cnt = __ldcg(&h[bin]);
-                if (found < 0 && c < K && c + cnt >= K) { found = bin; above = c; }
-                c += cnt;
-            }
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            if (found < 0 && c < K && c + cnt[j] >= K) found = kHistBins - 1 - (lane * PER + j);
+            c += cnt[j];
         }
         const unsigned m = __ballot_sync(FULL, found >= 0);
-        const int src = m ? __ffs(m) - 1 : 0;
-        const int fb = __shfl_sync(FULL, found, src);
-        const uint32_t ab = __shfl_sync(FULL, above, src);
-        if (lane == 0) {
-            sBinStar[warp] = m ? (uint32_t)fb : 0u;  // fewer than K ads: everything is a candidate
-            sAbove[warp] = m ? ab : 0u;
-        }
+        const int fb = __shfl_sync(FULL, found, m ? __ffs(m) - 1 : 0);
+        if (lane == 0) sBinStar[warp] = m ? (uint32_t)fb : 0u;   // < K ads: all are candidates
     }
     __syncthreads();
-
-    // ---- phase 4: compaction of candidates ----
     for (int range = blockIdx.x; range < p.n_ranges; range += gridDim.x) {
         const int64_t r0 = (int64_t)range * R;
-        const int64_t r1 = ((r0 + R < p.n_ads) ? r0 + R : p.n_ads);
-        const int rn = (int)(r1 - r0);
-        for (int i = tid; i < B * R; i += kThreads) {
-            const int b = i / R, r = i - b * R;
-            if (r < rn) {
-                const float s = __ldcg(&p.scores[(size_t)b * p.n_pad + r0 + r]);
-                if ((ord_of(s) >> (32 - kHistBits)) >= sBinStar[b]) {
-                    const uint32_t pos = atomicAdd(&p.cand_count[b], 1u);
-                    p.cand[(size_t)b * p.n_pad + pos] = kappa_of(s, p.ad_begin + (uint32_t)(r0 + r));
+        const int64_t r1 = (r0 + R < p.n_ads) ? r0 + R : p.n_ads;
+        for (int b = 0; b < B; ++b) {
+            const float* sc = p.scores + (size_t)b * p.n_pad;
+            const uint32_t bs = sBinStar[b];
+            for (int64_t base = r0; base < r1; base += kThreads) {
+                const int64_t a = base + tid;
+                float s = 0.f;
+                bool take = false;
+                if (a < r1) { s = __ldcg(&sc[a]); take = (ord_of(s) >> (32 - kHistBits)) >= bs; }
+                const unsigned m = __ballot_sync(FULL, take);
+                if (m) {
+                    const int leader = __ffs(m) - 1;
+                    uint32_t pos = 0;
+                    if (lane == leader) pos = atomicAdd(&p.cand_count[b], (uint32_t)__popc(m));
+                    pos = __shfl_sync(FULL, pos, leader);
+                    if (take)
+                        p.cand[(size_t)b * p.n_pad + pos + __popc(m & ((1u << lane) - 1u))] =
+                            kappa_of(s, p.ad_begin + (uint32_t)a);
                 }
             }
         }
     }
+    EBR_STAMP(8);
+    grid.sync();
+    EBR_STAMP(9);
 
-    EBR_STAMP(6);
-    cg::this_grid().sync();
-    EBR_STAMP(7);
-
-    // ---- phase 5: exact selection, one CTA per user ----
+    // ---- E: exact selection, one CTA per user; leave the workspace zeroed ----
     for (int b = blockIdx.x; b < B; b += gridDim.x) {
+        const int P = pow2ceil_i(p.K);
         uint64_t* sbuf = reinterpret_cast<uint64_t*>(smem);
+        uint32_t* shist = reinterpret_cast<uint32_t*>(sbuf + P);
+        uint64_t* scand = reinterpret_cast<uint64_t*>(shist + 256);
+        const int64_t scap = ((int64_t)p.smem_bytes - (int64_t)P * 8 - 1024) / 8;
         const int64_t n = (int64_t)__ldcg(&p.cand_count[b]);
         const uint64_t* cb = p.cand + (size_t)b * p.n_pad;
         const int nsel = cta_select_topk([cb](int64_t i) { return __ldcg(&cb[i]); }, n, p.K, sbuf,
-                                         reinterpret_cast<uint32_t*>(sbuf + pow2ceil_i(p.K)), sScalar);
+                                         scand, scap, shist, sScalar);
         cta_write_topk(sbuf, nsel, p.K, p.out_ids ? p.out_ids + (size_t)b * p.K : nullptr,
                        p.out_scores ? p.out_scores + (size_t)b * p.K : nullptr,
                        p.out_keys ? p.out_keys + (size_t)b * p.K : nullptr);
+        for (int i = tid; i < kHistBins; i += kThreads) p.ghist[(size_t)b * kHistBins + i] = 0;
+        if (tid == 0) p.cand_count[b] = 0;
         __syncthreads();
-        EBR_STAMP(8);
     }
+    if (blockIdx.x == 0 && tid == 0) p.header[0] = p.magic;
+    EBR_STAMP(10);
 }
 
 // --------------------------------------------------------------------------------------------
@@ -433,17 +454,18 @@ kern_t pick_kernel(int nb, int vpl) {
 }
 
 struct SmallLayout {
-    size_t off_err, off_hist, off_count, off_scores, off_cand, total;
+    size_t off_header, off_hist, off_count, off_scores, off_wide, off_cand, total;
 };
 
 SmallLayout small_layout(const ebr_index* idx, int B) {
     SmallLayout L;
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
     size_t o = 0;
-    L.off_err = o;    o = al(o + 16 + 16 * 8);   // error word + 16 phase stamps
+    L.off_header = o; o = al(o + 16 + 16 * 8);   // magic, error word, 16 phase stamps
     L.off_hist = o;   o = al(o + (size_t)B * kHistBins * 4);
     L.off_count = o;  o = al(o + (size_t)B * 4);
     L.off_scores = o; o = al(o + (size_t)B * idx->n_pad * 4);
+    L.off_wide = o;   o = al(o + (size_t)B * idx->n_pad * 4);
     L.off_cand = o;   o = al(o + (size_t)B * idx->n_pad * 8);
     L.total = o;
     return L;
@@ -456,37 +478,30 @@ size_t small_workspace_bytes(const ebr_index* idx, int32_t slots, int32_t k) {
     return small_layout(idx, kSmallMaxB).total;
 }
 
-// Runs users [0, B) (B <= kSmallMaxB) of one launch.
+// Runs users [b0, b0 + B) (B <= kSmallMaxB) in one launch.
 ebr_status run_small(const QueryArgs& q, int b0, int B) {
     const ebr_index* idx = q.idx;
-    SmallLayout L = small_layout(idx, B);
+    SmallLayout L = small_layout(idx, kSmallMaxB);   // fixed layout: any B shares one workspace
     char* ws = static_cast<char*>(q.workspace);
     const int esz = idx->dtype == EBR_BF16 ? 2 : 4;
     const int row_bytes = idx->d_pad * esz;
     int lpr, vpl;
     if (row_bytes <= 512) { lpr = row_bytes / 16; vpl = 1; }
     else { lpr = 32; vpl = row_bytes / 512; }
+    if (row_bytes > kStageBytes) return set_error(EBR_EUNSUPPORTED, "embedding row of %d bytes is too wide", row_bytes);
     int nb = 1;
     while (nb < B) nb <<= 1;
     kern_t k = idx->dtype == EBR_BF16 ? pick_kernel<__nv_bfloat16>(nb, vpl) : pick_kernel<float>(nb, vpl);
     if (!k) return set_error(EBR_EUNSUPPORTED, "embedding row of %d bytes is not supported", row_bytes);
 
     const int items_cap = B * idx->n_fields * q.slots;
-    const size_t item_bytes = (size_t)items_cap * (sizeof(Item) + 12) + 16;
-    const size_t hist_bytes = (size_t)B * kHistBins * 4;
-    const size_t sel_bytes = (size_t)pow2ceil_i(q.k) * 8 + 256 * 4 + 64;
-    const size_t smem_cap = 220 * 1024;
-    if (item_bytes + hist_bytes + 8 * 1024 > smem_cap)
-        return set_error(EBR_EUNSUPPORTED, "too many user slots for the latency path (%d)", items_cap);
-    // range size: one range per CTA if it fits, else as large as shared memory allows
-    const int sms = idx->sm_count;
-    int64_t R = (idx->n_ads + sms - 1) / sms;
-    const int64_t R_fit = (int64_t)((smem_cap - item_bytes - hist_bytes) / (8 * (size_t)B));
-    R = std::min<int64_t>(R, R_fit);
-    R = std::max<int64_t>(32, R & ~(int64_t)31);
-    const size_t p1_bytes = (size_t)8 * B * R + hist_bytes + item_bytes;
-    const size_t smem = std::max(p1_bytes, sel_bytes);
-    if (smem > 227 * 1024) return set_error(EBR_EUNSUPPORTED, "k=%d needs too much shared memory", q.k);
+    const size_t p1 = (size_t)kStages * kStageBytes + 2 * kStages * 8 + (size_t)B * kHistBins * 4 +
+                      (size_t)items_cap * sizeof(Item) + 8 + (size_t)(items_cap + 1) * 8;
+    const size_t sel_min = (size_t)pow2ceil_i(q.k) * 8 + 1024 + 64 * 1024;   // + >= 8k staged candidates
+    const size_t smem = std::max(p1, sel_min);
+    if (smem > 227 * 1024)
+        return set_error(EBR_EUNSUPPORTED, "latency path: %d user slots / k=%d need %zu B of shared memory",
+                         items_cap, q.k, smem);
 
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(small)");
@@ -494,8 +509,12 @@ ebr_status run_small(const QueryArgs& q, int b0, int B) {
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, smem);
     if (e != cudaSuccess || occ < 1) return cuda_check(e == cudaSuccess ? cudaErrorInvalidConfiguration : e, "occupancy(small)");
 
+    const int sms = idx->sm_count;
+    int64_t R = (idx->n_ads + sms - 1) / sms;
+    R = std::max<int64_t>(32, (R + 31) & ~(int64_t)31);
     SmallParams p;
     p.A = idx->A; p.d = idx->d; p.d_pad = idx->d_pad; p.lpr = lpr;
+    p.row_bytes = row_bytes; p.stage_rows = kStageBytes / row_bytes;
     p.n_ads = idx->n_ads; p.n_pad = idx->n_pad; p.ad_begin = (uint32_t)idx->ad_begin;
     p.key_chunk_off = idx->key_chunk_off; p.key_word_off = idx->key_word_off;
     p.hdr = idx->chunk_hdr; p.payload = idx->payload; p.cross_w = idx->cross_w;
@@ -504,12 +523,15 @@ ebr_status run_small(const QueryArgs& q, int b0, int B) {
     p.B = B; p.slots = q.slots; p.K = q.k;
     p.user_feat = q.user_feat + (size_t)b0 * idx->n_fields * q.slots;
     p.user_x = q.user_x + (size_t)b0 * idx->n_fields * q.slots;
-    p.err = reinterpret_cast<uint32_t*>(ws + L.off_err);
+    p.header = reinterpret_cast<uint32_t*>(ws + L.off_header);
     static const bool timers_on = getenv("EBR_PHASE_TIMERS") && getenv("EBR_PHASE_TIMERS")[0] == '1';
-    p.timers = timers_on ? reinterpret_cast<unsigned long long*>(ws + L.off_err + 16) : nullptr;
+    p.timers = timers_on ? reinterpret_cast<unsigned long long*>(ws + L.off_header + 16) : nullptr;
+    // the magic ties the workspace's zeroed state to this index geometry
+    p.magic = kMagic ^ (uint32_t)((uint64_t)idx->n_pad * 2654435761ull);
     p.ghist = reinterpret_cast<uint32_t*>(ws + L.off_hist);
     p.cand_count = reinterpret_cast<uint32_t*>(ws + L.off_count);
     p.scores = reinterpret_cast<float*>(ws + L.off_scores);
+    p.wide = reinterpret_cast<float*>(ws + L.off_wide);
     p.cand = reinterpret_cast<uint64_t*>(ws + L.off_cand);
     p.out_ids = q.out_ids ? q.out_ids + (size_t)b0 * q.k : nullptr;
     p.out_scores = q.out_scores ? q.out_scores + (size_t)b0 * q.k : nullptr;
@@ -517,13 +539,13 @@ ebr_status run_small(const QueryArgs& q, int b0, int B) {
     p.R = (int32_t)R;
     p.n_ranges = (int32_t)((idx->n_ads + R - 1) / R);
     p.items_cap = items_cap;
+    p.smem_bytes = (int32_t)smem;
 
-    // zero the per-call counters (histograms + candidate counts are contiguous)
-    // the first launch of a call also clears the device error word (flags of the last call)
-    const size_t z0 = (b0 == 0) ? L.off_err : L.off_hist;
-    e = cudaMemsetAsync(ws + z0, 0, L.off_scores - z0, q.stream);
-    if (e != cudaSuccess) return cuda_check(e, "memset(small)");
-    const int grid = std::max(1, std::min<int>(p.n_ranges, occ * sms));
+    if (timers_on) {
+        e = cudaMemsetAsync(ws + L.off_header + 16, 0, 16 * 8, q.stream);
+        if (e != cudaSuccess) return cuda_check(e, "memset(timers)");
+    }
+    const int grid = std::max(1, std::min<int>(std::max(p.n_ranges, B), occ * sms));
     void* args[] = {&p};
     e = cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(kThreads), args, smem, q.stream);
     if (e != cudaSuccess) return cuda_check(e, "launch(small)");

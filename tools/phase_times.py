@@ -23,14 +23,14 @@ ws = torch.empty(idx.workspace_bytes(Bn, S, c.k), dtype=torch.uint8, device=dev)
 ids = torch.empty((Bn, c.k), dtype=torch.int32, device=dev)
 sc = torch.empty((Bn, c.k), dtype=torch.float32, device=dev)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-names = ["start", "plan", "wide_done", "deep_done", "phase1_end", "sync1", "compact_end", "sync2", "select_end"]
+names = ["start", "plan", "wide_done", "deep_done", "B_end", "sync1", "fuse_end", "sync2", "compact_end", "sync3", "select_end"]
 acc = []
 for it in range(30):
     flush.fill_(it)
     torch.cuda.synchronize()
     ebr.score_topk(idx, emb, feat, x, c.k, ids, sc, ws)
     torch.cuda.synchronize()
-    t = ws[16:16 + 9 * 8].cpu().numpy().view(np.uint64).astype(np.float64)
+    t = ws[16:16 + 11 * 8].cpu().numpy().view(np.uint64).astype(np.float64)
     acc.append((t - t[0]) / 1e3)
 a = np.median(np.array(acc[5:]), axis=0)
 for n, v in zip(names, a):
