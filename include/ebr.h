@@ -112,10 +112,9 @@ size_t ebr_workspace_bytes(const ebr_index *idx, int32_t batch, int32_t slots, i
  *  out_ids    device, [batch][k] int32 global ad ids (ad_begin + local), best first.
  *  out_scores device, [batch][k] fp32 s(u,a) of those ads.
  *  workspace  device, >= ebr_workspace_bytes(idx, batch, slots, k) bytes, 256-byte aligned,
- *             caller-owned; one in-flight call per workspace.  Its contents are managed by the
- *             library: the first call on a buffer (or after it was used with an index of another
- *             size) initialises it inside the kernel and every call leaves it ready for the next,
- *             so each query is a single kernel launch.  Do not modify it between calls.
+ *             caller-owned; one in-flight call per workspace.  Initialise a new buffer once with
+ *             ebr_workspace_init(); every call then leaves it ready for the next, so each query
+ *             is a single kernel launch.  Do not modify it between calls.
  * Errors: EBR_EINVAL for batch < 1, slots out of range, k out of range, undersized workspace;
  *         EBR_ECUDA on a launch failure.  Duplicate (f,v) slots of one user add (reading A3).
  */
@@ -140,6 +139,13 @@ ebr_status ebr_score_topk_keys(const ebr_index *idx, const void *user_emb, int32
  * was outside [-1, V_f).  Returns EBR_EDEVICE if any bit was set, EBR_OK otherwise.
  */
 ebr_status ebr_query_error(void *workspace, void *stream, uint32_t *flags);
+
+/*
+ * async.  Prepares a freshly allocated workspace (zero fill + state word) for use with `idx`.
+ * Required once per buffer before its first ebr_score_topk* / ebr_score_topk_host call (and
+ * again if the buffer was written by anything else).  bytes = the buffer size.
+ */
+ebr_status ebr_workspace_init(const ebr_index *idx, void *workspace, size_t bytes, void *stream);
 
 /*
  * End-to-end variant with HOST buffers (the e2e measurement): copies user_emb, user_feat and

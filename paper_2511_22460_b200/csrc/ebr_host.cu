@@ -46,6 +46,7 @@ ebr_status cuda_check(cudaError_t e, const char* what) {
     } while (0)
 
 ebr_status run_small(const QueryArgs& q, int b0, int B);
+uint32_t workspace_magic(const ebr_index* idx);
 size_t small_workspace_bytes(const ebr_index* idx, int32_t slots, int32_t k);
 
 // ------------------------------------------------------------------------------------------
@@ -462,6 +463,21 @@ ebr_status ebr_score_topk_keys(const ebr_index* idx, const void* user_emb, int32
     if (!out_keys) return set_error(EBR_EINVAL, "null out_keys");
     return query_common(idx, user_emb, batch, user_feat, user_x, slots, k, nullptr, nullptr,
                         out_keys, workspace, workspace_bytes_, stream);
+}
+
+ebr_status ebr_workspace_init(const ebr_index* idx, void* workspace, size_t bytes, void* stream) {
+    if (!idx || !workspace) return set_error(EBR_EINVAL, "null argument");
+    if (reinterpret_cast<uintptr_t>(workspace) & 255) return set_error(EBR_EINVAL, "workspace not 256-byte aligned");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int prev = -1;
+    cudaGetDevice(&prev);
+    if (prev != idx->device) cudaSetDevice(idx->device);
+    EBR_CUDA(cudaMemsetAsync(workspace, 0, bytes, s));
+    const uint32_t magic = workspace_magic(idx);
+    EBR_CUDA(cudaMemcpyAsync(workspace, &magic, 4, cudaMemcpyHostToDevice, s));
+    EBR_CUDA(cudaStreamSynchronize(s));   // `magic` lives on this stack frame
+    if (prev >= 0 && prev != idx->device) cudaSetDevice(prev);
+    return EBR_OK;
 }
 
 ebr_status ebr_query_error(void* workspace, void* stream, uint32_t* flags) {

@@ -5,16 +5,18 @@
 //               {key i = base_f + v, w~ = fl32(w_i x_i), the key's chunk span}, and an
 //               exclusive scan of the items' chunk counts gives a flat chunk space
 //               (Alg. 2 l.352-353 "k_length", "ExclusiveScan").
-//   B  three warp roles run concurrently:
-//       producer  (1 warp)  streams this CTA's contiguous rows of A into a 6-stage shared-memory
-//                 ring with bulk copies (TMA engine, cp.async.bulk + mbarrier complete_tx);
-//       deep      (8 warps) A4: dot of each staged row with the B user vectors held in registers
-//                 (Eq. 1, fp32 FFMA), written to an L2-resident score scratch;
-//       wide      (7 warps) A2+A3: every wide warp of the GPU takes an equal slice of the flat
-//                 chunk space (the paper's LoadBalance, Alg. 2 l.354, realised as a
-//                 static split of equal-cost 32-posting chunks), decodes 16 chunks per two memory
-//                 round trips and adds w~ with L2 reductions red.global.add.f32 into a per-(user,
-//                 ad) fp32 array (Alg. 2 l.358 "AtomicAdd(scores[..], w)").
+//   B  two warp roles run concurrently:
+//       deep      (12 warps) A4: stream this CTA's contiguous rows of A once from HBM with 16-byte
+//                 non-allocating loads, 8 in flight per lane (measured: plain vector loads reach
+//                 the HBM peak, a bulk-copy ring at 1 CTA/SM does not -- tools/mb_stream.cu),
+//                 dot with the B user vectors held in registers (Eq. 1, fp32 FFMA), write the
+//                 deep score to an L2-resident scratch; then join the wide queue;
+//       wide      (4 warps) A2+A3: claim 16-chunk units of the flat chunk space from a global
+//                 queue (the paper's LoadBalance, Alg. 2 l.354: every chunk but a key's
+//                 last holds 32 postings, so units cost the same), fetch the 16 headers and all
+//                 payload words in two memory round trips, unpack + warp-scan each chunk and add
+//                 w~ with L2 reductions red.global.add.f32 into a per-(user, ad) fp32 array
+//                 (Alg. 2 l.358 "AtomicAdd(scores[..], w)").
 //   -- grid sync --
 //   C  A5 fuse: s = deep + wide (-0 -> +0), re-zero the wide array for the next call, per-user
 //      2048-bin histogram of ord(s)'s top 11 bits (warp-aggregated shared atomics).
@@ -25,8 +27,9 @@
 //   E  A6c one CTA per user: candidates staged in shared memory, exact radix select, bitonic sort,
 //      write the sorted top-K; re-zero the user's histogram and counter for the next call.
 //
-// The workspace is self-maintaining: the first call on a workspace (magic word mismatch) zeroes
-// it inside the kernel; every call leaves it zeroed.  So a query is exactly one launch.
+// The workspace is self-maintaining: ebr_workspace_init zeroes it once (or, failing that, the
+// first call sees the magic word missing and zeroes it in-kernel); every call leaves it zeroed.
+// So a query is exactly one launch.
 #include <cooperative_groups.h>
 #include <algorithm>
 #include <cstdio>
@@ -39,19 +42,18 @@ namespace cg = cooperative_groups;
 namespace ebr {
 namespace {
 
-constexpr int kProducerWarps = 1;
-constexpr int kDeepWarps = 8;
-constexpr int kWideWarps = 7;
-static_assert((kProducerWarps + kDeepWarps + kWideWarps) * 32 == kThreads, "CTA layout");
-constexpr int kStages = 6;
-constexpr int kStageBytes = 16 * 1024;
+constexpr int kDeepWarps = 12;   // stream A first, then help with the wide queue
+constexpr int kWideWarps = 4;    // wide queue from the start
+static_assert((kDeepWarps + kWideWarps) * 32 == kThreads, "CTA layout");
+constexpr int kUnroll = 8;       // 16-byte loads in flight per deep lane
+constexpr int kUnit = 16;        // chunks per wide work unit
 constexpr uint32_t kMagic = 0xEB200001u;
 
 struct SmallParams {
     // index
     const void* A;
     int32_t d, d_pad, lpr;      // lpr: lanes per row (row bytes = lpr * vpl * 16)
-    int32_t row_bytes, stage_rows;
+    int32_t row_bytes;
     int64_t n_ads, n_pad;
     uint32_t ad_begin;
     const uint32_t* key_chunk_off;
@@ -68,7 +70,7 @@ struct SmallParams {
     const int32_t* user_feat;   // [B][F][S]
     const float* user_x;
     // workspace
-    uint32_t* header;           // [0] magic, [1] error flags, then phase stamps
+    uint32_t* header;           // [0] magic, [1] error flags, [2] wide queue head, then stamps
     unsigned long long* timers; // optional phase stamps (EBR_PHASE_TIMERS=1), else null
     uint32_t magic;
     uint32_t* ghist;            // [B][kHistBins]
@@ -116,6 +118,14 @@ template <> struct Vec<__nv_bfloat16> {
     }
 };
 
+__device__ __forceinline__ uint4 ldg_stream(const void* ptr) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(ptr));
+    return r;
+}
+
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -130,10 +140,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
     const int B = p.B, R = p.R;
     const cg::grid_group grid = cg::this_grid();
     // ---- shared-memory carve-up ----
-    unsigned char* ring = smem;                                                   // [kStages][kStageBytes]
-    uint64_t* full = reinterpret_cast<uint64_t*>(ring + kStages * kStageBytes);   // [kStages]
-    uint64_t* empty = full + kStages;                                             // [kStages]
-    uint32_t* sHist = reinterpret_cast<uint32_t*>(empty + kStages);               // [B][bins]
+    uint32_t* sHist = reinterpret_cast<uint32_t*>(smem);                          // [B][bins]
     Item* sItems = reinterpret_cast<Item*>(sHist + (size_t)B * kHistBins);        // [items_cap]
     uint64_t* sChunkOff = reinterpret_cast<uint64_t*>(
         (reinterpret_cast<uintptr_t>(sItems + p.items_cap) + 7) & ~(uintptr_t)7);  // [items_cap + 1]
@@ -143,24 +150,16 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
 
     if (p.timers && blockIdx.x == 0 && tid == 0) p.timers[0] = gtimer();
     // ---- first use of this workspace: zero it (uniform decision across the grid) ----
-    if (tid == 0) {
-        sInit = (__ldcg(&p.header[0]) != p.magic);
-        for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kDeepWarps); }
-        fence_mbar_init();
-    }
+    if (tid == 0) sInit = (__ldcg(&p.header[0]) != p.magic);
     for (int i = tid; i < B * kHistBins; i += kThreads) sHist[i] = 0;
     __syncthreads();
-    if (sInit) {
-        for (int range = blockIdx.x; range < p.n_ranges; range += gridDim.x) {
-            const int64_t r0 = (int64_t)range * R;
-            const int64_t r1 = (r0 + R < p.n_ads) ? r0 + R : p.n_ads;
-            for (int b = 0; b < kSmallMaxB; ++b)     // every user slot of the fixed layout
-                for (int64_t a = r0 + tid; a < r1; a += kThreads) p.wide[(size_t)b * p.n_pad + a] = 0.f;
-        }
+    if (sInit) {   // workspace not initialised (ebr_workspace_init not called): do it here
+        const size_t nw = (size_t)kSmallMaxB * p.n_pad;
+        for (size_t i = (size_t)blockIdx.x * kThreads + tid; i < nw; i += (size_t)gridDim.x * kThreads) p.wide[i] = 0.f;
         if (blockIdx.x == 0) {
             for (int i = tid; i < kSmallMaxB * kHistBins; i += kThreads) p.ghist[i] = 0;
             if (tid < kSmallMaxB) p.cand_count[tid] = 0;
-            if (tid == 0) p.header[1] = 0;
+            if (tid == 0) { p.header[1] = 0; p.header[2] = 0; }
         }
         grid.sync();
     }
@@ -217,29 +216,10 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
     const int n_items = (int)sNItems;
     EBR_STAMP(1);
 
-    // ---- B: producer / deep / wide ----
-    if (warp == 0) {
-        if (lane == 0) {
-            const char* Abase = reinterpret_cast<const char*>(p.A);
-            uint32_t g = 0;
-            for (int range = blockIdx.x; range < p.n_ranges; range += gridDim.x) {
-                const int64_t r0 = (int64_t)range * R;
-                const int64_t r1 = (r0 + R < p.n_ads) ? r0 + R : p.n_ads;
-                for (int64_t s0 = r0; s0 < r1; s0 += p.stage_rows, ++g) {
-                    const int rows = (int)((r1 - s0 < p.stage_rows) ? (r1 - s0) : p.stage_rows);
-                    const int slot = g % kStages;
-                    const uint32_t round = g / kStages;
-                    if (round > 0) mbar_wait(&empty[slot], (round - 1) & 1);
-                    const uint32_t bytes = (uint32_t)rows * (uint32_t)p.row_bytes;
-                    mbar_arrive_expect_tx(&full[slot], bytes);
-                    bulk_g2s(ring + (size_t)slot * kStageBytes, Abase + s0 * p.row_bytes, bytes, &full[slot]);
-                }
-            }
-        }
-    } else if (warp <= kDeepWarps) {
+    // ---- B: deep warps stream A (then help), wide warps drain the global unit queue ----
+    if (warp < kDeepWarps) {
         using V = Vec<T>;
         constexpr int E = V::E;
-        const int dw = warp - 1;
         const int lpr = p.lpr;
         const int sub = lane / lpr, li = lane % lpr, rpw = 32 / lpr;
         float u[NB][VPL][E];
@@ -252,27 +232,33 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
                     const int j = (li + v * lpr) * E + e;
                     u[b][v][e] = (b < B && j < p.d) ? V::elem(p.U, (int64_t)b * p.d + j) : 0.f;
                 }
-        uint32_t g = 0;
+        const char* Abase = reinterpret_cast<const char*>(p.A);
         for (int range = blockIdx.x; range < p.n_ranges; range += gridDim.x) {
             const int64_t r0 = (int64_t)range * R;
             const int64_t r1 = (r0 + R < p.n_ads) ? r0 + R : p.n_ads;
-            for (int64_t s0 = r0; s0 < r1; s0 += p.stage_rows, ++g) {
-                const int rows = (int)((r1 - s0 < p.stage_rows) ? (r1 - s0) : p.stage_rows);
-                const int slot = g % kStages;
-                mbar_wait(&full[slot], (g / kStages) & 1);
-                const unsigned char* st = ring + (size_t)slot * kStageBytes;
-                for (int jb = dw * rpw; jb < rows; jb += kDeepWarps * rpw) {
-                    const int j = jb + sub;
-                    const bool ok = j < rows;
+            const int64_t step = (int64_t)kDeepWarps * rpw * kUnroll;
+            for (int64_t base = r0 + (int64_t)warp * rpw; base < r1; base += step) {
+                uint4 av[kUnroll][VPL];
+#pragma unroll
+                for (int q = 0; q < kUnroll; ++q) {
+                    const int64_t row = base + (int64_t)q * kDeepWarps * rpw + sub;
+#pragma unroll
+                    for (int v = 0; v < VPL; ++v) {
+                        if (row < r1)
+                            av[q][v] = ldg_stream(Abase + row * p.row_bytes + (int64_t)(li + v * lpr) * 16);
+                        else
+                            av[q][v] = make_uint4(0, 0, 0, 0);
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < kUnroll; ++q) {
                     float acc[NB];
 #pragma unroll
                     for (int b = 0; b < NB; ++b) acc[b] = 0.f;
 #pragma unroll
                     for (int v = 0; v < VPL; ++v) {
-                        uint4 raw = make_uint4(0, 0, 0, 0);
-                        if (ok) raw = *reinterpret_cast<const uint4*>(st + (size_t)j * p.row_bytes + (size_t)(li + v * lpr) * 16);
                         float a[E];
-                        V::unpack(raw, a);
+                        V::unpack(av[q][v], a);
 #pragma unroll
                         for (int b = 0; b < NB; ++b)
 #pragma unroll
@@ -284,44 +270,88 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
 #pragma unroll
                             for (int b = 0; b < NB; ++b) acc[b] += __shfl_xor_sync(FULL, acc[b], o);
                         }
-                    if (ok && li == 0) {
+                    const int64_t row = base + (int64_t)q * kDeepWarps * rpw + sub;
+                    if (li == 0 && row < r1) {
 #pragma unroll
                         for (int b = 0; b < NB; ++b)
-                            if (b < B) __stcg(&p.scores[(size_t)b * p.n_pad + s0 + j], acc[b]);
+                            if (b < B) __stcg(&p.scores[(size_t)b * p.n_pad + row], acc[b]);
                     }
                 }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[slot]);
             }
         }
         EBR_STAMP(3);
-    } else {
-        // wide: equal slices of the flat chunk space over every wide warp of the grid
+    }
+    {
+        // wide: 16-chunk units of the flat chunk space, claimed from a global queue
+        // (the paper's LoadBalance, Alg. 2 l.354); units may straddle items.
         const uint64_t Ttot = sChunkOff[n_items];
-        const uint64_t nw = (uint64_t)gridDim.x * kWideWarps;
-        const uint64_t gw = (uint64_t)blockIdx.x * kWideWarps + (warp - 1 - kDeepWarps);
-        const uint64_t f0 = Ttot * gw / nw, f1 = Ttot * (gw + 1) / nw;
-        if (f0 < f1) {
-            int lo = 0, hi = n_items - 1;   // last item with sChunkOff <= f0
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (sChunkOff[mid] <= f0) lo = mid; else hi = mid - 1;
+        const uint64_t n_units = (Ttot + kUnit - 1) / kUnit;
+        while (true) {
+            uint32_t unit = 0;
+            if (lane == 0) unit = atomicAdd(&p.header[2], 1u);
+            unit = __shfl_sync(FULL, unit, 0);
+            if (unit >= n_units) break;
+            const uint64_t f = (uint64_t)unit * kUnit + (lane & (kUnit - 1));
+            // this lane's chunk: item = last it with sChunkOff[it] <= f
+            uint2 h = make_uint2(0u, 0u);
+            uint32_t kwb = 0, dst_b = 0;
+            float w = 0.f;
+            const bool have = (lane < kUnit) && f < Ttot;
+            if (have) {
+                int lo = 0, hi = n_items - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (sChunkOff[mid] <= f) lo = mid; else hi = mid - 1;
+                }
+                const Item t = sItems[lo];
+                h = __ldg(&p.hdr[t.c0 + (uint32_t)(f - sChunkOff[lo])]);
+                kwb = t.kwb;
+                dst_b = t.b;
+                w = t.w;
             }
-            int it = lo;
-            uint64_t f = f0;
-            while (f < f1) {
-                while (sChunkOff[it + 1] <= f) ++it;
-                const Item t = sItems[it];
-                const uint32_t cb = t.c0 + (uint32_t)(f - sChunkOff[it]);
-                uint64_t nn = f1 - f;
-                if (nn > 16) nn = 16;
-                if (sChunkOff[it + 1] - f < nn) nn = sChunkOff[it + 1] - f;
-                const uint32_t n = (uint32_t)nn;
-                float* dst = p.wide + (size_t)t.b * p.n_pad;
-                const float w = t.w;
-                decode_unit16(p.hdr, p.payload, t.kwb, cb, cb + n, lane,
-                              [dst, w](uint32_t id) { atomicAdd(&dst[id], w); });
-                f += n;
+            uint32_t lo_w[kUnit], hi_w[kUnit];
+#pragma unroll
+            for (int q = 0; q < kUnit; ++q) {
+                const uint32_t meta = __shfl_sync(FULL, h.y, q);
+                const uint32_t kb = __shfl_sync(FULL, kwb, q);
+                lo_w[q] = 0u;
+                hi_w[q] = 0u;
+                const uint32_t n = (meta & 31u) + 1u, bw = (meta >> 5) & 31u;
+                if (lane >= 1 && (uint32_t)lane < n && bw) {
+                    const uint32_t bit = (uint32_t)(lane - 1) * bw;
+                    const uint32_t wi = kb + (meta >> 10) + (bit >> 5);
+                    lo_w[q] = __ldg(&p.payload[wi]);
+                    hi_w[q] = __ldg(&p.payload[wi + 1]);
+                }
+            }
+            const uint32_t nval = (uint32_t)min((uint64_t)kUnit, Ttot - (uint64_t)unit * kUnit);
+#pragma unroll
+            for (int q = 0; q < kUnit; ++q) {
+                if ((uint32_t)q >= nval) break;
+                const uint32_t meta = __shfl_sync(FULL, h.y, q);
+                const uint32_t first = __shfl_sync(FULL, h.x, q);
+                const uint32_t bq = __shfl_sync(FULL, dst_b, q);
+                const float wq = __shfl_sync(FULL, w, q);
+                const uint32_t n = (meta & 31u) + 1u, bw = (meta >> 5) & 31u;
+                uint32_t g;
+                if (lane == 0) {
+                    g = first;
+                } else if ((uint32_t)lane < n) {
+                    uint32_t v = 0u;
+                    if (bw) {
+                        const uint32_t bit = (uint32_t)(lane - 1) * bw;
+                        v = (uint32_t)(((((uint64_t)hi_w[q]) << 32) | lo_w[q]) >> (bit & 31u)) & ((1u << bw) - 1u);
+                    }
+                    g = v + 1u;
+                } else {
+                    g = 0u;
+                }
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t t = __shfl_up_sync(FULL, g, o);
+                    if (lane >= o) g += t;
+                }
+                if ((uint32_t)lane < n) atomicAdd(&p.wide[(size_t)bq * p.n_pad + g], wq);
             }
         }
         EBR_STAMP(2);
@@ -348,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
                     __stcg(&sc[a], s);
                     bin = ord_of(s) >> (32 - kHistBits);
                 }
-                warp_hist_add(sHist + b * kHistBins, bin, ok);
+                if (ok) atomicAdd(&sHist[b * kHistBins + bin], 1u);
             }
         }
     }
@@ -434,7 +464,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
         if (tid == 0) p.cand_count[b] = 0;
         __syncthreads();
     }
-    if (blockIdx.x == 0 && tid == 0) p.header[0] = p.magic;
+    if (blockIdx.x == 0 && tid == 0) { p.header[0] = p.magic; p.header[2] = 0; }
     EBR_STAMP(10);
 }
 
@@ -473,6 +503,10 @@ SmallLayout small_layout(const ebr_index* idx, int B) {
 
 }  // namespace
 
+uint32_t workspace_magic(const ebr_index* idx) {
+    return kMagic ^ (uint32_t)((uint64_t)idx->n_pad * 2654435761ull);
+}
+
 size_t small_workspace_bytes(const ebr_index* idx, int32_t slots, int32_t k) {
     (void)slots; (void)k;
     return small_layout(idx, kSmallMaxB).total;
@@ -488,15 +522,14 @@ ebr_status run_small(const QueryArgs& q, int b0, int B) {
     int lpr, vpl;
     if (row_bytes <= 512) { lpr = row_bytes / 16; vpl = 1; }
     else { lpr = 32; vpl = row_bytes / 512; }
-    if (row_bytes > kStageBytes) return set_error(EBR_EUNSUPPORTED, "embedding row of %d bytes is too wide", row_bytes);
     int nb = 1;
     while (nb < B) nb <<= 1;
     kern_t k = idx->dtype == EBR_BF16 ? pick_kernel<__nv_bfloat16>(nb, vpl) : pick_kernel<float>(nb, vpl);
     if (!k) return set_error(EBR_EUNSUPPORTED, "embedding row of %d bytes is not supported", row_bytes);
 
     const int items_cap = B * idx->n_fields * q.slots;
-    const size_t p1 = (size_t)kStages * kStageBytes + 2 * kStages * 8 + (size_t)B * kHistBins * 4 +
-                      (size_t)items_cap * sizeof(Item) + 8 + (size_t)(items_cap + 1) * 8;
+    const size_t p1 = (size_t)B * kHistBins * 4 + (size_t)items_cap * sizeof(Item) + 8 +
+                      (size_t)(items_cap + 1) * 8;
     const size_t sel_min = (size_t)pow2ceil_i(q.k) * 8 + 1024 + 64 * 1024;   // + >= 8k staged candidates
     const size_t smem = std::max(p1, sel_min);
     if (smem > 227 * 1024)
@@ -514,7 +547,7 @@ ebr_status run_small(const QueryArgs& q, int b0, int B) {
     R = std::max<int64_t>(32, (R + 31) & ~(int64_t)31);
     SmallParams p;
     p.A = idx->A; p.d = idx->d; p.d_pad = idx->d_pad; p.lpr = lpr;
-    p.row_bytes = row_bytes; p.stage_rows = kStageBytes / row_bytes;
+    p.row_bytes = row_bytes;
     p.n_ads = idx->n_ads; p.n_pad = idx->n_pad; p.ad_begin = (uint32_t)idx->ad_begin;
     p.key_chunk_off = idx->key_chunk_off; p.key_word_off = idx->key_word_off;
     p.hdr = idx->chunk_hdr; p.payload = idx->payload; p.cross_w = idx->cross_w;
@@ -527,7 +560,7 @@ ebr_status run_small(const QueryArgs& q, int b0, int B) {
     static const bool timers_on = getenv("EBR_PHASE_TIMERS") && getenv("EBR_PHASE_TIMERS")[0] == '1';
     p.timers = timers_on ? reinterpret_cast<unsigned long long*>(ws + L.off_header + 16) : nullptr;
     // the magic ties the workspace's zeroed state to this index geometry
-    p.magic = kMagic ^ (uint32_t)((uint64_t)idx->n_pad * 2654435761ull);
+    p.magic = workspace_magic(idx);
     p.ghist = reinterpret_cast<uint32_t*>(ws + L.off_hist);
     p.cand_count = reinterpret_cast<uint32_t*>(ws + L.off_count);
     p.scores = reinterpret_cast<float*>(ws + L.off_scores);

@@ -36,6 +36,7 @@ EXPORTS = {
     "ebr_score_topk": (ctypes.c_int, [_P, _P, _I32, _P, _P, _I32, _I32, _P, _P, _P, _SZ, _P]),
     "ebr_score_topk_keys": (ctypes.c_int, [_P, _P, _I32, _P, _P, _I32, _I32, _P, _P, _SZ, _P]),
     "ebr_query_error": (ctypes.c_int, [_P, _P, ctypes.POINTER(ctypes.c_uint32)]),
+    "ebr_workspace_init": (ctypes.c_int, [_P, _P, _SZ, _P]),
     "ebr_workspace_bytes_host": (_SZ, [_P, _I32, _I32, _I32]),
     "ebr_score_topk_host": (ctypes.c_int, [_P, _P, _I32, _P, _P, _I32, _I32, _P, _P, _P, _SZ, _P]),
     "ebr_merge_workspace_bytes": (_SZ, [_I32, _I32, _I32]),
@@ -201,6 +202,21 @@ def score_topk_host(idx: Index, user_emb: np.ndarray, user_feat: np.ndarray, use
                                     _t_ptr(workspace), workspace.numel() * workspace.element_size(),
                                     _stream_ptr(stream)),
            "ebr_score_topk_host")
+
+
+def workspace_init(idx: Index, workspace, stream=None):
+    _check(_lib.ebr_workspace_init(idx.handle, _t_ptr(workspace),
+                                   workspace.numel() * workspace.element_size(), _stream_ptr(stream)),
+           "ebr_workspace_init")
+
+
+def new_workspace(idx: Index, batch: int, slots: int, k: int, host: bool = False, device=None):
+    """Allocates (torch, uint8) and initialises a workspace for `idx`."""
+    import torch
+    n = idx.workspace_bytes_host(batch, slots, k) if host else idx.workspace_bytes(batch, slots, k)
+    ws = torch.empty(n, dtype=torch.uint8, device=device if device is not None else f"cuda:{idx.device}")
+    workspace_init(idx, ws)
+    return ws
 
 
 def query_error(workspace, stream=None) -> int:

@@ -29,7 +29,7 @@ def run(ebr, idx, users, k, keys=False, stream=None):
         np.int16 if users.user_emb.dtype == np.uint16 else np.float32)).to(dev)
     feat = torch.from_numpy(users.user_feat).to(dev)
     x = torch.from_numpy(users.user_x).to(dev)
-    ws = torch.empty(idx.workspace_bytes(B, S, k), dtype=torch.uint8, device=dev)
+    ws = ebr.new_workspace(idx, B, S, k)
     if keys:
         out = torch.empty((B, k), dtype=torch.int64, device=dev)
         ebr.score_topk_keys(idx, emb, feat, x, k, out, ws, stream)
@@ -179,6 +179,36 @@ def test_bad_user_value_raises_flag(ebr):
     assert ebr.query_error(ws) == 0          # cleared
 
 
+def test_workspace_reuse_across_indexes(ebr):
+    """One workspace serves successive indexes of the same geometry (state left clean)."""
+    inv, users = synth.make_config("C1", mode="exact", n_ads=5_000, batch=3)
+    idx = ebr.Index.of(inv)
+    ws = ebr.new_workspace(idx, 3, users.slots, 50)
+    o = oracle.Oracle.of(inv)
+    dev = torch.device("cuda")
+    for trial in range(3):
+        users2 = synth.make_users(inv, 3, mode="exact", seed=100 + trial)
+        ids = torch.empty((3, 50), dtype=torch.int32, device=dev)
+        sc = torch.empty((3, 50), dtype=torch.float32, device=dev)
+        ebr.score_topk(idx, torch.from_numpy(users2.user_emb).to(dev), torch.from_numpy(users2.user_feat).to(dev),
+                       torch.from_numpy(users2.user_x).to(dev), 50, ids, sc, ws)
+        torch.cuda.synchronize()
+        assert check_all(o, users2, ids.cpu().numpy(), sc.cpu().numpy(), 50, "exact") == 0
+
+
+def test_uninitialised_workspace_self_inits(ebr):
+    inv, users = synth.make_config("C1", mode="exact", n_ads=3_000, batch=2)
+    idx = ebr.Index.of(inv)
+    ws = torch.full((idx.workspace_bytes(2, users.slots, 20),), 7, dtype=torch.uint8, device="cuda")
+    dev = torch.device("cuda")
+    ids = torch.empty((2, 20), dtype=torch.int32, device=dev)
+    sc = torch.empty((2, 20), dtype=torch.float32, device=dev)
+    ebr.score_topk(idx, torch.from_numpy(users.user_emb).to(dev), torch.from_numpy(users.user_feat).to(dev),
+                   torch.from_numpy(users.user_x).to(dev), 20, ids, sc, ws)
+    torch.cuda.synchronize()
+    assert check_all(oracle.Oracle.of(inv), users, ids.cpu().numpy(), sc.cpu().numpy(), 20, "exact") == 0
+
+
 def test_invalid_arguments(ebr):
     inv, users = synth.make_config("C1", mode="exact", n_ads=100, batch=1)
     idx = ebr.Index.of(inv)
@@ -198,7 +228,7 @@ def test_host_variant_equals_device(ebr):
     inv, users = synth.make_config("C2", mode="real", n_ads=100_000, batch=3)
     idx = ebr.Index.of(inv)
     (ids, sc), _ = run(ebr, idx, users, 200)
-    ws = torch.empty(idx.workspace_bytes_host(3, users.slots, 200), dtype=torch.uint8, device="cuda")
+    ws = ebr.new_workspace(idx, 3, users.slots, 200, host=True)
     hid = np.empty((3, 200), np.int32)
     hsc = np.empty((3, 200), np.float32)
     ebr.score_topk_host(idx, users.user_emb, users.user_feat, users.user_x, 200, hid, hsc, ws)

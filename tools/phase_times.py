@@ -19,14 +19,14 @@ dev = torch.device("cuda")
 emb = torch.from_numpy(users.user_emb.view(np.int16) if users.user_emb.dtype == np.uint16 else users.user_emb).to(dev)
 feat = torch.from_numpy(users.user_feat).to(dev)
 x = torch.from_numpy(users.user_x).to(dev)
-ws = torch.empty(idx.workspace_bytes(Bn, S, c.k), dtype=torch.uint8, device=dev)
+ws = ebr.new_workspace(idx, Bn, S, c.k)
 ids = torch.empty((Bn, c.k), dtype=torch.int32, device=dev)
 sc = torch.empty((Bn, c.k), dtype=torch.float32, device=dev)
-flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+flush = torch.ones(64 << 20, dtype=torch.float32, device=dev)   # 256 MiB, read to flush L2 clean
 names = ["start", "plan", "wide_done", "deep_done", "B_end", "sync1", "fuse_end", "sync2", "compact_end", "sync3", "select_end"]
 acc = []
 for it in range(30):
-    flush.fill_(it)
+    flush.sum()
     torch.cuda.synchronize()
     ebr.score_topk(idx, emb, feat, x, c.k, ids, sc, ws)
     torch.cuda.synchronize()
