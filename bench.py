@@ -278,7 +278,7 @@ def main():
         t0 = time.perf_counter()
         for i in range(args.steps):
             with torch.cuda.stream(stream):
-                torch.sum(flush, out=flush_out)           # evict L2 clean (outside the events)
+                torch.sum(flush, dim=0, out=flush_out)           # evict L2 clean (outside the events)
                 ev[i][0].record(stream)
             step()
             with torch.cuda.stream(stream):
@@ -345,7 +345,7 @@ def main():
         e_ms = []
         for i in range(args.steps):
             with torch.cuda.stream(stream):
-                torch.sum(flush, out=flush_out)
+                torch.sum(flush, dim=0, out=flush_out)
             stream.synchronize()
             t = time.perf_counter()
             ebr.score_topk_host(idx, h_emb, h_feat, h_x, K, h_ids, h_sc, wsh, stream)

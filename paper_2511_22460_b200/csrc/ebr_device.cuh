@@ -324,9 +324,18 @@ __device__ __forceinline__ void cta_bitonic_desc(uint64_t* sbuf, int nsel) {
     }
 }
 
+__device__ __forceinline__ void stamp_max(unsigned long long* tm, int i) {
+    if (tm && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        atomicMax(&tm[i], t);
+    }
+}
+
 template <typename Get>
 __device__ int cta_select_topk(Get get, int64_t n, int K, uint64_t* sbuf, uint64_t* scand,
-                               int64_t scand_cap, uint32_t* shist, uint32_t* sscalar) {
+                               int64_t scand_cap, uint32_t* shist, uint32_t* sscalar,
+                               unsigned long long* tm = nullptr) {
     const int tid = threadIdx.x, nt = blockDim.x;
     int nsel;
     if (n <= (int64_t)K) {
@@ -336,11 +345,14 @@ __device__ int cta_select_topk(Get get, int64_t n, int K, uint64_t* sbuf, uint64
     } else if (scand && n <= scand_cap) {
         for (int64_t i = tid; i < n; i += nt) scand[i] = get(i);
         __syncthreads();
+        stamp_max(tm, 0);
         nsel = cta_radix_select([scand](int64_t i) { return scand[i]; }, n, K, sbuf, shist, sscalar);
     } else {
         nsel = cta_radix_select(get, n, K, sbuf, shist, sscalar);
     }
+    stamp_max(tm, 1);
     cta_bitonic_desc(sbuf, nsel);
+    stamp_max(tm, 2);
     return nsel;
 }
 

@@ -87,6 +87,7 @@ struct SmallParams {
     int32_t n_ranges;
     int32_t items_cap;          // >= B * F * S
     int32_t smem_bytes;
+    int32_t diag;               // EBR_DIAG bits (diagnostics only): 1 = skip wide, 2 = skip deep
 };
 
 struct Item {
@@ -217,7 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
     EBR_STAMP(1);
 
     // ---- B: deep warps stream A (then help), wide warps drain the global unit queue ----
-    if (warp < kDeepWarps) {
+    if (warp < kDeepWarps && !(p.diag & 2)) {
         using V = Vec<T>;
         constexpr int E = V::E;
         const int lpr = p.lpr;
@@ -285,7 +286,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
         // wide: 16-chunk units of the flat chunk space, claimed from a global queue
         // (the paper's LoadBalance, Alg. 2 l.354); units may straddle items.
         const uint64_t Ttot = sChunkOff[n_items];
-        const uint64_t n_units = (Ttot + kUnit - 1) / kUnit;
+        const uint64_t n_units = (p.diag & 1) ? 0 : (Ttot + kUnit - 1) / kUnit;
         while (true) {
             uint32_t unit = 0;
             if (lane == 0) unit = atomicAdd(&p.header[2], 1u);
@@ -360,25 +361,33 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
     grid.sync();
     EBR_STAMP(5);
 
-    // ---- C: fuse + histogram ----
+    // ---- C: fuse + histogram (8 independent elements in flight per thread) ----
+    constexpr int kIlp = 8;
     for (int range = blockIdx.x; range < p.n_ranges; range += gridDim.x) {
         const int64_t r0 = (int64_t)range * R;
         const int64_t r1 = (r0 + R < p.n_ads) ? r0 + R : p.n_ads;
         for (int b = 0; b < B; ++b) {
             float* sc = p.scores + (size_t)b * p.n_pad;
             float* wd = p.wide + (size_t)b * p.n_pad;
-            for (int64_t base = r0; base < r1; base += kThreads) {
-                const int64_t a = base + tid;
-                const bool ok = a < r1;
-                uint32_t bin = 0;
-                if (ok) {
-                    float s = __ldcg(&sc[a]) + __ldcg(&wd[a]);
-                    __stcg(&wd[a], 0.f);
-                    if (s == 0.f) s = 0.f;                      // -0 -> +0 (R14)
-                    __stcg(&sc[a], s);
-                    bin = ord_of(s) >> (32 - kHistBits);
+            for (int64_t base = r0; base < r1; base += (int64_t)kThreads * kIlp) {
+                float dv[kIlp], wv[kIlp];
+#pragma unroll
+                for (int q = 0; q < kIlp; ++q) {
+                    const int64_t a = base + q * kThreads + tid;
+                    dv[q] = 0.f; wv[q] = 0.f;
+                    if (a < r1) { dv[q] = __ldcg(&sc[a]); wv[q] = __ldcg(&wd[a]); }
                 }
-                if (ok) atomicAdd(&sHist[b * kHistBins + bin], 1u);
+#pragma unroll
+                for (int q = 0; q < kIlp; ++q) {
+                    const int64_t a = base + q * kThreads + tid;
+                    if (a < r1) {
+                        float s = dv[q] + wv[q];
+                        if (s == 0.f) s = 0.f;                  // -0 -> +0 (R14)
+                        __stcg(&wd[a], 0.f);
+                        __stcg(&sc[a], s);
+                        atomicAdd(&sHist[b * kHistBins + (ord_of(s) >> (32 - kHistBits))], 1u);
+                    }
+                }
             }
         }
     }
@@ -424,20 +433,27 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
         for (int b = 0; b < B; ++b) {
             const float* sc = p.scores + (size_t)b * p.n_pad;
             const uint32_t bs = sBinStar[b];
-            for (int64_t base = r0; base < r1; base += kThreads) {
-                const int64_t a = base + tid;
-                float s = 0.f;
-                bool take = false;
-                if (a < r1) { s = __ldcg(&sc[a]); take = (ord_of(s) >> (32 - kHistBits)) >= bs; }
-                const unsigned m = __ballot_sync(FULL, take);
-                if (m) {
-                    const int leader = __ffs(m) - 1;
-                    uint32_t pos = 0;
-                    if (lane == leader) pos = atomicAdd(&p.cand_count[b], (uint32_t)__popc(m));
-                    pos = __shfl_sync(FULL, pos, leader);
-                    if (take)
-                        p.cand[(size_t)b * p.n_pad + pos + __popc(m & ((1u << lane) - 1u))] =
-                            kappa_of(s, p.ad_begin + (uint32_t)a);
+            for (int64_t base = r0; base < r1; base += (int64_t)kThreads * kIlp) {
+                float sv[kIlp];
+#pragma unroll
+                for (int q = 0; q < kIlp; ++q) {
+                    const int64_t a = base + q * kThreads + tid;
+                    sv[q] = (a < r1) ? __ldcg(&sc[a]) : 0.f;
+                }
+#pragma unroll
+                for (int q = 0; q < kIlp; ++q) {
+                    const int64_t a = base + q * kThreads + tid;
+                    const bool take = (a < r1) && (ord_of(sv[q]) >> (32 - kHistBits)) >= bs;
+                    const unsigned m = __ballot_sync(FULL, take);
+                    if (m) {
+                        const int leader = __ffs(m) - 1;
+                        uint32_t pos = 0;
+                        if (lane == leader) pos = atomicAdd(&p.cand_count[b], (uint32_t)__popc(m));
+                        pos = __shfl_sync(FULL, pos, leader);
+                        if (take)
+                            p.cand[(size_t)b * p.n_pad + pos + __popc(m & ((1u << lane) - 1u))] =
+                                kappa_of(sv[q], p.ad_begin + (uint32_t)a);
+                    }
                 }
             }
         }
@@ -456,7 +472,8 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
         const int64_t n = (int64_t)__ldcg(&p.cand_count[b]);
         const uint64_t* cb = p.cand + (size_t)b * p.n_pad;
         const int nsel = cta_select_topk([cb](int64_t i) { return __ldcg(&cb[i]); }, n, p.K, sbuf,
-                                         scand, scap, shist, sScalar);
+                                         scand, scap, shist, sScalar,
+                                         (p.timers && b == 0) ? p.timers + 11 : nullptr);
         cta_write_topk(sbuf, nsel, p.K, p.out_ids ? p.out_ids + (size_t)b * p.K : nullptr,
                        p.out_scores ? p.out_scores + (size_t)b * p.K : nullptr,
                        p.out_keys ? p.out_keys + (size_t)b * p.K : nullptr);
@@ -558,6 +575,8 @@ ebr_status run_small(const QueryArgs& q, int b0, int B) {
     p.user_x = q.user_x + (size_t)b0 * idx->n_fields * q.slots;
     p.header = reinterpret_cast<uint32_t*>(ws + L.off_header);
     static const bool timers_on = getenv("EBR_PHASE_TIMERS") && getenv("EBR_PHASE_TIMERS")[0] == '1';
+    static const int diag = getenv("EBR_DIAG") ? atoi(getenv("EBR_DIAG")) : 0;
+    p.diag = diag;
     p.timers = timers_on ? reinterpret_cast<unsigned long long*>(ws + L.off_header + 16) : nullptr;
     // the magic ties the workspace's zeroed state to this index geometry
     p.magic = workspace_magic(idx);

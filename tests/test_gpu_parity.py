@@ -225,7 +225,8 @@ def test_invalid_arguments(ebr):
 # ---------------------------------------------------------------- host (e2e) variant, keys
 
 def test_host_variant_equals_device(ebr):
-    inv, users = synth.make_config("C2", mode="real", n_ads=100_000, batch=3)
+    # exact mode: the real-mode wide sum order is not deterministic across runs (reading R9)
+    inv, users = synth.make_config("C2", mode="exact", n_ads=100_000, batch=3)
     idx = ebr.Index.of(inv)
     (ids, sc), _ = run(ebr, idx, users, 200)
     ws = ebr.new_workspace(idx, 3, users.slots, 200, host=True)
