@@ -193,13 +193,13 @@ static ebr_status encode(const int32_t* ad_feat, int64_t n_ads, int32_t F, const
     return EBR_OK;
 }
 
-// Padded kernel row width: row bytes a power of two in [16, 512] (>= 128 B for bf16, the TMA
-// 128B-swizzle atom), or a multiple of 512 B.  Zero padding leaves every dot product exact.
+// Padded kernel row width: row bytes a power of two in [64, 512] (>= 128 B for bf16, the TMA
+// 128B-swizzle atom), or 1 KB / 2 KB.  Zero padding leaves every dot product exact.
 static int32_t padded_width(int32_t d, int esz) {
     int64_t bytes = (int64_t)d * esz;
-    int64_t p = (esz == 2) ? 128 : 16;
+    int64_t p = (esz == 2) ? 128 : 64;
     while (p < bytes && p < 512) p <<= 1;
-    if (bytes > 512) p = (bytes + 511) / 512 * 512;
+    if (bytes > 512) p = bytes <= 1024 ? 1024 : 2048;   // wider rows are rejected at build
     return (int32_t)(p / esz);
 }
 
@@ -347,6 +347,8 @@ ebr_status ebr_build_index(const void* ad_emb, ebr_dtype dtype, int64_t ad_begin
     if (!out) return set_error(EBR_EINVAL, "out is null");
     *out = nullptr;
     if (d < 1) return set_error(EBR_EINVAL, "d < 1");
+    if ((int64_t)d * (dtype == EBR_BF16 ? 2 : 4) > 2048)
+        return set_error(EBR_EUNSUPPORTED, "embedding rows above 2 KB (d=%d) are not supported", d);
     if (dtype != EBR_F32 && dtype != EBR_BF16) return set_error(EBR_EINVAL, "bad dtype");
     if (ad_begin < 0 || ad_begin >= ad_end) return set_error(EBR_EINVAL, "need 0 <= ad_begin < ad_end");
     if (ad_end > 0x7FFFFFFFll) return set_error(EBR_EINVAL, "ad_end > 2^31-1");

@@ -1,0 +1,508 @@
+// ebr_small.cu -- the latency path (small user batch, B <= 8 per launch): ONE cooperative,
+// persistent kernel per call (1 CTA per SM) runs every step of the hot path:
+//
+//   A  plan     (every CTA, deterministic order): each valid user slot becomes a work item
+//               {key i = base_f + v, w~ = fl32(w_i x_i), the key's chunk span}, and an
+//               exclusive scan of the items' chunk counts gives a flat chunk space
+//               (Alg. 2 l.352-353 "k_length", "ExclusiveScan").
+//   B  two warp roles run concurrently:
+//       deep      (12 warps) A4: stream this CTA's contiguous rows of A once from HBM with 16-byte
+//                 non-allocating loads, 8 in flight per lane (measured: plain vector loads reach
+//                 the HBM peak, a bulk-copy ring at 1 CTA/SM does not -- tools/mb_stream.cu),
+//                 dot with the B user vectors held in registers (Eq. 1, fp32 FFMA), write the
+//                 deep score to an L2-resident scratch; then join the wide queue;
+//       wide      (4 warps) A2+A3: claim 16-chunk units of the flat chunk space from a global
+//                 queue (the paper's LoadBalance, Alg. 2 l.354: every chunk but a key's
+//                 last holds 32 postings, so units cost the same), fetch the 16 headers and all
+//                 payload words in two memory round trips, unpack + warp-scan each chunk and add
+//                 w~ with L2 reductions red.global.add.f32 into a per-(user, ad) fp32 array
+//                 (Alg. 2 l.358 "AtomicAdd(scores[..], w)").
+//   -- grid sync --
+//   C  A5 fuse: s = deep + wide (-0 -> +0), re-zero the wide array for the next call, per-user
+//      2048-bin histogram of ord(s)'s top 11 bits (warp-aggregated shared atomics).
+//   -- grid sync --
+//   D  A6a each CTA finds, per user, the bin holding the K-th largest score; A6b every (user, ad)
+//      in a bin >= it is appended as a 64-bit key kappa (warp-aggregated global atomics).
+//   -- grid sync --
+//   E  A6c one CTA per user: candidates staged in shared memory, exact radix select, bitonic sort,
+//      write the sorted top-K; re-zero the user's histogram and counter for the next call.
+//
+// The workspace is self-maintaining: ebr_workspace_init zeroes it once (or, failing that, the
+// first call sees the magic word missing and zeroes it in-kernel); every call leaves it zeroed.
+// So a query is exactly one launch.
+#pragma once
+#include <cooperative_groups.h>
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "ebr_device.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace ebr {
+namespace small {
+
+constexpr int kDeepWarps = 12;   // stream A first, then help with the wide queue
+constexpr int kWideWarps = 4;    // wide queue from the start
+static_assert((kDeepWarps + kWideWarps) * 32 == kThreads, "CTA layout");
+constexpr int kUnroll = 8;       // 16-byte loads in flight per deep lane
+constexpr int kUnit = 16;        // chunks per wide work unit
+constexpr uint32_t kMagic = 0xEB200001u;
+
+struct SmallParams {
+    // index
+    const void* A;
+    int32_t d, d_pad;
+    int32_t row_bytes;
+    int64_t n_ads, n_pad;
+    uint32_t ad_begin;
+    const uint32_t* key_chunk_off;
+    const uint32_t* key_word_off;
+    const uint2* hdr;
+    const uint32_t* payload;
+    const float* cross_w;
+    const int32_t* field_card;
+    const int32_t* field_base;
+    int32_t n_fields;
+    // query (this launch's users)
+    const void* U;              // [B][d]
+    int32_t B, slots, K;
+    const int32_t* user_feat;   // [B][F][S]
+    const float* user_x;
+    // workspace
+    uint32_t* header;           // [0] magic, [1] error flags, [2] wide queue head, then stamps
+    unsigned long long* timers; // optional phase stamps (EBR_PHASE_TIMERS=1), else null
+    uint32_t magic;
+    uint32_t* ghist;            // [B][kHistBins]
+    uint32_t* cand_count;       // [B]
+    float* scores;              // [B][n_pad]  deep, then fused score
+    float* wide;                // [B][n_pad]  wide accumulator (zero between calls)
+    uint64_t* cand;             // [B][n_pad]
+    // outputs
+    int32_t* out_ids;           // [B][K] (already offset to this launch's first user)
+    float* out_scores;
+    uint64_t* out_keys;
+    // decomposition
+    int32_t R;                  // ads per range
+    int32_t n_ranges;
+    int32_t items_cap;          // >= B * F * S
+    int32_t smem_bytes;
+    int32_t diag;               // EBR_DIAG bits (diagnostics only): 1 = skip wide, 2 = skip deep
+};
+
+struct Item {
+    uint32_t key, c0, c1, b, kwb;
+    float w;
+};
+
+template <typename T> struct Vec;
+template <> struct Vec<float> {
+    static constexpr int E = 4;
+    __device__ static void unpack(const uint4& v, float* o) {
+        o[0] = __uint_as_float(v.x); o[1] = __uint_as_float(v.y);
+        o[2] = __uint_as_float(v.z); o[3] = __uint_as_float(v.w);
+    }
+    __device__ static float elem(const void* p, int64_t i) { return ((const float*)p)[i]; }
+};
+template <> struct Vec<__nv_bfloat16> {
+    static constexpr int E = 8;
+    __device__ static void unpack(const uint4& v, float* o) {
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            o[2 * j] = __uint_as_float(w[j] << 16);
+            o[2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
+        }
+    }
+    __device__ static float elem(const void* p, int64_t i) {
+        return __uint_as_float(((uint32_t)((const uint16_t*)p)[i]) << 16);
+    }
+};
+
+__device__ __forceinline__ uint4 ldg_stream(const void* ptr) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(ptr));
+    return r;
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define EBR_STAMP(i) do { if (p.timers && (tid & 31) == 0) atomicMax(&p.timers[i], gtimer()); } while (0)
+
+template <typename T, int NB, int LPR, int VPL>
+__global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int B = p.B, R = p.R;
+    const cg::grid_group grid = cg::this_grid();
+    // ---- shared-memory carve-up ----
+    uint32_t* sHist = reinterpret_cast<uint32_t*>(smem);                          // [B][bins]
+    Item* sItems = reinterpret_cast<Item*>(sHist + (size_t)B * kHistBins);        // [items_cap]
+    uint64_t* sChunkOff = reinterpret_cast<uint64_t*>(
+        (reinterpret_cast<uintptr_t>(sItems + p.items_cap) + 7) & ~(uintptr_t)7);  // [items_cap + 1]
+    __shared__ uint32_t sScan[40], sScalar[8], sNItems;
+    __shared__ uint32_t sBinStar[kSmallMaxB];
+    __shared__ int sInit;
+
+    if (p.timers && blockIdx.x == 0 && tid == 0) p.timers[0] = gtimer();
+    // ---- first use of this workspace: zero it (uniform decision across the grid) ----
+    if (tid == 0) sInit = (__ldcg(&p.header[0]) != p.magic);
+    for (int i = tid; i < B * kHistBins; i += kThreads) sHist[i] = 0;
+    __syncthreads();
+    if (sInit) {   // workspace not initialised (ebr_workspace_init not called): do it here
+        const size_t nw = (size_t)kSmallMaxB * p.n_pad;
+        for (size_t i = (size_t)blockIdx.x * kThreads + tid; i < nw; i += (size_t)gridDim.x * kThreads) p.wide[i] = 0.f;
+        if (blockIdx.x == 0) {
+            for (int i = tid; i < kSmallMaxB * kHistBins; i += kThreads) p.ghist[i] = 0;
+            if (tid < kSmallMaxB) p.cand_count[tid] = 0;
+            if (tid == 0) { p.header[1] = 0; p.header[2] = 0; }
+        }
+        grid.sync();
+    }
+
+    // ---- A: plan, deterministic item order ----
+    {
+        const int nslot = B * p.n_fields * p.slots;
+        const int per = (nslot + kThreads - 1) / kThreads;
+        const int s0 = min(nslot, tid * per), s1 = min(nslot, s0 + per);
+        uint32_t cnt = 0;
+        for (int i = s0; i < s1; ++i) {
+            const int f = (i / p.slots) % p.n_fields;
+            const int32_t v = p.user_feat[i];
+            if (v >= p.field_card[f]) {
+                if (blockIdx.x == 0) atomicOr(&p.header[1], 1u);   // bounds error: skip the slot
+                continue;
+            }
+            if (v < 0) continue;
+            const uint32_t key = (uint32_t)(p.field_base[f] + v);
+            if (__ldg(&p.key_chunk_off[key + 1]) > __ldg(&p.key_chunk_off[key])) ++cnt;
+        }
+        uint32_t total;
+        uint32_t pos = block_exclusive_scan(cnt, sScan, &total);
+        for (int i = s0; i < s1; ++i) {
+            const int b = i / (p.n_fields * p.slots);
+            const int f = (i / p.slots) % p.n_fields;
+            const int32_t v = p.user_feat[i];
+            if (v < 0 || v >= p.field_card[f]) continue;
+            const uint32_t key = (uint32_t)(p.field_base[f] + v);
+            Item it;
+            it.c0 = __ldg(&p.key_chunk_off[key]);
+            it.c1 = __ldg(&p.key_chunk_off[key + 1]);
+            if (it.c1 <= it.c0) continue;
+            it.key = key;
+            it.b = (uint32_t)b;
+            it.kwb = __ldg(&p.key_word_off[key]);
+            it.w = __fmul_rn(__ldg(&p.cross_w[key]), p.user_x[i]);   // w~ = fl32(w x), never an FMA (R10)
+            sItems[pos++] = it;
+        }
+        if (tid == 0) sNItems = total;
+        __syncthreads();
+        // exclusive scan of chunk counts over items
+        const int n_items = (int)sNItems;
+        const int per2 = (n_items + kThreads - 1) / kThreads;
+        const int i0 = min(n_items, tid * per2), i1 = min(n_items, i0 + per2);
+        uint32_t loc = 0;
+        for (int i = i0; i < i1; ++i) loc += sItems[i].c1 - sItems[i].c0;
+        uint32_t tot2;
+        uint64_t acc = block_exclusive_scan(loc, sScan, &tot2);
+        for (int i = i0; i < i1; ++i) { sChunkOff[i] = acc; acc += sItems[i].c1 - sItems[i].c0; }
+        if (tid == 0) sChunkOff[n_items] = tot2;
+        __syncthreads();
+    }
+    const int n_items = (int)sNItems;
+    EBR_STAMP(1);
+
+    // ---- B: deep warps stream A (then help), wide warps drain the global unit queue ----
+    if (warp < kDeepWarps && !(p.diag & 2)) {
+        using V = Vec<T>;
+        constexpr int E = V::E;
+        constexpr int lpr = LPR;
+        const int sub = lane / lpr, li = lane % lpr;
+        constexpr int rpw = 32 / lpr;
+        float u[NB][VPL][E];
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+#pragma unroll
+            for (int v = 0; v < VPL; ++v)
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const int j = (li + v * lpr) * E + e;
+                    u[b][v][e] = (b < B && j < p.d) ? V::elem(p.U, (int64_t)b * p.d + j) : 0.f;
+                }
+        const char* Abase = reinterpret_cast<const char*>(p.A);
+        for (int range = blockIdx.x; range < p.n_ranges; range += gridDim.x) {
+            const int64_t r0 = (int64_t)range * R;
+            const int64_t r1 = (r0 + R < p.n_ads) ? r0 + R : p.n_ads;
+            const int64_t step = (int64_t)kDeepWarps * rpw * kUnroll;
+            for (int64_t base = r0 + (int64_t)warp * rpw; base < r1; base += step) {
+                uint4 av[kUnroll][VPL];
+#pragma unroll
+                for (int q = 0; q < kUnroll; ++q) {
+                    const int64_t row = base + (int64_t)q * kDeepWarps * rpw + sub;
+#pragma unroll
+                    for (int v = 0; v < VPL; ++v) {
+                        if (row < r1)
+                            av[q][v] = ldg_stream(Abase + row * p.row_bytes + (int64_t)(li + v * lpr) * 16);
+                        else
+                            av[q][v] = make_uint4(0, 0, 0, 0);
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < kUnroll; ++q) {
+                    float acc[NB];
+#pragma unroll
+                    for (int b = 0; b < NB; ++b) acc[b] = 0.f;
+#pragma unroll
+                    for (int v = 0; v < VPL; ++v) {
+                        float a[E];
+                        V::unpack(av[q][v], a);
+#pragma unroll
+                        for (int b = 0; b < NB; ++b)
+#pragma unroll
+                            for (int e = 0; e < E; ++e) acc[b] = fmaf(a[e], u[b][v][e], acc[b]);
+                    }
+#pragma unroll
+                    for (int o = lpr / 2; o > 0; o >>= 1) {
+#pragma unroll
+                        for (int b = 0; b < NB; ++b) acc[b] += __shfl_xor_sync(FULL, acc[b], o);
+                    }
+                    const int64_t row = base + (int64_t)q * kDeepWarps * rpw + sub;
+                    if (li == 0 && row < r1) {
+#pragma unroll
+                        for (int b = 0; b < NB; ++b)
+                            if (b < B) __stcg(&p.scores[(size_t)b * p.n_pad + row], acc[b]);
+                    }
+                }
+            }
+        }
+        EBR_STAMP(3);
+    }
+    {
+        // wide: 16-chunk units of the flat chunk space, claimed from a global queue
+        // (the paper's LoadBalance, Alg. 2 l.354); units may straddle items.
+        const uint64_t Ttot = sChunkOff[n_items];
+        const uint64_t n_units = (p.diag & 1) ? 0 : (Ttot + kUnit - 1) / kUnit;
+        while (true) {
+            uint32_t unit = 0;
+            if (lane == 0) unit = atomicAdd(&p.header[2], 1u);
+            unit = __shfl_sync(FULL, unit, 0);
+            if (unit >= n_units) break;
+            const uint64_t f = (uint64_t)unit * kUnit + (lane & (kUnit - 1));
+            // this lane's chunk: item = last it with sChunkOff[it] <= f
+            uint2 h = make_uint2(0u, 0u);
+            uint32_t kwb = 0, dst_b = 0;
+            float w = 0.f;
+            const bool have = (lane < kUnit) && f < Ttot;
+            if (have) {
+                int lo = 0, hi = n_items - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (sChunkOff[mid] <= f) lo = mid; else hi = mid - 1;
+                }
+                const Item t = sItems[lo];
+                h = __ldg(&p.hdr[t.c0 + (uint32_t)(f - sChunkOff[lo])]);
+                kwb = t.kwb;
+                dst_b = t.b;
+                w = t.w;
+            }
+            uint32_t lo_w[kUnit], hi_w[kUnit];
+#pragma unroll
+            for (int q = 0; q < kUnit; ++q) {
+                const uint32_t meta = __shfl_sync(FULL, h.y, q);
+                const uint32_t kb = __shfl_sync(FULL, kwb, q);
+                lo_w[q] = 0u;
+                hi_w[q] = 0u;
+                const uint32_t n = (meta & 31u) + 1u, bw = (meta >> 5) & 31u;
+                if (lane >= 1 && (uint32_t)lane < n && bw) {
+                    const uint32_t bit = (uint32_t)(lane - 1) * bw;
+                    const uint32_t wi = kb + (meta >> 10) + (bit >> 5);
+                    lo_w[q] = __ldg(&p.payload[wi]);
+                    hi_w[q] = __ldg(&p.payload[wi + 1]);
+                }
+            }
+            const uint32_t nval = (uint32_t)min((uint64_t)kUnit, Ttot - (uint64_t)unit * kUnit);
+#pragma unroll
+            for (int q = 0; q < kUnit; ++q) {
+                if ((uint32_t)q >= nval) break;
+                const uint32_t meta = __shfl_sync(FULL, h.y, q);
+                const uint32_t first = __shfl_sync(FULL, h.x, q);
+                const uint32_t bq = __shfl_sync(FULL, dst_b, q);
+                const float wq = __shfl_sync(FULL, w, q);
+                const uint32_t n = (meta & 31u) + 1u, bw = (meta >> 5) & 31u;
+                uint32_t g;
+                if (lane == 0) {
+                    g = first;
+                } else if ((uint32_t)lane < n) {
+                    uint32_t v = 0u;
+                    if (bw) {
+                        const uint32_t bit = (uint32_t)(lane - 1) * bw;
+                        v = (uint32_t)(((((uint64_t)hi_w[q]) << 32) | lo_w[q]) >> (bit & 31u)) & ((1u << bw) - 1u);
+                    }
+                    g = v + 1u;
+                } else {
+                    g = 0u;
+                }
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t t = __shfl_up_sync(FULL, g, o);
+                    if (lane >= o) g += t;
+                }
+                if ((uint32_t)lane < n) atomicAdd(&p.wide[(size_t)bq * p.n_pad + g], wq);
+            }
+        }
+        EBR_STAMP(2);
+    }
+    EBR_STAMP(4);
+    grid.sync();
+    EBR_STAMP(5);
+
+    // ---- C: fuse + histogram (8 independent elements in flight per thread) ----
+    constexpr int kIlp = 8;
+    for (int range = blockIdx.x; range < p.n_ranges; range += gridDim.x) {
+        const int64_t r0 = (int64_t)range * R;
+        const int64_t r1 = (r0 + R < p.n_ads) ? r0 + R : p.n_ads;
+        for (int b = 0; b < B; ++b) {
+            float* sc = p.scores + (size_t)b * p.n_pad;
+            float* wd = p.wide + (size_t)b * p.n_pad;
+            for (int64_t base = r0; base < r1; base += (int64_t)kThreads * kIlp) {
+                float dv[kIlp], wv[kIlp];
+#pragma unroll
+                for (int q = 0; q < kIlp; ++q) {
+                    const int64_t a = base + q * kThreads + tid;
+                    dv[q] = 0.f; wv[q] = 0.f;
+                    if (a < r1) { dv[q] = __ldcg(&sc[a]); wv[q] = __ldcg(&wd[a]); }
+                }
+#pragma unroll
+                for (int q = 0; q < kIlp; ++q) {
+                    const int64_t a = base + q * kThreads + tid;
+                    if (a < r1) {
+                        float s = dv[q] + wv[q];
+                        if (s == 0.f) s = 0.f;                  // -0 -> +0 (R14)
+                        __stcg(&wd[a], 0.f);
+                        __stcg(&sc[a], s);
+                        atomicAdd(&sHist[b * kHistBins + (ord_of(s) >> (32 - kHistBits))], 1u);
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+    for (int i = tid; i < B * kHistBins; i += kThreads) {
+        const uint32_t c = sHist[i];
+        if (c) atomicAdd(&p.ghist[i], c);
+    }
+    EBR_STAMP(6);
+    grid.sync();
+    EBR_STAMP(7);
+
+    // ---- D: threshold bin per user (warp b), then compaction ----
+    if (warp < B) {
+        const uint32_t* h = p.ghist + (size_t)warp * kHistBins;
+        constexpr int PER = kHistBins / 32;
+        uint32_t cnt[PER];
+        uint32_t local = 0;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) { cnt[j] = __ldcg(&h[kHistBins - 1 - (lane * PER + j)]); local += cnt[j]; }
+        uint32_t incl = local;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t x = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += x;
+        }
+        uint32_t c = incl - local;
+        int found = -1;
+        const uint32_t K = (uint32_t)p.K;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            if (found < 0 && c < K && c + cnt[j] >= K) found = kHistBins - 1 - (lane * PER + j);
+            c += cnt[j];
+        }
+        const unsigned m = __ballot_sync(FULL, found >= 0);
+        const int fb = __shfl_sync(FULL, found, m ? __ffs(m) - 1 : 0);
+        if (lane == 0) sBinStar[warp] = m ? (uint32_t)fb : 0u;   // < K ads: all are candidates
+    }
+    __syncthreads();
+    for (int range = blockIdx.x; range < p.n_ranges; range += gridDim.x) {
+        const int64_t r0 = (int64_t)range * R;
+        const int64_t r1 = (r0 + R < p.n_ads) ? r0 + R : p.n_ads;
+        for (int b = 0; b < B; ++b) {
+            const float* sc = p.scores + (size_t)b * p.n_pad;
+            const uint32_t bs = sBinStar[b];
+            for (int64_t base = r0; base < r1; base += (int64_t)kThreads * kIlp) {
+                float sv[kIlp];
+#pragma unroll
+                for (int q = 0; q < kIlp; ++q) {
+                    const int64_t a = base + q * kThreads + tid;
+                    sv[q] = (a < r1) ? __ldcg(&sc[a]) : 0.f;
+                }
+#pragma unroll
+                for (int q = 0; q < kIlp; ++q) {
+                    const int64_t a = base + q * kThreads + tid;
+                    const bool take = (a < r1) && (ord_of(sv[q]) >> (32 - kHistBits)) >= bs;
+                    const unsigned m = __ballot_sync(FULL, take);
+                    if (m) {
+                        const int leader = __ffs(m) - 1;
+                        uint32_t pos = 0;
+                        if (lane == leader) pos = atomicAdd(&p.cand_count[b], (uint32_t)__popc(m));
+                        pos = __shfl_sync(FULL, pos, leader);
+                        if (take)
+                            p.cand[(size_t)b * p.n_pad + pos + __popc(m & ((1u << lane) - 1u))] =
+                                kappa_of(sv[q], p.ad_begin + (uint32_t)a);
+                    }
+                }
+            }
+        }
+    }
+    EBR_STAMP(8);
+    grid.sync();
+    EBR_STAMP(9);
+
+    // ---- E: exact selection, one CTA per user; leave the workspace zeroed ----
+    for (int b = blockIdx.x; b < B; b += gridDim.x) {
+        const int P = pow2ceil_i(p.K);
+        uint64_t* sbuf = reinterpret_cast<uint64_t*>(smem);
+        uint32_t* shist = reinterpret_cast<uint32_t*>(sbuf + P);
+        uint64_t* scand = reinterpret_cast<uint64_t*>(shist + 256);
+        const int64_t scap = ((int64_t)p.smem_bytes - (int64_t)P * 8 - 1024) / 8;
+        const int64_t n = (int64_t)__ldcg(&p.cand_count[b]);
+        const uint64_t* cb = p.cand + (size_t)b * p.n_pad;
+        const int nsel = cta_select_topk([cb](int64_t i) { return __ldcg(&cb[i]); }, n, p.K, sbuf,
+                                         scand, scap, shist, sScalar,
+                                         (p.timers && b == 0) ? p.timers + 11 : nullptr);
+        cta_write_topk(sbuf, nsel, p.K, p.out_ids ? p.out_ids + (size_t)b * p.K : nullptr,
+                       p.out_scores ? p.out_scores + (size_t)b * p.K : nullptr,
+                       p.out_keys ? p.out_keys + (size_t)b * p.K : nullptr);
+        for (int i = tid; i < kHistBins; i += kThreads) p.ghist[(size_t)b * kHistBins + i] = 0;
+        if (tid == 0) p.cand_count[b] = 0;
+        __syncthreads();
+    }
+    if (blockIdx.x == 0 && tid == 0) { p.header[0] = p.magic; p.header[2] = 0; }
+    EBR_STAMP(10);
+}
+
+typedef void (*kern_t)(const SmallParams);
+
+// kernel instances, one translation unit per (dtype, row shape) so they compile in parallel
+template <typename T, int LPR, int VPL>
+kern_t pick_nb(int nb);
+
+#define EBR_SMALL_INSTANTIATE(T, LPR, VPL)                     \
+    template <>                                                \
+    kern_t pick_nb<T, LPR, VPL>(int nb) {                      \
+        switch (nb) {                                          \
+            case 1: return small_kernel<T, 1, LPR, VPL>;       \
+            case 2: return small_kernel<T, 2, LPR, VPL>;       \
+            case 4: return small_kernel<T, 4, LPR, VPL>;       \
+            case 8: return small_kernel<T, 8, LPR, VPL>;       \
+        }                                                      \
+        return nullptr;                                        \
+    }
+
+}  // namespace small
+}  // namespace ebr
