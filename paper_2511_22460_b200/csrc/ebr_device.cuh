@@ -229,64 +229,109 @@ __device__ __forceinline__ void warp_hist_add(uint32_t* hist, uint32_t bin, bool
 
 // ------------------------------------------------------------------------------------------
 // A6: exact top-K of a set of unique 64-bit keys, by one CTA.
-//   1. radix select (8 passes of 8-bit digits, warp-aggregated shared histograms) finds the
-//      K-th largest key exactly;
-//   2. the keys >= it (exactly K, keys are unique) are gathered into shared memory;
-//   3. bitonic sort descending.
-// `get(i)` returns key i (global memory).  If n <= scand_cap the keys are first staged in
-// scand (shared).  sbuf holds >= pow2ceil(min(n,K)) keys; shist 256 words; sscalar 4 words.
-// Returns the number of selected keys (min(n, K)) sorted descending in sbuf[0..).
+//   1. the bits common to every key are skipped (AND/OR reduction);
+//   2. radix select with 11-bit digits, MSB first, finds the K-th largest key; it stops early as
+//      soon as the digit bucket holding the K-th is needed in full;
+//   3. the keys >= the threshold (exactly K: keys are unique) are gathered into shared memory;
+//   4. bitonic sort, descending (warp shuffles for strides < 32, registers for strides >= the
+//      CTA size, shared memory in between).
+// `get(i)` returns key i.  If n <= scand_cap the keys are first staged in scand (shared).
+// sbuf holds >= pow2ceil(min(n,K)) keys; shist kSelBins words; sscalar 8 words.
 // ------------------------------------------------------------------------------------------
+constexpr int kSelBits = 11;
+constexpr int kSelBins = 1 << kSelBits;
+
+__device__ __forceinline__ uint64_t warp_and64(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v &= __shfl_xor_sync(FULL, v, o);
+    return v;
+}
+__device__ __forceinline__ uint64_t warp_or64(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v |= __shfl_xor_sync(FULL, v, o);
+    return v;
+}
+
 template <typename Get>
 __device__ int cta_radix_select(Get get, int64_t n, int K, uint64_t* sbuf, uint32_t* shist,
                                 uint32_t* sscalar) {
-    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
-    uint64_t prefix = 0;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    uint64_t* sred = reinterpret_cast<uint64_t*>(shist);   // 2 x 32 words of scratch
+    // 1. common prefix of all keys
+    uint64_t va = ~0ull, vo = 0ull;
+    for (int64_t i = tid; i < n; i += nt) { const uint64_t x = get(i); va &= x; vo |= x; }
+    va = warp_and64(va);
+    vo = warp_or64(vo);
+    if (lane == 0) { sred[warp] = va; sred[32 + warp] = vo; }
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = (nt + 31) >> 5;
+        uint64_t a = lane < nw ? sred[lane] : ~0ull, o = lane < nw ? sred[32 + lane] : 0ull;
+        a = warp_and64(a);
+        o = warp_or64(o);
+        if (lane == 0) { sred[0] = a; sred[1] = o; }
+    }
+    __syncthreads();
+    const uint64_t kand = sred[0], kor = sred[1];
+    __syncthreads();
+    const uint64_t diff = kand ^ kor;                 // n > K >= 1 unique keys => diff != 0
+    int hi = 63 - __clzll((long long)diff);
+    uint64_t prefix = kand & ~((hi >= 63) ? ~0ull : ((2ull << hi) - 1ull));
     uint32_t need = (uint32_t)K;
-    for (int shift = 56; shift >= 0; shift -= 8) {
-        for (int i = tid; i < 256; i += nt) shist[i] = 0;
+    while (hi >= 0) {
+        const int width = hi + 1 < kSelBits ? hi + 1 : kSelBits;
+        const int shift = hi + 1 - width;
+        const uint32_t nb = 1u << width;
+        for (int i = tid; i < (int)nb; i += nt) shist[i] = 0;
         __syncthreads();
-        const uint64_t hmask = (shift == 56) ? 0ull : (~0ull << (shift + 8));
-        for (int64_t base = 0; base < n; base += nt) {
-            const int64_t i = base + tid;
-            uint64_t x = 0;
-            bool act = false;
-            if (i < n) { x = get(i); act = ((x ^ prefix) & hmask) == 0ull; }
-            warp_hist_add(shist, (uint32_t)(x >> shift) & 255u, act);
+        const uint64_t hmask = (hi >= 63) ? 0ull : ~((2ull << hi) - 1ull);
+        for (int64_t i = tid; i < n; i += nt) {
+            const uint64_t x = get(i);
+            if (((x ^ prefix) & hmask) == 0ull) atomicAdd(&shist[(uint32_t)(x >> shift) & (nb - 1u)], 1u);
         }
         __syncthreads();
-        if (tid < 32) {
-            // warp 0: digit t with count(>t) < need <= count(>=t), scanning 255..0
-            uint32_t cnt[8];
+        if (warp == 0) {
+            // digit t (scanning nb-1 .. 0): count(> t) < need <= count(>= t)
+            const int per = (int)(nb + 31) >> 5;
             uint32_t local = 0;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) { cnt[j] = shist[255 - (tid * 8 + j)]; local += cnt[j]; }
+            for (int j = 0; j < per; ++j) {
+                const int d = (int)nb - 1 - (lane * per + j);
+                if (d >= 0) local += shist[d];
+            }
             uint32_t incl = local;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t t = __shfl_up_sync(FULL, incl, o);
-                if (tid >= o) incl += t;
+                if (lane >= o) incl += t;
             }
             uint32_t c = incl - local;
             int found = -1;
-            uint32_t above = 0;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                if (found < 0 && c < need && c + cnt[j] >= need) { found = 255 - (tid * 8 + j); above = c; }
-                c += cnt[j];
+            uint32_t above = 0, cnt_t = 0;
+            if (c < need && c + local >= need) {
+                for (int j = 0; j < per; ++j) {
+                    const int d = (int)nb - 1 - (lane * per + j);
+                    if (d < 0) break;
+                    const uint32_t h = shist[d];
+                    if (found < 0 && c < need && c + h >= need) { found = d; above = c; cnt_t = h; }
+                    c += h;
+                }
             }
             const unsigned m = __ballot_sync(FULL, found >= 0);
             const int src = __ffs(m) - 1;
             const int t = __shfl_sync(FULL, found, src);
             const uint32_t ab = __shfl_sync(FULL, above, src);
-            if (tid == 0) { sscalar[0] = (uint32_t)t; sscalar[1] = ab; }
+            const uint32_t ct = __shfl_sync(FULL, cnt_t, src);
+            if (lane == 0) { sscalar[0] = (uint32_t)t; sscalar[1] = ab; sscalar[3] = ct; }
         }
         __syncthreads();
         prefix |= (uint64_t)sscalar[0] << shift;
         need -= sscalar[1];
+        const bool done = (sscalar[3] == need);     // the whole bucket is needed: stop here
         __syncthreads();
+        if (done) break;
+        hi = shift - 1;
     }
-    // prefix == the K-th largest key; gather the keys >= prefix (exactly K of them)
+    // gather the keys >= prefix (exactly K of them)
     if (tid == 0) sscalar[2] = 0;
     __syncthreads();
     for (int64_t base = 0; base < n; base += nt) {
@@ -304,12 +349,70 @@ __device__ int cta_radix_select(Get get, int64_t n, int K, uint64_t* sbuf, uint3
     return K;
 }
 
+// Bitonic sort (descending) of sbuf[0..P), P = pow2ceil(nsel), entries >= nsel padded with 0.
+// Element i lives in thread (i % nt), register (i / nt): strides < 32 use warp shuffles,
+// strides >= nt stay in registers, the others go through shared memory.
+template <int E>
+__device__ __forceinline__ void cta_bitonic_fast(uint64_t* sbuf, int P) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    uint64_t v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) { const int i = tid + e * nt; v[e] = i < P ? sbuf[i] : 0ull; }
+    for (int size = 2; size <= P; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            if (stride >= nt) {
+                const int em = stride / nt;
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const int e2 = e ^ em;
+                    if (e2 > e && e2 < E) {
+                        const int i = tid + e * nt;
+                        const bool desc = (i & size) == 0;
+                        const uint64_t a = v[e], b = v[e2];
+                        if ((a < b) == desc) { v[e] = b; v[e2] = a; }
+                    }
+                }
+            } else if (stride >= 32) {
+#pragma unroll
+                for (int e = 0; e < E; ++e) { const int i = tid + e * nt; if (i < P) sbuf[i] = v[e]; }
+                __syncthreads();
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const int i = tid + e * nt;
+                    if (i < P) {
+                        const uint64_t o = sbuf[i ^ stride];
+                        const bool lower = (i & stride) == 0, desc = (i & size) == 0;
+                        const uint64_t mx = v[e] > o ? v[e] : o, mn = v[e] > o ? o : v[e];
+                        v[e] = (lower == desc) ? mx : mn;
+                    }
+                }
+                __syncthreads();
+            } else {
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const int i = tid + e * nt;
+                    const uint64_t o = __shfl_xor_sync(FULL, v[e], stride);
+                    const bool lower = (i & stride) == 0, desc = (i & size) == 0;
+                    const uint64_t mx = v[e] > o ? v[e] : o, mn = v[e] > o ? o : v[e];
+                    v[e] = (lower == desc) ? mx : mn;
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) { const int i = tid + e * nt; if (i < P) sbuf[i] = v[e]; }
+    __syncthreads();
+}
+
 __device__ __forceinline__ void cta_bitonic_desc(uint64_t* sbuf, int nsel) {
     const int tid = threadIdx.x, nt = blockDim.x;
     int P = 1;
     while (P < nsel) P <<= 1;
     for (int i = nsel + tid; i < P; i += nt) sbuf[i] = 0ull;
     __syncthreads();
+    if (P <= nt) { cta_bitonic_fast<1>(sbuf, P); return; }
+    if (P <= 2 * nt) { cta_bitonic_fast<2>(sbuf, P); return; }
+    if (P <= 4 * nt) { cta_bitonic_fast<4>(sbuf, P); return; }
     for (int size = 2; size <= P; size <<= 1) {
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
             for (int i = tid; i < (P >> 1); i += nt) {
@@ -332,6 +435,7 @@ __device__ __forceinline__ void stamp_max(unsigned long long* tm, int i) {
     }
 }
 
+// Selects the min(n, K) largest keys, sorted descending into sbuf.  Returns that count.
 template <typename Get>
 __device__ int cta_select_topk(Get get, int64_t n, int K, uint64_t* sbuf, uint64_t* scand,
                                int64_t scand_cap, uint32_t* shist, uint32_t* sscalar,

@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(kThreads) merge_kernel(const uint64_t* __restr
     const int P = pow2ceil_i(K);
     uint64_t* sbuf = reinterpret_cast<uint64_t*>(smem);
     uint32_t* shist = reinterpret_cast<uint32_t*>(sbuf + P);
-    uint64_t* scand = reinterpret_cast<uint64_t*>(shist + 256);
+    uint64_t* scand = reinterpret_cast<uint64_t*>(shist + kSelBins);
     const int b = blockIdx.x;
     const int64_t n = (int64_t)G * K;
     auto get = [=](int64_t i) {
@@ -239,7 +239,7 @@ __global__ void decode_key_kernel(const uint2* __restrict__ hdr, const uint32_t*
 
 ebr_status run_merge(const uint64_t* gathered, int32_t G, int32_t batch, int32_t k,
                      int32_t* out_ids, float* out_scores, cudaStream_t stream) {
-    const size_t base = (size_t)pow2ceil_i(k) * 8 + 256 * 4;
+    const size_t base = (size_t)pow2ceil_i(k) * 8 + kSelBins * 4;
     const size_t cap_bytes = 200 * 1024 > base ? 200 * 1024 - base : 0;
     int64_t scand_cap = std::min<int64_t>((int64_t)G * k, (int64_t)(cap_bytes / 8));
     if (scand_cap < (int64_t)G * k) scand_cap = 0;   // too many: select straight from global

@@ -35,7 +35,7 @@ SmallLayout small_layout(const ebr_index* idx, int B) {
     size_t o = 0;
     L.off_header = o; o = al(o + 16 + 16 * 8);   // magic, error word, 16 phase stamps
     L.off_hist = o;   o = al(o + (size_t)B * kHistBins * 4);
-    L.off_count = o;  o = al(o + (size_t)B * 4);
+    L.off_count = o;  o = al(o + (size_t)B * (idx->sm_count + 1) * 4);   // [B][n_ranges]
     L.off_scores = o; o = al(o + (size_t)B * idx->n_pad * 4);
     L.off_wide = o;   o = al(o + (size_t)B * idx->n_pad * 4);
     L.off_cand = o;   o = al(o + (size_t)B * idx->n_pad * 8);
@@ -72,11 +72,21 @@ ebr_status run_small(const QueryArgs& q, int b0, int B) {
     if (!k) return set_error(EBR_EUNSUPPORTED, "embedding row of %d bytes is not supported", row_bytes);
 
     const int items_cap = B * idx->n_fields * q.slots;
-    const size_t p1 = (size_t)B * kHistBins * 4 + (size_t)items_cap * sizeof(Item) + 8 +
-                      (size_t)(items_cap + 1) * 8;
-    const size_t sel_min = (size_t)pow2ceil_i(q.k) * 8 + 1024 + 64 * 1024;   // + >= 8k staged candidates
+    const int sms = idx->sm_count;
+    int64_t R = (idx->n_ads + sms - 1) / sms;
+    R = std::max<int64_t>(32, (R + 31) & ~(int64_t)31);
+    const int n_ranges = (int)((idx->n_ads + R - 1) / R);
+    const size_t plan_bytes = (size_t)B * kHistBins * 4 + (size_t)items_cap * sizeof(Item) + 8 +
+                              (size_t)(items_cap + 1) * 8;
+    const size_t sel_min = (size_t)pow2ceil_i(q.k) * 8 + kSelBins * 4 + (size_t)(n_ranges + 2) * 4 +
+                           64 * 1024;   // + >= 8k staged candidates
+    const size_t cap = 227 * 1024;
+    // keep the CTA's deep/fused scores in shared memory when they fit
+    const size_t res_bytes = (size_t)B * R * 4;
+    const bool resident = plan_bytes + res_bytes <= cap - 8 * 1024;
+    const size_t p1 = plan_bytes + (resident ? res_bytes : 0);
     const size_t smem = std::max(p1, sel_min);
-    if (smem > 227 * 1024)
+    if (smem > cap)
         return set_error(EBR_EUNSUPPORTED, "latency path: %d user slots / k=%d need %zu B of shared memory",
                          items_cap, q.k, smem);
 
@@ -86,9 +96,6 @@ ebr_status run_small(const QueryArgs& q, int b0, int B) {
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, smem);
     if (e != cudaSuccess || occ < 1) return cuda_check(e == cudaSuccess ? cudaErrorInvalidConfiguration : e, "occupancy(small)");
 
-    const int sms = idx->sm_count;
-    int64_t R = (idx->n_ads + sms - 1) / sms;
-    R = std::max<int64_t>(32, (R + 31) & ~(int64_t)31);
     SmallParams p;
     p.A = idx->A; p.d = idx->d; p.d_pad = idx->d_pad;
     p.row_bytes = row_bytes;
@@ -116,7 +123,8 @@ ebr_status run_small(const QueryArgs& q, int b0, int B) {
     p.out_scores = q.out_scores ? q.out_scores + (size_t)b0 * q.k : nullptr;
     p.out_keys = q.out_keys ? q.out_keys + (size_t)b0 * q.k : nullptr;
     p.R = (int32_t)R;
-    p.n_ranges = (int32_t)((idx->n_ads + R - 1) / R);
+    p.n_ranges = n_ranges;
+    p.resident = resident ? 1 : 0;
     p.items_cap = items_cap;
     p.smem_bytes = (int32_t)smem;
 

@@ -75,10 +75,10 @@ struct SmallParams {
     unsigned long long* timers; // optional phase stamps (EBR_PHASE_TIMERS=1), else null
     uint32_t magic;
     uint32_t* ghist;            // [B][kHistBins]
-    uint32_t* cand_count;       // [B]
+    uint32_t* cand_count;       // [B][n_ranges] candidates per CTA segment
     float* scores;              // [B][n_pad]  deep, then fused score
     float* wide;                // [B][n_pad]  wide accumulator (zero between calls)
-    uint64_t* cand;             // [B][n_pad]
+    uint64_t* cand;             // [B][n_pad]  CTA r's segment starts at r * R
     // outputs
     int32_t* out_ids;           // [B][K] (already offset to this launch's first user)
     float* out_scores;
@@ -89,6 +89,7 @@ struct SmallParams {
     int32_t items_cap;          // >= B * F * S
     int32_t smem_bytes;
     int32_t diag;               // EBR_DIAG bits (diagnostics only): 1 = skip wide, 2 = skip deep
+    int32_t resident;           // deep / fused scores of the CTA's range kept in shared memory
 };
 
 struct Item {
@@ -135,6 +136,29 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #define EBR_STAMP(i) do { if (p.timers && (tid & 31) == 0) atomicMax(&p.timers[i], gtimer()); } while (0)
 
+// bar.sync/arrive on a named barrier (ids 1.. are free; 0 is __syncthreads)
+__device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// exclusive scan over the threads [t0, t0 + 32*nw) of a named-barrier group
+__device__ __forceinline__ uint32_t group_exclusive_scan(uint32_t v, uint32_t* scratch, uint32_t* total,
+                                                         int gtid, int nw, int bar_id) {
+    const int lane = gtid & 31, w = gtid >> 5;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) scratch[w] = incl;
+    nbar_sync(bar_id, nw * 32);
+    uint32_t before = 0, tot = 0;
+    for (int j = 0; j < nw; ++j) { const uint32_t x = scratch[j]; if (j < w) before += x; tot += x; }
+    *total = tot;
+    nbar_sync(bar_id, nw * 32);
+    return before + incl - v;
+}
+
 template <typename T, int NB, int LPR, int VPL>
 __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p) {
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -142,35 +166,42 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
     const int B = p.B, R = p.R;
     const cg::grid_group grid = cg::this_grid();
     // ---- shared-memory carve-up ----
-    uint32_t* sHist = reinterpret_cast<uint32_t*>(smem);                          // [B][bins]
+    float* sS = reinterpret_cast<float*>(smem);                                   // [B][R] if resident
+    uint32_t* sHist = reinterpret_cast<uint32_t*>(sS + (p.resident ? (size_t)B * R : 0));  // [B][bins]
     Item* sItems = reinterpret_cast<Item*>(sHist + (size_t)B * kHistBins);        // [items_cap]
     uint64_t* sChunkOff = reinterpret_cast<uint64_t*>(
         (reinterpret_cast<uintptr_t>(sItems + p.items_cap) + 7) & ~(uintptr_t)7);  // [items_cap + 1]
     __shared__ uint32_t sScan[40], sScalar[8], sNItems;
-    __shared__ uint32_t sBinStar[kSmallMaxB];
+    __shared__ uint32_t sBinStar[kSmallMaxB], sSeg[kSmallMaxB];
     __shared__ int sInit;
+
+    const bool has_range = (int)blockIdx.x < p.n_ranges;
+    const int64_t r0 = (int64_t)blockIdx.x * R;
+    const int64_t r1 = has_range ? ((r0 + R < p.n_ads) ? r0 + R : p.n_ads) : r0;
+    const int rn = (int)(r1 - r0);
 
     if (p.timers && blockIdx.x == 0 && tid == 0) p.timers[0] = gtimer();
     // ---- first use of this workspace: zero it (uniform decision across the grid) ----
     if (tid == 0) sInit = (__ldcg(&p.header[0]) != p.magic);
     for (int i = tid; i < B * kHistBins; i += kThreads) sHist[i] = 0;
+    if (tid < kSmallMaxB) sSeg[tid] = 0;
     __syncthreads();
-    if (sInit) {   // workspace not initialised (ebr_workspace_init not called): do it here
+    if (sInit) {   // ebr_workspace_init was not called: do it here
         const size_t nw = (size_t)kSmallMaxB * p.n_pad;
         for (size_t i = (size_t)blockIdx.x * kThreads + tid; i < nw; i += (size_t)gridDim.x * kThreads) p.wide[i] = 0.f;
         if (blockIdx.x == 0) {
             for (int i = tid; i < kSmallMaxB * kHistBins; i += kThreads) p.ghist[i] = 0;
-            if (tid < kSmallMaxB) p.cand_count[tid] = 0;
             if (tid == 0) { p.header[1] = 0; p.header[2] = 0; }
         }
         grid.sync();
     }
 
-    // ---- A: plan, deterministic item order ----
-    {
+    if (warp >= kDeepWarps) {
+        // ---- A: plan by the wide warps (deterministic item order; named barrier 1) ----
+        const int gt = tid - kDeepWarps * 32, NT = kWideWarps * 32;
         const int nslot = B * p.n_fields * p.slots;
-        const int per = (nslot + kThreads - 1) / kThreads;
-        const int s0 = min(nslot, tid * per), s1 = min(nslot, s0 + per);
+        const int per = (nslot + NT - 1) / NT;
+        const int s0 = min(nslot, gt * per), s1 = min(nslot, s0 + per);
         uint32_t cnt = 0;
         for (int i = s0; i < s1; ++i) {
             const int f = (i / p.slots) % p.n_fields;
@@ -184,7 +215,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
             if (__ldg(&p.key_chunk_off[key + 1]) > __ldg(&p.key_chunk_off[key])) ++cnt;
         }
         uint32_t total;
-        uint32_t pos = block_exclusive_scan(cnt, sScan, &total);
+        uint32_t pos = group_exclusive_scan(cnt, sScan, &total, gt, kWideWarps, 1);
         for (int i = s0; i < s1; ++i) {
             const int b = i / (p.n_fields * p.slots);
             const int f = (i / p.slots) % p.n_fields;
@@ -201,25 +232,22 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
             it.w = __fmul_rn(__ldg(&p.cross_w[key]), p.user_x[i]);   // w~ = fl32(w x), never an FMA (R10)
             sItems[pos++] = it;
         }
-        if (tid == 0) sNItems = total;
-        __syncthreads();
-        // exclusive scan of chunk counts over items
+        if (gt == 0) sNItems = total;
+        nbar_sync(1, NT);
         const int n_items = (int)sNItems;
-        const int per2 = (n_items + kThreads - 1) / kThreads;
-        const int i0 = min(n_items, tid * per2), i1 = min(n_items, i0 + per2);
+        const int per2 = (n_items + NT - 1) / NT;
+        const int i0 = min(n_items, gt * per2), i1 = min(n_items, i0 + per2);
         uint32_t loc = 0;
         for (int i = i0; i < i1; ++i) loc += sItems[i].c1 - sItems[i].c0;
         uint32_t tot2;
-        uint64_t acc = block_exclusive_scan(loc, sScan, &tot2);
+        uint64_t acc = group_exclusive_scan(loc, sScan, &tot2, gt, kWideWarps, 1);
         for (int i = i0; i < i1; ++i) { sChunkOff[i] = acc; acc += sItems[i].c1 - sItems[i].c0; }
-        if (tid == 0) sChunkOff[n_items] = tot2;
-        __syncthreads();
-    }
-    const int n_items = (int)sNItems;
-    EBR_STAMP(1);
-
-    // ---- B: deep warps stream A (then help), wide warps drain the global unit queue ----
-    if (warp < kDeepWarps && !(p.diag & 2)) {
+        if (gt == 0) sChunkOff[n_items] = tot2;
+        __threadfence_block();
+        nbar_arrive(2, kThreads);          // publish the plan to the deep warps (barrier 2)
+        EBR_STAMP(1);
+    } else if (!(p.diag & 2)) {
+        // ---- B (deep): stream this CTA's rows of A, 8 x 16-byte loads in flight per lane ----
         using V = Vec<T>;
         constexpr int E = V::E;
         constexpr int lpr = LPR;
@@ -236,56 +264,57 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
                     u[b][v][e] = (b < B && j < p.d) ? V::elem(p.U, (int64_t)b * p.d + j) : 0.f;
                 }
         const char* Abase = reinterpret_cast<const char*>(p.A);
-        for (int range = blockIdx.x; range < p.n_ranges; range += gridDim.x) {
-            const int64_t r0 = (int64_t)range * R;
-            const int64_t r1 = (r0 + R < p.n_ads) ? r0 + R : p.n_ads;
-            const int64_t step = (int64_t)kDeepWarps * rpw * kUnroll;
-            for (int64_t base = r0 + (int64_t)warp * rpw; base < r1; base += step) {
-                uint4 av[kUnroll][VPL];
+        constexpr int64_t step = (int64_t)kDeepWarps * rpw * kUnroll;
+        for (int64_t base = r0 + (int64_t)warp * rpw; base < r1; base += step) {
+            uint4 av[kUnroll][VPL];
 #pragma unroll
-                for (int q = 0; q < kUnroll; ++q) {
-                    const int64_t row = base + (int64_t)q * kDeepWarps * rpw + sub;
+            for (int q = 0; q < kUnroll; ++q) {
+                const int64_t row = base + (int64_t)q * kDeepWarps * rpw + sub;
 #pragma unroll
-                    for (int v = 0; v < VPL; ++v) {
-                        if (row < r1)
-                            av[q][v] = ldg_stream(Abase + row * p.row_bytes + (int64_t)(li + v * lpr) * 16);
-                        else
-                            av[q][v] = make_uint4(0, 0, 0, 0);
-                    }
+                for (int v = 0; v < VPL; ++v) {
+                    if (row < r1)
+                        av[q][v] = ldg_stream(Abase + row * p.row_bytes + (int64_t)(li + v * lpr) * 16);
+                    else
+                        av[q][v] = make_uint4(0, 0, 0, 0);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < kUnroll; ++q) {
+                float acc[NB];
+#pragma unroll
+                for (int b = 0; b < NB; ++b) acc[b] = 0.f;
+#pragma unroll
+                for (int v = 0; v < VPL; ++v) {
+                    float a[E];
+                    V::unpack(av[q][v], a);
+#pragma unroll
+                    for (int b = 0; b < NB; ++b)
+#pragma unroll
+                        for (int e = 0; e < E; ++e) acc[b] = fmaf(a[e], u[b][v][e], acc[b]);
                 }
 #pragma unroll
-                for (int q = 0; q < kUnroll; ++q) {
-                    float acc[NB];
+                for (int o = lpr / 2; o > 0; o >>= 1) {
 #pragma unroll
-                    for (int b = 0; b < NB; ++b) acc[b] = 0.f;
+                    for (int b = 0; b < NB; ++b) acc[b] += __shfl_xor_sync(FULL, acc[b], o);
+                }
+                const int64_t row = base + (int64_t)q * kDeepWarps * rpw + sub;
+                if (li == 0 && row < r1) {
 #pragma unroll
-                    for (int v = 0; v < VPL; ++v) {
-                        float a[E];
-                        V::unpack(av[q][v], a);
-#pragma unroll
-                        for (int b = 0; b < NB; ++b)
-#pragma unroll
-                            for (int e = 0; e < E; ++e) acc[b] = fmaf(a[e], u[b][v][e], acc[b]);
-                    }
-#pragma unroll
-                    for (int o = lpr / 2; o > 0; o >>= 1) {
-#pragma unroll
-                        for (int b = 0; b < NB; ++b) acc[b] += __shfl_xor_sync(FULL, acc[b], o);
-                    }
-                    const int64_t row = base + (int64_t)q * kDeepWarps * rpw + sub;
-                    if (li == 0 && row < r1) {
-#pragma unroll
-                        for (int b = 0; b < NB; ++b)
-                            if (b < B) __stcg(&p.scores[(size_t)b * p.n_pad + row], acc[b]);
-                    }
+                    for (int b = 0; b < NB; ++b)
+                        if (b < B) {
+                            if (p.resident) sS[(size_t)b * R + (row - r0)] = acc[b];
+                            else __stcg(&p.scores[(size_t)b * p.n_pad + row], acc[b]);
+                        }
                 }
             }
         }
         EBR_STAMP(3);
     }
+    if (warp < kDeepWarps) nbar_sync(2, kThreads);   // deep warps wait for the plan before helping
     {
-        // wide: 16-chunk units of the flat chunk space, claimed from a global queue
+        // ---- B (wide): 16-chunk units of the flat chunk space from a global queue ----
         // (the paper's LoadBalance, Alg. 2 l.354); units may straddle items.
+        const int n_items = (int)sNItems;
         const uint64_t Ttot = sChunkOff[n_items];
         const uint64_t n_units = (p.diag & 1) ? 0 : (Ttot + kUnit - 1) / kUnit;
         while (true) {
@@ -294,13 +323,11 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
             unit = __shfl_sync(FULL, unit, 0);
             if (unit >= n_units) break;
             const uint64_t f = (uint64_t)unit * kUnit + (lane & (kUnit - 1));
-            // this lane's chunk: item = last it with sChunkOff[it] <= f
             uint2 h = make_uint2(0u, 0u);
             uint32_t kwb = 0, dst_b = 0;
             float w = 0.f;
-            const bool have = (lane < kUnit) && f < Ttot;
-            if (have) {
-                int lo = 0, hi = n_items - 1;
+            if ((lane < kUnit) && f < Ttot) {
+                int lo = 0, hi = n_items - 1;     // item = last it with sChunkOff[it] <= f
                 while (lo < hi) {
                     const int mid = (lo + hi + 1) >> 1;
                     if (sChunkOff[mid] <= f) lo = mid; else hi = mid - 1;
@@ -364,30 +391,29 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
 
     // ---- C: fuse + histogram (8 independent elements in flight per thread) ----
     constexpr int kIlp = 8;
-    for (int range = blockIdx.x; range < p.n_ranges; range += gridDim.x) {
-        const int64_t r0 = (int64_t)range * R;
-        const int64_t r1 = (r0 + R < p.n_ads) ? r0 + R : p.n_ads;
-        for (int b = 0; b < B; ++b) {
-            float* sc = p.scores + (size_t)b * p.n_pad;
-            float* wd = p.wide + (size_t)b * p.n_pad;
-            for (int64_t base = r0; base < r1; base += (int64_t)kThreads * kIlp) {
-                float dv[kIlp], wv[kIlp];
+    for (int b = 0; b < B; ++b) {
+        float* sc = p.scores + (size_t)b * p.n_pad;
+        float* wd = p.wide + (size_t)b * p.n_pad;
+        for (int base = 0; base < rn; base += kThreads * kIlp) {
+            float dv[kIlp], wv[kIlp];
 #pragma unroll
-                for (int q = 0; q < kIlp; ++q) {
-                    const int64_t a = base + q * kThreads + tid;
-                    dv[q] = 0.f; wv[q] = 0.f;
-                    if (a < r1) { dv[q] = __ldcg(&sc[a]); wv[q] = __ldcg(&wd[a]); }
+            for (int q = 0; q < kIlp; ++q) {
+                const int r = base + q * kThreads + tid;
+                dv[q] = 0.f; wv[q] = 0.f;
+                if (r < rn) {
+                    dv[q] = p.resident ? sS[(size_t)b * R + r] : __ldcg(&sc[r0 + r]);
+                    wv[q] = __ldcg(&wd[r0 + r]);
                 }
+            }
 #pragma unroll
-                for (int q = 0; q < kIlp; ++q) {
-                    const int64_t a = base + q * kThreads + tid;
-                    if (a < r1) {
-                        float s = dv[q] + wv[q];
-                        if (s == 0.f) s = 0.f;                  // -0 -> +0 (R14)
-                        __stcg(&wd[a], 0.f);
-                        __stcg(&sc[a], s);
-                        atomicAdd(&sHist[b * kHistBins + (ord_of(s) >> (32 - kHistBits))], 1u);
-                    }
+            for (int q = 0; q < kIlp; ++q) {
+                const int r = base + q * kThreads + tid;
+                if (r < rn) {
+                    float s = dv[q] + wv[q];
+                    if (s == 0.f) s = 0.f;                  // -0 -> +0 (R14)
+                    __stcg(&wd[r0 + r], 0.f);               // leave the wide array zeroed
+                    if (p.resident) sS[(size_t)b * R + r] = s; else __stcg(&sc[r0 + r], s);
+                    atomicAdd(&sHist[b * kHistBins + (ord_of(s) >> (32 - kHistBits))], 1u);
                 }
             }
         }
@@ -401,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
     grid.sync();
     EBR_STAMP(7);
 
-    // ---- D: threshold bin per user (warp b), then compaction ----
+    // ---- D: threshold bin per user (warp b), then compaction into this CTA's segment ----
     if (warp < B) {
         const uint32_t* h = p.ghist + (size_t)warp * kHistBins;
         constexpr int PER = kHistBins / 32;
@@ -428,37 +454,34 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
         if (lane == 0) sBinStar[warp] = m ? (uint32_t)fb : 0u;   // < K ads: all are candidates
     }
     __syncthreads();
-    for (int range = blockIdx.x; range < p.n_ranges; range += gridDim.x) {
-        const int64_t r0 = (int64_t)range * R;
-        const int64_t r1 = (r0 + R < p.n_ads) ? r0 + R : p.n_ads;
-        for (int b = 0; b < B; ++b) {
-            const float* sc = p.scores + (size_t)b * p.n_pad;
-            const uint32_t bs = sBinStar[b];
-            for (int64_t base = r0; base < r1; base += (int64_t)kThreads * kIlp) {
-                float sv[kIlp];
+    for (int b = 0; b < B; ++b) {
+        const float* sc = p.scores + (size_t)b * p.n_pad;
+        uint64_t* seg = p.cand + (size_t)b * p.n_pad + r0;       // this CTA's candidate segment
+        const uint32_t bs = sBinStar[b];
+        for (int base = 0; base < rn; base += kThreads * kIlp) {
+            float sv[kIlp];
 #pragma unroll
-                for (int q = 0; q < kIlp; ++q) {
-                    const int64_t a = base + q * kThreads + tid;
-                    sv[q] = (a < r1) ? __ldcg(&sc[a]) : 0.f;
-                }
+            for (int q = 0; q < kIlp; ++q) {
+                const int r = base + q * kThreads + tid;
+                sv[q] = (r < rn) ? (p.resident ? sS[(size_t)b * R + r] : __ldcg(&sc[r0 + r])) : 0.f;
+            }
 #pragma unroll
-                for (int q = 0; q < kIlp; ++q) {
-                    const int64_t a = base + q * kThreads + tid;
-                    const bool take = (a < r1) && (ord_of(sv[q]) >> (32 - kHistBits)) >= bs;
-                    const unsigned m = __ballot_sync(FULL, take);
-                    if (m) {
-                        const int leader = __ffs(m) - 1;
-                        uint32_t pos = 0;
-                        if (lane == leader) pos = atomicAdd(&p.cand_count[b], (uint32_t)__popc(m));
-                        pos = __shfl_sync(FULL, pos, leader);
-                        if (take)
-                            p.cand[(size_t)b * p.n_pad + pos + __popc(m & ((1u << lane) - 1u))] =
-                                kappa_of(sv[q], p.ad_begin + (uint32_t)a);
-                    }
+            for (int q = 0; q < kIlp; ++q) {
+                const int r = base + q * kThreads + tid;
+                const bool take = (r < rn) && (ord_of(sv[q]) >> (32 - kHistBits)) >= bs;
+                const unsigned m = __ballot_sync(FULL, take);
+                if (m) {
+                    const int leader = __ffs(m) - 1;
+                    uint32_t pos = 0;
+                    if (lane == leader) pos = atomicAdd(&sSeg[b], (uint32_t)__popc(m));
+                    pos = __shfl_sync(FULL, pos, leader);
+                    if (take) seg[pos + __popc(m & ((1u << lane) - 1u))] = kappa_of(sv[q], p.ad_begin + (uint32_t)(r0 + r));
                 }
             }
         }
     }
+    __syncthreads();
+    if (tid < B && has_range) p.cand_count[(size_t)tid * p.n_ranges + blockIdx.x] = sSeg[tid];
     EBR_STAMP(8);
     grid.sync();
     EBR_STAMP(9);
@@ -468,18 +491,44 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
         const int P = pow2ceil_i(p.K);
         uint64_t* sbuf = reinterpret_cast<uint64_t*>(smem);
         uint32_t* shist = reinterpret_cast<uint32_t*>(sbuf + P);
-        uint64_t* scand = reinterpret_cast<uint64_t*>(shist + 256);
-        const int64_t scap = ((int64_t)p.smem_bytes - (int64_t)P * 8 - 1024) / 8;
-        const int64_t n = (int64_t)__ldcg(&p.cand_count[b]);
+        uint32_t* sOff = shist + kSelBins;                               // [n_ranges + 1]
+        uint64_t* scand = reinterpret_cast<uint64_t*>(sOff + ((p.n_ranges + 2) & ~1));
+        const int64_t scap = ((int64_t)p.smem_bytes - ((const char*)scand - (const char*)smem)) / 8;
+        // segment offsets: exclusive scan of the per-range candidate counts
+        if (warp == 0) {
+            uint32_t carry = 0;
+            for (int j0 = 0; j0 < p.n_ranges; j0 += 32) {
+                const int j = j0 + lane;
+                const uint32_t c = j < p.n_ranges ? __ldcg(&p.cand_count[(size_t)b * p.n_ranges + j]) : 0u;
+                uint32_t incl = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t t = __shfl_up_sync(FULL, incl, o);
+                    if (lane >= o) incl += t;
+                }
+                if (j < p.n_ranges) sOff[j] = carry + incl - c;
+                carry += __shfl_sync(FULL, incl, 31);
+            }
+            if (lane == 0) sOff[p.n_ranges] = carry;
+        }
+        __syncthreads();
+        const int64_t n = sOff[p.n_ranges];
         const uint64_t* cb = p.cand + (size_t)b * p.n_pad;
-        const int nsel = cta_select_topk([cb](int64_t i) { return __ldcg(&cb[i]); }, n, p.K, sbuf,
-                                         scand, scap, shist, sScalar,
+        const int nr = p.n_ranges, Rr = R;
+        auto get = [cb, sOff, nr, Rr](int64_t i) {
+            int lo = 0, hi = nr - 1;                 // segment = last j with sOff[j] <= i
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if ((int64_t)sOff[mid] <= i) lo = mid; else hi = mid - 1;
+            }
+            return __ldcg(&cb[(int64_t)lo * Rr + (i - sOff[lo])]);
+        };
+        const int nsel = cta_select_topk(get, n, p.K, sbuf, scand, scap, shist, sScalar,
                                          (p.timers && b == 0) ? p.timers + 11 : nullptr);
         cta_write_topk(sbuf, nsel, p.K, p.out_ids ? p.out_ids + (size_t)b * p.K : nullptr,
                        p.out_scores ? p.out_scores + (size_t)b * p.K : nullptr,
                        p.out_keys ? p.out_keys + (size_t)b * p.K : nullptr);
         for (int i = tid; i < kHistBins; i += kThreads) p.ghist[(size_t)b * kHistBins + i] = 0;
-        if (tid == 0) p.cand_count[b] = 0;
         __syncthreads();
     }
     if (blockIdx.x == 0 && tid == 0) { p.header[0] = p.magic; p.header[2] = 0; }
