@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
         uint64_t acc = group_exclusive_scan(loc, sScan, &tot2, gt, kWideWarps, 1);
         for (int i = i0; i < i1; ++i) { sChunkOff[i] = acc; acc += sItems[i].c1 - sItems[i].c0; }
         if (gt == 0) sChunkOff[n_items] = tot2;
-        __threadfence_block();
+        nbar_sync(1, NT);                  // the wide warps read each other's offsets next
         nbar_arrive(2, kThreads);          // publish the plan to the deep warps (barrier 2)
         EBR_STAMP(1);
     } else if (!(p.diag & 2)) {
