@@ -412,7 +412,6 @@ __device__ __forceinline__ void cta_bitonic_desc(uint64_t* sbuf, int nsel) {
     __syncthreads();
     if (P <= nt) { cta_bitonic_fast<1>(sbuf, P); return; }
     if (P <= 2 * nt) { cta_bitonic_fast<2>(sbuf, P); return; }
-    if (P <= 4 * nt) { cta_bitonic_fast<4>(sbuf, P); return; }
     for (int size = 2; size <= P; size <<= 1) {
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
             for (int i = tid; i < (P >> 1); i += nt) {

@@ -78,8 +78,9 @@ ebr_status run_small(const QueryArgs& q, int b0, int B) {
     const int n_ranges = (int)((idx->n_ads + R - 1) / R);
     const size_t plan_bytes = (size_t)B * kHistBins * 4 + (size_t)items_cap * sizeof(Item) + 8 +
                               (size_t)(items_cap + 1) * 8;
-    const size_t sel_min = (size_t)pow2ceil_i(q.k) * 8 + kSelBins * 4 + (size_t)(n_ranges + 2) * 4 +
-                           64 * 1024;   // + >= 8k staged candidates
+    // phase E: candidate staging (>= 16k keys) and the rare single-CTA fallback select
+    const size_t sel_min = std::max((size_t)(n_ranges + 2) * 4 + 128 * 1024,
+                                    (size_t)(n_ranges + 2) * 4 + (size_t)pow2ceil_i(q.k) * 8 + kSelBins * 4 + 64);
     const size_t cap = 227 * 1024;
     // keep the CTA's deep/fused scores in shared memory when they fit
     const size_t res_bytes = (size_t)B * R * 4;

@@ -427,16 +427,20 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
     grid.sync();
     EBR_STAMP(7);
 
-    // ---- D: threshold bin per user (warp b), then compaction into this CTA's segment ----
+    // ---- D: threshold bin per user, then compaction into this CTA's segment ----
+    // every CTA stages the global histograms with coalesced 16-byte loads (148 CTAs read the same
+    // 8 KB per user: uncoalesced 4-byte reads hot-spot the L2), then warp b scans user b's.
+    for (int i = tid; i < B * kHistBins / 4; i += kThreads)
+        reinterpret_cast<uint4*>(sHist)[i] = __ldcg(reinterpret_cast<const uint4*>(p.ghist) + i);
+    __syncthreads();
     if (warp < B) {
-        const uint32_t* h = p.ghist + (size_t)warp * kHistBins;
+        const uint32_t* h = sHist + (size_t)warp * kHistBins;
         constexpr int PER = kHistBins / 32;
-        uint32_t cnt[PER];
+        const int top = kHistBins - 1 - lane * PER;      // this lane scans bins top .. top-PER+1
         uint32_t local = 0;
-#pragma unroll
-        for (int j = 0; j < PER; ++j) { cnt[j] = __ldcg(&h[kHistBins - 1 - (lane * PER + j)]); local += cnt[j]; }
+#pragma unroll 8
+        for (int j = 0; j < PER; ++j) local += h[top - j];
         uint32_t incl = local;
-#pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t x = __shfl_up_sync(FULL, incl, o);
             if (lane >= o) incl += x;
@@ -444,16 +448,20 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
         uint32_t c = incl - local;
         int found = -1;
         const uint32_t K = (uint32_t)p.K;
-#pragma unroll
-        for (int j = 0; j < PER; ++j) {
-            if (found < 0 && c < K && c + cnt[j] >= K) found = kHistBins - 1 - (lane * PER + j);
-            c += cnt[j];
+        if (c < K && c + local >= K) {
+#pragma unroll 1
+            for (int j = 0; j < PER; ++j) {
+                const uint32_t cnt = h[top - j];
+                if (c + cnt >= K) { found = top - j; break; }
+                c += cnt;
+            }
         }
         const unsigned m = __ballot_sync(FULL, found >= 0);
         const int fb = __shfl_sync(FULL, found, m ? __ffs(m) - 1 : 0);
         if (lane == 0) sBinStar[warp] = m ? (uint32_t)fb : 0u;   // < K ads: all are candidates
     }
     __syncthreads();
+    EBR_STAMP(14);
     for (int b = 0; b < B; ++b) {
         const float* sc = p.scores + (size_t)b * p.n_pad;
         uint64_t* seg = p.cand + (size_t)b * p.n_pad + r0;       // this CTA's candidate segment
@@ -486,50 +494,90 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
     grid.sync();
     EBR_STAMP(9);
 
-    // ---- E: exact selection, one CTA per user; leave the workspace zeroed ----
-    for (int b = blockIdx.x; b < B; b += gridDim.x) {
-        const int P = pow2ceil_i(p.K);
-        uint64_t* sbuf = reinterpret_cast<uint64_t*>(smem);
-        uint32_t* shist = reinterpret_cast<uint32_t*>(sbuf + P);
-        uint32_t* sOff = shist + kSelBins;                               // [n_ranges + 1]
-        uint64_t* scand = reinterpret_cast<uint64_t*>(sOff + ((p.n_ranges + 2) & ~1));
-        const int64_t scap = ((int64_t)p.smem_bytes - ((const char*)scand - (const char*)smem)) / 8;
-        // segment offsets: exclusive scan of the per-range candidate counts
-        if (warp == 0) {
-            uint32_t carry = 0;
-            for (int j0 = 0; j0 < p.n_ranges; j0 += 32) {
-                const int j = j0 + lane;
+    // ---- E: exact top-K by rank, across the whole grid ----
+    // rank(x) = #{candidates > x}; kappa is unique per ad, so the ranks are a permutation and
+    // rank < K places x directly at its output position (score desc, id asc).  Every CTA stages
+    // the user's candidates in shared memory and ranks its slice, one warp per candidate.
+    {
+        uint32_t* sOff = reinterpret_cast<uint32_t*>(smem);                       // [n_ranges + 1]
+        uint64_t* sKeys = reinterpret_cast<uint64_t*>(sOff + ((p.n_ranges + 2) & ~1));
+        const int64_t kcap = ((int64_t)p.smem_bytes - ((const char*)sKeys - (const char*)smem)) / 8;
+        for (int b = 0; b < B; ++b) {
+            // segment offsets (coalesced load + block scan)
+            uint32_t tot = 0;
+            for (int j0 = 0; j0 < p.n_ranges; j0 += kThreads) {
+                const int j = j0 + tid;
                 const uint32_t c = j < p.n_ranges ? __ldcg(&p.cand_count[(size_t)b * p.n_ranges + j]) : 0u;
-                uint32_t incl = c;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t t = __shfl_up_sync(FULL, incl, o);
-                    if (lane >= o) incl += t;
+                uint32_t t2;
+                const uint32_t ex = block_exclusive_scan(c, sScan, &t2);
+                if (j < p.n_ranges) sOff[j] = tot + ex;
+                tot += t2;
+            }
+            if (tid == 0) sOff[p.n_ranges] = tot;
+            __syncthreads();
+            const int64_t n = tot;
+            const uint64_t* cb = p.cand + (size_t)b * p.n_pad;
+            const int K = p.K;
+            if (n > kcap) {
+                // rare (very dense threshold bin): one CTA selects straight from global memory
+                if ((int)blockIdx.x == b % (int)gridDim.x) {
+                    const int nr = p.n_ranges, Rr = R;
+                    const int P = pow2ceil_i(K);
+                    uint64_t* sbuf = sKeys;
+                    uint32_t* shist = reinterpret_cast<uint32_t*>(sbuf + P);
+                    auto get = [cb, sOff, nr, Rr](int64_t i) {
+                        int lo = 0, hi = nr - 1;
+                        while (lo < hi) {
+                            const int mid = (lo + hi + 1) >> 1;
+                            if ((int64_t)sOff[mid] <= i) lo = mid; else hi = mid - 1;
+                        }
+                        return __ldcg(&cb[(int64_t)lo * Rr + (i - sOff[lo])]);
+                    };
+                    const int nsel = cta_select_topk(get, n, K, sbuf, nullptr, 0, shist, sScalar);
+                    cta_write_topk(sbuf, nsel, K, p.out_ids ? p.out_ids + (size_t)b * K : nullptr,
+                                   p.out_scores ? p.out_scores + (size_t)b * K : nullptr,
+                                   p.out_keys ? p.out_keys + (size_t)b * K : nullptr);
                 }
-                if (j < p.n_ranges) sOff[j] = carry + incl - c;
-                carry += __shfl_sync(FULL, incl, 31);
+                __syncthreads();
+                continue;
             }
-            if (lane == 0) sOff[p.n_ranges] = carry;
+            // stage all candidates of user b (flattened over the segments)
+            for (int64_t i = tid; i < n; i += kThreads) {
+                int lo = 0, hi = p.n_ranges - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if ((int64_t)sOff[mid] <= i) lo = mid; else hi = mid - 1;
+                }
+                sKeys[i] = __ldcg(&cb[(int64_t)lo * R + (i - sOff[lo])]);
+            }
+            __syncthreads();
+            // rank this CTA's slice
+            const int64_t c0 = n * blockIdx.x / gridDim.x, c1 = n * (blockIdx.x + 1) / gridDim.x;
+            for (int64_t i = c0 + warp; i < c1; i += kThreads / 32) {
+                const uint64_t x = sKeys[i];
+                uint32_t greater = 0;
+                for (int64_t j = lane; j < n; j += 32) greater += (sKeys[j] > x) ? 1u : 0u;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) greater += __shfl_xor_sync(FULL, greater, o);
+                if (lane == 0 && greater < (uint32_t)K) {
+                    const size_t q = (size_t)b * K + greater;
+                    if (p.out_keys) p.out_keys[q] = x;
+                    if (p.out_ids) p.out_ids[q] = (int32_t)gid_of(x);
+                    if (p.out_scores) p.out_scores[q] = score_of(x);
+                }
+            }
+            // fewer than K candidates (K > shard size): pad with (id -1, -inf) / key 0
+            if (blockIdx.x == 0)
+                for (int64_t q = n + tid; q < K; q += kThreads) {
+                    const size_t o = (size_t)b * K + q;
+                    if (p.out_keys) p.out_keys[o] = 0ull;
+                    if (p.out_ids) p.out_ids[o] = -1;
+                    if (p.out_scores) p.out_scores[o] = __int_as_float(0xFF800000);
+                }
+            __syncthreads();
         }
-        __syncthreads();
-        const int64_t n = sOff[p.n_ranges];
-        const uint64_t* cb = p.cand + (size_t)b * p.n_pad;
-        const int nr = p.n_ranges, Rr = R;
-        auto get = [cb, sOff, nr, Rr](int64_t i) {
-            int lo = 0, hi = nr - 1;                 // segment = last j with sOff[j] <= i
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if ((int64_t)sOff[mid] <= i) lo = mid; else hi = mid - 1;
-            }
-            return __ldcg(&cb[(int64_t)lo * Rr + (i - sOff[lo])]);
-        };
-        const int nsel = cta_select_topk(get, n, p.K, sbuf, scand, scap, shist, sScalar,
-                                         (p.timers && b == 0) ? p.timers + 11 : nullptr);
-        cta_write_topk(sbuf, nsel, p.K, p.out_ids ? p.out_ids + (size_t)b * p.K : nullptr,
-                       p.out_scores ? p.out_scores + (size_t)b * p.K : nullptr,
-                       p.out_keys ? p.out_keys + (size_t)b * p.K : nullptr);
-        for (int i = tid; i < kHistBins; i += kThreads) p.ghist[(size_t)b * kHistBins + i] = 0;
-        __syncthreads();
+        // leave the histograms zeroed for the next call (all CTAs read them before sync #3)
+        for (int i = blockIdx.x * kThreads + tid; i < B * kHistBins; i += gridDim.x * kThreads) p.ghist[i] = 0;
     }
     if (blockIdx.x == 0 && tid == 0) { p.header[0] = p.magic; p.header[2] = 0; }
     EBR_STAMP(10);

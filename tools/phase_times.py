@@ -23,17 +23,19 @@ ws = ebr.new_workspace(idx, Bn, S, c.k)
 ids = torch.empty((Bn, c.k), dtype=torch.int32, device=dev)
 sc = torch.empty((Bn, c.k), dtype=torch.float32, device=dev)
 flush = torch.ones(64 << 20, dtype=torch.float32, device=dev)   # 256 MiB, read to flush L2 clean
-names = ["start", "plan", "wide_done", "deep_done", "B_end", "sync1", "fuse_end", "sync2", "compact_end", "sync3", "select_end", "sel_staged", "sel_radix", "sel_sorted"]
+names = ["start", "plan", "wide_done", "deep_done", "B_end", "sync1", "fuse_end", "sync2", "compact_end", "sync3", "select_end", "sel_staged", "sel_radix", "sel_sorted", "thresh_done"]
 acc = []
 for it in range(30):
-    flush.sum()
+    if not os.environ.get("NOFLUSH"):
+        flush.sum()
     torch.cuda.synchronize()
     ebr.score_topk(idx, emb, feat, x, c.k, ids, sc, ws)
     torch.cuda.synchronize()
-    t = ws[16:16 + 14 * 8].cpu().numpy().view(np.uint64).astype(np.float64)
+    t = ws[16:16 + 15 * 8].cpu().numpy().view(np.uint64).astype(np.float64)
     acc.append((t - t[0]) / 1e3)
 a = np.median(np.array(acc[5:]), axis=0)
-print("candidates (C2 user 0):", None)
+cc = ws[65792:65792 + 4 * 149].cpu().numpy().view(np.uint32)
+print("candidates user 0:", int(cc[:148].sum()), "max per CTA", int(cc[:148].max()))
 for n, v in zip(names, a):
     print(f"{n:12s} {v:8.2f} us")
 print("stats", idx.stats())
