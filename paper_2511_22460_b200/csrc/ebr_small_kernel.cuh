@@ -264,6 +264,56 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
                     u[b][v][e] = (b < B && j < p.d) ? V::elem(p.U, (int64_t)b * p.d + j) : 0.f;
                 }
         const char* Abase = reinterpret_cast<const char*>(p.A);
+        if constexpr (NB == 1 && VPL == 1 && LPR >= 4 && LPR <= 16) {
+            // 16 consecutive rows per lane group, 16 loads in flight per lane; transposed
+            // reduction: log2(LPR) butterfly steps each halving the live partials, so lane li ends
+            // with the sums of rows li*(16/LPR) .. +16/LPR-1 (15 shuffles per 16 rows for LPR=16)
+            constexpr int U = 16;
+            constexpr int OUT = U / LPR;
+            constexpr int64_t wrows = (int64_t)rpw * U;                  // rows per warp iteration
+            for (int64_t base = r0 + (int64_t)warp * wrows; base < r1; base += (int64_t)kDeepWarps * wrows) {
+                const int64_t g0 = base + (int64_t)sub * U;              // this lane group's first row
+                uint4 av[U];
+#pragma unroll
+                for (int q = 0; q < U; ++q)
+                    av[q] = (g0 + q < r1) ? ldg_stream(Abase + (g0 + q) * p.row_bytes + (int64_t)li * 16)
+                                          : make_uint4(0, 0, 0, 0);
+                float v[U];
+#pragma unroll
+                for (int q = 0; q < U; ++q) {
+                    float a[E];
+                    V::unpack(av[q], a);
+                    float acc = 0.f;
+#pragma unroll
+                    for (int e = 0; e < E; ++e) acc = fmaf(a[e], u[0][0][e], acc);
+                    v[q] = acc;
+                }
+                int live = U;
+#pragma unroll
+                for (int sft = LPR / 2; sft > 0; sft >>= 1) {
+                    const bool up = (li & sft) != 0;
+                    const int half = live / 2;
+#pragma unroll
+                    for (int j = 0; j < U / 2; ++j) {
+                        if (j < half) {
+                            const float send = up ? v[j] : v[j + half];
+                            const float keep = up ? v[j + half] : v[j];
+                            v[j] = keep + __shfl_xor_sync(FULL, send, sft);
+                        }
+                    }
+                    live = half;
+                }
+                const int64_t row0 = g0 + (int64_t)li * OUT;
+#pragma unroll
+                for (int j = 0; j < OUT; ++j) {
+                    const int64_t row = row0 + j;
+                    if (row < r1) {
+                        if (p.resident) sS[row - r0] = v[j];
+                        else __stcg(&p.scores[row], v[j]);
+                    }
+                }
+            }
+        } else {
         constexpr int64_t step = (int64_t)kDeepWarps * rpw * kUnroll;
         for (int64_t base = r0 + (int64_t)warp * rpw; base < r1; base += step) {
             uint4 av[kUnroll][VPL];
@@ -307,6 +357,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
                         }
                 }
             }
+        }
         }
         EBR_STAMP(3);
     }
