@@ -202,35 +202,69 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
         const int nslot = B * p.n_fields * p.slots;
         const int per = (nslot + NT - 1) / NT;
         const int s0 = min(nslot, gt * per), s1 = min(nslot, s0 + per);
+        // one pass over the slots: build each slot's item in registers (up to kPlanCache per
+        // thread), then scan the counts and store (the loads are the plan's whole cost)
+        constexpr int kPlanCache = 8;
+        Item cache[kPlanCache];
         uint32_t cnt = 0;
-        for (int i = s0; i < s1; ++i) {
-            const int f = (i / p.slots) % p.n_fields;
-            const int32_t v = p.user_feat[i];
-            if (v >= p.field_card[f]) {
-                if (blockIdx.x == 0) atomicOr(&p.header[1], 1u);   // bounds error: skip the slot
-                continue;
-            }
-            if (v < 0) continue;
-            const uint32_t key = (uint32_t)(p.field_base[f] + v);
-            if (__ldg(&p.key_chunk_off[key + 1]) > __ldg(&p.key_chunk_off[key])) ++cnt;
-        }
         uint32_t total;
-        uint32_t pos = group_exclusive_scan(cnt, sScan, &total, gt, kWideWarps, 1);
-        for (int i = s0; i < s1; ++i) {
-            const int b = i / (p.n_fields * p.slots);
-            const int f = (i / p.slots) % p.n_fields;
-            const int32_t v = p.user_feat[i];
-            if (v < 0 || v >= p.field_card[f]) continue;
-            const uint32_t key = (uint32_t)(p.field_base[f] + v);
-            Item it;
-            it.c0 = __ldg(&p.key_chunk_off[key]);
-            it.c1 = __ldg(&p.key_chunk_off[key + 1]);
-            if (it.c1 <= it.c0) continue;
-            it.key = key;
-            it.b = (uint32_t)b;
-            it.kwb = __ldg(&p.key_word_off[key]);
-            it.w = __fmul_rn(__ldg(&p.cross_w[key]), p.user_x[i]);   // w~ = fl32(w x), never an FMA (R10)
-            sItems[pos++] = it;
+        if (per <= kPlanCache) {
+#pragma unroll
+            for (int j = 0; j < kPlanCache; ++j) {
+                cache[j].c1 = 0; cache[j].c0 = 0;
+                const int i = s0 + j;
+                if (i >= s1) continue;
+                const int b = i / (p.n_fields * p.slots);
+                const int f = (i / p.slots) % p.n_fields;
+                const int32_t v = p.user_feat[i];
+                if (v >= p.field_card[f]) {
+                    if (blockIdx.x == 0) atomicOr(&p.header[1], 1u);   // bounds error: skip the slot
+                    continue;
+                }
+                if (v < 0) continue;
+                const uint32_t key = (uint32_t)(p.field_base[f] + v);
+                cache[j].key = key;
+                cache[j].b = (uint32_t)b;
+                cache[j].c0 = __ldg(&p.key_chunk_off[key]);
+                cache[j].c1 = __ldg(&p.key_chunk_off[key + 1]);
+                cache[j].kwb = __ldg(&p.key_word_off[key]);
+                cache[j].w = __fmul_rn(__ldg(&p.cross_w[key]), p.user_x[i]);   // w~ = fl32(w x), never an FMA (R10)
+            }
+#pragma unroll
+            for (int j = 0; j < kPlanCache; ++j) cnt += cache[j].c1 > cache[j].c0 ? 1u : 0u;
+            uint32_t pos = group_exclusive_scan(cnt, sScan, &total, gt, kWideWarps, 1);
+#pragma unroll
+            for (int j = 0; j < kPlanCache; ++j)
+                if (cache[j].c1 > cache[j].c0) sItems[pos++] = cache[j];
+        } else {
+            for (int i = s0; i < s1; ++i) {
+                const int f = (i / p.slots) % p.n_fields;
+                const int32_t v = p.user_feat[i];
+                if (v >= p.field_card[f]) {
+                    if (blockIdx.x == 0) atomicOr(&p.header[1], 1u);
+                    continue;
+                }
+                if (v < 0) continue;
+                const uint32_t key = (uint32_t)(p.field_base[f] + v);
+                if (__ldg(&p.key_chunk_off[key + 1]) > __ldg(&p.key_chunk_off[key])) ++cnt;
+            }
+            uint32_t pos = group_exclusive_scan(cnt, sScan, &total, gt, kWideWarps, 1);
+            for (int i = s0; i < s1; ++i) {
+                const int b = i / (p.n_fields * p.slots);
+                const int f = (i / p.slots) % p.n_fields;
+                const int32_t v = p.user_feat[i];
+                if (v < 0 || v >= p.field_card[f]) continue;
+                const uint32_t key = (uint32_t)(p.field_base[f] + v);
+                Item it;
+                it.c0 = __ldg(&p.key_chunk_off[key]);
+                it.c1 = __ldg(&p.key_chunk_off[key + 1]);
+                if (it.c1 <= it.c0) continue;
+                it.key = key;
+                it.b = (uint32_t)b;
+                it.kwb = __ldg(&p.key_word_off[key]);
+                it.w = __fmul_rn(__ldg(&p.cross_w[key]), p.user_x[i]);
+                sItems[pos++] = it;
+            }
         }
         if (gt == 0) sNItems = total;
         nbar_sync(1, NT);
@@ -364,36 +398,42 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
     if (warp < kDeepWarps) nbar_sync(2, kThreads);   // deep warps wait for the plan before helping
     {
         // ---- B (wide): 16-chunk units of the flat chunk space from a global queue ----
-        // (the paper's LoadBalance, Alg. 2 l.354); units may straddle items.
+        // (the paper's LoadBalance, Alg. 2 l.354); units may straddle items.  Software-pipelined:
+        // the next unit is claimed and its headers fetched while this unit's payload is in flight.
         const int n_items = (int)sNItems;
         const uint64_t Ttot = sChunkOff[n_items];
         const uint64_t n_units = (p.diag & 1) ? 0 : (Ttot + kUnit - 1) / kUnit;
-        while (true) {
+        struct UnitHdr { uint2 h; uint32_t kwb, b; float w; };
+        auto claim = [&]() -> uint32_t {
             uint32_t unit = 0;
             if (lane == 0) unit = atomicAdd(&p.header[2], 1u);
-            unit = __shfl_sync(FULL, unit, 0);
-            if (unit >= n_units) break;
+            return __shfl_sync(FULL, unit, 0);
+        };
+        auto fetch = [&](uint32_t unit) -> UnitHdr {
+            UnitHdr r{make_uint2(0u, 0u), 0u, 0u, 0.f};
             const uint64_t f = (uint64_t)unit * kUnit + (lane & (kUnit - 1));
-            uint2 h = make_uint2(0u, 0u);
-            uint32_t kwb = 0, dst_b = 0;
-            float w = 0.f;
-            if ((lane < kUnit) && f < Ttot) {
+            if (unit < n_units && lane < kUnit && f < Ttot) {
                 int lo = 0, hi = n_items - 1;     // item = last it with sChunkOff[it] <= f
                 while (lo < hi) {
                     const int mid = (lo + hi + 1) >> 1;
                     if (sChunkOff[mid] <= f) lo = mid; else hi = mid - 1;
                 }
                 const Item t = sItems[lo];
-                h = __ldg(&p.hdr[t.c0 + (uint32_t)(f - sChunkOff[lo])]);
-                kwb = t.kwb;
-                dst_b = t.b;
-                w = t.w;
+                r.h = __ldg(&p.hdr[t.c0 + (uint32_t)(f - sChunkOff[lo])]);
+                r.kwb = t.kwb;
+                r.b = t.b;
+                r.w = t.w;
             }
+            return r;
+        };
+        uint32_t unit = claim();
+        UnitHdr cur = fetch(unit);
+        while (unit < n_units) {
             uint32_t lo_w[kUnit], hi_w[kUnit];
 #pragma unroll
             for (int q = 0; q < kUnit; ++q) {
-                const uint32_t meta = __shfl_sync(FULL, h.y, q);
-                const uint32_t kb = __shfl_sync(FULL, kwb, q);
+                const uint32_t meta = __shfl_sync(FULL, cur.h.y, q);
+                const uint32_t kb = __shfl_sync(FULL, cur.kwb, q);
                 lo_w[q] = 0u;
                 hi_w[q] = 0u;
                 const uint32_t n = (meta & 31u) + 1u, bw = (meta >> 5) & 31u;
@@ -404,14 +444,16 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
                     hi_w[q] = __ldg(&p.payload[wi + 1]);
                 }
             }
+            const uint32_t nxt = claim();
+            const UnitHdr nh = fetch(nxt);
             const uint32_t nval = (uint32_t)min((uint64_t)kUnit, Ttot - (uint64_t)unit * kUnit);
 #pragma unroll
             for (int q = 0; q < kUnit; ++q) {
                 if ((uint32_t)q >= nval) break;
-                const uint32_t meta = __shfl_sync(FULL, h.y, q);
-                const uint32_t first = __shfl_sync(FULL, h.x, q);
-                const uint32_t bq = __shfl_sync(FULL, dst_b, q);
-                const float wq = __shfl_sync(FULL, w, q);
+                const uint32_t meta = __shfl_sync(FULL, cur.h.y, q);
+                const uint32_t first = __shfl_sync(FULL, cur.h.x, q);
+                const uint32_t bq = __shfl_sync(FULL, cur.b, q);
+                const float wq = __shfl_sync(FULL, cur.w, q);
                 const uint32_t n = (meta & 31u) + 1u, bw = (meta >> 5) & 31u;
                 uint32_t g;
                 if (lane == 0) {
@@ -433,6 +475,8 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
                 }
                 if ((uint32_t)lane < n) atomicAdd(&p.wide[(size_t)bq * p.n_pad + g], wq);
             }
+            unit = nxt;
+            cur = nh;
         }
         EBR_STAMP(2);
     }
@@ -441,7 +485,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
     EBR_STAMP(5);
 
     // ---- C: fuse + histogram (8 independent elements in flight per thread) ----
-    constexpr int kIlp = 8;
+    constexpr int kIlp = 4;
     for (int b = 0; b < B; ++b) {
         float* sc = p.scores + (size_t)b * p.n_pad;
         float* wd = p.wide + (size_t)b * p.n_pad;
@@ -479,37 +523,29 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
     EBR_STAMP(7);
 
     // ---- D: threshold bin per user, then compaction into this CTA's segment ----
-    // every CTA stages the global histograms with coalesced 16-byte loads (148 CTAs read the same
-    // 8 KB per user: uncoalesced 4-byte reads hot-spot the L2), then warp b scans user b's.
-    for (int i = tid; i < B * kHistBins / 4; i += kThreads)
-        reinterpret_cast<uint4*>(sHist)[i] = __ldcg(reinterpret_cast<const uint4*>(p.ghist) + i);
-    __syncthreads();
-    if (warp < B) {
-        const uint32_t* h = sHist + (size_t)warp * kHistBins;
-        constexpr int PER = kHistBins / 32;
-        const int top = kHistBins - 1 - lane * PER;      // this lane scans bins top .. top-PER+1
-        uint32_t local = 0;
-#pragma unroll 8
-        for (int j = 0; j < PER; ++j) local += h[top - j];
-        uint32_t incl = local;
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t x = __shfl_up_sync(FULL, incl, o);
-            if (lane >= o) incl += x;
-        }
-        uint32_t c = incl - local;
-        int found = -1;
+    // Block-wide: thread t holds bins [2044-4t, 2048-4t) (one coalesced 16-byte load), a block
+    // scan from the top bin gives each thread the count above its bins, and the thread whose
+    // bins hold the K-th largest score publishes the bin.  (Every CTA does this for itself.)
+    static_assert(kHistBins == 4 * kThreads, "threshold scan layout");
+    for (int b = 0; b < B; ++b) {
+        const uint4 hv = __ldcg(reinterpret_cast<const uint4*>(p.ghist + (size_t)b * kHistBins) + (kThreads - 1 - tid));
+        const uint32_t sum = hv.x + hv.y + hv.z + hv.w;     // bins 4(511-t) .. +3
+        uint32_t total;
+        const uint32_t above = block_exclusive_scan(sum, sScan, &total);
         const uint32_t K = (uint32_t)p.K;
-        if (c < K && c + local >= K) {
-#pragma unroll 1
-            for (int j = 0; j < PER; ++j) {
-                const uint32_t cnt = h[top - j];
-                if (c + cnt >= K) { found = top - j; break; }
-                c += cnt;
+        if (tid == 0 && total < K) sBinStar[b] = 0u;          // fewer than K ads: all are candidates
+        if (above < K && above + sum >= K) {
+            const int b0 = 4 * (kThreads - 1 - tid);
+            uint32_t c = above;
+            const uint32_t hs[4] = {hv.w, hv.z, hv.y, hv.x};  // descending bins b0+3 .. b0
+            int found = b0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (c + hs[j] >= K) { found = b0 + 3 - j; break; }
+                c += hs[j];
             }
+            sBinStar[b] = (uint32_t)found;
         }
-        const unsigned m = __ballot_sync(FULL, found >= 0);
-        const int fb = __shfl_sync(FULL, found, m ? __ffs(m) - 1 : 0);
-        if (lane == 0) sBinStar[warp] = m ? (uint32_t)fb : 0u;   // < K ads: all are candidates
     }
     __syncthreads();
     EBR_STAMP(14);
