@@ -52,6 +52,8 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
     common = ARCH + ["-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
                      f"-DEBR_GIT=\"{_git()}\"", "-I", os.path.join(ROOT, "include"),
                      "--expt-relaxed-constexpr"]
+    if os.environ.get("EBR_DEEP_WARPS"):
+        common += [f"-DEBR_DEEP_WARPS={int(os.environ['EBR_DEEP_WARPS'])}"]
     if os.environ.get("EBR_PTXAS_V"):
         common += ["-Xptxas", "-v"]
     objs, procs = [], []

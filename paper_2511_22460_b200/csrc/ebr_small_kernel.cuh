@@ -6,12 +6,12 @@
 //               exclusive scan of the items' chunk counts gives a flat chunk space
 //               (Alg. 2 l.352-353 "k_length", "ExclusiveScan").
 //   B  two warp roles run concurrently:
-//       deep      (12 warps) A4: stream this CTA's contiguous rows of A once from HBM with 16-byte
+//       deep      (10 warps) A4: stream this CTA's contiguous rows of A once from HBM with 16-byte
 //                 non-allocating loads, 8 in flight per lane (measured: plain vector loads reach
 //                 the HBM peak, a bulk-copy ring at 1 CTA/SM does not -- tools/mb_stream.cu),
 //                 dot with the B user vectors held in registers (Eq. 1, fp32 FFMA), write the
 //                 deep score to an L2-resident scratch; then join the wide queue;
-//       wide      (4 warps) A2+A3: claim 16-chunk units of the flat chunk space from a global
+//       wide      (6 warps) A2+A3: claim 16-chunk units of the flat chunk space from a global
 //                 queue (the paper's LoadBalance, Alg. 2 l.354: every chunk but a key's
 //                 last holds 32 postings, so units cost the same), fetch the 16 headers and all
 //                 payload words in two memory round trips, unpack + warp-scan each chunk and add
@@ -43,8 +43,11 @@ namespace cg = cooperative_groups;
 namespace ebr {
 namespace small {
 
-constexpr int kDeepWarps = 12;   // stream A first, then help with the wide queue
-constexpr int kWideWarps = 4;    // wide queue from the start
+#ifndef EBR_DEEP_WARPS
+#define EBR_DEEP_WARPS 10
+#endif
+constexpr int kDeepWarps = EBR_DEEP_WARPS;      // stream A first, then help with the wide queue
+constexpr int kWideWarps = 16 - kDeepWarps;     // plan, then the wide queue from the start
 static_assert((kDeepWarps + kWideWarps) * 32 == kThreads, "CTA layout");
 constexpr int kUnroll = 8;       // 16-byte loads in flight per deep lane
 constexpr int kUnit = 16;        // chunks per wide work unit
