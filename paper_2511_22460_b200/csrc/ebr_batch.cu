@@ -1,0 +1,545 @@
+// ebr_batch.cu -- the batched path (bf16 embeddings, user batch >= 16): the deep score is a dense
+// contraction D[ads x users] = A . U^T (Eq. 1 / Eq. 8 for every (user, ad) pair) and runs on the
+// 5th-generation tensor cores: TMA loads 128-ad x 64-dim tiles (128-byte swizzle), one elected
+// thread issues tcgen05.mma (kind::f16, bf16 inputs, fp32 accumulator in TMEM, M=128, N=users),
+// four epilogue warps read the accumulator with tcgen05.ld and fuse the wide term, the score key
+// and the top-K filter.  Per group of up to 128 users, one call runs:
+//
+//   1. plan_kernel     A1 for the group: work items (key, w~, chunk span), flat chunk offsets,
+//                      and the group's user embeddings as a zero-padded bf16 tile
+//   2. wide_kernel     A2+A3: every warp decodes an equal slice of the flat chunk space and adds
+//                      w~ into W[user][ad] (fp32) with L2 reductions (Alg. 2 l.358)
+//   3. gemm_kernel<0>  A4+A5 on a strided 1/16 sample of the ad tiles: s = deep + wide, stored
+//   4. theta_kernel    A6a per user: theta_u = the K-th largest key among the sampled ads.  The
+//                      sample is a subset of the inventory, so at least K ads have key >= theta_u
+//                      and the top-K is contained in {key >= theta_u} -- exact, not heuristic.
+//   5. gemm_kernel<1>  A4+A5+A6b on every tile: s = deep + wide (W re-zeroed for the next call),
+//                      keys >= theta_u appended to the user's candidate list
+//   6. final_kernel    A6c per user: exact radix select + sort of the candidates
+//   A user whose candidate list overflowed (possible only for massively tied scores) is recomputed
+//   by the latency path after a single stream synchronisation at the end of the call.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "ebr_tc.cuh"
+
+namespace ebr {
+ebr_status run_small(const QueryArgs& q, int b0, int B);
+
+namespace batch {
+
+constexpr int kGroup = 128;          // users per group (UMMA N)
+constexpr int kTileM = 128;          // ads per tile (UMMA M)
+constexpr int kBlockK = 64;          // bf16 elements per 128-byte swizzle row
+constexpr int kSampleStride = 16;    // every 16th tile is sampled for theta
+constexpr int kGemmThreads = 256;    // warp 0 TMA, 1 MMA, 2 TMEM alloc, 4..7 epilogue
+constexpr int kAccStages = 2;
+
+struct BItem {
+    uint32_t key, c0, c1, u, kwb;
+    float w;
+};
+
+struct BatchWs {   // workspace carve-up (device pointers)
+    uint32_t* header;     // [0] n_items, [1] overflow users, [3] workspace magic
+    BItem* items;         // [cap_items]
+    uint64_t* chunk_off;  // [cap_items + 1]
+    __nv_bfloat16* U;     // [kGroup][d_pad]
+    float* W;             // [kGroup][n_pad]
+    float* samp;          // [kGroup][n_samp]
+    uint64_t* theta;      // [kGroup]
+    uint32_t* cand_count; // [kGroup]
+    uint64_t* cand;       // [kGroup][cap]
+    uint32_t* overflow;   // [kGroup]
+};
+
+// ------------------------------------------------------------------------------------------
+// 0. workspace guard: W must be zero on entry (every filter pass leaves it zeroed).  A buffer not
+//    prepared by ebr_workspace_init (no magic word) is zeroed here once; the plan kernel, which
+//    runs after this grid completes, then records the magic.
+// ------------------------------------------------------------------------------------------
+constexpr uint32_t kBatchMagic = 0xEB2B0001u;
+__global__ void guard_kernel(BatchWs ws, size_t w_words, uint32_t magic) {
+    if (__ldcg(&ws.header[3]) == magic) return;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < w_words; i += (size_t)gridDim.x * blockDim.x)
+        ws.W[i] = 0.f;
+}
+
+// ------------------------------------------------------------------------------------------
+// 1. plan (one CTA)
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(512) plan_kernel(const uint32_t* __restrict__ key_chunk_off,
+                                                   const uint32_t* __restrict__ key_word_off,
+                                                   const float* __restrict__ cross_w,
+                                                   const int32_t* __restrict__ field_card,
+                                                   const int32_t* __restrict__ field_base, int F, int S,
+                                                   const int32_t* __restrict__ user_feat,
+                                                   const float* __restrict__ user_x,
+                                                   const uint16_t* __restrict__ user_emb, int d, int d_pad,
+                                                   int nu, int nu_pad, BatchWs ws, uint32_t* err,
+                                                   uint32_t magic) {
+    __shared__ uint32_t sScan[40];
+    __shared__ uint64_t sCarry;
+    const int tid = threadIdx.x;
+    // user tile (zero padded)
+    for (int i = tid; i < nu_pad * d_pad; i += blockDim.x) {
+        const int u = i / d_pad, j = i - u * d_pad;
+        const uint16_t v = (u < nu && j < d) ? user_emb[(size_t)u * d + j] : (uint16_t)0;
+        reinterpret_cast<uint16_t*>(ws.U)[i] = v;
+    }
+    const int nslot = nu * F * S;
+    uint32_t base = 0;
+    if (tid == 0) sCarry = 0;
+    __syncthreads();
+    for (int s0 = 0; s0 < nslot; s0 += blockDim.x) {
+        const int i = s0 + tid;
+        BItem it{};
+        bool ok = false;
+        if (i < nslot) {
+            const int f = (i / S) % F;
+            const int32_t v = user_feat[i];
+            if (v >= field_card[f]) atomicOr(err, 1u);
+            else if (v >= 0) {
+                const uint32_t key = (uint32_t)(field_base[f] + v);
+                it.c0 = key_chunk_off[key];
+                it.c1 = key_chunk_off[key + 1];
+                it.key = key;
+                it.u = (uint32_t)(i / (F * S));
+                it.kwb = key_word_off[key];
+                it.w = __fmul_rn(cross_w[key], user_x[i]);   // w~ = fl32(w x), never an FMA (R10)
+                ok = it.c1 > it.c0;
+            }
+        }
+        uint32_t tot;
+        const uint32_t pos = block_exclusive_scan(ok ? 1u : 0u, sScan, &tot);
+        uint32_t ctot;
+        const uint32_t cpre = block_exclusive_scan(ok ? it.c1 - it.c0 : 0u, sScan, &ctot);
+        if (ok) {
+            ws.items[base + pos] = it;
+            ws.chunk_off[base + pos] = sCarry + cpre;
+        }
+        __syncthreads();
+        if (tid == 0) sCarry += ctot;
+        base += tot;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        ws.header[0] = base;
+        ws.header[1] = 0;       // overflow users of this group
+        ws.header[3] = magic;   // W is known zeroed from here on
+        ws.chunk_off[base] = sCarry;
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// 2. wide: static equal slices of the flat chunk space, 16 chunks per two memory round trips
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) wide_kernel(const uint2* __restrict__ hdr, const uint32_t* __restrict__ payload,
+                                                   BatchWs ws, int64_t n_pad) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t n_items = __ldcg(&ws.header[0]);
+    if (n_items == 0) return;
+    const uint64_t T = __ldcg(&ws.chunk_off[n_items]);
+    const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x / 32);
+    const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const uint64_t f0 = T * gw / nw, f1 = T * (gw + 1) / nw;
+    if (f0 >= f1) return;
+    int lo = 0, hi = (int)n_items - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (__ldcg(&ws.chunk_off[mid]) <= f0) lo = mid; else hi = mid - 1;
+    }
+    int it = lo;
+    uint64_t f = f0;
+    uint64_t off_it = __ldcg(&ws.chunk_off[it]), off_next = __ldcg(&ws.chunk_off[it + 1]);
+    while (f < f1) {
+        while (off_next <= f) { ++it; off_it = off_next; off_next = __ldcg(&ws.chunk_off[it + 1]); }
+        const BItem t = ws.items[it];
+        const uint32_t cb = t.c0 + (uint32_t)(f - off_it);
+        uint64_t nn = f1 - f;
+        if (nn > 16) nn = 16;
+        if (off_next - f < nn) nn = off_next - f;
+        float* dst = ws.W + (size_t)t.u * n_pad;
+        const float w = t.w;
+        decode_unit16(hdr, payload, t.kwb, cb, cb + (uint32_t)nn, lane,
+                      [dst, w](uint32_t id) { atomicAdd(&dst[id], w); });
+        f += nn;
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// 3/5. tcgen05 GEMM with the fused epilogue
+// ------------------------------------------------------------------------------------------
+struct GemmParams {
+    int64_t n_ads, n_pad;
+    uint32_t ad_begin;
+    int d_pad, n_kb;       // K blocks of 64
+    int nu, nu_pad;        // users in this group (valid / padded to 32)
+    int n_tiles;           // tiles to process in this launch
+    int tile_stride;       // 1 (all tiles) or kSampleStride (sample)
+    int n_samp;            // sample buffer row length (ads)
+    int stages;
+    int64_t cap;           // candidate capacity per user
+    BatchWs ws;
+};
+
+template <int MODE>   // 0: sample (store s), 1: filter (append keys >= theta, re-zero W)
+__global__ void __launch_bounds__(kGemmThreads, 1)
+gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmU, const GemmParams p) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int a_stage_bytes = kTileM * 128 * p.n_kb;     // 128 rows x 128 B per K block
+    const int u_bytes = p.nu_pad * 128 * p.n_kb;
+    unsigned char* sU = smem;                                       // [n_kb][nu_pad rows x 128 B]
+    unsigned char* sA = smem + ((u_bytes + 1023) & ~1023);          // [stages][n_kb][128 x 128 B]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sA + (size_t)p.stages * a_stage_bytes);
+    uint64_t* full = bars;                       // [stages]
+    uint64_t* empty = bars + p.stages;           // [stages]
+    uint64_t* tfull = bars + 2 * p.stages;       // [kAccStages]
+    uint64_t* tempty = tfull + kAccStages;       // [kAccStages]
+    uint64_t* ufull = tempty + kAccStages;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ufull + 1);
+    uint64_t* sTheta = reinterpret_cast<uint64_t*>(tmem_slot + 2);  // [kGroup]
+
+    if (tid == 0) {
+        for (int s = 0; s < p.stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int s = 0; s < kAccStages; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 4); }
+        mbar_init(ufull, 1);
+        fence_mbar_init();
+    }
+    if (warp == 2) tc::tmem_alloc(tmem_slot, 256);            // 2 accumulator stages x 128 columns
+    if (MODE == 1)
+        for (int i = tid; i < p.nu_pad; i += kGemmThreads) sTheta[i] = __ldcg(&p.ws.theta[i]);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- TMA producer ----------------
+            tc::tma_prefetch(&tmA);
+            tc::tma_prefetch(&tmU);
+            mbar_arrive_expect_tx(ufull, (uint32_t)u_bytes);
+            for (int kb = 0; kb < p.n_kb; ++kb)
+                tc::tma_load_2d(sU + (size_t)kb * p.nu_pad * 128, &tmU, kb * kBlockK, 0, ufull);
+            int it = 0;
+            for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++it) {
+                const int slot = it % p.stages;
+                const uint32_t round = it / p.stages;
+                if (round > 0) mbar_wait(&empty[slot], (round - 1) & 1);
+                mbar_arrive_expect_tx(&full[slot], (uint32_t)a_stage_bytes);
+                const int row0 = t * p.tile_stride * kTileM;
+                for (int kb = 0; kb < p.n_kb; ++kb)
+                    tc::tma_load_2d(sA + (size_t)slot * a_stage_bytes + (size_t)kb * kTileM * 128, &tmA,
+                                    kb * kBlockK, row0, &full[slot]);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ---------------- MMA issuer (one thread) ----------------
+            const uint32_t idesc = tc::idesc_bf16_m128(p.nu_pad);
+            mbar_wait(ufull, 0);
+            tc::fence_after();
+            int it = 0;
+            for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++it) {
+                const int slot = it % p.stages;
+                const int acc = it % kAccStages;
+                const uint32_t around = it / kAccStages;
+                if (around > 0) mbar_wait(&tempty[acc], (around - 1) & 1);   // epilogue drained it
+                mbar_wait(&full[slot], (it / p.stages) & 1);
+                tc::fence_after();
+                const uint32_t d_tmem = tmem_base + (uint32_t)(acc * 128);
+                for (int kb = 0; kb < p.n_kb; ++kb) {
+                    const uint64_t da0 = tc::sdesc_sw128(sA + (size_t)slot * a_stage_bytes + (size_t)kb * kTileM * 128);
+                    const uint64_t db0 = tc::sdesc_sw128(sU + (size_t)kb * p.nu_pad * 128);
+#pragma unroll
+                    for (int k = 0; k < kBlockK / 16; ++k)   // +32 bytes per K step inside the swizzle row
+                        tc::umma_f16(d_tmem, da0 + (uint64_t)(k * 2), db0 + (uint64_t)(k * 2), idesc,
+                                     (kb | k) != 0);
+                }
+                tc::umma_commit(&empty[slot]);     // smem stage free once these MMAs completed
+                tc::umma_commit(&tfull[acc]);      // accumulator ready for the epilogue
+            }
+        }
+    } else if (warp >= 4) {
+        // ---------------- epilogue: TMEM -> registers, fuse, key, filter ----------------
+        const int q = warp & 3;                    // TMEM lane quadrant of this warp
+        const int row = q * 32 + lane;             // ad row inside the tile
+        int it = 0;
+        for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++it) {
+            const int acc = it % kAccStages;
+            mbar_wait(&tfull[acc], (it / kAccStages) & 1);
+            tc::fence_after();
+            const int64_t a = (int64_t)t * p.tile_stride * kTileM + row;   // shard-local ad
+            const bool valid = a < p.n_ads;
+            for (int c = 0; c < p.nu_pad; c += 32) {
+                uint32_t r[32];
+                tc::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * 128 + c), r);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const int u = c + j;
+                    float s = 0.f;
+                    bool live = valid && u < p.nu;
+                    if (live) {
+                        float* wp = p.ws.W + (size_t)u * p.n_pad + a;
+                        s = __uint_as_float(r[j]) + __ldcg(wp);
+                        if (s == 0.f) s = 0.f;                       // -0 -> +0 (R14)
+                        if (MODE == 1) __stcg(wp, 0.f);              // leave W zeroed
+                    }
+                    if (MODE == 0) {
+                        if (u < p.nu) p.ws.samp[(size_t)u * p.n_samp + (int64_t)t * kTileM + row] =
+                            valid ? s : __int_as_float(0xFF800000);
+                    } else {
+                        const uint64_t key = live ? kappa_of(s, p.ad_begin + (uint32_t)a) : 0ull;
+                        const bool take = live && key >= sTheta[u];
+                        const unsigned m = __ballot_sync(FULL, take);
+                        if (m) {
+                            const int leader = __ffs(m) - 1;
+                            uint32_t pos = 0;
+                            if (lane == leader) pos = atomicAdd(&p.ws.cand_count[u], (uint32_t)__popc(m));
+                            pos = __shfl_sync(FULL, pos, leader) + __popc(m & ((1u << lane) - 1u));
+                            if (take && pos < p.cap) p.ws.cand[(size_t)u * p.cap + pos] = key;
+                        }
+                    }
+                }
+            }
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+    }
+    __syncwarp();
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 2) tc::tmem_dealloc(tmem_base, 256);
+}
+
+// ------------------------------------------------------------------------------------------
+// 4. theta: the K-th largest key of each user's sampled ads
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(512, 1) theta_kernel(BatchWs ws, int n_samp, int K, uint32_t ad_begin, int nu) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint32_t sScalar[8];
+    const int u = blockIdx.x;
+    if (u >= nu) return;
+    const int P = pow2ceil_i(K);
+    uint64_t* sbuf = reinterpret_cast<uint64_t*>(smem);
+    uint32_t* shist = reinterpret_cast<uint32_t*>(sbuf + P);
+    const float* sp = ws.samp + (size_t)u * n_samp;
+    auto get = [sp, ad_begin](int64_t i) {
+        // sample slot i = tile (i / 128) of the sample = inventory tile (i / 128) * stride
+        const int64_t ad = (i / kTileM) * kSampleStride * kTileM + (i % kTileM);
+        return kappa_of(__ldcg(&sp[i]), ad_begin + (uint32_t)ad);
+    };
+    const int nsel = cta_select_topk(get, n_samp, K, sbuf, nullptr, 0, shist, sScalar);
+    if (threadIdx.x == 0) {
+        ws.theta[u] = (nsel >= K) ? sbuf[K - 1] : 0ull;
+        ws.cand_count[u] = 0;
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// 6. final: exact top-K of the candidates
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(512, 1) final_kernel(BatchWs ws, int64_t cap, int K, int nu, int32_t* out_ids,
+                                                       float* out_scores, uint64_t* out_keys, int64_t scap) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint32_t sScalar[8];
+    const int u = blockIdx.x;
+    if (u >= nu) return;
+    const int64_t n = __ldcg(&ws.cand_count[u]);
+    if (n > cap) {   // overflow: recomputed by the latency path
+        if (threadIdx.x == 0) { ws.overflow[u] = 1; atomicAdd(&ws.header[1], 1u); }
+        return;
+    }
+    const int P = pow2ceil_i(K);
+    uint64_t* sbuf = reinterpret_cast<uint64_t*>(smem);
+    uint32_t* shist = reinterpret_cast<uint32_t*>(sbuf + P);
+    uint64_t* scand = reinterpret_cast<uint64_t*>(shist + kSelBins);
+    const uint64_t* cb = ws.cand + (size_t)u * cap;
+    const int nsel = cta_select_topk([cb](int64_t i) { return __ldcg(&cb[i]); }, n, K, sbuf, scand, scap,
+                                     shist, sScalar);
+    cta_write_topk(sbuf, nsel, K, out_ids ? out_ids + (size_t)u * K : nullptr,
+                   out_scores ? out_scores + (size_t)u * K : nullptr, out_keys ? out_keys + (size_t)u * K : nullptr);
+}
+
+// ------------------------------------------------------------------------------------------
+// host
+// ------------------------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult qres;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &qres) == cudaSuccess &&
+            qres == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    }
+    return fn;
+}
+
+static bool encode_2d_bf16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, uint32_t box_inner,
+                           uint32_t box_rows) {
+    auto fn = get_encode();
+    if (!fn) return false;
+    const cuuint64_t dims[2] = {inner, rows};
+    const cuuint64_t strides[1] = {inner * 2};
+    const cuuint32_t box[2] = {box_inner, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+struct Layout {
+    size_t header, items, chunk_off, U, W, samp, theta, count, cand, overflow, total;
+    int64_t cap, n_samp, cap_items;
+};
+
+static Layout layout(const ebr_index* idx, int32_t slots, int32_t k) {
+    Layout L;
+    auto al = [](size_t x) { return (x + 1023) & ~(size_t)1023; };
+    const int64_t n_tiles = idx->n_pad / kTileM;
+    L.n_samp = ((n_tiles + kSampleStride - 1) / kSampleStride) * kTileM;
+    L.cap = std::max<int64_t>((int64_t)kSampleStride * k * 8, 1 << 16);
+    L.cap_items = (int64_t)kGroup * idx->n_fields * slots;
+    size_t o = 0;
+    L.header = o;    o = al(o + 64);
+    L.items = o;     o = al(o + (size_t)L.cap_items * sizeof(BItem));
+    L.chunk_off = o; o = al(o + (size_t)(L.cap_items + 1) * 8);
+    L.U = o;         o = al(o + (size_t)kGroup * idx->d_pad * 2);
+    L.W = o;         o = al(o + (size_t)kGroup * idx->n_pad * 4);
+    L.samp = o;      o = al(o + (size_t)kGroup * L.n_samp * 4);
+    L.theta = o;     o = al(o + (size_t)kGroup * 8);
+    L.count = o;     o = al(o + (size_t)kGroup * 4);
+    L.cand = o;      o = al(o + (size_t)kGroup * L.cap * 8);
+    L.overflow = o;  o = al(o + (size_t)kGroup * 4);
+    L.total = o;
+    return L;
+}
+
+static BatchWs carve(char* base, const Layout& L) {
+    BatchWs w;
+    w.header = reinterpret_cast<uint32_t*>(base + L.header);
+    w.items = reinterpret_cast<BItem*>(base + L.items);
+    w.chunk_off = reinterpret_cast<uint64_t*>(base + L.chunk_off);
+    w.U = reinterpret_cast<__nv_bfloat16*>(base + L.U);
+    w.W = reinterpret_cast<float*>(base + L.W);
+    w.samp = reinterpret_cast<float*>(base + L.samp);
+    w.theta = reinterpret_cast<uint64_t*>(base + L.theta);
+    w.cand_count = reinterpret_cast<uint32_t*>(base + L.count);
+    w.cand = reinterpret_cast<uint64_t*>(base + L.cand);
+    w.overflow = reinterpret_cast<uint32_t*>(base + L.overflow);
+    return w;
+}
+
+}  // namespace batch
+
+using namespace batch;
+
+bool batch_eligible(const ebr_index* idx, int32_t batch, int32_t k) {
+    if (getenv("EBR_NO_BATCH_PATH")) return false;
+    return idx->dtype == EBR_BF16 && batch >= 16 && idx->d_pad <= 256 &&
+           idx->n_ads >= (int64_t)4 * kSampleStride * std::max(k, kTileM) && get_encode() != nullptr;
+}
+
+size_t batch_workspace_bytes(const ebr_index* idx, int32_t slots, int32_t k) {
+    return layout(idx, slots, k).total + 1024;
+}
+
+// The workspace passed here is the batched region (after the latency path's region).
+ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
+    const ebr_index* idx = q.idx;
+    const Layout L = layout(idx, q.slots, q.k);
+    char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(region) + 1023) & ~(uintptr_t)1023);
+    BatchWs ws = carve(base, L);
+    const int n_kb = idx->d_pad / kBlockK;
+    const int stages = n_kb <= 2 ? 4 : 2;
+    const int n_tiles = (int)(idx->n_pad / kTileM);
+    const int n_samp_tiles = (int)(L.n_samp / kTileM);
+    const size_t w_words = (size_t)kGroup * idx->n_pad;
+    const uint32_t magic = kBatchMagic ^ (uint32_t)((uint64_t)idx->n_pad * 2654435761ull);
+    cudaError_t e = cudaMemsetAsync(ws.overflow, 0, (size_t)kGroup * 4, q.stream);
+    if (e != cudaSuccess) return cuda_check(e, "memset(overflow)");
+    guard_kernel<<<idx->sm_count * 2, 512, 0, q.stream>>>(ws, w_words, magic);
+    CUtensorMap tmA;
+    if (!encode_2d_bf16(&tmA, idx->A, (uint64_t)idx->d_pad, (uint64_t)idx->n_pad, kBlockK, kTileM))
+        return set_error(EBR_ECUDA, "cuTensorMapEncodeTiled(A) failed");
+    std::vector<int> overflow_users;
+    // test hook: a smaller candidate capacity exercises the overflow -> latency-path fallback
+    int64_t cap = L.cap;
+    if (const char* c = getenv("EBR_TEST_CAND_CAP")) cap = std::min<int64_t>(cap, std::max(1, atoi(c)));
+    for (int g0 = 0; g0 < q.batch; g0 += kGroup) {
+        const int nu = std::min(kGroup, q.batch - g0);
+        const int nu_pad = (nu + 31) & ~31;
+        CUtensorMap tmU;
+        if (!encode_2d_bf16(&tmU, ws.U, (uint64_t)idx->d_pad, (uint64_t)nu_pad, kBlockK, (uint32_t)nu_pad))
+            return set_error(EBR_ECUDA, "cuTensorMapEncodeTiled(U) failed");
+        plan_kernel<<<1, 512, 0, q.stream>>>(idx->key_chunk_off, idx->key_word_off, idx->cross_w, idx->field_card,
+                                             idx->field_base, idx->n_fields, q.slots,
+                                             q.user_feat + (size_t)g0 * idx->n_fields * q.slots,
+                                             q.user_x + (size_t)g0 * idx->n_fields * q.slots,
+                                             reinterpret_cast<const uint16_t*>(q.user_emb) + (size_t)g0 * idx->d,
+                                             idx->d, idx->d_pad, nu, nu_pad, ws, err_word, magic);
+        wide_kernel<<<idx->sm_count * 4, 256, 0, q.stream>>>(idx->chunk_hdr, idx->payload, ws, idx->n_pad);
+        GemmParams gp;
+        gp.n_ads = idx->n_ads; gp.n_pad = idx->n_pad; gp.ad_begin = (uint32_t)idx->ad_begin;
+        gp.d_pad = idx->d_pad; gp.n_kb = n_kb; gp.nu = nu; gp.nu_pad = nu_pad;
+        gp.n_samp = (int)L.n_samp; gp.stages = stages; gp.cap = cap; gp.ws = ws;
+        const size_t smem = 1024 + (((size_t)nu_pad * 128 * n_kb + 1023) & ~(size_t)1023) +
+                            (size_t)stages * kTileM * 128 * n_kb + 256 + (size_t)kGroup * 8;
+        // sample pass
+        gp.n_tiles = n_samp_tiles; gp.tile_stride = kSampleStride;
+        e = cudaFuncSetAttribute(gemm_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return cuda_check(e, "attr(gemm0)");
+        gemm_kernel<0><<<std::min(idx->sm_count, n_samp_tiles), kGemmThreads, smem, q.stream>>>(tmA, tmU, gp);
+        // theta
+        const size_t tsmem = (size_t)pow2ceil_i(q.k) * 8 + kSelBins * 4 + 64;
+        e = cudaFuncSetAttribute(theta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
+        if (e != cudaSuccess) return cuda_check(e, "attr(theta)");
+        theta_kernel<<<nu, 512, tsmem, q.stream>>>(ws, (int)L.n_samp, q.k, (uint32_t)idx->ad_begin, nu);
+        // filter pass over every tile
+        gp.n_tiles = n_tiles; gp.tile_stride = 1;
+        e = cudaFuncSetAttribute(gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return cuda_check(e, "attr(gemm1)");
+        gemm_kernel<1><<<std::min(idx->sm_count, n_tiles), kGemmThreads, smem, q.stream>>>(tmA, tmU, gp);
+        // final
+        const size_t fsmem = 200 * 1024;
+        const int64_t scap = (int64_t)(fsmem - (size_t)pow2ceil_i(q.k) * 8 - kSelBins * 4) / 8;
+        e = cudaFuncSetAttribute(final_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
+        if (e != cudaSuccess) return cuda_check(e, "attr(final)");
+        final_kernel<<<nu, 512, fsmem, q.stream>>>(ws, cap, q.k, nu,
+                                                   q.out_ids ? q.out_ids + (size_t)g0 * q.k : nullptr,
+                                                   q.out_scores ? q.out_scores + (size_t)g0 * q.k : nullptr,
+                                                   q.out_keys ? q.out_keys + (size_t)g0 * q.k : nullptr, scap);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_check(e, "launch(batch)");
+        // overflowed users of this group: one sync, then the exact latency path for them
+        uint32_t hdr[2] = {0, 0};
+        e = cudaMemcpyAsync(hdr, ws.header, 8, cudaMemcpyDeviceToHost, q.stream);
+        if (e != cudaSuccess) return cuda_check(e, "memcpy(header)");
+        e = cudaStreamSynchronize(q.stream);
+        if (e != cudaSuccess) return cuda_check(e, "sync(batch)");
+        if (hdr[1]) {
+            std::vector<uint32_t> of(nu);
+            e = cudaMemcpy(of.data(), ws.overflow, (size_t)nu * 4, cudaMemcpyDeviceToHost);
+            if (e != cudaSuccess) return cuda_check(e, "memcpy(overflow)");
+            for (int u = 0; u < nu; ++u)
+                if (of[u]) overflow_users.push_back(g0 + u);
+            e = cudaMemsetAsync(ws.overflow, 0, (size_t)kGroup * 4, q.stream);
+            if (e != cudaSuccess) return cuda_check(e, "memset(overflow)");
+        }
+    }
+    for (int u : overflow_users) {
+        ebr_status st = run_small(q, u, 1);
+        if (st != EBR_OK) return st;
+    }
+    return EBR_OK;
+}
+
+}  // namespace ebr

@@ -47,6 +47,9 @@ ebr_status cuda_check(cudaError_t e, const char* what) {
 
 ebr_status run_small(const QueryArgs& q, int b0, int B);
 uint32_t workspace_magic(const ebr_index* idx);
+bool batch_eligible(const ebr_index* idx, int32_t batch, int32_t k);
+size_t batch_workspace_bytes(const ebr_index* idx, int32_t slots, int32_t k);
+ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word);
 size_t small_workspace_bytes(const ebr_index* idx, int32_t slots, int32_t k);
 
 // ------------------------------------------------------------------------------------------
@@ -262,12 +265,21 @@ ebr_status run_debug_decode(const ebr_index* idx, int64_t key, int32_t* dev_out,
     return EBR_OK;
 }
 
+static size_t small_region(const ebr_index* idx, int32_t slots, int32_t k) {
+    return (small_workspace_bytes(idx, slots, k) + 1023) & ~(size_t)1023;
+}
+
 size_t workspace_bytes(const ebr_index* idx, int32_t batch, int32_t slots, int32_t k) {
-    (void)batch;
-    return small_workspace_bytes(idx, slots, k);
+    size_t n = small_region(idx, slots, k);
+    if (batch_eligible(idx, batch, k)) n += batch_workspace_bytes(idx, slots, k);
+    return n;
 }
 
 ebr_status run_query(const QueryArgs& q) {
+    if (batch_eligible(q.idx, q.batch, q.k)) {
+        char* ws = static_cast<char*>(q.workspace);
+        return run_batch(q, ws + small_region(q.idx, q.slots, q.k), reinterpret_cast<uint32_t*>(ws) + 1);
+    }
     for (int b0 = 0; b0 < q.batch; b0 += kSmallMaxB) {
         const int B = std::min(kSmallMaxB, q.batch - b0);
         ebr_status st = run_small(q, b0, B);

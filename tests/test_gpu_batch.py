@@ -1,0 +1,87 @@
+"""GPU parity of the batched tensor-core path (bf16, batch >= 16): tcgen05 GEMM + fused epilogue,
+sampled exact threshold, candidate selection -- against the CPU oracle, and against the latency
+path on the same inputs."""
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+from paper_2511_22460_b200 import synth  # noqa: E402
+from tests.test_gpu_parity import check_all, run  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def ebr():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2511_22460_b200 import ebr as m
+    return m
+
+
+
+@pytest.mark.parametrize("cfg,n,b,k", [("C3", 60_000, 40, 100),      # one group (pad 40 -> 64)
+                                       ("C3", 45_000, 200, 64),      # two groups (128 + 72)
+                                       ("C4", 90_001, 64, 300),      # d=64, F=64, alpha=1.2
+                                       ("C5", 70_000, 16, 128)])     # smallest eligible batch
+def test_batch_exact_bit_exact(ebr, cfg, n, b, k):
+    inv, users = synth.make_config(cfg, mode="exact", n_ads=n, batch=b)
+    idx = ebr.Index.of(inv)
+    (ids, sc), ws = run(ebr, idx, users, k)
+    assert check_all(oracle.Oracle.of(inv), users, ids, sc, k, "exact") == 0
+    assert ebr.query_error(ws) == 0
+
+
+@pytest.mark.parametrize("cfg,n,b,k", [("C3", 130_000, 130, 1000), ("C4", 100_000, 64, 1000)])
+def test_batch_real_tolerance(ebr, cfg, n, b, k):
+    inv, users = synth.make_config(cfg, mode="real", n_ads=n, batch=b)
+    idx = ebr.Index.of(inv)
+    (ids, sc), _ = run(ebr, idx, users, k)
+    o = oracle.Oracle.of(inv)
+    sel = list(range(0, b, max(1, b // 12)))      # a spread of users (full check is slow on CPU)
+    sub = synth.Users(len(sel), users.slots, users.user_emb[sel], users.user_feat[sel], users.user_x[sel])
+    check_all(o, sub, ids[sel], sc[sel], k, "real")
+
+
+def test_batch_equals_latency_path(ebr):
+    inv, users = synth.make_config("C3", mode="exact", n_ads=50_000, batch=48)
+    idx = ebr.Index.of(inv)
+    (ids_b, sc_b), _ = run(ebr, idx, users, 200)
+    os.environ["EBR_NO_BATCH_PATH"] = "1"
+    try:
+        (ids_s, sc_s), _ = run(ebr, idx, users, 200)
+    finally:
+        del os.environ["EBR_NO_BATCH_PATH"]
+    assert (ids_b == ids_s).all() and (sc_b == sc_s).all()
+
+
+def test_batch_overflow_falls_back_exactly(ebr):
+    inv, users = synth.make_config("C3", mode="exact", n_ads=40_000, batch=20)
+    idx = ebr.Index.of(inv)
+    os.environ["EBR_TEST_CAND_CAP"] = "300"       # < 16 K: every user overflows
+    try:
+        (ids, sc), _ = run(ebr, idx, users, 100)
+    finally:
+        del os.environ["EBR_TEST_CAND_CAP"]
+    assert check_all(oracle.Oracle.of(inv), users, ids, sc, 100, "exact") == 0
+
+
+def test_batch_workspace_reuse_and_keys(ebr):
+    inv, users = synth.make_config("C3", mode="exact", n_ads=40_000, batch=32)
+    idx = ebr.Index.of(inv)
+    ws = ebr.new_workspace(idx, 32, users.slots, 80)
+    dev = torch.device("cuda")
+    o = oracle.Oracle.of(inv)
+    for trial in range(3):
+        u2 = synth.make_users(inv, 32, mode="exact", seed=50 + trial)
+        emb = torch.from_numpy(u2.user_emb.view(np.int16)).to(dev)
+        feat = torch.from_numpy(u2.user_feat).to(dev)
+        x = torch.from_numpy(u2.user_x).to(dev)
+        ids = torch.empty((32, 80), dtype=torch.int32, device=dev)
+        sc = torch.empty((32, 80), dtype=torch.float32, device=dev)
+        ebr.score_topk(idx, emb, feat, x, 80, ids, sc, ws)
+        torch.cuda.synchronize()
+        assert check_all(o, u2, ids.cpu().numpy(), sc.cpu().numpy(), 80, "exact") == 0
