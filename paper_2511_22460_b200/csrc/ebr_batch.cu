@@ -48,7 +48,7 @@ struct BatchWs {   // workspace carve-up (device pointers)
     BItem* items;         // [cap_items]
     uint64_t* chunk_off;  // [cap_items + 1]
     __nv_bfloat16* U;     // [kGroup][d_pad]
-    float* W;             // [n_pad][kGroup]  ad-major: an epilogue thread reads its row's users
+    float* W;             // [kGroup][n_pad]  user-major: a chunk's postings hit neighbouring words
     float* samp;          // [kGroup][n_samp]
     uint64_t* theta;      // [kGroup]
     uint32_t* cand_count; // [kGroup]
@@ -162,10 +162,10 @@ __global__ void __launch_bounds__(256) wide_kernel(const uint2* __restrict__ hdr
         uint64_t nn = f1 - f;
         if (nn > 16) nn = 16;
         if (off_next - f < nn) nn = off_next - f;
-        float* dst = ws.W + t.u;
+        float* dst = ws.W + (size_t)t.u * n_pad;
         const float w = t.w;
         decode_unit16(hdr, payload, t.kwb, cb, cb + (uint32_t)nn, lane,
-                      [dst, w](uint32_t id) { atomicAdd(&dst[(size_t)id * kGroup], w); });
+                      [dst, w](uint32_t id) { atomicAdd(&dst[id], w); });
         f += nn;
     }
 }
@@ -277,21 +277,21 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             tc::fence_after();
             const int64_t a = (int64_t)t * p.tile_stride * kTileM + row;   // shard-local ad
             const bool valid = a < p.n_ads;
-            float* wrow = p.ws.W + (size_t)(valid ? a : 0) * kGroup;
+            float* wcol = p.ws.W + (valid ? a : 0);
             for (int c = 0; c < p.nu_pad; c += 32) {
-                // this row's 32 wide scores: 8 independent 16-byte loads issued before any use
-                float4 wv[8];
+                // this row's 32 wide scores: 32 independent loads (coalesced across the warp's
+                // consecutive ads) issued before any use
+                float wf[32];
 #pragma unroll
-                for (int v = 0; v < 8; ++v)
-                    wv[v] = valid ? __ldcg(reinterpret_cast<const float4*>(wrow + c) + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int j = 0; j < 32; ++j)
+                    wf[j] = (valid && c + j < p.nu) ? __ldcg(wcol + (size_t)(c + j) * p.n_pad) : 0.f;
                 uint32_t r[32];
                 tc::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * 128 + c), r);
                 if (MODE == 1 && valid) {
 #pragma unroll
-                    for (int v = 0; v < 8; ++v)        // leave W zeroed for the next call
-                        __stcg(reinterpret_cast<float4*>(wrow + c) + v, make_float4(0.f, 0.f, 0.f, 0.f));
+                    for (int j = 0; j < 32; ++j)       // leave W zeroed for the next call
+                        if (c + j < p.nu) __stcg(wcol + (size_t)(c + j) * p.n_pad, 0.f);
                 }
-                const float* wf = reinterpret_cast<const float*>(wv);
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
                     const int u = c + j;
