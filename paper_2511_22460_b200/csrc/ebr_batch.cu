@@ -35,7 +35,8 @@ constexpr int kGroup = 128;          // users per group (UMMA N)
 constexpr int kTileM = 128;          // ads per tile (UMMA M)
 constexpr int kBlockK = 64;          // bf16 elements per 128-byte swizzle row
 constexpr int kSampleStride = 16;    // every 16th tile is sampled for theta
-constexpr int kGemmThreads = 256;    // warp 0 TMA, 1 MMA, 2 TMEM alloc, 4..7 epilogue
+constexpr int kEpiWarps = 16;        // 4 per TMEM lane quadrant, one 32-column chunk each
+constexpr int kGemmThreads = 128 + 32 * kEpiWarps;   // warp 0 TMA, 1 MMA, 2 TMEM alloc, 4.. epilogue
 constexpr int kAccStages = 2;
 
 struct BItem {
@@ -204,16 +205,20 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     uint64_t* ufull = tempty + kAccStages;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ufull + 1);
     uint64_t* sTheta = reinterpret_cast<uint64_t*>(tmem_slot + 2);  // [kGroup]
+    float* sThetaS = reinterpret_cast<float*>(sTheta + kGroup);       // score part of theta, [kGroup]
 
     if (tid == 0) {
         for (int s = 0; s < p.stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (int s = 0; s < kAccStages; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 4); }
+        for (int s = 0; s < kAccStages; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], kEpiWarps); }
         mbar_init(ufull, 1);
         fence_mbar_init();
     }
     if (warp == 2) tc::tmem_alloc(tmem_slot, 256);            // 2 accumulator stages x 128 columns
     if (MODE == 1)
-        for (int i = tid; i < p.nu_pad; i += kGemmThreads) sTheta[i] = __ldcg(&p.ws.theta[i]);
+        for (int i = tid; i < p.nu_pad; i += kGemmThreads) {
+            sTheta[i] = __ldcg(&p.ws.theta[i]);
+            sThetaS[i] = score_of(sTheta[i]);       // key >= theta implies score >= this
+        }
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
@@ -268,7 +273,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         }
     } else if (warp >= 4) {
         // ---------------- epilogue: TMEM -> registers, fuse, key, filter ----------------
+        const int e = warp - 4;
         const int q = warp & 3;                    // TMEM lane quadrant of this warp
+        const int c = (e >> 2) * 32;               // this warp's 32 accumulator columns (users)
         const int row = q * 32 + lane;             // ad row inside the tile
         int it = 0;
         for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++it) {
@@ -277,8 +284,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             tc::fence_after();
             const int64_t a = (int64_t)t * p.tile_stride * kTileM + row;   // shard-local ad
             const bool valid = a < p.n_ads;
-            float* wcol = p.ws.W + (valid ? a : 0);
-            for (int c = 0; c < p.nu_pad; c += 32) {
+            if (c < p.nu_pad) {
+                float* wcol = p.ws.W + (valid ? a : 0);
                 // this row's 32 wide scores: 32 independent loads (coalesced across the warp's
                 // consecutive ads) issued before any use
                 float wf[32];
@@ -302,15 +309,18 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                         if (u < p.nu) p.ws.samp[(size_t)u * p.n_samp + (int64_t)t * kTileM + row] =
                             valid ? s : __int_as_float(0xFF800000);
                     } else {
-                        const uint64_t key = live ? kappa_of(s, p.ad_begin + (uint32_t)a) : 0ull;
-                        const bool take = live && key >= sTheta[u];
-                        const unsigned m = __ballot_sync(FULL, take);
-                        if (m) {
-                            const int leader = __ffs(m) - 1;
-                            uint32_t pos = 0;
-                            if (lane == leader) pos = atomicAdd(&p.ws.cand_count[u], (uint32_t)__popc(m));
-                            pos = __shfl_sync(FULL, pos, leader) + __popc(m & ((1u << lane) - 1u));
-                            if (take && pos < p.cap) p.ws.cand[(size_t)u * p.cap + pos] = key;
+                        const bool maybe = live && s >= sThetaS[u];   // cheap pre-filter
+                        if (__any_sync(FULL, maybe)) {
+                            const uint64_t key = maybe ? kappa_of(s, p.ad_begin + (uint32_t)a) : 0ull;
+                            const bool take = maybe && key >= sTheta[u];
+                            const unsigned m = __ballot_sync(FULL, take);
+                            if (m) {
+                                const int leader = __ffs(m) - 1;
+                                uint32_t pos = 0;
+                                if (lane == leader) pos = atomicAdd(&p.ws.cand_count[u], (uint32_t)__popc(m));
+                                pos = __shfl_sync(FULL, pos, leader) + __popc(m & ((1u << lane) - 1u));
+                                if (take && pos < p.cap) p.ws.cand[(size_t)u * p.cap + pos] = key;
+                            }
                         }
                     }
                 }
@@ -499,7 +509,7 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
         gp.d_pad = idx->d_pad; gp.n_kb = n_kb; gp.nu = nu; gp.nu_pad = nu_pad;
         gp.n_samp = (int)L.n_samp; gp.stages = stages; gp.cap = cap; gp.ws = ws;
         const size_t smem = 1024 + (((size_t)nu_pad * 128 * n_kb + 1023) & ~(size_t)1023) +
-                            (size_t)stages * kTileM * 128 * n_kb + 256 + (size_t)kGroup * 8;
+                            (size_t)stages * kTileM * 128 * n_kb + 256 + (size_t)kGroup * 12;
         // sample pass
         gp.n_tiles = n_samp_tiles; gp.tile_stride = kSampleStride;
         e = cudaFuncSetAttribute(gemm_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
