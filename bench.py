@@ -238,9 +238,10 @@ def main():
     K = args.k or cfg.k
     inv, users = synth.make_config(cfg, mode=args.mode, batch=B)
     N = inv.n_ads
-    Ns = ((N + world - 1) // world + 127) // 128 * 128
-    lo, hi = min(N, rank * Ns), min(N, (rank + 1) * Ns)
-    idx = ebr.Index.of(inv, lo=lo, hi=hi, device=local)
+    from paper_2511_22460_b200.dist import ShardedIndex
+    shard = ShardedIndex(inv, rank, world, device=local)
+    idx = shard.index
+    lo, hi = shard.lo, shard.hi
     st = idx.stats()
     stream = torch.cuda.Stream(device=dev)
     emb_np = users.user_emb
@@ -248,7 +249,7 @@ def main():
     feat = torch.from_numpy(users.user_feat).to(dev)
     x = torch.from_numpy(users.user_x).to(dev)
     S = users.slots
-    ws = ebr.new_workspace(idx, B, S, K)
+    ws = shard.workspace(B, S, K)
     ids = torch.empty((B, K), dtype=torch.int32, device=dev)
     sc = torch.empty((B, K), dtype=torch.float32, device=dev)
     keys = torch.empty((B, K), dtype=torch.int64, device=dev)
@@ -257,13 +258,7 @@ def main():
     flush_out = torch.empty((), dtype=torch.float32, device=dev)
 
     def step():
-        if world == 1:
-            ebr.score_topk(idx, emb, feat, x, K, ids, sc, ws, stream)
-        else:
-            ebr.score_topk_keys(idx, emb, feat, x, K, keys, ws, stream)
-            with torch.cuda.stream(stream):
-                dist.all_gather_into_tensor(gathered, keys)
-            ebr.merge_topk(gathered, world, B, K, ids, sc, stream)
+        shard.query(emb, feat, x, K, ids, sc, stream, local_keys=keys, gathered=gathered)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -329,34 +324,55 @@ def main():
             "index": {"build_ms": st["build_ms"], "index_bytes": st["index_bytes"],
                       "nnz": st["nnz"], "chunks": st["chunks"]},
             "clocks": clk.summary(),
-            "gpu_launches": args.steps * ((B + 7) // 8 + (1 if world > 1 else 0)),
+            "gpu_launches": args.steps * (idx.query_launches(B, S, K) + (1 if world > 1 else 0)),
             "wall_s_timed_region": wall,
         }
-    # e2e through the host-buffer C-ABI call (pinned host memory, copies inside the region)
-    if world == 1 and not args.profile:
-        wsh = ebr.new_workspace(idx, B, S, K, host=True)
-        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
+    # e2e through the public API with HOST buffers: N=1 -> the C-ABI host call (H2D, query, D2H,
+    # sync inside the library); N>1 -> pinned H2D + sharded query (+ all-gather + merge) + D2H
+    if not args.profile:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
         h_emb = pin(emb_np.view(np.int16) if emb_np.dtype == np.uint16 else emb_np)
         h_feat, h_x = pin(users.user_feat), pin(users.user_x)
-        h_ids = torch.empty((B, K), dtype=torch.int32).pin_memory().numpy()
-        h_sc = torch.empty((B, K), dtype=torch.float32).pin_memory().numpy()
+        h_ids = torch.empty((B, K), dtype=torch.int32).pin_memory()
+        h_sc = torch.empty((B, K), dtype=torch.float32).pin_memory()
+        if world == 1:
+            wsh = ebr.new_workspace(idx, B, S, K, host=True)
+            n_h = [h_emb.numpy(), h_feat.numpy(), h_x.numpy(), h_ids.numpy(), h_sc.numpy()]
+            run_e2e = lambda: ebr.score_topk_host(idx, n_h[0], n_h[1], n_h[2], K, n_h[3], n_h[4], wsh, stream)  # noqa: E731
+            timing = "host wall clock around ebr_score_topk_host (H2D + query + D2H + sync)"
+        else:
+            def run_e2e():
+                with torch.cuda.stream(stream):
+                    emb.copy_(h_emb, non_blocking=True)
+                    feat.copy_(h_feat, non_blocking=True)
+                    x.copy_(h_x, non_blocking=True)
+                step()
+                with torch.cuda.stream(stream):
+                    h_ids.copy_(ids, non_blocking=True)
+                    h_sc.copy_(sc, non_blocking=True)
+                stream.synchronize()
+            timing = "host wall clock: pinned H2D + sharded query + all-gather + merge + D2H + sync"
         for _ in range(3):
-            ebr.score_topk_host(idx, h_emb, h_feat, h_x, K, h_ids, h_sc, wsh, stream)
+            run_e2e()
         e_ms = []
-        for i in range(args.steps):
+        n_e2e = min(args.steps, 500)
+        for i in range(n_e2e):
             with torch.cuda.stream(stream):
                 torch.sum(flush, dim=0, out=flush_out)
             stream.synchronize()
+            if world > 1:
+                dist.barrier()
             t = time.perf_counter()
-            ebr.score_topk_host(idx, h_emb, h_feat, h_x, K, h_ids, h_sc, wsh, stream)
+            run_e2e()
             e_ms.append((time.perf_counter() - t) * 1e3)
-        e_ms = np.array(e_ms)
+        e_arr = torch.tensor([float(np.mean(e_ms))], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e_arr, op=dist.ReduceOp.MAX)
         if line is not None:
-            line["e2e"] = {"value": B / (e_ms.mean() / 1e3), "unit": "users/s",
+            line["e2e"] = {"value": B / (float(e_arr.item()) / 1e3), "unit": "users/s",
                            "h2d_bytes_per_step": int(h_emb.nbytes + h_feat.nbytes + h_x.nbytes),
                            "d2h_bytes_per_step": int(h_ids.nbytes + h_sc.nbytes),
-                           "p50_us": float(np.percentile(e_ms, 50) * 1e3),
-                           "timing": "host wall clock around ebr_score_topk_host (H2D + query + D2H + sync)"}
+                           "p50_us": float(np.percentile(e_ms, 50) * 1e3), "timing": timing}
     if rank == 0 and not args.no_cpu_baseline and not args.profile:
         line["cpu_baseline"] = cpu_baseline(cfg, inv, users, K)
     if rank == 0:

@@ -45,6 +45,7 @@ EXPORTS = {
     "ebr_index_stats": (ctypes.c_int, [_P, _P]),
     "ebr_encode_host": (ctypes.c_int, [_P, _I64, _I32, _P, _I64, _P, _P, _P, _I64, _P, _I64,
                                        ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
+    "ebr_query_launches": (_I32, [_P, _I32, _I32, _I32]),
     "ebr_last_error": (ctypes.c_char_p, []),
     "ebr_version": (ctypes.c_char_p, []),
 }
@@ -161,6 +162,9 @@ class Index:
         if n == 0:
             raise EbrError(1, "ebr_workspace_bytes_host")
         return int(n)
+
+    def query_launches(self, batch: int, slots: int, k: int) -> int:
+        return int(_lib.ebr_query_launches(self._h, batch, slots, k))
 
     def debug_decode(self, key: int) -> np.ndarray:
         n = _I64()
