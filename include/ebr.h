@@ -62,7 +62,7 @@ typedef enum { EBR_F32 = 0, EBR_BF16 = 1 } ebr_dtype;
  *             already concatenated; reading R19).  Rows are zero-padded on the device to the
  *             kernel width (exact).
  *  ad_feat    host, [n][n_fields] int32, the ad's value v in field f, -1 = empty (L_{a,i}=0).
- *             Defines L: L[a, base_f + v] = 1 (reading A1).  Must be in [-1, V_f).
+ *             Defines L: L[a, base_f + v] = 1 (reading R1).  Must be in [-1, V_f).
  *  field_card host, [n_fields] int32 V_f >= 1; key i = base_f + v with base_f = sum_{g<f} V_g.
  *  cross_w    host, [n_keys] fp32, the learned weight w_i of every key (Eq. 9).
  *  n_keys     must equal sum V_f and be < 2^31.
@@ -116,7 +116,7 @@ size_t ebr_workspace_bytes(const ebr_index *idx, int32_t batch, int32_t slots, i
  *             ebr_workspace_init(); every call then leaves it ready for the next, so each query
  *             is a single kernel launch.  Do not modify it between calls.
  * Errors: EBR_EINVAL for batch < 1, slots out of range, k out of range, undersized workspace;
- *         EBR_ECUDA on a launch failure.  Duplicate (f,v) slots of one user add (reading A3).
+ *         EBR_ECUDA on a launch failure.  Duplicate (f,v) slots of one user add (reading R3).
  */
 ebr_status ebr_score_topk(const ebr_index *idx, const void *user_emb, int32_t batch,
                           const int32_t *user_feat, const float *user_x, int32_t slots, int32_t k,

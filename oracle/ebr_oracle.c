@@ -15,7 +15,7 @@
  *        T_u[i] = sum over the user's slots carrying key i of w_i * x_i  (w~_i = w_i x_i),
  *        and wide(u,a) = sum_f T_u[key(a,f)], i.e. sum_i T_u[i] L_{a,i} (L_{a,i}=1 iff ad a has
  *        value v in field f with i = base_f + v; "keys are the feature indices,
- *        values are the ad indices"; reading A1 in DESIGN.md).
+ *        values are the ad indices"; reading R1 in DESIGN.md).
  *      * also returns sigma(a) = sum_j |h_u[j] h_a[j]| + sum_hits |w~|, the summation-error scale
  *        the tolerances are stated against (reading R12).
  *  - oracle_wide_pairs_user (scorer B): the wide term by explicit feature-pair enumeration --

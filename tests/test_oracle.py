@@ -200,7 +200,7 @@ def test_wide_linearity_and_conservation():
 
 
 def test_duplicate_slot_is_additive():
-    # Reading A3: the same (f, v) twice in one user adds.
+    # Reading R3: the same (f, v) twice in one user adds.
     feat = np.array([[0], [1]], np.int32)
     o = oracle.Oracle(_zero_emb(2), feat, [2], [1.0, 10.0])
     uf = np.array([[0, 0]], np.int32)
