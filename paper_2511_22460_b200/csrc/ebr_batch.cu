@@ -7,13 +7,14 @@
 //
 //   1. plan_kernel     A1 for the group: work items (key, w~, chunk span), flat chunk offsets,
 //                      and the group's user embeddings as a zero-padded bf16 tile
-//   2. wide_kernel     A2+A3: every warp decodes an equal slice of the flat chunk space and adds
-//                      w~ into W[user][ad] (fp32) with L2 reductions (Alg. 2 l.358)
+//   2. span_kernel     for every item and 16k-ad chunk, where the item's postings enter the chunk
+//      wide_smem_kernel A2+A3: CTA (ad chunk, user) decodes the user's postings in its chunk and
+//                      accumulates w~ in shared memory (Alg. 2 l.358), then writes W[user][ad]
 //   3. gemm_kernel<0>  A4+A5 on a strided 1/16 sample of the ad tiles: s = deep + wide, stored
 //   4. theta_kernel    A6a per user: theta_u = the K-th largest key among the sampled ads.  The
 //                      sample is a subset of the inventory, so at least K ads have key >= theta_u
 //                      and the top-K is contained in {key >= theta_u} -- exact, not heuristic.
-//   5. gemm_kernel<1>  A4+A5+A6b on every tile: s = deep + wide (W re-zeroed for the next call),
+//   5. gemm_kernel<1>  A4+A5+A6b on every tile: s = deep + wide,
 //                      keys >= theta_u appended to the user's candidate list
 //   6. final_kernel    A6c per user: exact radix select + sort of the candidates
 //   A user whose candidate list overflowed (possible only for massively tied scores) is recomputed
@@ -55,19 +56,11 @@ struct BatchWs {   // workspace carve-up (device pointers)
     uint32_t* cand_count; // [kGroup]
     uint64_t* cand;       // [kGroup][cap]
     uint32_t* overflow;   // [kGroup]
+    uint32_t* user_item;  // [kGroup + 1]  items of group user u: [user_item[u], user_item[u+1])
+    uint32_t* span;       // [cap_items][n_chunks_R + 1] first chunk of the item with first id >= j*R
 };
 
-// ------------------------------------------------------------------------------------------
-// 0. workspace guard: W must be zero on entry (every filter pass leaves it zeroed).  A buffer not
-//    prepared by ebr_workspace_init (no magic word) is zeroed here once; the plan kernel, which
-//    runs after this grid completes, then records the magic.
-// ------------------------------------------------------------------------------------------
-constexpr uint32_t kBatchMagic = 0xEB2B0001u;
-__global__ void guard_kernel(BatchWs ws, size_t w_words, uint32_t magic) {
-    if (__ldcg(&ws.header[3]) == magic) return;
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < w_words; i += (size_t)gridDim.x * blockDim.x)
-        ws.W[i] = 0.f;
-}
+constexpr int kWideR = 16384;         // ads per shared-memory accumulation chunk (64 KB fp32)
 
 // ------------------------------------------------------------------------------------------
 // 1. plan (one CTA)
@@ -80,8 +73,7 @@ __global__ void __launch_bounds__(512) plan_kernel(const uint32_t* __restrict__ 
                                                    const int32_t* __restrict__ user_feat,
                                                    const float* __restrict__ user_x,
                                                    const uint16_t* __restrict__ user_emb, int d, int d_pad,
-                                                   int nu, int nu_pad, BatchWs ws, uint32_t* err,
-                                                   uint32_t magic) {
+                                                   int nu, int nu_pad, BatchWs ws, uint32_t* err) {
     __shared__ uint32_t sScan[40];
     __shared__ uint64_t sCarry;
     const int tid = threadIdx.x;
@@ -130,45 +122,99 @@ __global__ void __launch_bounds__(512) plan_kernel(const uint32_t* __restrict__ 
     if (tid == 0) {
         ws.header[0] = base;
         ws.header[1] = 0;       // overflow users of this group
-        ws.header[3] = magic;   // W is known zeroed from here on
         ws.chunk_off[base] = sCarry;
+    }
+    __syncthreads();
+    // items are in slot order, i.e. grouped by user: first item of each user by binary search
+    for (int u = tid; u <= nu; u += blockDim.x) {
+        int lo = 0, hi = (int)base;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if ((int)ws.items[mid].u < u) lo = mid + 1; else hi = mid;
+        }
+        ws.user_item[u] = (uint32_t)lo;
     }
 }
 
 // ------------------------------------------------------------------------------------------
-// 2. wide: static equal slices of the flat chunk space, 16 chunks per two memory round trips
+// 2a. spans: for every item and every kWideR-ad chunk j, the first of the item's posting chunks
+//     whose first id is >= j*R (one warp per item, lanes binary-search different boundaries)
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) wide_kernel(const uint2* __restrict__ hdr, const uint32_t* __restrict__ payload,
-                                                   BatchWs ws, int64_t n_pad) {
+__global__ void __launch_bounds__(256) span_kernel(const uint2* __restrict__ hdr, BatchWs ws, int nj) {
     const int lane = threadIdx.x & 31;
     const uint32_t n_items = __ldcg(&ws.header[0]);
-    if (n_items == 0) return;
-    const uint64_t T = __ldcg(&ws.chunk_off[n_items]);
-    const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x / 32);
-    const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-    const uint64_t f0 = T * gw / nw, f1 = T * (gw + 1) / nw;
-    if (f0 >= f1) return;
-    int lo = 0, hi = (int)n_items - 1;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (__ldcg(&ws.chunk_off[mid]) <= f0) lo = mid; else hi = mid - 1;
+    const uint32_t i = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    if (i >= n_items) return;
+    const BItem t = ws.items[i];
+    for (int j = lane; j <= nj; j += 32) {
+        const uint32_t x = (uint32_t)((int64_t)j * kWideR);
+        uint32_t lo = t.c0, hi = t.c1;           // first chunk with first >= x
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (__ldg(&hdr[mid]).x < x) lo = mid + 1; else hi = mid;
+        }
+        ws.span[(size_t)i * (nj + 1) + j] = lo;
     }
-    int it = lo;
-    uint64_t f = f0;
-    uint64_t off_it = __ldcg(&ws.chunk_off[it]), off_next = __ldcg(&ws.chunk_off[it + 1]);
-    while (f < f1) {
-        while (off_next <= f) { ++it; off_it = off_next; off_next = __ldcg(&ws.chunk_off[it + 1]); }
-        const BItem t = ws.items[it];
-        const uint32_t cb = t.c0 + (uint32_t)(f - off_it);
-        uint64_t nn = f1 - f;
-        if (nn > 16) nn = 16;
-        if (off_next - f < nn) nn = off_next - f;
-        float* dst = ws.W + (size_t)t.u * n_pad;
-        const float w = t.w;
-        decode_unit16(hdr, payload, t.kwb, cb, cb + (uint32_t)nn, lane,
-                      [dst, w](uint32_t id) { atomicAdd(&dst[id], w); });
-        f += nn;
+}
+
+// ------------------------------------------------------------------------------------------
+// 2b. wide: CTA (chunk j, user u) decodes the user's postings inside ads [j*R, (j+1)*R) and
+//     accumulates w~ in shared memory (Alg. 2 l.355-358, with the per-ad accumulator on chip);
+//     units of 16 posting chunks are load-balanced over the CTA's warps by an exclusive scan of
+//     the items' unit counts (the paper's ExclusiveScan + LoadBalance, l.353-354).  The chunk is
+//     then written to W with coalesced 16-byte stores -- W needs no zeroing and no atomics.
+// ------------------------------------------------------------------------------------------
+constexpr int kWideThreads = 256;
+constexpr int kWideItems = 256;   // items per pass of the unit scan
+__global__ void __launch_bounds__(kWideThreads) wide_smem_kernel(const uint2* __restrict__ hdr,
+                                                                 const uint32_t* __restrict__ payload,
+                                                                 BatchWs ws, int nj, int64_t n_pad) {
+    extern __shared__ __align__(16) float acc[];      // [kWideR]
+    __shared__ uint32_t sLo[kWideItems], sUoff[kWideItems + 1], sScan[40];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = kWideThreads / 32;
+    const int j = blockIdx.x, u = blockIdx.y;
+    const int64_t a0 = (int64_t)j * kWideR;
+    const int64_t a1 = (a0 + kWideR < n_pad) ? a0 + kWideR : n_pad;
+    for (int i = tid; i < kWideR; i += kWideThreads) acc[i] = 0.f;
+    const uint32_t i0 = __ldcg(&ws.user_item[u]), i1 = __ldcg(&ws.user_item[u + 1]);
+    __syncthreads();
+    for (uint32_t ib = i0; ib < i1; ib += kWideItems) {
+        const uint32_t ni = min((uint32_t)kWideItems, i1 - ib);
+        uint32_t nu_units = 0, lo = 0;
+        if ((uint32_t)tid < ni) {
+            const uint32_t it = ib + tid;
+            const uint32_t* sp = ws.span + (size_t)it * (nj + 1);
+            const uint32_t c0 = ws.items[it].c0;
+            const uint32_t s0 = __ldcg(&sp[j]), s1 = __ldcg(&sp[j + 1]);
+            lo = s0 > c0 ? s0 - 1 : c0;              // the chunk before may reach into this range
+            nu_units = (s1 - lo + 15) / 16;
+            if (s1 <= lo) nu_units = 0;
+        }
+        uint32_t tot;
+        const uint32_t pre = block_exclusive_scan(nu_units, sScan, &tot);
+        if ((uint32_t)tid < ni) { sLo[tid] = lo; sUoff[tid] = pre; }
+        if (tid == 0) sUoff[ni] = tot;
+        __syncthreads();
+        for (uint32_t unit = warp; unit < tot; unit += nwarps) {
+            int l = 0, h = (int)ni - 1;               // item = last with sUoff <= unit
+            while (l < h) {
+                const int mid = (l + h + 1) >> 1;
+                if (sUoff[mid] <= unit) l = mid; else h = mid - 1;
+            }
+            const BItem t = ws.items[ib + l];
+            const uint32_t cb = sLo[l] + (unit - sUoff[l]) * 16;
+            const uint32_t s1 = __ldcg(&ws.span[(size_t)(ib + l) * (nj + 1) + j + 1]);
+            const uint32_t ce = min(cb + 16, s1);
+            const float w = t.w;
+            decode_unit16(hdr, payload, t.kwb, cb, ce, lane, [&](uint32_t id) {
+                if ((int64_t)id >= a0 && (int64_t)id < a1) atomicAdd(&acc[id - a0], w);
+            });
+        }
+        __syncthreads();
     }
+    float4* dst = reinterpret_cast<float4*>(ws.W + (size_t)u * n_pad + a0);
+    const float4* src = reinterpret_cast<const float4*>(acc);
+    for (int64_t i = tid; i < (a1 - a0) / 4; i += kWideThreads) __stcg(&dst[i], src[i]);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -294,11 +340,6 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     wf[j] = (valid && c + j < p.nu) ? __ldcg(wcol + (size_t)(c + j) * p.n_pad) : 0.f;
                 uint32_t r[32];
                 tc::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * 128 + c), r);
-                if (MODE == 1 && valid) {
-#pragma unroll
-                    for (int j = 0; j < 32; ++j)       // leave W zeroed for the next call
-                        if (c + j < p.nu) __stcg(wcol + (size_t)(c + j) * p.n_pad, 0.f);
-                }
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
                     const int u = c + j;
@@ -414,8 +455,8 @@ static bool encode_2d_bf16(CUtensorMap* m, const void* base, uint64_t inner, uin
 }
 
 struct Layout {
-    size_t header, items, chunk_off, U, W, samp, theta, count, cand, overflow, total;
-    int64_t cap, n_samp, cap_items;
+    size_t header, items, chunk_off, U, W, samp, theta, count, cand, overflow, user_item, span, total;
+    int64_t cap, n_samp, cap_items, nj;
 };
 
 static Layout layout(const ebr_index* idx, int32_t slots, int32_t k) {
@@ -436,6 +477,9 @@ static Layout layout(const ebr_index* idx, int32_t slots, int32_t k) {
     L.count = o;     o = al(o + (size_t)kGroup * 4);
     L.cand = o;      o = al(o + (size_t)kGroup * L.cap * 8);
     L.overflow = o;  o = al(o + (size_t)kGroup * 4);
+    L.nj = (idx->n_pad + kWideR - 1) / kWideR;
+    L.user_item = o; o = al(o + (size_t)(kGroup + 1) * 4);
+    L.span = o;      o = al(o + (size_t)L.cap_items * (L.nj + 1) * 4);
     L.total = o;
     return L;
 }
@@ -452,6 +496,8 @@ static BatchWs carve(char* base, const Layout& L) {
     w.cand_count = reinterpret_cast<uint32_t*>(base + L.count);
     w.cand = reinterpret_cast<uint64_t*>(base + L.cand);
     w.overflow = reinterpret_cast<uint32_t*>(base + L.overflow);
+    w.user_item = reinterpret_cast<uint32_t*>(base + L.user_item);
+    w.span = reinterpret_cast<uint32_t*>(base + L.span);
     return w;
 }
 
@@ -479,11 +525,10 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
     const int stages = n_kb <= 2 ? 4 : 2;
     const int n_tiles = (int)(idx->n_pad / kTileM);
     const int n_samp_tiles = (int)(L.n_samp / kTileM);
-    const size_t w_words = (size_t)kGroup * idx->n_pad;
-    const uint32_t magic = kBatchMagic ^ (uint32_t)((uint64_t)idx->n_pad * 2654435761ull);
     cudaError_t e = cudaMemsetAsync(ws.overflow, 0, (size_t)kGroup * 4, q.stream);
     if (e != cudaSuccess) return cuda_check(e, "memset(overflow)");
-    guard_kernel<<<idx->sm_count * 2, 512, 0, q.stream>>>(ws, w_words, magic);
+    e = cudaFuncSetAttribute(wide_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kWideR * 4);
+    if (e != cudaSuccess) return cuda_check(e, "attr(wide)");
     CUtensorMap tmA;
     if (!encode_2d_bf16(&tmA, idx->A, (uint64_t)idx->d_pad, (uint64_t)idx->n_pad, kBlockK, kTileM))
         return set_error(EBR_ECUDA, "cuTensorMapEncodeTiled(A) failed");
@@ -502,8 +547,11 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
                                              q.user_feat + (size_t)g0 * idx->n_fields * q.slots,
                                              q.user_x + (size_t)g0 * idx->n_fields * q.slots,
                                              reinterpret_cast<const uint16_t*>(q.user_emb) + (size_t)g0 * idx->d,
-                                             idx->d, idx->d_pad, nu, nu_pad, ws, err_word, magic);
-        wide_kernel<<<idx->sm_count * 4, 256, 0, q.stream>>>(idx->chunk_hdr, idx->payload, ws, idx->n_pad);
+                                             idx->d, idx->d_pad, nu, nu_pad, ws, err_word);
+        const int max_items = nu * idx->n_fields * q.slots;
+        span_kernel<<<(max_items + 7) / 8, 256, 0, q.stream>>>(idx->chunk_hdr, ws, (int)L.nj);
+        wide_smem_kernel<<<dim3((unsigned)L.nj, (unsigned)nu), kWideThreads, kWideR * 4, q.stream>>>(
+            idx->chunk_hdr, idx->payload, ws, (int)L.nj, idx->n_pad);
         GemmParams gp;
         gp.n_ads = idx->n_ads; gp.n_pad = idx->n_pad; gp.ad_begin = (uint32_t)idx->ad_begin;
         gp.d_pad = idx->d_pad; gp.n_kb = n_kb; gp.nu = nu; gp.nu_pad = nu_pad;

@@ -301,7 +301,7 @@ const char* ebr_last_error(void) { return g_last_error.c_str(); }
 
 int32_t ebr_query_launches(const ebr_index* idx, int32_t batch, int32_t slots, int32_t k) {
     if (!idx || batch < 1 || slots < 1 || k < 1) return 0;
-    if (batch_eligible(idx, batch, k)) return ((batch + 127) / 128) * 8;   // memset + 7 kernels per group
+    if (batch_eligible(idx, batch, k)) return 1 + ((batch + 127) / 128) * 7;   // memset + 7 kernels per group
     return (batch + kSmallMaxB - 1) / kSmallMaxB;
 }
 
