@@ -60,7 +60,7 @@ struct BatchWs {   // workspace carve-up (device pointers)
     uint32_t* span;       // [cap_items][n_chunks_R + 1] first chunk of the item with first id >= j*R
 };
 
-constexpr int kWideR = 16384;         // ads per shared-memory accumulation chunk (64 KB fp32)
+constexpr int kWideR = 8192;          // ads per shared-memory accumulation chunk (2 x 32 KB)
 
 // ------------------------------------------------------------------------------------------
 // 1. plan (one CTA)
@@ -159,36 +159,63 @@ __global__ void __launch_bounds__(256) span_kernel(const uint2* __restrict__ hdr
 
 // ------------------------------------------------------------------------------------------
 // 2b. wide: CTA (chunk j, user u) decodes the user's postings inside ads [j*R, (j+1)*R) and
-//     accumulates w~ in shared memory (Alg. 2 l.355-358, with the per-ad accumulator on chip);
-//     units of 16 posting chunks are load-balanced over the CTA's warps by an exclusive scan of
+//     accumulates w~ on chip (Alg. 2 l.355-358 with the per-ad accumulator in shared memory).
+//     Accumulation is 48-bit fixed point over two native 32-bit shared atomics: with
+//     S = 46 - ceil(log2(sum_i |w~_i|)) for the user, each w~ becomes F = rint(w~ 2^S), split as
+//     F = H*2^16 + L (L = low 16 bits); sum H and sum L cannot overflow and the total is exact
+//     integer arithmetic -- order-free (deterministic) and finer than fp32 (error <= 2^-47 of the
+//     bound per hit; exact for dyadic inputs).  fp32 shared atomics are CAS loops on sm_100a.
+//     Units of 16 posting chunks are load-balanced over the CTA's warps by an exclusive scan of
 //     the items' unit counts (the paper's ExclusiveScan + LoadBalance, l.353-354).  The chunk is
-//     then written to W with coalesced 16-byte stores -- W needs no zeroing and no atomics.
+//     then written to W (fp32) with coalesced stores -- no global atomics, nothing to re-zero.
 // ------------------------------------------------------------------------------------------
 constexpr int kWideThreads = 256;
 constexpr int kWideItems = 256;   // items per pass of the unit scan
-__global__ void __launch_bounds__(kWideThreads) wide_smem_kernel(const uint2* __restrict__ hdr,
-                                                                 const uint32_t* __restrict__ payload,
-                                                                 BatchWs ws, int nj, int64_t n_pad) {
-    extern __shared__ __align__(16) float acc[];      // [kWideR]
+__global__ void __launch_bounds__(kWideThreads, 3) wide_smem_kernel(const uint2* __restrict__ hdr,
+                                                                    const uint32_t* __restrict__ payload,
+                                                                    BatchWs ws, int nj, int64_t n_pad) {
+    extern __shared__ __align__(16) int32_t accH[];   // [kWideR] high parts, then [kWideR] low parts
+    uint32_t* accL = reinterpret_cast<uint32_t*>(accH + kWideR);
     __shared__ uint32_t sLo[kWideItems], sUoff[kWideItems + 1], sScan[40];
+    __shared__ int32_t sH[kWideItems];
+    __shared__ uint32_t sL[kWideItems];
+    __shared__ float sBound[8];
+    __shared__ int sShift;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = kWideThreads / 32;
     const int j = blockIdx.x, u = blockIdx.y;
     const int64_t a0 = (int64_t)j * kWideR;
     const int64_t a1 = (a0 + kWideR < n_pad) ? a0 + kWideR : n_pad;
-    for (int i = tid; i < kWideR; i += kWideThreads) acc[i] = 0.f;
+    for (int i = tid; i < kWideR; i += kWideThreads) { accH[i] = 0; accL[i] = 0u; }
     const uint32_t i0 = __ldcg(&ws.user_item[u]), i1 = __ldcg(&ws.user_item[u + 1]);
+    // the user's fixed-point scale (same in every CTA of the user: depends on its items only)
+    float bnd = 0.f;
+    for (uint32_t it = i0 + tid; it < i1; it += kWideThreads) bnd += fabsf(ws.items[it].w);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) bnd += __shfl_xor_sync(FULL, bnd, o);
+    if (lane == 0) sBound[warp] = bnd;
     __syncthreads();
+    if (tid == 0) {
+        float tb = 0.f;
+        for (int w = 0; w < nwarps; ++w) tb += sBound[w];
+        int e = 0;
+        frexpf(tb * 1.0001f + 1e-30f, &e);          // tb < 2^e
+        sShift = 46 - e;
+    }
+    __syncthreads();
+    const int S = sShift;
     for (uint32_t ib = i0; ib < i1; ib += kWideItems) {
         const uint32_t ni = min((uint32_t)kWideItems, i1 - ib);
         uint32_t nu_units = 0, lo = 0;
         if ((uint32_t)tid < ni) {
             const uint32_t it = ib + tid;
             const uint32_t* sp = ws.span + (size_t)it * (nj + 1);
-            const uint32_t c0 = ws.items[it].c0;
+            const BItem t = ws.items[it];
             const uint32_t s0 = __ldcg(&sp[j]), s1 = __ldcg(&sp[j + 1]);
-            lo = s0 > c0 ? s0 - 1 : c0;              // the chunk before may reach into this range
-            nu_units = (s1 - lo + 15) / 16;
-            if (s1 <= lo) nu_units = 0;
+            lo = s0 > t.c0 ? s0 - 1 : t.c0;           // the chunk before may reach into this range
+            nu_units = s1 > lo ? (s1 - lo + 15) / 16 : 0;
+            const long long F = __double2ll_rn(ldexp((double)t.w, S));
+            sH[tid] = (int32_t)(F >> 16);
+            sL[tid] = (uint32_t)(F & 0xFFFF);
         }
         uint32_t tot;
         const uint32_t pre = block_exclusive_scan(nu_units, sScan, &tot);
@@ -201,20 +228,34 @@ __global__ void __launch_bounds__(kWideThreads) wide_smem_kernel(const uint2* __
                 const int mid = (l + h + 1) >> 1;
                 if (sUoff[mid] <= unit) l = mid; else h = mid - 1;
             }
-            const BItem t = ws.items[ib + l];
+            const uint32_t it = ib + l;
             const uint32_t cb = sLo[l] + (unit - sUoff[l]) * 16;
-            const uint32_t s1 = __ldcg(&ws.span[(size_t)(ib + l) * (nj + 1) + j + 1]);
+            const uint32_t s1 = __ldcg(&ws.span[(size_t)it * (nj + 1) + j + 1]);
             const uint32_t ce = min(cb + 16, s1);
-            const float w = t.w;
-            decode_unit16(hdr, payload, t.kwb, cb, ce, lane, [&](uint32_t id) {
-                if ((int64_t)id >= a0 && (int64_t)id < a1) atomicAdd(&acc[id - a0], w);
+            const int32_t H = sH[l];
+            const uint32_t L = sL[l];
+            decode_unit16(hdr, payload, ws.items[it].kwb, cb, ce, lane, [&](uint32_t id) {
+                if ((int64_t)id >= a0 && (int64_t)id < a1) {
+                    atomicAdd(&accH[id - a0], H);
+                    atomicAdd(&accL[id - a0], L);
+                }
             });
         }
         __syncthreads();
     }
+    const double inv = ldexp(1.0, -S);
     float4* dst = reinterpret_cast<float4*>(ws.W + (size_t)u * n_pad + a0);
-    const float4* src = reinterpret_cast<const float4*>(acc);
-    for (int64_t i = tid; i < (a1 - a0) / 4; i += kWideThreads) __stcg(&dst[i], src[i]);
+    for (int64_t i = tid; i < (a1 - a0) / 4; i += kWideThreads) {
+        float4 v;
+        float* vf = reinterpret_cast<float*>(&v);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int64_t r = i * 4 + q;
+            const long long tot = (long long)accH[r] * 65536ll + (long long)accL[r];
+            vf[q] = (float)((double)tot * inv);
+        }
+        __stcg(&dst[i], v);
+    }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -527,7 +568,7 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
     const int n_samp_tiles = (int)(L.n_samp / kTileM);
     cudaError_t e = cudaMemsetAsync(ws.overflow, 0, (size_t)kGroup * 4, q.stream);
     if (e != cudaSuccess) return cuda_check(e, "memset(overflow)");
-    e = cudaFuncSetAttribute(wide_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kWideR * 4);
+    e = cudaFuncSetAttribute(wide_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kWideR * 8);
     if (e != cudaSuccess) return cuda_check(e, "attr(wide)");
     CUtensorMap tmA;
     if (!encode_2d_bf16(&tmA, idx->A, (uint64_t)idx->d_pad, (uint64_t)idx->n_pad, kBlockK, kTileM))
@@ -550,7 +591,7 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
                                              idx->d, idx->d_pad, nu, nu_pad, ws, err_word);
         const int max_items = nu * idx->n_fields * q.slots;
         span_kernel<<<(max_items + 7) / 8, 256, 0, q.stream>>>(idx->chunk_hdr, ws, (int)L.nj);
-        wide_smem_kernel<<<dim3((unsigned)L.nj, (unsigned)nu), kWideThreads, kWideR * 4, q.stream>>>(
+        wide_smem_kernel<<<dim3((unsigned)L.nj, (unsigned)nu), kWideThreads, kWideR * 8, q.stream>>>(
             idx->chunk_hdr, idx->payload, ws, (int)L.nj, idx->n_pad);
         GemmParams gp;
         gp.n_ads = idx->n_ads; gp.n_pad = idx->n_pad; gp.ad_begin = (uint32_t)idx->ad_begin;
