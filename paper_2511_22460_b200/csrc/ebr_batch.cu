@@ -57,7 +57,8 @@ struct BatchWs {   // workspace carve-up (device pointers)
     uint64_t* cand;       // [kGroup][cap]
     uint32_t* overflow;   // [kGroup]
     uint32_t* user_item;  // [kGroup + 1]  items of group user u: [user_item[u], user_item[u+1])
-    uint32_t* span;       // [cap_items][n_chunks_R + 1] first chunk of the item with first id >= j*R
+    uint32_t* span;       // [nj + 1][cap_items] first chunk of item i with first id >= j*R
+    uint32_t* span_lo;    // [nj][cap_items]     first chunk of item i holding an id >= j*R
 };
 
 constexpr int kWideR = 8192;          // ads per shared-memory accumulation chunk (2 x 32 KB)
@@ -137,10 +138,14 @@ __global__ void __launch_bounds__(512) plan_kernel(const uint32_t* __restrict__ 
 }
 
 // ------------------------------------------------------------------------------------------
-// 2a. spans: for every item and every kWideR-ad chunk j, the first of the item's posting chunks
-//     whose first id is >= j*R (one warp per item, lanes binary-search different boundaries)
+// 2a. spans: for every item and every kWideR-ad chunk j, the item's posting chunks that hold an
+//     id in [j*R, (j+1)*R): [span_lo[j][i], span[j+1][i]).  One warp per item, lanes binary-search
+//     different boundaries over the chunk first ids; chunk_last decides whether the chunk that
+//     straddles j*R reaches into the range (so an item with no posting there costs nothing).
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) span_kernel(const uint2* __restrict__ hdr, BatchWs ws, int nj) {
+__global__ void __launch_bounds__(256) span_kernel(const uint2* __restrict__ hdr,
+                                                   const uint32_t* __restrict__ chunk_last,
+                                                   BatchWs ws, int nj, int cap_items) {
     const int lane = threadIdx.x & 31;
     const uint32_t n_items = __ldcg(&ws.header[0]);
     const uint32_t i = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
@@ -153,7 +158,11 @@ __global__ void __launch_bounds__(256) span_kernel(const uint2* __restrict__ hdr
             const uint32_t mid = (lo + hi) >> 1;
             if (__ldg(&hdr[mid]).x < x) lo = mid + 1; else hi = mid;
         }
-        ws.span[(size_t)i * (nj + 1) + j] = lo;
+        ws.span[(size_t)j * cap_items + i] = lo;
+        if (j < nj) {
+            const bool straddles = lo > t.c0 && __ldg(&chunk_last[lo - 1]) >= x;
+            ws.span_lo[(size_t)j * cap_items + i] = straddles ? lo - 1 : lo;
+        }
     }
 }
 
@@ -173,7 +182,8 @@ constexpr int kWideThreads = 256;
 constexpr int kWideItems = 256;   // items per pass of the unit scan
 __global__ void __launch_bounds__(kWideThreads, 3) wide_smem_kernel(const uint2* __restrict__ hdr,
                                                                     const uint32_t* __restrict__ payload,
-                                                                    BatchWs ws, int nj, int64_t n_pad) {
+                                                                    BatchWs ws, int nj, int64_t n_pad,
+                                                                    int cap_items) {
     extern __shared__ __align__(16) int32_t accH[];   // [kWideR] high parts, then [kWideR] low parts
     uint32_t* accL = reinterpret_cast<uint32_t*>(accH + kWideR);
     __shared__ uint32_t sLo[kWideItems], sUoff[kWideItems + 1], sScan[40];
@@ -208,10 +218,9 @@ __global__ void __launch_bounds__(kWideThreads, 3) wide_smem_kernel(const uint2*
         uint32_t nu_units = 0, lo = 0;
         if ((uint32_t)tid < ni) {
             const uint32_t it = ib + tid;
-            const uint32_t* sp = ws.span + (size_t)it * (nj + 1);
             const BItem t = ws.items[it];
-            const uint32_t s0 = __ldcg(&sp[j]), s1 = __ldcg(&sp[j + 1]);
-            lo = s0 > t.c0 ? s0 - 1 : t.c0;           // the chunk before may reach into this range
+            lo = __ldcg(&ws.span_lo[(size_t)j * cap_items + it]);
+            const uint32_t s1 = __ldcg(&ws.span[(size_t)(j + 1) * cap_items + it]);
             nu_units = s1 > lo ? (s1 - lo + 15) / 16 : 0;
             const long long F = __double2ll_rn(ldexp((double)t.w, S));
             sH[tid] = (int32_t)(F >> 16);
@@ -230,7 +239,7 @@ __global__ void __launch_bounds__(kWideThreads, 3) wide_smem_kernel(const uint2*
             }
             const uint32_t it = ib + l;
             const uint32_t cb = sLo[l] + (unit - sUoff[l]) * 16;
-            const uint32_t s1 = __ldcg(&ws.span[(size_t)it * (nj + 1) + j + 1]);
+            const uint32_t s1 = __ldcg(&ws.span[(size_t)(j + 1) * cap_items + it]);
             const uint32_t ce = min(cb + 16, s1);
             const int32_t H = sH[l];
             const uint32_t L = sL[l];
@@ -496,7 +505,7 @@ static bool encode_2d_bf16(CUtensorMap* m, const void* base, uint64_t inner, uin
 }
 
 struct Layout {
-    size_t header, items, chunk_off, U, W, samp, theta, count, cand, overflow, user_item, span, total;
+    size_t header, items, chunk_off, U, W, samp, theta, count, cand, overflow, user_item, span, span_lo, total;
     int64_t cap, n_samp, cap_items, nj;
 };
 
@@ -521,6 +530,7 @@ static Layout layout(const ebr_index* idx, int32_t slots, int32_t k) {
     L.nj = (idx->n_pad + kWideR - 1) / kWideR;
     L.user_item = o; o = al(o + (size_t)(kGroup + 1) * 4);
     L.span = o;      o = al(o + (size_t)L.cap_items * (L.nj + 1) * 4);
+    L.span_lo = o;   o = al(o + (size_t)L.cap_items * L.nj * 4);
     L.total = o;
     return L;
 }
@@ -539,6 +549,7 @@ static BatchWs carve(char* base, const Layout& L) {
     w.overflow = reinterpret_cast<uint32_t*>(base + L.overflow);
     w.user_item = reinterpret_cast<uint32_t*>(base + L.user_item);
     w.span = reinterpret_cast<uint32_t*>(base + L.span);
+    w.span_lo = reinterpret_cast<uint32_t*>(base + L.span_lo);
     return w;
 }
 
@@ -590,9 +601,10 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
                                              reinterpret_cast<const uint16_t*>(q.user_emb) + (size_t)g0 * idx->d,
                                              idx->d, idx->d_pad, nu, nu_pad, ws, err_word);
         const int max_items = nu * idx->n_fields * q.slots;
-        span_kernel<<<(max_items + 7) / 8, 256, 0, q.stream>>>(idx->chunk_hdr, ws, (int)L.nj);
+        span_kernel<<<(max_items + 7) / 8, 256, 0, q.stream>>>(idx->chunk_hdr, idx->chunk_last, ws, (int)L.nj,
+                                                               (int)L.cap_items);
         wide_smem_kernel<<<dim3((unsigned)L.nj, (unsigned)nu), kWideThreads, kWideR * 8, q.stream>>>(
-            idx->chunk_hdr, idx->payload, ws, (int)L.nj, idx->n_pad);
+            idx->chunk_hdr, idx->payload, ws, (int)L.nj, idx->n_pad, (int)L.cap_items);
         GemmParams gp;
         gp.n_ads = idx->n_ads; gp.n_pad = idx->n_pad; gp.ad_begin = (uint32_t)idx->ad_begin;
         gp.d_pad = idx->d_pad; gp.n_kb = n_kb; gp.nu = nu; gp.nu_pad = nu_pad;

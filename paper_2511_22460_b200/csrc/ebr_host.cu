@@ -56,7 +56,7 @@ size_t small_workspace_bytes(const ebr_index* idx, int32_t slots, int32_t k);
 // host encoder
 // ------------------------------------------------------------------------------------------
 struct Encoded {
-    std::vector<uint32_t> key_chunk_off, key_word_off, hdr, payload;
+    std::vector<uint32_t> key_chunk_off, key_word_off, hdr, payload, last;
     int64_t nnz = 0;
 };
 
@@ -148,6 +148,7 @@ static ebr_status encode(const int32_t* ad_feat, int64_t n_ads, int32_t F, const
     }
     out.key_chunk_off[n_keys] = (uint32_t)cacc;
     out.hdr.assign(2 * cacc, 0);
+    out.last.assign(cacc, 0);
     out.payload.assign(wacc + 2, 0);   // two guard words: the decoder reads word w+1
     int64_t nnz = 0;
     for (int f = 0; f < F; ++f) nnz += (int64_t)lists[f].size();
@@ -171,6 +172,7 @@ static ebr_status encode(const int32_t* ad_feat, int64_t n_ads, int32_t F, const
                     const uint32_t b = bit_width(mx);
                     const uint32_t n = (uint32_t)(c1 - c0);
                     out.hdr[2 * (size_t)c] = (uint32_t)L[c0];
+                    out.last[c] = (uint32_t)L[c1 - 1];
                     out.hdr[2 * (size_t)c + 1] = (n - 1u) | (b << 5) | (rel << 10);
                     if (b) {
                         for (int64_t j = c0 + 1; j < c1; ++j) {
@@ -348,7 +350,7 @@ void ebr_free_index(ebr_index* idx) {
     int prev = -1;
     cudaGetDevice(&prev);
     cudaSetDevice(idx->device);
-    void* ptrs[] = {idx->A, idx->key_chunk_off, idx->key_word_off, idx->chunk_hdr, idx->payload,
+    void* ptrs[] = {idx->A, idx->key_chunk_off, idx->key_word_off, idx->chunk_hdr, idx->chunk_last, idx->payload,
                     idx->cross_w, idx->field_card, idx->field_base};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -421,6 +423,7 @@ ebr_status ebr_build_index(const void* ad_emb, ebr_dtype dtype, int64_t ad_begin
         EBR_TRY(upload((void**)&idx->key_chunk_off, enc.key_chunk_off.data(), enc.key_chunk_off.size() * 4));
         EBR_TRY(upload((void**)&idx->key_word_off, enc.key_word_off.data(), enc.key_word_off.size() * 4));
         EBR_TRY(upload((void**)&idx->chunk_hdr, enc.hdr.data(), enc.hdr.size() * 4));
+        EBR_TRY(upload((void**)&idx->chunk_last, enc.last.data(), enc.last.size() * 4));
         EBR_TRY(upload((void**)&idx->payload, enc.payload.data(), enc.payload.size() * 4));
         EBR_TRY(upload((void**)&idx->cross_w, cross_w, (size_t)n_keys * 4));
         std::vector<int32_t> fb(n_fields);
@@ -621,7 +624,7 @@ ebr_status ebr_index_stats(const ebr_index* idx, ebr_stats* o) {
     o->nnz = idx->nnz;
     o->chunks = idx->n_chunks;
     o->payload_words = idx->n_words;
-    o->index_bytes = (idx->n_keys * 2 + 1) * 4 + idx->n_chunks * 8 + (idx->n_words + 2) * 4 + idx->n_keys * 4;
+    o->index_bytes = (idx->n_keys * 2 + 1) * 4 + idx->n_chunks * 12 + (idx->n_words + 2) * 4 + idx->n_keys * 4;
     o->emb_bytes = idx->n_pad * idx->d_pad * esz;
     o->build_ms = idx->build_ms;
     return EBR_OK;

@@ -22,6 +22,7 @@ struct ebr_index {
     uint32_t* key_chunk_off;        // [M+1]
     uint32_t* key_word_off;         // [M]
     uint2* chunk_hdr;               // [C]  {first local id, meta}
+    uint32_t* chunk_last;           // [C]  last local id of each chunk (exact chunk spans per ad range)
     uint32_t* payload;              // [W + 2] (2 guard words)
     float* cross_w;                 // [M]
     int32_t* field_card;            // [F]
