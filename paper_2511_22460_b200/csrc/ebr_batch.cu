@@ -186,9 +186,9 @@ __global__ void __launch_bounds__(kWideThreads, 3) wide_smem_kernel(const uint2*
                                                                     int cap_items) {
     extern __shared__ __align__(16) int32_t accH[];   // [kWideR] high parts, then [kWideR] low parts
     uint32_t* accL = reinterpret_cast<uint32_t*>(accH + kWideR);
-    __shared__ uint32_t sLo[kWideItems], sUoff[kWideItems + 1], sScan[40];
+    __shared__ uint32_t sLo[kWideItems], sHi[kWideItems], sUoff[kWideItems + 1], sScan[40];
     __shared__ int32_t sH[kWideItems];
-    __shared__ uint32_t sL[kWideItems];
+    __shared__ uint32_t sL[kWideItems], sKwb[kWideItems];
     __shared__ float sBound[8];
     __shared__ int sShift;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = kWideThreads / 32;
@@ -225,25 +225,22 @@ __global__ void __launch_bounds__(kWideThreads, 3) wide_smem_kernel(const uint2*
             const long long F = __double2ll_rn(ldexp((double)t.w, S));
             sH[tid] = (int32_t)(F >> 16);
             sL[tid] = (uint32_t)(F & 0xFFFF);
+            sHi[tid] = s1;
+            sKwb[tid] = t.kwb;
         }
         uint32_t tot;
         const uint32_t pre = block_exclusive_scan(nu_units, sScan, &tot);
         if ((uint32_t)tid < ni) { sLo[tid] = lo; sUoff[tid] = pre; }
         if (tid == 0) sUoff[ni] = tot;
         __syncthreads();
-        for (uint32_t unit = warp; unit < tot; unit += nwarps) {
-            int l = 0, h = (int)ni - 1;               // item = last with sUoff <= unit
-            while (l < h) {
-                const int mid = (l + h + 1) >> 1;
-                if (sUoff[mid] <= unit) l = mid; else h = mid - 1;
-            }
-            const uint32_t it = ib + l;
+        int l = 0;                                    // units are visited in increasing order:
+        for (uint32_t unit = warp; unit < tot; unit += nwarps) {   // walk the item index forward
+            while (sUoff[l + 1] <= unit) ++l;
             const uint32_t cb = sLo[l] + (unit - sUoff[l]) * 16;
-            const uint32_t s1 = __ldcg(&ws.span[(size_t)(j + 1) * cap_items + it]);
-            const uint32_t ce = min(cb + 16, s1);
+            const uint32_t ce = min(cb + 16, sHi[l]);
             const int32_t H = sH[l];
             const uint32_t L = sL[l];
-            decode_unit16(hdr, payload, ws.items[it].kwb, cb, ce, lane, [&](uint32_t id) {
+            decode_unit16(hdr, payload, sKwb[l], cb, ce, lane, [&](uint32_t id) {
                 if ((int64_t)id >= a0 && (int64_t)id < a1) {
                     atomicAdd(&accH[id - a0], H);
                     atomicAdd(&accL[id - a0], L);

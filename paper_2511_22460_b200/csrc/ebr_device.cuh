@@ -108,9 +108,10 @@ __device__ __forceinline__ void decode_unit16(const uint2* __restrict__ hdr,
     uint32_t lo[16], hi[16];
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
-        const uint32_t meta = __shfl_sync(FULL, h.y, q);
         lo[q] = 0u;
         hi[q] = 0u;
+        if ((uint32_t)q >= nc) break;                // warp-uniform: short units stop early
+        const uint32_t meta = __shfl_sync(FULL, h.y, q);
         const uint32_t n = (meta & 31u) + 1u, b = (meta >> 5) & 31u;
         if ((uint32_t)q < nc && lane >= 1 && (uint32_t)lane < n && b) {
             const uint32_t bit = (uint32_t)(lane - 1) * b;
