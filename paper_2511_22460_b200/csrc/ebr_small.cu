@@ -85,7 +85,11 @@ ebr_status run_small(const QueryArgs& q, int b0, int B) {
     // keep the CTA's deep/fused scores in shared memory when they fit
     const size_t res_bytes = (size_t)B * R * 4;
     const bool resident = plan_bytes + res_bytes <= cap - 8 * 1024;
-    const size_t p1 = plan_bytes + (resident ? res_bytes : 0);
+    // local wide accumulation: spans/unit offsets/fixed-point parts per item + 2 x [B][R] words
+    const size_t local_bytes = (size_t)items_cap * 20 + 32 + (size_t)B * R * 8;
+    static const bool no_local = getenv("EBR_NO_LOCAL_WIDE") != nullptr;
+    const bool local_wide = !no_local && resident && B <= 2 && plan_bytes + res_bytes + local_bytes <= cap - 8 * 1024;
+    const size_t p1 = plan_bytes + (resident ? res_bytes : 0) + (local_wide ? local_bytes : 0);
     const size_t smem = std::max(p1, sel_min);
     if (smem > cap)
         return set_error(EBR_EUNSUPPORTED, "latency path: %d user slots / k=%d need %zu B of shared memory",
@@ -126,6 +130,8 @@ ebr_status run_small(const QueryArgs& q, int b0, int B) {
     p.R = (int32_t)R;
     p.n_ranges = n_ranges;
     p.resident = resident ? 1 : 0;
+    p.local_wide = local_wide ? 1 : 0;
+    p.chunk_last = idx->chunk_last;
     p.items_cap = items_cap;
     p.smem_bytes = (int32_t)smem;
 

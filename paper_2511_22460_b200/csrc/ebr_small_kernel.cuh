@@ -93,6 +93,8 @@ struct SmallParams {
     int32_t smem_bytes;
     int32_t diag;               // EBR_DIAG bits (diagnostics only): 1 = skip wide, 2 = skip deep
     int32_t resident;           // deep / fused scores of the CTA's range kept in shared memory
+    int32_t local_wide;         // wide term accumulated per CTA range in shared memory (B <= 2)
+    const uint32_t* chunk_last; // [C] last id of each posting chunk (exact per-range spans)
 };
 
 struct Item {
@@ -174,9 +176,19 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
     Item* sItems = reinterpret_cast<Item*>(sHist + (size_t)B * kHistBins);        // [items_cap]
     uint64_t* sChunkOff = reinterpret_cast<uint64_t*>(
         (reinterpret_cast<uintptr_t>(sItems + p.items_cap) + 7) & ~(uintptr_t)7);  // [items_cap + 1]
-    __shared__ uint32_t sScan[40], sScalar[8], sNItems;
+    // local-wide mode: per-item chunk span inside this CTA's range, unit offsets, fixed-point
+    // parts, and the 48-bit accumulators (high parts, low 16-bit parts) for [B][R] ads
+    uint32_t* sSpanLo = reinterpret_cast<uint32_t*>(sChunkOff + p.items_cap + 1);
+    uint32_t* sSpanHi = sSpanLo + p.items_cap;
+    uint32_t* sUoffL = sSpanHi + p.items_cap;                                    // [items_cap + 1]
+    int32_t* sHpart = reinterpret_cast<int32_t*>(sUoffL + p.items_cap + 1);
+    uint32_t* sLpart = reinterpret_cast<uint32_t*>(sHpart + p.items_cap);
+    int32_t* accH = reinterpret_cast<int32_t*>(
+        (reinterpret_cast<uintptr_t>(sLpart + p.items_cap) + 15) & ~(uintptr_t)15);  // [B][R]
+    uint32_t* accL = reinterpret_cast<uint32_t*>(accH + (p.local_wide ? (size_t)B * R : 0));
+    __shared__ uint32_t sScan[40], sScalar[8], sNItems, sUnitCtr, sNUnits;
     __shared__ uint32_t sBinStar[kSmallMaxB], sSeg[kSmallMaxB];
-    __shared__ int sInit;
+    __shared__ int sInit, sShiftB[kSmallMaxB];
 
     const bool has_range = (int)blockIdx.x < p.n_ranges;
     const int64_t r0 = (int64_t)blockIdx.x * R;
@@ -185,8 +197,10 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
 
     if (p.timers && blockIdx.x == 0 && tid == 0) p.timers[0] = gtimer();
     // ---- first use of this workspace: zero it (uniform decision across the grid) ----
-    if (tid == 0) sInit = (__ldcg(&p.header[0]) != p.magic);
+    if (tid == 0) { sInit = (__ldcg(&p.header[0]) != p.magic); sUnitCtr = 0; sNUnits = 0; }
     for (int i = tid; i < B * kHistBins; i += kThreads) sHist[i] = 0;
+    if (p.local_wide)
+        for (int i = tid; i < B * R; i += kThreads) { accH[i] = 0; accL[i] = 0u; }
     if (tid < kSmallMaxB) sSeg[tid] = 0;
     __syncthreads();
     if (sInit) {   // ebr_workspace_init was not called: do it here
@@ -281,6 +295,50 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
         for (int i = i0; i < i1; ++i) { sChunkOff[i] = acc; acc += sItems[i].c1 - sItems[i].c0; }
         if (gt == 0) sChunkOff[n_items] = tot2;
         nbar_sync(1, NT);                  // the wide warps read each other's offsets next
+        if (p.local_wide) {
+            // per-user fixed-point scale: bound = (#items) * max|w~| >= any sum of hits
+            if (gt < B) {
+                float mx = 0.f;
+                int cnt_b = 0;
+                for (int i = 0; i < n_items; ++i)
+                    if ((int)sItems[i].b == gt) { mx = fmaxf(mx, fabsf(sItems[i].w)); ++cnt_b; }
+                int e = 0;
+                frexpf(mx * (float)cnt_b * 1.0001f + 1e-30f, &e);
+                sShiftB[gt] = 46 - e;
+            }
+            nbar_sync(1, NT);
+            // exact chunk span of every item inside [r0, r1): first chunk whose last id >= r0,
+            // first chunk whose first id >= r1 (binary searches, one lane per item)
+            uint32_t my_units = 0;
+            const int per3 = (n_items + NT - 1) / NT;
+            const int j0 = min(n_items, gt * per3), j1 = min(n_items, j0 + per3);
+            for (int i = j0; i < j1; ++i) {
+                const Item t = sItems[i];
+                uint32_t lo = t.c0, hi = t.c1;
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (__ldg(&p.chunk_last[mid]) < (uint32_t)r0) lo = mid + 1; else hi = mid;
+                }
+                uint32_t lo2 = lo, hi2 = t.c1;
+                while (lo2 < hi2) {
+                    const uint32_t mid = (lo2 + hi2) >> 1;
+                    if (__ldg(&p.hdr[mid]).x < (uint32_t)r1) lo2 = mid + 1; else hi2 = mid;
+                }
+                sSpanLo[i] = lo;
+                sSpanHi[i] = lo2;
+                const uint32_t nu_i = lo2 > lo ? (lo2 - lo + kUnit - 1) / kUnit : 0u;
+                sUoffL[i] = nu_i;                      // scanned below
+                my_units += nu_i;
+                const long long F = __double2ll_rn(ldexp((double)t.w, sShiftB[t.b]));
+                sHpart[i] = (int32_t)(F >> 16);
+                sLpart[i] = (uint32_t)(F & 0xFFFF);
+            }
+            uint32_t tot_u;
+            uint32_t pre = group_exclusive_scan(my_units, sScan, &tot_u, gt, kWideWarps, 1);
+            for (int i = j0; i < j1; ++i) { const uint32_t c = sUoffL[i]; sUoffL[i] = pre; pre += c; }
+            if (gt == 0) { sUoffL[n_items] = tot_u; sNUnits = tot_u; }
+            nbar_sync(1, NT);
+        }
         nbar_arrive(2, kThreads);          // publish the plan to the deep warps (barrier 2)
         EBR_STAMP(1);
     } else if (!(p.diag & 2)) {
@@ -399,7 +457,40 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
         EBR_STAMP(3);
     }
     if (warp < kDeepWarps) nbar_sync(2, kThreads);   // deep warps wait for the plan before helping
-    {
+    if (p.local_wide) {
+        // ---- B (wide, local): 16-chunk units of this CTA's item spans, claimed from a shared
+        // counter (ExclusiveScan + LoadBalance, Alg. 2 l.353-354), accumulated in shared memory
+        // as 48-bit fixed point over two native 32-bit atomics (exact for dyadic inputs) ----
+        const uint32_t n_units = (p.diag & 1) ? 0u : sNUnits;
+        const int n_items = (int)sNItems;
+        int l = 0;
+        while (true) {
+            uint32_t unit = 0;
+            if (lane == 0) unit = atomicAdd(&sUnitCtr, 1u);
+            unit = __shfl_sync(FULL, unit, 0);
+            if (unit >= n_units) break;
+            int lo_i = 0, hi_i = n_items - 1;          // item = last with sUoffL <= unit
+            while (lo_i < hi_i) {
+                const int mid = (lo_i + hi_i + 1) >> 1;
+                if (sUoffL[mid] <= unit) lo_i = mid; else hi_i = mid - 1;
+            }
+            l = lo_i;
+            const uint32_t cb = sSpanLo[l] + (unit - sUoffL[l]) * kUnit;
+            const uint32_t ce = min(cb + (uint32_t)kUnit, sSpanHi[l]);
+            const Item t = sItems[l];
+            const int32_t H = sHpart[l];
+            const uint32_t L = sLpart[l];
+            int32_t* ah = accH + (size_t)t.b * R;
+            uint32_t* al = accL + (size_t)t.b * R;
+            decode_unit16(p.hdr, p.payload, t.kwb, cb, ce, lane, [&](uint32_t id) {
+                if (id >= (uint32_t)r0 && id < (uint32_t)r1) {
+                    atomicAdd(&ah[id - (uint32_t)r0], H);
+                    atomicAdd(&al[id - (uint32_t)r0], L);
+                }
+            });
+        }
+        EBR_STAMP(2);
+    } else {
         // ---- B (wide): 16-chunk units of the flat chunk space from a global queue ----
         // (the paper's LoadBalance, Alg. 2 l.354); units may straddle items.  Software-pipelined:
         // the next unit is claimed and its headers fetched while this unit's payload is in flight.
@@ -484,11 +575,25 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
         EBR_STAMP(2);
     }
     EBR_STAMP(4);
-    grid.sync();
+    if (p.local_wide) __syncthreads();   // the CTA's wide term is complete (no other CTA adds to it)
+    else grid.sync();                    // every CTA's reductions into the wide array are complete
     EBR_STAMP(5);
 
     // ---- C: fuse + histogram (8 independent elements in flight per thread) ----
     constexpr int kIlp = 4;
+    if (p.local_wide) {
+        for (int b = 0; b < B; ++b) {
+            const double inv = ldexp(1.0, -sShiftB[b]);
+            for (int r = tid; r < rn; r += kThreads) {
+                const size_t o = (size_t)b * R + r;
+                const long long acc = (long long)accH[o] * 65536ll + (long long)accL[o];
+                float s = sS[o] + (float)((double)acc * inv);
+                if (s == 0.f) s = 0.f;                      // -0 -> +0 (R14)
+                sS[o] = s;
+                atomicAdd(&sHist[b * kHistBins + (ord_of(s) >> (32 - kHistBits))], 1u);
+            }
+        }
+    } else
     for (int b = 0; b < B; ++b) {
         float* sc = p.scores + (size_t)b * p.n_pad;
         float* wd = p.wide + (size_t)b * p.n_pad;
