@@ -491,31 +491,79 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
         // as 48-bit fixed point over two native 32-bit atomics (exact for dyadic inputs) ----
         const uint32_t n_units = (p.diag & 1) ? 0u : sNUnits;
         const int n_items = (int)sNItems;
-        int l = 0;
-        while (true) {
+        struct LUnit { uint32_t unit; int l; uint32_t cb, nc; uint2 h; };
+        auto next_unit = [&]() -> LUnit {          // claim a unit and start its header loads
+            LUnit r;
             uint32_t unit = 0;
             if (lane == 0) unit = atomicAdd(&sUnitCtr, 1u);
-            unit = __shfl_sync(FULL, unit, 0);
-            if (unit >= n_units) break;
-            int lo_i = 0, hi_i = n_items - 1;          // item = last with sUoffL <= unit
-            while (lo_i < hi_i) {
-                const int mid = (lo_i + hi_i + 1) >> 1;
-                if (sUoffL[mid] <= unit) lo_i = mid; else hi_i = mid - 1;
+            r.unit = __shfl_sync(FULL, unit, 0);
+            r.l = 0; r.cb = 0; r.nc = 0; r.h = make_uint2(0u, 0u);
+            if (r.unit < n_units) {
+                int lo_i = 0, hi_i = n_items - 1;  // item = last with sUoffL <= unit
+                while (lo_i < hi_i) {
+                    const int mid = (lo_i + hi_i + 1) >> 1;
+                    if (sUoffL[mid] <= r.unit) lo_i = mid; else hi_i = mid - 1;
+                }
+                r.l = lo_i;
+                r.cb = sSpanLo[lo_i] + (r.unit - sUoffL[lo_i]) * kUnit;
+                r.nc = min(r.cb + (uint32_t)kUnit, sSpanHi[lo_i]) - r.cb;
+                if ((uint32_t)lane < r.nc) r.h = __ldg(&p.hdr[r.cb + lane]);
             }
-            l = lo_i;
-            const uint32_t cb = sSpanLo[l] + (unit - sUoffL[l]) * kUnit;
-            const uint32_t ce = min(cb + (uint32_t)kUnit, sSpanHi[l]);
-            const Item t = sItems[l];
-            const int32_t H = sHpart[l];
-            const uint32_t L = sLpart[l];
+            return r;
+        };
+        LUnit cur = next_unit();
+        while (cur.unit < n_units) {
+            const Item t = sItems[cur.l];
+            uint32_t lo_w[kUnit], hi_w[kUnit];
+#pragma unroll
+            for (int q = 0; q < kUnit; ++q) {
+                lo_w[q] = 0u;
+                hi_w[q] = 0u;
+                if ((uint32_t)q >= cur.nc) break;
+                const uint32_t meta = __shfl_sync(FULL, cur.h.y, q);
+                const uint32_t n = (meta & 31u) + 1u, bw = (meta >> 5) & 31u;
+                if (lane >= 1 && (uint32_t)lane < n && bw) {
+                    const uint32_t bit = (uint32_t)(lane - 1) * bw;
+                    const uint32_t wi = t.kwb + (meta >> 10) + (bit >> 5);
+                    lo_w[q] = __ldg(&p.payload[wi]);
+                    hi_w[q] = __ldg(&p.payload[wi + 1]);
+                }
+            }
+            const LUnit nxt = next_unit();             // overlaps this unit's payload round trip
+            const int32_t H = sHpart[cur.l];
+            const uint32_t L = sLpart[cur.l];
             int32_t* ah = accH + (size_t)t.b * R;
             uint32_t* al = accL + (size_t)t.b * R;
-            decode_unit16(p.hdr, p.payload, t.kwb, cb, ce, lane, [&](uint32_t id) {
-                if (id >= (uint32_t)r0 && id < (uint32_t)r1) {
-                    atomicAdd(&ah[id - (uint32_t)r0], H);
-                    atomicAdd(&al[id - (uint32_t)r0], L);
+#pragma unroll
+            for (int q = 0; q < kUnit; ++q) {
+                if ((uint32_t)q >= cur.nc) break;
+                const uint32_t meta = __shfl_sync(FULL, cur.h.y, q);
+                const uint32_t first = __shfl_sync(FULL, cur.h.x, q);
+                const uint32_t n = (meta & 31u) + 1u, bw = (meta >> 5) & 31u;
+                uint32_t g;
+                if (lane == 0) {
+                    g = first;
+                } else if ((uint32_t)lane < n) {
+                    uint32_t v = 0u;
+                    if (bw) {
+                        const uint32_t bit = (uint32_t)(lane - 1) * bw;
+                        v = (uint32_t)(((((uint64_t)hi_w[q]) << 32) | lo_w[q]) >> (bit & 31u)) & ((1u << bw) - 1u);
+                    }
+                    g = v + 1u;
+                } else {
+                    g = 0u;
                 }
-            });
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t tt = __shfl_up_sync(FULL, g, o);
+                    if (lane >= o) g += tt;
+                }
+                if ((uint32_t)lane < n && g >= (uint32_t)r0 && g < (uint32_t)r1) {
+                    atomicAdd(&ah[g - (uint32_t)r0], H);
+                    atomicAdd(&al[g - (uint32_t)r0], L);
+                }
+            }
+            cur = nxt;
         }
         EBR_STAMP(2);
     } else {
