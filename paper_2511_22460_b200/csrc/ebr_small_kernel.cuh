@@ -196,6 +196,29 @@ __device__ __forceinline__ uint32_t group_exclusive_scan(uint32_t v, uint32_t* s
     return before + incl - v;
 }
 
+// The rare single-CTA selection (threshold bin denser than the staging buffer), kept out of line so
+// its code does not sit in the common path's instruction stream.
+static __device__ __noinline__ void small_fallback_select(const SmallParams& p, int b, int64_t n,
+                                                   const uint64_t* cb, const uint32_t* sOff,
+                                                   uint64_t* sKeys, uint32_t* sScalar) {
+    const int K = p.K, nr = p.n_ranges, Rr = p.R;
+    const int P = pow2ceil_i(K);
+    uint64_t* sbuf = sKeys;
+    uint32_t* shist = reinterpret_cast<uint32_t*>(sbuf + P);
+    auto get = [cb, sOff, nr, Rr](int64_t i) {
+        int lo = 0, hi = nr - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if ((int64_t)sOff[mid] <= i) lo = mid; else hi = mid - 1;
+        }
+        return __ldcg(&cb[(int64_t)lo * Rr + (i - sOff[lo])]);
+    };
+    const int nsel = cta_select_topk(get, n, K, sbuf, nullptr, 0, shist, sScalar);
+    cta_write_topk(sbuf, nsel, K, p.out_ids ? p.out_ids + (size_t)b * K : nullptr,
+                   p.out_scores ? p.out_scores + (size_t)b * K : nullptr,
+                   p.out_keys ? p.out_keys + (size_t)b * K : nullptr);
+}
+
 template <typename T, int NB, int LPR, int VPL>
 __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p) {
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -791,24 +814,8 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
             const int K = p.K;
             if (n > kcap) {
                 // rare (very dense threshold bin): one CTA selects straight from global memory
-                if ((int)blockIdx.x == b % (int)gridDim.x) {
-                    const int nr = p.n_ranges, Rr = R;
-                    const int P = pow2ceil_i(K);
-                    uint64_t* sbuf = sKeys;
-                    uint32_t* shist = reinterpret_cast<uint32_t*>(sbuf + P);
-                    auto get = [cb, sOff, nr, Rr](int64_t i) {
-                        int lo = 0, hi = nr - 1;
-                        while (lo < hi) {
-                            const int mid = (lo + hi + 1) >> 1;
-                            if ((int64_t)sOff[mid] <= i) lo = mid; else hi = mid - 1;
-                        }
-                        return __ldcg(&cb[(int64_t)lo * Rr + (i - sOff[lo])]);
-                    };
-                    const int nsel = cta_select_topk(get, n, K, sbuf, nullptr, 0, shist, sScalar);
-                    cta_write_topk(sbuf, nsel, K, p.out_ids ? p.out_ids + (size_t)b * K : nullptr,
-                                   p.out_scores ? p.out_scores + (size_t)b * K : nullptr,
-                                   p.out_keys ? p.out_keys + (size_t)b * K : nullptr);
-                }
+                if ((int)blockIdx.x == b % (int)gridDim.x)
+                    small_fallback_select(p, b, n, cb, sOff, sKeys, sScalar);
                 __syncthreads();
                 continue;
             }
