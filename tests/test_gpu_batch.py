@@ -85,3 +85,22 @@ def test_batch_workspace_reuse_and_keys(ebr):
         ebr.score_topk(idx, emb, feat, x, 80, ids, sc, ws)
         torch.cuda.synchronize()
         assert check_all(o, u2, ids.cpu().numpy(), sc.cpu().numpy(), 80, "exact") == 0
+
+
+@pytest.mark.parametrize("cfg", ["C3", "C4"])
+def test_full_size_sampled_users(ebr, cfg):
+    """BASELINE.json configs 3 and 4 at full size and batch, in bench.py's launch configuration
+    (one call for the whole batch); a few users are checked against the oracle's full scoring
+    and brute-force sort (the oracle finishes one 10M-ad user in seconds)."""
+    c = synth.CONFIGS[cfg]
+    inv, users = synth.make_config(cfg, mode="real")
+    idx = ebr.Index.of(inv)
+    (ids, sc), _ = run(ebr, idx, users, c.k)
+    o = oracle.Oracle.of(inv)
+    sel = [0, users.batch // 2, users.batch - 1]
+    sub = synth.Users(len(sel), users.slots, users.user_emb[sel], users.user_feat[sel], users.user_x[sel])
+    check_all(o, sub, ids[sel], sc[sel], c.k, "real")
+    # every user: ids unique, inside the inventory, scores sorted
+    assert ((ids >= 0) & (ids < inv.n_ads)).all()
+    assert all(len(np.unique(r)) == c.k for r in ids)
+    assert (np.diff(sc, axis=1) <= 0).all()
