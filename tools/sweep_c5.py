@@ -38,5 +38,5 @@ for B in Bs:
         m = float(np.median(ms))
         print(json.dumps({"B": B, "K": K, "ms": m, "users_per_s": B / m * 1e3,
                           "ads_scored_per_s": B * inv.n_ads / m * 1e3,
-                          "path": "tensor-core batched" if idx.query_launches(B, users.slots, K) > (B + 7) // 8 else "latency"}), flush=True)
+                          "path": "tensor-core batched" if idx.query_launches(B, users.slots, K) == 1 + ((B + 127) // 128) * 7 else "latency"}), flush=True)
         del ws
