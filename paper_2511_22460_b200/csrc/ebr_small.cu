@@ -26,7 +26,7 @@ kern_t pick_kernel(int nb, int lpr, int vpl) {
 }
 
 struct SmallLayout {
-    size_t off_header, off_hist, off_count, off_scores, off_wide, off_cand, total;
+    size_t off_header, off_hist, off_count, off_scores, off_cand, total;
 };
 
 SmallLayout small_layout(const ebr_index* idx, int B) {
@@ -37,7 +37,6 @@ SmallLayout small_layout(const ebr_index* idx, int B) {
     L.off_hist = o;   o = al(o + (size_t)B * kHistBins * 4);
     L.off_count = o;  o = al(o + (size_t)B * (idx->sm_count + 1) * 4);   // [B][n_ranges]
     L.off_scores = o; o = al(o + (size_t)B * idx->n_pad * 4);
-    L.off_wide = o;   o = al(o + (size_t)B * idx->n_pad * 4);
     L.off_cand = o;   o = al(o + (size_t)B * idx->n_pad * 8);
     L.total = o;
     return L;
@@ -76,20 +75,20 @@ ebr_status run_small(const QueryArgs& q, int b0, int B) {
     int64_t R = (idx->n_ads + sms - 1) / sms;
     R = std::max<int64_t>(32, (R + 31) & ~(int64_t)31);
     const int n_ranges = (int)((idx->n_ads + R - 1) / R);
-    const size_t plan_bytes = (size_t)B * kHistBins * 4 + (size_t)items_cap * sizeof(Item) + 8 +
-                              (size_t)(items_cap + 1) * 8;
+    // per item: the Item + span lo/hi + unit offset + fixed-point parts
+    const size_t plan_bytes = (size_t)B * kHistBins * 4 + (size_t)items_cap * (sizeof(Item) + 20) + 64;
     // phase E: candidate staging (>= 16k keys) and the rare single-CTA fallback select
     const size_t sel_min = std::max((size_t)(n_ranges + 2) * 4 + 128 * 1024,
                                     (size_t)(n_ranges + 2) * 4 + (size_t)pow2ceil_i(q.k) * 8 + kSelBins * 4 + 64);
     const size_t cap = 227 * 1024;
-    // keep the CTA's deep/fused scores in shared memory when they fit
-    const size_t res_bytes = (size_t)B * R * 4;
-    const bool resident = plan_bytes + res_bytes <= cap - 8 * 1024;
-    // local wide accumulation: spans/unit offsets/fixed-point parts per item + 2 x [B][R] words
-    const size_t local_bytes = (size_t)items_cap * 20 + 32 + (size_t)B * R * 8;
-    static const bool no_local = getenv("EBR_NO_LOCAL_WIDE") != nullptr;
-    const bool local_wide = !no_local && resident && B <= 2 && plan_bytes + res_bytes + local_bytes <= cap - 8 * 1024;
-    const size_t p1 = plan_bytes + (resident ? res_bytes : 0) + (local_wide ? local_bytes : 0);
+    if (plan_bytes + 8 * 1024 + (size_t)B * 32 * 12 > cap)
+        return set_error(EBR_EUNSUPPORTED, "latency path: %d user slots need too much shared memory", items_cap);
+    // tile: as many ads as fit (deep fp32 + two 32-bit accumulator words per user and ad)
+    int64_t T = (int64_t)((cap - 8 * 1024 - plan_bytes) / ((size_t)B * 12));
+    T = std::min<int64_t>(T, 16384) & ~(int64_t)31;
+    const bool resident = T >= R;
+    if (resident) T = R;
+    const size_t p1 = plan_bytes + (size_t)B * T * 12;
     const size_t smem = std::max(p1, sel_min);
     if (smem > cap)
         return set_error(EBR_EUNSUPPORTED, "latency path: %d user slots / k=%d need %zu B of shared memory",
@@ -122,7 +121,6 @@ ebr_status run_small(const QueryArgs& q, int b0, int B) {
     p.ghist = reinterpret_cast<uint32_t*>(ws + L.off_hist);
     p.cand_count = reinterpret_cast<uint32_t*>(ws + L.off_count);
     p.scores = reinterpret_cast<float*>(ws + L.off_scores);
-    p.wide = reinterpret_cast<float*>(ws + L.off_wide);
     p.cand = reinterpret_cast<uint64_t*>(ws + L.off_cand);
     p.out_ids = q.out_ids ? q.out_ids + (size_t)b0 * q.k : nullptr;
     p.out_scores = q.out_scores ? q.out_scores + (size_t)b0 * q.k : nullptr;
@@ -130,7 +128,7 @@ ebr_status run_small(const QueryArgs& q, int b0, int B) {
     p.R = (int32_t)R;
     p.n_ranges = n_ranges;
     p.resident = resident ? 1 : 0;
-    p.local_wide = local_wide ? 1 : 0;
+    p.T = (int32_t)T;
     p.chunk_last = idx->chunk_last;
     p.items_cap = items_cap;
     p.smem_bytes = (int32_t)smem;

@@ -5,21 +5,22 @@
 //               {key i = base_f + v, w~ = fl32(w_i x_i), the key's chunk span}, and an
 //               exclusive scan of the items' chunk counts gives a flat chunk space
 //               (Alg. 2 l.352-353 "k_length", "ExclusiveScan").
-//   B  two warp roles run concurrently:
-//       deep      (10 warps) A4: stream this CTA's contiguous rows of A once from HBM with 16-byte
-//                 non-allocating loads, 8 in flight per lane (measured: plain vector loads reach
-//                 the HBM peak, a bulk-copy ring at 1 CTA/SM does not -- tools/mb_stream.cu),
-//                 dot with the B user vectors held in registers (Eq. 1, fp32 FFMA), write the
-//                 deep score to an L2-resident scratch; then join the wide queue;
-//       wide      (6 warps) A2+A3: claim 16-chunk units of the flat chunk space from a global
-//                 queue (the paper's LoadBalance, Alg. 2 l.354: every chunk but a key's
-//                 last holds 32 postings, so units cost the same), fetch the 16 headers and all
-//                 payload words in two memory round trips, unpack + warp-scan each chunk and add
-//                 w~ with L2 reductions red.global.add.f32 into a per-(user, ad) fp32 array
-//                 (Alg. 2 l.358 "AtomicAdd(scores[..], w)").
-//   -- grid sync --
-//   C  A5 fuse: s = deep + wide (-0 -> +0), re-zero the wide array for the next call, per-user
-//      2048-bin histogram of ord(s)'s top 11 bits (warp-aggregated shared atomics).
+//   B  the CTA's contiguous ad range in tiles of T ads (one tile when it fits shared memory);
+//      per tile two warp roles run concurrently:
+//       deep      (10 warps) A4: stream the tile's rows of A once from HBM with 16-byte
+//                 non-allocating loads, 16 rows in flight per lane group (measured: plain vector
+//                 loads reach the HBM peak, a bulk-copy ring at 1 CTA/SM does not --
+//                 tools/mb_stream.cu), fp32 FFMA with the user vectors in registers and a
+//                 transposed butterfly reduction; deep scores land in shared memory;
+//       wide      (6 warps) A2+A3: the exact chunk span of every item inside the tile (galloping
+//                 search on chunk_last / chunk first ids), an exclusive scan of 16-chunk unit counts
+//                 and a shared unit counter (the paper's ExclusiveScan + LoadBalance, Alg. 2
+//                 l.353-354: every chunk but a key's last holds 32 postings, so units cost the
+//                 same), software-pipelined decode, and w~ accumulated in shared memory as 48-bit
+//                 fixed point over two native 32-bit atomics (Alg. 2 l.358 AtomicAdd, on chip).
+//      The deep warps join the wide units when their rows are done.
+//   C  A5 fuse the tile: s = deep + wide (-0 -> +0), per-user 2048-bin histogram of ord(s)'s top
+//      11 bits; s stays in shared memory (one tile) or goes to an L2 scratch (several tiles).
 //   -- grid sync --
 //   D  A6a each CTA finds, per user, the bin holding the K-th largest score; A6b every (user, ad)
 //      in a bin >= it is appended as a 64-bit key kappa (warp-aggregated global atomics).
@@ -74,13 +75,12 @@ struct SmallParams {
     const int32_t* user_feat;   // [B][F][S]
     const float* user_x;
     // workspace
-    uint32_t* header;           // [0] magic, [1] error flags, [2] wide queue head, then stamps
+    uint32_t* header;           // [0] magic, [1] error flags, then phase stamps
     unsigned long long* timers; // optional phase stamps (EBR_PHASE_TIMERS=1), else null
     uint32_t magic;
     uint32_t* ghist;            // [B][kHistBins]
     uint32_t* cand_count;       // [B][n_ranges] candidates per CTA segment
     float* scores;              // [B][n_pad]  deep, then fused score
-    float* wide;                // [B][n_pad]  wide accumulator (zero between calls)
     uint64_t* cand;             // [B][n_pad]  CTA r's segment starts at r * R
     // outputs
     int32_t* out_ids;           // [B][K] (already offset to this launch's first user)
@@ -92,8 +92,8 @@ struct SmallParams {
     int32_t items_cap;          // >= B * F * S
     int32_t smem_bytes;
     int32_t diag;               // EBR_DIAG bits (diagnostics only): 1 = skip wide, 2 = skip deep
-    int32_t resident;           // deep / fused scores of the CTA's range kept in shared memory
-    int32_t local_wide;         // wide term accumulated per CTA range in shared memory (B <= 2)
+    int32_t resident;           // one tile covers the CTA's range: fused scores stay in shared memory
+    int32_t T;                  // ads per tile (shared-memory accumulation granule)
     const uint32_t* chunk_last; // [C] last id of each posting chunk (exact per-range spans)
 };
 
@@ -219,28 +219,24 @@ static __device__ __noinline__ void small_fallback_select(const SmallParams& p, 
                    p.out_keys ? p.out_keys + (size_t)b * K : nullptr);
 }
 
-template <typename T, int NB, int LPR, int VPL>
+template <typename T_, int NB, int LPR, int VPL>
 __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p) {
     extern __shared__ __align__(1024) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int B = p.B, R = p.R;
     const cg::grid_group grid = cg::this_grid();
     // ---- shared-memory carve-up ----
-    float* sS = reinterpret_cast<float*>(smem);                                   // [B][R] if resident
-    uint32_t* sHist = reinterpret_cast<uint32_t*>(sS + (p.resident ? (size_t)B * R : 0));  // [B][bins]
+    const int T = p.T;                                                            // ads per tile
+    float* sS = reinterpret_cast<float*>(smem);                                   // [B][T] deep, then fused
+    int32_t* accH = reinterpret_cast<int32_t*>(sS + (size_t)B * T);              // [B][T] wide, high parts
+    uint32_t* accL = reinterpret_cast<uint32_t*>(accH + (size_t)B * T);          // [B][T] wide, low 16 bits
+    uint32_t* sHist = accL + (size_t)B * T;                                       // [B][bins]
     Item* sItems = reinterpret_cast<Item*>(sHist + (size_t)B * kHistBins);        // [items_cap]
-    uint64_t* sChunkOff = reinterpret_cast<uint64_t*>(
-        (reinterpret_cast<uintptr_t>(sItems + p.items_cap) + 7) & ~(uintptr_t)7);  // [items_cap + 1]
-    // local-wide mode: per-item chunk span inside this CTA's range, unit offsets, fixed-point
-    // parts, and the 48-bit accumulators (high parts, low 16-bit parts) for [B][R] ads
-    uint32_t* sSpanLo = reinterpret_cast<uint32_t*>(sChunkOff + p.items_cap + 1);
-    uint32_t* sSpanHi = sSpanLo + p.items_cap;
-    uint32_t* sUoffL = sSpanHi + p.items_cap;                                    // [items_cap + 1]
-    int32_t* sHpart = reinterpret_cast<int32_t*>(sUoffL + p.items_cap + 1);
-    uint32_t* sLpart = reinterpret_cast<uint32_t*>(sHpart + p.items_cap);
-    int32_t* accH = reinterpret_cast<int32_t*>(
-        (reinterpret_cast<uintptr_t>(sLpart + p.items_cap) + 15) & ~(uintptr_t)15);  // [B][R]
-    uint32_t* accL = reinterpret_cast<uint32_t*>(accH + (p.local_wide ? (size_t)B * R : 0));
+    uint32_t* sSpanLo = reinterpret_cast<uint32_t*>(sItems + p.items_cap);        // [items_cap]
+    uint32_t* sSpanHi = sSpanLo + p.items_cap;                                    // [items_cap]
+    uint32_t* sUoffL = sSpanHi + p.items_cap;                                     // [items_cap + 1]
+    int32_t* sHpart = reinterpret_cast<int32_t*>(sUoffL + p.items_cap + 1);      // [items_cap]
+    uint32_t* sLpart = reinterpret_cast<uint32_t*>(sHpart + p.items_cap);        // [items_cap]
     __shared__ uint32_t sScan[40], sScalar[8], sNItems, sUnitCtr, sNUnits;
     __shared__ uint32_t sBinStar[kSmallMaxB], sSeg[kSmallMaxB];
     __shared__ int sInit, sShiftB[kSmallMaxB];
@@ -249,28 +245,33 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
     const int64_t r0 = (int64_t)blockIdx.x * R;
     const int64_t r1 = has_range ? ((r0 + R < p.n_ads) ? r0 + R : p.n_ads) : r0;
     const int rn = (int)(r1 - r0);
+    const bool resident = p.resident;                 // one tile covers the range: keep s in smem
 
     if (p.timers && blockIdx.x == 0 && tid == 0) p.timers[0] = gtimer();
     // ---- first use of this workspace: zero it (uniform decision across the grid) ----
     if (tid == 0) { sInit = (__ldcg(&p.header[0]) != p.magic); sUnitCtr = 0; sNUnits = 0; }
     for (int i = tid; i < B * kHistBins; i += kThreads) sHist[i] = 0;
-    if (p.local_wide)
-        for (int i = tid; i < B * R; i += kThreads) { accH[i] = 0; accL[i] = 0u; }
+    for (int i = tid; i < B * T; i += kThreads) { accH[i] = 0; accL[i] = 0u; }
     if (tid < kSmallMaxB) sSeg[tid] = 0;
     __syncthreads();
     if (sInit) {   // ebr_workspace_init was not called: do it here
-        const size_t nw = (size_t)kSmallMaxB * p.n_pad;
-        for (size_t i = (size_t)blockIdx.x * kThreads + tid; i < nw; i += (size_t)gridDim.x * kThreads) p.wide[i] = 0.f;
         if (blockIdx.x == 0) {
             for (int i = tid; i < kSmallMaxB * kHistBins; i += kThreads) p.ghist[i] = 0;
-            if (tid == 0) { p.header[1] = 0; p.header[2] = 0; }
+            if (tid == 0) p.header[1] = 0;
         }
         grid.sync();
     }
 
+    using V = Vec<T_>;
+    constexpr int E = V::E;
+    constexpr int lpr = LPR;
+    const int sub = lane / lpr, li = lane % lpr;
+    constexpr int rpw = 32 / lpr;
+    float u[NB][VPL][E];
+    const int gt = tid - kDeepWarps * 32;
+    constexpr int NT = kWideWarps * 32;
     if (warp >= kDeepWarps) {
         // ---- A: plan by the wide warps (deterministic item order; named barrier 1) ----
-        const int gt = tid - kDeepWarps * 32, NT = kWideWarps * 32;
         const int nslot = B * p.n_fields * p.slots;
         const int per = (nslot + NT - 1) / NT;
         const int s0 = min(nslot, gt * per), s1 = min(nslot, s0 + per);
@@ -340,66 +341,28 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
         }
         if (gt == 0) sNItems = total;
         nbar_sync(1, NT);
-        const int n_items = (int)sNItems;
-        const int per2 = (n_items + NT - 1) / NT;
-        const int i0 = min(n_items, gt * per2), i1 = min(n_items, i0 + per2);
-        uint32_t loc = 0;
-        for (int i = i0; i < i1; ++i) loc += sItems[i].c1 - sItems[i].c0;
-        uint32_t tot2;
-        uint64_t acc = group_exclusive_scan(loc, sScan, &tot2, gt, kWideWarps, 1);
-        for (int i = i0; i < i1; ++i) { sChunkOff[i] = acc; acc += sItems[i].c1 - sItems[i].c0; }
-        if (gt == 0) sChunkOff[n_items] = tot2;
-        nbar_sync(1, NT);                  // the wide warps read each other's offsets next
-        if (p.local_wide) {
-            // per-user fixed-point scale: bound = (#items) * max|w~| >= any sum of hits
-            if (gt < B) {
-                float mx = 0.f;
-                int cnt_b = 0;
-                for (int i = 0; i < n_items; ++i)
-                    if ((int)sItems[i].b == gt) { mx = fmaxf(mx, fabsf(sItems[i].w)); ++cnt_b; }
-                int e = 0;
-                frexpf(mx * (float)cnt_b * 1.0001f + 1e-30f, &e);
-                sShiftB[gt] = 46 - e;
-            }
-            nbar_sync(1, NT);
-            // exact chunk span of every item inside [r0, r1): first chunk whose last id >= r0,
-            // first chunk whose first id >= r1 (binary searches, one lane per item)
-            uint32_t my_units = 0;
-            const int per3 = (n_items + NT - 1) / NT;
-            const int j0 = min(n_items, gt * per3), j1 = min(n_items, j0 + per3);
-            for (int i = j0; i < j1; ++i) {
-                const Item t = sItems[i];
-                const double frac0 = (double)r0 / (double)p.n_ads, frac1 = (double)r1 / (double)p.n_ads;
-                const uint32_t nch = t.c1 - t.c0;
-                const uint32_t lo = gallop_lower_bound([&](uint32_t c) { return __ldg(&p.chunk_last[c]); },
-                                                       t.c0, t.c1, (uint32_t)r0, t.c0 + (uint32_t)(frac0 * nch));
-                const uint32_t lo2 = gallop_lower_bound([&](uint32_t c) { return __ldg(&p.hdr[c]).x; },
-                                                        lo, t.c1, (uint32_t)r1, t.c0 + (uint32_t)(frac1 * nch));
-                sSpanLo[i] = lo;
-                sSpanHi[i] = lo2;
-                const uint32_t nu_i = lo2 > lo ? (lo2 - lo + kUnit - 1) / kUnit : 0u;
-                sUoffL[i] = nu_i;                      // scanned below
-                my_units += nu_i;
-                const long long F = __double2ll_rn(ldexp((double)t.w, sShiftB[t.b]));
-                sHpart[i] = (int32_t)(F >> 16);
-                sLpart[i] = (uint32_t)(F & 0xFFFF);
-            }
-            uint32_t tot_u;
-            uint32_t pre = group_exclusive_scan(my_units, sScan, &tot_u, gt, kWideWarps, 1);
-            for (int i = j0; i < j1; ++i) { const uint32_t c = sUoffL[i]; sUoffL[i] = pre; pre += c; }
-            if (gt == 0) { sUoffL[n_items] = tot_u; sNUnits = tot_u; }
-            nbar_sync(1, NT);
+        // per-user fixed-point scale: bound = (#items) * max|w~| >= any sum of one ad's hits
+        if (gt < B) {
+            const int n_items = (int)sNItems;
+            float mx = 0.f;
+            int cnt_b = 0;
+            for (int i = 0; i < n_items; ++i)
+                if ((int)sItems[i].b == gt) { mx = fmaxf(mx, fabsf(sItems[i].w)); ++cnt_b; }
+            int e = 0;
+            frexpf(mx * (float)cnt_b * 1.0001f + 1e-30f, &e);
+            sShiftB[gt] = 46 - e;
         }
-        nbar_arrive(2, kThreads);          // publish the plan to the deep warps (barrier 2)
+        nbar_sync(1, NT);
+        for (int i = gt; i < (int)sNItems; i += NT) {
+            const Item t = sItems[i];
+            const long long F = __double2ll_rn(ldexp((double)t.w, sShiftB[t.b]));
+            sHpart[i] = (int32_t)(F >> 16);
+            sLpart[i] = (uint32_t)(F & 0xFFFF);
+            sSpanHi[i] = t.c0;                 // search start for the first tile
+        }
+        nbar_sync(1, NT);
         EBR_STAMP(1);
-    } else if (!(p.diag & 2)) {
-        // ---- B (deep): stream this CTA's rows of A, 8 x 16-byte loads in flight per lane ----
-        using V = Vec<T>;
-        constexpr int E = V::E;
-        constexpr int lpr = LPR;
-        const int sub = lane / lpr, li = lane % lpr;
-        constexpr int rpw = 32 / lpr;
-        float u[NB][VPL][E];
+    } else {
 #pragma unroll
         for (int b = 0; b < NB; ++b)
 #pragma unroll
@@ -409,318 +372,234 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
                     const int j = (li + v * lpr) * E + e;
                     u[b][v][e] = (b < B && j < p.d) ? V::elem(p.U, (int64_t)b * p.d + j) : 0.f;
                 }
-        const char* Abase = reinterpret_cast<const char*>(p.A);
-        if constexpr (NB == 1 && VPL == 1 && LPR >= 4 && LPR <= 16) {
-            // 16 consecutive rows per lane group, 16 loads in flight per lane; transposed
-            // reduction: log2(LPR) butterfly steps each halving the live partials, so lane li ends
-            // with the sums of rows li*(16/LPR) .. +16/LPR-1 (15 shuffles per 16 rows for LPR=16)
-            constexpr int U = 16;
-            constexpr int OUT = U / LPR;
-            constexpr int64_t wrows = (int64_t)rpw * U;                  // rows per warp iteration
-            for (int64_t base = r0 + (int64_t)warp * wrows; base < r1; base += (int64_t)kDeepWarps * wrows) {
-                const int64_t g0 = base + (int64_t)sub * U;              // this lane group's first row
-                uint4 av[U];
-#pragma unroll
-                for (int q = 0; q < U; ++q)
-                    av[q] = (g0 + q < r1) ? ldg_stream(Abase + (g0 + q) * p.row_bytes + (int64_t)li * 16)
-                                          : make_uint4(0, 0, 0, 0);
-                float v[U];
-#pragma unroll
-                for (int q = 0; q < U; ++q) {
-                    float a[E];
-                    V::unpack(av[q], a);
-                    float acc = 0.f;
-#pragma unroll
-                    for (int e = 0; e < E; ++e) acc = fmaf(a[e], u[0][0][e], acc);
-                    v[q] = acc;
-                }
-                int live = U;
-#pragma unroll
-                for (int sft = LPR / 2; sft > 0; sft >>= 1) {
-                    const bool up = (li & sft) != 0;
-                    const int half = live / 2;
-#pragma unroll
-                    for (int j = 0; j < U / 2; ++j) {
-                        if (j < half) {
-                            const float send = up ? v[j] : v[j + half];
-                            const float keep = up ? v[j + half] : v[j];
-                            v[j] = keep + __shfl_xor_sync(FULL, send, sft);
-                        }
-                    }
-                    live = half;
-                }
-                const int64_t row0 = g0 + (int64_t)li * OUT;
-#pragma unroll
-                for (int j = 0; j < OUT; ++j) {
-                    const int64_t row = row0 + j;
-                    if (row < r1) {
-                        if (p.resident) sS[row - r0] = v[j];
-                        else __stcg(&p.scores[row], v[j]);
-                    }
-                }
-            }
-        } else {
-        constexpr int64_t step = (int64_t)kDeepWarps * rpw * kUnroll;
-        for (int64_t base = r0 + (int64_t)warp * rpw; base < r1; base += step) {
-            uint4 av[kUnroll][VPL];
-#pragma unroll
-            for (int q = 0; q < kUnroll; ++q) {
-                const int64_t row = base + (int64_t)q * kDeepWarps * rpw + sub;
-#pragma unroll
-                for (int v = 0; v < VPL; ++v) {
-                    if (row < r1)
-                        av[q][v] = ldg_stream(Abase + row * p.row_bytes + (int64_t)(li + v * lpr) * 16);
-                    else
-                        av[q][v] = make_uint4(0, 0, 0, 0);
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < kUnroll; ++q) {
-                float acc[NB];
-#pragma unroll
-                for (int b = 0; b < NB; ++b) acc[b] = 0.f;
-#pragma unroll
-                for (int v = 0; v < VPL; ++v) {
-                    float a[E];
-                    V::unpack(av[q][v], a);
-#pragma unroll
-                    for (int b = 0; b < NB; ++b)
-#pragma unroll
-                        for (int e = 0; e < E; ++e) acc[b] = fmaf(a[e], u[b][v][e], acc[b]);
-                }
-#pragma unroll
-                for (int o = lpr / 2; o > 0; o >>= 1) {
-#pragma unroll
-                    for (int b = 0; b < NB; ++b) acc[b] += __shfl_xor_sync(FULL, acc[b], o);
-                }
-                const int64_t row = base + (int64_t)q * kDeepWarps * rpw + sub;
-                if (li == 0 && row < r1) {
-#pragma unroll
-                    for (int b = 0; b < NB; ++b)
-                        if (b < B) {
-                            if (p.resident) sS[(size_t)b * R + (row - r0)] = acc[b];
-                            else __stcg(&p.scores[(size_t)b * p.n_pad + row], acc[b]);
-                        }
-                }
-            }
-        }
-        }
-        EBR_STAMP(3);
     }
-    if (warp < kDeepWarps) nbar_sync(2, kThreads);   // deep warps wait for the plan before helping
-    if (p.local_wide) {
-        // ---- B (wide, local): 16-chunk units of this CTA's item spans, claimed from a shared
-        // counter (ExclusiveScan + LoadBalance, Alg. 2 l.353-354), accumulated in shared memory
-        // as 48-bit fixed point over two native 32-bit atomics (exact for dyadic inputs) ----
-        const uint32_t n_units = (p.diag & 1) ? 0u : sNUnits;
-        const int n_items = (int)sNItems;
-        struct LUnit { uint32_t unit; int l; uint32_t cb, nc; uint2 h; };
-        auto next_unit = [&]() -> LUnit {          // claim a unit and start its header loads
-            LUnit r;
-            uint32_t unit = 0;
-            if (lane == 0) unit = atomicAdd(&sUnitCtr, 1u);
-            r.unit = __shfl_sync(FULL, unit, 0);
-            r.l = 0; r.cb = 0; r.nc = 0; r.h = make_uint2(0u, 0u);
-            if (r.unit < n_units) {
-                int lo_i = 0, hi_i = n_items - 1;  // item = last with sUoffL <= unit
-                while (lo_i < hi_i) {
-                    const int mid = (lo_i + hi_i + 1) >> 1;
-                    if (sUoffL[mid] <= r.unit) lo_i = mid; else hi_i = mid - 1;
-                }
-                r.l = lo_i;
-                r.cb = sSpanLo[lo_i] + (r.unit - sUoffL[lo_i]) * kUnit;
-                r.nc = min(r.cb + (uint32_t)kUnit, sSpanHi[lo_i]) - r.cb;
-                if ((uint32_t)lane < r.nc) r.h = __ldg(&p.hdr[r.cb + lane]);
-            }
-            return r;
-        };
-        LUnit cur = next_unit();
-        while (cur.unit < n_units) {
-            const Item t = sItems[cur.l];
-            uint32_t lo_w[kUnit], hi_w[kUnit];
-#pragma unroll
-            for (int q = 0; q < kUnit; ++q) {
-                lo_w[q] = 0u;
-                hi_w[q] = 0u;
-                if ((uint32_t)q >= cur.nc) break;
-                const uint32_t meta = __shfl_sync(FULL, cur.h.y, q);
-                const uint32_t n = (meta & 31u) + 1u, bw = (meta >> 5) & 31u;
-                if (lane >= 1 && (uint32_t)lane < n && bw) {
-                    const uint32_t bit = (uint32_t)(lane - 1) * bw;
-                    const uint32_t wi = t.kwb + (meta >> 10) + (bit >> 5);
-                    lo_w[q] = __ldg(&p.payload[wi]);
-                    hi_w[q] = __ldg(&p.payload[wi + 1]);
-                }
-            }
-            const LUnit nxt = next_unit();             // overlaps this unit's payload round trip
-            const int32_t H = sHpart[cur.l];
-            const uint32_t L = sLpart[cur.l];
-            int32_t* ah = accH + (size_t)t.b * R;
-            uint32_t* al = accL + (size_t)t.b * R;
-#pragma unroll
-            for (int q = 0; q < kUnit; ++q) {
-                if ((uint32_t)q >= cur.nc) break;
-                const uint32_t meta = __shfl_sync(FULL, cur.h.y, q);
-                const uint32_t first = __shfl_sync(FULL, cur.h.x, q);
-                const uint32_t n = (meta & 31u) + 1u, bw = (meta >> 5) & 31u;
-                uint32_t g;
-                if (lane == 0) {
-                    g = first;
-                } else if ((uint32_t)lane < n) {
-                    uint32_t v = 0u;
-                    if (bw) {
-                        const uint32_t bit = (uint32_t)(lane - 1) * bw;
-                        v = (uint32_t)(((((uint64_t)hi_w[q]) << 32) | lo_w[q]) >> (bit & 31u)) & ((1u << bw) - 1u);
-                    }
-                    g = v + 1u;
-                } else {
-                    g = 0u;
-                }
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t tt = __shfl_up_sync(FULL, g, o);
-                    if (lane >= o) g += tt;
-                }
-                if ((uint32_t)lane < n && g >= (uint32_t)r0 && g < (uint32_t)r1) {
-                    atomicAdd(&ah[g - (uint32_t)r0], H);
-                    atomicAdd(&al[g - (uint32_t)r0], L);
-                }
-            }
-            cur = nxt;
-        }
-        EBR_STAMP(2);
-    } else {
-        // ---- B (wide): 16-chunk units of the flat chunk space from a global queue ----
-        // (the paper's LoadBalance, Alg. 2 l.354); units may straddle items.  Software-pipelined:
-        // the next unit is claimed and its headers fetched while this unit's payload is in flight.
-        const int n_items = (int)sNItems;
-        const uint64_t Ttot = sChunkOff[n_items];
-        const uint64_t n_units = (p.diag & 1) ? 0 : (Ttot + kUnit - 1) / kUnit;
-        struct UnitHdr { uint2 h; uint32_t kwb, b; float w; };
-        auto claim = [&]() -> uint32_t {
-            uint32_t unit = 0;
-            if (lane == 0) unit = atomicAdd(&p.header[2], 1u);
-            return __shfl_sync(FULL, unit, 0);
-        };
-        auto fetch = [&](uint32_t unit) -> UnitHdr {
-            UnitHdr r{make_uint2(0u, 0u), 0u, 0u, 0.f};
-            const uint64_t f = (uint64_t)unit * kUnit + (lane & (kUnit - 1));
-            if (unit < n_units && lane < kUnit && f < Ttot) {
-                int lo = 0, hi = n_items - 1;     // item = last it with sChunkOff[it] <= f
-                while (lo < hi) {
-                    const int mid = (lo + hi + 1) >> 1;
-                    if (sChunkOff[mid] <= f) lo = mid; else hi = mid - 1;
-                }
-                const Item t = sItems[lo];
-                r.h = __ldg(&p.hdr[t.c0 + (uint32_t)(f - sChunkOff[lo])]);
-                r.kwb = t.kwb;
-                r.b = t.b;
-                r.w = t.w;
-            }
-            return r;
-        };
-        uint32_t unit = claim();
-        UnitHdr cur = fetch(unit);
-        while (unit < n_units) {
-            uint32_t lo_w[kUnit], hi_w[kUnit];
-#pragma unroll
-            for (int q = 0; q < kUnit; ++q) {
-                const uint32_t meta = __shfl_sync(FULL, cur.h.y, q);
-                const uint32_t kb = __shfl_sync(FULL, cur.kwb, q);
-                lo_w[q] = 0u;
-                hi_w[q] = 0u;
-                const uint32_t n = (meta & 31u) + 1u, bw = (meta >> 5) & 31u;
-                if (lane >= 1 && (uint32_t)lane < n && bw) {
-                    const uint32_t bit = (uint32_t)(lane - 1) * bw;
-                    const uint32_t wi = kb + (meta >> 10) + (bit >> 5);
-                    lo_w[q] = __ldg(&p.payload[wi]);
-                    hi_w[q] = __ldg(&p.payload[wi + 1]);
-                }
-            }
-            const uint32_t nxt = claim();
-            const UnitHdr nh = fetch(nxt);
-            const uint32_t nval = (uint32_t)min((uint64_t)kUnit, Ttot - (uint64_t)unit * kUnit);
-#pragma unroll
-            for (int q = 0; q < kUnit; ++q) {
-                if ((uint32_t)q >= nval) break;
-                const uint32_t meta = __shfl_sync(FULL, cur.h.y, q);
-                const uint32_t first = __shfl_sync(FULL, cur.h.x, q);
-                const uint32_t bq = __shfl_sync(FULL, cur.b, q);
-                const float wq = __shfl_sync(FULL, cur.w, q);
-                const uint32_t n = (meta & 31u) + 1u, bw = (meta >> 5) & 31u;
-                uint32_t g;
-                if (lane == 0) {
-                    g = first;
-                } else if ((uint32_t)lane < n) {
-                    uint32_t v = 0u;
-                    if (bw) {
-                        const uint32_t bit = (uint32_t)(lane - 1) * bw;
-                        v = (uint32_t)(((((uint64_t)hi_w[q]) << 32) | lo_w[q]) >> (bit & 31u)) & ((1u << bw) - 1u);
-                    }
-                    g = v + 1u;
-                } else {
-                    g = 0u;
-                }
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t t = __shfl_up_sync(FULL, g, o);
-                    if (lane >= o) g += t;
-                }
-                if ((uint32_t)lane < n) atomicAdd(&p.wide[(size_t)bq * p.n_pad + g], wq);
-            }
-            unit = nxt;
-            cur = nh;
-        }
-        EBR_STAMP(2);
-    }
-    EBR_STAMP(4);
-    if (p.local_wide) __syncthreads();   // the CTA's wide term is complete (no other CTA adds to it)
-    else grid.sync();                    // every CTA's reductions into the wide array are complete
-    EBR_STAMP(5);
 
-    // ---- C: fuse + histogram (8 independent elements in flight per thread) ----
-    constexpr int kIlp = 4;
-    if (p.local_wide) {
+    // ---- B: the CTA's range in tiles of T ads; per tile the deep warps stream A while the
+    //      wide warps locate and decode the tile's postings, then the CTA fuses the tile ----
+    for (int64_t t0 = r0; t0 < r1; t0 += T) {
+        const int64_t t1 = (t0 + T < r1) ? t0 + T : r1;
+        if (warp >= kDeepWarps) {
+            // exact chunk span of every item inside [t0, t1): first chunk whose last id >= t0,
+            // first chunk whose first id >= t1 (galloping from the previous tile's end)
+            const int n_items = (int)sNItems;
+            const int per3 = (n_items + NT - 1) / NT;
+            const int j0 = min(n_items, gt * per3), j1 = min(n_items, j0 + per3);
+            uint32_t my_units = 0;
+            for (int i = j0; i < j1; ++i) {
+                const Item t = sItems[i];
+                const uint32_t g0 = (t0 == r0)
+                    ? t.c0 + (uint32_t)((double)t0 / (double)p.n_ads * (double)(t.c1 - t.c0)) : sSpanHi[i];
+                const uint32_t lo = gallop_lower_bound([&](uint32_t c) { return __ldg(&p.chunk_last[c]); },
+                                                       t.c0, t.c1, (uint32_t)t0, g0);
+                const uint32_t g1 = lo + (uint32_t)((double)(t1 - t0) / (double)p.n_ads * (double)(t.c1 - t.c0));
+                const uint32_t lo2 = gallop_lower_bound([&](uint32_t c) { return __ldg(&p.hdr[c]).x; },
+                                                        lo, t.c1, (uint32_t)t1, g1);
+                sSpanLo[i] = lo;
+                sSpanHi[i] = lo2;
+                const uint32_t nu_i = lo2 > lo ? (lo2 - lo + kUnit - 1) / kUnit : 0u;
+                sUoffL[i] = nu_i;                      // scanned below
+                my_units += nu_i;
+            }
+            uint32_t tot_u;
+            uint32_t pre = group_exclusive_scan(my_units, sScan, &tot_u, gt, kWideWarps, 1);
+            for (int i = j0; i < j1; ++i) { const uint32_t c = sUoffL[i]; sUoffL[i] = pre; pre += c; }
+            if (gt == 0) { sUoffL[n_items] = tot_u; sNUnits = tot_u; }
+            nbar_sync(1, NT);
+            nbar_arrive(2, kThreads);          // publish the tile's units to the deep warps (barrier 2)
+        } else if (!(p.diag & 2)) {
+            // ---- deep: stream rows [t0, t1) of A ----
+            const char* Abase = reinterpret_cast<const char*>(p.A);
+            if constexpr (NB == 1 && VPL == 1 && LPR >= 4 && LPR <= 16) {
+                // 16 consecutive rows per lane group, 16 loads in flight per lane; transposed
+                // reduction: log2(LPR) butterfly steps each halving the live partials, so lane li
+                // ends with the sums of rows li*(16/LPR) .. (15 shuffles per 16 rows for LPR=16)
+                constexpr int U = 16;
+                constexpr int OUT = U / LPR;
+                constexpr int64_t wrows = (int64_t)rpw * U;              // rows per warp iteration
+                for (int64_t base = t0 + (int64_t)warp * wrows; base < t1; base += (int64_t)kDeepWarps * wrows) {
+                    const int64_t g0 = base + (int64_t)sub * U;          // this lane group's first row
+                    uint4 av[U];
+#pragma unroll
+                    for (int q = 0; q < U; ++q)
+                        av[q] = (g0 + q < t1) ? ldg_stream(Abase + (g0 + q) * p.row_bytes + (int64_t)li * 16)
+                                              : make_uint4(0, 0, 0, 0);
+                    float v[U];
+#pragma unroll
+                    for (int q = 0; q < U; ++q) {
+                        float a[E];
+                        V::unpack(av[q], a);
+                        float acc = 0.f;
+#pragma unroll
+                        for (int e = 0; e < E; ++e) acc = fmaf(a[e], u[0][0][e], acc);
+                        v[q] = acc;
+                    }
+                    int live = U;
+#pragma unroll
+                    for (int sft = LPR / 2; sft > 0; sft >>= 1) {
+                        const bool up = (li & sft) != 0;
+                        const int half = live / 2;
+#pragma unroll
+                        for (int j = 0; j < U / 2; ++j) {
+                            if (j < half) {
+                                const float send = up ? v[j] : v[j + half];
+                                const float keep = up ? v[j + half] : v[j];
+                                v[j] = keep + __shfl_xor_sync(FULL, send, sft);
+                            }
+                        }
+                        live = half;
+                    }
+                    const int64_t row0 = g0 + (int64_t)li * OUT;
+#pragma unroll
+                    for (int j = 0; j < OUT; ++j)
+                        if (row0 + j < t1) sS[row0 + j - t0] = v[j];
+                }
+            } else {
+                constexpr int64_t step = (int64_t)kDeepWarps * rpw * kUnroll;
+                for (int64_t base = t0 + (int64_t)warp * rpw; base < t1; base += step) {
+                    uint4 av[kUnroll][VPL];
+#pragma unroll
+                    for (int q = 0; q < kUnroll; ++q) {
+                        const int64_t row = base + (int64_t)q * kDeepWarps * rpw + sub;
+#pragma unroll
+                        for (int v = 0; v < VPL; ++v)
+                            av[q][v] = (row < t1) ? ldg_stream(Abase + row * p.row_bytes + (int64_t)(li + v * lpr) * 16)
+                                                  : make_uint4(0, 0, 0, 0);
+                    }
+#pragma unroll
+                    for (int q = 0; q < kUnroll; ++q) {
+                        float acc[NB];
+#pragma unroll
+                        for (int b = 0; b < NB; ++b) acc[b] = 0.f;
+#pragma unroll
+                        for (int v = 0; v < VPL; ++v) {
+                            float a[E];
+                            V::unpack(av[q][v], a);
+#pragma unroll
+                            for (int b = 0; b < NB; ++b)
+#pragma unroll
+                                for (int e = 0; e < E; ++e) acc[b] = fmaf(a[e], u[b][v][e], acc[b]);
+                        }
+#pragma unroll
+                        for (int o = lpr / 2; o > 0; o >>= 1) {
+#pragma unroll
+                            for (int b = 0; b < NB; ++b) acc[b] += __shfl_xor_sync(FULL, acc[b], o);
+                        }
+                        const int64_t row = base + (int64_t)q * kDeepWarps * rpw + sub;
+                        if (li == 0 && row < t1) {
+#pragma unroll
+                            for (int b = 0; b < NB; ++b)
+                                if (b < B) sS[(size_t)b * T + (row - t0)] = acc[b];
+                        }
+                    }
+                }
+            }
+            EBR_STAMP(3);
+        }
+        if (warp < kDeepWarps) nbar_sync(2, kThreads);   // deep warps wait for the tile's units
+        {
+            // ---- wide: 16-chunk units of the tile's item spans, claimed from a shared counter
+            // (ExclusiveScan + LoadBalance, Alg. 2 l.353-354), software-pipelined, accumulated in
+            // shared memory as 48-bit fixed point over two native 32-bit atomics (fp32 shared
+            // atomics are CAS loops on sm_100a); exact for dyadic inputs, order-free ----
+            const uint32_t n_units = (p.diag & 1) ? 0u : sNUnits;
+            const int n_items = (int)sNItems;
+            struct LUnit { uint32_t unit; int l; uint32_t cb, nc; uint2 h; };
+            auto next_unit = [&]() -> LUnit {          // claim a unit and start its header loads
+                LUnit r;
+                uint32_t unit = 0;
+                if (lane == 0) unit = atomicAdd(&sUnitCtr, 1u);
+                r.unit = __shfl_sync(FULL, unit, 0);
+                r.l = 0; r.cb = 0; r.nc = 0; r.h = make_uint2(0u, 0u);
+                if (r.unit < n_units) {
+                    int lo_i = 0, hi_i = n_items - 1;  // item = last with sUoffL <= unit
+                    while (lo_i < hi_i) {
+                        const int mid = (lo_i + hi_i + 1) >> 1;
+                        if (sUoffL[mid] <= r.unit) lo_i = mid; else hi_i = mid - 1;
+                    }
+                    r.l = lo_i;
+                    r.cb = sSpanLo[lo_i] + (r.unit - sUoffL[lo_i]) * kUnit;
+                    r.nc = min(r.cb + (uint32_t)kUnit, sSpanHi[lo_i]) - r.cb;
+                    if ((uint32_t)lane < r.nc) r.h = __ldg(&p.hdr[r.cb + lane]);
+                }
+                return r;
+            };
+            LUnit cur = next_unit();
+            while (cur.unit < n_units) {
+                const Item t = sItems[cur.l];
+                uint32_t lo_w[kUnit], hi_w[kUnit];
+#pragma unroll
+                for (int q = 0; q < kUnit; ++q) {
+                    lo_w[q] = 0u;
+                    hi_w[q] = 0u;
+                    if ((uint32_t)q >= cur.nc) break;
+                    const uint32_t meta = __shfl_sync(FULL, cur.h.y, q);
+                    const uint32_t n = (meta & 31u) + 1u, bw = (meta >> 5) & 31u;
+                    if (lane >= 1 && (uint32_t)lane < n && bw) {
+                        const uint32_t bit = (uint32_t)(lane - 1) * bw;
+                        const uint32_t wi = t.kwb + (meta >> 10) + (bit >> 5);
+                        lo_w[q] = __ldg(&p.payload[wi]);
+                        hi_w[q] = __ldg(&p.payload[wi + 1]);
+                    }
+                }
+                const LUnit nxt = next_unit();             // overlaps this unit's payload round trip
+                const int32_t H = sHpart[cur.l];
+                const uint32_t L = sLpart[cur.l];
+                int32_t* ah = accH + (size_t)t.b * T;
+                uint32_t* al = accL + (size_t)t.b * T;
+#pragma unroll
+                for (int q = 0; q < kUnit; ++q) {
+                    if ((uint32_t)q >= cur.nc) break;
+                    const uint32_t meta = __shfl_sync(FULL, cur.h.y, q);
+                    const uint32_t first = __shfl_sync(FULL, cur.h.x, q);
+                    const uint32_t n = (meta & 31u) + 1u, bw = (meta >> 5) & 31u;
+                    uint32_t g;
+                    if (lane == 0) {
+                        g = first;
+                    } else if ((uint32_t)lane < n) {
+                        uint32_t v = 0u;
+                        if (bw) {
+                            const uint32_t bit = (uint32_t)(lane - 1) * bw;
+                            v = (uint32_t)(((((uint64_t)hi_w[q]) << 32) | lo_w[q]) >> (bit & 31u)) & ((1u << bw) - 1u);
+                        }
+                        g = v + 1u;
+                    } else {
+                        g = 0u;
+                    }
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t tt = __shfl_up_sync(FULL, g, o);
+                        if (lane >= o) g += tt;
+                    }
+                    if ((uint32_t)lane < n && g >= (uint32_t)t0 && g < (uint32_t)t1) {
+                        atomicAdd(&ah[g - (uint32_t)t0], H);
+                        atomicAdd(&al[g - (uint32_t)t0], L);
+                    }
+                }
+                cur = nxt;
+            }
+            EBR_STAMP(2);
+        }
+        __syncthreads();                           // the tile's deep and wide parts are complete
+        // ---- C: fuse the tile + histogram (no other CTA contributes to this range) ----
+        const int tn = (int)(t1 - t0);
         for (int b = 0; b < B; ++b) {
             const double inv = ldexp(1.0, -sShiftB[b]);
-            for (int r = tid; r < rn; r += kThreads) {
-                const size_t o = (size_t)b * R + r;
+            float* sc = p.scores + (size_t)b * p.n_pad + t0;
+            for (int r = tid; r < tn; r += kThreads) {
+                const size_t o = (size_t)b * T + r;
                 const long long acc = (long long)accH[o] * 65536ll + (long long)accL[o];
                 float s = sS[o] + (float)((double)acc * inv);
                 if (s == 0.f) s = 0.f;                      // -0 -> +0 (R14)
-                sS[o] = s;
+                if (resident) sS[o] = s; else __stcg(&sc[r], s);
+                accH[o] = 0; accL[o] = 0u;
                 atomicAdd(&sHist[b * kHistBins + (ord_of(s) >> (32 - kHistBits))], 1u);
             }
         }
-    } else
-    for (int b = 0; b < B; ++b) {
-        float* sc = p.scores + (size_t)b * p.n_pad;
-        float* wd = p.wide + (size_t)b * p.n_pad;
-        for (int base = 0; base < rn; base += kThreads * kIlp) {
-            float dv[kIlp], wv[kIlp];
-#pragma unroll
-            for (int q = 0; q < kIlp; ++q) {
-                const int r = base + q * kThreads + tid;
-                dv[q] = 0.f; wv[q] = 0.f;
-                if (r < rn) {
-                    dv[q] = p.resident ? sS[(size_t)b * R + r] : __ldcg(&sc[r0 + r]);
-                    wv[q] = __ldcg(&wd[r0 + r]);
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < kIlp; ++q) {
-                const int r = base + q * kThreads + tid;
-                if (r < rn) {
-                    float s = dv[q] + wv[q];
-                    if (s == 0.f) s = 0.f;                  // -0 -> +0 (R14)
-                    __stcg(&wd[r0 + r], 0.f);               // leave the wide array zeroed
-                    if (p.resident) sS[(size_t)b * R + r] = s; else __stcg(&sc[r0 + r], s);
-                    atomicAdd(&sHist[b * kHistBins + (ord_of(s) >> (32 - kHistBits))], 1u);
-                }
-            }
-        }
+        if (tid == 0) sUnitCtr = 0;
+        __syncthreads();
     }
-    __syncthreads();
+    EBR_STAMP(4);
+    EBR_STAMP(5);
     for (int i = tid; i < B * kHistBins; i += kThreads) {
         const uint32_t c = sHist[i];
         if (c) atomicAdd(&p.ghist[i], c);
@@ -729,6 +608,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
     grid.sync();
     EBR_STAMP(7);
 
+    constexpr int kIlp = 4;
     // ---- D: threshold bin per user, then compaction into this CTA's segment ----
     // Block-wide: thread t holds bins [2044-4t, 2048-4t) (one coalesced 16-byte load), a block
     // scan from the top bin gives each thread the count above its bins, and the thread whose
@@ -765,7 +645,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
 #pragma unroll
             for (int q = 0; q < kIlp; ++q) {
                 const int r = base + q * kThreads + tid;
-                sv[q] = (r < rn) ? (p.resident ? sS[(size_t)b * R + r] : __ldcg(&sc[r0 + r])) : 0.f;
+                sv[q] = (r < rn) ? (resident ? sS[(size_t)b * T + r] : __ldcg(&sc[r0 + r])) : 0.f;
             }
 #pragma unroll
             for (int q = 0; q < kIlp; ++q) {
@@ -857,7 +737,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
         // leave the histograms zeroed for the next call (all CTAs read them before sync #3)
         for (int i = blockIdx.x * kThreads + tid; i < B * kHistBins; i += gridDim.x * kThreads) p.ghist[i] = 0;
     }
-    if (blockIdx.x == 0 && tid == 0) { p.header[0] = p.magic; p.header[2] = 0; }
+    if (blockIdx.x == 0 && tid == 0) p.header[0] = p.magic;
     EBR_STAMP(10);
 }
 
