@@ -215,7 +215,7 @@ ebr_status ebr_encode_host(const int32_t *ad_feat, int64_t n_ads, int32_t n_fiel
                            int64_t *n_words);
 
 /* Number of CUDA kernels (and memsets) one ebr_score_topk* call with these arguments enqueues on
- * its stream (the latency path: one cooperative launch per 8 users; the batched tensor-core path:
+ * its stream (the latency path: one cooperative launch per 4 users; the batched tensor-core path:
  * 1 memset plus 7 launches per group of 128 users).  Excludes the rare overflow fallback. */
 int32_t ebr_query_launches(const ebr_index *idx, int32_t batch, int32_t slots, int32_t k);
 

@@ -37,7 +37,7 @@ namespace ebr {
 // Fixed design constants.
 constexpr int kHistBits = 11;               // first-level radix histogram of ord(score)
 constexpr int kHistBins = 1 << kHistBits;
-constexpr int kSmallMaxB = 8;               // users per launch of the latency-path kernel
+constexpr int kSmallMaxB = 4;               // users per launch of the latency-path kernel
 constexpr int kThreads = 512;               // CTA size of the small-batch / select kernels
 
 struct QueryArgs {

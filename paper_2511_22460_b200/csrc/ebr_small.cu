@@ -66,7 +66,7 @@ ebr_status run_small(const QueryArgs& q, int b0, int B) {
     if (row_bytes <= 512) { lpr = row_bytes / 16; vpl = 1; }
     else { lpr = 32; vpl = row_bytes / 512; }
     int nb = 1;
-    while (nb < B) nb <<= 1;
+    while (nb < B) nb <<= 1;      // 1, 2 or 4 (kSmallMaxB)
     kern_t k = idx->dtype == EBR_BF16 ? pick_kernel<__nv_bfloat16>(nb, lpr, vpl) : pick_kernel<float>(nb, lpr, vpl);
     if (!k) return set_error(EBR_EUNSUPPORTED, "embedding row of %d bytes is not supported", row_bytes);
 

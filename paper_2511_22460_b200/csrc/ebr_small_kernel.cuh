@@ -1,4 +1,4 @@
-// ebr_small.cu -- the latency path (small user batch, B <= 8 per launch): ONE cooperative,
+// ebr_small_kernel.cuh -- the latency path (small user batch, B <= 4 per launch): ONE cooperative,
 // persistent kernel per call (1 CTA per SM) runs every step of the hot path:
 //
 //   A  plan     (every CTA, deterministic order): each valid user slot becomes a work item
@@ -590,8 +590,12 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
                 const long long acc = (long long)accH[o] * 65536ll + (long long)accL[o];
                 float s = sS[o] + (float)((double)acc * inv);
                 if (s == 0.f) s = 0.f;                      // -0 -> +0 (R14)
-                if (resident) sS[o] = s; else __stcg(&sc[r], s);
-                accH[o] = 0; accL[o] = 0u;
+                if (resident) {
+                    sS[o] = s;                               // the prologue re-zeroes acc per call
+                } else {
+                    __stcg(&sc[r], s);
+                    accH[o] = 0; accL[o] = 0u;               // next tile accumulates from zero
+                }
                 atomicAdd(&sHist[b * kHistBins + (ord_of(s) >> (32 - kHistBits))], 1u);
             }
         }
@@ -754,7 +758,6 @@ kern_t pick_nb(int nb);
             case 1: return small_kernel<T, 1, LPR, VPL>;       \
             case 2: return small_kernel<T, 2, LPR, VPL>;       \
             case 4: return small_kernel<T, 4, LPR, VPL>;       \
-            case 8: return small_kernel<T, 8, LPR, VPL>;       \
         }                                                      \
         return nullptr;                                        \
     }
