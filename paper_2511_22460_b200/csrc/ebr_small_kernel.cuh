@@ -7,12 +7,12 @@
 //               (Alg. 2 l.352-353 "k_length", "ExclusiveScan").
 //   B  the CTA's contiguous ad range in tiles of T ads (one tile when it fits shared memory);
 //      per tile two warp roles run concurrently:
-//       deep      (10 warps) A4: stream the tile's rows of A once from HBM with 16-byte
+//       deep      (8 warps) A4: stream the tile's rows of A once from HBM with 16-byte
 //                 non-allocating loads, 16 rows in flight per lane group (measured: plain vector
 //                 loads reach the HBM peak, a bulk-copy ring at 1 CTA/SM does not --
 //                 tools/mb_stream.cu), fp32 FFMA with the user vectors in registers and a
 //                 transposed butterfly reduction; deep scores land in shared memory;
-//       wide      (6 warps) A2+A3: the exact chunk span of every item inside the tile (galloping
+//       wide      (8 warps) A2+A3: the exact chunk span of every item inside the tile (galloping
 //                 search on chunk_last / chunk first ids), an exclusive scan of 16-chunk unit counts
 //                 and a shared unit counter (the paper's ExclusiveScan + LoadBalance, Alg. 2
 //                 l.353-354: every chunk but a key's last holds 32 postings, so units cost the
@@ -45,7 +45,7 @@ namespace ebr {
 namespace small {
 
 #ifndef EBR_DEEP_WARPS
-#define EBR_DEEP_WARPS 10
+#define EBR_DEEP_WARPS 8
 #endif
 constexpr int kDeepWarps = EBR_DEEP_WARPS;      // stream A first, then help with the wide queue
 constexpr int kWideWarps = 16 - kDeepWarps;     // plan, then the wide queue from the start
