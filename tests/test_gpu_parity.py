@@ -272,3 +272,14 @@ def test_shard_smaller_than_k_pads(ebr):
     ebr.merge_topk(gathered, 2, 2, k, ids, sc)
     torch.cuda.synchronize()
     assert check_all(oracle.Oracle.of(inv), users, ids.cpu().numpy(), sc.cpu().numpy(), k, "exact") == 0
+
+
+@pytest.mark.parametrize("dtype,b", [("f32", 1), ("bf16", 3)])
+def test_multi_tile_latency_path(ebr, dtype, b):
+    """Inventories whose per-CTA range exceeds one shared-memory tile (N > 148 x 16384): the
+    latency kernel loops over tiles and keeps fused scores in the L2 scratch."""
+    inv = synth.make_inventory(3_000_001, 64, 12, dtype=dtype, mode="exact", seed=77)
+    users = synth.make_users(inv, b, mode="exact", seed=78)
+    idx = ebr.Index.of(inv)
+    (ids, sc), _ = run(ebr, idx, users, 300)
+    assert check_all(oracle.Oracle.of(inv), users, ids, sc, 300, "exact") == 0
