@@ -373,18 +373,20 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         int it = 0;
         for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++it) {
             const int acc = it % kAccStages;
-            mbar_wait(&tfull[acc], (it / kAccStages) & 1);
-            tc::fence_after();
             const int64_t a = (int64_t)t * p.tile_stride * kTileM + row;   // shard-local ad
             const bool valid = a < p.n_ads;
-            if (c < p.nu_pad) {
-                float* wcol = p.ws.W + (valid ? a : 0);
-                // this row's 32 wide scores: 32 independent loads (coalesced across the warp's
-                // consecutive ads) issued before any use
-                float wf[32];
+            // this row's 32 wide scores: 32 independent loads (coalesced across the warp's
+            // consecutive ads), issued before waiting for the accumulator so they overlap the MMA
+            float wf[32];
+            {
+                const float* wcol = p.ws.W + (valid ? a : 0);
 #pragma unroll
                 for (int j = 0; j < 32; ++j)
                     wf[j] = (valid && c + j < p.nu) ? __ldcg(wcol + (size_t)(c + j) * p.n_pad) : 0.f;
+            }
+            mbar_wait(&tfull[acc], (it / kAccStages) & 1);
+            tc::fence_after();
+            if (c < p.nu_pad) {
                 uint32_t r[32];
                 tc::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * 128 + c), r);
 #pragma unroll
@@ -427,22 +429,119 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 // ------------------------------------------------------------------------------------------
 // 4. theta: the K-th largest key of each user's sampled ads
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(512, 1) theta_kernel(BatchWs ws, int n_samp, int K, uint32_t ad_begin, int nu) {
+// Two histogram passes over ord(score) (11 + 11 bits; per-warp-group private histograms, 8-wide
+// vector loads in flight) narrow the K-th largest down to a 22-bit score prefix T; the sampled keys
+// with ord >= T (K plus the few in T's bucket) are compacted into shared memory and the exact K-th
+// largest key is selected there.  Only if that bucket is huge (massive score ties) does the kernel
+// fall back to the radix select over the whole sample in global memory.
+constexpr int kThetaThreads = 1024;
+constexpr int kThetaCopies = 8;    // private histograms (warps w and w+8, w+16, ... share one)
+
+__device__ __forceinline__ uint32_t samp_ord(float s) { return ord_of(s); }
+
+// Warp 0: the digit t with count(> t) < need <= count(>= t) in hist[0..2048); writes
+// sScalar[0] = t, sScalar[1] = count(> t).
+__device__ __forceinline__ void theta_find_digit(const uint32_t* hist, uint32_t need, uint32_t* sScalar) {
+    const int lane = threadIdx.x & 31;
+    constexpr int per = 2048 / 32;
+    uint32_t local = 0;
+    for (int j = 0; j < per; ++j) local += hist[2047 - (lane * per + j)];
+    uint32_t incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += t;
+    }
+    uint32_t c = incl - local;
+    int found = -1;
+    uint32_t above = 0;
+    if (c < need && c + local >= need) {
+        for (int j = 0; j < per; ++j) {
+            const int d = 2047 - (lane * per + j);
+            const uint32_t h = hist[d];
+            if (found < 0 && c + h >= need) { found = d; above = c; }
+            c += h;
+        }
+    }
+    const unsigned m = __ballot_sync(FULL, found >= 0);
+    const int src = m ? __ffs(m) - 1 : 0;
+    const int t = __shfl_sync(FULL, found, src);
+    const uint32_t ab = __shfl_sync(FULL, above, src);
+    if (lane == 0) { sScalar[0] = m ? (uint32_t)t : 0u; sScalar[1] = m ? ab : 0u; }
+}
+
+__global__ void __launch_bounds__(kThetaThreads, 1) theta_kernel(BatchWs ws, int n_samp, int K, uint32_t ad_begin,
+                                                                int nu, int scap) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint32_t sScalar[8];
     const int u = blockIdx.x;
     if (u >= nu) return;
+    const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5;
     const int P = pow2ceil_i(K);
-    uint64_t* sbuf = reinterpret_cast<uint64_t*>(smem);
-    uint32_t* shist = reinterpret_cast<uint32_t*>(sbuf + P);
+    uint64_t* sbuf = reinterpret_cast<uint64_t*>(smem);                 // [P]
+    uint32_t* hist = reinterpret_cast<uint32_t*>(sbuf + P);             // [kThetaCopies][2048]
+    uint64_t* scand = reinterpret_cast<uint64_t*>(hist + kThetaCopies * 2048);   // [scap]
+    uint32_t* myh = hist + (warp % kThetaCopies) * 2048;
     const float* sp = ws.samp + (size_t)u * n_samp;
-    auto get = [sp, ad_begin](int64_t i) {
-        // sample slot i = tile (i / 128) of the sample = inventory tile (i / 128) * stride
-        const int64_t ad = (i / kTileM) * kSampleStride * kTileM + (i % kTileM);
-        return kappa_of(__ldcg(&sp[i]), ad_begin + (uint32_t)ad);
-    };
-    const int nsel = cta_select_topk(get, n_samp, K, sbuf, nullptr, 0, shist, sScalar);
-    if (threadIdx.x == 0) {
+    const float4* sp4 = reinterpret_cast<const float4*>(sp);
+    const int n4 = n_samp / 4;                                          // n_samp is a multiple of 128
+    auto ad_of = [](int64_t i) { return (i / kTileM) * kSampleStride * kTileM + (i % kTileM); };
+    uint32_t prefix = 0, need = (uint32_t)K;
+    for (int pass = 0; pass < 2; ++pass) {
+        const int shift = pass == 0 ? 21 : 10;
+        for (int i = tid; i < kThetaCopies * 2048; i += nt) hist[i] = 0;
+        __syncthreads();
+        for (int i = tid; i < n4; i += 2 * nt) {
+            float4 v[2];
+            v[0] = __ldcg(&sp4[i]);
+            v[1] = (i + nt < n4) ? __ldcg(&sp4[i + nt]) : make_float4(0.f, 0.f, 0.f, 0.f);
+            const int nv = (i + nt < n4) ? 2 : 1;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                if (q >= nv) break;
+                const float f[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const uint32_t o = samp_ord(f[r]);
+                    if (pass == 0 || (o >> 21) == (prefix >> 21)) atomicAdd(&myh[(o >> shift) & 2047u], 1u);
+                }
+            }
+        }
+        __syncthreads();
+        for (int b = tid; b < 2048; b += nt) {
+            uint32_t s = 0;
+#pragma unroll
+            for (int c = 0; c < kThetaCopies; ++c) s += hist[c * 2048 + b];
+            hist[b] = s;
+        }
+        __syncthreads();
+        if (warp == 0) theta_find_digit(hist, need, sScalar);
+        __syncthreads();
+        prefix |= sScalar[0] << shift;
+        need -= sScalar[1];
+        __syncthreads();
+    }
+    // keys with ord >= prefix: at least K of them; compact into shared memory
+    if (tid == 0) sScalar[2] = 0;
+    __syncthreads();
+    for (int i = tid; i < n_samp; i += nt) {
+        const float s = __ldcg(&sp[i]);
+        if (samp_ord(s) >= prefix) {
+            const uint32_t pos = atomicAdd(&sScalar[2], 1u);
+            if ((int)pos < scap) scand[pos] = kappa_of(s, ad_begin + (uint32_t)ad_of(i));
+        }
+    }
+    __syncthreads();
+    const int64_t cnt = sScalar[2];
+    __syncthreads();
+    int nsel;
+    if (cnt <= scap) {
+        nsel = cta_select_topk([scand](int64_t i) { return scand[i]; }, cnt, K, sbuf, nullptr, 0, hist, sScalar);
+    } else {
+        auto get = [sp, ad_begin, ad_of](int64_t i) { return kappa_of(__ldcg(&sp[i]), ad_begin + (uint32_t)ad_of(i)); };
+        nsel = cta_select_topk(get, n_samp, K, sbuf, nullptr, 0, hist, sScalar);
+    }
+    if (tid == 0) {
         ws.theta[u] = (nsel >= K) ? sbuf[K - 1] : 0ull;
         ws.cand_count[u] = 0;
     }
@@ -614,10 +713,12 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
         if (e != cudaSuccess) return cuda_check(e, "attr(gemm0)");
         gemm_kernel<0><<<std::min(idx->sm_count, n_samp_tiles), kGemmThreads, smem, q.stream>>>(tmA, tmU, gp);
         // theta
-        const size_t tsmem = (size_t)pow2ceil_i(q.k) * 8 + kSelBins * 4 + 64;
+        const size_t tsmem = 200 * 1024;
+        const int tscap = (int)((tsmem - (size_t)pow2ceil_i(q.k) * 8 - kThetaCopies * 2048 * 4) / 8);
         e = cudaFuncSetAttribute(theta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
         if (e != cudaSuccess) return cuda_check(e, "attr(theta)");
-        theta_kernel<<<nu, 512, tsmem, q.stream>>>(ws, (int)L.n_samp, q.k, (uint32_t)idx->ad_begin, nu);
+        theta_kernel<<<nu, kThetaThreads, tsmem, q.stream>>>(ws, (int)L.n_samp, q.k, (uint32_t)idx->ad_begin, nu,
+                                                             tscap);
         // filter pass over every tile
         gp.n_tiles = n_tiles; gp.tile_stride = 1;
         e = cudaFuncSetAttribute(gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
