@@ -26,7 +26,7 @@ kern_t pick_kernel(int nb, int lpr, int vpl) {
 }
 
 struct SmallLayout {
-    size_t off_header, off_hist, off_count, off_scores, off_cand, total;
+    size_t off_header, off_hist, off_count, off_scores, off_cand, off_timers, total;
 };
 
 SmallLayout small_layout(const ebr_index* idx, int B) {
@@ -38,6 +38,7 @@ SmallLayout small_layout(const ebr_index* idx, int B) {
     L.off_count = o;  o = al(o + (size_t)B * (idx->sm_count + 1) * 4);   // [B][n_ranges]
     L.off_scores = o; o = al(o + (size_t)B * idx->n_pad * 4);
     L.off_cand = o;   o = al(o + (size_t)B * idx->n_pad * 8);
+    L.off_timers = o; o = al(o + (size_t)(idx->sm_count + 1) * 16 * 8);   // per-CTA phase stamps
     L.total = o;
     return L;
 }
@@ -76,7 +77,7 @@ ebr_status run_small(const QueryArgs& q, int b0, int B) {
     R = std::max<int64_t>(32, (R + 31) & ~(int64_t)31);
     const int n_ranges = (int)((idx->n_ads + R - 1) / R);
     // per item: the Item + span lo/hi + unit offset + fixed-point parts
-    const size_t plan_bytes = (size_t)B * kHistBins * 4 + (size_t)items_cap * (sizeof(Item) + 20) + 64;
+    const size_t plan_bytes = (size_t)kHistCopies * B * kHistBins * 4 + (size_t)items_cap * (sizeof(Item) + 20) + 64;
     // phase E: candidate staging (>= 16k keys) and the rare single-CTA fallback select
     const size_t sel_min = std::max((size_t)(n_ranges + 2) * 4 + 128 * 1024,
                                     (size_t)(n_ranges + 2) * 4 + (size_t)pow2ceil_i(q.k) * 8 + kSelBins * 4 + 64);
@@ -115,7 +116,7 @@ ebr_status run_small(const QueryArgs& q, int b0, int B) {
     static const bool timers_on = getenv("EBR_PHASE_TIMERS") && getenv("EBR_PHASE_TIMERS")[0] == '1';
     static const int diag = getenv("EBR_DIAG") ? atoi(getenv("EBR_DIAG")) : 0;
     p.diag = diag;
-    p.timers = timers_on ? reinterpret_cast<unsigned long long*>(ws + L.off_header + 16) : nullptr;
+    p.timers = timers_on ? reinterpret_cast<unsigned long long*>(ws + L.off_timers) : nullptr;
     // the magic ties the workspace's zeroed state to this index geometry
     p.magic = workspace_magic(idx);
     p.ghist = reinterpret_cast<uint32_t*>(ws + L.off_hist);
@@ -134,7 +135,7 @@ ebr_status run_small(const QueryArgs& q, int b0, int B) {
     p.smem_bytes = (int32_t)smem;
 
     if (timers_on) {
-        e = cudaMemsetAsync(ws + L.off_header + 16, 0, 16 * 8, q.stream);
+        e = cudaMemsetAsync(ws + L.off_timers, 0, (size_t)(sms + 1) * 16 * 8, q.stream);
         if (e != cudaSuccess) return cuda_check(e, "memset(timers)");
     }
     const int grid = std::max(1, std::min<int>(std::max(p.n_ranges, B), occ * sms));

@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libebr.so")
+# EBR_LIB: an alternative build of the same library (A/B measurements); default the in-tree one
+LIB_PATH = os.environ.get("EBR_LIB") or os.path.join(_HERE, "libebr.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`"
