@@ -1,8 +1,10 @@
-# A/B of two library builds on one box (bench lines, C2): EBR_LIB=<alt .so> vs the in-tree build
-ALT=${ALT:-/root/repo/ab_libs_head.so}
+# A/B of library builds / EBR_DIAG settings on one box (bench lines, C2).  Each ALTS entry is
+# "<.so path or cur>:<EBR_DIAG>"; "cur" is the in-tree build.
+ALTS=${ALTS:-"/root/repo/ab_libs_head.so:0 cur:0"}
 for rep in 1 2 3; do
-  for v in alt cur; do
-    if [ $v = alt ]; then L=$ALT; else L=""; fi
-    EBR_LIB=$L timeout 200 python bench.py --steps 1000 --no-cpu-baseline ${BENCH_ARGS} 2>/dev/null | tail -n 1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v', round(d['ms_per_step']*1000,2), round(d['roofline']['frac'],4), d['clocks']['sm_mhz'])" >> gpurun_out/ab.txt
+  for v in $ALTS; do
+    lib=${v%%:*}; dg=${v##*:}
+    if [ $lib = cur ]; then L=""; else L=$lib; fi
+    EBR_LIB=$L EBR_DIAG=$dg timeout 200 python bench.py --steps 1000 --no-cpu-baseline ${BENCH_ARGS} 2>/dev/null | tail -n 1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$(basename $lib):$dg', round(d['ms_per_step']*1000,2), round(d['roofline']['frac'],4), d['clocks']['sm_mhz'])" >> gpurun_out/ab.txt
   done
 done
