@@ -198,6 +198,10 @@ typedef struct {
     int64_t index_bytes;  /* directory + headers + payload + w                 */
     int64_t emb_bytes;    /* device bytes of A                                 */
     double build_ms;      /* host encode + upload wall time                    */
+    int32_t n_hot;        /* dense hot-key columns of L (bf16 indexes; 0 = none) */
+    int32_t pad0;
+    int64_t hot_nnz;      /* postings covered by the hot columns               */
+    int64_t hot_bytes;    /* device bytes of the one-hot columns H             */
 } ebr_stats;
 ebr_status ebr_index_stats(const ebr_index *idx, ebr_stats *out);
 

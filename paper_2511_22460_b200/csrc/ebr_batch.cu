@@ -39,6 +39,8 @@ constexpr int kSampleStride = 16;    // every 16th tile is sampled for theta
 constexpr int kEpiWarps = 16;        // 4 per TMEM lane quadrant, one 32-column chunk each
 constexpr int kGemmThreads = 128 + 32 * kEpiWarps;   // warp 0 TMA, 1 MMA, 2 TMEM alloc, 4.. epilogue
 constexpr int kAccStages = 2;
+constexpr int kHotPieces = 3;        // w~ = hi + mid + lo in bf16: 24 significant bits, exact (R22)
+constexpr int kBlockBytes = kTileM * 128;   // one ring stage: 128 ads x 64 bf16 (one K block)
 
 struct BItem {
     uint32_t key, c0, c1, u, kwb;
@@ -74,16 +76,21 @@ __global__ void __launch_bounds__(512) plan_kernel(const uint32_t* __restrict__ 
                                                    const int32_t* __restrict__ user_feat,
                                                    const float* __restrict__ user_x,
                                                    const uint16_t* __restrict__ user_emb, int d, int d_pad,
-                                                   int nu, int nu_pad, BatchWs ws, uint32_t* err) {
+                                                   int nu, int nu_pad, const int32_t* __restrict__ hot_slot,
+                                                   int n_hot, int u_cols, BatchWs ws, uint32_t* err) {
+    extern __shared__ float sHot[];          // [nu_pad][n_hot] sum of w~ per (user, hot slot)
     __shared__ uint32_t sScan[40];
     __shared__ uint64_t sCarry;
     const int tid = threadIdx.x;
-    // user tile (zero padded)
+    uint16_t* U = reinterpret_cast<uint16_t*>(ws.U);
+    // user tile, deep part (zero padded): U[u][0..d_pad)
     for (int i = tid; i < nu_pad * d_pad; i += blockDim.x) {
         const int u = i / d_pad, j = i - u * d_pad;
         const uint16_t v = (u < nu && j < d) ? user_emb[(size_t)u * d + j] : (uint16_t)0;
-        reinterpret_cast<uint16_t*>(ws.U)[i] = v;
+        U[(size_t)u * u_cols + j] = v;
     }
+    for (int i = tid; i < nu_pad * n_hot; i += blockDim.x) sHot[i] = 0.f;
+    __syncthreads();
     const int nslot = nu * F * S;
     uint32_t base = 0;
     if (tid == 0) sCarry = 0;
@@ -104,7 +111,9 @@ __global__ void __launch_bounds__(512) plan_kernel(const uint32_t* __restrict__ 
                 it.u = (uint32_t)(i / (F * S));
                 it.kwb = key_word_off[key];
                 it.w = __fmul_rn(cross_w[key], user_x[i]);   // w~ = fl32(w x), never an FMA (R10)
-                ok = it.c1 > it.c0;
+                const int32_t h = n_hot ? hot_slot[key] : -1;
+                if (h >= 0 && h < n_hot) atomicAdd(&sHot[it.u * n_hot + h], it.w);   // dense column (R22)
+                else ok = it.c1 > it.c0;
             }
         }
         uint32_t tot;
@@ -126,6 +135,19 @@ __global__ void __launch_bounds__(512) plan_kernel(const uint32_t* __restrict__ 
         ws.chunk_off[base] = sCarry;
     }
     __syncthreads();
+    // user tile, hot part: w~ of hot slot h as kHotPieces bf16 terms (hi, mid, lo; R22) in
+    // U[u][d_pad + ((h/64)*kHotPieces + p)*64 + h%64] -- one 64-column K block per (block, piece)
+    for (int i = tid; i < nu_pad * n_hot; i += blockDim.x) {
+        const int u = i / n_hot, h = i - u * n_hot;
+        float r = sHot[i];
+        uint16_t* dst = U + (size_t)u * u_cols + d_pad + (size_t)(h >> 6) * kHotPieces * 64 + (h & 63);
+#pragma unroll
+        for (int p = 0; p < kHotPieces; ++p) {
+            const __nv_bfloat16 b = __float2bfloat16_rn(r);
+            dst[p * 64] = __bfloat16_as_ushort(b);
+            r -= __bfloat162float(b);            // exact (Sterbenz-type cancellation of the top bits)
+        }
+    }
     // items are in slot order, i.e. grouped by user: first item of each user by binary search
     for (int u = tid; u <= nu; u += blockDim.x) {
         int lo = 0, hi = (int)base;
@@ -270,7 +292,9 @@ __global__ void __launch_bounds__(kWideThreads, 3) wide_smem_kernel(const uint2*
 struct GemmParams {
     int64_t n_ads, n_pad;
     uint32_t ad_begin;
-    int d_pad, n_kb;       // K blocks of 64
+    int d_pad, n_kb;       // deep K blocks of 64
+    int n_hb;              // hot-key K blocks of 64 (A side: H; B side: kHotPieces blocks each)
+    int u_blocks;          // K blocks of the user tile: n_kb + n_hb * kHotPieces
     int nu, nu_pad;        // users in this group (valid / padded to 32)
     int n_tiles;           // tiles to process in this launch
     int tile_stride;       // 1 (all tiles) or kSampleStride (sample)
@@ -282,15 +306,16 @@ struct GemmParams {
 
 template <int MODE>   // 0: sample (store s), 1: filter (append keys >= theta, re-zero W)
 __global__ void __launch_bounds__(kGemmThreads, 1)
-gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmU, const GemmParams p) {
+gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmH,
+            const __grid_constant__ CUtensorMap tmU, const GemmParams p) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int a_stage_bytes = kTileM * 128 * p.n_kb;     // 128 rows x 128 B per K block
-    const int u_bytes = p.nu_pad * 128 * p.n_kb;
-    unsigned char* sU = smem;                                       // [n_kb][nu_pad rows x 128 B]
-    unsigned char* sA = smem + ((u_bytes + 1023) & ~1023);          // [stages][n_kb][128 x 128 B]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sA + (size_t)p.stages * a_stage_bytes);
+    const int u_bytes = p.nu_pad * 128 * p.u_blocks;
+    const int nkt = p.n_kb + p.n_hb;                                // A-side K blocks per tile
+    unsigned char* sU = smem;                                       // [u_blocks][nu_pad rows x 128 B]
+    unsigned char* sA = smem + ((u_bytes + 1023) & ~1023);          // ring: [stages][128 x 128 B]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sA + (size_t)p.stages * kBlockBytes);
     uint64_t* full = bars;                       // [stages]
     uint64_t* empty = bars + p.stages;           // [stages]
     uint64_t* tfull = bars + 2 * p.stages;       // [kAccStages]
@@ -321,20 +346,24 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         if (lane == 0) {
             // ---------------- TMA producer ----------------
             tc::tma_prefetch(&tmA);
+            if (p.n_hb) tc::tma_prefetch(&tmH);
             tc::tma_prefetch(&tmU);
             mbar_arrive_expect_tx(ufull, (uint32_t)u_bytes);
-            for (int kb = 0; kb < p.n_kb; ++kb)
+            for (int kb = 0; kb < p.u_blocks; ++kb)
                 tc::tma_load_2d(sU + (size_t)kb * p.nu_pad * 128, &tmU, kb * kBlockK, 0, ufull);
-            int it = 0;
-            for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++it) {
-                const int slot = it % p.stages;
-                const uint32_t round = it / p.stages;
-                if (round > 0) mbar_wait(&empty[slot], (round - 1) & 1);
-                mbar_arrive_expect_tx(&full[slot], (uint32_t)a_stage_bytes);
+            uint32_t gb = 0;                                 // ring position (one K block per stage)
+            for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
                 const int row0 = t * p.tile_stride * kTileM;
-                for (int kb = 0; kb < p.n_kb; ++kb)
-                    tc::tma_load_2d(sA + (size_t)slot * a_stage_bytes + (size_t)kb * kTileM * 128, &tmA,
-                                    kb * kBlockK, row0, &full[slot]);
+                for (int kb = 0; kb < nkt; ++kb, ++gb) {
+                    const uint32_t slot = gb % p.stages, round = gb / p.stages;
+                    if (round > 0) mbar_wait(&empty[slot], (round - 1) & 1);
+                    mbar_arrive_expect_tx(&full[slot], (uint32_t)kBlockBytes);
+                    if (kb < p.n_kb)
+                        tc::tma_load_2d(sA + (size_t)slot * kBlockBytes, &tmA, kb * kBlockK, row0, &full[slot]);
+                    else
+                        tc::tma_load_2d(sA + (size_t)slot * kBlockBytes, &tmH, (kb - p.n_kb) * kBlockK, row0,
+                                        &full[slot]);
+                }
             }
         }
     } else if (warp == 1) {
@@ -344,23 +373,30 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             mbar_wait(ufull, 0);
             tc::fence_after();
             int it = 0;
+            uint32_t gb = 0;
             for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++it) {
-                const int slot = it % p.stages;
                 const int acc = it % kAccStages;
                 const uint32_t around = it / kAccStages;
                 if (around > 0) mbar_wait(&tempty[acc], (around - 1) & 1);   // epilogue drained it
-                mbar_wait(&full[slot], (it / p.stages) & 1);
-                tc::fence_after();
                 const uint32_t d_tmem = tmem_base + (uint32_t)(acc * 128);
-                for (int kb = 0; kb < p.n_kb; ++kb) {
-                    const uint64_t da0 = tc::sdesc_sw128(sA + (size_t)slot * a_stage_bytes + (size_t)kb * kTileM * 128);
-                    const uint64_t db0 = tc::sdesc_sw128(sU + (size_t)kb * p.nu_pad * 128);
+                for (int kb = 0; kb < nkt; ++kb, ++gb) {
+                    const uint32_t slot = gb % p.stages;
+                    mbar_wait(&full[slot], (gb / p.stages) & 1);
+                    tc::fence_after();
+                    const uint64_t da0 = tc::sdesc_sw128(sA + (size_t)slot * kBlockBytes);
+                    // deep block kb pairs with user block kb; hot block h with its kHotPieces
+                    // user blocks (the same one-hot A tile times hi, mid and lo of w~)
+                    const int np = kb < p.n_kb ? 1 : kHotPieces;
+                    const int ub0 = kb < p.n_kb ? kb : p.n_kb + (kb - p.n_kb) * kHotPieces;
+                    for (int pc = 0; pc < np; ++pc) {
+                        const uint64_t db0 = tc::sdesc_sw128(sU + (size_t)(ub0 + pc) * p.nu_pad * 128);
 #pragma unroll
-                    for (int k = 0; k < kBlockK / 16; ++k)   // +32 bytes per K step inside the swizzle row
-                        tc::umma_f16(d_tmem, da0 + (uint64_t)(k * 2), db0 + (uint64_t)(k * 2), idesc,
-                                     (kb | k) != 0);
+                        for (int k = 0; k < kBlockK / 16; ++k)   // +32 bytes per K step inside the swizzle row
+                            tc::umma_f16(d_tmem, da0 + (uint64_t)(k * 2), db0 + (uint64_t)(k * 2), idesc,
+                                         (kb | pc | k) != 0);
+                    }
+                    tc::umma_commit(&empty[slot]);     // ring stage free once these MMAs completed
                 }
-                tc::umma_commit(&empty[slot]);     // smem stage free once these MMAs completed
                 tc::umma_commit(&tfull[acc]);      // accumulator ready for the epilogue
             }
         }
@@ -616,7 +652,7 @@ static Layout layout(const ebr_index* idx, int32_t slots, int32_t k) {
     L.header = o;    o = al(o + 64);
     L.items = o;     o = al(o + (size_t)L.cap_items * sizeof(BItem));
     L.chunk_off = o; o = al(o + (size_t)(L.cap_items + 1) * 8);
-    L.U = o;         o = al(o + (size_t)kGroup * idx->d_pad * 2);
+    L.U = o;         o = al(o + (size_t)kGroup * (idx->d_pad + kHotPieces * idx->n_hot) * 2);
     L.W = o;         o = al(o + (size_t)kGroup * idx->n_pad * 4);
     L.samp = o;      o = al(o + (size_t)kGroup * L.n_samp * 4);
     L.theta = o;     o = al(o + (size_t)kGroup * 8);
@@ -670,16 +706,27 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
     char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(region) + 1023) & ~(uintptr_t)1023);
     BatchWs ws = carve(base, L);
     const int n_kb = idx->d_pad / kBlockK;
-    const int stages = n_kb <= 2 ? 4 : 2;
     const int n_tiles = (int)(idx->n_pad / kTileM);
     const int n_samp_tiles = (int)(L.n_samp / kTileM);
     cudaError_t e = cudaMemsetAsync(ws.overflow, 0, (size_t)kGroup * 4, q.stream);
     if (e != cudaSuccess) return cuda_check(e, "memset(overflow)");
     e = cudaFuncSetAttribute(wide_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kWideR * 8);
     if (e != cudaSuccess) return cuda_check(e, "attr(wide)");
-    CUtensorMap tmA;
+    CUtensorMap tmA, tmH;
     if (!encode_2d_bf16(&tmA, idx->A, (uint64_t)idx->d_pad, (uint64_t)idx->n_pad, kBlockK, kTileM))
         return set_error(EBR_ECUDA, "cuTensorMapEncodeTiled(A) failed");
+    if (idx->n_hot > 0) {
+        if (!encode_2d_bf16(&tmH, idx->H, (uint64_t)idx->n_hot, (uint64_t)idx->n_pad, kBlockK, kTileM))
+            return set_error(EBR_ECUDA, "cuTensorMapEncodeTiled(H) failed");
+    } else {
+        tmH = tmA;   // unused
+    }
+    int max_smem = 0;
+    e = cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, idx->device);
+    if (e != cudaSuccess) return cuda_check(e, "attr(max smem)");
+    e = cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kGroup * kMaxHot * 4);
+    if (e != cudaSuccess) return cuda_check(e, "attr(plan)");
     std::vector<int> overflow_users;
     // test hook: a smaller candidate capacity exercises the overflow -> latency-path fallback
     int64_t cap = L.cap;
@@ -687,15 +734,27 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
     for (int g0 = 0; g0 < q.batch; g0 += kGroup) {
         const int nu = std::min(kGroup, q.batch - g0);
         const int nu_pad = (nu + 31) & ~31;
+        // hot K blocks: as many as fit next to the resident user tile with >= 4 ring stages
+        const size_t fixed = 1024 + 256 + (size_t)kGroup * 12;
+        auto smem_of = [&](int hb, int st) {
+            return fixed + (((size_t)nu_pad * 128 * (n_kb + kHotPieces * hb) + 1023) & ~(size_t)1023) +
+                   (size_t)st * kBlockBytes;
+        };
+        int n_hb = idx->n_hot / 64;
+        if (getenv("EBR_NO_HOT")) n_hb = 0;
+        while (n_hb > 0 && smem_of(n_hb, 4) > (size_t)max_smem) --n_hb;
+        int stages = 4;
+        while (stages < 8 && smem_of(n_hb, stages + 1) <= (size_t)max_smem) ++stages;
+        const int u_blocks = n_kb + kHotPieces * n_hb;
+        const int u_cols = u_blocks * kBlockK;
         CUtensorMap tmU;
-        if (!encode_2d_bf16(&tmU, ws.U, (uint64_t)idx->d_pad, (uint64_t)nu_pad, kBlockK, (uint32_t)nu_pad))
+        if (!encode_2d_bf16(&tmU, ws.U, (uint64_t)u_cols, (uint64_t)nu_pad, kBlockK, (uint32_t)nu_pad))
             return set_error(EBR_ECUDA, "cuTensorMapEncodeTiled(U) failed");
-        plan_kernel<<<1, 512, 0, q.stream>>>(idx->key_chunk_off, idx->key_word_off, idx->cross_w, idx->field_card,
-                                             idx->field_base, idx->n_fields, q.slots,
-                                             q.user_feat + (size_t)g0 * idx->n_fields * q.slots,
-                                             q.user_x + (size_t)g0 * idx->n_fields * q.slots,
-                                             reinterpret_cast<const uint16_t*>(q.user_emb) + (size_t)g0 * idx->d,
-                                             idx->d, idx->d_pad, nu, nu_pad, ws, err_word);
+        plan_kernel<<<1, 512, (size_t)nu_pad * n_hb * 64 * 4, q.stream>>>(
+            idx->key_chunk_off, idx->key_word_off, idx->cross_w, idx->field_card, idx->field_base, idx->n_fields,
+            q.slots, q.user_feat + (size_t)g0 * idx->n_fields * q.slots, q.user_x + (size_t)g0 * idx->n_fields * q.slots,
+            reinterpret_cast<const uint16_t*>(q.user_emb) + (size_t)g0 * idx->d, idx->d, idx->d_pad, nu, nu_pad,
+            idx->hot_slot, n_hb * 64, u_cols, ws, err_word);
         const int max_items = nu * idx->n_fields * q.slots;
         span_kernel<<<(max_items + 7) / 8, 256, 0, q.stream>>>(idx->chunk_hdr, idx->chunk_last, ws, (int)L.nj,
                                                                (int)L.cap_items);
@@ -703,15 +762,15 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
             idx->chunk_hdr, idx->payload, ws, (int)L.nj, idx->n_pad, (int)L.cap_items);
         GemmParams gp;
         gp.n_ads = idx->n_ads; gp.n_pad = idx->n_pad; gp.ad_begin = (uint32_t)idx->ad_begin;
-        gp.d_pad = idx->d_pad; gp.n_kb = n_kb; gp.nu = nu; gp.nu_pad = nu_pad;
+        gp.d_pad = idx->d_pad; gp.n_kb = n_kb; gp.n_hb = n_hb; gp.u_blocks = u_blocks;
+        gp.nu = nu; gp.nu_pad = nu_pad;
         gp.n_samp = (int)L.n_samp; gp.stages = stages; gp.cap = cap; gp.ws = ws;
-        const size_t smem = 1024 + (((size_t)nu_pad * 128 * n_kb + 1023) & ~(size_t)1023) +
-                            (size_t)stages * kTileM * 128 * n_kb + 256 + (size_t)kGroup * 12;
+        const size_t smem = smem_of(n_hb, stages);
         // sample pass
         gp.n_tiles = n_samp_tiles; gp.tile_stride = kSampleStride;
         e = cudaFuncSetAttribute(gemm_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return cuda_check(e, "attr(gemm0)");
-        gemm_kernel<0><<<std::min(idx->sm_count, n_samp_tiles), kGemmThreads, smem, q.stream>>>(tmA, tmU, gp);
+        gemm_kernel<0><<<std::min(idx->sm_count, n_samp_tiles), kGemmThreads, smem, q.stream>>>(tmA, tmH, tmU, gp);
         // theta
         const size_t tsmem = 200 * 1024;
         const int tscap = (int)((tsmem - (size_t)pow2ceil_i(q.k) * 8 - kThetaCopies * 2048 * 4) / 8);
@@ -723,7 +782,7 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
         gp.n_tiles = n_tiles; gp.tile_stride = 1;
         e = cudaFuncSetAttribute(gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return cuda_check(e, "attr(gemm1)");
-        gemm_kernel<1><<<std::min(idx->sm_count, n_tiles), kGemmThreads, smem, q.stream>>>(tmA, tmU, gp);
+        gemm_kernel<1><<<std::min(idx->sm_count, n_tiles), kGemmThreads, smem, q.stream>>>(tmA, tmH, tmU, gp);
         // final
         const size_t fsmem = 200 * 1024;
         const int64_t scap = (int64_t)(fsmem - (size_t)pow2ceil_i(q.k) * 8 - kSelBins * 4) / 8;

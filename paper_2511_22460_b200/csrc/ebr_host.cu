@@ -13,6 +13,7 @@
 #include <chrono>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -57,6 +58,7 @@ size_t small_workspace_bytes(const ebr_index* idx, int32_t slots, int32_t k);
 // ------------------------------------------------------------------------------------------
 struct Encoded {
     std::vector<uint32_t> key_chunk_off, key_word_off, hdr, payload, last;
+    std::vector<int64_t> key_count;   // postings per key
     int64_t nnz = 0;
 };
 
@@ -88,6 +90,7 @@ static ebr_status encode(const int32_t* ad_feat, int64_t n_ads, int32_t F, const
     std::vector<int64_t> base(F + 1, 0);
     for (int f = 0; f < F; ++f) base[f + 1] = base[f] + card[f];
     std::vector<uint32_t> nchunks(n_keys, 0), nwords(n_keys, 0);
+    out.key_count.assign(n_keys, 0);
     std::vector<std::vector<int32_t>> lists(F);
     std::vector<std::vector<int64_t>> loff(F);
     const int T = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 32u));
@@ -114,6 +117,7 @@ static ebr_status encode(const int32_t* ad_feat, int64_t n_ads, int32_t F, const
             for (int v = 0; v < V; ++v) {
                 const int64_t n = off[v + 1] - off[v];
                 const int64_t key = base[f] + v;
+                out.key_count[key] = n;
                 nchunks[key] = (uint32_t)((n + 31) / 32);
                 uint64_t words = 0;
                 for (int64_t c0 = off[v]; c0 < off[v + 1]; c0 += 32) {
@@ -206,6 +210,74 @@ static int32_t padded_width(int32_t d, int esz) {
     while (p < bytes && p < 512) p <<= 1;
     if (bytes > 512) p = bytes <= 1024 ? 1024 : 2048;   // wider rows are rejected at build
     return (int32_t)(p / esz);
+}
+
+// ------------------------------------------------------------------------------------------
+// Hot keys (bf16 indexes): the kMaxHot keys with the longest posting lists -- and at least
+// max(64, n/512) postings, below which a dense column costs more than the compressed list --
+// also get a dense column of L, H[a][h] in bf16 (1.0 / 0.0), that the batched path contracts on
+// the tensor cores.  The posting lists stay complete (the latency path and the
+// batched path's cold keys read them).  EBR_HOT_KEYS=<n> caps the count (0 disables).
+// ------------------------------------------------------------------------------------------
+__global__ void hot_fill_kernel(const int32_t* __restrict__ feat, int64_t n, int F,
+                                const int32_t* __restrict__ field_base, const int32_t* __restrict__ hot_slot,
+                                uint16_t* __restrict__ H, int n_hot) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n * F) return;
+    const int64_t a = i / F;
+    const int f = (int)(i - a * F);
+    const int32_t v = feat[i];
+    if (v < 0) return;
+    const int32_t h = hot_slot[field_base[f] + v];
+    if (h >= 0) H[a * n_hot + h] = 0x3F80;   // bf16 1.0
+}
+
+static ebr_status build_hot(ebr_index* idx, const Encoded& enc, const int32_t* ad_feat, cudaStream_t stream) {
+    int cap = kMaxHot;
+    if (const char* e = getenv("EBR_HOT_KEYS")) cap = std::max(0, std::min(kMaxHot, atoi(e)));
+    const int64_t M = idx->n_keys, n = idx->n_ads;
+    const int64_t min_count = std::max<int64_t>(64, n / 512);
+    std::vector<int32_t> cand;
+    for (int64_t k = 0; k < M; ++k)
+        if (enc.key_count[k] >= min_count) cand.push_back((int32_t)k);
+    std::sort(cand.begin(), cand.end(), [&](int32_t x, int32_t y) {
+        return enc.key_count[x] != enc.key_count[y] ? enc.key_count[x] > enc.key_count[y] : x < y;
+    });
+    if ((int64_t)cand.size() > cap) cand.resize(cap);
+    const int n_hot = (int)((cand.size() + 63) / 64 * 64);
+    idx->n_hot = n_hot;
+    if (n_hot == 0) return EBR_OK;
+    std::vector<int32_t> slot(M, -1), key(n_hot, -1);
+    for (size_t h = 0; h < cand.size(); ++h) {
+        slot[cand[h]] = (int32_t)h;
+        key[h] = cand[h];
+        idx->hot_nnz += enc.key_count[cand[h]];
+    }
+    EBR_CUDA(cudaMalloc(&idx->hot_slot, (size_t)M * 4));
+    EBR_CUDA(cudaMemcpyAsync(idx->hot_slot, slot.data(), (size_t)M * 4, cudaMemcpyHostToDevice, stream));
+    EBR_CUDA(cudaMalloc(&idx->hot_key, (size_t)n_hot * 4));
+    EBR_CUDA(cudaMemcpyAsync(idx->hot_key, key.data(), (size_t)n_hot * 4, cudaMemcpyHostToDevice, stream));
+    const size_t hbytes = (size_t)idx->n_pad * n_hot * 2;
+    EBR_CUDA(cudaMalloc(&idx->H, hbytes));
+    EBR_CUDA(cudaMemsetAsync(idx->H, 0, hbytes, stream));
+    const int F = idx->n_fields;
+    const int64_t chunk = std::max<int64_t>(1, (int64_t)(256 << 20) / (4 * std::max(F, 1)));   // 256 MB of values
+    int32_t* dfeat = nullptr;
+    EBR_CUDA(cudaMalloc(&dfeat, (size_t)std::min(chunk, n) * F * 4));
+    for (int64_t a0 = 0; a0 < n; a0 += chunk) {
+        const int64_t m = std::min(chunk, n - a0);
+        cudaError_t e = cudaMemcpyAsync(dfeat, ad_feat + a0 * F, (size_t)m * F * 4, cudaMemcpyHostToDevice, stream);
+        if (e == cudaSuccess) {
+            const int64_t tot = m * F;
+            hot_fill_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, stream>>>(
+                dfeat, m, F, idx->field_base, idx->hot_slot, static_cast<uint16_t*>(idx->H) + a0 * n_hot, n_hot);
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess) e = cudaStreamSynchronize(stream);   // dfeat is reused
+        if (e != cudaSuccess) { cudaFree(dfeat); return cuda_check(e, "hot columns"); }
+    }
+    cudaFree(dfeat);
+    return EBR_OK;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -351,7 +423,7 @@ void ebr_free_index(ebr_index* idx) {
     cudaGetDevice(&prev);
     cudaSetDevice(idx->device);
     void* ptrs[] = {idx->A, idx->key_chunk_off, idx->key_word_off, idx->chunk_hdr, idx->chunk_last, idx->payload,
-                    idx->cross_w, idx->field_card, idx->field_base};
+                    idx->cross_w, idx->field_card, idx->field_base, idx->hot_slot, idx->hot_key, idx->H};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     free(idx->tmap_A);
@@ -431,6 +503,10 @@ ebr_status ebr_build_index(const void* ad_emb, ebr_dtype dtype, int64_t ad_begin
         for (int f = 0; f < n_fields; ++f) { fb[f] = (int32_t)acc; acc += field_card[f]; }
         EBR_TRY(upload((void**)&idx->field_card, field_card, (size_t)n_fields * 4));
         EBR_TRY(upload((void**)&idx->field_base, fb.data(), (size_t)n_fields * 4));
+        if (dtype == EBR_BF16) {
+            st = build_hot(idx, enc, ad_feat, stream);
+            if (st) return fail(st);
+        }
         EBR_TRY(cudaStreamSynchronize(stream));
 #undef EBR_TRY
         idx->build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -627,6 +703,9 @@ ebr_status ebr_index_stats(const ebr_index* idx, ebr_stats* o) {
     o->index_bytes = (idx->n_keys * 2 + 1) * 4 + idx->n_chunks * 12 + (idx->n_words + 2) * 4 + idx->n_keys * 4;
     o->emb_bytes = idx->n_pad * idx->d_pad * esz;
     o->build_ms = idx->build_ms;
+    o->n_hot = idx->n_hot;
+    o->hot_nnz = idx->hot_nnz;
+    o->hot_bytes = (int64_t)idx->n_pad * idx->n_hot * 2;
     return EBR_OK;
 }
 

@@ -104,3 +104,58 @@ def test_full_size_sampled_users(ebr, cfg):
     assert ((ids >= 0) & (ids < inv.n_ads)).all()
     assert all(len(np.unique(r)) == c.k for r in ids)
     assert (np.diff(sc, axis=1) <= 0).all()
+
+
+# ---- hot keys: dense one-hot columns of L contracted on the tensor cores (R22) ----
+
+def test_hot_columns_built(ebr):
+    inv, _ = synth.make_config("C3", mode="exact", n_ads=60_000, batch=16)
+    st = ebr.Index.of(inv).stats()
+    assert st["n_hot"] > 0 and st["n_hot"] % 64 == 0
+    assert 0 < st["hot_nnz"] <= st["nnz"]
+    assert st["hot_bytes"] == st["n_hot"] * 2 * ((inv.n_ads + 127) // 128 * 128)
+    inv32, _ = synth.make_config("C2", mode="exact", n_ads=20_000, batch=1)
+    assert ebr.Index.of(inv32).stats()["n_hot"] == 0          # fp32 indexes never take the batched path
+
+
+@pytest.mark.parametrize("cfg,n,b,k", [("C3", 70_000, 48, 150), ("C4", 60_000, 64, 400)])
+def test_batch_hot_equals_cold(ebr, cfg, n, b, k):
+    """exact mode: the hot columns (tensor cores) and the compressed lists (shared-memory
+    scatter) give bit-identical top-K ids and scores."""
+    inv, users = synth.make_config(cfg, mode="exact", n_ads=n, batch=b)
+    idx = ebr.Index.of(inv)
+    assert idx.stats()["n_hot"] > 0
+    (ids_h, sc_h), _ = run(ebr, idx, users, k)
+    os.environ["EBR_NO_HOT"] = "1"
+    try:
+        (ids_c, sc_c), _ = run(ebr, idx, users, k)
+    finally:
+        del os.environ["EBR_NO_HOT"]
+    assert (ids_h == ids_c).all() and (sc_h == sc_c).all()
+    assert check_all(oracle.Oracle.of(inv), users, ids_h, sc_h, k, "exact") == 0
+
+
+def test_batch_hot_duplicate_slots(ebr):
+    """R3: the same (field, value) twice in one user adds twice -- also when the key is hot."""
+    inv, users = synth.make_config("C3", mode="exact", n_ads=50_000, batch=24)
+    uf = users.user_feat.copy()
+    ux = users.user_x.copy()
+    uf[:, :4, 1] = uf[:, :4, 0]                   # low-cardinality fields: hot keys
+    ux[:, :4, 1] = np.where(uf[:, :4, 1] >= 0, 0.5, 0.0).astype(np.float32)
+    users = synth.Users(users.batch, users.slots, users.user_emb, uf, ux)
+    idx = ebr.Index.of(inv)
+    (ids, sc), _ = run(ebr, idx, users, 100)
+    assert check_all(oracle.Oracle.of(inv), users, ids, sc, 100, "exact") == 0
+
+
+def test_batch_without_hot_columns(ebr):
+    """EBR_HOT_KEYS=0 at build: no dense columns, every key through the compressed lists."""
+    os.environ["EBR_HOT_KEYS"] = "0"
+    try:
+        inv, users = synth.make_config("C4", mode="exact", n_ads=40_000, batch=20)
+        idx = ebr.Index.of(inv)
+    finally:
+        del os.environ["EBR_HOT_KEYS"]
+    assert idx.stats()["n_hot"] == 0
+    (ids, sc), _ = run(ebr, idx, users, 120)
+    assert check_all(oracle.Oracle.of(inv), users, ids, sc, 120, "exact") == 0
