@@ -292,6 +292,10 @@ def main():
     users_s = B * args.steps / (tot_ms / 1e3)
 
     line = None
+    batched = idx.query_launches(B, S, K) != (B + 3) // 4
+    kernel_label = ("whole batched step per 128-user group: plan, span, wide_smem, gemm_kernel<0> (sample), "
+                    "theta, gemm_kernel<1> (tcgen05 + fused filter), final -- timed as one" if batched else
+                    "small_kernel (fused plan+decode+wide+GEMV+fuse+top-K, 1 launch per <=4 users)")
     if rank == 0:
         emb_b, post_b, io_b = algorithmic_bytes(ebr, inv, users, st, lo, hi)
         alg = emb_b + post_b + io_b + 8 * B * K
@@ -318,7 +322,7 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic,
                          "peak_kind": peak_kind,
-                         "kernel": "small_kernel (fused plan+decode+wide+GEMV+fuse+top-K, 1 launch)",
+                         "kernel": kernel_label,
                          "alg_bytes_per_launch": alg,
                          "alg_bytes_split": {"embeddings": emb_b, "postings": post_b, "io": io_b + 8 * B * K}},
             "index": {"build_ms": st["build_ms"], "index_bytes": st["index_bytes"],

@@ -45,8 +45,9 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in sources() + headers() + [__file__])
 
 
-def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, jobs: int | None = None, out: str | None = None) -> str:
+    lib = out or LIB
+    if not force and not out and not stale():
         return LIB
     os.makedirs(BUILD, exist_ok=True)
     common = ARCH + ["-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
@@ -54,6 +55,8 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
                      "--expt-relaxed-constexpr"]
     if os.environ.get("EBR_DEEP_WARPS"):
         common += [f"-DEBR_DEEP_WARPS={int(os.environ['EBR_DEEP_WARPS'])}"]
+    if os.environ.get("EBR_NVCC_DEFS"):             # A/B variants: e.g. "-DEBR_WIDE_R=16384"
+        common += os.environ["EBR_NVCC_DEFS"].split()
     if os.environ.get("EBR_PTXAS_V"):
         common += ["-Xptxas", "-v"]
     objs, procs = [], []
@@ -73,12 +76,12 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
             failed.append(src)
     if failed:
         raise RuntimeError(f"nvcc failed for {failed}")
-    tmp = LIB + f".{os.getpid()}.tmp"
+    tmp = lib + f".{os.getpid()}.tmp"
     subprocess.check_call([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart"])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(LIB)
+    o = [a.split("=", 1)[1] for a in sys.argv if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, verbose=True, out=o[0] if o else None))

@@ -36,9 +36,14 @@ constexpr int kGroup = 128;          // users per group (UMMA N)
 constexpr int kTileM = 128;          // ads per tile (UMMA M)
 constexpr int kBlockK = 64;          // bf16 elements per 128-byte swizzle row
 constexpr int kSampleStride = 16;    // every 16th tile is sampled for theta
-constexpr int kEpiWarps = 16;        // 4 per TMEM lane quadrant, one 32-column chunk each
-constexpr int kGemmThreads = 128 + 32 * kEpiWarps;   // warp 0 TMA, 1 MMA, 2 TMEM alloc, 4.. epilogue
-constexpr int kAccStages = 2;
+constexpr int kEpiWarps = 8;         // 2 per TMEM lane quadrant, two 32-column chunks each
+constexpr int kEpiChunks = kGroup / 32 / (kEpiWarps / 4);
+constexpr int kLoadWarps = 16;       // 4 per TMEM lane quadrant, one 32-column chunk each
+constexpr int kEpiWarp0 = 4;
+constexpr int kLoadWarp0 = kEpiWarp0 + kEpiWarps;
+constexpr int kGemmThreads = 32 * (kLoadWarp0 + kLoadWarps);   // 0 TMA, 1 MMA, 2 TMEM alloc, 3 idle
+constexpr int kAccStages = 4;        // TMEM: 4 x 128 columns = all 512
+constexpr int kWPrefetch = 4;        // tiles of W streamed into L2 ahead of the loader warps
 constexpr int kHotPieces = 3;        // w~ = hi + mid + lo in bf16: 24 significant bits, exact (R22)
 constexpr int kBlockBytes = kTileM * 128;   // one ring stage: 128 ads x 64 bf16 (one K block)
 
@@ -52,18 +57,25 @@ struct BatchWs {   // workspace carve-up (device pointers)
     BItem* items;         // [cap_items]
     uint64_t* chunk_off;  // [cap_items + 1]
     __nv_bfloat16* U;     // [kGroup][d_pad]
-    float* W;             // [kGroup][n_pad]  user-major: a chunk's postings hit neighbouring words
+    float* W;             // [n_tiles][kGroup][128] tile-major: one tile's block is contiguous
     float* samp;          // [kGroup][n_samp]
     uint64_t* theta;      // [kGroup]
     uint32_t* cand_count; // [kGroup]
     uint64_t* cand;       // [kGroup][cap]
     uint32_t* overflow;   // [kGroup]
     uint32_t* user_item;  // [kGroup + 1]  items of group user u: [user_item[u], user_item[u+1])
+    int32_t* user_shift;  // [kGroup] fixed-point scale S_u of the user's cold wide sum
     uint32_t* span;       // [nj + 1][cap_items] first chunk of item i with first id >= j*R
     uint32_t* span_lo;    // [nj][cap_items]     first chunk of item i holding an id >= j*R
 };
 
-constexpr int kWideR = 8192;          // ads per shared-memory accumulation chunk (2 x 32 KB)
+#ifndef EBR_WIDE_R
+#define EBR_WIDE_R 32768
+#endif
+#ifndef EBR_WIDE_T
+#define EBR_WIDE_T 1024
+#endif
+constexpr int kWideR = EBR_WIDE_R;     // ads per shared-memory accumulation chunk (int32 each)
 
 // ------------------------------------------------------------------------------------------
 // 1. plan (one CTA)
@@ -80,6 +92,7 @@ __global__ void __launch_bounds__(512) plan_kernel(const uint32_t* __restrict__ 
                                                    int n_hot, int u_cols, BatchWs ws, uint32_t* err) {
     extern __shared__ float sHot[];          // [nu_pad][n_hot] sum of w~ per (user, hot slot)
     __shared__ uint32_t sScan[40];
+    __shared__ float sBound[kGroup];         // sum |w~| of each user's cold items
     __shared__ uint64_t sCarry;
     const int tid = threadIdx.x;
     uint16_t* U = reinterpret_cast<uint16_t*>(ws.U);
@@ -90,6 +103,7 @@ __global__ void __launch_bounds__(512) plan_kernel(const uint32_t* __restrict__ 
         U[(size_t)u * u_cols + j] = v;
     }
     for (int i = tid; i < nu_pad * n_hot; i += blockDim.x) sHot[i] = 0.f;
+    for (int i = tid; i < kGroup; i += blockDim.x) sBound[i] = 0.f;
     __syncthreads();
     const int nslot = nu * F * S;
     uint32_t base = 0;
@@ -114,6 +128,7 @@ __global__ void __launch_bounds__(512) plan_kernel(const uint32_t* __restrict__ 
                 const int32_t h = n_hot ? hot_slot[key] : -1;
                 if (h >= 0 && h < n_hot) atomicAdd(&sHot[it.u * n_hot + h], it.w);   // dense column (R22)
                 else ok = it.c1 > it.c0;
+                if (ok) atomicAdd(&sBound[it.u], fabsf(it.w));
             }
         }
         uint32_t tot;
@@ -135,6 +150,13 @@ __global__ void __launch_bounds__(512) plan_kernel(const uint32_t* __restrict__ 
         ws.chunk_off[base] = sCarry;
     }
     __syncthreads();
+    // fixed-point scale of each user's cold wide sum: |sum| <= bound < 2^e, S = 30 - e keeps every
+    // partial sum inside int32 (and int32 addition is modular anyway)
+    for (int u = tid; u < kGroup; u += blockDim.x) {
+        int e = 0;
+        frexpf(sBound[u] * 1.0001f + 1e-30f, &e);
+        ws.user_shift[u] = 30 - e;
+    }
     // user tile, hot part: w~ of hot slot h as kHotPieces bf16 terms (hi, mid, lo; R22) in
     // U[u][d_pad + ((h/64)*kHotPieces + p)*64 + h%64] -- one 64-column K block per (block, piece)
     for (int i = tid; i < nu_pad * n_hot; i += blockDim.x) {
@@ -189,52 +211,39 @@ __global__ void __launch_bounds__(256) span_kernel(const uint2* __restrict__ hdr
 }
 
 // ------------------------------------------------------------------------------------------
-// 2b. wide: CTA (chunk j, user u) decodes the user's postings inside ads [j*R, (j+1)*R) and
-//     accumulates w~ on chip (Alg. 2 l.355-358 with the per-ad accumulator in shared memory).
-//     Accumulation is 48-bit fixed point over two native 32-bit shared atomics: with
-//     S = 46 - ceil(log2(sum_i |w~_i|)) for the user, each w~ becomes F = rint(w~ 2^S), split as
-//     F = H*2^16 + L (L = low 16 bits); sum H and sum L cannot overflow and the total is exact
-//     integer arithmetic -- order-free (deterministic) and finer than fp32 (error <= 2^-47 of the
-//     bound per hit; exact for dyadic inputs).  fp32 shared atomics are CAS loops on sm_100a.
-//     Units of 16 posting chunks are load-balanced over the CTA's warps by an exclusive scan of
-//     the items' unit counts (the paper's ExclusiveScan + LoadBalance, l.353-354).  The chunk is
-//     then written to W (fp32) with coalesced stores -- no global atomics, nothing to re-zero.
+// 2b. wide (cold keys): CTA (chunk j, user u) decodes the user's cold postings inside ads
+//     [j*R, (j+1)*R) and accumulates w~ on chip (Alg. 2 l.355-358 with the per-ad accumulator in
+//     shared memory).  Accumulation is 32-bit fixed point over native shared integer atomics: with
+//     the user's scale S (plan_kernel: |any partial sum| <= sum |w~| < 2^(30-S)), each w~ becomes
+//     rint(w~ 2^S); integer addition is exact and order-free (deterministic), and the one rounding
+//     is the final int -> fp32 conversion (exact for the dyadic inputs of exact mode; otherwise the
+//     quantisation error is <= 2^-31 of the user's bound per hit).  fp32 shared atomics are CAS
+//     loops on sm_100a.  Units of 16 posting chunks are load-balanced over the CTA's warps by an
+//     exclusive scan of the items' unit counts (the paper's ExclusiveScan + LoadBalance,
+//     l.353-354).  W is written tile-major with coalesced 16-byte stores; nothing to re-zero.
 // ------------------------------------------------------------------------------------------
-constexpr int kWideThreads = 256;
-constexpr int kWideItems = 256;   // items per pass of the unit scan
-__global__ void __launch_bounds__(kWideThreads, 3) wide_smem_kernel(const uint2* __restrict__ hdr,
+constexpr int kWideThreads = EBR_WIDE_T;
+constexpr int kWideItems = kWideThreads;   // items per pass of the unit scan
+constexpr int kWideMinBlocks = (2048 / kWideThreads) < (200 * 1024 / (kWideR * 4)) ? (2048 / kWideThreads)
+                                                                                    : (200 * 1024 / (kWideR * 4));
+__global__ void __launch_bounds__(kWideThreads, kWideMinBlocks > 0 ? kWideMinBlocks : 1) wide_smem_kernel(const uint2* __restrict__ hdr,
                                                                     const uint32_t* __restrict__ payload,
                                                                     BatchWs ws, int nj, int64_t n_pad,
                                                                     int cap_items) {
-    extern __shared__ __align__(16) int32_t accH[];   // [kWideR] high parts, then [kWideR] low parts
-    uint32_t* accL = reinterpret_cast<uint32_t*>(accH + kWideR);
+    extern __shared__ __align__(16) int32_t acc[];   // [kWideR]
     __shared__ uint32_t sLo[kWideItems], sHi[kWideItems], sUoff[kWideItems + 1], sScan[40];
-    __shared__ int32_t sH[kWideItems];
-    __shared__ uint32_t sL[kWideItems], sKwb[kWideItems];
-    __shared__ float sBound[8];
-    __shared__ int sShift;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = kWideThreads / 32;
+    __shared__ int32_t sF[kWideItems];
+    __shared__ uint32_t sKwb[kWideItems];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = kWideThreads / 32;
     const int j = blockIdx.x, u = blockIdx.y;
     const int64_t a0 = (int64_t)j * kWideR;
     const int64_t a1 = (a0 + kWideR < n_pad) ? a0 + kWideR : n_pad;
-    for (int i = tid; i < kWideR; i += kWideThreads) { accH[i] = 0; accL[i] = 0u; }
-    const uint32_t i0 = __ldcg(&ws.user_item[u]), i1 = __ldcg(&ws.user_item[u + 1]);
-    // the user's fixed-point scale (same in every CTA of the user: depends on its items only)
-    float bnd = 0.f;
-    for (uint32_t it = i0 + tid; it < i1; it += kWideThreads) bnd += fabsf(ws.items[it].w);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) bnd += __shfl_xor_sync(FULL, bnd, o);
-    if (lane == 0) sBound[warp] = bnd;
-    __syncthreads();
-    if (tid == 0) {
-        float tb = 0.f;
-        for (int w = 0; w < nwarps; ++w) tb += sBound[w];
-        int e = 0;
-        frexpf(tb * 1.0001f + 1e-30f, &e);          // tb < 2^e
-        sShift = 46 - e;
+    {
+        int4* a4 = reinterpret_cast<int4*>(acc);
+        for (int i = tid; i < kWideR / 4; i += kWideThreads) a4[i] = make_int4(0, 0, 0, 0);
     }
-    __syncthreads();
-    const int S = sShift;
+    const uint32_t i0 = __ldcg(&ws.user_item[u]), i1 = __ldcg(&ws.user_item[u + 1]);
+    const int S = __ldcg(&ws.user_shift[u]);
     for (uint32_t ib = i0; ib < i1; ib += kWideItems) {
         const uint32_t ni = min((uint32_t)kWideItems, i1 - ib);
         uint32_t nu_units = 0, lo = 0;
@@ -244,9 +253,7 @@ __global__ void __launch_bounds__(kWideThreads, 3) wide_smem_kernel(const uint2*
             lo = __ldcg(&ws.span_lo[(size_t)j * cap_items + it]);
             const uint32_t s1 = __ldcg(&ws.span[(size_t)(j + 1) * cap_items + it]);
             nu_units = s1 > lo ? (s1 - lo + 15) / 16 : 0;
-            const long long F = __double2ll_rn(ldexp((double)t.w, S));
-            sH[tid] = (int32_t)(F >> 16);
-            sL[tid] = (uint32_t)(F & 0xFFFF);
+            sF[tid] = (int32_t)__float2ll_rn(ldexpf(t.w, S));   // |w~ 2^S| < 2^30
             sHi[tid] = s1;
             sKwb[tid] = t.kwb;
         }
@@ -255,34 +262,85 @@ __global__ void __launch_bounds__(kWideThreads, 3) wide_smem_kernel(const uint2*
         if ((uint32_t)tid < ni) { sLo[tid] = lo; sUoff[tid] = pre; }
         if (tid == 0) sUoff[ni] = tot;
         __syncthreads();
-        int l = 0;                                    // units are visited in increasing order:
-        for (uint32_t unit = warp; unit < tot; unit += nwarps) {   // walk the item index forward
-            while (sUoff[l + 1] <= unit) ++l;
-            const uint32_t cb = sLo[l] + (unit - sUoff[l]) * 16;
-            const uint32_t ce = min(cb + 16, sHi[l]);
-            const int32_t H = sH[l];
-            const uint32_t L = sL[l];
-            decode_unit16(hdr, payload, sKwb[l], cb, ce, lane, [&](uint32_t id) {
-                if ((int64_t)id >= a0 && (int64_t)id < a1) {
-                    atomicAdd(&accH[id - a0], H);
-                    atomicAdd(&accL[id - a0], L);
+        // a warp's units (unit = warp, warp + nwarps, ...) are visited in increasing order, so the
+        // item index walks forward; software-pipelined: the next unit's chunk headers are in
+        // flight while this unit's payload words are extracted and scattered
+        struct BUnit { int l; uint32_t cb, nc; uint2 h; };
+        int lw = 0;
+        auto start = [&](uint32_t unit) -> BUnit {
+            BUnit r{0, 0u, 0u, make_uint2(0u, 0u)};
+            if (unit < tot) {
+                while (sUoff[lw + 1] <= unit) ++lw;
+                r.l = lw;
+                r.cb = sLo[lw] + (unit - sUoff[lw]) * 16;
+                r.nc = min(r.cb + 16, sHi[lw]) - r.cb;
+                if ((uint32_t)lane < r.nc) r.h = __ldg(&hdr[r.cb + lane]);
+            }
+            return r;
+        };
+        BUnit cur = start(warp);
+        for (uint32_t unit = warp; unit < tot; unit += nwarps) {
+            const uint32_t kwb = sKwb[cur.l];
+            uint32_t lo_w[16], hi_w[16];
+#pragma unroll
+            for (int qq = 0; qq < 16; ++qq) {
+                lo_w[qq] = 0u;
+                hi_w[qq] = 0u;
+                if ((uint32_t)qq >= cur.nc) break;             // warp-uniform
+                const uint32_t meta = __shfl_sync(FULL, cur.h.y, qq);
+                const uint32_t n = (meta & 31u) + 1u, bw = (meta >> 5) & 31u;
+                if (lane >= 1 && (uint32_t)lane < n && bw) {
+                    const uint32_t bit = (uint32_t)(lane - 1) * bw;
+                    const uint32_t wi = kwb + (meta >> 10) + (bit >> 5);
+                    lo_w[qq] = __ldg(&payload[wi]);
+                    hi_w[qq] = __ldg(&payload[wi + 1]);
                 }
-            });
+            }
+            const BUnit nxt = start(unit + nwarps);          // overlaps this unit's payload round trip
+            const int32_t Fv = sF[cur.l];
+#pragma unroll
+            for (int qq = 0; qq < 16; ++qq) {
+                if ((uint32_t)qq >= cur.nc) break;
+                const uint32_t meta = __shfl_sync(FULL, cur.h.y, qq);
+                const uint32_t first = __shfl_sync(FULL, cur.h.x, qq);
+                const uint32_t n = (meta & 31u) + 1u, bw = (meta >> 5) & 31u;
+                uint32_t g;
+                if (lane == 0) {
+                    g = first;
+                } else if ((uint32_t)lane < n) {
+                    uint32_t v = 0u;
+                    if (bw) {
+                        const uint32_t bit = (uint32_t)(lane - 1) * bw;
+                        v = (uint32_t)(((((uint64_t)hi_w[qq]) << 32) | lo_w[qq]) >> (bit & 31u)) & ((1u << bw) - 1u);
+                    }
+                    g = v + 1u;
+                } else {
+                    g = 0u;
+                }
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t t = __shfl_up_sync(FULL, g, o);
+                    if (lane >= o) g += t;
+                }
+                if ((uint32_t)lane < n && (int64_t)g >= a0 && (int64_t)g < a1) atomicAdd(&acc[g - a0], Fv);
+            }
+            cur = nxt;
         }
         __syncthreads();
     }
-    const double inv = ldexp(1.0, -S);
-    float4* dst = reinterpret_cast<float4*>(ws.W + (size_t)u * n_pad + a0);
+    const float inv = ldexpf(1.f, -S);
+    const int64_t t0 = a0 / kTileM;
+    // dense W[tile][u][row]: the chunk spans (a1 - a0) / 128 tiles; 32 float4 per (tile, user) row
+    const int4* a4 = reinterpret_cast<const int4*>(acc);
     for (int64_t i = tid; i < (a1 - a0) / 4; i += kWideThreads) {
-        float4 v;
-        float* vf = reinterpret_cast<float*>(&v);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int64_t r = i * 4 + q;
-            const long long tot = (long long)accH[r] * 65536ll + (long long)accL[r];
-            vf[q] = (float)((double)tot * inv);
-        }
-        __stcg(&dst[i], v);
+        const int4 v = a4[i];
+        float4 o;
+        o.x = v.x ? (float)v.x * inv : 0.f;          // int -> fp32: the one rounding; * 2^-S exact
+        o.y = v.y ? (float)v.y * inv : 0.f;
+        o.z = v.z ? (float)v.z * inv : 0.f;
+        o.w = v.w ? (float)v.w * inv : 0.f;
+        const int64_t t = t0 + (i >> 5);
+        __stcg(reinterpret_cast<float4*>(ws.W + ((size_t)t * kGroup + u) * kTileM) + (i & 31), o);
     }
 }
 
@@ -304,7 +362,7 @@ struct GemmParams {
     BatchWs ws;
 };
 
-template <int MODE>   // 0: sample (store s), 1: filter (append keys >= theta, re-zero W)
+template <int MODE>   // 0: sample (store s), 1: filter (append keys >= theta)
 __global__ void __launch_bounds__(kGemmThreads, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmH,
             const __grid_constant__ CUtensorMap tmU, const GemmParams p) {
@@ -318,20 +376,25 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     uint64_t* bars = reinterpret_cast<uint64_t*>(sA + (size_t)p.stages * kBlockBytes);
     uint64_t* full = bars;                       // [stages]
     uint64_t* empty = bars + p.stages;           // [stages]
-    uint64_t* tfull = bars + 2 * p.stages;       // [kAccStages]
-    uint64_t* tempty = tfull + kAccStages;       // [kAccStages]
-    uint64_t* ufull = tempty + kAccStages;
+    uint64_t* tfull = bars + 2 * p.stages;       // [kAccStages] MMA done -> epilogue
+    uint64_t* tempty = tfull + kAccStages;       // [kAccStages] epilogue drained -> wide loaders
+    uint64_t* wready = tempty + kAccStages;      // [kAccStages] wide term stored -> MMA
+    uint64_t* ufull = wready + kAccStages;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ufull + 1);
     uint64_t* sTheta = reinterpret_cast<uint64_t*>(tmem_slot + 2);  // [kGroup]
     float* sThetaS = reinterpret_cast<float*>(sTheta + kGroup);       // score part of theta, [kGroup]
 
     if (tid == 0) {
         for (int s = 0; s < p.stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (int s = 0; s < kAccStages; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], kEpiWarps); }
+        for (int s = 0; s < kAccStages; ++s) {
+            mbar_init(&tfull[s], 1);
+            mbar_init(&tempty[s], kEpiWarps);
+            mbar_init(&wready[s], kLoadWarps);
+        }
         mbar_init(ufull, 1);
         fence_mbar_init();
     }
-    if (warp == 2) tc::tmem_alloc(tmem_slot, 256);            // 2 accumulator stages x 128 columns
+    if (warp == 2) tc::tmem_alloc(tmem_slot, kAccStages * 128);     // kAccStages x 128 user columns
     if (MODE == 1)
         for (int i = tid; i < p.nu_pad; i += kGemmThreads) {
             sTheta[i] = __ldcg(&p.ws.theta[i]);
@@ -369,6 +432,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     } else if (warp == 1) {
         if (lane == 0) {
             // ---------------- MMA issuer (one thread) ----------------
+            // The accumulator stage already holds the tile's wide term (stored by the loader warps),
+            // so every MMA accumulates: D = W + A U^T (+ H (hi, mid, lo)^T).
             const uint32_t idesc = tc::idesc_bf16_m128(p.nu_pad);
             mbar_wait(ufull, 0);
             tc::fence_after();
@@ -376,8 +441,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             uint32_t gb = 0;
             for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++it) {
                 const int acc = it % kAccStages;
-                const uint32_t around = it / kAccStages;
-                if (around > 0) mbar_wait(&tempty[acc], (around - 1) & 1);   // epilogue drained it
+                mbar_wait(&wready[acc], (it / kAccStages) & 1);
+                tc::fence_after();
                 const uint32_t d_tmem = tmem_base + (uint32_t)(acc * 128);
                 for (int kb = 0; kb < nkt; ++kb, ++gb) {
                     const uint32_t slot = gb % p.stages;
@@ -392,51 +457,103 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                         const uint64_t db0 = tc::sdesc_sw128(sU + (size_t)(ub0 + pc) * p.nu_pad * 128);
 #pragma unroll
                         for (int k = 0; k < kBlockK / 16; ++k)   // +32 bytes per K step inside the swizzle row
-                            tc::umma_f16(d_tmem, da0 + (uint64_t)(k * 2), db0 + (uint64_t)(k * 2), idesc,
-                                         (kb | pc | k) != 0);
+                            tc::umma_f16(d_tmem, da0 + (uint64_t)(k * 2), db0 + (uint64_t)(k * 2), idesc, 1u);
                     }
                     tc::umma_commit(&empty[slot]);     // ring stage free once these MMAs completed
                 }
                 tc::umma_commit(&tfull[acc]);      // accumulator ready for the epilogue
             }
         }
-    } else if (warp >= 4) {
-        // ---------------- epilogue: TMEM -> registers, fuse, key, filter ----------------
-        const int e = warp - 4;
+    } else if (warp >= kLoadWarp0) {
+        // ---------------- wide loaders: W -> TMEM accumulator stage (before the MMA) ----------------
+        // loader warp l owns TMEM lane quadrant q (rows q*32..q*32+31) and users c..c+31.  The
+        // global loads of tile it are issued before waiting for the stage, so their latency
+        // overlaps the epilogue of the tile that held it (kAccStages tiles earlier).
+        const int l = warp - kLoadWarp0;
+        const int q = warp & 3;
+        const int c = (l >> 2) * 32;
+        const int row = q * 32 + lane;
+        const bool pf = l == 0 && lane == 0;     // one thread streams the W blocks into L2 ahead
+        auto prefetch = [&](int t) {
+            if (t < p.n_tiles)
+                tc::bulk_prefetch_l2(p.ws.W + (size_t)t * p.tile_stride * kGroup * kTileM, (uint32_t)p.nu * kTileM * 4);
+        };
+        if (pf)
+            for (int k = 0; k < kWPrefetch; ++k) prefetch(blockIdx.x + k * gridDim.x);
+        int it = 0;
+        for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++it) {
+            const int acc = it % kAccStages;
+            const int64_t tw = (int64_t)t * p.tile_stride;              // global tile index
+            const bool valid = tw * kTileM + row < p.n_ads;
+            if (pf) prefetch(t + kWPrefetch * gridDim.x);
+            uint32_t wf[32];
+            if (c < p.nu_pad) {
+                const float* wcol = p.ws.W + ((size_t)tw * kGroup + c) * kTileM + row;
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    wf[j] = (valid && c + j < p.nu) ? __float_as_uint(__ldcg(wcol + (size_t)j * kTileM)) : 0u;
+            }
+            if (it >= kAccStages) mbar_wait(&tempty[acc], ((it / kAccStages) - 1) & 1);
+            tc::fence_after();
+            if (c < p.nu_pad) {
+                tc::tmem_st32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * 128 + c), wf);
+            }
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&wready[acc]);
+        }
+    } else if (warp >= kEpiWarp0) {
+        // ---------------- epilogue: TMEM -> registers, key, filter ----------------
+        const int e = warp - kEpiWarp0;
         const int q = warp & 3;                    // TMEM lane quadrant of this warp
-        const int c = (e >> 2) * 32;               // this warp's 32 accumulator columns (users)
         const int row = q * 32 + lane;             // ad row inside the tile
         int it = 0;
         for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++it) {
             const int acc = it % kAccStages;
             const int64_t a = (int64_t)t * p.tile_stride * kTileM + row;   // shard-local ad
             const bool valid = a < p.n_ads;
-            // this row's 32 wide scores: 32 independent loads (coalesced across the warp's
-            // consecutive ads), issued before waiting for the accumulator so they overlap the MMA
-            float wf[32];
-            {
-                const float* wcol = p.ws.W + (valid ? a : 0);
-#pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    wf[j] = (valid && c + j < p.nu) ? __ldcg(wcol + (size_t)(c + j) * p.n_pad) : 0.f;
-            }
             mbar_wait(&tfull[acc], (it / kAccStages) & 1);
             tc::fence_after();
-            if (c < p.nu_pad) {
+#pragma unroll 1
+            for (int ch = 0; ch < kEpiChunks; ++ch) {
+                const int c = (e >> 2) * (32 * kEpiChunks) + ch * 32;   // this chunk's 32 users
+                if (c >= p.nu_pad) break;
                 uint32_t r[32];
                 tc::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * 128 + c), r);
+                const int nuc = p.nu - c;                 // valid users in these 32 columns
+                const uint32_t umask = nuc >= 32 ? 0xFFFFFFFFu : (nuc > 0 ? (1u << nuc) - 1u : 0u);
+                if (MODE == 0) {
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const int u = c + j;
-                    const bool live = valid && u < p.nu;
-                    float s = __uint_as_float(r[j]) + wf[j];
-                    if (s == 0.f) s = 0.f;                       // -0 -> +0 (R14)
-                    if (MODE == 0) {
-                        if (u < p.nu) p.ws.samp[(size_t)u * p.n_samp + (int64_t)t * kTileM + row] =
-                            valid ? s : __int_as_float(0xFF800000);
-                    } else {
-                        const bool maybe = live && s >= sThetaS[u];   // cheap pre-filter
-                        if (__any_sync(FULL, maybe)) {
+                    for (int j = 0; j < 32; ++j) {
+                        float s = __uint_as_float(r[j]);
+                        if (s == 0.f) s = 0.f;                       // -0 -> +0 (R14)
+                        if ((umask >> j) & 1u)
+                            p.ws.samp[(size_t)(c + j) * p.n_samp + (int64_t)t * kTileM + row] =
+                                valid ? s : __int_as_float(0xFF800000);
+                    }
+                } else {
+                    // branch-free pre-filter of all 32 columns, then the exact key compare only
+                    // for the columns where some lane passed
+                    uint32_t pass = 0;
+                    const float4* th4 = reinterpret_cast<const float4*>(sThetaS + c);
+#pragma unroll
+                    for (int j4 = 0; j4 < 8; ++j4) {
+                        const float4 th = th4[j4];
+                        pass |= (__uint_as_float(r[j4 * 4 + 0]) >= th.x ? 1u : 0u) << (j4 * 4 + 0);
+                        pass |= (__uint_as_float(r[j4 * 4 + 1]) >= th.y ? 1u : 0u) << (j4 * 4 + 1);
+                        pass |= (__uint_as_float(r[j4 * 4 + 2]) >= th.z ? 1u : 0u) << (j4 * 4 + 2);
+                        pass |= (__uint_as_float(r[j4 * 4 + 3]) >= th.w ? 1u : 0u) << (j4 * 4 + 3);
+                    }
+                    pass &= valid ? umask : 0u;
+                    const uint32_t cols = __reduce_or_sync(FULL, pass);
+                    if (cols) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            if (!((cols >> j) & 1u)) continue;          // warp-uniform
+                            const int u = c + j;
+                            const bool maybe = (pass >> j) & 1u;
+                            float s = __uint_as_float(r[j]);
+                            if (s == 0.f) s = 0.f;                       // -0 -> +0 (R14)
                             const uint64_t key = maybe ? kappa_of(s, p.ad_begin + (uint32_t)a) : 0ull;
                             const bool take = maybe && key >= sTheta[u];
                             const unsigned m = __ballot_sync(FULL, take);
@@ -451,6 +568,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     }
                 }
             }
+            // every chunk of this stage is in registers (and consumed): hand it to the loaders
             tc::fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -459,7 +577,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     __syncwarp();
     tc::fence_before();
     __syncthreads();
-    if (warp == 2) tc::tmem_dealloc(tmem_base, 256);
+    if (warp == 2) tc::tmem_dealloc(tmem_base, kAccStages * 128);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -637,7 +755,7 @@ static bool encode_2d_bf16(CUtensorMap* m, const void* base, uint64_t inner, uin
 }
 
 struct Layout {
-    size_t header, items, chunk_off, U, W, samp, theta, count, cand, overflow, user_item, span, span_lo, total;
+    size_t header, items, chunk_off, U, W, samp, theta, count, cand, overflow, user_item, user_shift, span, span_lo, total;
     int64_t cap, n_samp, cap_items, nj;
 };
 
@@ -661,6 +779,7 @@ static Layout layout(const ebr_index* idx, int32_t slots, int32_t k) {
     L.overflow = o;  o = al(o + (size_t)kGroup * 4);
     L.nj = (idx->n_pad + kWideR - 1) / kWideR;
     L.user_item = o; o = al(o + (size_t)(kGroup + 1) * 4);
+    L.user_shift = o; o = al(o + (size_t)kGroup * 4);
     L.span = o;      o = al(o + (size_t)L.cap_items * (L.nj + 1) * 4);
     L.span_lo = o;   o = al(o + (size_t)L.cap_items * L.nj * 4);
     L.total = o;
@@ -680,6 +799,7 @@ static BatchWs carve(char* base, const Layout& L) {
     w.cand = reinterpret_cast<uint64_t*>(base + L.cand);
     w.overflow = reinterpret_cast<uint32_t*>(base + L.overflow);
     w.user_item = reinterpret_cast<uint32_t*>(base + L.user_item);
+    w.user_shift = reinterpret_cast<int32_t*>(base + L.user_shift);
     w.span = reinterpret_cast<uint32_t*>(base + L.span);
     w.span_lo = reinterpret_cast<uint32_t*>(base + L.span_lo);
     return w;
@@ -710,7 +830,7 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
     const int n_samp_tiles = (int)(L.n_samp / kTileM);
     cudaError_t e = cudaMemsetAsync(ws.overflow, 0, (size_t)kGroup * 4, q.stream);
     if (e != cudaSuccess) return cuda_check(e, "memset(overflow)");
-    e = cudaFuncSetAttribute(wide_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kWideR * 8);
+    e = cudaFuncSetAttribute(wide_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kWideR * 4);
     if (e != cudaSuccess) return cuda_check(e, "attr(wide)");
     CUtensorMap tmA, tmH;
     if (!encode_2d_bf16(&tmA, idx->A, (uint64_t)idx->d_pad, (uint64_t)idx->n_pad, kBlockK, kTileM))
@@ -735,7 +855,7 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
         const int nu = std::min(kGroup, q.batch - g0);
         const int nu_pad = (nu + 31) & ~31;
         // hot K blocks: as many as fit next to the resident user tile with >= 4 ring stages
-        const size_t fixed = 1024 + 256 + (size_t)kGroup * 12;
+        const size_t fixed = 1024 + 512 + (size_t)kGroup * 12;
         auto smem_of = [&](int hb, int st) {
             return fixed + (((size_t)nu_pad * 128 * (n_kb + kHotPieces * hb) + 1023) & ~(size_t)1023) +
                    (size_t)st * kBlockBytes;
@@ -758,7 +878,7 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
         const int max_items = nu * idx->n_fields * q.slots;
         span_kernel<<<(max_items + 7) / 8, 256, 0, q.stream>>>(idx->chunk_hdr, idx->chunk_last, ws, (int)L.nj,
                                                                (int)L.cap_items);
-        wide_smem_kernel<<<dim3((unsigned)L.nj, (unsigned)nu), kWideThreads, kWideR * 8, q.stream>>>(
+        wide_smem_kernel<<<dim3((unsigned)L.nj, (unsigned)nu), kWideThreads, kWideR * 4, q.stream>>>(
             idx->chunk_hdr, idx->payload, ws, (int)L.nj, idx->n_pad, (int)L.cap_items);
         GemmParams gp;
         gp.n_ads = idx->n_ads; gp.n_pad = idx->n_pad; gp.ad_begin = (uint32_t)idx->ad_begin;
