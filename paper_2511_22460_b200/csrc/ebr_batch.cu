@@ -1,21 +1,20 @@
 // ebr_batch.cu -- the batched path (bf16 embeddings, user batch >= 16): the deep score is a dense
 // contraction D[ads x users] = A . U^T (Eq. 1 / Eq. 8 for every (user, ad) pair) and runs on the
-// 5th-generation tensor cores: TMA loads 128-ad x 64-dim tiles (128-byte swizzle), one elected
-// thread issues tcgen05.mma (kind::f16, bf16 inputs, fp32 accumulator in TMEM, M=128, N=users),
-// four epilogue warps read the accumulator with tcgen05.ld and fuse the wide term, the score key
-// and the top-K filter.  Per group of up to 128 users, one call runs:
+// 5th-generation tensor cores, together with the wide term of the hot keys (the longest posting
+// lists, kept as dense one-hot columns H of L -- DESIGN.md R22): D = W + A U_deep^T + H U_hot^T,
+// where U_hot holds each user's w~ as three exact bf16 terms and W is the cold keys' wide term
+// decoded from the compressed inverted lists.  Per group of up to 128 users, one call runs:
 //
-//   1. plan_kernel     A1 for the group: work items (key, w~, chunk span), flat chunk offsets,
-//                      and the group's user embeddings as a zero-padded bf16 tile
-//   2. span_kernel     for every item and 16k-ad chunk, where the item's postings enter the chunk
-//      wide_smem_kernel A2+A3: CTA (ad chunk, user) decodes the user's postings in its chunk and
-//                      accumulates w~ in shared memory (Alg. 2 l.358), then writes W[user][ad]
-//   3. gemm_kernel<0>  A4+A5 on a strided 1/16 sample of the ad tiles: s = deep + wide, stored
+//   1. plan_kernel     A1: hot slots -> U_hot (hi, mid, lo), cold slots -> work items, the per-user
+//                      fixed-point scale, and the deep part of the bf16 user tile U
+//   2. span_kernel     for every cold item and kWideR-ad range, the chunks holding ids in the range
+//      wide_smem_kernel A2+A3 for cold keys: CTA (range, user) decodes the user's postings in the
+//                      range and accumulates w~ in shared memory (Alg. 2 l.358), then writes W
+//   3. gemm_kernel<0>  A4+A5 on a strided 1/16 sample of the ad tiles: s = W + deep + hot, stored
 //   4. theta_kernel    A6a per user: theta_u = the K-th largest key among the sampled ads.  The
 //                      sample is a subset of the inventory, so at least K ads have key >= theta_u
 //                      and the top-K is contained in {key >= theta_u} -- exact, not heuristic.
-//   5. gemm_kernel<1>  A4+A5+A6b on every tile: s = deep + wide,
-//                      keys >= theta_u appended to the user's candidate list
+//   5. gemm_kernel<1>  A4+A5+A6b on every tile: keys >= theta_u appended to the user's candidates
 //   6. final_kernel    A6c per user: exact radix select + sort of the candidates
 //   A user whose candidate list overflowed (possible only for massively tied scores) is recomputed
 //   by the latency path after a single stream synchronisation at the end of the call.
@@ -57,7 +56,8 @@ struct BatchWs {   // workspace carve-up (device pointers)
     BItem* items;         // [cap_items]
     uint64_t* chunk_off;  // [cap_items + 1]
     __nv_bfloat16* U;     // [kGroup][d_pad]
-    float* W;             // [n_tiles][kGroup][128] tile-major: one tile's block is contiguous
+    float* W;             // [n_tiles][kGroup][128] tile-major value slabs (sparse: compacted prefix)
+    uint32_t* Wm;         // [n_tiles][kGroup][4] row masks of the sparse W
     float* samp;          // [kGroup][n_samp]
     uint64_t* theta;      // [kGroup]
     uint32_t* cand_count; // [kGroup]
@@ -70,10 +70,13 @@ struct BatchWs {   // workspace carve-up (device pointers)
 };
 
 #ifndef EBR_WIDE_R
-#define EBR_WIDE_R 32768
+#define EBR_WIDE_R 24576
+#endif
+#ifndef EBR_SPARSE_W
+#define EBR_SPARSE_W 0
 #endif
 #ifndef EBR_WIDE_T
-#define EBR_WIDE_T 1024
+#define EBR_WIDE_T 512
 #endif
 constexpr int kWideR = EBR_WIDE_R;     // ads per shared-memory accumulation chunk (int32 each)
 
@@ -330,6 +333,31 @@ __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks > 0 ? kWideMinBlo
     }
     const float inv = ldexpf(1.f, -S);
     const int64_t t0 = a0 / kTileM;
+#if EBR_SPARSE_W
+    // sparse W: per (tile, user) a 128-bit mask of the rows with a nonzero cold sum and the values
+    // of those rows compacted to the front of the (tile, user) slab (cold hits touch ~15% of the
+    // pairs at C3), so the GEMM's wide loaders read ~1/5 of the dense bytes
+    const int ntl = (int)((a1 - a0) / kTileM);
+    for (int tl = warp; tl < ntl; tl += nwarps) {
+        const int64_t t = t0 + tl;
+        int32_t v[4];
+        uint32_t m[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            v[q] = acc[tl * kTileM + q * 32 + lane];
+            m[q] = __ballot_sync(FULL, v[q] != 0);
+        }
+        if (lane == 0)
+            __stcg(reinterpret_cast<uint4*>(ws.Wm) + (size_t)t * kGroup + u, make_uint4(m[0], m[1], m[2], m[3]));
+        float* slab = ws.W + ((size_t)t * kGroup + u) * kTileM;
+        uint32_t base = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (v[q]) __stcg(slab + base + __popc(m[q] & ((1u << lane) - 1u)), (float)v[q] * inv);  // the one rounding
+            base += __popc(m[q]);
+        }
+    }
+#else
     // dense W[tile][u][row]: the chunk spans (a1 - a0) / 128 tiles; 32 float4 per (tile, user) row
     const int4* a4 = reinterpret_cast<const int4*>(acc);
     for (int64_t i = tid; i < (a1 - a0) / 4; i += kWideThreads) {
@@ -342,6 +370,7 @@ __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks > 0 ? kWideMinBlo
         const int64_t t = t0 + (i >> 5);
         __stcg(reinterpret_cast<float4*>(ws.W + ((size_t)t * kGroup + u) * kTileM) + (i & 31), o);
     }
+#endif
 }
 
 // ------------------------------------------------------------------------------------------
@@ -475,11 +504,35 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         const int row = q * 32 + lane;
         const bool pf = l == 0 && lane == 0;     // one thread streams the W blocks into L2 ahead
         auto prefetch = [&](int t) {
-            if (t < p.n_tiles)
+            if (t < p.n_tiles) {
+#if EBR_SPARSE_W
+                tc::bulk_prefetch_l2(p.ws.Wm + (size_t)t * p.tile_stride * kGroup * 4, (uint32_t)p.nu * 16);
+#else
                 tc::bulk_prefetch_l2(p.ws.W + (size_t)t * p.tile_stride * kGroup * kTileM, (uint32_t)p.nu * kTileM * 4);
+#endif
+            }
         };
         if (pf)
             for (int k = 0; k < kWPrefetch; ++k) prefetch(blockIdx.x + k * gridDim.x);
+#if EBR_SPARSE_W
+        // lane j holds user (c+j)'s row-mask word for this warp's quadrant and the count of set
+        // rows in the quadrants before it; loaded one tile ahead
+        auto load_mask = [&](int t, uint32_t& w, uint32_t& bse) {
+            w = 0u; bse = 0u;
+            if (t < p.n_tiles && c + lane < p.nu) {
+                const uint4 mk = __ldcg(reinterpret_cast<const uint4*>(p.ws.Wm) +
+                                        (size_t)t * p.tile_stride * kGroup + c + lane);
+                const uint32_t wd[4] = {mk.x, mk.y, mk.z, mk.w};
+#pragma unroll
+                for (int qq = 0; qq < 4; ++qq) {
+                    if (qq < q) bse += __popc(wd[qq]);
+                    if (qq == q) w = wd[qq];
+                }
+            }
+        };
+        uint32_t mw, mb;
+        load_mask(blockIdx.x, mw, mb);
+#endif
         int it = 0;
         for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++it) {
             const int acc = it % kAccStages;
@@ -488,10 +541,24 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             if (pf) prefetch(t + kWPrefetch * gridDim.x);
             uint32_t wf[32];
             if (c < p.nu_pad) {
+#if EBR_SPARSE_W
+                const uint32_t lt = (1u << lane) - 1u;
+                const float* slab0 = p.ws.W + ((size_t)tw * kGroup + c) * kTileM;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const uint32_t m = __shfl_sync(FULL, mw, j);
+                    const uint32_t b = __shfl_sync(FULL, mb, j);
+                    wf[j] = ((m >> lane) & 1u) ? __float_as_uint(__ldcg(slab0 + (size_t)j * kTileM + b + __popc(m & lt)))
+                                               : 0u;
+                }
+                load_mask(t + gridDim.x, mw, mb);               // next tile's masks in flight
+                (void)valid;
+#else
                 const float* wcol = p.ws.W + ((size_t)tw * kGroup + c) * kTileM + row;
 #pragma unroll
                 for (int j = 0; j < 32; ++j)
                     wf[j] = (valid && c + j < p.nu) ? __float_as_uint(__ldcg(wcol + (size_t)j * kTileM)) : 0u;
+#endif
             }
             if (it >= kAccStages) mbar_wait(&tempty[acc], ((it / kAccStages) - 1) & 1);
             tc::fence_after();
@@ -755,7 +822,7 @@ static bool encode_2d_bf16(CUtensorMap* m, const void* base, uint64_t inner, uin
 }
 
 struct Layout {
-    size_t header, items, chunk_off, U, W, samp, theta, count, cand, overflow, user_item, user_shift, span, span_lo, total;
+    size_t header, items, chunk_off, U, W, samp, theta, count, cand, overflow, user_item, user_shift, Wm, span, span_lo, total;
     int64_t cap, n_samp, cap_items, nj;
 };
 
@@ -780,6 +847,7 @@ static Layout layout(const ebr_index* idx, int32_t slots, int32_t k) {
     L.nj = (idx->n_pad + kWideR - 1) / kWideR;
     L.user_item = o; o = al(o + (size_t)(kGroup + 1) * 4);
     L.user_shift = o; o = al(o + (size_t)kGroup * 4);
+    L.Wm = o;        o = al(o + (size_t)(idx->n_pad / kTileM) * kGroup * 16);
     L.span = o;      o = al(o + (size_t)L.cap_items * (L.nj + 1) * 4);
     L.span_lo = o;   o = al(o + (size_t)L.cap_items * L.nj * 4);
     L.total = o;
@@ -800,6 +868,7 @@ static BatchWs carve(char* base, const Layout& L) {
     w.overflow = reinterpret_cast<uint32_t*>(base + L.overflow);
     w.user_item = reinterpret_cast<uint32_t*>(base + L.user_item);
     w.user_shift = reinterpret_cast<int32_t*>(base + L.user_shift);
+    w.Wm = reinterpret_cast<uint32_t*>(base + L.Wm);
     w.span = reinterpret_cast<uint32_t*>(base + L.span);
     w.span_lo = reinterpret_cast<uint32_t*>(base + L.span_lo);
     return w;
