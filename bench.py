@@ -41,8 +41,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="few steps, no side measurements (for ncu)")
-    ap.add_argument("--no-graph", action="store_true",
-                    help="launch the library call directly every step instead of replaying a CUDA graph of it")
+    ap.add_argument("--graph", action="store_true",
+                    help="replay a CUDA graph of the library call each step (latency path, 1 GPU); measured "
+                         "no faster than the direct call (profiles/r01_mb_launch.txt), so off by default")
     return ap.parse_args()
 
 
@@ -263,10 +264,10 @@ def main():
         shard.query(emb, feat, x, K, ids, sc, stream, local_keys=keys, gathered=gathered)
 
     step = call
-    # One GPU, latency path: the step is replayed as a CUDA graph of the library call (the same
-    # cooperative kernel, enqueued without the per-call host work -- what a serving loop does).
-    # The batched path synchronises once per call (overflow check) and is launched directly.
-    use_graph = (world == 1 and not args.no_graph
+    # --graph (1 GPU, latency path): replay a CUDA graph of the library call (the same cooperative
+    # kernel, enqueued without the per-call host work).  The batched path synchronises once per
+    # call (overflow check) and is always launched directly.
+    use_graph = (world == 1 and args.graph
                  and idx.query_launches(B, S, K) == (B + 3) // 4)
     for _ in range(max(args.warmup, 3)):
         call()

@@ -37,12 +37,15 @@ constexpr int kBlockK = 64;          // bf16 elements per 128-byte swizzle row
 constexpr int kSampleStride = 16;    // every 16th tile is sampled for theta
 constexpr int kEpiWarps = 8;         // 2 per TMEM lane quadrant, two 32-column chunks each
 constexpr int kEpiChunks = kGroup / 32 / (kEpiWarps / 4);
-constexpr int kLoadWarps = 16;       // 4 per TMEM lane quadrant, one 32-column chunk each
+constexpr int kLoadWarps = 4;        // one per TMEM lane quadrant, every 32-column chunk in turn
 constexpr int kEpiWarp0 = 4;
 constexpr int kLoadWarp0 = kEpiWarp0 + kEpiWarps;
-constexpr int kGemmThreads = 32 * (kLoadWarp0 + kLoadWarps);   // 0 TMA, 1 MMA, 2 TMEM alloc, 3 idle
+constexpr int kGemmThreads = 32 * (kLoadWarp0 + kLoadWarps);   // 0 TMA, 1 MMA, 2 TMEM alloc, 3 W bulk copies
 constexpr int kAccStages = 4;        // TMEM: 4 x 128 columns = all 512
-constexpr int kWPrefetch = 4;        // tiles of W streamed into L2 ahead of the loader warps
+#ifndef EBR_WPF
+#define EBR_WPF 4
+#endif
+constexpr int kWPrefetch = EBR_WPF;  // tiles of W streamed into L2 ahead of their bulk copies
 constexpr int kHotPieces = 3;        // w~ = hi + mid + lo in bf16: 24 significant bits, exact (R22)
 constexpr int kBlockBytes = kTileM * 128;   // one ring stage: 128 ads x 64 bf16 (one K block)
 
@@ -56,8 +59,7 @@ struct BatchWs {   // workspace carve-up (device pointers)
     BItem* items;         // [cap_items]
     uint64_t* chunk_off;  // [cap_items + 1]
     __nv_bfloat16* U;     // [kGroup][d_pad]
-    float* W;             // [n_tiles][kGroup][128] tile-major value slabs (sparse: compacted prefix)
-    uint32_t* Wm;         // [n_tiles][kGroup][4] row masks of the sparse W
+    float* W;             // [n_tiles][kGroup][128] tile-major: a tile's 32-user chunk is 16 KB contiguous
     float* samp;          // [kGroup][n_samp]
     uint64_t* theta;      // [kGroup]
     uint32_t* cand_count; // [kGroup]
@@ -72,8 +74,8 @@ struct BatchWs {   // workspace carve-up (device pointers)
 #ifndef EBR_WIDE_R
 #define EBR_WIDE_R 24576
 #endif
-#ifndef EBR_SPARSE_W
-#define EBR_SPARSE_W 0
+#ifndef EBR_W_RING
+#define EBR_W_RING 1
 #endif
 #ifndef EBR_WIDE_T
 #define EBR_WIDE_T 512
@@ -333,31 +335,6 @@ __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks > 0 ? kWideMinBlo
     }
     const float inv = ldexpf(1.f, -S);
     const int64_t t0 = a0 / kTileM;
-#if EBR_SPARSE_W
-    // sparse W: per (tile, user) a 128-bit mask of the rows with a nonzero cold sum and the values
-    // of those rows compacted to the front of the (tile, user) slab (cold hits touch ~15% of the
-    // pairs at C3), so the GEMM's wide loaders read ~1/5 of the dense bytes
-    const int ntl = (int)((a1 - a0) / kTileM);
-    for (int tl = warp; tl < ntl; tl += nwarps) {
-        const int64_t t = t0 + tl;
-        int32_t v[4];
-        uint32_t m[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            v[q] = acc[tl * kTileM + q * 32 + lane];
-            m[q] = __ballot_sync(FULL, v[q] != 0);
-        }
-        if (lane == 0)
-            __stcg(reinterpret_cast<uint4*>(ws.Wm) + (size_t)t * kGroup + u, make_uint4(m[0], m[1], m[2], m[3]));
-        float* slab = ws.W + ((size_t)t * kGroup + u) * kTileM;
-        uint32_t base = 0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if (v[q]) __stcg(slab + base + __popc(m[q] & ((1u << lane) - 1u)), (float)v[q] * inv);  // the one rounding
-            base += __popc(m[q]);
-        }
-    }
-#else
     // dense W[tile][u][row]: the chunk spans (a1 - a0) / 128 tiles; 32 float4 per (tile, user) row
     const int4* a4 = reinterpret_cast<const int4*>(acc);
     for (int64_t i = tid; i < (a1 - a0) / 4; i += kWideThreads) {
@@ -370,7 +347,6 @@ __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks > 0 ? kWideMinBlo
         const int64_t t = t0 + (i >> 5);
         __stcg(reinterpret_cast<float4*>(ws.W + ((size_t)t * kGroup + u) * kTileM) + (i & 31), o);
     }
-#endif
 }
 
 // ------------------------------------------------------------------------------------------
@@ -386,7 +362,8 @@ struct GemmParams {
     int n_tiles;           // tiles to process in this launch
     int tile_stride;       // 1 (all tiles) or kSampleStride (sample)
     int n_samp;            // sample buffer row length (ads)
-    int stages;
+    int stages;            // A/H ring stages (16 KB each)
+    int wstages;           // W ring stages (one 32-user x 128-ad fp32 chunk = 16 KB each)
     int64_t cap;           // candidate capacity per user
     BatchWs ws;
 };
@@ -402,10 +379,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     const int nkt = p.n_kb + p.n_hb;                                // A-side K blocks per tile
     unsigned char* sU = smem;                                       // [u_blocks][nu_pad rows x 128 B]
     unsigned char* sA = smem + ((u_bytes + 1023) & ~1023);          // ring: [stages][128 x 128 B]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sA + (size_t)p.stages * kBlockBytes);
+    float* sW = reinterpret_cast<float*>(sA + (size_t)p.stages * kBlockBytes);   // [wstages][32][128]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sA + (size_t)(p.stages + p.wstages) * kBlockBytes);
     uint64_t* full = bars;                       // [stages]
     uint64_t* empty = bars + p.stages;           // [stages]
-    uint64_t* tfull = bars + 2 * p.stages;       // [kAccStages] MMA done -> epilogue
+    uint64_t* wfull = bars + 2 * p.stages;       // [wstages] W chunk landed
+    uint64_t* wempty = wfull + p.wstages;        // [wstages] W chunk read by its 4 loader warps
+    uint64_t* tfull = wempty + p.wstages;        // [kAccStages] MMA done -> epilogue
     uint64_t* tempty = tfull + kAccStages;       // [kAccStages] epilogue drained -> wide loaders
     uint64_t* wready = tempty + kAccStages;      // [kAccStages] wide term stored -> MMA
     uint64_t* ufull = wready + kAccStages;
@@ -415,6 +395,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 
     if (tid == 0) {
         for (int s = 0; s < p.stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int s = 0; s < p.wstages; ++s) { mbar_init(&wfull[s], 1); mbar_init(&wempty[s], 4); }
         for (int s = 0; s < kAccStages; ++s) {
             mbar_init(&tfull[s], 1);
             mbar_init(&tempty[s], kEpiWarps);
@@ -444,6 +425,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             for (int kb = 0; kb < p.u_blocks; ++kb)
                 tc::tma_load_2d(sU + (size_t)kb * p.nu_pad * 128, &tmU, kb * kBlockK, 0, ufull);
             uint32_t gb = 0;                                 // ring position (one K block per stage)
+            const uint64_t pol = tc::policy_evict_first();   // A and H are read once per pass
             for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
                 const int row0 = t * p.tile_stride * kTileM;
                 for (int kb = 0; kb < nkt; ++kb, ++gb) {
@@ -451,10 +433,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     if (round > 0) mbar_wait(&empty[slot], (round - 1) & 1);
                     mbar_arrive_expect_tx(&full[slot], (uint32_t)kBlockBytes);
                     if (kb < p.n_kb)
-                        tc::tma_load_2d(sA + (size_t)slot * kBlockBytes, &tmA, kb * kBlockK, row0, &full[slot]);
+                        tc::tma_load_2d_hint(sA + (size_t)slot * kBlockBytes, &tmA, kb * kBlockK, row0, &full[slot], pol);
                     else
-                        tc::tma_load_2d(sA + (size_t)slot * kBlockBytes, &tmH, (kb - p.n_kb) * kBlockK, row0,
-                                        &full[slot]);
+                        tc::tma_load_2d_hint(sA + (size_t)slot * kBlockBytes, &tmH, (kb - p.n_kb) * kBlockK, row0,
+                                             &full[slot], pol);
                 }
             }
         }
@@ -493,76 +475,60 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 tc::umma_commit(&tfull[acc]);      // accumulator ready for the epilogue
             }
         }
-    } else if (warp >= kLoadWarp0) {
-        // ---------------- wide loaders: W -> TMEM accumulator stage (before the MMA) ----------------
-        // loader warp l owns TMEM lane quadrant q (rows q*32..q*32+31) and users c..c+31.  The
-        // global loads of tile it are issued before waiting for the stage, so their latency
-        // overlaps the epilogue of the tile that held it (kAccStages tiles earlier).
-        const int l = warp - kLoadWarp0;
-        const int q = warp & 3;
-        const int c = (l >> 2) * 32;
-        const int row = q * 32 + lane;
-        const bool pf = l == 0 && lane == 0;     // one thread streams the W blocks into L2 ahead
-        auto prefetch = [&](int t) {
-            if (t < p.n_tiles) {
-#if EBR_SPARSE_W
-                tc::bulk_prefetch_l2(p.ws.Wm + (size_t)t * p.tile_stride * kGroup * 4, (uint32_t)p.nu * 16);
-#else
-                tc::bulk_prefetch_l2(p.ws.W + (size_t)t * p.tile_stride * kGroup * kTileM, (uint32_t)p.nu * kTileM * 4);
-#endif
-            }
-        };
-        if (pf)
+    } else if (warp == 3) {
+        if (lane == 0) {
+            // ---------------- W producer: the tile's 16 KB user chunks of W -> smem ring ----------------
+            // (bulk copies, the blocks streamed into L2 kWPrefetch tiles ahead)
+            const int nwc = p.nu_pad / 32;
+            const uint64_t keep = tc::policy_evict_last(), drop = tc::policy_evict_first();
+            auto prefetch = [&](int t) {     // held in L2 (evict_last) until its bulk copy reads it
+                if (t < p.n_tiles)
+                    tc::bulk_prefetch_l2_hint(p.ws.W + (size_t)t * p.tile_stride * kGroup * kTileM,
+                                              (uint32_t)p.nu_pad * kTileM * 4, keep);
+            };
             for (int k = 0; k < kWPrefetch; ++k) prefetch(blockIdx.x + k * gridDim.x);
-#if EBR_SPARSE_W
-        // lane j holds user (c+j)'s row-mask word for this warp's quadrant and the count of set
-        // rows in the quadrants before it; loaded one tile ahead
-        auto load_mask = [&](int t, uint32_t& w, uint32_t& bse) {
-            w = 0u; bse = 0u;
-            if (t < p.n_tiles && c + lane < p.nu) {
-                const uint4 mk = __ldcg(reinterpret_cast<const uint4*>(p.ws.Wm) +
-                                        (size_t)t * p.tile_stride * kGroup + c + lane);
-                const uint32_t wd[4] = {mk.x, mk.y, mk.z, mk.w};
-#pragma unroll
-                for (int qq = 0; qq < 4; ++qq) {
-                    if (qq < q) bse += __popc(wd[qq]);
-                    if (qq == q) w = wd[qq];
+            uint32_t g = 0;
+            for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
+                prefetch(t + kWPrefetch * gridDim.x);
+                const float* src = p.ws.W + (size_t)t * p.tile_stride * kGroup * kTileM;
+                for (int ch = 0; ch < nwc; ++ch, ++g) {
+                    const uint32_t slot = g % p.wstages, round = g / p.wstages;
+                    if (round > 0) mbar_wait(&wempty[slot], (round - 1) & 1);
+                    mbar_arrive_expect_tx(&wfull[slot], (uint32_t)kBlockBytes);
+                    tc::bulk_g2s_hint(sW + (size_t)slot * 32 * kTileM, src + (size_t)ch * 32 * kTileM,
+                                      (uint32_t)kBlockBytes, &wfull[slot], drop);
                 }
             }
-        };
-        uint32_t mw, mb;
-        load_mask(blockIdx.x, mw, mb);
-#endif
+        }
+    } else if (warp >= kLoadWarp0) {
+        // ---------------- wide loaders: W -> TMEM accumulator stage (before the MMA) ----------------
+        // loader warp q owns TMEM lane quadrant q (rows q*32..q*32+31) and walks the tile's 32-user
+        // chunks in ring order (the 4 loader warps are the only consumers of every W slot and take
+        // them strictly in sequence, so mbarrier parities never alias): read its 32 x 32 block
+        // from smem (conflict-free: lanes read consecutive rows), free the slot, and store the block
+        // into the accumulator stage once the epilogue has drained it (kAccStages tiles earlier).
+        const int q = warp & 3;
+        const int row = q * 32 + lane;
+        const int nwc = p.nu_pad / 32;
         int it = 0;
+        uint32_t g = 0;
         for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++it) {
             const int acc = it % kAccStages;
             const int64_t tw = (int64_t)t * p.tile_stride;              // global tile index
             const bool valid = tw * kTileM + row < p.n_ads;
-            if (pf) prefetch(t + kWPrefetch * gridDim.x);
-            uint32_t wf[32];
-            if (c < p.nu_pad) {
-#if EBR_SPARSE_W
-                const uint32_t lt = (1u << lane) - 1u;
-                const float* slab0 = p.ws.W + ((size_t)tw * kGroup + c) * kTileM;
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const uint32_t m = __shfl_sync(FULL, mw, j);
-                    const uint32_t b = __shfl_sync(FULL, mb, j);
-                    wf[j] = ((m >> lane) & 1u) ? __float_as_uint(__ldcg(slab0 + (size_t)j * kTileM + b + __popc(m & lt)))
-                                               : 0u;
-                }
-                load_mask(t + gridDim.x, mw, mb);               // next tile's masks in flight
-                (void)valid;
-#else
-                const float* wcol = p.ws.W + ((size_t)tw * kGroup + c) * kTileM + row;
+            for (int ch = 0; ch < nwc; ++ch, ++g) {
+                const int c = ch * 32;
+                const uint32_t slot = g % p.wstages;
+                mbar_wait(&wfull[slot], (g / p.wstages) & 1);
+                const float* w = sW + (size_t)slot * 32 * kTileM + row;
+                uint32_t wf[32];
 #pragma unroll
                 for (int j = 0; j < 32; ++j)
-                    wf[j] = (valid && c + j < p.nu) ? __float_as_uint(__ldcg(wcol + (size_t)j * kTileM)) : 0u;
-#endif
-            }
-            if (it >= kAccStages) mbar_wait(&tempty[acc], ((it / kAccStages) - 1) & 1);
-            tc::fence_after();
-            if (c < p.nu_pad) {
+                    wf[j] = (valid && c + j < p.nu) ? __float_as_uint(w[j * kTileM]) : 0u;
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&wempty[slot]);
+                if (ch == 0 && it >= kAccStages) mbar_wait(&tempty[acc], ((it / kAccStages) - 1) & 1);
+                tc::fence_after();
                 tc::tmem_st32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * 128 + c), wf);
             }
             tc::fence_before();
@@ -822,7 +788,7 @@ static bool encode_2d_bf16(CUtensorMap* m, const void* base, uint64_t inner, uin
 }
 
 struct Layout {
-    size_t header, items, chunk_off, U, W, samp, theta, count, cand, overflow, user_item, user_shift, Wm, span, span_lo, total;
+    size_t header, items, chunk_off, U, W, samp, theta, count, cand, overflow, user_item, user_shift, span, span_lo, total;
     int64_t cap, n_samp, cap_items, nj;
 };
 
@@ -847,7 +813,6 @@ static Layout layout(const ebr_index* idx, int32_t slots, int32_t k) {
     L.nj = (idx->n_pad + kWideR - 1) / kWideR;
     L.user_item = o; o = al(o + (size_t)(kGroup + 1) * 4);
     L.user_shift = o; o = al(o + (size_t)kGroup * 4);
-    L.Wm = o;        o = al(o + (size_t)(idx->n_pad / kTileM) * kGroup * 16);
     L.span = o;      o = al(o + (size_t)L.cap_items * (L.nj + 1) * 4);
     L.span_lo = o;   o = al(o + (size_t)L.cap_items * L.nj * 4);
     L.total = o;
@@ -868,7 +833,6 @@ static BatchWs carve(char* base, const Layout& L) {
     w.overflow = reinterpret_cast<uint32_t*>(base + L.overflow);
     w.user_item = reinterpret_cast<uint32_t*>(base + L.user_item);
     w.user_shift = reinterpret_cast<int32_t*>(base + L.user_shift);
-    w.Wm = reinterpret_cast<uint32_t*>(base + L.Wm);
     w.span = reinterpret_cast<uint32_t*>(base + L.span);
     w.span_lo = reinterpret_cast<uint32_t*>(base + L.span_lo);
     return w;
@@ -925,9 +889,10 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
         const int nu_pad = (nu + 31) & ~31;
         // hot K blocks: as many as fit next to the resident user tile with >= 4 ring stages
         const size_t fixed = 1024 + 512 + (size_t)kGroup * 12;
+        const int wstages = 2;
         auto smem_of = [&](int hb, int st) {
             return fixed + (((size_t)nu_pad * 128 * (n_kb + kHotPieces * hb) + 1023) & ~(size_t)1023) +
-                   (size_t)st * kBlockBytes;
+                   (size_t)(st + wstages) * kBlockBytes;
         };
         int n_hb = idx->n_hot / 64;
         if (getenv("EBR_NO_HOT")) n_hb = 0;
@@ -953,7 +918,7 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
         gp.n_ads = idx->n_ads; gp.n_pad = idx->n_pad; gp.ad_begin = (uint32_t)idx->ad_begin;
         gp.d_pad = idx->d_pad; gp.n_kb = n_kb; gp.n_hb = n_hb; gp.u_blocks = u_blocks;
         gp.nu = nu; gp.nu_pad = nu_pad;
-        gp.n_samp = (int)L.n_samp; gp.stages = stages; gp.cap = cap; gp.ws = ws;
+        gp.n_samp = (int)L.n_samp; gp.stages = stages; gp.wstages = wstages; gp.cap = cap; gp.ws = ws;
         const size_t smem = smem_of(n_hb, stages);
         // sample pass
         gp.n_tiles = n_samp_tiles; gp.tile_stride = kSampleStride;
