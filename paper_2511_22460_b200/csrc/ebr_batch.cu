@@ -430,7 +430,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 const int row0 = t * p.tile_stride * kTileM;
                 for (int kb = 0; kb < nkt; ++kb, ++gb) {
                     const uint32_t slot = gb % p.stages, round = gb / p.stages;
-                    if (round > 0) mbar_wait(&empty[slot], (round - 1) & 1);
+                    if (round > 0) mbar_wait_sleep(&empty[slot], (round - 1) & 1);
                     mbar_arrive_expect_tx(&full[slot], (uint32_t)kBlockBytes);
                     if (kb < p.n_kb)
                         tc::tma_load_2d_hint(sA + (size_t)slot * kBlockBytes, &tmA, kb * kBlockK, row0, &full[slot], pol);
@@ -446,18 +446,18 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             // The accumulator stage already holds the tile's wide term (stored by the loader warps),
             // so every MMA accumulates: D = W + A U^T (+ H (hi, mid, lo)^T).
             const uint32_t idesc = tc::idesc_bf16_m128(p.nu_pad);
-            mbar_wait(ufull, 0);
+            mbar_wait_sleep(ufull, 0);
             tc::fence_after();
             int it = 0;
             uint32_t gb = 0;
             for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++it) {
                 const int acc = it % kAccStages;
-                mbar_wait(&wready[acc], (it / kAccStages) & 1);
+                mbar_wait_sleep(&wready[acc], (it / kAccStages) & 1);
                 tc::fence_after();
                 const uint32_t d_tmem = tmem_base + (uint32_t)(acc * 128);
                 for (int kb = 0; kb < nkt; ++kb, ++gb) {
                     const uint32_t slot = gb % p.stages;
-                    mbar_wait(&full[slot], (gb / p.stages) & 1);
+                    mbar_wait_sleep(&full[slot], (gb / p.stages) & 1);
                     tc::fence_after();
                     const uint64_t da0 = tc::sdesc_sw128(sA + (size_t)slot * kBlockBytes);
                     // deep block kb pairs with user block kb; hot block h with its kHotPieces
@@ -493,7 +493,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 const float* src = p.ws.W + (size_t)t * p.tile_stride * kGroup * kTileM;
                 for (int ch = 0; ch < nwc; ++ch, ++g) {
                     const uint32_t slot = g % p.wstages, round = g / p.wstages;
-                    if (round > 0) mbar_wait(&wempty[slot], (round - 1) & 1);
+                    if (round > 0) mbar_wait_sleep(&wempty[slot], (round - 1) & 1);
                     mbar_arrive_expect_tx(&wfull[slot], (uint32_t)kBlockBytes);
                     tc::bulk_g2s_hint(sW + (size_t)slot * 32 * kTileM, src + (size_t)ch * 32 * kTileM,
                                       (uint32_t)kBlockBytes, &wfull[slot], drop);
@@ -519,7 +519,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             for (int ch = 0; ch < nwc; ++ch, ++g) {
                 const int c = ch * 32;
                 const uint32_t slot = g % p.wstages;
-                mbar_wait(&wfull[slot], (g / p.wstages) & 1);
+                mbar_wait_sleep(&wfull[slot], (g / p.wstages) & 1);
                 const float* w = sW + (size_t)slot * 32 * kTileM + row;
                 uint32_t wf[32];
 #pragma unroll
@@ -527,7 +527,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     wf[j] = (valid && c + j < p.nu) ? __float_as_uint(w[j * kTileM]) : 0u;
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&wempty[slot]);
-                if (ch == 0 && it >= kAccStages) mbar_wait(&tempty[acc], ((it / kAccStages) - 1) & 1);
+                if (ch == 0 && it >= kAccStages) mbar_wait_sleep(&tempty[acc], ((it / kAccStages) - 1) & 1);
                 tc::fence_after();
                 tc::tmem_st32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * 128 + c), wf);
             }
@@ -545,7 +545,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             const int acc = it % kAccStages;
             const int64_t a = (int64_t)t * p.tile_stride * kTileM + row;   // shard-local ad
             const bool valid = a < p.n_ads;
-            mbar_wait(&tfull[acc], (it / kAccStages) & 1);
+            mbar_wait_sleep(&tfull[acc], (it / kAccStages) & 1);
             tc::fence_after();
 #pragma unroll 1
             for (int ch = 0; ch < kEpiChunks; ++ch) {
@@ -578,14 +578,19 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                         pass |= (__uint_as_float(r[j4 * 4 + 3]) >= th.w ? 1u : 0u) << (j4 * 4 + 3);
                     }
                     pass &= valid ? umask : 0u;
-                    const uint32_t cols = __reduce_or_sync(FULL, pass);
-                    if (cols) {
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            if (!((cols >> j) & 1u)) continue;          // warp-uniform
+                    // compact (not unrolled) loop over the columns where some lane passed: the
+                    // unrolled form overflowed the instruction cache (ncu: no_instruction stalls)
+                    uint32_t cols = __reduce_or_sync(FULL, pass);
+#pragma unroll 1
+                    while (cols) {
+                        const int j = __ffs(cols) - 1;
+                        cols &= cols - 1u;
+                        {
                             const int u = c + j;
                             const bool maybe = (pass >> j) & 1u;
-                            float s = __uint_as_float(r[j]);
+                            float s = 0.f;
+#pragma unroll
+                            for (int jj = 0; jj < 32; ++jj) s = (jj == j) ? __uint_as_float(r[jj]) : s;
                             if (s == 0.f) s = 0.f;                       // -0 -> +0 (R14)
                             const uint64_t key = maybe ? kappa_of(s, p.ad_begin + (uint32_t)a) : 0ull;
                             const bool take = maybe && key >= sTheta[u];

@@ -210,6 +210,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity)
         : "memory");
 }
+// the same wait with a suspend-time hint: the thread sleeps in the barrier (woken when the phase
+// completes) instead of re-issuing try_wait, leaving issue slots to the warps that do the work
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+        : "memory");
+}
 // 1-D bulk copy global -> shared, completion counted on `bar` (bytes % 16 == 0, 16-B aligned)
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile(
