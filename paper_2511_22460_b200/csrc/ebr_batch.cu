@@ -229,6 +229,10 @@ __global__ void __launch_bounds__(256) span_kernel(const uint2* __restrict__ hdr
 // ------------------------------------------------------------------------------------------
 constexpr int kWideThreads = EBR_WIDE_T;
 constexpr int kWideItems = kWideThreads;   // items per pass of the unit scan
+#ifndef EBR_BUNIT
+#define EBR_BUNIT 8
+#endif
+constexpr int kBUnit = EBR_BUNIT;          // posting chunks per work unit (<= 32)
 constexpr int kWideMinBlocks = (2048 / kWideThreads) < (200 * 1024 / (kWideR * 4)) ? (2048 / kWideThreads)
                                                                                     : (200 * 1024 / (kWideR * 4));
 __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks > 0 ? kWideMinBlocks : 1) wide_smem_kernel(const uint2* __restrict__ hdr,
@@ -236,7 +240,7 @@ __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks > 0 ? kWideMinBlo
                                                                     BatchWs ws, int nj, int64_t n_pad,
                                                                     int cap_items) {
     extern __shared__ __align__(16) int32_t acc[];   // [kWideR]
-    __shared__ uint32_t sLo[kWideItems], sHi[kWideItems], sUoff[kWideItems + 1], sScan[40];
+    __shared__ uint32_t sLo[kWideItems], sHi[kWideItems], sUoff[kWideItems + 1], sScan[40], sCtr;
     __shared__ int32_t sF[kWideItems];
     __shared__ uint32_t sKwb[kWideItems];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = kWideThreads / 32;
@@ -257,7 +261,7 @@ __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks > 0 ? kWideMinBlo
             const BItem t = ws.items[it];
             lo = __ldcg(&ws.span_lo[(size_t)j * cap_items + it]);
             const uint32_t s1 = __ldcg(&ws.span[(size_t)(j + 1) * cap_items + it]);
-            nu_units = s1 > lo ? (s1 - lo + 15) / 16 : 0;
+            nu_units = s1 > lo ? (s1 - lo + kBUnit - 1) / kBUnit : 0;
             sF[tid] = (int32_t)__float2ll_rn(ldexpf(t.w, S));   // |w~ 2^S| < 2^30
             sHi[tid] = s1;
             sKwb[tid] = t.kwb;
@@ -265,30 +269,33 @@ __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks > 0 ? kWideMinBlo
         uint32_t tot;
         const uint32_t pre = block_exclusive_scan(nu_units, sScan, &tot);
         if ((uint32_t)tid < ni) { sLo[tid] = lo; sUoff[tid] = pre; }
-        if (tid == 0) sUoff[ni] = tot;
+        if (tid == 0) { sUoff[ni] = tot; sCtr = 0u; }
         __syncthreads();
-        // a warp's units (unit = warp, warp + nwarps, ...) are visited in increasing order, so the
-        // item index walks forward; software-pipelined: the next unit's chunk headers are in
-        // flight while this unit's payload words are extracted and scattered
-        struct BUnit { int l; uint32_t cb, nc; uint2 h; };
+        // units of up to kBUnit chunks are claimed dynamically from a shared counter (load balance
+        // across the CTA's warps; a warp's claims increase, so its item index walks forward) and
+        // software-pipelined: the next unit's chunk headers are in flight while this unit's
+        // payload words are extracted and scattered
+        struct BUnit { uint32_t unit; int l; uint32_t cb, nc; uint2 h; };
         int lw = 0;
-        auto start = [&](uint32_t unit) -> BUnit {
-            BUnit r{0, 0u, 0u, make_uint2(0u, 0u)};
-            if (unit < tot) {
-                while (sUoff[lw + 1] <= unit) ++lw;
+        auto start = [&]() -> BUnit {
+            uint32_t unit = 0;
+            if (lane == 0) unit = atomicAdd(&sCtr, 1u);
+            BUnit r{__shfl_sync(FULL, unit, 0), 0, 0u, 0u, make_uint2(0u, 0u)};
+            if (r.unit < tot) {
+                while (sUoff[lw + 1] <= r.unit) ++lw;
                 r.l = lw;
-                r.cb = sLo[lw] + (unit - sUoff[lw]) * 16;
-                r.nc = min(r.cb + 16, sHi[lw]) - r.cb;
+                r.cb = sLo[lw] + (r.unit - sUoff[lw]) * kBUnit;
+                r.nc = min(r.cb + kBUnit, sHi[lw]) - r.cb;
                 if ((uint32_t)lane < r.nc) r.h = __ldg(&hdr[r.cb + lane]);
             }
             return r;
         };
-        BUnit cur = start(warp);
-        for (uint32_t unit = warp; unit < tot; unit += nwarps) {
+        BUnit cur = start();
+        while (cur.unit < tot) {
             const uint32_t kwb = sKwb[cur.l];
-            uint32_t lo_w[16], hi_w[16];
+            uint32_t lo_w[kBUnit], hi_w[kBUnit];
 #pragma unroll
-            for (int qq = 0; qq < 16; ++qq) {
+            for (int qq = 0; qq < kBUnit; ++qq) {
                 lo_w[qq] = 0u;
                 hi_w[qq] = 0u;
                 if ((uint32_t)qq >= cur.nc) break;             // warp-uniform
@@ -301,10 +308,10 @@ __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks > 0 ? kWideMinBlo
                     hi_w[qq] = __ldg(&payload[wi + 1]);
                 }
             }
-            const BUnit nxt = start(unit + nwarps);          // overlaps this unit's payload round trip
+            const BUnit nxt = start();                       // overlaps this unit's payload round trip
             const int32_t Fv = sF[cur.l];
 #pragma unroll
-            for (int qq = 0; qq < 16; ++qq) {
+            for (int qq = 0; qq < kBUnit; ++qq) {
                 if ((uint32_t)qq >= cur.nc) break;
                 const uint32_t meta = __shfl_sync(FULL, cur.h.y, qq);
                 const uint32_t first = __shfl_sync(FULL, cur.h.x, qq);

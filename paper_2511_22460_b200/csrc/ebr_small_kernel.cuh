@@ -51,7 +51,10 @@ constexpr int kDeepWarps = EBR_DEEP_WARPS;      // stream A first, then help wit
 constexpr int kWideWarps = 16 - kDeepWarps;     // plan, then the wide queue from the start
 static_assert((kDeepWarps + kWideWarps) * 32 == kThreads, "CTA layout");
 constexpr int kUnroll = 8;       // 16-byte loads in flight per deep lane
-constexpr int kUnit = 16;        // chunks per wide work unit
+#ifndef EBR_SUNIT
+#define EBR_SUNIT 16
+#endif
+constexpr int kUnit = EBR_SUNIT; // chunks per wide work unit
 constexpr int kHistCopies = 4;   // private shared-memory histogram copies (fuse contention)
 constexpr uint32_t kMagic = 0xEB200001u;
 
