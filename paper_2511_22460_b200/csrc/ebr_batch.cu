@@ -85,7 +85,7 @@ constexpr int kWideR = EBR_WIDE_R;     // ads per shared-memory accumulation chu
 // ------------------------------------------------------------------------------------------
 // 1. plan (one CTA)
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(512) plan_kernel(const uint32_t* __restrict__ key_chunk_off,
+__global__ void __launch_bounds__(1024) plan_kernel(const uint32_t* __restrict__ key_chunk_off,
                                                    const uint32_t* __restrict__ key_word_off,
                                                    const float* __restrict__ cross_w,
                                                    const int32_t* __restrict__ field_card,
@@ -916,7 +916,7 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
         CUtensorMap tmU;
         if (!encode_2d_bf16(&tmU, ws.U, (uint64_t)u_cols, (uint64_t)nu_pad, kBlockK, (uint32_t)nu_pad))
             return set_error(EBR_ECUDA, "cuTensorMapEncodeTiled(U) failed");
-        plan_kernel<<<1, 512, (size_t)nu_pad * n_hb * 64 * 4, q.stream>>>(
+        plan_kernel<<<1, 1024, (size_t)nu_pad * n_hb * 64 * 4, q.stream>>>(
             idx->key_chunk_off, idx->key_word_off, idx->cross_w, idx->field_card, idx->field_base, idx->n_fields,
             q.slots, q.user_feat + (size_t)g0 * idx->n_fields * q.slots, q.user_x + (size_t)g0 * idx->n_fields * q.slots,
             reinterpret_cast<const uint16_t*>(q.user_emb) + (size_t)g0 * idx->d, idx->d, idx->d_pad, nu, nu_pad,
