@@ -74,7 +74,10 @@ typedef enum { EBR_F32 = 0, EBR_BF16 = 1 } ebr_dtype;
  * Device layout: ad embeddings A[n_pad][d_pad]; the posting lists of
  * every key as 32-posting chunks, delta-coded and bit-packed (DESIGN.md "Posting-chunk wire
  * format"), with an SoA directory key_chunk_off[M+1], key_word_off[M], chunk_hdr[C] (u32 pairs)
- * and payload words; w[M].
+ * and payload words; w[M].  bf16 indexes also keep the up to 256 longest posting lists (>= max(64,
+ * n/512) postings) as dense one-hot columns H[n_pad][n_hot] of L in bf16 for the batched
+ * tensor-core path (R22; EBR_HOT_KEYS=<n> caps n_hot, 0 disables); the compressed lists
+ * stay complete.  Device memory: A + H + the encoded lists (ebr_index_stats reports the sizes).
  */
 ebr_status ebr_build_index(const void *ad_emb, ebr_dtype dtype, int64_t ad_begin, int64_t ad_end,
                            int32_t d, const int32_t *ad_feat, int32_t n_fields,

@@ -233,6 +233,7 @@ constexpr int kWideItems = kWideThreads;   // items per pass of the unit scan
 #define EBR_BUNIT 8
 #endif
 constexpr int kBUnit = EBR_BUNIT;          // posting chunks per work unit (<= 32)
+constexpr int kUnitMap = 2048;             // units with a direct unit -> item entry (beyond: a walk)
 constexpr int kWideMinBlocks = (2048 / kWideThreads) < (200 * 1024 / (kWideR * 4)) ? (2048 / kWideThreads)
                                                                                     : (200 * 1024 / (kWideR * 4));
 __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks > 0 ? kWideMinBlocks : 1) wide_smem_kernel(const uint2* __restrict__ hdr,
@@ -241,6 +242,7 @@ __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks > 0 ? kWideMinBlo
                                                                     int cap_items) {
     extern __shared__ __align__(16) int32_t acc[];   // [kWideR]
     __shared__ uint32_t sLo[kWideItems], sHi[kWideItems], sUoff[kWideItems + 1], sScan[40], sCtr;
+    __shared__ uint16_t sUnitItem[kUnitMap];
     __shared__ int32_t sF[kWideItems];
     __shared__ uint32_t sKwb[kWideItems];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = kWideThreads / 32;
@@ -268,7 +270,11 @@ __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks > 0 ? kWideMinBlo
         }
         uint32_t tot;
         const uint32_t pre = block_exclusive_scan(nu_units, sScan, &tot);
-        if ((uint32_t)tid < ni) { sLo[tid] = lo; sUoff[tid] = pre; }
+        if ((uint32_t)tid < ni) {
+            sLo[tid] = lo;
+            sUoff[tid] = pre;
+            for (uint32_t v = pre; v < pre + nu_units && v < (uint32_t)kUnitMap; ++v) sUnitItem[v] = (uint16_t)tid;
+        }
         if (tid == 0) { sUoff[ni] = tot; sCtr = 0u; }
         __syncthreads();
         // units of up to kBUnit chunks are claimed dynamically from a shared counter (load balance
@@ -282,7 +288,8 @@ __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks > 0 ? kWideMinBlo
             if (lane == 0) unit = atomicAdd(&sCtr, 1u);
             BUnit r{__shfl_sync(FULL, unit, 0), 0, 0u, 0u, make_uint2(0u, 0u)};
             if (r.unit < tot) {
-                while (sUoff[lw + 1] <= r.unit) ++lw;
+                if (r.unit < (uint32_t)kUnitMap) lw = sUnitItem[r.unit];       // unit -> item map
+                else while (sUoff[lw + 1] <= r.unit) ++lw;
                 r.l = lw;
                 r.cb = sLo[lw] + (r.unit - sUoff[lw]) * kBUnit;
                 r.nc = min(r.cb + kBUnit, sHi[lw]) - r.cb;
@@ -718,7 +725,11 @@ __global__ void __launch_bounds__(kThetaThreads, 1) theta_kernel(BatchWs ws, int
         __syncthreads();
         prefix |= sScalar[0] << shift;
         need -= sScalar[1];
+        // one pass is enough when every key in the digit's bin and above fits the compaction
+        // buffer: then compact {ord >> 21 >= digit} directly (the second histogram pass is skipped)
+        const bool done = pass == 0 && (uint64_t)sScalar[1] + hist[sScalar[0]] <= (uint64_t)scap;
         __syncthreads();
+        if (done) break;
     }
     // keys with ord >= prefix: at least K of them; compact into shared memory
     if (tid == 0) sScalar[2] = 0;
@@ -856,7 +867,10 @@ using namespace batch;
 
 bool batch_eligible(const ebr_index* idx, int32_t batch, int32_t k) {
     if (getenv("EBR_NO_BATCH_PATH")) return false;
-    return idx->dtype == EBR_BF16 && batch >= 16 && idx->d_pad <= 256 &&
+    // small batches take the tensor-core path too on large inventories, where the latency path's
+    // per-user wide scratch no longer fits L2 (C5 sweep: B=4 at 20 M ads 3.9 ms latency path)
+    const bool big = idx->n_ads >= ((int64_t)1 << 21);
+    return idx->dtype == EBR_BF16 && (batch >= 16 || (big && batch >= 4)) && idx->d_pad <= 256 &&
            idx->n_ads >= (int64_t)4 * kSampleStride * std::max(k, kTileM) && get_encode() != nullptr;
 }
 
@@ -906,7 +920,10 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
             return fixed + (((size_t)nu_pad * 128 * (n_kb + kHotPieces * hb) + 1023) & ~(size_t)1023) +
                    (size_t)(st + wstages) * kBlockBytes;
         };
+        // hot K blocks pay per ad (2 B x 64 keys of H) and save per (ad, user) hit; block b (in
+        // decreasing coverage) pays off from ~2, 14, 30, 60 users: cap by group size
         int n_hb = idx->n_hot / 64;
+        n_hb = std::min(n_hb, nu < 14 ? 1 : nu < 30 ? 2 : nu < 60 ? 3 : 4);
         if (getenv("EBR_NO_HOT")) n_hb = 0;
         while (n_hb > 0 && smem_of(n_hb, 4) > (size_t)max_smem) --n_hb;
         int stages = 4;

@@ -159,3 +159,13 @@ def test_batch_without_hot_columns(ebr):
     assert idx.stats()["n_hot"] == 0
     (ids, sc), _ = run(ebr, idx, users, 120)
     assert check_all(oracle.Oracle.of(inv), users, ids, sc, 120, "exact") == 0
+
+
+def test_batch_small_batch_large_inventory(ebr):
+    """B = 4 on a >= 2^21-ad bf16 inventory takes the tensor-core path (one hot K block): exact."""
+    inv, users = synth.make_config("C3", mode="exact", n_ads=2_200_000, batch=4)
+    idx = ebr.Index.of(inv)
+    assert idx.query_launches(4, users.slots, 100) != 1      # not the single latency-path launch
+    (ids, sc), ws = run(ebr, idx, users, 100)
+    assert check_all(oracle.Oracle.of(inv), users, ids, sc, 100, "exact") == 0
+    assert ebr.query_error(ws) == 0
