@@ -153,7 +153,10 @@ ebr_status ebr_workspace_init(const ebr_index *idx, void *workspace, size_t byte
 /*
  * End-to-end variant with HOST buffers (the e2e measurement): copies user_emb, user_feat and
  * user_x host->device, runs ebr_score_topk, copies ids and scores device->host and synchronises
- * `stream` before returning.  Host buffers should be pinned for full speed.
+ * `stream` before returning.  Requests whose inputs and outputs each fit 1 MB are staged through
+ * a library-owned, thread-local pinned buffer (one H2D and one D2H copy: per-copy latency
+ * dominates at these sizes); larger ones copy each array directly, so their host buffers should
+ * be pinned for full speed.  Not reentrant within one thread across streams.
  * workspace: device, >= ebr_workspace_bytes_host(idx, batch, slots, k).
  */
 size_t ebr_workspace_bytes_host(const ebr_index *idx, int32_t batch, int32_t slots, int32_t k);

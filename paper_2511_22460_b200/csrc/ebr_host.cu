@@ -631,14 +631,45 @@ ebr_status ebr_score_topk_host(const ebr_index* idx, const void* user_emb_host, 
     int prev = -1;
     cudaGetDevice(&prev);
     if (prev != idx->device) cudaSetDevice(idx->device);
-    EBR_CUDA(cudaMemcpyAsync(d_emb, user_emb_host, (size_t)batch * idx->d * esz, cudaMemcpyHostToDevice, s));
-    EBR_CUDA(cudaMemcpyAsync(d_feat, user_feat_host, nfs * 4, cudaMemcpyHostToDevice, s));
-    EBR_CUDA(cudaMemcpyAsync(d_x, user_x_host, nfs * 4, cudaMemcpyHostToDevice, s));
+    const size_t in_bytes = (size_t)(reinterpret_cast<char*>(d_ids) - d_emb);       // emb | feat | x
+    const size_t out_bytes = (size_t)(reinterpret_cast<char*>(d_sc) - reinterpret_cast<char*>(d_ids)) +
+                             (size_t)batch * k * 4;                                  // ids | scores
+    // small requests (latency path): one H2D and one D2H through a pinned staging buffer (the
+    // per-copy latency, not the bytes, dominates); large ones copy each array directly
+    thread_local char* pin = nullptr;
+    thread_local size_t pin_bytes = 0;
+    const size_t need = std::max(in_bytes, out_bytes);
+    const bool staged = need <= ((size_t)1 << 20);
+    if (staged && pin_bytes < need) {
+        if (pin) cudaFreeHost(pin);
+        pin = nullptr;
+        pin_bytes = 0;
+        if (cudaMallocHost(&pin, need) == cudaSuccess) pin_bytes = need;
+    }
+    if (staged && pin) {
+        memcpy(pin, user_emb_host, (size_t)batch * idx->d * esz);
+        memcpy(pin + (reinterpret_cast<char*>(d_feat) - d_emb), user_feat_host, nfs * 4);
+        memcpy(pin + (reinterpret_cast<char*>(d_x) - d_emb), user_x_host, nfs * 4);
+        EBR_CUDA(cudaMemcpyAsync(d_emb, pin, in_bytes, cudaMemcpyHostToDevice, s));
+    } else {
+        EBR_CUDA(cudaMemcpyAsync(d_emb, user_emb_host, (size_t)batch * idx->d * esz, cudaMemcpyHostToDevice, s));
+        EBR_CUDA(cudaMemcpyAsync(d_feat, user_feat_host, nfs * 4, cudaMemcpyHostToDevice, s));
+        EBR_CUDA(cudaMemcpyAsync(d_x, user_x_host, nfs * 4, cudaMemcpyHostToDevice, s));
+    }
     ebr_status r = ebr_score_topk(idx, d_emb, batch, d_feat, d_x, slots, k, d_ids, d_sc, workspace, w, stream_v);
     if (r != EBR_OK) return r;
-    EBR_CUDA(cudaMemcpyAsync(out_ids_host, d_ids, (size_t)batch * k * 4, cudaMemcpyDeviceToHost, s));
-    EBR_CUDA(cudaMemcpyAsync(out_scores_host, d_sc, (size_t)batch * k * 4, cudaMemcpyDeviceToHost, s));
-    EBR_CUDA(cudaStreamSynchronize(s));
+    if (staged && pin) {
+        // the H2D above read `pin`; this D2H is stream-ordered after it, so reusing it is safe
+        EBR_CUDA(cudaMemcpyAsync(pin, d_ids, out_bytes, cudaMemcpyDeviceToHost, s));
+        EBR_CUDA(cudaStreamSynchronize(s));
+        memcpy(out_ids_host, pin, (size_t)batch * k * 4);
+        memcpy(out_scores_host, pin + (reinterpret_cast<char*>(d_sc) - reinterpret_cast<char*>(d_ids)),
+               (size_t)batch * k * 4);
+    } else {
+        EBR_CUDA(cudaMemcpyAsync(out_ids_host, d_ids, (size_t)batch * k * 4, cudaMemcpyDeviceToHost, s));
+        EBR_CUDA(cudaMemcpyAsync(out_scores_host, d_sc, (size_t)batch * k * 4, cudaMemcpyDeviceToHost, s));
+        EBR_CUDA(cudaStreamSynchronize(s));
+    }
     if (prev >= 0 && prev != idx->device) cudaSetDevice(prev);
     return EBR_OK;
 }

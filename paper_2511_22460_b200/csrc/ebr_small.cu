@@ -1,4 +1,7 @@
 // ebr_small.cu -- host side of the latency path (see ebr_small_kernel.cuh for the kernel).
+#include <mutex>
+#include <vector>
+
 #include "ebr_small_kernel.cuh"
 
 namespace ebr {
@@ -95,11 +98,37 @@ ebr_status run_small(const QueryArgs& q, int b0, int B) {
         return set_error(EBR_EUNSUPPORTED, "latency path: %d user slots / k=%d need %zu B of shared memory",
                          items_cap, q.k, smem);
 
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(small)");
+    // the attribute and the occupancy of a (kernel, smem, device) are fixed: computed once (the
+    // per-call host work is part of the end-to-end latency of a query)
+    // (the max-dynamic-smem attribute is per kernel and shapes its occupancy, so it is re-set
+    // whenever this call's size differs from the last one set for the kernel on this device)
+    struct OccKey { kern_t k; size_t smem; int dev; int occ; };
+    struct AttrKey { kern_t k; int dev; size_t smem; };
+    static std::mutex occ_mu;
+    static std::vector<OccKey> occ_cache;
+    static std::vector<AttrKey> attr_set;
     int occ = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, smem);
-    if (e != cudaSuccess || occ < 1) return cuda_check(e == cudaSuccess ? cudaErrorInvalidConfiguration : e, "occupancy(small)");
+    cudaError_t e = cudaSuccess;
+    {
+        std::lock_guard<std::mutex> lk(occ_mu);
+        AttrKey* cur = nullptr;
+        for (AttrKey& a : attr_set)
+            if (a.k == k && a.dev == idx->device) cur = &a;
+        if (!cur || cur->smem != smem) {
+            e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(small)");
+            if (cur) cur->smem = smem;
+            else attr_set.push_back({k, idx->device, smem});
+        }
+        for (const OccKey& o : occ_cache)
+            if (o.k == k && o.smem == smem && o.dev == idx->device) { occ = o.occ; break; }
+        if (!occ) {
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, smem);
+            if (e != cudaSuccess || occ < 1)
+                return cuda_check(e == cudaSuccess ? cudaErrorInvalidConfiguration : e, "occupancy(small)");
+            occ_cache.push_back({k, smem, idx->device, occ});
+        }
+    }
 
     SmallParams p;
     p.A = idx->A; p.d = idx->d; p.d_pad = idx->d_pad;

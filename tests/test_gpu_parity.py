@@ -236,6 +236,21 @@ def test_host_variant_equals_device(ebr):
     assert (hid == ids).all() and (hsc == sc).all()
 
 
+def test_host_variant_staged_and_direct(ebr):
+    """both copy strategies of ebr_score_topk_host: a small request (pinned staging, one H2D and
+    one D2H) after a large one (> 1 MB of outputs: one copy per array), then small again"""
+    inv, users = synth.make_config("C2", mode="exact", n_ads=100_000, batch=70)
+    idx = ebr.Index.of(inv)
+    for b, k in ((2, 50), (70, 2000), (5, 300)):
+        sub = synth.Users(b, users.slots, users.user_emb[:b], users.user_feat[:b], users.user_x[:b])
+        (ids, sc), _ = run(ebr, idx, sub, k)
+        ws = ebr.new_workspace(idx, b, users.slots, k, host=True)
+        hid = np.empty((b, k), np.int32)
+        hsc = np.empty((b, k), np.float32)
+        ebr.score_topk_host(idx, sub.user_emb, sub.user_feat, sub.user_x, k, hid, hsc, ws)
+        assert (hid == ids).all() and (hsc == sc).all()
+
+
 # ---------------------------------------------------------------- A7: shard + merge == 1 GPU
 
 @pytest.mark.parametrize("G", [2, 3, 8])
