@@ -169,3 +169,27 @@ def test_batch_small_batch_large_inventory(ebr):
     (ids, sc), ws = run(ebr, idx, users, 100)
     assert check_all(oracle.Oracle.of(inv), users, ids, sc, 100, "exact") == 0
     assert ebr.query_error(ws) == 0
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_batch_sharded_merge_equals_single(ebr, G):
+    """A7 over the tensor-core path: each ad-range shard (own hot columns, own encoded lists)
+    emits kappa keys, the merge of the G lists equals the one-index answer bit for bit."""
+    inv, users = synth.make_config("C3", mode="exact", n_ads=160_000, batch=40)
+    k = 150
+    (ids1, sc1), _ = run(ebr, ebr.Index.of(inv), users, k)
+    bounds = (np.linspace(0, inv.n_ads, G + 1) // 128 * 128).astype(int)
+    bounds[-1] = inv.n_ads
+    parts = []
+    for g in range(G):
+        idx = ebr.Index.of(inv, lo=bounds[g], hi=bounds[g + 1])
+        assert idx.query_launches(40, users.slots, k) != 10      # the batched path on every shard
+        keys, _ = run(ebr, idx, users, k, keys=True)
+        parts.append(keys)
+    gathered = torch.from_numpy(np.stack(parts).view(np.int64)).cuda()
+    ids = torch.empty((40, k), dtype=torch.int32, device="cuda")
+    sc = torch.empty((40, k), dtype=torch.float32, device="cuda")
+    ebr.merge_topk(gathered, G, 40, k, ids, sc)
+    torch.cuda.synchronize()
+    assert (ids.cpu().numpy() == ids1).all() and (sc.cpu().numpy() == sc1).all()
+    assert check_all(oracle.Oracle.of(inv), users, ids1, sc1, k, "exact") == 0
