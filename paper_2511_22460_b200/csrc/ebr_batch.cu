@@ -19,6 +19,7 @@
 //   A user whose candidate list overflowed (possible only for massively tied scores) is recomputed
 //   by the latency path after a single stream synchronisation at the end of the call.
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -152,6 +153,7 @@ __global__ void __launch_bounds__(1024) plan_kernel(const uint32_t* __restrict__
     if (tid == 0) {
         ws.header[0] = base;
         ws.header[1] = 0;       // overflow users of this group
+        ws.header[2] = 0;       // users with fewer than K candidates (theta rank below K)
         ws.chunk_off[base] = sCarry;
     }
     __syncthreads();
@@ -771,6 +773,13 @@ __global__ void __launch_bounds__(512, 1) final_kernel(BatchWs ws, int64_t cap, 
         if (threadIdx.x == 0) { ws.overflow[u] = 1; atomicAdd(&ws.header[1], 1u); }
         return;
     }
+    // fewer than K ads reached theta (possible only when theta was taken at a rank below K of the
+    // sample): the top-K is not guaranteed inside the candidates -- the host reruns the group with
+    // rank K (inventories reaching this path hold >= 64 K ads, so n >= K otherwise)
+    if (n < K) {
+        if (threadIdx.x == 0) atomicAdd(&ws.header[2], 1u);
+        return;
+    }
     const int P = pow2ceil_i(K);
     uint64_t* sbuf = reinterpret_cast<uint64_t*>(smem);
     uint32_t* shist = reinterpret_cast<uint32_t*>(sbuf + P);
@@ -954,35 +963,57 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
         e = cudaFuncSetAttribute(gemm_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return cuda_check(e, "attr(gemm0)");
         gemm_kernel<0><<<std::min(idx->sm_count, n_samp_tiles), kGemmThreads, smem, q.stream>>>(tmA, tmH, tmU, gp);
-        // theta
+        // theta at sample rank r, the filter pass over every tile, the final select.  The sample
+        // is every 16th tile, so ~K/16 sampled keys lie above the K-th largest overall: taking
+        // theta at r = K/16 + 5 sqrt(K/16) + 8 (< K) instead of K cuts the candidates ~10x; a
+        // user left with fewer than K candidates (counted by final_kernel) makes the group rerun
+        // with r = K, which guarantees >= K candidates (exact either way)
         const size_t tsmem = 200 * 1024;
         const int tscap = (int)((tsmem - (size_t)pow2ceil_i(q.k) * 8 - kThetaCopies * 2048 * 4) / 8);
         e = cudaFuncSetAttribute(theta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
         if (e != cudaSuccess) return cuda_check(e, "attr(theta)");
-        theta_kernel<<<nu, kThetaThreads, tsmem, q.stream>>>(ws, (int)L.n_samp, q.k, (uint32_t)idx->ad_begin, nu,
-                                                             tscap);
-        // filter pass over every tile
-        gp.n_tiles = n_tiles; gp.tile_stride = 1;
         e = cudaFuncSetAttribute(gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return cuda_check(e, "attr(gemm1)");
-        gemm_kernel<1><<<std::min(idx->sm_count, n_tiles), kGemmThreads, smem, q.stream>>>(tmA, tmH, tmU, gp);
-        // final
         const size_t fsmem = 200 * 1024;
         const int64_t scap = (int64_t)(fsmem - (size_t)pow2ceil_i(q.k) * 8 - kSelBins * 4) / 8;
         e = cudaFuncSetAttribute(final_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
         if (e != cudaSuccess) return cuda_check(e, "attr(final)");
-        final_kernel<<<nu, 512, fsmem, q.stream>>>(ws, cap, q.k, nu,
-                                                   q.out_ids ? q.out_ids + (size_t)g0 * q.k : nullptr,
-                                                   q.out_scores ? q.out_scores + (size_t)g0 * q.k : nullptr,
-                                                   q.out_keys ? q.out_keys + (size_t)g0 * q.k : nullptr, scap);
+        const double ks = (double)q.k / kSampleStride;
+        int rank = (int)std::ceil(ks + 5.0 * std::sqrt(ks) + 8.0);
+        if (getenv("EBR_THETA_RANK")) rank = atoi(getenv("EBR_THETA_RANK"));   // test hook
+        rank = std::max(1, std::min(rank, q.k));
+        auto select_pass = [&](int r) {
+            theta_kernel<<<nu, kThetaThreads, tsmem, q.stream>>>(ws, (int)L.n_samp, r, (uint32_t)idx->ad_begin, nu,
+                                                                 tscap);
+            gp.n_tiles = n_tiles; gp.tile_stride = 1;
+            gemm_kernel<1><<<std::min(idx->sm_count, n_tiles), kGemmThreads, smem, q.stream>>>(tmA, tmH, tmU, gp);
+            final_kernel<<<nu, 512, fsmem, q.stream>>>(ws, cap, q.k, nu,
+                                                       q.out_ids ? q.out_ids + (size_t)g0 * q.k : nullptr,
+                                                       q.out_scores ? q.out_scores + (size_t)g0 * q.k : nullptr,
+                                                       q.out_keys ? q.out_keys + (size_t)g0 * q.k : nullptr, scap);
+        };
+        select_pass(rank);
         e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_check(e, "launch(batch)");
-        // overflowed users of this group: one sync, then the exact latency path for them
-        uint32_t hdr[2] = {0, 0};
-        e = cudaMemcpyAsync(hdr, ws.header, 8, cudaMemcpyDeviceToHost, q.stream);
+        uint32_t hdr[3] = {0, 0, 0};
+        e = cudaMemcpyAsync(hdr, ws.header, 12, cudaMemcpyDeviceToHost, q.stream);
         if (e != cudaSuccess) return cuda_check(e, "memcpy(header)");
         e = cudaStreamSynchronize(q.stream);
         if (e != cudaSuccess) return cuda_check(e, "sync(batch)");
+        if (hdr[2] && rank < q.k) {
+            // shortfall: the whole group again with theta at rank K (W and the sample are reused)
+            e = cudaMemsetAsync(ws.overflow, 0, (size_t)kGroup * 4, q.stream);
+            if (e == cudaSuccess) e = cudaMemsetAsync(ws.header + 1, 0, 8, q.stream);
+            if (e != cudaSuccess) return cuda_check(e, "memset(rerun)");
+            select_pass(q.k);
+            e = cudaGetLastError();
+            if (e != cudaSuccess) return cuda_check(e, "launch(batch rerun)");
+            e = cudaMemcpyAsync(hdr, ws.header, 12, cudaMemcpyDeviceToHost, q.stream);
+            if (e != cudaSuccess) return cuda_check(e, "memcpy(header)");
+            e = cudaStreamSynchronize(q.stream);
+            if (e != cudaSuccess) return cuda_check(e, "sync(batch)");
+        }
+        // overflowed users of this group: the exact latency path for them
         if (hdr[1]) {
             std::vector<uint32_t> of(nu);
             e = cudaMemcpy(of.data(), ws.overflow, (size_t)nu * 4, cudaMemcpyDeviceToHost);

@@ -193,3 +193,16 @@ def test_batch_sharded_merge_equals_single(ebr, G):
     torch.cuda.synchronize()
     assert (ids.cpu().numpy() == ids1).all() and (sc.cpu().numpy() == sc1).all()
     assert check_all(oracle.Oracle.of(inv), users, ids1, sc1, k, "exact") == 0
+
+
+def test_batch_theta_rank_shortfall_reruns_exactly(ebr):
+    """theta taken at a sample rank far below K leaves users with fewer than K candidates: the
+    group is rerun at rank K and the answer stays exact."""
+    inv, users = synth.make_config("C3", mode="exact", n_ads=60_000, batch=24)
+    idx = ebr.Index.of(inv)
+    os.environ["EBR_THETA_RANK"] = "1"
+    try:
+        (ids, sc), _ = run(ebr, idx, users, 200)
+    finally:
+        del os.environ["EBR_THETA_RANK"]
+    assert check_all(oracle.Oracle.of(inv), users, ids, sc, 200, "exact") == 0
