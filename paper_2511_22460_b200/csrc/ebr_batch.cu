@@ -56,7 +56,7 @@ struct BItem {
 };
 
 struct BatchWs {   // workspace carve-up (device pointers)
-    uint32_t* header;     // [0] n_items, [1] overflow users, [3] workspace magic
+    uint32_t* header;     // [0] n_items, [1] overflow users, [2] users short of K candidates
     BItem* items;         // [cap_items]
     uint64_t* chunk_off;  // [cap_items + 1]
     __nv_bfloat16* U;     // [kGroup][d_pad]
@@ -74,9 +74,6 @@ struct BatchWs {   // workspace carve-up (device pointers)
 
 #ifndef EBR_WIDE_R
 #define EBR_WIDE_R 24576
-#endif
-#ifndef EBR_W_RING
-#define EBR_W_RING 1
 #endif
 #ifndef EBR_WIDE_T
 #define EBR_WIDE_T 512
