@@ -73,10 +73,10 @@ struct BatchWs {   // workspace carve-up (device pointers)
 };
 
 #ifndef EBR_WIDE_R
-#define EBR_WIDE_R 24576
+#define EBR_WIDE_R 16384
 #endif
 #ifndef EBR_WIDE_T
-#define EBR_WIDE_T 512
+#define EBR_WIDE_T 384
 #endif
 constexpr int kWideR = EBR_WIDE_R;     // ads per shared-memory accumulation chunk (int32 each)
 
@@ -232,7 +232,10 @@ constexpr int kWideItems = kWideThreads;   // items per pass of the unit scan
 #define EBR_BUNIT 8
 #endif
 constexpr int kBUnit = EBR_BUNIT;          // posting chunks per work unit (<= 32)
-constexpr int kUnitMap = 2048;             // units with a direct unit -> item entry (beyond: a walk)
+#ifndef EBR_UNIT_MAP
+#define EBR_UNIT_MAP 1024
+#endif
+constexpr int kUnitMap = EBR_UNIT_MAP;     // units with a direct unit -> item entry (beyond: a walk)
 constexpr int kWideMinBlocks = (2048 / kWideThreads) < (200 * 1024 / (kWideR * 4)) ? (2048 / kWideThreads)
                                                                                     : (200 * 1024 / (kWideR * 4));
 __global__ void __launch_bounds__(kWideThreads, kWideMinBlocks > 0 ? kWideMinBlocks : 1) wide_smem_kernel(const uint2* __restrict__ hdr,
