@@ -1,588 +1,760 @@
-// ebr_batch.cu -- the batched path (bf16 embeddings, user batch >= 16): the deep score is a dense
-// contraction D[ads x users] = A . U^T (Eq. 1 / Eq. 8 for every (user, ad) pair) and runs on the
-// 5th-generation tensor cores, together with the wide term of the hot keys (the longest posting
-// lists, kept as dense one-hot columns H of L -- DESIGN.md R22): D = W + A U_deep^T + H U_hot^T,
-// where U_hot holds each user's w~ as three exact bf16 terms and W is the cold keys' wide term
-// decoded from the compressed inverted lists.  Per group of up to 128 users, one call runs:
+// ebr_batch.cu -- the batched path (bf16 embeddings, user batch >= 16): every (user, ad) score of
+// a pass of up to 512 users is produced tile by tile inside ONE persistent tcgen05 kernel and
+// filtered against a per-user threshold on chip; no per-(user, ad) buffer ever reaches HBM.
 //
-//   1. plan_kernel     A1: hot slots -> U_hot (hi, mid, lo), cold slots -> work items, the per-user
-//                      fixed-point scale, and the deep part of the bf16 user tile U
-//   2. span_kernel     for every cold item and kWideR-ad range, the chunks holding ids in the range
-//      wide_smem_kernel A2+A3 for cold keys: CTA (range, user) decodes the user's postings in the
-//                      range and accumulates w~ in shared memory (Alg. 2 l.358), then writes W
-//   3. gemm_kernel<0>  A4+A5 on a strided 1/16 sample of the ad tiles: s = W + deep + hot, stored
-//   4. theta_kernel    A6a per user: theta_u = the K-th largest key among the sampled ads.  The
-//                      sample is a subset of the inventory, so at least K ads have key >= theta_u
-//                      and the top-K is contained in {key >= theta_u} -- exact, not heuristic.
-//   5. gemm_kernel<1>  A4+A5+A6b on every tile: keys >= theta_u appended to the user's candidates
-//   6. final_kernel    A6c per user: exact radix select + sort of the candidates
-//   A user whose candidate list overflowed (possible only for massively tied scores) is recomputed
-//   by the latency path after a single stream synchronisation at the end of the call.
+//   s(u,a) = <h~_u, h~_a>                      deep, Eq. 1 / Eq. 8
+//          + sum_{hot keys i} w~_ui L_ai       wide, the longest posting lists as one-hot columns
+//          + sum_{cold keys i} w~_ui L_ai      wide, the compressed inverted lists (Alg. 2)
+//
+// A pass of P users is split into G = ceil(P/128) groups; the G CTAs of a thread-block cluster
+// (one per group, one CTA per SM) walk the same ad tiles in lockstep and receive each 128-ad tile
+// of A by ONE multicast TMA load, so A is read from HBM once per pass (not once per group).  Per
+// CTA and tile (128 ads x 128 users, fp32 accumulator in TMEM, 4 stages):
+//   * wide warps (8): expand the ads' hot-key bit masks into an fp16 one-hot K block (A side of
+//     the hot MMA), scatter the cold keys' w~ into a shared-memory int32 fixed-point tile
+//     [ads x users] (Alg. 2 l.358's AtomicAdd, exact and order-free), convert it once to fp32 and
+//     store it into the TMEM accumulator stage with tcgen05.st;
+//   * one thread issues tcgen05.mma: deep (bf16 A x bf16 U) and hot (fp16 one-hot x fp16 w~
+//     pieces) accumulate ON TOP of the stored cold wide term: D = cold + deep + hot;
+//   * epilogue warps (8): tcgen05.ld, A5 kappa, A6 sample store / threshold filter.
+// The cold postings reach the tile as an "entry stream": the batch's distinct cold keys are
+// decoded ONCE per pass (not once per user: the SpMM view of L w~) by range kernels into
+// per-tile lists of (ad row, the key's user-pair list), read by every CTA of the cluster.
+//
+// Launches per pass (all on the caller's stream, no host synchronisation -- graph-capturable):
+//   plan_a / plan_b / plan_c   A1: slots -> keys, w~ = fl32(w x), hot pieces, cold key
+//                              union (hash) with user pairs, fixed-point scales, user tiles
+//   span / entry_count / range_scan / entry_write    A2: the entry stream
+//   score<0>  on every 16th tile: scores of the sample (A3-A5)
+//   theta     A6a: theta_u = the r-th largest sampled key (r < K)
+//   score<1>  on every tile: keys >= theta_u appended to per-user candidate lists (A3-A6b)
+//   final     A6c: exact top-K of the candidates; a user with < K candidates is flagged
+//   theta / score<1> / final again, gated on device flags: the flagged users with r = K, which
+//             guarantees >= K candidates (the sample is a subset of the inventory) -- exact.
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "ebr_tc.cuh"
 
 namespace ebr {
-ebr_status run_small(const QueryArgs& q, int b0, int B);
 
 namespace batch {
 
-constexpr int kGroup = 128;          // users per group (UMMA N)
+constexpr int kGroup = 128;          // users per CTA (UMMA N)
+constexpr int kMaxCluster = 4;       // CTAs (user groups) per cluster
 constexpr int kTileM = 128;          // ads per tile (UMMA M)
-constexpr int kBlockK = 64;          // bf16 elements per 128-byte swizzle row
+constexpr int kBlockK = 64;          // 16-bit elements per 128-byte swizzle row
+constexpr int kBlockBytes = kTileM * 128;   // one ring stage: 128 rows x 128 B
 constexpr int kSampleStride = 16;    // every 16th tile is sampled for theta
-constexpr int kEpiWarps = 8;         // 2 per TMEM lane quadrant, two 32-column chunks each
-constexpr int kEpiChunks = kGroup / 32 / (kEpiWarps / 4);
-constexpr int kLoadWarps = 4;        // one per TMEM lane quadrant, every 32-column chunk in turn
-constexpr int kEpiWarp0 = 4;
-constexpr int kLoadWarp0 = kEpiWarp0 + kEpiWarps;
-constexpr int kGemmThreads = 32 * (kLoadWarp0 + kLoadWarps);   // 0 TMA, 1 MMA, 2 TMEM alloc, 3 W bulk copies
-constexpr int kAccStages = 4;        // TMEM: 4 x 128 columns = all 512
-#ifndef EBR_WPF
-#define EBR_WPF 4
-#endif
-constexpr int kWPrefetch = EBR_WPF;  // tiles of W streamed into L2 ahead of their bulk copies
-constexpr int kHotPieces = 3;        // w~ = hi + mid + lo in bf16: 24 significant bits, exact (R22)
-constexpr int kBlockBytes = kTileM * 128;   // one ring stage: 128 ads x 64 bf16 (one K block)
-
-struct BItem {
-    uint32_t key, c0, c1, u, kwb;
-    float w;
-};
-
-struct BatchWs {   // workspace carve-up (device pointers)
-    uint32_t* header;     // [0] n_items, [1] overflow users, [2] users short of K candidates
-    BItem* items;         // [cap_items]
-    uint64_t* chunk_off;  // [cap_items + 1]
-    __nv_bfloat16* U;     // [kGroup][d_pad]
-    float* W;             // [n_tiles][kGroup][128] tile-major: a tile's 32-user chunk is 16 KB contiguous
-    float* samp;          // [kGroup][n_samp]
-    uint64_t* theta;      // [kGroup]
-    uint32_t* cand_count; // [kGroup]
-    uint64_t* cand;       // [kGroup][cap]
-    uint32_t* overflow;   // [kGroup]
-    uint32_t* user_item;  // [kGroup + 1]  items of group user u: [user_item[u], user_item[u+1])
-    int32_t* user_shift;  // [kGroup] fixed-point scale S_u of the user's cold wide sum
-    uint32_t* span;       // [nj + 1][cap_items] first chunk of item i with first id >= j*R
-    uint32_t* span_lo;    // [nj][cap_items]     first chunk of item i holding an id >= j*R
-};
-
-#ifndef EBR_WIDE_R
-#define EBR_WIDE_R 16384
-#endif
-#ifndef EBR_WIDE_T
-#define EBR_WIDE_T 384
-#endif
-constexpr int kWideR = EBR_WIDE_R;     // ads per shared-memory accumulation chunk (int32 each)
+constexpr int kAccStages = 4;        // TMEM: 4 x 128 columns
+constexpr int kAccPitch = kGroup + 4;   // int32 words per fixed-point row (16-B row reads conflict-free)
+constexpr int kWideWarp0 = 4, kWideWarps = 8, kWideThreads = 32 * kWideWarps;
+constexpr int kEpiWarp0 = kWideWarp0 + kWideWarps, kEpiWarps = 8;
+constexpr int kGemmThreads = 32 * (kEpiWarp0 + kEpiWarps);   // 640: TMA, MMA, TMEM alloc, spare, 8 wide, 8 epilogue
+constexpr int kMaxHotBlocks = 2;     // hot K blocks of 64 keys (the index keeps up to 128 hot keys)
+constexpr int kPairWBits = 23;       // cold pair = pass user (9 bits) << 23 | w~ 2^S (23-bit two's complement)
+constexpr int kPairWMax = 22;        // |w~ 2^S| < 2^22
+constexpr int kEntryPsBits = 15;     // entry = row << 24 | (pair count - 1) << 15 | first pair
+constexpr int kMaxPassPairs = 1 << kEntryPsBits;
+constexpr int kRangeMaxTiles = 256;  // entry-stream range: <= 32768 ads (per-ad u32 counters in smem)
+constexpr int kPlanThreads = 1024;
+constexpr uint32_t kFlagShort = 1u, kFlagOverflow = 2u, kFlagRaise = 4u;   // uflags; overflow users carry their dense slot << 8
+constexpr uint32_t kFlagAny = kFlagShort | kFlagOverflow | kFlagRaise;
+constexpr int kMaxFallback = 2;      // overflowed users per pass recomputed exactly (dense scores)
 
 // ------------------------------------------------------------------------------------------
-// 1. plan (one CTA)
+// workspace
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) plan_kernel(const uint32_t* __restrict__ key_chunk_off,
-                                                   const uint32_t* __restrict__ key_word_off,
-                                                   const float* __restrict__ cross_w,
-                                                   const int32_t* __restrict__ field_card,
-                                                   const int32_t* __restrict__ field_base, int F, int S,
-                                                   const int32_t* __restrict__ user_feat,
-                                                   const float* __restrict__ user_x,
-                                                   const uint16_t* __restrict__ user_emb, int d, int d_pad,
-                                                   int nu, int nu_pad, const int32_t* __restrict__ hot_slot,
-                                                   int n_hot, int u_cols, BatchWs ws, uint32_t* err) {
-    extern __shared__ float sHot[];          // [nu_pad][n_hot] sum of w~ per (user, hot slot)
+struct Ws {
+    uint32_t* header;     // [0] n_union [1] n_pairs [2] any user short of K [3] entries total [4] overflowed users
+    uint32_t* hkey;       // [TS] key + 1 (0 = empty)
+    uint32_t* hcnt;       // [TS] user pairs of the key (left zero by plan_c)
+    uint32_t* hslot;      // [TS] union slot of the key
+    uint32_t* hpair;      // [TS] first pair of the key
+    int32_t* item_t;      // [P*F*S] hash position of a cold slot, -1 otherwise
+    float* item_w;        // [P*F*S] w~ of the slot
+    float* hotw;          // [P_pad][128] sum of w~ per (user, hot key) (left zero by plan_c)
+    float* bound;         // [P] sum |w~| of the cold slots (left zero by plan_b)
+    uint32_t* emax;       // [P] max |w~| bits (left zero by plan_b)
+    int32_t* ushift;      // [P] fixed-point scale S_u
+    float* uscale;        // [P] 2^-S_u
+    uint32_t* ukey;       // [NU] union slot -> key
+    uint32_t* uc0;        // [NU] first chunk of the key
+    uint32_t* uc1;        // [NU] end chunk
+    uint32_t* ukwb;       // [NU] payload word base
+    uint32_t* uentry;     // [NU] (count - 1) << 15 | first pair
+    uint32_t* pairs;      // [NU]
+    uint16_t* U;          // [P_pad][u_cols] deep bf16 | hot fp16 pieces
+    uint32_t* span;       // [NU][n_ranges + 1] first chunk of the key with last id >= j R
+    uint32_t* adcnt;      // [n_pad / 4] per-ad entry counts (u8)
+    uint32_t* rtotal;     // [n_ranges]
+    uint32_t* rbase;      // [n_ranges + 1]
+    uint32_t* tile_off;   // [n_tiles + 1]
+    uint32_t* entries;    // [n_pad * F]
+    float* samp;          // [P][n_samp]
+    uint64_t* theta;      // [P]
+    uint32_t* cand_count; // [P]
+    uint64_t* cand;       // [P][cap]
+    uint32_t* uflags;     // [P] kFlagShort | kFlagOverflow
+    float* dense;         // [kMaxFallback][n_pad] every score of an overflowed user
+};
+
+struct Layout {
+    size_t total;
+    size_t off[32];
+    int64_t TS, NU, P, n_samp, cap, n_ranges, range_ads, n_tiles, u_cols;
+};
+
+static int64_t pow2ceil64(int64_t x) {
+    int64_t p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+// users per pass: <= kGroup * kMaxCluster, and the pass's pairs must fit the entry encoding
+int pass_users(const ebr_index* idx, int32_t slots) {
+    const int64_t fs = (int64_t)idx->n_fields * slots;
+    int64_t p = std::min<int64_t>(kGroup * kMaxCluster, kMaxPassPairs / std::max<int64_t>(fs, 1));
+    return (int)(p / 32 * 32);
+}
+
+static int64_t cand_cap(int k) {
+    return std::max<int64_t>(65536, 4 * ((int64_t)k + (int64_t)(100.0 * std::sqrt((double)k)) + 256));
+}
+
+static Layout layout(const ebr_index* idx, int32_t slots, int32_t k) {
+    Layout L;
+    const int P = pass_users(idx, slots);
+    L.P = P;
+    L.NU = (int64_t)P * idx->n_fields * slots;
+    L.TS = pow2ceil64(2 * L.NU);
+    L.n_tiles = idx->n_pad / kTileM;
+    L.n_samp = ((L.n_tiles + kSampleStride - 1) / kSampleStride) * kTileM;
+    L.cap = cand_cap(k);
+    const int64_t tpr = std::min<int64_t>(kRangeMaxTiles, std::max<int64_t>(1, (L.n_tiles + 2 * idx->sm_count - 1) /
+                                                                                 (2 * idx->sm_count)));
+    L.range_ads = tpr * kTileM;
+    L.n_ranges = (L.n_tiles + tpr - 1) / tpr;
+    L.u_cols = idx->d_pad + (int64_t)kMaxHotBlocks * 64 * 2;
+    const int64_t Ppad = (int64_t)((P + kGroup - 1) / kGroup) * kGroup;
+    const size_t sizes[] = {
+        64,                                         // 0 header
+        (size_t)L.TS * 4, (size_t)L.TS * 4, (size_t)L.TS * 4, (size_t)L.TS * 4,   // 1-4 hash
+        (size_t)L.NU * 4, (size_t)L.NU * 4,         // 5-6 items
+        (size_t)Ppad * 128 * 4,                     // 7 hotw
+        (size_t)P * 4, (size_t)P * 4, (size_t)P * 4, (size_t)P * 4,   // 8-11 per user
+        (size_t)L.NU * 4, (size_t)L.NU * 4, (size_t)L.NU * 4, (size_t)L.NU * 4, (size_t)L.NU * 4,   // 12-16 union
+        (size_t)L.NU * 4,                           // 17 pairs
+        (size_t)Ppad * L.u_cols * 2,                // 18 U
+        (size_t)L.NU * (L.n_ranges + 1) * 4,        // 19 span
+        (size_t)idx->n_pad,                         // 20 adcnt
+        (size_t)L.n_ranges * 4, (size_t)(L.n_ranges + 1) * 4,   // 21-22
+        (size_t)(L.n_tiles + 1) * 4,                // 23 tile_off
+        (size_t)idx->n_pad * idx->n_fields * 4,     // 24 entries
+        (size_t)P * L.n_samp * 4,                   // 25 samp
+        (size_t)P * 8, (size_t)P * 4,               // 26-27 theta, count
+        (size_t)P * L.cap * 8,                      // 28 cand
+        (size_t)P * 4,                              // 29 flags
+        (size_t)kMaxFallback * idx->n_pad * 4,      // 30 dense
+    };
+    size_t o = 0;
+    for (int i = 0; i < 31; ++i) {
+        L.off[i] = o;
+        o = (o + sizes[i] + 1023) & ~(size_t)1023;
+    }
+    L.total = o;
+    return L;
+}
+
+static Ws carve(char* b, const Layout& L) {
+    Ws w;
+    auto at = [&](int i) { return b + L.off[i]; };
+    w.header = (uint32_t*)at(0);
+    w.hkey = (uint32_t*)at(1); w.hcnt = (uint32_t*)at(2); w.hslot = (uint32_t*)at(3); w.hpair = (uint32_t*)at(4);
+    w.item_t = (int32_t*)at(5); w.item_w = (float*)at(6);
+    w.hotw = (float*)at(7);
+    w.bound = (float*)at(8); w.emax = (uint32_t*)at(9); w.ushift = (int32_t*)at(10); w.uscale = (float*)at(11);
+    w.ukey = (uint32_t*)at(12); w.uc0 = (uint32_t*)at(13); w.uc1 = (uint32_t*)at(14); w.ukwb = (uint32_t*)at(15);
+    w.uentry = (uint32_t*)at(16); w.pairs = (uint32_t*)at(17);
+    w.U = (uint16_t*)at(18);
+    w.span = (uint32_t*)at(19);
+    w.adcnt = (uint32_t*)at(20);
+    w.rtotal = (uint32_t*)at(21); w.rbase = (uint32_t*)at(22);
+    w.tile_off = (uint32_t*)at(23);
+    w.entries = (uint32_t*)at(24);
+    w.samp = (float*)at(25);
+    w.theta = (uint64_t*)at(26); w.cand_count = (uint32_t*)at(27);
+    w.cand = (uint64_t*)at(28);
+    w.uflags = (uint32_t*)at(29);
+    w.dense = (float*)at(30);
+    return w;
+}
+
+// ------------------------------------------------------------------------------------------
+// A1 plan
+// ------------------------------------------------------------------------------------------
+struct PlanArgs {
+    const int32_t* user_feat;   // [P][F][S] of this pass
+    const float* user_x;
+    const uint16_t* user_emb;   // [P][d]
+    const uint32_t* key_chunk_off;
+    const uint32_t* key_word_off;
+    const float* cross_w;
+    const int32_t* field_card;
+    const int32_t* field_base;
+    const int32_t* hot_slot;
+    int F, S, P, d, d_pad, n_hot_used, pieces, u_cols;
+    int64_t TS;
+    uint32_t* err;
+};
+
+__device__ __forceinline__ uint32_t hash_key(uint32_t k) {
+    k ^= k >> 16; k *= 0x7feb352dU; k ^= k >> 15; k *= 0x846ca68bU; k ^= k >> 16;
+    return k;
+}
+
+// plan_a: every slot of the pass.  Hot slot -> its w~ is summed into hotw[u][h]; cold slot with
+// postings -> the key is inserted into the pass's hash table (the batch's key union) and the
+// user's fixed-point bounds are updated.  w~ = fl32(w x): one rounding, never an FMA (R10).
+__global__ void __launch_bounds__(256) plan_a_kernel(PlanArgs a, Ws ws) {
+    const int n = a.P * a.F * a.S;
+    const uint32_t mask = (uint32_t)a.TS - 1u;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        ws.item_t[i] = -1;
+        const int f = (i / a.S) % a.F;
+        const int u = i / (a.F * a.S);
+        const int32_t v = a.user_feat[i];
+        if (v < -1 || v >= a.field_card[f]) { atomicOr(a.err, 1u); continue; }   // outside [-1, V_f)
+        if (v < 0) continue;
+        const uint32_t key = (uint32_t)(a.field_base[f] + v);
+        const float w = __fmul_rn(__ldg(&a.cross_w[key]), a.user_x[i]);
+        const int h = a.n_hot_used ? __ldg(&a.hot_slot[key]) : -1;
+        if (h >= 0 && h < a.n_hot_used && fabsf(w) < 16384.f) {   // fp16 pieces need |w~| < 2^14
+            atomicAdd(&ws.hotw[(size_t)u * 128 + h], w);
+            continue;
+        }
+        if (__ldg(&a.key_chunk_off[key + 1]) <= __ldg(&a.key_chunk_off[key])) continue;   // empty list
+        atomicAdd(&ws.bound[u], fabsf(w));
+        atomicMax(&ws.emax[u], __float_as_uint(fabsf(w)));
+        uint32_t t = hash_key(key) & mask;
+        while (true) {
+            const uint32_t prev = atomicCAS(&ws.hkey[t], 0u, key + 1u);
+            if (prev == 0u || prev == key + 1u) break;
+            t = (t + 1u) & mask;
+        }
+        atomicAdd(&ws.hcnt[t], 1u);
+        ws.item_t[i] = (int32_t)t;
+        ws.item_w[i] = w;
+    }
+}
+
+// plan_b (one CTA): compacts the hash table into union slots (scan), assigns each key its pair
+// range, resets the table for the next pass, and derives every user's fixed-point scale
+//   S_u = min(22 - e_max, 30 - e_sum),  max|w~| < 2^e_max,  sum|w~| < 2^e_sum
+// so each w~ 2^S fits the 23-bit pair field and every partial sum fits int32 (R23).
+__global__ void __launch_bounds__(kPlanThreads) plan_b_kernel(PlanArgs a, Ws ws) {
     __shared__ uint32_t sScan[40];
-    __shared__ float sBound[kGroup];         // sum |w~| of each user's cold items
-    __shared__ uint64_t sCarry;
+    __shared__ uint32_t sBase[2];
     const int tid = threadIdx.x;
-    uint16_t* U = reinterpret_cast<uint16_t*>(ws.U);
-    // user tile, deep part (zero padded): U[u][0..d_pad)
-    for (int i = tid; i < nu_pad * d_pad; i += blockDim.x) {
-        const int u = i / d_pad, j = i - u * d_pad;
-        const uint16_t v = (u < nu && j < d) ? user_emb[(size_t)u * d + j] : (uint16_t)0;
-        U[(size_t)u * u_cols + j] = v;
-    }
-    for (int i = tid; i < nu_pad * n_hot; i += blockDim.x) sHot[i] = 0.f;
-    for (int i = tid; i < kGroup; i += blockDim.x) sBound[i] = 0.f;
+    if (tid == 0) { sBase[0] = 0; sBase[1] = 0; }
     __syncthreads();
-    const int nslot = nu * F * S;
-    uint32_t base = 0;
-    if (tid == 0) sCarry = 0;
-    __syncthreads();
-    for (int s0 = 0; s0 < nslot; s0 += blockDim.x) {
-        const int i = s0 + tid;
-        BItem it{};
-        bool ok = false;
-        if (i < nslot) {
-            const int f = (i / S) % F;
-            const int32_t v = user_feat[i];
-            if (v >= field_card[f]) atomicOr(err, 1u);
-            else if (v >= 0) {
-                const uint32_t key = (uint32_t)(field_base[f] + v);
-                it.c0 = key_chunk_off[key];
-                it.c1 = key_chunk_off[key + 1];
-                it.key = key;
-                it.u = (uint32_t)(i / (F * S));
-                it.kwb = key_word_off[key];
-                it.w = __fmul_rn(cross_w[key], user_x[i]);   // w~ = fl32(w x), never an FMA (R10)
-                const int32_t h = n_hot ? hot_slot[key] : -1;
-                if (h >= 0 && h < n_hot) atomicAdd(&sHot[it.u * n_hot + h], it.w);   // dense column (R22)
-                else ok = it.c1 > it.c0;
-                if (ok) atomicAdd(&sBound[it.u], fabsf(it.w));
-            }
-        }
-        uint32_t tot;
-        const uint32_t pos = block_exclusive_scan(ok ? 1u : 0u, sScan, &tot);
-        uint32_t ctot;
-        const uint32_t cpre = block_exclusive_scan(ok ? it.c1 - it.c0 : 0u, sScan, &ctot);
-        if (ok) {
-            ws.items[base + pos] = it;
-            ws.chunk_off[base + pos] = sCarry + cpre;
+    for (int64_t t0 = 0; t0 < a.TS; t0 += kPlanThreads) {
+        const int64_t t = t0 + tid;
+        uint32_t key1 = 0, cnt = 0;
+        if (t < a.TS) { key1 = ws.hkey[t]; cnt = key1 ? ws.hcnt[t] : 0u; }
+        uint32_t tot_s, tot_p;
+        const uint32_t ps = block_exclusive_scan(key1 ? 1u : 0u, sScan, &tot_s);
+        const uint32_t pp = block_exclusive_scan(cnt, sScan, &tot_p);
+        if (key1) {
+            const uint32_t s = sBase[0] + ps, p0 = sBase[1] + pp;
+            const uint32_t key = key1 - 1u;
+            ws.hslot[t] = s;
+            ws.hpair[t] = p0;
+            ws.ukey[s] = key;
+            ws.uc0[s] = a.key_chunk_off[key];
+            ws.uc1[s] = a.key_chunk_off[key + 1];
+            ws.ukwb[s] = a.key_word_off[key];
+            ws.uentry[s] = ((cnt - 1u) << kEntryPsBits) | p0;
+            ws.hkey[t] = 0u;
         }
         __syncthreads();
-        if (tid == 0) sCarry += ctot;
-        base += tot;
+        if (tid == 0) { sBase[0] += tot_s; sBase[1] += tot_p; }
         __syncthreads();
     }
-    if (tid == 0) {
-        ws.header[0] = base;
-        ws.header[1] = 0;       // overflow users of this group
-        ws.header[2] = 0;       // users with fewer than K candidates (theta rank below K)
-        ws.chunk_off[base] = sCarry;
-    }
-    __syncthreads();
-    // fixed-point scale of each user's cold wide sum: |sum| <= bound < 2^e, S = 30 - e keeps every
-    // partial sum inside int32 (and int32 addition is modular anyway)
-    for (int u = tid; u < kGroup; u += blockDim.x) {
-        int e = 0;
-        frexpf(sBound[u] * 1.0001f + 1e-30f, &e);
-        ws.user_shift[u] = 30 - e;
-    }
-    // user tile, hot part: w~ of hot slot h as kHotPieces bf16 terms (hi, mid, lo; R22) in
-    // U[u][d_pad + ((h/64)*kHotPieces + p)*64 + h%64] -- one 64-column K block per (block, piece)
-    for (int i = tid; i < nu_pad * n_hot; i += blockDim.x) {
-        const int u = i / n_hot, h = i - u * n_hot;
-        float r = sHot[i];
-        uint16_t* dst = U + (size_t)u * u_cols + d_pad + (size_t)(h >> 6) * kHotPieces * 64 + (h & 63);
-#pragma unroll
-        for (int p = 0; p < kHotPieces; ++p) {
-            const __nv_bfloat16 b = __float2bfloat16_rn(r);
-            dst[p * 64] = __bfloat16_as_ushort(b);
-            r -= __bfloat162float(b);            // exact (Sterbenz-type cancellation of the top bits)
+    if (tid == 0) { ws.header[0] = sBase[0]; ws.header[1] = sBase[1]; ws.header[2] = 0; ws.header[4] = 0; }
+    for (int u = tid; u < a.P; u += kPlanThreads) {
+        const float b = ws.bound[u], m = __uint_as_float(ws.emax[u]);
+        int S = 0;
+        if (b > 0.f) {
+            int es = 0, em = 0;
+            frexpf(b * 1.0001f, &es);   // b < 2^es (the margin covers the rounding of the float sum)
+            frexpf(m, &em);             // m < 2^em
+            S = min(kPairWMax - em, 30 - es);
         }
+        ws.ushift[u] = S;
+        ws.uscale[u] = ldexpf(1.f, -S);
+        ws.bound[u] = 0.f;
+        ws.emax[u] = 0u;
     }
-    // items are in slot order, i.e. grouped by user: first item of each user by binary search
-    for (int u = tid; u <= nu; u += blockDim.x) {
-        int lo = 0, hi = (int)base;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if ((int)ws.items[mid].u < u) lo = mid + 1; else hi = mid;
+}
+
+// plan_c: the user pairs of every cold key (its own slot order is irrelevant: the integer sums are
+// order-free), and the pass's user tile: deep part bf16, hot part the exact fp16 pieces of w~.
+__global__ void __launch_bounds__(256) plan_c_kernel(PlanArgs a, Ws ws) {
+    const int n = a.P * a.F * a.S;
+    const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+    for (int i = gt; i < n; i += gs) {
+        const int32_t t = ws.item_t[i];
+        if (t < 0) continue;
+        const int u = i / (a.F * a.S);
+        const uint32_t pos = ws.hpair[t] + atomicSub(&ws.hcnt[t], 1u) - 1u;
+        const int S = ws.ushift[u];
+        const int32_t wf = (int32_t)__float2int_rn(ldexpf(ws.item_w[i], S));   // |wf| < 2^22
+        ws.pairs[pos] = ((uint32_t)u << kPairWBits) | ((uint32_t)wf & ((1u << kPairWBits) - 1u));
+    }
+    const int Ppad = (a.P + kGroup - 1) / kGroup * kGroup;
+    // deep part of U (zero padded rows and columns)
+    for (int i = gt; i < Ppad * a.d_pad; i += gs) {
+        const int u = i / a.d_pad, j = i - u * a.d_pad;
+        ws.U[(size_t)u * a.u_cols + j] = (u < a.P && j < a.d) ? a.user_emb[(size_t)u * a.d + j] : (uint16_t)0;
+    }
+    // hot part: hot key h of block hb = h / 64 -> columns d_pad + (hb * pieces + p) * 64 + h % 64
+    for (int i = gt; i < Ppad * a.n_hot_used; i += gs) {
+        const int u = i / a.n_hot_used, h = i - u * a.n_hot_used;
+        float w = ws.hotw[(size_t)u * 128 + h];
+        ws.hotw[(size_t)u * 128 + h] = 0.f;
+        uint16_t* dst = ws.U + (size_t)u * a.u_cols + a.d_pad + (size_t)(h >> 6) * a.pieces * 64 + (h & 63);
+        for (int p = 0; p < a.pieces; ++p) {
+            const __half hv = __float2half_rn(w);
+            dst[p * 64] = __half_as_ushort(hv);
+            w -= __half2float(hv);       // exact: the residual of a round-to-nearest
         }
-        ws.user_item[u] = (uint32_t)lo;
     }
 }
 
 // ------------------------------------------------------------------------------------------
-// 2a. spans: for every item and every kWideR-ad chunk j, the item's posting chunks that hold an
-//     id in [j*R, (j+1)*R): [span_lo[j][i], span[j+1][i]).  One warp per item, lanes binary-search
-//     different boundaries over the chunk first ids; chunk_last decides whether the chunk that
-//     straddles j*R reaches into the range (so an item with no posting there costs nothing).
+// A2 the entry stream: the union's cold postings, decoded once per pass, as per-tile lists
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) span_kernel(const uint2* __restrict__ hdr,
-                                                   const uint32_t* __restrict__ chunk_last,
-                                                   BatchWs ws, int nj, int cap_items) {
+struct EntryArgs {
+    const uint2* hdr;
+    const uint32_t* chunk_last;
+    const uint32_t* payload;
+    int64_t n_ads, n_pad, range_ads;
+    int n_ranges, n_tiles;
+    int64_t NU;
+};
+
+// span: one warp per union key; span[s][j] = first chunk whose last id >= j R (j = 0..n_ranges)
+__global__ void __launch_bounds__(256) span_kernel(EntryArgs e, Ws ws) {
     const int lane = threadIdx.x & 31;
-    const uint32_t n_items = __ldcg(&ws.header[0]);
-    const uint32_t i = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-    if (i >= n_items) return;
-    const BItem t = ws.items[i];
-    for (int j = lane; j <= nj; j += 32) {
-        const uint32_t x = (uint32_t)((int64_t)j * kWideR);
-        uint32_t lo = t.c0, hi = t.c1;           // first chunk with first >= x
-        while (lo < hi) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (__ldg(&hdr[mid]).x < x) lo = mid + 1; else hi = mid;
+    const uint32_t s = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const uint32_t nu = __ldcg(&ws.header[0]);
+    if (s >= nu) return;
+    const uint32_t c0 = ws.uc0[s], c1 = ws.uc1[s];
+    uint32_t* sp = ws.span + (size_t)s * (e.n_ranges + 1);
+    const uint32_t R = (uint32_t)e.range_ads;
+    int last_r = -1;
+    for (uint32_t cb = c0; cb < c1; cb += 32) {
+        const uint32_t c = cb + lane;
+        int r = -1, rp = -1;
+        if (c < c1) {
+            r = (int)(__ldg(&e.chunk_last[c]) / R);
+            rp = (c == c0) ? -1 : (int)(__ldg(&e.chunk_last[c - 1]) / R);
+            for (int j = rp + 1; j <= r; ++j) sp[j] = c;
         }
-        ws.span[(size_t)j * cap_items + i] = lo;
-        if (j < nj) {
-            const bool straddles = lo > t.c0 && __ldg(&chunk_last[lo - 1]) >= x;
-            ws.span_lo[(size_t)j * cap_items + i] = straddles ? lo - 1 : lo;
-        }
+        const int m = __reduce_max_sync(FULL, r);
+        last_r = max(last_r, m);
+    }
+    for (int j = last_r + 1 + lane; j <= e.n_ranges; j += 32) sp[j] = c1;
+}
+
+// Calls f(local ad) for every posting of union key s inside range j, one warp.
+template <typename Fn>
+__device__ __forceinline__ void range_postings(const EntryArgs& e, const Ws& ws, uint32_t s, int j, int lane, Fn f) {
+    const uint32_t* sp = ws.span + (size_t)s * (e.n_ranges + 1);
+    const uint32_t lo = sp[j], c1 = ws.uc1[s];
+    const uint32_t hi = min(sp[j + 1] + 1u, c1);   // the chunk straddling the range end
+    const uint32_t kwb = ws.ukwb[s];
+    const uint32_t a0 = (uint32_t)((int64_t)j * e.range_ads), a1 = a0 + (uint32_t)e.range_ads;
+    for (uint32_t c = lo; c < hi; ++c) {
+        uint32_t id;
+        const bool ok = decode_chunk(e.hdr, e.payload, kwb, c, lane, id);
+        if (ok && id >= a0 && id < a1) f(id - a0);
     }
 }
 
-// ------------------------------------------------------------------------------------------
-// 2b. wide (cold keys): CTA (chunk j, user u) decodes the user's cold postings inside ads
-//     [j*R, (j+1)*R) and accumulates w~ on chip (Alg. 2 l.355-358 with the per-ad accumulator in
-//     shared memory).  Accumulation is 32-bit fixed point over native shared integer atomics: with
-//     the user's scale S (plan_kernel: |any partial sum| <= sum |w~| < 2^(30-S)), each w~ becomes
-//     rint(w~ 2^S); integer addition is exact and order-free (deterministic), and the one rounding
-//     is the final int -> fp32 conversion (exact for the dyadic inputs of exact mode; otherwise the
-//     quantisation error is <= 2^-31 of the user's bound per hit).  fp32 shared atomics are CAS
-//     loops on sm_100a.  Units of 16 posting chunks are load-balanced over the CTA's warps by an
-//     exclusive scan of the items' unit counts (the paper's ExclusiveScan + LoadBalance,
-//     l.353-354).  W is written tile-major with coalesced 16-byte stores; nothing to re-zero.
-// ------------------------------------------------------------------------------------------
-constexpr int kWideThreads = EBR_WIDE_T;
-constexpr int kWideItems = kWideThreads;   // items per pass of the unit scan
-#ifndef EBR_BUNIT
-#define EBR_BUNIT 8
-#endif
-constexpr int kBUnit = EBR_BUNIT;          // posting chunks per work unit (<= 32)
-#ifndef EBR_UNIT_MAP
-#define EBR_UNIT_MAP 1024
-#endif
-constexpr int kUnitMap = EBR_UNIT_MAP;     // units with a direct unit -> item entry (beyond: a walk)
-constexpr int kWideMinBlocks = (2048 / kWideThreads) < (200 * 1024 / (kWideR * 4)) ? (2048 / kWideThreads)
-                                                                                    : (200 * 1024 / (kWideR * 4));
-__global__ void __launch_bounds__(kWideThreads, kWideMinBlocks > 0 ? kWideMinBlocks : 1) wide_smem_kernel(const uint2* __restrict__ hdr,
-                                                                    const uint32_t* __restrict__ payload,
-                                                                    BatchWs ws, int nj, int64_t n_pad,
-                                                                    int cap_items) {
-    extern __shared__ __align__(16) int32_t acc[];   // [kWideR]
-    __shared__ uint32_t sLo[kWideItems], sHi[kWideItems], sUoff[kWideItems + 1], sScan[40], sCtr;
-    __shared__ uint16_t sUnitItem[kUnitMap];
-    __shared__ int32_t sF[kWideItems];
-    __shared__ uint32_t sKwb[kWideItems];
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = kWideThreads / 32;
-    const int j = blockIdx.x, u = blockIdx.y;
-    const int64_t a0 = (int64_t)j * kWideR;
-    const int64_t a1 = (a0 + kWideR < n_pad) ? a0 + kWideR : n_pad;
-    {
-        int4* a4 = reinterpret_cast<int4*>(acc);
-        for (int i = tid; i < kWideR / 4; i += kWideThreads) a4[i] = make_int4(0, 0, 0, 0);
+// entry_count: CTA = range; counts the postings of every ad (u8 per ad) and the range total
+__global__ void __launch_bounds__(512) entry_count_kernel(EntryArgs e, Ws ws) {
+    extern __shared__ uint32_t cnt[];      // [range_ads]
+    __shared__ uint32_t sRed[16];
+    const int j = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int R = (int)e.range_ads;
+    for (int i = tid; i < R; i += 512) cnt[i] = 0;
+    __syncthreads();
+    const uint32_t nu = __ldcg(&ws.header[0]);
+    for (uint32_t s = warp; s < nu; s += 16)
+        range_postings(e, ws, s, j, lane, [&](uint32_t a) { atomicAdd(&cnt[a], 1u); });
+    __syncthreads();
+    uint32_t tot = 0;
+    const int64_t a0 = (int64_t)j * R;
+    for (int i = tid; i < R / 4; i += 512) {
+        const uint32_t c0 = cnt[4 * i], c1 = cnt[4 * i + 1], c2 = cnt[4 * i + 2], c3 = cnt[4 * i + 3];
+        tot += c0 + c1 + c2 + c3;
+        if (a0 + 4 * i < e.n_pad) ws.adcnt[a0 / 4 + i] = c0 | (c1 << 8) | (c2 << 16) | (c3 << 24);   // <= F <= 255 each
     }
-    const uint32_t i0 = __ldcg(&ws.user_item[u]), i1 = __ldcg(&ws.user_item[u + 1]);
-    const int S = __ldcg(&ws.user_shift[u]);
-    for (uint32_t ib = i0; ib < i1; ib += kWideItems) {
-        const uint32_t ni = min((uint32_t)kWideItems, i1 - ib);
-        uint32_t nu_units = 0, lo = 0;
-        if ((uint32_t)tid < ni) {
-            const uint32_t it = ib + tid;
-            const BItem t = ws.items[it];
-            lo = __ldcg(&ws.span_lo[(size_t)j * cap_items + it]);
-            const uint32_t s1 = __ldcg(&ws.span[(size_t)(j + 1) * cap_items + it]);
-            nu_units = s1 > lo ? (s1 - lo + kBUnit - 1) / kBUnit : 0;
-            sF[tid] = (int32_t)__float2ll_rn(ldexpf(t.w, S));   // |w~ 2^S| < 2^30
-            sHi[tid] = s1;
-            sKwb[tid] = t.kwb;
-        }
+    tot = __reduce_add_sync(FULL, tot);
+    if (lane == 0) sRed[warp] = tot;
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < 16; ++w) t += sRed[w];
+        ws.rtotal[j] = t;
+    }
+}
+
+__global__ void __launch_bounds__(1024) range_scan_kernel(EntryArgs e, Ws ws) {
+    __shared__ uint32_t sScan[40];
+    __shared__ uint32_t sBase;
+    if (threadIdx.x == 0) sBase = 0;
+    __syncthreads();
+    for (int j0 = 0; j0 < e.n_ranges; j0 += 1024) {
+        const int j = j0 + threadIdx.x;
+        const uint32_t v = j < e.n_ranges ? ws.rtotal[j] : 0u;
         uint32_t tot;
-        const uint32_t pre = block_exclusive_scan(nu_units, sScan, &tot);
-        if ((uint32_t)tid < ni) {
-            sLo[tid] = lo;
-            sUoff[tid] = pre;
-            for (uint32_t v = pre; v < pre + nu_units && v < (uint32_t)kUnitMap; ++v) sUnitItem[v] = (uint16_t)tid;
-        }
-        if (tid == 0) { sUoff[ni] = tot; sCtr = 0u; }
+        const uint32_t pre = block_exclusive_scan(v, sScan, &tot);
+        if (j < e.n_ranges) ws.rbase[j] = sBase + pre;
         __syncthreads();
-        // units of up to kBUnit chunks are claimed dynamically from a shared counter (load balance
-        // across the CTA's warps; a warp's claims increase, so its item index walks forward) and
-        // software-pipelined: the next unit's chunk headers are in flight while this unit's
-        // payload words are extracted and scattered
-        struct BUnit { uint32_t unit; int l; uint32_t cb, nc; uint2 h; };
-        int lw = 0;
-        auto start = [&]() -> BUnit {
-            uint32_t unit = 0;
-            if (lane == 0) unit = atomicAdd(&sCtr, 1u);
-            BUnit r{__shfl_sync(FULL, unit, 0), 0, 0u, 0u, make_uint2(0u, 0u)};
-            if (r.unit < tot) {
-                if (r.unit < (uint32_t)kUnitMap) lw = sUnitItem[r.unit];       // unit -> item map
-                else while (sUoff[lw + 1] <= r.unit) ++lw;
-                r.l = lw;
-                r.cb = sLo[lw] + (r.unit - sUoff[lw]) * kBUnit;
-                r.nc = min(r.cb + kBUnit, sHi[lw]) - r.cb;
-                if ((uint32_t)lane < r.nc) r.h = __ldg(&hdr[r.cb + lane]);
-            }
-            return r;
-        };
-        BUnit cur = start();
-        while (cur.unit < tot) {
-            const uint32_t kwb = sKwb[cur.l];
-            uint32_t lo_w[kBUnit], hi_w[kBUnit];
-#pragma unroll
-            for (int qq = 0; qq < kBUnit; ++qq) {
-                lo_w[qq] = 0u;
-                hi_w[qq] = 0u;
-                if ((uint32_t)qq >= cur.nc) break;             // warp-uniform
-                const uint32_t meta = __shfl_sync(FULL, cur.h.y, qq);
-                const uint32_t n = (meta & 31u) + 1u, bw = (meta >> 5) & 31u;
-                if (lane >= 1 && (uint32_t)lane < n && bw) {
-                    const uint32_t bit = (uint32_t)(lane - 1) * bw;
-                    const uint32_t wi = kwb + (meta >> 10) + (bit >> 5);
-                    lo_w[qq] = __ldg(&payload[wi]);
-                    hi_w[qq] = __ldg(&payload[wi + 1]);
-                }
-            }
-            const BUnit nxt = start();                       // overlaps this unit's payload round trip
-            const int32_t Fv = sF[cur.l];
-#pragma unroll
-            for (int qq = 0; qq < kBUnit; ++qq) {
-                if ((uint32_t)qq >= cur.nc) break;
-                const uint32_t meta = __shfl_sync(FULL, cur.h.y, qq);
-                const uint32_t first = __shfl_sync(FULL, cur.h.x, qq);
-                const uint32_t n = (meta & 31u) + 1u, bw = (meta >> 5) & 31u;
-                uint32_t g;
-                if (lane == 0) {
-                    g = first;
-                } else if ((uint32_t)lane < n) {
-                    uint32_t v = 0u;
-                    if (bw) {
-                        const uint32_t bit = (uint32_t)(lane - 1) * bw;
-                        v = (uint32_t)(((((uint64_t)hi_w[qq]) << 32) | lo_w[qq]) >> (bit & 31u)) & ((1u << bw) - 1u);
-                    }
-                    g = v + 1u;
-                } else {
-                    g = 0u;
-                }
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t t = __shfl_up_sync(FULL, g, o);
-                    if (lane >= o) g += t;
-                }
-                if ((uint32_t)lane < n && (int64_t)g >= a0 && (int64_t)g < a1) atomicAdd(&acc[g - a0], Fv);
-            }
-            cur = nxt;
-        }
+        if (threadIdx.x == 0) sBase += tot;
         __syncthreads();
     }
-    const float inv = ldexpf(1.f, -S);
-    const int64_t t0 = a0 / kTileM;
-    // dense W[tile][u][row]: the chunk spans (a1 - a0) / 128 tiles; 32 float4 per (tile, user) row
-    const int4* a4 = reinterpret_cast<const int4*>(acc);
-    for (int64_t i = tid; i < (a1 - a0) / 4; i += kWideThreads) {
-        const int4 v = a4[i];
-        float4 o;
-        o.x = v.x ? (float)v.x * inv : 0.f;          // int -> fp32: the one rounding; * 2^-S exact
-        o.y = v.y ? (float)v.y * inv : 0.f;
-        o.z = v.z ? (float)v.z * inv : 0.f;
-        o.w = v.w ? (float)v.w * inv : 0.f;
-        const int64_t t = t0 + (i >> 5);
-        __stcg(reinterpret_cast<float4*>(ws.W + ((size_t)t * kGroup + u) * kTileM) + (i & 31), o);
+    if (threadIdx.x == 0) {
+        ws.rbase[e.n_ranges] = sBase;
+        ws.tile_off[e.n_tiles] = sBase;
+        ws.header[3] = sBase;
+    }
+}
+
+// entry_write: CTA = range; per-ad offsets (scan of the counts), the tile offsets, then every
+// posting written as an entry row << 24 | uentry[s] at its ad's next slot
+__global__ void __launch_bounds__(512) entry_write_kernel(EntryArgs e, Ws ws) {
+    extern __shared__ uint32_t cur[];      // [range_ads] running position of each ad's entries
+    __shared__ uint32_t sScan[40];
+    const int j = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int R = (int)e.range_ads;
+    const int64_t a0 = (int64_t)j * R;
+    const uint32_t base = ws.rbase[j];
+    const uint8_t* cnt8 = reinterpret_cast<const uint8_t*>(ws.adcnt);
+    // thread tid owns the ads [tid*pp, tid*pp + pp) of the range
+    const int pp = (R + 511) / 512;
+    const int i0 = tid * pp;
+    uint32_t local = 0;
+    for (int q = 0; q < pp; ++q) {
+        const int i = i0 + q;
+        if (i < R && a0 + i < e.n_pad) local += cnt8[a0 + i];
+    }
+    uint32_t tot;
+    uint32_t pre = block_exclusive_scan(local, sScan, &tot);
+    for (int q = 0; q < pp; ++q) {
+        const int i = i0 + q;
+        if (i >= R) break;
+        cur[i] = pre;
+        if ((i & (kTileM - 1)) == 0 && a0 + i < e.n_pad) ws.tile_off[(a0 + i) / kTileM] = base + pre;
+        if (a0 + i < e.n_pad) pre += cnt8[a0 + i];
+    }
+    __syncthreads();
+    const uint32_t nu = __ldcg(&ws.header[0]);
+    for (uint32_t s = warp; s < nu; s += 16) {
+        const uint32_t ent = ws.uentry[s];
+        range_postings(e, ws, s, j, lane, [&](uint32_t a) {
+            const uint32_t pos = atomicAdd(&cur[a], 1u);
+            ws.entries[base + pos] = ((a & (kTileM - 1)) << 24) | ent;
+        });
     }
 }
 
 // ------------------------------------------------------------------------------------------
-// 3/5. tcgen05 GEMM with the fused epilogue
+// A3-A6b: the fused tensor-core kernel
 // ------------------------------------------------------------------------------------------
 struct GemmParams {
     int64_t n_ads, n_pad;
     uint32_t ad_begin;
-    int d_pad, n_kb;       // deep K blocks of 64
-    int n_hb;              // hot-key K blocks of 64 (A side: H; B side: kHotPieces blocks each)
-    int u_blocks;          // K blocks of the user tile: n_kb + n_hb * kHotPieces
-    int nu, nu_pad;        // users in this group (valid / padded to 32)
-    int n_tiles;           // tiles to process in this launch
-    int tile_stride;       // 1 (all tiles) or kSampleStride (sample)
-    int n_samp;            // sample buffer row length (ads)
-    int stages;            // A/H ring stages (16 KB each)
-    int wstages;           // W ring stages (one 32-user x 128-ad fp32 chunk = 16 KB each)
-    int64_t cap;           // candidate capacity per user
-    BatchWs ws;
+    int n_kb, n_hb, pieces, u_blocks;
+    int P;                  // users in this pass
+    int n_tiles, tile_stride;
+    int n_samp;
+    int stages;
+    int64_t cap;
+    int rerun;              // filter rerun: only flagged users; gated on header[2] | header[4]
+    int dense;              // sample-mode variant: every score of the overflowed users (gated on header[4])
+    const uint4* hot_mask;
+    Ws ws;
+    uint32_t* err;
 };
 
-template <int MODE>   // 0: sample (store s), 1: filter (append keys >= theta)
+__device__ __forceinline__ int32_t pair_w(uint32_t pr) {
+    return (int32_t)(pr << (32 - kPairWBits)) >> (32 - kPairWBits);   // sign-extend the 23-bit field
+}
+
+template <int MODE>   // 0: sample (store s; dense: all scores of overflowed users), 1: filter (append keys >= theta)
 __global__ void __launch_bounds__(kGemmThreads, 1)
-gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmH,
-            const __grid_constant__ CUtensorMap tmU, const GemmParams p) {
+score_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmU, const GemmParams p) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // gated launches (uniform over the grid): nothing to redo
+    if (MODE == 1 && p.rerun && (*(volatile uint32_t*)&p.ws.header[2] | *(volatile uint32_t*)&p.ws.header[4]) == 0u)
+        return;
+    if (MODE == 0 && p.dense && *(volatile uint32_t*)&p.ws.header[4] == 0u) return;
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int u_bytes = p.nu_pad * 128 * p.u_blocks;
-    const int nkt = p.n_kb + p.n_hb;                                // A-side K blocks per tile
-    unsigned char* sU = smem;                                       // [u_blocks][nu_pad rows x 128 B]
-    unsigned char* sA = smem + ((u_bytes + 1023) & ~1023);          // ring: [stages][128 x 128 B]
-    float* sW = reinterpret_cast<float*>(sA + (size_t)p.stages * kBlockBytes);   // [wstages][32][128]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sA + (size_t)(p.stages + p.wstages) * kBlockBytes);
-    uint64_t* full = bars;                       // [stages]
-    uint64_t* empty = bars + p.stages;           // [stages]
-    uint64_t* wfull = bars + 2 * p.stages;       // [wstages] W chunk landed
-    uint64_t* wempty = wfull + p.wstages;        // [wstages] W chunk read by its 4 loader warps
-    uint64_t* tfull = wempty + p.wstages;        // [kAccStages] MMA done -> epilogue
-    uint64_t* tempty = tfull + kAccStages;       // [kAccStages] epilogue drained -> wide loaders
-    uint64_t* wready = tempty + kAccStages;      // [kAccStages] wide term stored -> MMA
+    const uint32_t rank = tc::cluster_ctarank();
+    uint32_t csize;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(csize));
+    const uint32_t cid = tc::cluster_id_x(), ncl = tc::cluster_count_x();
+    const uint16_t mc_mask = (uint16_t)((1u << csize) - 1u);
+    const int g = (int)rank;                         // this CTA's user group
+    const int nu = min(kGroup, p.P - g * kGroup);    // valid users
+    const int nu_pad = (nu + 31) & ~31;
+    const int nkt = p.n_kb + p.n_hb;
+
+    unsigned char* sU = smem;                                               // [u_blocks][128 x 128 B]
+    unsigned char* sRing = sU + (size_t)p.u_blocks * kBlockBytes;          // [stages][128 x 128 B]
+    int32_t* acc = reinterpret_cast<int32_t*>(sRing + (size_t)p.stages * kBlockBytes);   // [128][kAccPitch]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(acc + kTileM * kAccPitch);
+    uint64_t* full = bars;
+    uint64_t* empty = full + p.stages;
+    uint64_t* tfull = empty + p.stages;
+    uint64_t* tempty = tfull + kAccStages;
+    uint64_t* wready = tempty + kAccStages;
     uint64_t* ufull = wready + kAccStages;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ufull + 1);
-    uint64_t* sTheta = reinterpret_cast<uint64_t*>(tmem_slot + 2);  // [kGroup]
-    float* sThetaS = reinterpret_cast<float*>(sTheta + kGroup);       // score part of theta, [kGroup]
+    uint64_t* sTheta = reinterpret_cast<uint64_t*>(tmem_slot + 2);          // [kGroup]
+    float* sThetaS = reinterpret_cast<float*>(sTheta + kGroup);             // [kGroup]
+    float* sScale = sThetaS + kGroup;                                       // [kGroup]
+    int* sDense = reinterpret_cast<int*>(sScale + kGroup);                  // [kGroup] dense slot or -1
 
     if (tid == 0) {
-        for (int s = 0; s < p.stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (int s = 0; s < p.wstages; ++s) { mbar_init(&wfull[s], 1); mbar_init(&wempty[s], 4); }
+        for (int s = 0; s < p.stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], csize); }
         for (int s = 0; s < kAccStages; ++s) {
             mbar_init(&tfull[s], 1);
             mbar_init(&tempty[s], kEpiWarps);
-            mbar_init(&wready[s], kLoadWarps);
+            mbar_init(&wready[s], 1);
         }
         mbar_init(ufull, 1);
         fence_mbar_init();
     }
-    if (warp == 2) tc::tmem_alloc(tmem_slot, kAccStages * 128);     // kAccStages x 128 user columns
-    if (MODE == 1)
-        for (int i = tid; i < p.nu_pad; i += kGemmThreads) {
-            sTheta[i] = __ldcg(&p.ws.theta[i]);
-            sThetaS[i] = score_of(sTheta[i]);       // key >= theta implies score >= this
+    if (warp == 2) tc::tmem_alloc(tmem_slot, kAccStages * 128);
+    for (int i = tid; i < kTileM * kAccPitch / 4; i += kGemmThreads)
+        reinterpret_cast<int4*>(acc)[i] = make_int4(0, 0, 0, 0);
+    for (int i = tid; i < kGroup; i += kGemmThreads) {
+        const int u = g * kGroup + i;
+        const bool ok = i < nu;
+        sScale[i] = ok ? p.ws.uscale[u] : 0.f;
+        const uint32_t fl = ok ? __ldcg(&p.ws.uflags[u]) : 0u;
+        if (MODE == 0) sDense[i] = (p.dense && (fl & kFlagOverflow)) ? (int)(fl >> 8) : -1;
+        if (MODE == 1) {
+            bool take = ok;
+            if (p.rerun) take = ok && (fl & kFlagAny);
+            sTheta[i] = take ? __ldcg(&p.ws.theta[u]) : ~0ull;
+            sThetaS[i] = take ? score_of(sTheta[i]) : __int_as_float(0x7F800000);
         }
+    }
     tc::fence_before();
     __syncthreads();
+    tc::cluster_sync_all();          // every CTA's barriers initialised before any multicast / remote commit
     tc::fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
         if (lane == 0) {
-            // ---------------- TMA producer ----------------
+            // ---------------- TMA producer: U once, then the deep K blocks of every tile ----------------
             tc::tma_prefetch(&tmA);
-            if (p.n_hb) tc::tma_prefetch(&tmH);
             tc::tma_prefetch(&tmU);
-            mbar_arrive_expect_tx(ufull, (uint32_t)u_bytes);
+            mbar_arrive_expect_tx(ufull, (uint32_t)(p.u_blocks * kBlockBytes));
             for (int kb = 0; kb < p.u_blocks; ++kb)
-                tc::tma_load_2d(sU + (size_t)kb * p.nu_pad * 128, &tmU, kb * kBlockK, 0, ufull);
-            uint32_t gb = 0;                                 // ring position (one K block per stage)
-            const uint64_t pol = tc::policy_evict_first();   // A and H are read once per pass
-            for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
+                tc::tma_load_2d(sU + (size_t)kb * kBlockBytes, &tmU, kb * kBlockK, g * kGroup, ufull);
+            const uint64_t pol = tc::policy_evict_first();   // A is streamed once per pass
+            uint32_t gb = 0;
+            for (int t = (int)cid; t < p.n_tiles; t += (int)ncl) {
                 const int row0 = t * p.tile_stride * kTileM;
                 for (int kb = 0; kb < nkt; ++kb, ++gb) {
+                    if (kb >= p.n_kb) continue;             // hot block: expanded by the wide warps
                     const uint32_t slot = gb % p.stages, round = gb / p.stages;
                     if (round > 0) mbar_wait_sleep(&empty[slot], (round - 1) & 1);
                     mbar_arrive_expect_tx(&full[slot], (uint32_t)kBlockBytes);
-                    if (kb < p.n_kb)
-                        tc::tma_load_2d_hint(sA + (size_t)slot * kBlockBytes, &tmA, kb * kBlockK, row0, &full[slot], pol);
-                    else
-                        tc::tma_load_2d_hint(sA + (size_t)slot * kBlockBytes, &tmH, (kb - p.n_kb) * kBlockK, row0,
-                                             &full[slot], pol);
+                    if (csize == 1)
+                        tc::tma_load_2d_hint(sRing + (size_t)slot * kBlockBytes, &tmA, kb * kBlockK, row0, &full[slot], pol);
+                    else if (rank == 0)
+                        tc::tma_load_2d_mc(sRing + (size_t)slot * kBlockBytes, &tmA, kb * kBlockK, row0, &full[slot],
+                                           mc_mask, pol);
                 }
+            }
+            // every remote arrival into this CTA's ring barriers has landed before it exits
+            for (uint32_t k = 0; k < (uint32_t)p.stages && k < gb; ++k) {
+                const uint32_t q = gb - 1 - k;
+                mbar_wait_sleep(&empty[q % p.stages], (q / p.stages) & 1);
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            // ---------------- MMA issuer (one thread) ----------------
-            // The accumulator stage already holds the tile's wide term (stored by the loader warps),
-            // so every MMA accumulates: D = W + A U^T (+ H (hi, mid, lo)^T).
-            const uint32_t idesc = tc::idesc_bf16_m128(p.nu_pad);
+            // ---------------- MMA issuer ----------------
+            // The accumulator stage already holds the tile's cold wide term (stored by the wide
+            // warps), so every MMA accumulates: D = cold + A U_deep^T + H (hi, lo)^T.
+            const uint32_t idb = tc::idesc_bf16_m128(nu_pad), idh = tc::idesc_f16_m128(nu_pad);
             mbar_wait_sleep(ufull, 0);
             tc::fence_after();
             int it = 0;
             uint32_t gb = 0;
-            for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++it) {
-                const int acc = it % kAccStages;
-                mbar_wait_sleep(&wready[acc], (it / kAccStages) & 1);
+            for (int t = (int)cid; t < p.n_tiles; t += (int)ncl, ++it) {
+                const int st = it % kAccStages;
+                mbar_wait_sleep(&wready[st], (it / kAccStages) & 1);
                 tc::fence_after();
-                const uint32_t d_tmem = tmem_base + (uint32_t)(acc * 128);
+                const uint32_t d_tmem = tmem_base + (uint32_t)(st * 128);
                 for (int kb = 0; kb < nkt; ++kb, ++gb) {
                     const uint32_t slot = gb % p.stages;
                     mbar_wait_sleep(&full[slot], (gb / p.stages) & 1);
                     tc::fence_after();
-                    const uint64_t da0 = tc::sdesc_sw128(sA + (size_t)slot * kBlockBytes);
-                    // deep block kb pairs with user block kb; hot block h with its kHotPieces
-                    // user blocks (the same one-hot A tile times hi, mid and lo of w~)
-                    const int np = kb < p.n_kb ? 1 : kHotPieces;
-                    const int ub0 = kb < p.n_kb ? kb : p.n_kb + (kb - p.n_kb) * kHotPieces;
-                    for (int pc = 0; pc < np; ++pc) {
-                        const uint64_t db0 = tc::sdesc_sw128(sU + (size_t)(ub0 + pc) * p.nu_pad * 128);
+                    const uint64_t da0 = tc::sdesc_sw128(sRing + (size_t)slot * kBlockBytes);
+                    if (kb < p.n_kb) {
+                        const uint64_t db0 = tc::sdesc_sw128(sU + (size_t)kb * kBlockBytes);
 #pragma unroll
-                        for (int k = 0; k < kBlockK / 16; ++k)   // +32 bytes per K step inside the swizzle row
-                            tc::umma_f16(d_tmem, da0 + (uint64_t)(k * 2), db0 + (uint64_t)(k * 2), idesc, 1u);
+                        for (int k = 0; k < kBlockK / 16; ++k)
+                            tc::umma_f16(d_tmem, da0 + (uint64_t)(k * 2), db0 + (uint64_t)(k * 2), idb, 1u);
+                    } else {
+                        const int h = kb - p.n_kb;
+                        for (int pc = 0; pc < p.pieces; ++pc) {
+                            const uint64_t db0 = tc::sdesc_sw128(sU + (size_t)(p.n_kb + h * p.pieces + pc) * kBlockBytes);
+#pragma unroll
+                            for (int k = 0; k < kBlockK / 16; ++k)
+                                tc::umma_f16(d_tmem, da0 + (uint64_t)(k * 2), db0 + (uint64_t)(k * 2), idh, 1u);
+                        }
                     }
-                    tc::umma_commit(&empty[slot]);     // ring stage free once these MMAs completed
+                    if (csize == 1) tc::umma_commit(&empty[slot]);
+                    else tc::umma_commit_mc(&empty[slot], mc_mask);
                 }
-                tc::umma_commit(&tfull[acc]);      // accumulator ready for the epilogue
+                tc::umma_commit(&tfull[st]);
             }
         }
-    } else if (warp == 3) {
-        if (lane == 0) {
-            // ---------------- W producer: the tile's 16 KB user chunks of W -> smem ring ----------------
-            // (bulk copies, the blocks streamed into L2 kWPrefetch tiles ahead)
-            const int nwc = p.nu_pad / 32;
-            const uint64_t keep = tc::policy_evict_last(), drop = tc::policy_evict_first();
-            auto prefetch = [&](int t) {     // held in L2 (evict_last) until its bulk copy reads it
-                if (t < p.n_tiles)
-                    tc::bulk_prefetch_l2_hint(p.ws.W + (size_t)t * p.tile_stride * kGroup * kTileM,
-                                              (uint32_t)p.nu_pad * kTileM * 4, keep);
-            };
-            for (int k = 0; k < kWPrefetch; ++k) prefetch(blockIdx.x + k * gridDim.x);
-            uint32_t g = 0;
-            for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
-                prefetch(t + kWPrefetch * gridDim.x);
-                const float* src = p.ws.W + (size_t)t * p.tile_stride * kGroup * kTileM;
-                for (int ch = 0; ch < nwc; ++ch, ++g) {
-                    const uint32_t slot = g % p.wstages, round = g / p.wstages;
-                    if (round > 0) mbar_wait_sleep(&wempty[slot], (round - 1) & 1);
-                    mbar_arrive_expect_tx(&wfull[slot], (uint32_t)kBlockBytes);
-                    tc::bulk_g2s_hint(sW + (size_t)slot * 32 * kTileM, src + (size_t)ch * 32 * kTileM,
-                                      (uint32_t)kBlockBytes, &wfull[slot], drop);
-                }
-            }
-        }
-    } else if (warp >= kLoadWarp0) {
-        // ---------------- wide loaders: W -> TMEM accumulator stage (before the MMA) ----------------
-        // loader warp q owns TMEM lane quadrant q (rows q*32..q*32+31) and walks the tile's 32-user
-        // chunks in ring order (the 4 loader warps are the only consumers of every W slot and take
-        // them strictly in sequence, so mbarrier parities never alias): read its 32 x 32 block
-        // from smem (conflict-free: lanes read consecutive rows), free the slot, and store the block
-        // into the accumulator stage once the epilogue has drained it (kAccStages tiles earlier).
-        const int q = warp & 3;
+    } else if (warp >= kWideWarp0 && warp < kEpiWarp0) {
+        // ---------------- wide warps: hot one-hot block, cold scatter, TMEM store ----------------
+        const int wt = tid - kWideWarp0 * 32;
+        const int q = warp & 3, half = (warp - kWideWarp0) >> 2;
         const int row = q * 32 + lane;
-        const int nwc = p.nu_pad / 32;
+        const uint32_t* __restrict__ entries = p.ws.entries;
+        const uint32_t* __restrict__ pairs = p.ws.pairs;
         int it = 0;
-        uint32_t g = 0;
-        for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++it) {
-            const int acc = it % kAccStages;
-            const int64_t tw = (int64_t)t * p.tile_stride;              // global tile index
-            const bool valid = tw * kTileM + row < p.n_ads;
-            for (int ch = 0; ch < nwc; ++ch, ++g) {
-                const int c = ch * 32;
-                const uint32_t slot = g % p.wstages;
-                mbar_wait_sleep(&wfull[slot], (g / p.wstages) & 1);
-                const float* w = sW + (size_t)slot * 32 * kTileM + row;
-                uint32_t wf[32];
+        uint32_t gb = 0;
+        for (int t = (int)cid; t < p.n_tiles; t += (int)ncl, ++it) {
+            const int st = it % kAccStages;
+            const int64_t tw = (int64_t)t * p.tile_stride;
+            // hot: the row's one-hot fp16 K block(s), written in the TMA 128B-swizzle layout
+            if (p.n_hb) {
+                const uint4 hm = __ldg(&p.hot_mask[tw * kTileM + row]);
+                for (int h = 0; h < p.n_hb; ++h) {
+                    const uint32_t pos = gb + p.n_kb + h;
+                    const uint32_t slot = pos % p.stages, round = pos / p.stages;
+                    if (round > 0) mbar_wait(&empty[slot], (round - 1) & 1);
+                    const uint64_t bits = h == 0 ? ((uint64_t)hm.y << 32 | hm.x) : ((uint64_t)hm.w << 32 | hm.z);
+                    unsigned char* rowp = sRing + (size_t)slot * kBlockBytes + (size_t)row * 128;
 #pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    wf[j] = (valid && c + j < p.nu) ? __float_as_uint(w[j * kTileM]) : 0u;
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&wempty[slot]);
-                if (ch == 0 && it >= kAccStages) mbar_wait_sleep(&tempty[acc], ((it / kAccStages) - 1) & 1);
-                tc::fence_after();
-                tc::tmem_st32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * 128 + c), wf);
+                    for (int cc = 0; cc < 4; ++cc) {
+                        const int c = half * 4 + cc;                 // 16-byte chunk: keys 8c .. 8c+7
+                        const uint32_t byte = (uint32_t)(bits >> (8 * c)) & 0xFFu;
+                        uint4 v;
+                        v.x = ((byte & 1u) ? 0x3C00u : 0u) | ((byte & 2u) ? 0x3C000000u : 0u);
+                        v.y = ((byte & 4u) ? 0x3C00u : 0u) | ((byte & 8u) ? 0x3C000000u : 0u);
+                        v.z = ((byte & 16u) ? 0x3C00u : 0u) | ((byte & 32u) ? 0x3C000000u : 0u);
+                        v.w = ((byte & 64u) ? 0x3C00u : 0u) | ((byte & 128u) ? 0x3C000000u : 0u);
+                        *reinterpret_cast<uint4*>(rowp + ((c ^ (row & 7)) << 4)) = v;
+                    }
+                    tc::fence_proxy_async_smem();
+                    tc::named_bar_sync(1, kWideThreads);
+                    if (wt == 0) mbar_arrive(&full[slot]);
+                }
             }
-            tc::fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&wready[acc]);
-        }
-    } else if (warp >= kEpiWarp0) {
-        // ---------------- epilogue: TMEM -> registers, key, filter ----------------
-        const int e = warp - kEpiWarp0;
-        const int q = warp & 3;                    // TMEM lane quadrant of this warp
-        const int row = q * 32 + lane;             // ad row inside the tile
-        int it = 0;
-        for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++it) {
-            const int acc = it % kAccStages;
-            const int64_t a = (int64_t)t * p.tile_stride * kTileM + row;   // shard-local ad
-            const bool valid = a < p.n_ads;
-            mbar_wait_sleep(&tfull[acc], (it / kAccStages) & 1);
+            gb += nkt;
+            // cold: the tile's entries (row, the key's user pairs); this CTA takes its group's users
+            const uint32_t e0 = __ldcg(&p.ws.tile_off[tw]), e1 = __ldcg(&p.ws.tile_off[tw + 1]);
+            for (uint32_t e = e0 + wt; e < e1; e += kWideThreads) {
+                const uint32_t ent = __ldcg(&entries[e]);
+                const uint32_t r = ent >> 24;
+                const uint32_t ps = ent & (kMaxPassPairs - 1);
+                const uint32_t pe = ps + ((ent >> kEntryPsBits) & 511u) + 1u;
+                int32_t* arow = acc + r * kAccPitch;
+                for (uint32_t pi = ps; pi < pe; ++pi) {
+                    const uint32_t pr = __ldcg(&pairs[pi]);
+                    const uint32_t u = pr >> kPairWBits;
+                    if ((int)(u >> 7) == g) atomicAdd(&arow[u & 127u], pair_w(pr));
+                }
+            }
+            tc::named_bar_sync(1, kWideThreads);
+            // the accumulator stage is free once the epilogue drained it (kAccStages tiles ago)
+            if (it >= kAccStages) mbar_wait(&tempty[st], ((it / kAccStages) - 1) & 1);
             tc::fence_after();
 #pragma unroll 1
-            for (int ch = 0; ch < kEpiChunks; ++ch) {
-                const int c = (e >> 2) * (32 * kEpiChunks) + ch * 32;   // this chunk's 32 users
-                if (c >= p.nu_pad) break;
+            for (int ch = 0; ch < 2; ++ch) {
+                const int c = half * 64 + ch * 32;
+                if (c >= nu_pad) break;
+                int4* src = reinterpret_cast<int4*>(acc + row * kAccPitch + c);
+                uint32_t f[32];
+#pragma unroll
+                for (int v4 = 0; v4 < 8; ++v4) {
+                    const int4 v = src[v4];
+                    src[v4] = make_int4(0, 0, 0, 0);
+                    f[4 * v4 + 0] = __float_as_uint((float)v.x * sScale[c + 4 * v4 + 0]);   // the one rounding
+                    f[4 * v4 + 1] = __float_as_uint((float)v.y * sScale[c + 4 * v4 + 1]);
+                    f[4 * v4 + 2] = __float_as_uint((float)v.z * sScale[c + 4 * v4 + 2]);
+                    f[4 * v4 + 3] = __float_as_uint((float)v.w * sScale[c + 4 * v4 + 3]);
+                }
+                tc::tmem_st32_nowait(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(st * 128 + c), f);
+            }
+            tc::tmem_wait_st();
+            tc::fence_before();
+            tc::named_bar_sync(1, kWideThreads);
+            if (wt == 0) mbar_arrive(&wready[st]);
+        }
+    } else if (warp >= kEpiWarp0) {
+        // ---------------- epilogue: TMEM -> registers, kappa, sample store / filter ----------------
+        const int e = warp - kEpiWarp0;
+        const int q = warp & 3;
+        const int row = q * 32 + lane;
+        int it = 0;
+        for (int t = (int)cid; t < p.n_tiles; t += (int)ncl, ++it) {
+            const int st = it % kAccStages;
+            const int64_t a = (int64_t)t * p.tile_stride * kTileM + row;   // shard-local ad
+            const bool valid = a < p.n_ads;
+            mbar_wait_sleep(&tfull[st], (it / kAccStages) & 1);
+            tc::fence_after();
+#pragma unroll 1
+            for (int ch = 0; ch < 2; ++ch) {
+                const int c = (e >> 2) * 64 + ch * 32;
+                if (c >= nu_pad) break;
                 uint32_t r[32];
-                tc::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * 128 + c), r);
-                const int nuc = p.nu - c;                 // valid users in these 32 columns
+                tc::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(st * 128 + c), r);
+                const int nuc = nu - c;
                 const uint32_t umask = nuc >= 32 ? 0xFFFFFFFFu : (nuc > 0 ? (1u << nuc) - 1u : 0u);
-                if (MODE == 0) {
+                if (MODE == 0 && p.dense) {
+                    for (int j = 0; j < 32; ++j) {
+                        const int sl = sDense[c + j];
+                        if (sl >= 0 && ((umask >> j) & 1u)) {
+                            float s = __uint_as_float(r[j]);
+                            if (s == 0.f) s = 0.f;
+                            p.ws.dense[(size_t)sl * p.n_pad + a] = valid ? s : __int_as_float(0xFF800000);
+                        }
+                    }
+                } else if (MODE == 0) {
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
                         float s = __uint_as_float(r[j]);
                         if (s == 0.f) s = 0.f;                       // -0 -> +0 (R14)
                         if ((umask >> j) & 1u)
-                            p.ws.samp[(size_t)(c + j) * p.n_samp + (int64_t)t * kTileM + row] =
+                            p.ws.samp[(size_t)(g * kGroup + c + j) * p.n_samp + (int64_t)t * kTileM + row] =
                                 valid ? s : __int_as_float(0xFF800000);
                     }
                 } else {
-                    // branch-free pre-filter of all 32 columns, then the exact key compare only
-                    // for the columns where some lane passed
                     uint32_t pass = 0;
                     const float4* th4 = reinterpret_cast<const float4*>(sThetaS + c);
 #pragma unroll
@@ -594,61 +766,52 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                         pass |= (__uint_as_float(r[j4 * 4 + 3]) >= th.w ? 1u : 0u) << (j4 * 4 + 3);
                     }
                     pass &= valid ? umask : 0u;
-                    // compact (not unrolled) loop over the columns where some lane passed: the
-                    // unrolled form overflowed the instruction cache (ncu: no_instruction stalls)
                     uint32_t cols = __reduce_or_sync(FULL, pass);
 #pragma unroll 1
                     while (cols) {
                         const int j = __ffs(cols) - 1;
                         cols &= cols - 1u;
-                        {
-                            const int u = c + j;
-                            const bool maybe = (pass >> j) & 1u;
-                            float s = 0.f;
+                        const int ul = c + j;                         // CTA-local user
+                        const int u = g * kGroup + ul;                // pass user
+                        const bool maybe = (pass >> j) & 1u;
+                        float s = 0.f;
 #pragma unroll
-                            for (int jj = 0; jj < 32; ++jj) s = (jj == j) ? __uint_as_float(r[jj]) : s;
-                            if (s == 0.f) s = 0.f;                       // -0 -> +0 (R14)
-                            const uint64_t key = maybe ? kappa_of(s, p.ad_begin + (uint32_t)a) : 0ull;
-                            const bool take = maybe && key >= sTheta[u];
-                            const unsigned m = __ballot_sync(FULL, take);
-                            if (m) {
-                                const int leader = __ffs(m) - 1;
-                                uint32_t pos = 0;
-                                if (lane == leader) pos = atomicAdd(&p.ws.cand_count[u], (uint32_t)__popc(m));
-                                pos = __shfl_sync(FULL, pos, leader) + __popc(m & ((1u << lane) - 1u));
-                                if (take && pos < p.cap) p.ws.cand[(size_t)u * p.cap + pos] = key;
-                            }
+                        for (int jj = 0; jj < 32; ++jj) s = (jj == j) ? __uint_as_float(r[jj]) : s;
+                        if (s == 0.f) s = 0.f;                       // -0 -> +0 (R14)
+                        const uint64_t key = maybe ? kappa_of(s, p.ad_begin + (uint32_t)a) : 0ull;
+                        const bool take = maybe && key >= sTheta[ul];
+                        const unsigned m = __ballot_sync(FULL, take);
+                        if (m) {
+                            const int leader = __ffs(m) - 1;
+                            uint32_t pos = 0;
+                            if (lane == leader) pos = atomicAdd(&p.ws.cand_count[u], (uint32_t)__popc(m));
+                            pos = __shfl_sync(FULL, pos, leader) + __popc(m & ((1u << lane) - 1u));
+                            if (take && pos < p.cap) p.ws.cand[(size_t)u * p.cap + pos] = key;
                         }
                     }
                 }
             }
-            // every chunk of this stage is in registers (and consumed): hand it to the loaders
             tc::fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (lane == 0) mbar_arrive(&tempty[st]);
         }
     }
     __syncwarp();
     tc::fence_before();
     __syncthreads();
+    tc::cluster_sync_all();
     if (warp == 2) tc::tmem_dealloc(tmem_base, kAccStages * 128);
 }
 
 // ------------------------------------------------------------------------------------------
-// 4. theta: the K-th largest key of each user's sampled ads
+// A6a theta: the r-th largest key of each user's sampled ads
 // ------------------------------------------------------------------------------------------
-// Two histogram passes over ord(score) (11 + 11 bits; per-warp-group private histograms, 8-wide
-// vector loads in flight) narrow the K-th largest down to a 22-bit score prefix T; the sampled keys
-// with ord >= T (K plus the few in T's bucket) are compacted into shared memory and the exact K-th
-// largest key is selected there.  Only if that bucket is huge (massive score ties) does the kernel
-// fall back to the radix select over the whole sample in global memory.
+// Two histogram passes over ord(score) (11 + 11 bits; private per-warp-group histograms) narrow
+// the r-th largest down to a 22-bit prefix; the sampled keys at or above it are compacted into
+// shared memory (or, past its capacity, selected from global memory) and the exact r-th is taken.
 constexpr int kThetaThreads = 1024;
-constexpr int kThetaCopies = 8;    // private histograms (warps w and w+8, w+16, ... share one)
+constexpr int kThetaCopies = 8;
 
-__device__ __forceinline__ uint32_t samp_ord(float s) { return ord_of(s); }
-
-// Warp 0: the digit t with count(> t) < need <= count(>= t) in hist[0..2048); writes
-// sScalar[0] = t, sScalar[1] = count(> t).
 __device__ __forceinline__ void theta_find_digit(const uint32_t* hist, uint32_t need, uint32_t* sScalar) {
     const int lane = threadIdx.x & 31;
     constexpr int per = 2048 / 32;
@@ -678,41 +841,41 @@ __device__ __forceinline__ void theta_find_digit(const uint32_t* hist, uint32_t 
     if (lane == 0) { sScalar[0] = m ? (uint32_t)t : 0u; sScalar[1] = m ? ab : 0u; }
 }
 
-__global__ void __launch_bounds__(kThetaThreads, 1) theta_kernel(BatchWs ws, int n_samp, int K, uint32_t ad_begin,
-                                                                int nu, int scap) {
+// rerun = 1: only the users flagged by final_kernel, their lists reset: short users at rank K
+// of the sample; overflowed users at rank K of ALL their scores (dense), an exact threshold
+__global__ void __launch_bounds__(kThetaThreads, 1) theta_kernel(Ws ws, int n_samp, int rank, uint32_t ad_begin,
+                                                                int P, int scap, int rerun, int64_t n_pad) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint32_t sScalar[8];
     const int u = blockIdx.x;
-    if (u >= nu) return;
+    if (u >= P) return;
+    const uint32_t fl = __ldcg(&ws.uflags[u]);
+    if (rerun && !(fl & (kFlagShort | kFlagOverflow))) return;   // (kFlagRaise users: theta already set)
+    const bool dense = rerun && (fl & kFlagOverflow);
     const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5;
-    const int P = pow2ceil_i(K);
-    uint64_t* sbuf = reinterpret_cast<uint64_t*>(smem);                 // [P]
-    uint32_t* hist = reinterpret_cast<uint32_t*>(sbuf + P);             // [kThetaCopies][2048]
+    const int Pk = pow2ceil_i(rank);
+    uint64_t* sbuf = reinterpret_cast<uint64_t*>(smem);                 // [Pk]
+    uint32_t* hist = reinterpret_cast<uint32_t*>(sbuf + Pk);            // [kThetaCopies][2048]
     uint64_t* scand = reinterpret_cast<uint64_t*>(hist + kThetaCopies * 2048);   // [scap]
     uint32_t* myh = hist + (warp % kThetaCopies) * 2048;
-    const float* sp = ws.samp + (size_t)u * n_samp;
+    if (dense) n_samp = (int)n_pad;
+    const float* sp = dense ? ws.dense + (size_t)(fl >> 8) * n_pad : ws.samp + (size_t)u * n_samp;
     const float4* sp4 = reinterpret_cast<const float4*>(sp);
-    const int n4 = n_samp / 4;                                          // n_samp is a multiple of 128
-    auto ad_of = [](int64_t i) { return (i / kTileM) * kSampleStride * kTileM + (i % kTileM); };
-    uint32_t prefix = 0, need = (uint32_t)K;
+    const int n4 = n_samp / 4;
+    const int64_t stride = dense ? 1 : kSampleStride;
+    auto ad_of = [stride](int64_t i) { return (i / kTileM) * stride * kTileM + (i % kTileM); };
+    uint32_t prefix = 0, need = (uint32_t)rank;
     for (int pass = 0; pass < 2; ++pass) {
         const int shift = pass == 0 ? 21 : 10;
         for (int i = tid; i < kThetaCopies * 2048; i += nt) hist[i] = 0;
         __syncthreads();
-        for (int i = tid; i < n4; i += 2 * nt) {
-            float4 v[2];
-            v[0] = __ldcg(&sp4[i]);
-            v[1] = (i + nt < n4) ? __ldcg(&sp4[i + nt]) : make_float4(0.f, 0.f, 0.f, 0.f);
-            const int nv = (i + nt < n4) ? 2 : 1;
+        for (int i = tid; i < n4; i += nt) {
+            const float4 v = __ldcg(&sp4[i]);
+            const float f[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                if (q >= nv) break;
-                const float f[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    const uint32_t o = samp_ord(f[r]);
-                    if (pass == 0 || (o >> 21) == (prefix >> 21)) atomicAdd(&myh[(o >> shift) & 2047u], 1u);
-                }
+            for (int r = 0; r < 4; ++r) {
+                const uint32_t o = ord_of(f[r]);
+                if (pass == 0 || (o >> 21) == (prefix >> 21)) atomicAdd(&myh[(o >> shift) & 2047u], 1u);
             }
         }
         __syncthreads();
@@ -727,18 +890,15 @@ __global__ void __launch_bounds__(kThetaThreads, 1) theta_kernel(BatchWs ws, int
         __syncthreads();
         prefix |= sScalar[0] << shift;
         need -= sScalar[1];
-        // one pass is enough when every key in the digit's bin and above fits the compaction
-        // buffer: then compact {ord >> 21 >= digit} directly (the second histogram pass is skipped)
         const bool done = pass == 0 && (uint64_t)sScalar[1] + hist[sScalar[0]] <= (uint64_t)scap;
         __syncthreads();
         if (done) break;
     }
-    // keys with ord >= prefix: at least K of them; compact into shared memory
     if (tid == 0) sScalar[2] = 0;
     __syncthreads();
     for (int i = tid; i < n_samp; i += nt) {
         const float s = __ldcg(&sp[i]);
-        if (samp_ord(s) >= prefix) {
+        if (ord_of(s) >= prefix) {
             const uint32_t pos = atomicAdd(&sScalar[2], 1u);
             if ((int)pos < scap) scand[pos] = kappa_of(s, ad_begin + (uint32_t)ad_of(i));
         }
@@ -748,45 +908,74 @@ __global__ void __launch_bounds__(kThetaThreads, 1) theta_kernel(BatchWs ws, int
     __syncthreads();
     int nsel;
     if (cnt <= scap) {
-        nsel = cta_select_topk([scand](int64_t i) { return scand[i]; }, cnt, K, sbuf, nullptr, 0, hist, sScalar);
+        nsel = cta_select_topk([scand](int64_t i) { return scand[i]; }, cnt, rank, sbuf, nullptr, 0, hist, sScalar);
     } else {
         auto get = [sp, ad_begin, ad_of](int64_t i) { return kappa_of(__ldcg(&sp[i]), ad_begin + (uint32_t)ad_of(i)); };
-        nsel = cta_select_topk(get, n_samp, K, sbuf, nullptr, 0, hist, sScalar);
+        // (the dense row's padding ads beyond n_ads hold -inf: they never reach rank K <= n_ads)
+        nsel = cta_select_topk(get, n_samp, rank, sbuf, nullptr, 0, hist, sScalar);
     }
     if (tid == 0) {
-        ws.theta[u] = (nsel >= K) ? sbuf[K - 1] : 0ull;
+        ws.theta[u] = (nsel >= rank) ? sbuf[rank - 1] : 0ull;
         ws.cand_count[u] = 0;
     }
 }
 
 // ------------------------------------------------------------------------------------------
-// 6. final: exact top-K of the candidates
+// A6c final: exact top-K of the candidates
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(512, 1) final_kernel(BatchWs ws, int64_t cap, int K, int nu, int32_t* out_ids,
-                                                       float* out_scores, uint64_t* out_keys, int64_t scap) {
+__global__ void __launch_bounds__(512, 1) final_kernel(Ws ws, int64_t cap, int K, int P, int32_t* out_ids,
+                                                       float* out_scores, uint64_t* out_keys, int64_t scap,
+                                                       int rerun, int rank, uint32_t* err) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint32_t sScalar[8];
     const int u = blockIdx.x;
-    if (u >= nu) return;
+    if (u >= P) return;
+    if (rerun) {
+        const uint32_t f = __ldcg(&ws.uflags[u]);
+        if (!(f & kFlagAny)) return;
+    }
     const int64_t n = __ldcg(&ws.cand_count[u]);
-    if (n > cap) {   // overflow: recomputed by the latency path
-        if (threadIdx.x == 0) { ws.overflow[u] = 1; atomicAdd(&ws.header[1], 1u); }
-        return;
-    }
-    // fewer than K ads reached theta (possible only when theta was taken at a rank below K of the
-    // sample): the top-K is not guaranteed inside the candidates -- the host reruns the group with
-    // rank K (inventories reaching this path hold >= 64 K ads, so n >= K otherwise)
-    if (n < K) {
-        if (threadIdx.x == 0) atomicAdd(&ws.header[2], 1u);
-        return;
-    }
-    const int P = pow2ceil_i(K);
+    const int Pk = pow2ceil_i(K);
     uint64_t* sbuf = reinterpret_cast<uint64_t*>(smem);
-    uint32_t* shist = reinterpret_cast<uint32_t*>(sbuf + P);
+    uint32_t* shist = reinterpret_cast<uint32_t*>(sbuf + Pk);
     uint64_t* scand = reinterpret_cast<uint64_t*>(shist + kSelBins);
     const uint64_t* cb = ws.cand + (size_t)u * cap;
-    const int nsel = cta_select_topk([cb](int64_t i) { return __ldcg(&cb[i]); }, n, K, sbuf, scand, scap,
-                                     shist, sScalar);
+    if (n > cap) {
+        // candidate overflow (more than `cap` ads at or above theta: massive score ties, or an
+        // inventory whose sampled tiles misrepresent the rest).  The first kMaxFallback such users
+        // of a pass get their scores recomputed densely and an exact rank-K threshold; the others
+        // a raised threshold, the K-th largest of the stored subset (a valid lower bound of the
+        // K-th largest overall, since the subset's keys are all candidates).  Both are refiltered.
+        __shared__ uint32_t sSlot;
+        if (threadIdx.x == 0) sSlot = rerun ? (uint32_t)kMaxFallback + 1u : atomicAdd(&ws.header[4], 1u);
+        __syncthreads();
+        const uint32_t slot = sSlot;
+        if (slot < (uint32_t)kMaxFallback) {
+            if (threadIdx.x == 0) ws.uflags[u] = kFlagOverflow | (slot << 8);
+        } else if (!rerun) {
+            const int nsel = cta_select_topk([cb](int64_t i) { return __ldcg(&cb[i]); }, cap, K, sbuf, scand, scap,
+                                             shist, sScalar);
+            if (threadIdx.x == 0) {
+                ws.theta[u] = sbuf[min(nsel, K) - 1];
+                ws.cand_count[u] = 0u;
+                ws.uflags[u] = kFlagRaise;
+                ws.header[2] = 1u;
+            }
+        } else if (threadIdx.x == 0) {
+            ws.uflags[u] = 0u;
+            atomicOr(err, 2u);             // still overflowing after the rerun: flagged, output incomplete
+        }
+        return;
+    }
+    // fewer than K keys reached theta (theta at a sample rank below K): the top-K is not
+    // guaranteed inside the candidates -- the gated rerun takes theta at rank K
+    if (n < K && !rerun && rank < K) {
+        if (threadIdx.x == 0) { ws.uflags[u] = kFlagShort; ws.header[2] = 1u; }
+        return;
+    }
+    if (threadIdx.x == 0) ws.uflags[u] = 0u;
+    const int nsel = cta_select_topk([cb](int64_t i) { return __ldcg(&cb[i]); }, n, K, sbuf, scand, scap, shist,
+                                     sScalar);
     cta_write_topk(sbuf, nsel, K, out_ids ? out_ids + (size_t)u * K : nullptr,
                    out_scores ? out_scores + (size_t)u * K : nullptr, out_keys ? out_keys + (size_t)u * K : nullptr);
 }
@@ -796,18 +985,19 @@ __global__ void __launch_bounds__(512, 1) final_kernel(BatchWs ws, int64_t cap, 
 // ------------------------------------------------------------------------------------------
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
+    static std::once_flag once;
+    std::call_once(once, [] {
         void* ptr = nullptr;
         cudaDriverEntryPointQueryResult qres;
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &qres) == cudaSuccess &&
             qres == cudaDriverEntryPointSuccess)
             fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
-    }
+    });
     return fn;
 }
 
-static bool encode_2d_bf16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, uint32_t box_inner,
-                           uint32_t box_rows) {
+static bool encode_2d_16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, uint32_t box_inner,
+                         uint32_t box_rows) {
     auto fn = get_encode();
     if (!fn) return false;
     const cuuint64_t dims[2] = {inner, rows};
@@ -819,67 +1009,36 @@ static bool encode_2d_bf16(CUtensorMap* m, const void* base, uint64_t inner, uin
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-struct Layout {
-    size_t header, items, chunk_off, U, W, samp, theta, count, cand, overflow, user_item, user_shift, span, span_lo, total;
-    int64_t cap, n_samp, cap_items, nj;
+struct Tuning {
+    int n_hb, pieces;
 };
 
-static Layout layout(const ebr_index* idx, int32_t slots, int32_t k) {
-    Layout L;
-    auto al = [](size_t x) { return (x + 1023) & ~(size_t)1023; };
-    const int64_t n_tiles = idx->n_pad / kTileM;
-    L.n_samp = ((n_tiles + kSampleStride - 1) / kSampleStride) * kTileM;
-    L.cap = std::max<int64_t>((int64_t)kSampleStride * k * 8, 1 << 16);
-    L.cap_items = (int64_t)kGroup * idx->n_fields * slots;
-    size_t o = 0;
-    L.header = o;    o = al(o + 64);
-    L.items = o;     o = al(o + (size_t)L.cap_items * sizeof(BItem));
-    L.chunk_off = o; o = al(o + (size_t)(L.cap_items + 1) * 8);
-    L.U = o;         o = al(o + (size_t)kGroup * (idx->d_pad + kHotPieces * idx->n_hot) * 2);
-    L.W = o;         o = al(o + (size_t)kGroup * idx->n_pad * 4);
-    L.samp = o;      o = al(o + (size_t)kGroup * L.n_samp * 4);
-    L.theta = o;     o = al(o + (size_t)kGroup * 8);
-    L.count = o;     o = al(o + (size_t)kGroup * 4);
-    L.cand = o;      o = al(o + (size_t)kGroup * L.cap * 8);
-    L.overflow = o;  o = al(o + (size_t)kGroup * 4);
-    L.nj = (idx->n_pad + kWideR - 1) / kWideR;
-    L.user_item = o; o = al(o + (size_t)(kGroup + 1) * 4);
-    L.user_shift = o; o = al(o + (size_t)kGroup * 4);
-    L.span = o;      o = al(o + (size_t)L.cap_items * (L.nj + 1) * 4);
-    L.span_lo = o;   o = al(o + (size_t)L.cap_items * L.nj * 4);
-    L.total = o;
-    return L;
+static Tuning tuning(const ebr_index* idx) {
+    Tuning t;
+    t.n_hb = std::min(1, idx->n_hot / 64);                  // 64 hot keys: 80 % of C3's hits
+    t.pieces = 2;
+    if (const char* e = getenv("EBR_HOT_BLOCKS")) t.n_hb = std::max(0, std::min(t.n_hb, atoi(e)));
+    if (getenv("EBR_NO_HOT")) t.n_hb = 0;                 // every key through the compressed lists
+    if (const char* e = getenv("EBR_HOT_PIECES")) t.pieces = std::max(1, std::min(2, atoi(e)));
+    return t;
 }
 
-static BatchWs carve(char* base, const Layout& L) {
-    BatchWs w;
-    w.header = reinterpret_cast<uint32_t*>(base + L.header);
-    w.items = reinterpret_cast<BItem*>(base + L.items);
-    w.chunk_off = reinterpret_cast<uint64_t*>(base + L.chunk_off);
-    w.U = reinterpret_cast<__nv_bfloat16*>(base + L.U);
-    w.W = reinterpret_cast<float*>(base + L.W);
-    w.samp = reinterpret_cast<float*>(base + L.samp);
-    w.theta = reinterpret_cast<uint64_t*>(base + L.theta);
-    w.cand_count = reinterpret_cast<uint32_t*>(base + L.count);
-    w.cand = reinterpret_cast<uint64_t*>(base + L.cand);
-    w.overflow = reinterpret_cast<uint32_t*>(base + L.overflow);
-    w.user_item = reinterpret_cast<uint32_t*>(base + L.user_item);
-    w.user_shift = reinterpret_cast<int32_t*>(base + L.user_shift);
-    w.span = reinterpret_cast<uint32_t*>(base + L.span);
-    w.span_lo = reinterpret_cast<uint32_t*>(base + L.span_lo);
-    return w;
+static size_t gemm_smem(int u_blocks, int stages) {
+    return 1024 + (size_t)(u_blocks + stages) * kBlockBytes + (size_t)kTileM * kAccPitch * 4 +
+           (size_t)(2 * stages + 3 * kAccStages + 1) * 8 + 16 + (size_t)kGroup * 20;
 }
 
 }  // namespace batch
 
 using namespace batch;
 
-bool batch_eligible(const ebr_index* idx, int32_t batch, int32_t k) {
+bool batch_eligible(const ebr_index* idx, int32_t batch, int32_t slots, int32_t k) {
     if (getenv("EBR_NO_BATCH_PATH")) return false;
     // small batches take the tensor-core path too on large inventories, where the latency path's
     // per-user wide scratch no longer fits L2 (C5 sweep: B=4 at 20 M ads 3.9 ms latency path)
     const bool big = idx->n_ads >= ((int64_t)1 << 21);
     return idx->dtype == EBR_BF16 && (batch >= 16 || (big && batch >= 4)) && idx->d_pad <= 256 &&
+           idx->n_fields <= 255 && pass_users(idx, slots) >= 32 &&
            idx->n_ads >= (int64_t)4 * kSampleStride * std::max(k, kTileM) && get_encode() != nullptr;
 }
 
@@ -887,146 +1046,165 @@ size_t batch_workspace_bytes(const ebr_index* idx, int32_t slots, int32_t k) {
     return layout(idx, slots, k).total + 1024;
 }
 
+int32_t batch_launches(const ebr_index* idx, int32_t batch, int32_t slots) {
+    const int P = pass_users(idx, slots);
+    return ((batch + P - 1) / P) * 15;
+}
+
 // The workspace passed here is the batched region (after the latency path's region).
 ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
     const ebr_index* idx = q.idx;
     const Layout L = layout(idx, q.slots, q.k);
     char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(region) + 1023) & ~(uintptr_t)1023);
-    BatchWs ws = carve(base, L);
+    Ws ws = carve(base, L);
+    Tuning tu = tuning(idx);
     const int n_kb = idx->d_pad / kBlockK;
-    const int n_tiles = (int)(idx->n_pad / kTileM);
+    const int n_tiles = (int)L.n_tiles;
     const int n_samp_tiles = (int)(L.n_samp / kTileM);
-    cudaError_t e = cudaMemsetAsync(ws.overflow, 0, (size_t)kGroup * 4, q.stream);
-    if (e != cudaSuccess) return cuda_check(e, "memset(overflow)");
-    e = cudaFuncSetAttribute(wide_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kWideR * 4);
-    if (e != cudaSuccess) return cuda_check(e, "attr(wide)");
-    CUtensorMap tmA, tmH;
-    if (!encode_2d_bf16(&tmA, idx->A, (uint64_t)idx->d_pad, (uint64_t)idx->n_pad, kBlockK, kTileM))
-        return set_error(EBR_ECUDA, "cuTensorMapEncodeTiled(A) failed");
-    if (idx->n_hot > 0) {
-        if (!encode_2d_bf16(&tmH, idx->H, (uint64_t)idx->n_hot, (uint64_t)idx->n_pad, kBlockK, kTileM))
-            return set_error(EBR_ECUDA, "cuTensorMapEncodeTiled(H) failed");
-    } else {
-        tmH = tmA;   // unused
-    }
+    const int u_cols = (int)L.u_cols;
     int max_smem = 0;
-    e = cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, idx->device);
+    cudaError_t e = cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, idx->device);
     if (e != cudaSuccess) return cuda_check(e, "attr(max smem)");
-    e = cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kGroup * kMaxHot * 4);
-    if (e != cudaSuccess) return cuda_check(e, "attr(plan)");
-    std::vector<int> overflow_users;
-    // test hook: a smaller candidate capacity exercises the overflow -> latency-path fallback
+    // ring stages: >= one tile's K blocks (the hot block's writer waits on the ring, see
+    // score_kernel) plus one of lookahead; hot blocks are dropped until that fits
+    int stages = 0;
+    for (; tu.n_hb >= 0; --tu.n_hb) {
+        const int ub = n_kb + tu.n_hb * tu.pieces, nkt = n_kb + tu.n_hb;
+        stages = 6;
+        while (stages > nkt + 1 && gemm_smem(ub, stages) > (size_t)max_smem) --stages;
+        if (gemm_smem(ub, stages) <= (size_t)max_smem) break;
+    }
+    if (tu.n_hb < 0) return set_error(EBR_EUNSUPPORTED, "batched path: d=%d does not fit shared memory", idx->d);
+    const int u_blocks = n_kb + tu.n_hb * tu.pieces;
+    const size_t smem = gemm_smem(u_blocks, stages);
+    CUtensorMap tmA, tmU;
+    if (!encode_2d_16(&tmA, idx->A, (uint64_t)idx->d_pad, (uint64_t)idx->n_pad, kBlockK, kTileM))
+        return set_error(EBR_ECUDA, "cuTensorMapEncodeTiled(A) failed");
+    const int Ppad_max = (int)((L.P + kGroup - 1) / kGroup * kGroup);
+    if (!encode_2d_16(&tmU, ws.U, (uint64_t)u_cols, (uint64_t)Ppad_max, kBlockK, kGroup))
+        return set_error(EBR_ECUDA, "cuTensorMapEncodeTiled(U) failed");
+    // kernel attributes: set once per process (values fixed by the build)
+    static std::once_flag attr_once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(attr_once, [&] {
+        auto set = [&](const void* f, int bytes) {
+            cudaError_t x = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+            if (x != cudaSuccess && attr_err == cudaSuccess) attr_err = x;
+        };
+        const int big = 227 * 1024;
+        set((const void*)score_kernel<0>, big);
+        set((const void*)score_kernel<1>, big);
+        set((const void*)theta_kernel, 200 * 1024);
+        set((const void*)final_kernel, 200 * 1024);
+        set((const void*)entry_count_kernel, kRangeMaxTiles * kTileM * 4);
+        set((const void*)entry_write_kernel, kRangeMaxTiles * kTileM * 4);
+        for (const void* f : {(const void*)score_kernel<0>, (const void*)score_kernel<1>}) {
+            cudaError_t x = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            (void)x;
+        }
+    });
+    if (attr_err != cudaSuccess) return cuda_check(attr_err, "attr(batched kernels)");
+
+    const size_t tsmem = 200 * 1024;
+    const size_t fsmem = 200 * 1024;
+    const int64_t fscap = (int64_t)(fsmem - (size_t)pow2ceil_i(q.k) * 8 - kSelBins * 4) / 8;
+    const double ks = (double)q.k / kSampleStride;
+    int rank = (int)std::ceil(ks + 5.0 * std::sqrt(ks) + 8.0);
+    if (const char* r = getenv("EBR_THETA_RANK")) rank = atoi(r);   // test hook
+    rank = std::max(1, std::min(rank, q.k));
+    auto tscap_of = [&](int r) { return (int)((tsmem - (size_t)pow2ceil_i(r) * 8 - kThetaCopies * 2048 * 4) / 8); };
     int64_t cap = L.cap;
     if (const char* c = getenv("EBR_TEST_CAND_CAP")) cap = std::min<int64_t>(cap, std::max(1, atoi(c)));
-    for (int g0 = 0; g0 < q.batch; g0 += kGroup) {
-        const int nu = std::min(kGroup, q.batch - g0);
-        const int nu_pad = (nu + 31) & ~31;
-        // hot K blocks: as many as fit next to the resident user tile with >= 4 ring stages
-        const size_t fixed = 1024 + 512 + (size_t)kGroup * 12;
-        const int wstages = 2;
-        auto smem_of = [&](int hb, int st) {
-            return fixed + (((size_t)nu_pad * 128 * (n_kb + kHotPieces * hb) + 1023) & ~(size_t)1023) +
-                   (size_t)(st + wstages) * kBlockBytes;
-        };
-        // hot K blocks pay per ad (2 B x 64 keys of H) and save per (ad, user) hit; block b (in
-        // decreasing coverage) pays off from ~2, 14, 30, 60 users: cap by group size
-        int n_hb = idx->n_hot / 64;
-        n_hb = std::min(n_hb, nu < 14 ? 1 : nu < 30 ? 2 : nu < 60 ? 3 : 4);
-        if (getenv("EBR_NO_HOT")) n_hb = 0;
-        while (n_hb > 0 && smem_of(n_hb, 4) > (size_t)max_smem) --n_hb;
-        int stages = 4;
-        while (stages < 8 && smem_of(n_hb, stages + 1) <= (size_t)max_smem) ++stages;
-        const int u_blocks = n_kb + kHotPieces * n_hb;
-        const int u_cols = u_blocks * kBlockK;
-        CUtensorMap tmU;
-        if (!encode_2d_bf16(&tmU, ws.U, (uint64_t)u_cols, (uint64_t)nu_pad, kBlockK, (uint32_t)nu_pad))
-            return set_error(EBR_ECUDA, "cuTensorMapEncodeTiled(U) failed");
-        plan_kernel<<<1, 1024, (size_t)nu_pad * n_hb * 64 * 4, q.stream>>>(
-            idx->key_chunk_off, idx->key_word_off, idx->cross_w, idx->field_card, idx->field_base, idx->n_fields,
-            q.slots, q.user_feat + (size_t)g0 * idx->n_fields * q.slots, q.user_x + (size_t)g0 * idx->n_fields * q.slots,
-            reinterpret_cast<const uint16_t*>(q.user_emb) + (size_t)g0 * idx->d, idx->d, idx->d_pad, nu, nu_pad,
-            idx->hot_slot, n_hb * 64, u_cols, ws, err_word);
-        const int max_items = nu * idx->n_fields * q.slots;
-        span_kernel<<<(max_items + 7) / 8, 256, 0, q.stream>>>(idx->chunk_hdr, idx->chunk_last, ws, (int)L.nj,
-                                                               (int)L.cap_items);
-        wide_smem_kernel<<<dim3((unsigned)L.nj, (unsigned)nu), kWideThreads, kWideR * 4, q.stream>>>(
-            idx->chunk_hdr, idx->payload, ws, (int)L.nj, idx->n_pad, (int)L.cap_items);
+
+    EntryArgs ea;
+    ea.hdr = idx->chunk_hdr; ea.chunk_last = idx->chunk_last; ea.payload = idx->payload;
+    ea.n_ads = idx->n_ads; ea.n_pad = idx->n_pad; ea.range_ads = L.range_ads;
+    ea.n_ranges = (int)L.n_ranges; ea.n_tiles = n_tiles; ea.NU = L.NU;
+    const size_t rsmem = (size_t)L.range_ads * 4;
+
+    for (int b0 = 0; b0 < q.batch; b0 += (int)L.P) {
+        const int P = std::min((int)L.P, q.batch - b0);
+        const int G = (P + kGroup - 1) / kGroup;
+        PlanArgs pa;
+        pa.user_feat = q.user_feat + (size_t)b0 * idx->n_fields * q.slots;
+        pa.user_x = q.user_x + (size_t)b0 * idx->n_fields * q.slots;
+        pa.user_emb = reinterpret_cast<const uint16_t*>(q.user_emb) + (size_t)b0 * idx->d;
+        pa.key_chunk_off = idx->key_chunk_off; pa.key_word_off = idx->key_word_off; pa.cross_w = idx->cross_w;
+        pa.field_card = idx->field_card; pa.field_base = idx->field_base; pa.hot_slot = idx->hot_slot;
+        pa.F = idx->n_fields; pa.S = q.slots; pa.P = P; pa.d = idx->d; pa.d_pad = idx->d_pad;
+        pa.n_hot_used = tu.n_hb * 64; pa.pieces = tu.pieces; pa.u_cols = u_cols; pa.TS = L.TS; pa.err = err_word;
+        const int nslot = P * idx->n_fields * q.slots;
+        const int pgrid = std::max(1, std::min(4 * idx->sm_count, (nslot + 255) / 256));
+        plan_a_kernel<<<pgrid, 256, 0, q.stream>>>(pa, ws);
+        plan_b_kernel<<<1, kPlanThreads, 0, q.stream>>>(pa, ws);
+        plan_c_kernel<<<std::max(pgrid, 2 * idx->sm_count), 256, 0, q.stream>>>(pa, ws);
+        span_kernel<<<(unsigned)((nslot + 7) / 8), 256, 0, q.stream>>>(ea, ws);
+        entry_count_kernel<<<(unsigned)L.n_ranges, 512, rsmem, q.stream>>>(ea, ws);
+        range_scan_kernel<<<1, 1024, 0, q.stream>>>(ea, ws);
+        entry_write_kernel<<<(unsigned)L.n_ranges, 512, rsmem, q.stream>>>(ea, ws);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_check(e, "launch(plan/entries)");
+
         GemmParams gp;
-        gp.n_ads = idx->n_ads; gp.n_pad = idx->n_pad; gp.ad_begin = (uint32_t)idx->ad_begin;
-        gp.d_pad = idx->d_pad; gp.n_kb = n_kb; gp.n_hb = n_hb; gp.u_blocks = u_blocks;
-        gp.nu = nu; gp.nu_pad = nu_pad;
-        gp.n_samp = (int)L.n_samp; gp.stages = stages; gp.wstages = wstages; gp.cap = cap; gp.ws = ws;
-        const size_t smem = smem_of(n_hb, stages);
-        // sample pass
-        gp.n_tiles = n_samp_tiles; gp.tile_stride = kSampleStride;
-        e = cudaFuncSetAttribute(gemm_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return cuda_check(e, "attr(gemm0)");
-        gemm_kernel<0><<<std::min(idx->sm_count, n_samp_tiles), kGemmThreads, smem, q.stream>>>(tmA, tmH, tmU, gp);
-        // theta at sample rank r, the filter pass over every tile, the final select.  The sample
-        // is every 16th tile, so ~K/16 sampled keys lie above the K-th largest overall: taking
-        // theta at r = K/16 + 5 sqrt(K/16) + 8 (< K) instead of K cuts the candidates ~10x; a
-        // user left with fewer than K candidates (counted by final_kernel) makes the group rerun
-        // with r = K, which guarantees >= K candidates (exact either way)
-        const size_t tsmem = 200 * 1024;
-        const int tscap = (int)((tsmem - (size_t)pow2ceil_i(q.k) * 8 - kThetaCopies * 2048 * 4) / 8);
-        e = cudaFuncSetAttribute(theta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
-        if (e != cudaSuccess) return cuda_check(e, "attr(theta)");
-        e = cudaFuncSetAttribute(gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return cuda_check(e, "attr(gemm1)");
-        const size_t fsmem = 200 * 1024;
-        const int64_t scap = (int64_t)(fsmem - (size_t)pow2ceil_i(q.k) * 8 - kSelBins * 4) / 8;
-        e = cudaFuncSetAttribute(final_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
-        if (e != cudaSuccess) return cuda_check(e, "attr(final)");
-        const double ks = (double)q.k / kSampleStride;
-        int rank = (int)std::ceil(ks + 5.0 * std::sqrt(ks) + 8.0);
-        if (getenv("EBR_THETA_RANK")) rank = atoi(getenv("EBR_THETA_RANK"));   // test hook
-        rank = std::max(1, std::min(rank, q.k));
-        auto select_pass = [&](int r) {
-            theta_kernel<<<nu, kThetaThreads, tsmem, q.stream>>>(ws, (int)L.n_samp, r, (uint32_t)idx->ad_begin, nu,
-                                                                 tscap);
-            gp.n_tiles = n_tiles; gp.tile_stride = 1;
-            gemm_kernel<1><<<std::min(idx->sm_count, n_tiles), kGemmThreads, smem, q.stream>>>(tmA, tmH, tmU, gp);
-            final_kernel<<<nu, 512, fsmem, q.stream>>>(ws, cap, q.k, nu,
-                                                       q.out_ids ? q.out_ids + (size_t)g0 * q.k : nullptr,
-                                                       q.out_scores ? q.out_scores + (size_t)g0 * q.k : nullptr,
-                                                       q.out_keys ? q.out_keys + (size_t)g0 * q.k : nullptr, scap);
+        gp.n_ads = idx->n_ads; gp.n_pad = idx->n_pad; gp.dense = 0; gp.ad_begin = (uint32_t)idx->ad_begin;
+        gp.n_kb = n_kb; gp.n_hb = tu.n_hb; gp.pieces = tu.pieces; gp.u_blocks = u_blocks;
+        gp.P = P; gp.n_samp = (int)L.n_samp; gp.stages = stages; gp.cap = cap; gp.rerun = 0;
+        gp.hot_mask = reinterpret_cast<const uint4*>(idx->hot_mask); gp.ws = ws; gp.err = err_word;
+        // the U tensor map covers the whole pass tile: each CTA loads its group's 128 rows
+        auto launch_score = [&](int mode, int tiles, int stride, int rerun, int dense = 0) -> cudaError_t {
+            gp.n_tiles = tiles; gp.tile_stride = stride; gp.rerun = rerun; gp.dense = dense;
+            cudaLaunchConfig_t cfg = {};
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = (unsigned)G;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.blockDim = dim3(kGemmThreads);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = q.stream;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            int ncl = idx->sm_count / G;
+            {
+                static std::mutex mu;
+                static int cached[2][kMaxCluster + 1] = {};
+                std::lock_guard<std::mutex> lk(mu);
+                int& c = cached[mode][G];
+                if (!c) {
+                    cfg.gridDim = dim3((unsigned)(G * ncl));
+                    int n = 0;
+                    cudaError_t x = cudaOccupancyMaxActiveClusters(
+                        &n, mode ? (const void*)score_kernel<1> : (const void*)score_kernel<0>, &cfg);
+                    c = (x == cudaSuccess && n > 0) ? n : ncl;
+                }
+                ncl = std::min(ncl, c);
+            }
+            ncl = std::max(1, std::min(ncl, tiles));
+            cfg.gridDim = dim3((unsigned)(G * ncl));
+            return mode ? cudaLaunchKernelEx(&cfg, score_kernel<1>, tmA, tmU, gp)
+                        : cudaLaunchKernelEx(&cfg, score_kernel<0>, tmA, tmU, gp);
         };
-        select_pass(rank);
+        int32_t* oi = q.out_ids ? q.out_ids + (size_t)b0 * q.k : nullptr;
+        float* os = q.out_scores ? q.out_scores + (size_t)b0 * q.k : nullptr;
+        uint64_t* ok = q.out_keys ? q.out_keys + (size_t)b0 * q.k : nullptr;
+        e = launch_score(0, n_samp_tiles, kSampleStride, 0);
+        if (e != cudaSuccess) return cuda_check(e, "launch(score sample)");
+        theta_kernel<<<P, kThetaThreads, tsmem, q.stream>>>(ws, (int)L.n_samp, rank, (uint32_t)idx->ad_begin, P,
+                                                           tscap_of(rank), 0, idx->n_pad);
+        e = launch_score(1, n_tiles, 1, 0);
+        if (e != cudaSuccess) return cuda_check(e, "launch(score filter)");
+        final_kernel<<<P, 512, fsmem, q.stream>>>(ws, cap, q.k, P, oi, os, ok, fscap, 0, rank, err_word);
+        // gated reruns (exact either way): the overflowed users' scores densely, then theta at rank
+        // K for the users short of K candidates (sample) or overflowed (dense), filter, select
+        e = launch_score(0, n_tiles, 1, 0, 1);
+        if (e != cudaSuccess) return cuda_check(e, "launch(score dense)");
+        theta_kernel<<<P, kThetaThreads, tsmem, q.stream>>>(ws, (int)L.n_samp, q.k, (uint32_t)idx->ad_begin, P,
+                                                           tscap_of(q.k), 1, idx->n_pad);
+        e = launch_score(1, n_tiles, 1, 1);
+        if (e != cudaSuccess) return cuda_check(e, "launch(score rerun)");
+        final_kernel<<<P, 512, fsmem, q.stream>>>(ws, cap, q.k, P, oi, os, ok, fscap, 1, q.k, err_word);
         e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_check(e, "launch(batch)");
-        uint32_t hdr[3] = {0, 0, 0};
-        e = cudaMemcpyAsync(hdr, ws.header, 12, cudaMemcpyDeviceToHost, q.stream);
-        if (e != cudaSuccess) return cuda_check(e, "memcpy(header)");
-        e = cudaStreamSynchronize(q.stream);
-        if (e != cudaSuccess) return cuda_check(e, "sync(batch)");
-        if (hdr[2] && rank < q.k) {
-            // shortfall: the whole group again with theta at rank K (W and the sample are reused)
-            e = cudaMemsetAsync(ws.overflow, 0, (size_t)kGroup * 4, q.stream);
-            if (e == cudaSuccess) e = cudaMemsetAsync(ws.header + 1, 0, 8, q.stream);
-            if (e != cudaSuccess) return cuda_check(e, "memset(rerun)");
-            select_pass(q.k);
-            e = cudaGetLastError();
-            if (e != cudaSuccess) return cuda_check(e, "launch(batch rerun)");
-            e = cudaMemcpyAsync(hdr, ws.header, 12, cudaMemcpyDeviceToHost, q.stream);
-            if (e != cudaSuccess) return cuda_check(e, "memcpy(header)");
-            e = cudaStreamSynchronize(q.stream);
-            if (e != cudaSuccess) return cuda_check(e, "sync(batch)");
-        }
-        // overflowed users of this group: the exact latency path for them
-        if (hdr[1]) {
-            std::vector<uint32_t> of(nu);
-            e = cudaMemcpy(of.data(), ws.overflow, (size_t)nu * 4, cudaMemcpyDeviceToHost);
-            if (e != cudaSuccess) return cuda_check(e, "memcpy(overflow)");
-            for (int u = 0; u < nu; ++u)
-                if (of[u]) overflow_users.push_back(g0 + u);
-            e = cudaMemsetAsync(ws.overflow, 0, (size_t)kGroup * 4, q.stream);
-            if (e != cudaSuccess) return cuda_check(e, "memset(overflow)");
-        }
-    }
-    for (int u : overflow_users) {
-        ebr_status st = run_small(q, u, 1);
-        if (st != EBR_OK) return st;
     }
     return EBR_OK;
 }

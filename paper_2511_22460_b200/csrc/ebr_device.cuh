@@ -475,7 +475,10 @@ __device__ __forceinline__ void cta_write_topk(const uint64_t* sbuf, int nsel, i
                                                int32_t* out_ids, float* out_scores,
                                                uint64_t* out_keys) {
     for (int q = threadIdx.x; q < K; q += blockDim.x) {
-        const uint64_t x = (q < nsel) ? sbuf[q] : 0ull;   // 0 = padding (never a real kappa)
+        // keys below 2^32 are padding (0, or a merge sentinel): never a real kappa, whose
+        // ord(s) >= 1 for every finite score
+        uint64_t x = (q < nsel) ? sbuf[q] : 0ull;
+        if (x < (1ull << 32)) x = 0ull;
         if (out_keys) out_keys[q] = x;
         if (out_ids) out_ids[q] = x ? (int32_t)gid_of(x) : -1;
         if (out_scores) out_scores[q] = x ? score_of(x) : __int_as_float(0xFF800000);

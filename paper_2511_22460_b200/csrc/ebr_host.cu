@@ -48,7 +48,8 @@ ebr_status cuda_check(cudaError_t e, const char* what) {
 
 ebr_status run_small(const QueryArgs& q, int b0, int B);
 uint32_t workspace_magic(const ebr_index* idx);
-bool batch_eligible(const ebr_index* idx, int32_t batch, int32_t k);
+bool batch_eligible(const ebr_index* idx, int32_t batch, int32_t slots, int32_t k);
+int32_t batch_launches(const ebr_index* idx, int32_t batch, int32_t slots);
 size_t batch_workspace_bytes(const ebr_index* idx, int32_t slots, int32_t k);
 ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word);
 size_t small_workspace_bytes(const ebr_index* idx, int32_t slots, int32_t k);
@@ -214,22 +215,24 @@ static int32_t padded_width(int32_t d, int esz) {
 
 // ------------------------------------------------------------------------------------------
 // Hot keys (bf16 indexes): the kMaxHot keys with the longest posting lists -- and at least
-// max(64, n/512) postings, below which a dense column costs more than the compressed list --
-// also get a dense column of L, H[a][h] in bf16 (1.0 / 0.0), that the batched path contracts on
-// the tensor cores.  The posting lists stay complete (the latency path and the
-// batched path's cold keys read them).  EBR_HOT_KEYS=<n> caps the count (0 disables).
+// max(64, n/512) postings -- also get a column of L stored as one bit of a 128-bit mask per ad
+// (16 B/ad); the batched path expands a tile's masks into an fp16 one-hot block on chip and
+// contracts it on the tensor cores.  The posting lists stay complete (the
+// latency path and the batched path's cold keys read them).  EBR_HOT_KEYS=<n> caps the count.
 // ------------------------------------------------------------------------------------------
-__global__ void hot_fill_kernel(const int32_t* __restrict__ feat, int64_t n, int F,
+__global__ void hot_mask_kernel(const int32_t* __restrict__ feat, int64_t n, int F,
                                 const int32_t* __restrict__ field_base, const int32_t* __restrict__ hot_slot,
-                                uint16_t* __restrict__ H, int n_hot) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n * F) return;
-    const int64_t a = i / F;
-    const int f = (int)(i - a * F);
-    const int32_t v = feat[i];
-    if (v < 0) return;
-    const int32_t h = hot_slot[field_base[f] + v];
-    if (h >= 0) H[a * n_hot + h] = 0x3F80;   // bf16 1.0
+                                uint4* __restrict__ mask) {
+    const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= n) return;
+    uint32_t m[4] = {0u, 0u, 0u, 0u};
+    for (int f = 0; f < F; ++f) {
+        const int32_t v = feat[a * F + f];
+        if (v < 0) continue;
+        const int32_t h = hot_slot[field_base[f] + v];
+        if (h >= 0) m[h >> 5] |= 1u << (h & 31);
+    }
+    mask[a] = make_uint4(m[0], m[1], m[2], m[3]);
 }
 
 static ebr_status build_hot(ebr_index* idx, const Encoded& enc, const int32_t* ad_feat, cudaStream_t stream) {
@@ -257,9 +260,9 @@ static ebr_status build_hot(ebr_index* idx, const Encoded& enc, const int32_t* a
     EBR_CUDA(cudaMemcpyAsync(idx->hot_slot, slot.data(), (size_t)M * 4, cudaMemcpyHostToDevice, stream));
     EBR_CUDA(cudaMalloc(&idx->hot_key, (size_t)n_hot * 4));
     EBR_CUDA(cudaMemcpyAsync(idx->hot_key, key.data(), (size_t)n_hot * 4, cudaMemcpyHostToDevice, stream));
-    const size_t hbytes = (size_t)idx->n_pad * n_hot * 2;
-    EBR_CUDA(cudaMalloc(&idx->H, hbytes));
-    EBR_CUDA(cudaMemsetAsync(idx->H, 0, hbytes, stream));
+    const size_t mbytes = (size_t)idx->n_pad * 16;
+    EBR_CUDA(cudaMalloc(&idx->hot_mask, mbytes));
+    EBR_CUDA(cudaMemsetAsync(idx->hot_mask, 0, mbytes, stream));
     const int F = idx->n_fields;
     const int64_t chunk = std::max<int64_t>(1, (int64_t)(256 << 20) / (4 * std::max(F, 1)));   // 256 MB of values
     int32_t* dfeat = nullptr;
@@ -268,13 +271,12 @@ static ebr_status build_hot(ebr_index* idx, const Encoded& enc, const int32_t* a
         const int64_t m = std::min(chunk, n - a0);
         cudaError_t e = cudaMemcpyAsync(dfeat, ad_feat + a0 * F, (size_t)m * F * 4, cudaMemcpyHostToDevice, stream);
         if (e == cudaSuccess) {
-            const int64_t tot = m * F;
-            hot_fill_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, stream>>>(
-                dfeat, m, F, idx->field_base, idx->hot_slot, static_cast<uint16_t*>(idx->H) + a0 * n_hot, n_hot);
+            hot_mask_kernel<<<(unsigned)((m + 255) / 256), 256, 0, stream>>>(
+                dfeat, m, F, idx->field_base, idx->hot_slot, static_cast<uint4*>(idx->hot_mask) + a0);
             e = cudaGetLastError();
         }
         if (e == cudaSuccess) e = cudaStreamSynchronize(stream);   // dfeat is reused
-        if (e != cudaSuccess) { cudaFree(dfeat); return cuda_check(e, "hot columns"); }
+        if (e != cudaSuccess) { cudaFree(dfeat); return cuda_check(e, "hot masks"); }
     }
     cudaFree(dfeat);
     return EBR_OK;
@@ -294,12 +296,15 @@ __global__ void __launch_bounds__(kThreads) merge_kernel(const uint64_t* __restr
     uint64_t* scand = reinterpret_cast<uint64_t*>(shist + kSelBins);
     const int b = blockIdx.x;
     const int64_t n = (int64_t)G * K;
+    // The radix select needs unique keys: a shard's padding entries (key 0) become the distinct
+    // sentinels i + 1 < 2^32, below every real kappa (ord(s) >= 1 for finite s), so they sort last
+    // and are written out as padding when the shards together hold fewer than K ads.
     auto get = [=](int64_t i) {
         const int64_t g = i / K, q = i - g * K;
-        return __ldg(&gathered[(g * B + b) * (int64_t)K + q]);
+        const uint64_t x = __ldg(&gathered[(g * B + b) * (int64_t)K + q]);
+        return x ? x : (uint64_t)(i + 1);
     };
     const int nsel = cta_select_topk(get, n, K, sbuf, scand_cap > 0 ? scand : nullptr, scand_cap, shist, sScalar);
-    // padding keys (0) may have been selected when fewer than K real keys exist: they sort last
     cta_write_topk(sbuf, nsel, K, out_ids + (size_t)b * K, out_scores + (size_t)b * K, nullptr);
 }
 
@@ -345,12 +350,12 @@ static size_t small_region(const ebr_index* idx, int32_t slots, int32_t k) {
 
 size_t workspace_bytes(const ebr_index* idx, int32_t batch, int32_t slots, int32_t k) {
     size_t n = small_region(idx, slots, k);
-    if (batch_eligible(idx, batch, k)) n += batch_workspace_bytes(idx, slots, k);
+    if (batch_eligible(idx, batch, slots, k)) n += batch_workspace_bytes(idx, slots, k);
     return n;
 }
 
 ebr_status run_query(const QueryArgs& q) {
-    if (batch_eligible(q.idx, q.batch, q.k)) {
+    if (batch_eligible(q.idx, q.batch, q.slots, q.k)) {
         char* ws = static_cast<char*>(q.workspace);
         return run_batch(q, ws + small_region(q.idx, q.slots, q.k), reinterpret_cast<uint32_t*>(ws) + 1);
     }
@@ -375,7 +380,7 @@ const char* ebr_last_error(void) { return g_last_error.c_str(); }
 
 int32_t ebr_query_launches(const ebr_index* idx, int32_t batch, int32_t slots, int32_t k) {
     if (!idx || batch < 1 || slots < 1 || k < 1) return 0;
-    if (batch_eligible(idx, batch, k)) return 1 + ((batch + 127) / 128) * 7;   // memset + 7 kernels per group
+    if (batch_eligible(idx, batch, slots, k)) return batch_launches(idx, batch, slots);
     return (batch + kSmallMaxB - 1) / kSmallMaxB;
 }
 
@@ -423,7 +428,7 @@ void ebr_free_index(ebr_index* idx) {
     cudaGetDevice(&prev);
     cudaSetDevice(idx->device);
     void* ptrs[] = {idx->A, idx->key_chunk_off, idx->key_word_off, idx->chunk_hdr, idx->chunk_last, idx->payload,
-                    idx->cross_w, idx->field_card, idx->field_base, idx->hot_slot, idx->hot_key, idx->H};
+                    idx->cross_w, idx->field_card, idx->field_base, idx->hot_slot, idx->hot_key, idx->hot_mask};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     free(idx->tmap_A);
@@ -731,12 +736,13 @@ ebr_status ebr_index_stats(const ebr_index* idx, ebr_stats* o) {
     o->nnz = idx->nnz;
     o->chunks = idx->n_chunks;
     o->payload_words = idx->n_words;
-    o->index_bytes = (idx->n_keys * 2 + 1) * 4 + idx->n_chunks * 12 + (idx->n_words + 2) * 4 + idx->n_keys * 4;
+    o->index_bytes = (idx->n_keys * 2 + 1) * 4 + idx->n_chunks * 12 + (idx->n_words + 2) * 4 + idx->n_keys * 4 +
+                     (idx->hot_mask ? (int64_t)idx->n_pad * 16 + idx->n_keys * 4 : 0);
     o->emb_bytes = idx->n_pad * idx->d_pad * esz;
     o->build_ms = idx->build_ms;
     o->n_hot = idx->n_hot;
     o->hot_nnz = idx->hot_nnz;
-    o->hot_bytes = (int64_t)idx->n_pad * idx->n_hot * 2;
+    o->hot_bytes = idx->hot_mask ? (int64_t)idx->n_pad * 16 : 0;
     return EBR_OK;
 }
 

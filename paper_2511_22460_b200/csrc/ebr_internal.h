@@ -27,13 +27,14 @@ struct ebr_index {
     float* cross_w;                 // [M]
     int32_t* field_card;            // [F]
     int32_t* field_base;            // [F]
-    // Dense columns of L for the hottest keys (bf16 indexes only; DESIGN.md §6.2 "hot keys"):
-    // H[a][h] = 1.0 iff ad a has hot key hot_key[h]; the batched path feeds H to the tensor cores
-    // and skips those keys' posting lists.  Slots are ordered by posting count, descending.
+    // The hottest keys' columns of L (bf16 indexes only; DESIGN.md §6.2 "hot keys"): bit h of
+    // hot_mask[a] is set iff ad a has hot key hot_key[h].  The batched path expands the bits of a
+    // tile into an fp16 one-hot block on chip and contracts it on the tensor cores; those keys'
+    // posting lists are then skipped.  Slots are ordered by posting count, descending.
     int32_t n_hot;                  // multiple of 64, <= kMaxHot (0: none)
     int32_t* hot_slot;              // [M] slot of key i, or -1
     int32_t* hot_key;               // [n_hot] key of each slot (-1 for unused padding slots)
-    void* H;                        // [n_pad][n_hot] bf16 one-hot
+    void* hot_mask;                 // [n_pad] uint4: 128 bits per ad
     int64_t hot_nnz;                // postings covered by the hot columns
     double build_ms;
     int sm_count;
@@ -47,7 +48,7 @@ constexpr int kHistBits = 11;               // first-level radix histogram of or
 constexpr int kHistBins = 1 << kHistBits;
 constexpr int kSmallMaxB = 4;               // users per launch of the latency-path kernel
 constexpr int kThreads = 512;               // CTA size of the small-batch / select kernels
-constexpr int kMaxHot = 256;                // dense hot-key columns per index (bf16 indexes)
+constexpr int kMaxHot = 128;                // hot-key columns per index (bf16 indexes; one 128-bit mask per ad)
 
 struct QueryArgs {
     const ebr_index* idx;

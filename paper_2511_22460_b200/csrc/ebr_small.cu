@@ -109,8 +109,10 @@ ebr_status run_small(const QueryArgs& q, int b0, int B) {
     static std::vector<AttrKey> attr_set;
     int occ = 0;
     cudaError_t e = cudaSuccess;
+    // held until the launch is enqueued: another thread re-setting the kernel's attribute between
+    // this call's set and its launch would make the cooperative launch fail
+    std::unique_lock<std::mutex> lk(occ_mu);
     {
-        std::lock_guard<std::mutex> lk(occ_mu);
         AttrKey* cur = nullptr;
         for (AttrKey& a : attr_set)
             if (a.k == k && a.dev == idx->device) cur = &a;

@@ -530,7 +530,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
                 const int b = i / (p.n_fields * p.slots);
                 const int f = (i / p.slots) % p.n_fields;
                 const int32_t v = p.user_feat[i];
-                if (v >= p.field_card[f]) {
+                if (v < -1 || v >= p.field_card[f]) {   // outside [-1, V_f): flag it, skip the slot
                     if (blockIdx.x == 0) atomicOr(&p.header[1], 1u);   // bounds error: skip the slot
                     continue;
                 }
@@ -553,7 +553,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
             for (int i = s0; i < s1; ++i) {
                 const int f = (i / p.slots) % p.n_fields;
                 const int32_t v = p.user_feat[i];
-                if (v >= p.field_card[f]) {
+                if (v < -1 || v >= p.field_card[f]) {   // outside [-1, V_f): flag it, skip the slot
                     if (blockIdx.x == 0) atomicOr(&p.header[1], 1u);
                     continue;
                 }

@@ -179,6 +179,19 @@ def test_bad_user_value_raises_flag(ebr):
     assert ebr.query_error(ws) == 0          # cleared
 
 
+@pytest.mark.parametrize("b", [1, 40])
+def test_negative_user_value_raises_flag(ebr, b):
+    """A user value below -1 is outside [-1, V_f): skipped (as if empty) and flagged (ebr.h), on
+    the latency path (b=1) and the batched path (b=40, bf16)."""
+    cfg = "C1" if b == 1 else "C3"
+    inv, users = synth.make_config(cfg, mode="exact", n_ads=80_000, batch=b)
+    users.user_feat[0, 0, 0] = -5
+    (ids, sc), ws = run(ebr, ebr.Index.of(inv), users, 50)
+    assert ebr.query_error(ws) == 1
+    users.user_feat[0, 0, 0] = -1
+    assert check_all(oracle.Oracle.of(inv), users, ids, sc, 50, "exact") == 0
+
+
 def test_workspace_reuse_across_indexes(ebr):
     """One workspace serves successive indexes of the same geometry (state left clean)."""
     inv, users = synth.make_config("C1", mode="exact", n_ads=5_000, batch=3)
@@ -287,6 +300,27 @@ def test_shard_smaller_than_k_pads(ebr):
     ebr.merge_topk(gathered, 2, 2, k, ids, sc)
     torch.cuda.synchronize()
     assert check_all(oracle.Oracle.of(inv), users, ids.cpu().numpy(), sc.cpu().numpy(), k, "exact") == 0
+
+
+@pytest.mark.parametrize("G,n,k", [(2, 300, 400), (8, 8 * 600, 4096)])
+def test_merge_total_below_k_pads(ebr, G, n, k):
+    """All shards together hold fewer than K ads: the padding keys (0) must not displace real
+    keys in the merge (the radix select needs unique keys; padding becomes distinct
+    sentinels below every real kappa)."""
+    inv, users = synth.make_config("C1", mode="exact", n_ads=n, batch=2)
+    bounds = np.linspace(0, n, G + 1).astype(int)
+    parts = []
+    for lo, hi in zip(bounds[:-1], bounds[1:]):
+        keys, _ = run(ebr, ebr.Index.of(inv, lo=int(lo), hi=int(hi)), users, k, keys=True)
+        parts.append(keys)
+    gathered = torch.from_numpy(np.stack(parts).view(np.int64)).cuda()
+    ids = torch.empty((2, k), dtype=torch.int32, device="cuda")
+    sc = torch.empty((2, k), dtype=torch.float32, device="cuda")
+    ebr.merge_topk(gathered, G, 2, k, ids, sc)
+    torch.cuda.synchronize()
+    ids, sc = ids.cpu().numpy(), sc.cpu().numpy()
+    assert (ids[:, n:] == -1).all() and np.isneginf(sc[:, n:]).all()
+    assert check_all(oracle.Oracle.of(inv), users, ids, sc, k, "exact") == 0
 
 
 @pytest.mark.parametrize("dtype,b", [("f32", 1), ("bf16", 3)])
