@@ -24,7 +24,7 @@
 // Launches per pass (all on the caller's stream, no host synchronisation -- graph-capturable):
 //   plan_a / plan_b / plan_c   A1: slots -> keys, w~ = fl32(w x), hot pieces, cold key
 //                              union (hash) with user pairs, fixed-point scales, user tiles
-//   span / entry_count / range_scan / entry_write    A2: the entry stream
+//   entry_bin / entry_sort     A2: the entry stream (decode once, bucket by ad range, sort by ad)
 //   score<0>  on every 16th tile: scores of the sample (A3-A5)
 //   theta     A6a: theta_u = the r-th largest sampled key (r < K)
 //   score<1>  on every tile: keys >= theta_u appended to per-user candidate lists (A3-A6b)
@@ -45,27 +45,37 @@ namespace ebr {
 
 namespace batch {
 
-constexpr int kGroup = 128;          // users per CTA (UMMA N)
-constexpr int kMaxCluster = 4;       // CTAs (user groups) per cluster
+constexpr int kGroup = 128;          // users per CTA (UMMA M: TMEM lanes)
+constexpr int kMaxCluster = 2;       // CTAs (user groups) per cluster: <= 256 users per pass
 constexpr int kTileM = 128;          // ads per tile (UMMA M)
 constexpr int kBlockK = 64;          // 16-bit elements per 128-byte swizzle row
 constexpr int kBlockBytes = kTileM * 128;   // one ring stage: 128 rows x 128 B
 constexpr int kSampleStride = 16;    // every 16th tile is sampled for theta
-constexpr int kAccStages = 4;        // TMEM: 4 x 128 columns
 constexpr int kAccPitch = kGroup + 4;   // int32 words per fixed-point row (16-B row reads conflict-free)
-constexpr int kWideWarp0 = 4, kWideWarps = 8, kWideThreads = 32 * kWideWarps;
+#ifndef EBR_WIDE_WARPS
+#define EBR_WIDE_WARPS 16
+#endif
+constexpr int kWideWarp0 = 4, kWideWarps = EBR_WIDE_WARPS, kWideThreads = 32 * kWideWarps;
 constexpr int kEpiWarp0 = kWideWarp0 + kWideWarps, kEpiWarps = 8;
-constexpr int kGemmThreads = 32 * (kEpiWarp0 + kEpiWarps);   // 640: TMA, MMA, TMEM alloc, spare, 8 wide, 8 epilogue
+constexpr int kGemmThreads = 32 * (kEpiWarp0 + kEpiWarps);   // TMA, MMA, 2 hot, wide, 8 epilogue
 constexpr int kMaxHotBlocks = 2;     // hot K blocks of 64 keys (the index keeps up to 128 hot keys)
-constexpr int kPairWBits = 23;       // cold pair = pass user (9 bits) << 23 | w~ 2^S (23-bit two's complement)
-constexpr int kPairWMax = 22;        // |w~ 2^S| < 2^22
-constexpr int kEntryPsBits = 15;     // entry = row << 24 | (pair count - 1) << 15 | first pair
-constexpr int kMaxPassPairs = 1 << kEntryPsBits;
-constexpr int kRangeMaxTiles = 256;  // entry-stream range: <= 32768 ads (per-ad u32 counters in smem)
+constexpr int kPairUBits = 7;        // cold pair = w~ 2^S (25-bit two's complement) << 7 | user in the group
+constexpr int kPairWMax = 24;        // |w~ 2^S| < 2^24
+constexpr int kMaxUnion = 1 << 15;   // union key slots per pass (15 bits in the level-1 bin entries)
+constexpr int kBinMaxEntries = 32768; // entry bin: worst case (bin ads x F) sorted in 128 KB of smem
 constexpr int kPlanThreads = 1024;
 constexpr uint32_t kFlagShort = 1u, kFlagOverflow = 2u, kFlagRaise = 4u;   // uflags; overflow users carry their dense slot << 8
 constexpr uint32_t kFlagAny = kFlagShort | kFlagOverflow | kFlagRaise;
 constexpr int kMaxFallback = 2;      // overflowed users per pass recomputed exactly (dense scores)
+
+constexpr int kMaxAccStages = 3;
+// shared memory of the fused kernel: the ad/hot ring, the fixed-point cold tile [users][ads],
+// barriers, per-user scalars and the byte -> one-hot table, then the group's slot -> pair offsets
+// and its pairs
+__host__ __device__ constexpr size_t score_smem_fixed(int stages) {
+    return (size_t)stages * kBlockBytes + (size_t)kGroup * kAccPitch * 4 +
+           (size_t)(2 * stages + 3 * kMaxAccStages + 1) * 8 + 16 + (size_t)kGroup * 20 + 256 * 16;
+}
 
 // ------------------------------------------------------------------------------------------
 // workspace
@@ -73,9 +83,9 @@ constexpr int kMaxFallback = 2;      // overflowed users per pass recomputed exa
 struct Ws {
     uint32_t* header;     // [0] n_union [1] n_pairs [2] any user short of K [3] entries total [4] overflowed users
     uint32_t* hkey;       // [TS] key + 1 (0 = empty)
-    uint32_t* hcnt;       // [TS] user pairs of the key (left zero by plan_c)
+    uint32_t* hcnt;       // [TS][kMaxCluster] user pairs of the key per group (left zero by plan_c)
     uint32_t* hslot;      // [TS] union slot of the key
-    uint32_t* hpair;      // [TS] first pair of the key
+    uint32_t* hpair;      // [TS][kMaxCluster] first pair of the key in its group's list
     int32_t* item_t;      // [P*F*S] hash position of a cold slot, -1 otherwise
     float* item_w;        // [P*F*S] w~ of the slot
     float* hotw;          // [P_pad][128] sum of w~ per (user, hot key) (left zero by plan_c)
@@ -87,27 +97,28 @@ struct Ws {
     uint32_t* uc0;        // [NU] first chunk of the key
     uint32_t* uc1;        // [NU] end chunk
     uint32_t* ukwb;       // [NU] payload word base
-    uint32_t* uentry;     // [NU] (count - 1) << 15 | first pair
-    uint32_t* pairs;      // [NU]
+    uint16_t* toff;       // [kMaxCluster][NU + 1] first pair of union slot s in group g's list (u16)
+    uint32_t* pairs;      // [kMaxCluster][kGroup * F * S] each group's pairs, by union slot
     uint16_t* U;          // [P_pad][u_cols] deep bf16 | hot fp16 pieces
-    uint32_t* span;       // [NU][n_ranges + 1] first chunk of the key with last id >= j R
-    uint32_t* adcnt;      // [n_pad / 4] per-ad entry counts (u8)
-    uint32_t* rtotal;     // [n_ranges]
-    uint32_t* rbase;      // [n_ranges + 1]
-    uint32_t* tile_off;   // [n_tiles + 1]
-    uint32_t* entries;    // [n_pad * F]
+    uint32_t* uchunk;     // [NU + 1] exclusive scan of the union keys' chunk counts
+    uint32_t* bin_cnt;    // [n_bins] entries in each ad-range bin (left zero by entry_sort)
+    uint32_t* tile_beg;   // [kMaxCluster][n_tiles] first entry of each tile in group g's stream
+    uint32_t* tile_end;   // [kMaxCluster][n_tiles]
+    uint32_t* gentries;   // [pool] the groups' entry streams (bins claim their ranges)
+    uint32_t* entries;    // [n_bins][bin_cap] level-1 bins (bin_cap = bin_ads * F: an ad has <= F keys)
     float* samp;          // [P][n_samp]
     uint64_t* theta;      // [P]
     uint32_t* cand_count; // [P]
     uint64_t* cand;       // [P][cap]
     uint32_t* uflags;     // [P] kFlagShort | kFlagOverflow
     float* dense;         // [kMaxFallback][n_pad] every score of an overflowed user
+    unsigned long long* prof;   // [32] cycle accounting of the fused kernel's roles (EBR_DIAG & 4)
 };
 
 struct Layout {
     size_t total;
     size_t off[32];
-    int64_t TS, NU, P, n_samp, cap, n_ranges, range_ads, n_tiles, u_cols;
+    int64_t TS, NU, P, n_samp, cap, n_bins, bin_ads, bin_cap, n_tiles, u_cols, gcap, pool;
 };
 
 static int64_t pow2ceil64(int64_t x) {
@@ -116,10 +127,15 @@ static int64_t pow2ceil64(int64_t x) {
     return p;
 }
 
-// users per pass: <= kGroup * kMaxCluster, and the pass's pairs must fit the entry encoding
+// users per pass: <= kGroup * kMaxCluster, the union slots must fit 15 bits and a group's pairs
+// the u16 offsets
 int pass_users(const ebr_index* idx, int32_t slots) {
     const int64_t fs = (int64_t)idx->n_fields * slots;
-    int64_t p = std::min<int64_t>(kGroup * kMaxCluster, kMaxPassPairs / std::max<int64_t>(fs, 1));
+    int64_t p = std::min<int64_t>(kGroup * kMaxCluster, kMaxUnion / std::max<int64_t>(fs, 1));
+    if ((int64_t)kGroup * fs > 65535) p = 0;
+    // shared memory of the fused kernel: slot offsets (2 B x P F S) + a group's pairs (4 B x 128 F S)
+    // next to the fixed part and >= 4 ring stages
+    while (p > 32 && 1024 + score_smem_fixed(4) + 2 * (p * fs + 2) + 4 * (int64_t)kGroup * fs > 232448) p -= 32;
     return (int)(p / 32 * 32);
 }
 
@@ -132,38 +148,44 @@ static Layout layout(const ebr_index* idx, int32_t slots, int32_t k) {
     const int P = pass_users(idx, slots);
     L.P = P;
     L.NU = (int64_t)P * idx->n_fields * slots;
+    L.gcap = (int64_t)kGroup * idx->n_fields * slots;
     L.TS = pow2ceil64(2 * L.NU);
     L.n_tiles = idx->n_pad / kTileM;
     L.n_samp = ((L.n_tiles + kSampleStride - 1) / kSampleStride) * kTileM;
     L.cap = cand_cap(k);
-    const int64_t tpr = std::min<int64_t>(kRangeMaxTiles, std::max<int64_t>(1, (L.n_tiles + 2 * idx->sm_count - 1) /
-                                                                                 (2 * idx->sm_count)));
-    L.range_ads = tpr * kTileM;
-    L.n_ranges = (L.n_tiles + tpr - 1) / tpr;
+    // entry bins: as many ads as keep a bin's worst case (bin_ads * F entries) in 128 KB of smem
+    L.bin_ads = std::max<int64_t>(kTileM, std::min<int64_t>(4096, (kBinMaxEntries / std::max(1, idx->n_fields)) / kTileM * kTileM));
+    L.bin_cap = L.bin_ads * idx->n_fields;
+    L.n_bins = (idx->n_pad + L.bin_ads - 1) / L.bin_ads;
+    // group streams: an (ad, key) entry appears once per group querying the key, so at most
+    // min(groups, ...) x F entries per ad; sized for the pass's largest group count
+    L.pool = (int64_t)std::min<int64_t>(kMaxCluster, (P + kGroup - 1) / kGroup) * idx->n_pad * idx->n_fields;
     L.u_cols = idx->d_pad + (int64_t)kMaxHotBlocks * 64 * 2;
     const int64_t Ppad = (int64_t)((P + kGroup - 1) / kGroup) * kGroup;
     const size_t sizes[] = {
         64,                                         // 0 header
-        (size_t)L.TS * 4, (size_t)L.TS * 4, (size_t)L.TS * 4, (size_t)L.TS * 4,   // 1-4 hash
+        (size_t)L.TS * 4, (size_t)L.TS * 4 * kMaxCluster, (size_t)L.TS * 4, (size_t)L.TS * 4 * kMaxCluster,   // 1-4 hash
         (size_t)L.NU * 4, (size_t)L.NU * 4,         // 5-6 items
         (size_t)Ppad * 128 * 4,                     // 7 hotw
         (size_t)P * 4, (size_t)P * 4, (size_t)P * 4, (size_t)P * 4,   // 8-11 per user
-        (size_t)L.NU * 4, (size_t)L.NU * 4, (size_t)L.NU * 4, (size_t)L.NU * 4, (size_t)L.NU * 4,   // 12-16 union
-        (size_t)L.NU * 4,                           // 17 pairs
+        (size_t)L.NU * 4, (size_t)L.NU * 4, (size_t)L.NU * 4, (size_t)L.NU * 4,   // 12-15 union
+        (size_t)kMaxCluster * (L.NU + 1) * 2,       // 16 toff
+        (size_t)kMaxCluster * L.gcap * 4,           // 17 pairs
         (size_t)Ppad * L.u_cols * 2,                // 18 U
-        (size_t)L.NU * (L.n_ranges + 1) * 4,        // 19 span
-        (size_t)idx->n_pad,                         // 20 adcnt
-        (size_t)L.n_ranges * 4, (size_t)(L.n_ranges + 1) * 4,   // 21-22
-        (size_t)(L.n_tiles + 1) * 4,                // 23 tile_off
-        (size_t)idx->n_pad * idx->n_fields * 4,     // 24 entries
+        (size_t)(L.NU + 1) * 4,                     // 19 uchunk
+        (size_t)L.n_bins * 4,                       // 20 bin_cnt
+        (size_t)L.n_tiles * 4 * kMaxCluster, (size_t)L.n_tiles * 4 * kMaxCluster,   // 21-22 tile_beg / tile_end
+        (size_t)L.pool * 4,                         // 23 gentries
+        (size_t)L.n_bins * L.bin_cap * 4,           // 24 entries
         (size_t)P * L.n_samp * 4,                   // 25 samp
         (size_t)P * 8, (size_t)P * 4,               // 26-27 theta, count
         (size_t)P * L.cap * 8,                      // 28 cand
         (size_t)P * 4,                              // 29 flags
         (size_t)kMaxFallback * idx->n_pad * 4,      // 30 dense
+        32 * 8,                                     // 31 prof
     };
     size_t o = 0;
-    for (int i = 0; i < 31; ++i) {
+    for (int i = 0; i < 32; ++i) {
         L.off[i] = o;
         o = (o + sizes[i] + 1023) & ~(size_t)1023;
     }
@@ -180,18 +202,19 @@ static Ws carve(char* b, const Layout& L) {
     w.hotw = (float*)at(7);
     w.bound = (float*)at(8); w.emax = (uint32_t*)at(9); w.ushift = (int32_t*)at(10); w.uscale = (float*)at(11);
     w.ukey = (uint32_t*)at(12); w.uc0 = (uint32_t*)at(13); w.uc1 = (uint32_t*)at(14); w.ukwb = (uint32_t*)at(15);
-    w.uentry = (uint32_t*)at(16); w.pairs = (uint32_t*)at(17);
+    w.toff = (uint16_t*)at(16); w.pairs = (uint32_t*)at(17);
     w.U = (uint16_t*)at(18);
-    w.span = (uint32_t*)at(19);
-    w.adcnt = (uint32_t*)at(20);
-    w.rtotal = (uint32_t*)at(21); w.rbase = (uint32_t*)at(22);
-    w.tile_off = (uint32_t*)at(23);
+    w.uchunk = (uint32_t*)at(19);
+    w.bin_cnt = (uint32_t*)at(20);
+    w.tile_beg = (uint32_t*)at(21); w.tile_end = (uint32_t*)at(22);
+    w.gentries = (uint32_t*)at(23);
     w.entries = (uint32_t*)at(24);
     w.samp = (float*)at(25);
     w.theta = (uint64_t*)at(26); w.cand_count = (uint32_t*)at(27);
     w.cand = (uint64_t*)at(28);
     w.uflags = (uint32_t*)at(29);
     w.dense = (float*)at(30);
+    w.prof = (unsigned long long*)at(31);
     return w;
 }
 
@@ -209,7 +232,7 @@ struct PlanArgs {
     const int32_t* field_base;
     const int32_t* hot_slot;
     int F, S, P, d, d_pad, n_hot_used, pieces, u_cols;
-    int64_t TS;
+    int64_t TS, NU, gcap;
     uint32_t* err;
 };
 
@@ -247,46 +270,96 @@ __global__ void __launch_bounds__(256) plan_a_kernel(PlanArgs a, Ws ws) {
             if (prev == 0u || prev == key + 1u) break;
             t = (t + 1u) & mask;
         }
-        atomicAdd(&ws.hcnt[t], 1u);
+        atomicAdd(&ws.hcnt[(size_t)t * kMaxCluster + u / kGroup], 1u);
         ws.item_t[i] = (int32_t)t;
         ws.item_w[i] = w;
     }
 }
 
-// plan_b (one CTA): compacts the hash table into union slots (scan), assigns each key its pair
-// range, resets the table for the next pass, and derives every user's fixed-point scale
-//   S_u = min(22 - e_max, 30 - e_sum),  max|w~| < 2^e_max,  sum|w~| < 2^e_sum
-// so each w~ 2^S fits the 23-bit pair field and every partial sum fits int32 (R23).
+// plan_b (one CTA): compacts the hash table into union slots, gives each (slot, group) its range
+// in the group's pair list, resets the table for the next pass, and derives every user's
+// fixed-point scale
+//   S_u = min(24 - e_max, 30 - e_sum),  max|w~| < 2^e_max,  sum|w~| < 2^e_sum
+// so each w~ 2^S fits the 25-bit pair field and every partial sum fits int32 (R23).
+// Each thread scans a run of table positions; one block scan combines the runs (6 sums at once).
+constexpr int kPlanNV = 2 + kMaxCluster;   // slots, chunks, per-group pairs
 __global__ void __launch_bounds__(kPlanThreads) plan_b_kernel(PlanArgs a, Ws ws) {
-    __shared__ uint32_t sScan[40];
-    __shared__ uint32_t sBase[2];
-    const int tid = threadIdx.x;
-    if (tid == 0) { sBase[0] = 0; sBase[1] = 0; }
-    __syncthreads();
-    for (int64_t t0 = 0; t0 < a.TS; t0 += kPlanThreads) {
-        const int64_t t = t0 + tid;
-        uint32_t key1 = 0, cnt = 0;
-        if (t < a.TS) { key1 = ws.hkey[t]; cnt = key1 ? ws.hcnt[t] : 0u; }
-        uint32_t tot_s, tot_p;
-        const uint32_t ps = block_exclusive_scan(key1 ? 1u : 0u, sScan, &tot_s);
-        const uint32_t pp = block_exclusive_scan(cnt, sScan, &tot_p);
-        if (key1) {
-            const uint32_t s = sBase[0] + ps, p0 = sBase[1] + pp;
-            const uint32_t key = key1 - 1u;
-            ws.hslot[t] = s;
-            ws.hpair[t] = p0;
-            ws.ukey[s] = key;
-            ws.uc0[s] = a.key_chunk_off[key];
-            ws.uc1[s] = a.key_chunk_off[key + 1];
-            ws.ukwb[s] = a.key_word_off[key];
-            ws.uentry[s] = ((cnt - 1u) << kEntryPsBits) | p0;
-            ws.hkey[t] = 0u;
-        }
-        __syncthreads();
-        if (tid == 0) { sBase[0] += tot_s; sBase[1] += tot_p; }
-        __syncthreads();
+    __shared__ uint32_t sW[kPlanThreads / 32][kPlanNV];
+    __shared__ uint32_t sTot[kPlanNV];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t per = (a.TS + kPlanThreads - 1) / kPlanThreads;
+    const int64_t t0 = (int64_t)tid * per, t1 = min(a.TS, t0 + per);
+    uint32_t v[kPlanNV] = {};
+    for (int64_t t = t0; t < t1; ++t) {
+        const uint32_t key1 = ws.hkey[t];
+        if (!key1) continue;
+        v[0] += 1u;
+        v[1] += a.key_chunk_off[key1] - a.key_chunk_off[key1 - 1u];
+        for (int g = 0; g < kMaxCluster; ++g) v[2 + g] += ws.hcnt[t * kMaxCluster + g];
     }
-    if (tid == 0) { ws.header[0] = sBase[0]; ws.header[1] = sBase[1]; ws.header[2] = 0; ws.header[4] = 0; }
+    // block exclusive scan of v[] over threads
+    uint32_t incl[kPlanNV];
+#pragma unroll
+    for (int i = 0; i < kPlanNV; ++i) {
+        uint32_t x = v[i];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, x, o);
+            if (lane >= o) x += y;
+        }
+        incl[i] = x;
+        if (lane == 31) sW[warp][i] = x;
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int i = 0; i < kPlanNV; ++i) {
+            const uint32_t w = sW[lane][i];
+            uint32_t x = w;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(FULL, x, o);
+                if (lane >= o) x += y;
+            }
+            sW[lane][i] = x - w;
+            if (lane == 31) sTot[i] = x;
+        }
+    }
+    __syncthreads();
+    uint32_t base[kPlanNV];
+#pragma unroll
+    for (int i = 0; i < kPlanNV; ++i) base[i] = sW[warp][i] + incl[i] - v[i];
+    for (int64_t t = t0; t < t1; ++t) {
+        const uint32_t key1 = ws.hkey[t];
+        if (!key1) continue;
+        const uint32_t key = key1 - 1u, sl = base[0];
+        const uint32_t c0 = a.key_chunk_off[key], c1 = a.key_chunk_off[key + 1];
+        ws.hslot[t] = sl;
+        ws.ukey[sl] = key;
+        ws.uc0[sl] = c0;
+        ws.uc1[sl] = c1;
+        ws.ukwb[sl] = a.key_word_off[key];
+        ws.uchunk[sl] = base[1];
+        for (int g = 0; g < kMaxCluster; ++g) {
+            ws.toff[(size_t)g * (a.NU + 1) + sl] = (uint16_t)base[2 + g];
+            ws.hpair[t * kMaxCluster + g] = base[2 + g];
+            base[2 + g] += ws.hcnt[t * kMaxCluster + g];
+        }
+        base[0] += 1u;
+        base[1] += c1 - c0;
+        ws.hkey[t] = 0u;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const uint32_t nu = sTot[0];
+        ws.header[0] = nu; ws.header[1] = 0; ws.header[2] = 0; ws.header[4] = 0; ws.header[6] = 0;
+        ws.header[5] = sTot[1];                 // chunks of the union
+        ws.uchunk[nu] = sTot[1];
+        for (int g = 0; g < kMaxCluster; ++g) {
+            ws.header[8 + g] = sTot[2 + g];     // pairs of group g
+            ws.toff[(size_t)g * (a.NU + 1) + nu] = (uint16_t)sTot[2 + g];
+        }
+    }
     for (int u = tid; u < a.P; u += kPlanThreads) {
         const float b = ws.bound[u], m = __uint_as_float(ws.emax[u]);
         int S = 0;
@@ -311,11 +384,12 @@ __global__ void __launch_bounds__(256) plan_c_kernel(PlanArgs a, Ws ws) {
     for (int i = gt; i < n; i += gs) {
         const int32_t t = ws.item_t[i];
         if (t < 0) continue;
-        const int u = i / (a.F * a.S);
-        const uint32_t pos = ws.hpair[t] + atomicSub(&ws.hcnt[t], 1u) - 1u;
+        const int u = i / (a.F * a.S), g = u / kGroup;
+        const size_t hc = (size_t)t * kMaxCluster + g;
+        const uint32_t pos = ws.hpair[hc] + atomicSub(&ws.hcnt[hc], 1u) - 1u;
         const int S = ws.ushift[u];
-        const int32_t wf = (int32_t)__float2int_rn(ldexpf(ws.item_w[i], S));   // |wf| < 2^22
-        ws.pairs[pos] = ((uint32_t)u << kPairWBits) | ((uint32_t)wf & ((1u << kPairWBits) - 1u));
+        const int32_t wf = (int32_t)__float2int_rn(ldexpf(ws.item_w[i], S));   // |wf| < 2^24
+        ws.pairs[(size_t)g * a.gcap + pos] = ((uint32_t)wf << kPairUBits) | (uint32_t)(u % kGroup);
     }
     const int Ppad = (a.P + kGroup - 1) / kGroup * kGroup;
     // deep part of U (zero padded rows and columns)
@@ -338,178 +412,185 @@ __global__ void __launch_bounds__(256) plan_c_kernel(PlanArgs a, Ws ws) {
 }
 
 // ------------------------------------------------------------------------------------------
-// A2 the entry stream: the union's cold postings, decoded once per pass, as per-tile lists
+// A2 the entry stream: the union's cold postings, decoded ONCE per pass, as per-tile lists
 // ------------------------------------------------------------------------------------------
+// Level 1 (entry_bin): the union keys' chunks are decoded warp-cooperatively in key order (each
+// chunk once; Alg. 2 l.355-357 with the chunk codec), every posting appended to the bin of its
+// ad range; the lanes of a chunk that hit the same bin share one atomic (warp aggregation).
+// Level 2 (entry_sort): one CTA per bin sorts the bin by ad in shared memory (counting sort) and
+// writes it back with the per-tile bounds: entry = ad row << 24 | union slot.
 struct EntryArgs {
     const uint2* hdr;
-    const uint32_t* chunk_last;
     const uint32_t* payload;
-    int64_t n_ads, n_pad, range_ads;
-    int n_ranges, n_tiles;
-    int64_t NU;
+    int64_t n_ads, n_pad;
+    int bin_ads, n_bins, n_tiles;
+    int64_t bin_cap;
+    int G;                  // user groups of the pass
+    int NU;                 // union slot capacity (toff row length - 1)
 };
 
-// span: one warp per union key; span[s][j] = first chunk whose last id >= j R (j = 0..n_ranges)
-__global__ void __launch_bounds__(256) span_kernel(EntryArgs e, Ws ws) {
+__global__ void __launch_bounds__(256) entry_bin_kernel(EntryArgs e, Ws ws) {
     const int lane = threadIdx.x & 31;
-    const uint32_t s = blockIdx.x * 8 + (threadIdx.x >> 5);
-    const uint32_t nu = __ldcg(&ws.header[0]);
-    if (s >= nu) return;
-    const uint32_t c0 = ws.uc0[s], c1 = ws.uc1[s];
-    uint32_t* sp = ws.span + (size_t)s * (e.n_ranges + 1);
-    const uint32_t R = (uint32_t)e.range_ads;
-    int last_r = -1;
-    for (uint32_t cb = c0; cb < c1; cb += 32) {
-        const uint32_t c = cb + lane;
-        int r = -1, rp = -1;
-        if (c < c1) {
-            r = (int)(__ldg(&e.chunk_last[c]) / R);
-            rp = (c == c0) ? -1 : (int)(__ldg(&e.chunk_last[c - 1]) / R);
-            for (int j = rp + 1; j <= r; ++j) sp[j] = c;
+    const uint32_t nu = __ldcg(&ws.header[0]), total = __ldcg(&ws.header[5]);
+    const uint32_t n_items = (total + 31) / 32;
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t R = (uint32_t)e.bin_ads;
+    for (uint32_t item = gw; item < n_items; item += nw) {
+        const uint32_t g0 = item * 32;
+        // the key holding chunk g0: last s with uchunk[s] <= g0 (warp 32-ary search)
+        uint32_t lo = 0, hi = nu;                 // answer in [lo, hi)
+        while (hi - lo > 1) {
+            const uint32_t step = (hi - lo + 31) / 32;
+            const uint32_t pidx = lo + lane * step;
+            const bool le = pidx < hi && __ldcg(&ws.uchunk[pidx]) <= g0;
+            const uint32_t cntle = __popc(__ballot_sync(FULL, le));   // lanes 0..cntle-1 have uchunk <= g0
+            const uint32_t nlo = lo + (cntle - 1) * step;
+            hi = min(hi, nlo + step);
+            lo = nlo;
         }
-        const int m = __reduce_max_sync(FULL, r);
-        last_r = max(last_r, m);
-    }
-    for (int j = last_r + 1 + lane; j <= e.n_ranges; j += 32) sp[j] = c1;
-}
-
-// Calls f(local ad) for every posting of union key s inside range j, one warp.
-template <typename Fn>
-__device__ __forceinline__ void range_postings(const EntryArgs& e, const Ws& ws, uint32_t s, int j, int lane, Fn f) {
-    const uint32_t* sp = ws.span + (size_t)s * (e.n_ranges + 1);
-    const uint32_t lo = sp[j], c1 = ws.uc1[s];
-    const uint32_t hi = min(sp[j + 1] + 1u, c1);   // the chunk straddling the range end
-    const uint32_t kwb = ws.ukwb[s];
-    const uint32_t a0 = (uint32_t)((int64_t)j * e.range_ads), a1 = a0 + (uint32_t)e.range_ads;
-    for (uint32_t c = lo; c < hi; ++c) {
-        uint32_t id;
-        const bool ok = decode_chunk(e.hdr, e.payload, kwb, c, lane, id);
-        if (ok && id >= a0 && id < a1) f(id - a0);
-    }
-}
-
-// entry_count: CTA = range; counts the postings of every ad (u8 per ad) and the range total
-__global__ void __launch_bounds__(512) entry_count_kernel(EntryArgs e, Ws ws) {
-    extern __shared__ uint32_t cnt[];      // [range_ads]
-    __shared__ uint32_t sRed[16];
-    const int j = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int R = (int)e.range_ads;
-    for (int i = tid; i < R; i += 512) cnt[i] = 0;
-    __syncthreads();
-    const uint32_t nu = __ldcg(&ws.header[0]);
-    for (uint32_t s = warp; s < nu; s += 16)
-        range_postings(e, ws, s, j, lane, [&](uint32_t a) { atomicAdd(&cnt[a], 1u); });
-    __syncthreads();
-    uint32_t tot = 0;
-    const int64_t a0 = (int64_t)j * R;
-    for (int i = tid; i < R / 4; i += 512) {
-        const uint32_t c0 = cnt[4 * i], c1 = cnt[4 * i + 1], c2 = cnt[4 * i + 2], c3 = cnt[4 * i + 3];
-        tot += c0 + c1 + c2 + c3;
-        if (a0 + 4 * i < e.n_pad) ws.adcnt[a0 / 4 + i] = c0 | (c1 << 8) | (c2 << 16) | (c3 << 24);   // <= F <= 255 each
-    }
-    tot = __reduce_add_sync(FULL, tot);
-    if (lane == 0) sRed[warp] = tot;
-    __syncthreads();
-    if (tid == 0) {
-        uint32_t t = 0;
-        for (int w = 0; w < 16; ++w) t += sRed[w];
-        ws.rtotal[j] = t;
+        uint32_t s = lo;
+        uint32_t s_end = __ldcg(&ws.uchunk[s + 1]);
+        const uint32_t gend = min(total, g0 + 32);
+        for (uint32_t gi = g0; gi < gend; ++gi) {
+            while (gi >= s_end) { ++s; s_end = __ldcg(&ws.uchunk[s + 1]); }
+            const uint32_t c = __ldcg(&ws.uc0[s]) + (gi - __ldcg(&ws.uchunk[s]));
+            uint32_t id;
+            const bool ok = decode_chunk(e.hdr, e.payload, __ldcg(&ws.ukwb[s]), c, lane, id);
+            const uint32_t r = ok ? id / R : 0xFFFFFFFFu;
+            const unsigned act = __ballot_sync(FULL, ok);
+            if (ok) {
+                const unsigned peers = __match_any_sync(act, r);
+                const int leader = __ffs(peers) - 1;
+                uint32_t base = 0;
+                if (lane == leader) base = atomicAdd(&ws.bin_cnt[r], (uint32_t)__popc(peers));
+                base = __shfl_sync(peers, base, leader);
+                const uint32_t pos = base + __popc(peers & ((1u << lane) - 1u));
+                ws.entries[(size_t)r * e.bin_cap + pos] = ((id - r * R) << 15) | s;   // s < 2^15
+            }
+        }
     }
 }
 
-__global__ void __launch_bounds__(1024) range_scan_kernel(EntryArgs e, Ws ws) {
-    __shared__ uint32_t sScan[40];
-    __shared__ uint32_t sBase;
-    if (threadIdx.x == 0) sBase = 0;
+// Level 2: CTA = bin.  Every bin entry (ad, union slot) is expanded to the streams of the groups
+// whose users query the slot; each group's part of the bin is ordered by (tile, pair-count class)
+// so a warp's consecutive entries carry similar work in the fused kernel.
+constexpr int kCountClasses = 8;
+__global__ void __launch_bounds__(512) entry_sort_kernel(EntryArgs e, Ws ws) {
+    extern __shared__ uint32_t smem_u[];
+    uint32_t* buf = smem_u;                               // [bin_cap]
+    uint32_t* off = smem_u + e.bin_cap;                   // [G][tiles_per_bin * kCountClasses]
+    __shared__ uint32_t sN, sBase[kMaxCluster];
+    const int r = blockIdx.x, tid = threadIdx.x;
+    const int tpb = e.bin_ads / kTileM, nb = tpb * kCountClasses, G = e.G;
+    if (tid == 0) { sN = ws.bin_cnt[r]; ws.bin_cnt[r] = 0u; }   // left zero for the next pass
+    for (int i = tid; i < G * nb; i += 512) off[i] = 0;
     __syncthreads();
-    for (int j0 = 0; j0 < e.n_ranges; j0 += 1024) {
-        const int j = j0 + threadIdx.x;
-        const uint32_t v = j < e.n_ranges ? ws.rtotal[j] : 0u;
-        uint32_t tot;
-        const uint32_t pre = block_exclusive_scan(v, sScan, &tot);
-        if (j < e.n_ranges) ws.rbase[j] = sBase + pre;
-        __syncthreads();
-        if (threadIdx.x == 0) sBase += tot;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        ws.rbase[e.n_ranges] = sBase;
-        ws.tile_off[e.n_tiles] = sBase;
-        ws.header[3] = sBase;
-    }
-}
-
-// entry_write: CTA = range; per-ad offsets (scan of the counts), the tile offsets, then every
-// posting written as an entry row << 24 | uentry[s] at its ad's next slot
-__global__ void __launch_bounds__(512) entry_write_kernel(EntryArgs e, Ws ws) {
-    extern __shared__ uint32_t cur[];      // [range_ads] running position of each ad's entries
-    __shared__ uint32_t sScan[40];
-    const int j = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int R = (int)e.range_ads;
-    const int64_t a0 = (int64_t)j * R;
-    const uint32_t base = ws.rbase[j];
-    const uint8_t* cnt8 = reinterpret_cast<const uint8_t*>(ws.adcnt);
-    // thread tid owns the ads [tid*pp, tid*pp + pp) of the range
-    const int pp = (R + 511) / 512;
-    const int i0 = tid * pp;
-    uint32_t local = 0;
-    for (int q = 0; q < pp; ++q) {
-        const int i = i0 + q;
-        if (i < R && a0 + i < e.n_pad) local += cnt8[a0 + i];
-    }
-    uint32_t tot;
-    uint32_t pre = block_exclusive_scan(local, sScan, &tot);
-    for (int q = 0; q < pp; ++q) {
-        const int i = i0 + q;
-        if (i >= R) break;
-        cur[i] = pre;
-        if ((i & (kTileM - 1)) == 0 && a0 + i < e.n_pad) ws.tile_off[(a0 + i) / kTileM] = base + pre;
-        if (a0 + i < e.n_pad) pre += cnt8[a0 + i];
+    const uint32_t n = sN;
+    const uint32_t* ent = ws.entries + (size_t)r * e.bin_cap;
+    const size_t trow = (size_t)e.NU + 1;
+    auto cls = [](uint32_t c) { return min(c, (uint32_t)kCountClasses) - 1u; };
+    for (uint32_t i = tid; i < n; i += 512) {
+        const uint32_t v = __ldcg(&ent[i]);
+        buf[i] = v;
+        const uint32_t a = v >> 15, sl = v & 0x7FFFu;
+        const uint32_t b = (a / kTileM) * kCountClasses;
+        for (int g = 0; g < G; ++g) {
+            const uint32_t c = (uint32_t)__ldg(&ws.toff[g * trow + sl + 1]) - __ldg(&ws.toff[g * trow + sl]);
+            if (c) atomicAdd(&off[g * nb + b + cls(c)], 1u);
+        }
     }
     __syncthreads();
-    const uint32_t nu = __ldcg(&ws.header[0]);
-    for (uint32_t s = warp; s < nu; s += 16) {
-        const uint32_t ent = ws.uentry[s];
-        range_postings(e, ws, s, j, lane, [&](uint32_t a) {
-            const uint32_t pos = atomicAdd(&cur[a], 1u);
-            ws.entries[base + pos] = ((a & (kTileM - 1)) << 24) | ent;
-        });
+    // per group: exclusive scan of the buckets (warp g), the group's range claimed from the pool
+    const int warp = tid >> 5, lane = tid & 31;
+    if (warp < G) {
+        uint32_t* o = off + warp * nb;
+        uint32_t carry = 0;
+        for (int b0 = 0; b0 < nb; b0 += 32) {
+            const uint32_t x = (b0 + lane < nb) ? o[b0 + lane] : 0u;
+            uint32_t incl = x;
+#pragma unroll
+            for (int k = 1; k < 32; k <<= 1) {
+                const uint32_t y = __shfl_up_sync(FULL, incl, k);
+                if (lane >= k) incl += y;
+            }
+            if (b0 + lane < nb) o[b0 + lane] = carry + incl - x;
+            carry += __shfl_sync(FULL, incl, 31);
+        }
+        uint32_t base = 0;
+        if (lane == 0) base = carry ? atomicAdd(&ws.header[6], carry) : 0u;
+        base = __shfl_sync(FULL, base, 0);
+        if (lane == 0) sBase[warp] = base;
+        // tile bounds of this group's stream
+        const int64_t t0 = (int64_t)r * tpb;
+        for (int tl = lane; tl < tpb; tl += 32) {
+            const int64_t t = t0 + tl;
+            if (t >= e.n_tiles) continue;
+            ws.tile_beg[(size_t)warp * e.n_tiles + t] = base + o[tl * kCountClasses];
+            ws.tile_end[(size_t)warp * e.n_tiles + t] = base + ((tl + 1 < tpb) ? o[(tl + 1) * kCountClasses] : carry);
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = tid; i < n; i += 512) {
+        const uint32_t v = buf[i];
+        const uint32_t a = v >> 15, sl = v & 0x7FFFu;
+        const uint32_t b = (a / kTileM) * kCountClasses;
+        const uint32_t out = ((a & (kTileM - 1)) << 24) | sl;
+        for (int g = 0; g < G; ++g) {
+            const uint32_t c = (uint32_t)__ldg(&ws.toff[g * trow + sl + 1]) - __ldg(&ws.toff[g * trow + sl]);
+            if (c) {
+                const uint32_t pos = atomicAdd(&off[g * nb + b + cls(c)], 1u);
+                ws.gentries[sBase[g] + pos] = out;
+            }
+        }
     }
 }
 
 // ------------------------------------------------------------------------------------------
 // A3-A6b: the fused tensor-core kernel
 // ------------------------------------------------------------------------------------------
+// D[users x ads] = cold + U A^T (+ U_hot H^T), per CTA 128 users (TMEM lanes) x 128-ad tiles:
+// the CTA's users are the MMA's A operand and stay resident in TMEM for the whole launch (loaded
+// once), the ad tiles are B, streamed by TMA into a shared-memory ring (multicast to the cluster)
+// and, for the hot keys, expanded from bit masks into fp16 one-hot blocks in the same ring.
 struct GemmParams {
     int64_t n_ads, n_pad;
     uint32_t ad_begin;
-    int n_kb, n_hb, pieces, u_blocks;
+    int n_kb, n_hb, pieces;
     int P;                  // users in this pass
     int n_tiles, tile_stride;
     int n_samp;
-    int stages;
+    int stages;             // ring stages (16 KB each)
+    int acc_stages;         // TMEM accumulator stages (128 columns each)
+    int u_cols;             // 16-bit columns of the pass's user tile U
     int64_t cap;
     int rerun;              // filter rerun: only flagged users; gated on header[2] | header[4]
     int dense;              // sample-mode variant: every score of the overflowed users (gated on header[4])
     const uint4* hot_mask;
     Ws ws;
     uint32_t* err;
+    int diag;               // A/B experiments (EBR_DIAG): 1 skip the cold scatter, 2 skip the epilogue work
+    int NU;                 // union slot capacity of the pass (toff row length - 1)
+    int gcap;               // pair capacity of a group's list
+    int n_tiles_all;        // tiles of the inventory (row length of the group streams' tile bounds)
 };
 
-__device__ __forceinline__ int32_t pair_w(uint32_t pr) {
-    return (int32_t)(pr << (32 - kPairWBits)) >> (32 - kPairWBits);   // sign-extend the 23-bit field
-}
+// role cycle accounting (EBR_DIAG & 4): prof[slot] += clock64 delta, from one thread per role
+#define EBR_PROF_T0 const long long _pt0 = (p.diag & 4) ? clock64() : 0
+#define EBR_PROF_ADD(slot) do { if ((p.diag & 4)) atomicAdd(&p.ws.prof[slot], (unsigned long long)(clock64() - _pt0)); } while (0)
 
 template <int MODE>   // 0: sample (store s; dense: all scores of overflowed users), 1: filter (append keys >= theta)
 __global__ void __launch_bounds__(kGemmThreads, 1)
-score_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmU, const GemmParams p) {
+score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // gated launches (uniform over the grid): nothing to redo
     if (MODE == 1 && p.rerun && (*(volatile uint32_t*)&p.ws.header[2] | *(volatile uint32_t*)&p.ws.header[4]) == 0u)
         return;
     if (MODE == 0 && p.dense && *(volatile uint32_t*)&p.ws.header[4] == 0u) return;
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    // 1024-byte alignment (SW128 tiles) by an integer offset into the shared array: the pointers
+    // below stay in the shared state space (LDS/STS/ATOMS, not generic accesses)
+    unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const long long _pk0 = (p.diag & 4) ? clock64() : 0;
     const uint32_t rank = tc::cluster_ctarank();
     uint32_t csize;
     asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(csize));
@@ -517,44 +598,54 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
     const uint16_t mc_mask = (uint16_t)((1u << csize) - 1u);
     const int g = (int)rank;                         // this CTA's user group
     const int nu = min(kGroup, p.P - g * kGroup);    // valid users
-    const int nu_pad = (nu + 31) & ~31;
     const int nkt = p.n_kb + p.n_hb;
+    const int a_cols = 32 * (p.n_kb + p.n_hb * p.pieces);   // TMEM columns of the users' A operand
+    const int nst = p.acc_stages;
 
-    unsigned char* sU = smem;                                               // [u_blocks][128 x 128 B]
-    unsigned char* sRing = sU + (size_t)p.u_blocks * kBlockBytes;          // [stages][128 x 128 B]
-    int32_t* acc = reinterpret_cast<int32_t*>(sRing + (size_t)p.stages * kBlockBytes);   // [128][kAccPitch]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(acc + kTileM * kAccPitch);
+    unsigned char* sRing = smem;                                            // [stages][128 ads x 128 B]
+    int32_t* acc = reinterpret_cast<int32_t*>(sRing + (size_t)p.stages * kBlockBytes);   // [128 users][kAccPitch]
+    uint4* sLut = reinterpret_cast<uint4*>(acc + kGroup * kAccPitch);       // [256] byte -> 8 fp16 {0, 1} (16-B aligned)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sLut + 256);
     uint64_t* full = bars;
     uint64_t* empty = full + p.stages;
     uint64_t* tfull = empty + p.stages;
-    uint64_t* tempty = tfull + kAccStages;
-    uint64_t* wready = tempty + kAccStages;
-    uint64_t* ufull = wready + kAccStages;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ufull + 1);
+    uint64_t* tempty = tfull + kMaxAccStages;
+    uint64_t* wready = tempty + kMaxAccStages;
+    uint64_t* aready = wready + kMaxAccStages;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aready + 1);
     uint64_t* sTheta = reinterpret_cast<uint64_t*>(tmem_slot + 2);          // [kGroup]
     float* sThetaS = reinterpret_cast<float*>(sTheta + kGroup);             // [kGroup]
     float* sScale = sThetaS + kGroup;                                       // [kGroup]
     int* sDense = reinterpret_cast<int*>(sScale + kGroup);                  // [kGroup] dense slot or -1
+    uint16_t* sT = reinterpret_cast<uint16_t*>(sDense + kGroup);            // [n_union + 1] slot -> first pair
+    const uint32_t n_union = __ldcg(&p.ws.header[0]), n_gp = __ldcg(&p.ws.header[8 + g]);
+    uint32_t* sPairs = reinterpret_cast<uint32_t*>(sT + ((n_union + 2) & ~1u));   // [n_gp]
 
     if (tid == 0) {
         for (int s = 0; s < p.stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], csize); }
-        for (int s = 0; s < kAccStages; ++s) {
+        for (int s = 0; s < kMaxAccStages; ++s) {
             mbar_init(&tfull[s], 1);
             mbar_init(&tempty[s], kEpiWarps);
             mbar_init(&wready[s], 1);
         }
-        mbar_init(ufull, 1);
+        mbar_init(aready, 4);
         fence_mbar_init();
     }
-    if (warp == 2) tc::tmem_alloc(tmem_slot, kAccStages * 128);
-    for (int i = tid; i < kTileM * kAccPitch / 4; i += kGemmThreads)
+    if (warp == 2) tc::tmem_alloc(tmem_slot, 512);
+    for (int i = tid; i < kGroup * kAccPitch / 4; i += kGemmThreads)
         reinterpret_cast<int4*>(acc)[i] = make_int4(0, 0, 0, 0);
+    for (int b = tid; b < 256; b += kGemmThreads) {
+        auto h2 = [b](int k) { return ((b >> k) & 1 ? 0x3C00u : 0u) | ((b >> (k + 1)) & 1 ? 0x3C000000u : 0u); };
+        sLut[b] = make_uint4(h2(0), h2(2), h2(4), h2(6));
+    }
+    for (uint32_t i = tid; i <= n_union; i += kGemmThreads) sT[i] = __ldcg(&p.ws.toff[(size_t)g * (p.NU + 1) + i]);
+    for (uint32_t i = tid; i < n_gp; i += kGemmThreads) sPairs[i] = __ldcg(&p.ws.pairs[(size_t)g * p.gcap + i]);
     for (int i = tid; i < kGroup; i += kGemmThreads) {
         const int u = g * kGroup + i;
         const bool ok = i < nu;
         sScale[i] = ok ? p.ws.uscale[u] : 0.f;
         const uint32_t fl = ok ? __ldcg(&p.ws.uflags[u]) : 0u;
-        if (MODE == 0) sDense[i] = (p.dense && (fl & kFlagOverflow)) ? (int)(fl >> 8) : -1;
+        sDense[i] = (MODE == 0 && p.dense && (fl & kFlagOverflow)) ? (int)(fl >> 8) : -1;
         if (MODE == 1) {
             bool take = ok;
             if (p.rerun) take = ok && (fl & kFlagAny);
@@ -570,20 +661,16 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
 
     if (warp == 0) {
         if (lane == 0) {
-            // ---------------- TMA producer: U once, then the deep K blocks of every tile ----------------
+            // ---------------- TMA producer: the deep K blocks of every ad tile ----------------
             tc::tma_prefetch(&tmA);
-            tc::tma_prefetch(&tmU);
-            mbar_arrive_expect_tx(ufull, (uint32_t)(p.u_blocks * kBlockBytes));
-            for (int kb = 0; kb < p.u_blocks; ++kb)
-                tc::tma_load_2d(sU + (size_t)kb * kBlockBytes, &tmU, kb * kBlockK, g * kGroup, ufull);
             const uint64_t pol = tc::policy_evict_first();   // A is streamed once per pass
             uint32_t gb = 0;
             for (int t = (int)cid; t < p.n_tiles; t += (int)ncl) {
                 const int row0 = t * p.tile_stride * kTileM;
                 for (int kb = 0; kb < nkt; ++kb, ++gb) {
-                    if (kb >= p.n_kb) continue;             // hot block: expanded by the wide warps
+                    if (kb >= p.n_kb) continue;             // hot block: expanded by the hot warps
                     const uint32_t slot = gb % p.stages, round = gb / p.stages;
-                    if (round > 0) mbar_wait_sleep(&empty[slot], (round - 1) & 1);
+                    if (round > 0) { EBR_PROF_T0; mbar_wait_sleep(&empty[slot], (round - 1) & 1); EBR_PROF_ADD(0); }
                     mbar_arrive_expect_tx(&full[slot], (uint32_t)kBlockBytes);
                     if (csize == 1)
                         tc::tma_load_2d_hint(sRing + (size_t)slot * kBlockBytes, &tmA, kb * kBlockK, row0, &full[slot], pol);
@@ -602,34 +689,33 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
         if (lane == 0) {
             // ---------------- MMA issuer ----------------
             // The accumulator stage already holds the tile's cold wide term (stored by the wide
-            // warps), so every MMA accumulates: D = cold + A U_deep^T + H (hi, lo)^T.
-            const uint32_t idb = tc::idesc_bf16_m128(nu_pad), idh = tc::idesc_f16_m128(nu_pad);
-            mbar_wait_sleep(ufull, 0);
+            // warps), so every MMA accumulates: D = cold + U A^T + U_hot (one-hot)^T.
+            const uint32_t idb = tc::idesc_bf16_m128(kTileM), idh = tc::idesc_f16_m128(kTileM);
+            mbar_wait_sleep(aready, 0);                   // users' A operand in TMEM
             tc::fence_after();
             int it = 0;
             uint32_t gb = 0;
             for (int t = (int)cid; t < p.n_tiles; t += (int)ncl, ++it) {
-                const int st = it % kAccStages;
-                mbar_wait_sleep(&wready[st], (it / kAccStages) & 1);
+                const int st = it % nst;
+                { EBR_PROF_T0; mbar_wait_sleep(&wready[st], (it / nst) & 1); EBR_PROF_ADD(1); }
                 tc::fence_after();
-                const uint32_t d_tmem = tmem_base + (uint32_t)(st * 128);
+                const uint32_t d_tmem = tmem_base + (uint32_t)(a_cols + st * kTileM);
                 for (int kb = 0; kb < nkt; ++kb, ++gb) {
                     const uint32_t slot = gb % p.stages;
-                    mbar_wait_sleep(&full[slot], (gb / p.stages) & 1);
+                    { EBR_PROF_T0; mbar_wait_sleep(&full[slot], (gb / p.stages) & 1); EBR_PROF_ADD(2); }
                     tc::fence_after();
-                    const uint64_t da0 = tc::sdesc_sw128(sRing + (size_t)slot * kBlockBytes);
+                    const uint64_t db0 = tc::sdesc_sw128(sRing + (size_t)slot * kBlockBytes);
                     if (kb < p.n_kb) {
-                        const uint64_t db0 = tc::sdesc_sw128(sU + (size_t)kb * kBlockBytes);
 #pragma unroll
                         for (int k = 0; k < kBlockK / 16; ++k)
-                            tc::umma_f16(d_tmem, da0 + (uint64_t)(k * 2), db0 + (uint64_t)(k * 2), idb, 1u);
+                            tc::umma_f16_ts(d_tmem, tmem_base + (uint32_t)(kb * 32 + k * 8), db0 + (uint64_t)(k * 2), idb, 1u);
                     } else {
                         const int h = kb - p.n_kb;
                         for (int pc = 0; pc < p.pieces; ++pc) {
-                            const uint64_t db0 = tc::sdesc_sw128(sU + (size_t)(p.n_kb + h * p.pieces + pc) * kBlockBytes);
+                            const uint32_t ac = (uint32_t)(32 * (p.n_kb + h * p.pieces + pc));
 #pragma unroll
                             for (int k = 0; k < kBlockK / 16; ++k)
-                                tc::umma_f16(d_tmem, da0 + (uint64_t)(k * 2), db0 + (uint64_t)(k * 2), idh, 1u);
+                                tc::umma_f16_ts(d_tmem, tmem_base + ac + (uint32_t)(k * 8), db0 + (uint64_t)(k * 2), idh, 1u);
                         }
                     }
                     if (csize == 1) tc::umma_commit(&empty[slot]);
@@ -638,159 +724,245 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                 tc::umma_commit(&tfull[st]);
             }
         }
-    } else if (warp >= kWideWarp0 && warp < kEpiWarp0) {
-        // ---------------- wide warps: hot one-hot block, cold scatter, TMEM store ----------------
-        const int wt = tid - kWideWarp0 * 32;
-        const int q = warp & 3, half = (warp - kWideWarp0) >> 2;
-        const int row = q * 32 + lane;
-        const uint32_t* __restrict__ entries = p.ws.entries;
-        const uint32_t* __restrict__ pairs = p.ws.pairs;
-        int it = 0;
-        uint32_t gb = 0;
-        for (int t = (int)cid; t < p.n_tiles; t += (int)ncl, ++it) {
-            const int st = it % kAccStages;
-            const int64_t tw = (int64_t)t * p.tile_stride;
-            // hot: the row's one-hot fp16 K block(s), written in the TMA 128B-swizzle layout
-            if (p.n_hb) {
-                const uint4 hm = __ldg(&p.hot_mask[tw * kTileM + row]);
+    } else if (warp == 2 || warp == 3) {
+        // ---------------- hot warps: the tile's hot-key one-hot fp16 K block(s) ----------------
+        // Thread hw owns ad rows hw and hw + 64; each row's 64-key block is 8 chunks of 16 B written
+        // in the TMA 128B-swizzle layout (chunk c of row r at (c ^ (r & 7)) * 16).  The masks of
+        // the next tile are loaded while this one is written.
+        if (p.n_hb) {
+            const int hw = tid - 64;
+            uint4 hm[2], hn[2];
+            auto load = [&](int tt, uint4 (&m)[2]) {
+                if (tt < p.n_tiles) {
+                    const int64_t tw = (int64_t)tt * p.tile_stride;
+                    m[0] = __ldg(&p.hot_mask[tw * kTileM + hw]);
+                    m[1] = __ldg(&p.hot_mask[tw * kTileM + hw + 64]);
+                }
+            };
+            load((int)cid, hn);
+            uint32_t gb = 0;
+            for (int t = (int)cid; t < p.n_tiles; t += (int)ncl) {
+                hm[0] = hn[0];
+                hm[1] = hn[1];
+                load(t + (int)ncl, hn);
                 for (int h = 0; h < p.n_hb; ++h) {
                     const uint32_t pos = gb + p.n_kb + h;
                     const uint32_t slot = pos % p.stages, round = pos / p.stages;
-                    if (round > 0) mbar_wait(&empty[slot], (round - 1) & 1);
-                    const uint64_t bits = h == 0 ? ((uint64_t)hm.y << 32 | hm.x) : ((uint64_t)hm.w << 32 | hm.z);
-                    unsigned char* rowp = sRing + (size_t)slot * kBlockBytes + (size_t)row * 128;
+                    if (round > 0) { EBR_PROF_T0; mbar_wait(&empty[slot], (round - 1) & 1); if (hw == 0) EBR_PROF_ADD(3); }
 #pragma unroll
-                    for (int cc = 0; cc < 4; ++cc) {
-                        const int c = half * 4 + cc;                 // 16-byte chunk: keys 8c .. 8c+7
-                        const uint32_t byte = (uint32_t)(bits >> (8 * c)) & 0xFFu;
-                        uint4 v;
-                        v.x = ((byte & 1u) ? 0x3C00u : 0u) | ((byte & 2u) ? 0x3C000000u : 0u);
-                        v.y = ((byte & 4u) ? 0x3C00u : 0u) | ((byte & 8u) ? 0x3C000000u : 0u);
-                        v.z = ((byte & 16u) ? 0x3C00u : 0u) | ((byte & 32u) ? 0x3C000000u : 0u);
-                        v.w = ((byte & 64u) ? 0x3C00u : 0u) | ((byte & 128u) ? 0x3C000000u : 0u);
-                        *reinterpret_cast<uint4*>(rowp + ((c ^ (row & 7)) << 4)) = v;
+                    for (int rr = 0; rr < 2; ++rr) {
+                        const int row = hw + rr * 64;
+                        const uint64_t bits = h == 0 ? ((uint64_t)hm[rr].y << 32 | hm[rr].x)
+                                                     : ((uint64_t)hm[rr].w << 32 | hm[rr].z);
+                        unsigned char* rowp = sRing + (size_t)slot * kBlockBytes + (size_t)row * 128;
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) {                  // 16-byte chunk: keys 8c .. 8c+7
+                            const uint32_t byte = (uint32_t)(bits >> (8 * c)) & 0xFFu;
+                            *reinterpret_cast<uint4*>(rowp + ((c ^ (row & 7)) << 4)) = sLut[byte];
+                        }
                     }
                     tc::fence_proxy_async_smem();
-                    tc::named_bar_sync(1, kWideThreads);
-                    if (wt == 0) mbar_arrive(&full[slot]);
+                    tc::named_bar_sync(2, 64);
+                    if (hw == 0) mbar_arrive(&full[slot]);
+                }
+                gb += nkt;
+            }
+        }
+    } else if (warp >= kWideWarp0 && warp < kEpiWarp0) {
+        // ---------------- wide warps: users' A operand once, then cold scatter + TMEM store ----------------
+        const int wt = tid - kWideWarp0 * 32;
+        const int q = warp & 3;                          // TMEM lane quadrant = users 32q .. 32q + 31
+        const int cj = (warp - kWideWarp0) >> 2;         // this warp's 32-ad column chunk of a tile
+        const int urow = q * 32 + lane;                  // the user (TMEM lane) of this thread
+        if (warp < kWideWarp0 + 4) {
+            // U row of this user -> TMEM A columns (two 16-bit K elements per 32-bit column)
+            const uint32_t* urow_p = reinterpret_cast<const uint32_t*>(p.ws.U) +
+                                     (size_t)(g * kGroup + urow) * (p.u_cols / 2);
+            for (int c0 = 0; c0 < a_cols; c0 += 32) {
+                uint32_t v[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = __ldcg(&urow_p[c0 + j]);
+                tc::tmem_st32_nowait(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
+            }
+            tc::tmem_wait_st();
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(aready);
+        }
+        const uint32_t* __restrict__ entries = p.ws.gentries;
+        constexpr int kE = kWideWarps >= 16 ? 4 : 8;   // entries per thread and batch (registers)
+        constexpr uint32_t kNoEntry = 0xFFFFFFFFu;     // (a real entry has bit 31 clear)
+        // software pipeline over tiles: the entry bounds two tiles ahead and the first entries one
+        // tile ahead are in flight while the current tile is processed
+        auto bounds = [&](int tt, uint32_t& b, uint32_t& e) {
+            b = e = 0u;
+            if (tt < p.n_tiles) {
+                const size_t ti = (size_t)g * p.n_tiles_all + (size_t)tt * p.tile_stride;
+                b = __ldcg(&p.ws.tile_beg[ti]);
+                e = __ldcg(&p.ws.tile_end[ti]);
+            }
+        };
+        uint32_t cur_beg, cur_end, nxt_beg, nxt_end, nent[kE];
+        bounds((int)cid, cur_beg, cur_end);
+        bounds((int)cid + (int)ncl, nxt_beg, nxt_end);
+#pragma unroll
+        for (int i = 0; i < kE; ++i) {
+            const uint32_t e = cur_beg + wt + i * kWideThreads;
+            nent[i] = e < cur_end ? __ldcs(&entries[e]) : kNoEntry;
+        }
+        const float uscale = sScale[urow];
+        int it = 0;
+        for (int t = (int)cid; t < p.n_tiles; t += (int)ncl, ++it) {
+            const int st = it % nst;
+            const long long _pc0 = (p.diag & 4) ? clock64() : 0;
+            // cold: the tile's entries (ad row, union slot) of this CTA's group stream; the slot's
+            // pairs (user, w~ 2^S) are in shared memory (sT: first pair per slot)
+            {
+                const uint32_t e0 = cur_beg, e1 = (p.diag & 1) ? cur_beg : cur_end;
+                const uint32_t nbatch = (e1 - e0 + kE * kWideThreads - 1) / (kE * kWideThreads);
+                for (uint32_t batch = 0, eb = e0 + wt; batch < nbatch; eb += kE * kWideThreads, ++batch) {
+                    uint32_t ent[kE];
+#pragma unroll
+                    for (int i = 0; i < kE; ++i) {
+                        const uint32_t e = eb + i * kWideThreads;
+                        ent[i] = batch == 0 ? nent[i] : (e < e1 ? __ldcs(&entries[e]) : kNoEntry);
+                    }
+#pragma unroll
+                    for (int i = 0; i < kE; ++i) {
+                        if (ent[i] == kNoEntry) continue;
+                        const uint32_t a = ent[i] >> 24, sl = ent[i] & 0xFFFFFFu;
+                        const uint32_t lo = sT[sl], hi = sT[sl + 1];
+                        for (uint32_t qq = lo; qq < hi; ++qq) {
+                            const uint32_t pr = sPairs[qq];
+                            atomicAdd(&acc[(pr & (kGroup - 1)) * kAccPitch + a], (int32_t)pr >> kPairUBits);
+                        }
+                    }
                 }
             }
-            gb += nkt;
-            // cold: the tile's entries (row, the key's user pairs); this CTA takes its group's users
-            const uint32_t e0 = __ldcg(&p.ws.tile_off[tw]), e1 = __ldcg(&p.ws.tile_off[tw + 1]);
-            for (uint32_t e = e0 + wt; e < e1; e += kWideThreads) {
-                const uint32_t ent = __ldcg(&entries[e]);
-                const uint32_t r = ent >> 24;
-                const uint32_t ps = ent & (kMaxPassPairs - 1);
-                const uint32_t pe = ps + ((ent >> kEntryPsBits) & 511u) + 1u;
-                int32_t* arow = acc + r * kAccPitch;
-                for (uint32_t pi = ps; pi < pe; ++pi) {
-                    const uint32_t pr = __ldcg(&pairs[pi]);
-                    const uint32_t u = pr >> kPairWBits;
-                    if ((int)(u >> 7) == g) atomicAdd(&arow[u & 127u], pair_w(pr));
+            // next tile's entries, in flight during the store phase
+            {
+                cur_beg = nxt_beg;
+                cur_end = nxt_end;
+#pragma unroll
+                for (int i = 0; i < kE; ++i) {
+                    const uint32_t e = cur_beg + wt + i * kWideThreads;
+                    nent[i] = e < cur_end ? __ldcs(&entries[e]) : kNoEntry;
                 }
+                bounds(t + 2 * (int)ncl, nxt_beg, nxt_end);
             }
             tc::named_bar_sync(1, kWideThreads);
-            // the accumulator stage is free once the epilogue drained it (kAccStages tiles ago)
-            if (it >= kAccStages) mbar_wait(&tempty[st], ((it / kAccStages) - 1) & 1);
+            if ((p.diag & 4) && wt == 0) atomicAdd(&p.ws.prof[4], (unsigned long long)(clock64() - _pc0));
+            // the accumulator stage is free once the epilogue drained it (nst tiles ago)
+            if (it >= nst) { EBR_PROF_T0; mbar_wait(&tempty[st], ((it / nst) - 1) & 1); if (wt == 0) EBR_PROF_ADD(5); }
+            const long long _ps0 = (p.diag & 4) ? clock64() : 0;
             tc::fence_after();
-#pragma unroll 1
-            for (int ch = 0; ch < 2; ++ch) {
-                const int c = half * 64 + ch * 32;
-                if (c >= nu_pad) break;
-                int4* src = reinterpret_cast<int4*>(acc + row * kAccPitch + c);
+            {
+                // this user's 32 ads of the tile: fixed point -> fp32 (the one rounding), zeroed
+                int4* src = reinterpret_cast<int4*>(acc + urow * kAccPitch + cj * 32);
                 uint32_t f[32];
 #pragma unroll
                 for (int v4 = 0; v4 < 8; ++v4) {
                     const int4 v = src[v4];
                     src[v4] = make_int4(0, 0, 0, 0);
-                    f[4 * v4 + 0] = __float_as_uint((float)v.x * sScale[c + 4 * v4 + 0]);   // the one rounding
-                    f[4 * v4 + 1] = __float_as_uint((float)v.y * sScale[c + 4 * v4 + 1]);
-                    f[4 * v4 + 2] = __float_as_uint((float)v.z * sScale[c + 4 * v4 + 2]);
-                    f[4 * v4 + 3] = __float_as_uint((float)v.w * sScale[c + 4 * v4 + 3]);
+                    f[4 * v4 + 0] = __float_as_uint((float)v.x * uscale);
+                    f[4 * v4 + 1] = __float_as_uint((float)v.y * uscale);
+                    f[4 * v4 + 2] = __float_as_uint((float)v.z * uscale);
+                    f[4 * v4 + 3] = __float_as_uint((float)v.w * uscale);
                 }
-                tc::tmem_st32_nowait(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(st * 128 + c), f);
+                tc::tmem_st32_nowait(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a_cols + st * kTileM + cj * 32), f);
             }
             tc::tmem_wait_st();
             tc::fence_before();
             tc::named_bar_sync(1, kWideThreads);
             if (wt == 0) mbar_arrive(&wready[st]);
+            if ((p.diag & 4) && wt == 0) atomicAdd(&p.ws.prof[6], (unsigned long long)(clock64() - _ps0));
         }
     } else if (warp >= kEpiWarp0) {
         // ---------------- epilogue: TMEM -> registers, kappa, sample store / filter ----------------
+        // thread = one user (TMEM lane) x half of the tile's ads (two 32-column chunks)
         const int e = warp - kEpiWarp0;
         const int q = warp & 3;
-        const int row = q * 32 + lane;
+        const int ul = q * 32 + lane;                    // CTA-local user
+        const int u = g * kGroup + ul;                   // pass user
+        const bool uok = ul < nu;
+        const int hf = e >> 2;
+        float thS = 0.f;
+        uint64_t th = 0;
+        int dslot = -1;
+        if (MODE == 1) { thS = sThetaS[ul]; th = sTheta[ul]; }
+        else dslot = sDense[ul];
         int it = 0;
         for (int t = (int)cid; t < p.n_tiles; t += (int)ncl, ++it) {
-            const int st = it % kAccStages;
-            const int64_t a = (int64_t)t * p.tile_stride * kTileM + row;   // shard-local ad
-            const bool valid = a < p.n_ads;
-            mbar_wait_sleep(&tfull[st], (it / kAccStages) & 1);
+            const int st = it % nst;
+            const int64_t a0 = (int64_t)t * p.tile_stride * kTileM;   // shard-local first ad of the tile
+            { EBR_PROF_T0; mbar_wait_sleep(&tfull[st], (it / nst) & 1); if (warp == kEpiWarp0 && lane == 0) EBR_PROF_ADD(7); }
             tc::fence_after();
+            const long long _pe0 = (p.diag & 4) ? clock64() : 0;
 #pragma unroll 1
-            for (int ch = 0; ch < 2; ++ch) {
-                const int c = (e >> 2) * 64 + ch * 32;
-                if (c >= nu_pad) break;
+            for (int ch = 0; ch < 2 && !(p.diag & 2); ++ch) {
+                const int c = hf * 64 + ch * 32;
                 uint32_t r[32];
-                tc::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(st * 128 + c), r);
-                const int nuc = nu - c;
-                const uint32_t umask = nuc >= 32 ? 0xFFFFFFFFu : (nuc > 0 ? (1u << nuc) - 1u : 0u);
-                if (MODE == 0 && p.dense) {
-                    for (int j = 0; j < 32; ++j) {
-                        const int sl = sDense[c + j];
-                        if (sl >= 0 && ((umask >> j) & 1u)) {
-                            float s = __uint_as_float(r[j]);
-                            if (s == 0.f) s = 0.f;
-                            p.ws.dense[(size_t)sl * p.n_pad + a] = valid ? s : __int_as_float(0xFF800000);
-                        }
-                    }
-                } else if (MODE == 0) {
+                tc::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a_cols + st * kTileM + c), r);
+                const int64_t ac = a0 + c;
+                const int nval = (int)min((int64_t)32, max((int64_t)0, p.n_ads - ac));   // valid ads in the chunk
+                if (MODE == 0) {
+                    if (p.dense) {
+                        if (dslot >= 0) {
+                            float* dst = p.ws.dense + (size_t)dslot * p.n_pad + ac;
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        float s = __uint_as_float(r[j]);
-                        if (s == 0.f) s = 0.f;                       // -0 -> +0 (R14)
-                        if ((umask >> j) & 1u)
-                            p.ws.samp[(size_t)(g * kGroup + c + j) * p.n_samp + (int64_t)t * kTileM + row] =
-                                valid ? s : __int_as_float(0xFF800000);
+                            for (int j = 0; j < 32; ++j) {
+                                float s = __uint_as_float(r[j]);
+                                if (s == 0.f) s = 0.f;                       // -0 -> +0 (R14)
+                                dst[j] = j < nval ? s : __int_as_float(0xFF800000);
+                            }
+                        }
+                    } else if (uok) {
+                        float4* dst = reinterpret_cast<float4*>(p.ws.samp + (size_t)u * p.n_samp + (int64_t)t * kTileM + c);
+#pragma unroll
+                        for (int j4 = 0; j4 < 8; ++j4) {
+                            float o[4];
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                float s = __uint_as_float(r[4 * j4 + k]);
+                                if (s == 0.f) s = 0.f;                       // -0 -> +0 (R14)
+                                o[k] = (4 * j4 + k) < nval ? s : __int_as_float(0xFF800000);
+                            }
+                            dst[j4] = make_float4(o[0], o[1], o[2], o[3]);
+                        }
                     }
                 } else {
                     uint32_t pass = 0;
-                    const float4* th4 = reinterpret_cast<const float4*>(sThetaS + c);
 #pragma unroll
-                    for (int j4 = 0; j4 < 8; ++j4) {
-                        const float4 th = th4[j4];
-                        pass |= (__uint_as_float(r[j4 * 4 + 0]) >= th.x ? 1u : 0u) << (j4 * 4 + 0);
-                        pass |= (__uint_as_float(r[j4 * 4 + 1]) >= th.y ? 1u : 0u) << (j4 * 4 + 1);
-                        pass |= (__uint_as_float(r[j4 * 4 + 2]) >= th.z ? 1u : 0u) << (j4 * 4 + 2);
-                        pass |= (__uint_as_float(r[j4 * 4 + 3]) >= th.w ? 1u : 0u) << (j4 * 4 + 3);
-                    }
-                    pass &= valid ? umask : 0u;
-                    uint32_t cols = __reduce_or_sync(FULL, pass);
+                    for (int j = 0; j < 32; ++j) pass |= (__uint_as_float(r[j]) >= thS ? 1u : 0u) << j;
+                    pass &= nval >= 32 ? 0xFFFFFFFFu : ((1u << nval) - 1u);
+                    if (!uok) pass = 0u;
+                    // exact key compare, then this user's appends (one atomic per thread and chunk)
+                    uint32_t take = 0;
+                    if (pass) {
 #pragma unroll 1
-                    while (cols) {
-                        const int j = __ffs(cols) - 1;
-                        cols &= cols - 1u;
-                        const int ul = c + j;                         // CTA-local user
-                        const int u = g * kGroup + ul;                // pass user
-                        const bool maybe = (pass >> j) & 1u;
-                        float s = 0.f;
+                        for (uint32_t m = pass; m; m &= m - 1u) {
+                            const int j = __ffs(m) - 1;
+                            float s = 0.f;
 #pragma unroll
-                        for (int jj = 0; jj < 32; ++jj) s = (jj == j) ? __uint_as_float(r[jj]) : s;
-                        if (s == 0.f) s = 0.f;                       // -0 -> +0 (R14)
-                        const uint64_t key = maybe ? kappa_of(s, p.ad_begin + (uint32_t)a) : 0ull;
-                        const bool take = maybe && key >= sTheta[ul];
-                        const unsigned m = __ballot_sync(FULL, take);
-                        if (m) {
-                            const int leader = __ffs(m) - 1;
-                            uint32_t pos = 0;
-                            if (lane == leader) pos = atomicAdd(&p.ws.cand_count[u], (uint32_t)__popc(m));
-                            pos = __shfl_sync(FULL, pos, leader) + __popc(m & ((1u << lane) - 1u));
-                            if (take && pos < p.cap) p.ws.cand[(size_t)u * p.cap + pos] = key;
+                            for (int jj = 0; jj < 32; ++jj) s = (jj == j) ? __uint_as_float(r[jj]) : s;
+                            if (s == 0.f) s = 0.f;                       // -0 -> +0 (R14)
+                            if (kappa_of(s, p.ad_begin + (uint32_t)(ac + j)) >= th) take |= 1u << j;
+                        }
+                    }
+                    if (take) {
+                        uint32_t pos = atomicAdd(&p.ws.cand_count[u], (uint32_t)__popc(take));
+                        for (uint32_t m = take; m; m &= m - 1u, ++pos) {
+                            const int j = __ffs(m) - 1;
+                            float s = 0.f;
+#pragma unroll
+                            for (int jj = 0; jj < 32; ++jj) s = (jj == j) ? __uint_as_float(r[jj]) : s;
+                            if (s == 0.f) s = 0.f;
+                            if (pos < p.cap) p.ws.cand[(size_t)u * p.cap + pos] = kappa_of(s, p.ad_begin + (uint32_t)(ac + j));
                         }
                     }
                 }
             }
+            if ((p.diag & 4) && warp == kEpiWarp0 && lane == 0) atomicAdd(&p.ws.prof[8], (unsigned long long)(clock64() - _pe0));
             tc::fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[st]);
@@ -800,7 +972,11 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
     tc::fence_before();
     __syncthreads();
     tc::cluster_sync_all();
-    if (warp == 2) tc::tmem_dealloc(tmem_base, kAccStages * 128);
+    if ((p.diag & 4) && tid == 0) {
+        atomicAdd(&p.ws.prof[9], 1ull);
+        atomicAdd(&p.ws.prof[10], (unsigned long long)(clock64() - _pk0));
+    }
+    if (warp == 2) tc::tmem_dealloc(tmem_base, 512);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1009,13 +1185,21 @@ static bool encode_2d_16(CUtensorMap* m, const void* base, uint64_t inner, uint6
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// EBR_TRACE=1: synchronise and report after every launch of the batched path (debugging only)
+static void trace(cudaStream_t st, const char* what) {
+    static const bool on = getenv("EBR_TRACE") != nullptr;
+    if (!on) return;
+    const cudaError_t e = cudaStreamSynchronize(st);
+    fprintf(stderr, "[ebr] %s: %s\n", what, cudaGetErrorString(e));
+}
+
 struct Tuning {
     int n_hb, pieces;
 };
 
 static Tuning tuning(const ebr_index* idx) {
     Tuning t;
-    t.n_hb = std::min(1, idx->n_hot / 64);                  // 64 hot keys: 80 % of C3's hits
+    t.n_hb = std::min(kMaxHotBlocks, idx->n_hot / 64);     // up to 128 hot keys: 89 % of C3's hits
     t.pieces = 2;
     if (const char* e = getenv("EBR_HOT_BLOCKS")) t.n_hb = std::max(0, std::min(t.n_hb, atoi(e)));
     if (getenv("EBR_NO_HOT")) t.n_hb = 0;                 // every key through the compressed lists
@@ -1023,9 +1207,8 @@ static Tuning tuning(const ebr_index* idx) {
     return t;
 }
 
-static size_t gemm_smem(int u_blocks, int stages) {
-    return 1024 + (size_t)(u_blocks + stages) * kBlockBytes + (size_t)kTileM * kAccPitch * 4 +
-           (size_t)(2 * stages + 3 * kAccStages + 1) * 8 + 16 + (size_t)kGroup * 20;
+static size_t gemm_smem(const Layout& L, int stages) {
+    return 1024 + score_smem_fixed(stages) + (size_t)(L.NU + 2) * 2 + (size_t)L.gcap * 4;
 }
 
 }  // namespace batch
@@ -1048,7 +1231,7 @@ size_t batch_workspace_bytes(const ebr_index* idx, int32_t slots, int32_t k) {
 
 int32_t batch_launches(const ebr_index* idx, int32_t batch, int32_t slots) {
     const int P = pass_users(idx, slots);
-    return ((batch + P - 1) / P) * 15;
+    return ((batch + P - 1) / P) * 13;
 }
 
 // The workspace passed here is the batched region (after the latency path's region).
@@ -1066,23 +1249,22 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
     cudaError_t e = cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, idx->device);
     if (e != cudaSuccess) return cuda_check(e, "attr(max smem)");
     // ring stages: >= one tile's K blocks (the hot block's writer waits on the ring, see
-    // score_kernel) plus one of lookahead; hot blocks are dropped until that fits
-    int stages = 0;
+    // score_kernel) plus one of lookahead; TMEM: the users' A operand (32 columns per 64 K) and
+    // >= 2 accumulator stages of 128 columns; hot blocks are dropped until both fit
+    int stages = 0, acc_stages = 0;
     for (; tu.n_hb >= 0; --tu.n_hb) {
-        const int ub = n_kb + tu.n_hb * tu.pieces, nkt = n_kb + tu.n_hb;
+        const int nkt = n_kb + tu.n_hb;
+        acc_stages = std::min(kMaxAccStages, (512 - 32 * (n_kb + tu.n_hb * tu.pieces)) / kTileM);
+        if (acc_stages < 2) continue;
         stages = 6;
-        while (stages > nkt + 1 && gemm_smem(ub, stages) > (size_t)max_smem) --stages;
-        if (gemm_smem(ub, stages) <= (size_t)max_smem) break;
+        while (stages > nkt + 1 && gemm_smem(L, stages) > (size_t)max_smem) --stages;
+        if (gemm_smem(L, stages) <= (size_t)max_smem) break;
     }
-    if (tu.n_hb < 0) return set_error(EBR_EUNSUPPORTED, "batched path: d=%d does not fit shared memory", idx->d);
-    const int u_blocks = n_kb + tu.n_hb * tu.pieces;
-    const size_t smem = gemm_smem(u_blocks, stages);
-    CUtensorMap tmA, tmU;
+    if (tu.n_hb < 0) return set_error(EBR_EUNSUPPORTED, "batched path: d=%d does not fit shared memory / TMEM", idx->d);
+    const size_t smem = gemm_smem(L, stages);
+    CUtensorMap tmA;
     if (!encode_2d_16(&tmA, idx->A, (uint64_t)idx->d_pad, (uint64_t)idx->n_pad, kBlockK, kTileM))
         return set_error(EBR_ECUDA, "cuTensorMapEncodeTiled(A) failed");
-    const int Ppad_max = (int)((L.P + kGroup - 1) / kGroup * kGroup);
-    if (!encode_2d_16(&tmU, ws.U, (uint64_t)u_cols, (uint64_t)Ppad_max, kBlockK, kGroup))
-        return set_error(EBR_ECUDA, "cuTensorMapEncodeTiled(U) failed");
     // kernel attributes: set once per process (values fixed by the build)
     static std::once_flag attr_once;
     static cudaError_t attr_err = cudaSuccess;
@@ -1096,8 +1278,7 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
         set((const void*)score_kernel<1>, big);
         set((const void*)theta_kernel, 200 * 1024);
         set((const void*)final_kernel, 200 * 1024);
-        set((const void*)entry_count_kernel, kRangeMaxTiles * kTileM * 4);
-        set((const void*)entry_write_kernel, kRangeMaxTiles * kTileM * 4);
+        set((const void*)entry_sort_kernel, (kBinMaxEntries + 4096 / kTileM * kCountClasses * kMaxCluster) * 4);
         for (const void* f : {(const void*)score_kernel<0>, (const void*)score_kernel<1>}) {
             cudaError_t x = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
             (void)x;
@@ -1117,14 +1298,16 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
     if (const char* c = getenv("EBR_TEST_CAND_CAP")) cap = std::min<int64_t>(cap, std::max(1, atoi(c)));
 
     EntryArgs ea;
-    ea.hdr = idx->chunk_hdr; ea.chunk_last = idx->chunk_last; ea.payload = idx->payload;
-    ea.n_ads = idx->n_ads; ea.n_pad = idx->n_pad; ea.range_ads = L.range_ads;
-    ea.n_ranges = (int)L.n_ranges; ea.n_tiles = n_tiles; ea.NU = L.NU;
-    const size_t rsmem = (size_t)L.range_ads * 4;
+    ea.hdr = idx->chunk_hdr; ea.payload = idx->payload;
+    ea.n_ads = idx->n_ads; ea.n_pad = idx->n_pad; ea.bin_ads = (int)L.bin_ads;
+    ea.n_bins = (int)L.n_bins; ea.n_tiles = n_tiles; ea.bin_cap = L.bin_cap;
+    const size_t ssmem = (size_t)(L.bin_cap + (L.bin_ads / kTileM) * kCountClasses * kMaxCluster) * 4;
+    ea.NU = (int)L.NU;
 
     for (int b0 = 0; b0 < q.batch; b0 += (int)L.P) {
         const int P = std::min((int)L.P, q.batch - b0);
         const int G = (P + kGroup - 1) / kGroup;
+        ea.G = G;
         PlanArgs pa;
         pa.user_feat = q.user_feat + (size_t)b0 * idx->n_fields * q.slots;
         pa.user_x = q.user_x + (size_t)b0 * idx->n_fields * q.slots;
@@ -1132,24 +1315,30 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
         pa.key_chunk_off = idx->key_chunk_off; pa.key_word_off = idx->key_word_off; pa.cross_w = idx->cross_w;
         pa.field_card = idx->field_card; pa.field_base = idx->field_base; pa.hot_slot = idx->hot_slot;
         pa.F = idx->n_fields; pa.S = q.slots; pa.P = P; pa.d = idx->d; pa.d_pad = idx->d_pad;
-        pa.n_hot_used = tu.n_hb * 64; pa.pieces = tu.pieces; pa.u_cols = u_cols; pa.TS = L.TS; pa.err = err_word;
+        pa.n_hot_used = tu.n_hb * 64; pa.pieces = tu.pieces; pa.u_cols = u_cols; pa.TS = L.TS; pa.NU = L.NU; pa.gcap = L.gcap; pa.err = err_word;
         const int nslot = P * idx->n_fields * q.slots;
         const int pgrid = std::max(1, std::min(4 * idx->sm_count, (nslot + 255) / 256));
         plan_a_kernel<<<pgrid, 256, 0, q.stream>>>(pa, ws);
+        trace(q.stream, "plan_a");
         plan_b_kernel<<<1, kPlanThreads, 0, q.stream>>>(pa, ws);
+        trace(q.stream, "plan_b");
         plan_c_kernel<<<std::max(pgrid, 2 * idx->sm_count), 256, 0, q.stream>>>(pa, ws);
-        span_kernel<<<(unsigned)((nslot + 7) / 8), 256, 0, q.stream>>>(ea, ws);
-        entry_count_kernel<<<(unsigned)L.n_ranges, 512, rsmem, q.stream>>>(ea, ws);
-        range_scan_kernel<<<1, 1024, 0, q.stream>>>(ea, ws);
-        entry_write_kernel<<<(unsigned)L.n_ranges, 512, rsmem, q.stream>>>(ea, ws);
+        trace(q.stream, "plan_c");
+        entry_bin_kernel<<<8 * idx->sm_count, 256, 0, q.stream>>>(ea, ws);
+        trace(q.stream, "entry_bin");
+        entry_sort_kernel<<<(unsigned)L.n_bins, 512, ssmem, q.stream>>>(ea, ws);
+        trace(q.stream, "entry_sort");
         e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_check(e, "launch(plan/entries)");
 
         GemmParams gp;
         gp.n_ads = idx->n_ads; gp.n_pad = idx->n_pad; gp.dense = 0; gp.ad_begin = (uint32_t)idx->ad_begin;
-        gp.n_kb = n_kb; gp.n_hb = tu.n_hb; gp.pieces = tu.pieces; gp.u_blocks = u_blocks;
+        gp.n_kb = n_kb; gp.n_hb = tu.n_hb; gp.pieces = tu.pieces; gp.acc_stages = acc_stages; gp.u_cols = u_cols;
         gp.P = P; gp.n_samp = (int)L.n_samp; gp.stages = stages; gp.cap = cap; gp.rerun = 0;
         gp.hot_mask = reinterpret_cast<const uint4*>(idx->hot_mask); gp.ws = ws; gp.err = err_word;
+        static const int diag = getenv("EBR_DIAG") ? atoi(getenv("EBR_DIAG")) : 0;
+        gp.diag = diag;
+        gp.NU = (int)L.NU; gp.gcap = (int)L.gcap; gp.n_tiles_all = n_tiles;
         // the U tensor map covers the whole pass tile: each CTA loads its group's 128 rows
         auto launch_score = [&](int mode, int tiles, int stride, int rerun, int dense = 0) -> cudaError_t {
             gp.n_tiles = tiles; gp.tile_stride = stride; gp.rerun = rerun; gp.dense = dense;
@@ -1181,28 +1370,48 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
             }
             ncl = std::max(1, std::min(ncl, tiles));
             cfg.gridDim = dim3((unsigned)(G * ncl));
-            return mode ? cudaLaunchKernelEx(&cfg, score_kernel<1>, tmA, tmU, gp)
-                        : cudaLaunchKernelEx(&cfg, score_kernel<0>, tmA, tmU, gp);
+            return mode ? cudaLaunchKernelEx(&cfg, score_kernel<1>, tmA, gp)
+                        : cudaLaunchKernelEx(&cfg, score_kernel<0>, tmA, gp);
         };
         int32_t* oi = q.out_ids ? q.out_ids + (size_t)b0 * q.k : nullptr;
         float* os = q.out_scores ? q.out_scores + (size_t)b0 * q.k : nullptr;
         uint64_t* ok = q.out_keys ? q.out_keys + (size_t)b0 * q.k : nullptr;
         e = launch_score(0, n_samp_tiles, kSampleStride, 0);
         if (e != cudaSuccess) return cuda_check(e, "launch(score sample)");
+        trace(q.stream, "score sample");
         theta_kernel<<<P, kThetaThreads, tsmem, q.stream>>>(ws, (int)L.n_samp, rank, (uint32_t)idx->ad_begin, P,
                                                            tscap_of(rank), 0, idx->n_pad);
+        trace(q.stream, "theta");
         e = launch_score(1, n_tiles, 1, 0);
         if (e != cudaSuccess) return cuda_check(e, "launch(score filter)");
+        trace(q.stream, "score filter");
+        if (diag & 4) {
+            unsigned long long h[32];
+            cudaMemcpyAsync(h, ws.prof, sizeof h, cudaMemcpyDeviceToHost, q.stream);
+            cudaStreamSynchronize(q.stream);
+            const double c = h[9] ? (double)h[9] : 1.0;
+            fprintf(stderr, "[ebr prof] per CTA Mcycles (sample+filter): total %.2f tma_wait_empty %.2f mma_wait_wready %.2f "
+                            "mma_wait_full %.2f hot_wait_empty %.2f wide_cold %.2f wide_wait_tempty %.2f wide_store %.2f "
+                            "epi_wait_tfull %.2f epi_work %.2f (CTAs %llu)\n",
+                    h[10] / c / 1e6, h[0] / c / 1e6, h[1] / c / 1e6, h[2] / c / 1e6, h[3] / c / 1e6, h[4] / c / 1e6,
+                    h[5] / c / 1e6, h[6] / c / 1e6, h[7] / c / 1e6, h[8] / c / 1e6, h[9]);
+            cudaMemsetAsync(ws.prof, 0, sizeof h, q.stream);
+        }
         final_kernel<<<P, 512, fsmem, q.stream>>>(ws, cap, q.k, P, oi, os, ok, fscap, 0, rank, err_word);
+        trace(q.stream, "final");
         // gated reruns (exact either way): the overflowed users' scores densely, then theta at rank
         // K for the users short of K candidates (sample) or overflowed (dense), filter, select
         e = launch_score(0, n_tiles, 1, 0, 1);
         if (e != cudaSuccess) return cuda_check(e, "launch(score dense)");
+        trace(q.stream, "score dense");
         theta_kernel<<<P, kThetaThreads, tsmem, q.stream>>>(ws, (int)L.n_samp, q.k, (uint32_t)idx->ad_begin, P,
                                                            tscap_of(q.k), 1, idx->n_pad);
+        trace(q.stream, "theta rerun");
         e = launch_score(1, n_tiles, 1, 1);
         if (e != cudaSuccess) return cuda_check(e, "launch(score rerun)");
+        trace(q.stream, "score rerun");
         final_kernel<<<P, 512, fsmem, q.stream>>>(ws, cap, q.k, P, oi, os, ok, fscap, 1, q.k, err_word);
+        trace(q.stream, "final rerun");
         e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_check(e, "launch(batch)");
     }

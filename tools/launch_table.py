@@ -1,5 +1,7 @@
-"""Summarise an ncu --metrics gpu__time_duration.sum --csv launch list: per-kernel count/avg/share."""
-import csv, sys
+"""Summarise an ncu --csv launch list: per kernel the launch count, average duration, share of the
+summed duration and (when captured) average DRAM bytes read + written per launch."""
+import csv
+import sys
 
 rows = list(csv.reader(open(sys.argv[1])))
 h, agg = None, {}
@@ -9,8 +11,16 @@ for r in rows:
         continue
     if h and len(r) == len(h):
         d = dict(zip(h, r))
-        if d.get("Metric Name") == "gpu__time_duration.sum":
-            agg.setdefault(d["Kernel Name"][:70], []).append(float(d["Metric Value"]))
-tot = sum(sum(v) for v in agg.values())
-for k, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
-    print(f"{len(v):5d} launches  avg {sum(v)/len(v)/1e3:10.1f} us  share {100*sum(v)/tot:5.1f}%  {k}")
+        k = (d["Kernel Name"][:70], d.get("ID", ""))
+        agg.setdefault(k, {})[d.get("Metric Name")] = float(d["Metric Value"].replace(",", ""))
+per = {}
+for (name, _), m in agg.items():
+    e = per.setdefault(name, {"n": 0, "t": 0.0, "b": 0.0})
+    e["n"] += 1
+    e["t"] += m.get("gpu__time_duration.sum", 0.0)
+    e["b"] += m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
+tot = sum(e["t"] for e in per.values()) or 1.0
+for name, e in sorted(per.items(), key=lambda x: -x[1]["t"]):
+    n = e["n"]
+    print(f"{n:5d} launches  avg {e['t'] / n / 1e3:10.1f} us  share {100 * e['t'] / tot:5.1f}%  "
+          f"dram/launch {e['b'] / n / 1e6:9.1f} MB  {name}")
