@@ -62,7 +62,7 @@ constexpr int kMaxHotBlocks = 2;     // hot K blocks of 64 keys (the index keeps
 constexpr int kPairUBits = 7;        // cold pair = w~ 2^S (25-bit two's complement) << 7 | user in the group
 constexpr int kPairWMax = 24;        // |w~ 2^S| < 2^24
 constexpr int kMaxUnion = 1 << 15;   // union key slots per pass (15 bits in the level-1 bin entries)
-constexpr int kBinMaxEntries = 32768; // entry bin: worst case (bin ads x F) sorted in 128 KB of smem
+constexpr int kBinAdsMax = 1024;     // ads per entry bin (8 tiles; 10 bits of the bin entry)
 constexpr int kPlanThreads = 1024;
 constexpr uint32_t kFlagShort = 1u, kFlagOverflow = 2u, kFlagRaise = 4u;   // uflags; overflow users carry their dense slot << 8
 constexpr uint32_t kFlagAny = kFlagShort | kFlagOverflow | kFlagRaise;
@@ -98,6 +98,7 @@ struct Ws {
     uint32_t* uc1;        // [NU] end chunk
     uint32_t* ukwb;       // [NU] payload word base
     uint16_t* toff;       // [kMaxCluster][NU + 1] first pair of union slot s in group g's list (u16)
+    uint32_t* ucls;       // [NU] per group g, 3 bits at 3g: 0 = no user of g, else min(pairs, 7)
     uint32_t* pairs;      // [kMaxCluster][kGroup * F * S] each group's pairs, by union slot
     uint16_t* U;          // [P_pad][u_cols] deep bf16 | hot fp16 pieces
     uint32_t* uchunk;     // [NU + 1] exclusive scan of the union keys' chunk counts
@@ -154,7 +155,7 @@ static Layout layout(const ebr_index* idx, int32_t slots, int32_t k) {
     L.n_samp = ((L.n_tiles + kSampleStride - 1) / kSampleStride) * kTileM;
     L.cap = cand_cap(k);
     // entry bins: as many ads as keep a bin's worst case (bin_ads * F entries) in 128 KB of smem
-    L.bin_ads = std::max<int64_t>(kTileM, std::min<int64_t>(4096, (kBinMaxEntries / std::max(1, idx->n_fields)) / kTileM * kTileM));
+    L.bin_ads = kBinAdsMax;
     L.bin_cap = L.bin_ads * idx->n_fields;
     L.n_bins = (idx->n_pad + L.bin_ads - 1) / L.bin_ads;
     // group streams: an (ad, key) entry appears once per group querying the key, so at most
@@ -169,7 +170,7 @@ static Layout layout(const ebr_index* idx, int32_t slots, int32_t k) {
         (size_t)Ppad * 128 * 4,                     // 7 hotw
         (size_t)P * 4, (size_t)P * 4, (size_t)P * 4, (size_t)P * 4,   // 8-11 per user
         (size_t)L.NU * 4, (size_t)L.NU * 4, (size_t)L.NU * 4, (size_t)L.NU * 4,   // 12-15 union
-        (size_t)kMaxCluster * (L.NU + 1) * 2,       // 16 toff
+        (((size_t)kMaxCluster * (L.NU + 1) * 2 + 15) & ~(size_t)15) + (size_t)L.NU * 4,   // 16 toff | ucls
         (size_t)kMaxCluster * L.gcap * 4,           // 17 pairs
         (size_t)Ppad * L.u_cols * 2,                // 18 U
         (size_t)(L.NU + 1) * 4,                     // 19 uchunk
@@ -203,6 +204,7 @@ static Ws carve(char* b, const Layout& L) {
     w.bound = (float*)at(8); w.emax = (uint32_t*)at(9); w.ushift = (int32_t*)at(10); w.uscale = (float*)at(11);
     w.ukey = (uint32_t*)at(12); w.uc0 = (uint32_t*)at(13); w.uc1 = (uint32_t*)at(14); w.ukwb = (uint32_t*)at(15);
     w.toff = (uint16_t*)at(16); w.pairs = (uint32_t*)at(17);
+    w.ucls = reinterpret_cast<uint32_t*>(at(16) + (((size_t)kMaxCluster * (L.NU + 1) * 2 + 15) & ~(size_t)15));
     w.U = (uint16_t*)at(18);
     w.uchunk = (uint32_t*)at(19);
     w.bin_cnt = (uint32_t*)at(20);
@@ -340,11 +342,15 @@ __global__ void __launch_bounds__(kPlanThreads) plan_b_kernel(PlanArgs a, Ws ws)
         ws.uc1[sl] = c1;
         ws.ukwb[sl] = a.key_word_off[key];
         ws.uchunk[sl] = base[1];
+        uint32_t cls = 0;
         for (int g = 0; g < kMaxCluster; ++g) {
+            const uint32_t c = ws.hcnt[t * kMaxCluster + g];
             ws.toff[(size_t)g * (a.NU + 1) + sl] = (uint16_t)base[2 + g];
             ws.hpair[t * kMaxCluster + g] = base[2 + g];
-            base[2 + g] += ws.hcnt[t * kMaxCluster + g];
+            base[2 + g] += c;
+            cls |= min(c, 7u) << (3 * g);
         }
+        ws.ucls[sl] = cls;
         base[0] += 1u;
         base[1] += c1 - c0;
         ws.hkey[t] = 0u;
@@ -429,56 +435,64 @@ struct EntryArgs {
     int NU;                 // union slot capacity (toff row length - 1)
 };
 
+// Work item = 16 consecutive chunks of the union (in slot order); each key's part is decoded by
+// decode_unit16_warp (all headers, then all payload words in flight: two memory round trips per
+// item).  Bin entry = ad in bin << 21 | the slot's group classes << 15 | slot.
+constexpr int kBinEntryAdShift = 21;
 __global__ void __launch_bounds__(256) entry_bin_kernel(EntryArgs e, Ws ws) {
     const int lane = threadIdx.x & 31;
     const uint32_t nu = __ldcg(&ws.header[0]), total = __ldcg(&ws.header[5]);
-    const uint32_t n_items = (total + 31) / 32;
+    const uint32_t n_items = (total + 15) / 16;
     const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
     const uint32_t R = (uint32_t)e.bin_ads;
     for (uint32_t item = gw; item < n_items; item += nw) {
-        const uint32_t g0 = item * 32;
+        uint32_t g0 = item * 16;
+        const uint32_t gend = min(total, g0 + 16);
         // the key holding chunk g0: last s with uchunk[s] <= g0 (warp 32-ary search)
-        uint32_t lo = 0, hi = nu;                 // answer in [lo, hi)
+        uint32_t lo = 0, hi = nu;
         while (hi - lo > 1) {
             const uint32_t step = (hi - lo + 31) / 32;
             const uint32_t pidx = lo + lane * step;
             const bool le = pidx < hi && __ldcg(&ws.uchunk[pidx]) <= g0;
-            const uint32_t cntle = __popc(__ballot_sync(FULL, le));   // lanes 0..cntle-1 have uchunk <= g0
+            const uint32_t cntle = __popc(__ballot_sync(FULL, le));
             const uint32_t nlo = lo + (cntle - 1) * step;
             hi = min(hi, nlo + step);
             lo = nlo;
         }
-        uint32_t s = lo;
-        uint32_t s_end = __ldcg(&ws.uchunk[s + 1]);
-        const uint32_t gend = min(total, g0 + 32);
-        for (uint32_t gi = g0; gi < gend; ++gi) {
-            while (gi >= s_end) { ++s; s_end = __ldcg(&ws.uchunk[s + 1]); }
-            const uint32_t c = __ldcg(&ws.uc0[s]) + (gi - __ldcg(&ws.uchunk[s]));
-            uint32_t id;
-            const bool ok = decode_chunk(e.hdr, e.payload, __ldcg(&ws.ukwb[s]), c, lane, id);
-            const uint32_t r = ok ? id / R : 0xFFFFFFFFu;
-            const unsigned act = __ballot_sync(FULL, ok);
-            if (ok) {
-                const unsigned peers = __match_any_sync(act, r);
-                const int leader = __ffs(peers) - 1;
-                uint32_t base = 0;
-                if (lane == leader) base = atomicAdd(&ws.bin_cnt[r], (uint32_t)__popc(peers));
-                base = __shfl_sync(peers, base, leader);
-                const uint32_t pos = base + __popc(peers & ((1u << lane) - 1u));
-                ws.entries[(size_t)r * e.bin_cap + pos] = ((id - r * R) << 15) | s;   // s < 2^15
-            }
+        for (uint32_t s = lo; g0 < gend; ++s) {
+            const uint32_t s_beg = __ldcg(&ws.uchunk[s]), s_end = __ldcg(&ws.uchunk[s + 1]);
+            const uint32_t sub_end = min(gend, s_end);
+            const uint32_t c0 = __ldcg(&ws.uc0[s]) + (g0 - s_beg);
+            const uint32_t tag = (__ldcg(&ws.ucls[s]) << 15) | s;
+            decode_unit16_warp(e.hdr, e.payload, __ldcg(&ws.ukwb[s]), c0, c0 + (sub_end - g0), lane,
+                               [&](uint32_t id, bool ok) {
+                const uint32_t r = ok ? id / R : 0xFFFFFFFFu;
+                const unsigned act = __ballot_sync(FULL, ok);
+                if (ok) {
+                    const unsigned peers = __match_any_sync(act, r);
+                    const int leader = __ffs(peers) - 1;
+                    uint32_t base = 0;
+                    if (lane == leader) base = atomicAdd(&ws.bin_cnt[r], (uint32_t)__popc(peers));
+                    base = __shfl_sync(peers, base, leader);
+                    const uint32_t pos = base + __popc(peers & ((1u << lane) - 1u));
+                    ws.entries[(size_t)r * e.bin_cap + pos] = ((id - r * R) << kBinEntryAdShift) | tag;
+                }
+            });
+            g0 = sub_end;
         }
     }
 }
 
-// Level 2: CTA = bin.  Every bin entry (ad, union slot) is expanded to the streams of the groups
-// whose users query the slot; each group's part of the bin is ordered by (tile, pair-count class)
-// so a warp's consecutive entries carry similar work in the fused kernel.
-constexpr int kCountClasses = 8;
+// Level 2: CTA = bin.  Every bin entry (ad, group classes, union slot) is expanded to the streams
+// of the groups whose users query the slot; each group's part of the bin is ordered by (tile,
+// pair-count class) so a warp's consecutive entries carry similar work in the fused kernel.  The
+// bin is staged in shared memory when it fits (the common case), else read twice from L2.
+constexpr int kCountClasses = 7;
+constexpr int kSortStage = 16384;    // bin entries staged in shared memory (64 KB)
 __global__ void __launch_bounds__(512) entry_sort_kernel(EntryArgs e, Ws ws) {
     extern __shared__ uint32_t smem_u[];
-    uint32_t* buf = smem_u;                               // [bin_cap]
-    uint32_t* off = smem_u + e.bin_cap;                   // [G][tiles_per_bin * kCountClasses]
+    uint32_t* off = smem_u;                               // [G][tiles_per_bin * kCountClasses]
+    uint32_t* buf = smem_u + kMaxCluster * (kBinAdsMax / kTileM) * kCountClasses;   // [kSortStage]
     __shared__ uint32_t sN, sBase[kMaxCluster];
     const int r = blockIdx.x, tid = threadIdx.x;
     const int tpb = e.bin_ads / kTileM, nb = tpb * kCountClasses, G = e.G;
@@ -486,17 +500,15 @@ __global__ void __launch_bounds__(512) entry_sort_kernel(EntryArgs e, Ws ws) {
     for (int i = tid; i < G * nb; i += 512) off[i] = 0;
     __syncthreads();
     const uint32_t n = sN;
+    const bool staged = n <= (uint32_t)kSortStage;
     const uint32_t* ent = ws.entries + (size_t)r * e.bin_cap;
-    const size_t trow = (size_t)e.NU + 1;
-    auto cls = [](uint32_t c) { return min(c, (uint32_t)kCountClasses) - 1u; };
     for (uint32_t i = tid; i < n; i += 512) {
         const uint32_t v = __ldcg(&ent[i]);
-        buf[i] = v;
-        const uint32_t a = v >> 15, sl = v & 0x7FFFu;
-        const uint32_t b = (a / kTileM) * kCountClasses;
+        if (staged) buf[i] = v;
+        const uint32_t b = ((v >> kBinEntryAdShift) / kTileM) * kCountClasses;
         for (int g = 0; g < G; ++g) {
-            const uint32_t c = (uint32_t)__ldg(&ws.toff[g * trow + sl + 1]) - __ldg(&ws.toff[g * trow + sl]);
-            if (c) atomicAdd(&off[g * nb + b + cls(c)], 1u);
+            const uint32_t c = (v >> (15 + 3 * g)) & 7u;   // 0: no user of group g, else min(pairs, 7)
+            if (c) atomicAdd(&off[g * nb + b + c - 1], 1u);
         }
     }
     __syncthreads();
@@ -531,14 +543,14 @@ __global__ void __launch_bounds__(512) entry_sort_kernel(EntryArgs e, Ws ws) {
     }
     __syncthreads();
     for (uint32_t i = tid; i < n; i += 512) {
-        const uint32_t v = buf[i];
-        const uint32_t a = v >> 15, sl = v & 0x7FFFu;
+        const uint32_t v = staged ? buf[i] : __ldcg(&ent[i]);
+        const uint32_t a = v >> kBinEntryAdShift, sl = v & 0x7FFFu;
         const uint32_t b = (a / kTileM) * kCountClasses;
         const uint32_t out = ((a & (kTileM - 1)) << 24) | sl;
         for (int g = 0; g < G; ++g) {
-            const uint32_t c = (uint32_t)__ldg(&ws.toff[g * trow + sl + 1]) - __ldg(&ws.toff[g * trow + sl]);
+            const uint32_t c = (v >> (15 + 3 * g)) & 7u;
             if (c) {
-                const uint32_t pos = atomicAdd(&off[g * nb + b + cls(c)], 1u);
+                const uint32_t pos = atomicAdd(&off[g * nb + b + c - 1], 1u);
                 ws.gentries[sBase[g] + pos] = out;
             }
         }
@@ -1278,7 +1290,7 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
         set((const void*)score_kernel<1>, big);
         set((const void*)theta_kernel, 200 * 1024);
         set((const void*)final_kernel, 200 * 1024);
-        set((const void*)entry_sort_kernel, (kBinMaxEntries + 4096 / kTileM * kCountClasses * kMaxCluster) * 4);
+        set((const void*)entry_sort_kernel, (int)(((size_t)(kBinAdsMax / kTileM) * kCountClasses * kMaxCluster + kSortStage) * 4));
         for (const void* f : {(const void*)score_kernel<0>, (const void*)score_kernel<1>}) {
             cudaError_t x = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
             (void)x;
@@ -1301,7 +1313,7 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
     ea.hdr = idx->chunk_hdr; ea.payload = idx->payload;
     ea.n_ads = idx->n_ads; ea.n_pad = idx->n_pad; ea.bin_ads = (int)L.bin_ads;
     ea.n_bins = (int)L.n_bins; ea.n_tiles = n_tiles; ea.bin_cap = L.bin_cap;
-    const size_t ssmem = (size_t)(L.bin_cap + (L.bin_ads / kTileM) * kCountClasses * kMaxCluster) * 4;
+    const size_t ssmem = ((size_t)(kBinAdsMax / kTileM) * kCountClasses * kMaxCluster + kSortStage) * 4;
     ea.NU = (int)L.NU;
 
     for (int b0 = 0; b0 < q.batch; b0 += (int)L.P) {

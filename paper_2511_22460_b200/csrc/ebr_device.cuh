@@ -148,6 +148,58 @@ __device__ __forceinline__ void decode_unit16(const uint2* __restrict__ hdr,
     }
 }
 
+// decode_unit16 for warp-collective consumers: f(id, ok) is called on EVERY lane for each chunk
+// (ok = the lane holds a posting), so f may use __match_any_sync / __shfl_sync over the full warp.
+template <typename F>
+__device__ __forceinline__ void decode_unit16_warp(const uint2* __restrict__ hdr,
+                                                   const uint32_t* __restrict__ payload, uint32_t kwb,
+                                                   uint32_t cb, uint32_t ce, int lane, F f) {
+    const uint32_t nc = ce - cb;
+    uint2 h = make_uint2(0u, 0u);
+    if ((uint32_t)lane < nc) h = __ldg(&hdr[cb + lane]);
+    uint32_t lo[16], hi[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        lo[q] = 0u;
+        hi[q] = 0u;
+        if ((uint32_t)q >= nc) break;                // warp-uniform
+        const uint32_t meta = __shfl_sync(FULL, h.y, q);
+        const uint32_t n = (meta & 31u) + 1u, b = (meta >> 5) & 31u;
+        if (lane >= 1 && (uint32_t)lane < n && b) {
+            const uint32_t bit = (uint32_t)(lane - 1) * b;
+            const uint32_t w = kwb + (meta >> 10) + (bit >> 5);
+            lo[q] = __ldg(&payload[w]);
+            hi[q] = __ldg(&payload[w + 1]);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        if ((uint32_t)q >= nc) break;
+        const uint32_t meta = __shfl_sync(FULL, h.y, q);
+        const uint32_t first = __shfl_sync(FULL, h.x, q);
+        const uint32_t n = (meta & 31u) + 1u, b = (meta >> 5) & 31u;
+        uint32_t g;
+        if (lane == 0) {
+            g = first;
+        } else if ((uint32_t)lane < n) {
+            uint32_t v = 0u;
+            if (b) {
+                const uint32_t bit = (uint32_t)(lane - 1) * b;
+                v = (uint32_t)(((((uint64_t)hi[q]) << 32) | lo[q]) >> (bit & 31u)) & ((1u << b) - 1u);
+            }
+            g = v + 1u;
+        } else {
+            g = 0u;
+        }
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(FULL, g, o);
+            if (lane >= o) g += t;
+        }
+        f(g, (uint32_t)lane < n);
+    }
+}
+
 // Block-wide exclusive scan of one value per thread (blockDim.x <= 1024); returns the prefix and
 // writes the total to *total.  `scratch` holds >= 33 words.  Contains __syncthreads().
 __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* scratch, uint32_t* total) {
