@@ -6,10 +6,16 @@ inverted list + deep dual-tower inner product + fused top-K), i.e. every SURVEY.
 for N > 1 GPUs the inventory is sharded by ad range (strong scaling of a fixed inventory) and
 each step adds the NCCL all-gather of the per-shard top-K keys and the merge kernel.
 
-Default workload: BASELINE.json config 2 ("1M ads, d=64, 32 cross features, batch 1, K=500 on
-1 B200 (latency path)").  Prints ONE JSON line on rank 0.
+Default workload: BASELINE.json config 3 ("10M ads, d=128 bf16, 32 cross features, batch 256,
+K=1000 sharded over 8 B200") -- the north star's "10M-ad batched scorer"; at --gpus 1 it is the
+N=1 point of that strong-scaling curve.  C2 (the latency path) and the others via --config.
+Prints ONE JSON line on rank 0.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+
+--gpus N > 1 without torchrun's environment re-executes itself under
+`python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1`.
+--dry-run starts the ranks on CPU (gloo) and checks the sharding/gather plumbing only.
 """
 from __future__ import annotations
 
@@ -32,9 +38,11 @@ from paper_2511_22460_b200 import synth  # noqa: E402
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--steps", type=int, default=None, help="default: 100 (batched configs), 2000 (C1/C2)")
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU/gloo: start the ranks, shard, all-gather; no GPU work (plumbing check)")
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--mode", default="real")
@@ -42,18 +50,69 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="few steps, no side measurements (for ncu)")
     ap.add_argument("--graph", action="store_true",
-                    help="replay a CUDA graph of the library call each step (latency path, 1 GPU); measured "
-                         "no faster than the direct call (profiles/r01_mb_launch.txt), so off by default")
-    return ap.parse_args()
+                    help="replay a CUDA graph of the library call each step (1 GPU; both paths are "
+                         "host-sync free and capturable)")
+    a = ap.parse_args()
+    if a.steps is None:
+        a.steps = 2000 if a.config in ("C1", "C2") else 100
+    return a
 
 
-def peaks():
+def maybe_spawn(args) -> bool:
+    """--gpus N > 1 started as a plain process: re-run this command under torchrun (one rank per
+    GPU, rendezvous on 127.0.0.1) and return True once it finished (the exit code is forwarded)."""
+    if args.gpus <= 1 or "RANK" in os.environ:
+        return False
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    rc = subprocess.call(cmd)
+    if rc:
+        sys.exit(rc)
+    return True
+
+
+def cpu_model() -> str:
     try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            p = json.load(f)
-        return float(p["hbm_gbs"]), "measured"
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
     except Exception:
-        return 6650.0, "fallback"
+        pass
+    return "unknown"
+
+
+def dry_run(args, cfg, rank, world):
+    """Plumbing check without a GPU: gloo process group, this rank's shard range, one all-gather of
+    per-rank [B][K] int64 payloads shaped like the top-K keys; rank 0 prints one JSON line."""
+    import torch
+    import torch.distributed as dist
+    from paper_2511_22460_b200.dist import gather_keys, shard_range
+    if world > 1:
+        dist.init_process_group("gloo")
+    B = args.batch or cfg.batch
+    K = args.k or cfg.k
+    lo, hi = shard_range(cfg.n_ads, world, rank)
+    local = torch.full((B, K), rank, dtype=torch.int64)
+    local[:, 0] = lo
+    local[:, 1] = hi
+    g = gather_keys(local) if world > 1 else local[None]
+    ranges = [(int(g[r, 0, 0]), int(g[r, 0, 1])) for r in range(world)]
+    ok = (ranges[0][0] == 0 and ranges[-1][1] == cfg.n_ads and
+          all(ranges[r][1] == ranges[r + 1][0] for r in range(world - 1)) and
+          all(int(g[r, 0, 2]) == r for r in range(world)) if K > 2 else True)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "backend": "gloo" if world > 1 else "none",
+                          "config": config_dict(cfg, B, K, world), "shards": ranges, "gather_ok": bool(ok)}),
+              flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    if not ok:
+        sys.exit(1)
 
 
 class Clocks:
@@ -115,30 +174,56 @@ class Clocks:
                 "samples": len(sm)}
 
 
-def algorithmic_bytes(ebr, inv, users, idx_stats, lo, hi):
-    """N_s*d*e (embeddings, once) + P_U (encoded postings of the batch's
-    distinct keys in the shard: 8-byte chunk headers + payload words) + inputs + outputs."""
+def peaks_all():
+    """MEASURED_PEAKS.json (driver-written): HBM GB/s, bf16 TFLOP/s burst and sustained."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return {"hbm": float(p["hbm_gbs"]), "tc_burst": float(p["bf16_tflops"]),
+                "tc_sustained": float(p.get("bf16_tflops_sustained", p["bf16_tflops"])), "kind": "measured"}
+    except Exception:   # B200_PROFILING.md fallbacks
+        return {"hbm": 6650.0, "tc_burst": 1620.0, "tc_sustained": 1370.0, "kind": "fallback"}
+
+
+def r_scatter():
+    """Measured shared-memory integer red.add rate (hits/s over the GPU) from tools/mb_units.cu
+    (profiles/r_scatter.json), the ALU bound of the wide scatter."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r_scatter.json")) as f:
+            r = json.load(f)
+        return float(r["hits_per_s"]), r.get("source", "profiles/r_scatter.json")
+    except Exception:
+        return None, "unmeasured"
+
+
+def work_model(ebr, inv, users, idx_stats, lo, hi, K):
+    """SURVEY.md §8(d) algorithmic work of one step on this shard:
+    bytes = N_s*d*e (embeddings, read once) + P_U (encoded postings of the batch's distinct keys:
+            8-byte chunk headers + payload words + 12 B of directory per key) + user inputs +
+            8*B*K output keys;
+    flops = 2*B*N_s*d;  hits = sum over users and their keys of |posting_k| inside the shard."""
     kco, kwo, hdr, pay = ebr.encode_host(inv.ad_feat[lo:hi], inv.field_card)
     base = np.concatenate([[0], np.cumsum(inv.field_card)[:-1]]).astype(np.int64)
     F, S = users.user_feat.shape[1:]
-    keys = set()
-    for b in range(users.batch):
-        for f in range(F):
-            for s in range(S):
-                v = users.user_feat[b, f, s]
-                if v >= 0:
-                    keys.add(int(base[f] + v))
-    keys = np.array(sorted(keys), np.int64)
-    nch = (kco[keys + 1].astype(np.int64) - kco[keys]).sum()
-    # payload words of a key = next key's word base - this one's (keys are laid out in order)
+    uf = users.user_feat.astype(np.int64)
+    keys_all = (uf + base[None, :, None])[uf >= 0]
+    keys = np.unique(keys_all)
+    plen = (kco[1:].astype(np.int64) - kco[:-1])          # chunks per key
+    nch = int(plen[keys].sum())
     wend = np.append(kwo.astype(np.int64), len(pay))
-    words = (wend[keys + 1] - wend[keys]).sum()
-    hits = 0
+    words = int((wend[keys + 1] - wend[keys]).sum())
+    # postings per key inside the shard (hits = sum over every user's keys)
+    af = inv.ad_feat[lo:hi].astype(np.int64)
+    cnt = np.bincount((af + base[None, :])[af >= 0], minlength=int(base[-1] + inv.field_card[-1]))
+    hits = int(cnt[keys_all].sum())
     esz = 2 if inv.dtype == "bf16" else 4
-    emb = (hi - lo) * idx_stats["d_pad"] * esz
-    postings = int(nch) * 8 + int(words) * 4 + len(keys) * 12
-    io = users.batch * (inv.d * esz + 8 * F * S)
-    return emb, postings, io
+    n_s = hi - lo
+    emb = n_s * inv.d * esz
+    postings = nch * 8 + words * 4 + len(keys) * 12
+    io = users.batch * (inv.d * esz + 8 * F * S) + 8 * users.batch * K
+    flops = 2.0 * users.batch * n_s * inv.d
+    return {"bytes": emb + postings + io, "emb_bytes": emb, "posting_bytes": postings, "io_bytes": io,
+            "flops": flops, "hits": hits, "hits_per_user_ad": hits / max(1, users.batch * n_s)}
 
 
 def run_reference(args, cfg, rank, world):
@@ -182,6 +267,7 @@ def run_reference(args, cfg, rank, world):
         "config": config_dict(cfg, B, K, world),
         "ads_scored_per_s": ads_s,
         "cpu_baseline": {"value": users_s, "unit": "users/s", "cores": nu, "kind": "oracle",
+                         "cpu_model": cpu_model(),
                          "sample": f"per step {nu} user(s) x the first {n_sub} of {inv.n_ads} ads "
                                    f"(rescaled by ads-scored/s); full-inventory single-thread "
                                    f"{per_user_full:.3f} s/user"},
@@ -217,14 +303,19 @@ def cpu_baseline(cfg, inv, users, K, budget_s=15.0):
     dt = time.perf_counter() - t
     return {"value": n / dt, "unit": "users/s", "cores": min(threads, n), "kind": "oracle",
             "sample": f"{n} users (drawn from the batch) x all {inv.n_ads} ads, brute-force sort",
-            "single_thread_s_per_user": one}
+            "single_thread_s_per_user": one, "cpu_model": cpu_model(), "host_cores": threads}
 
 
 def main():
     args = parse()
+    if maybe_spawn(args):
+        return
     cfg = synth.CONFIGS[args.config]
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.dry_run:
+        dry_run(args, cfg, rank, world)
+        return
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
         return
@@ -252,23 +343,20 @@ def main():
     feat = torch.from_numpy(users.user_feat).to(dev)
     x = torch.from_numpy(users.user_x).to(dev)
     S = users.slots
-    ws = shard.workspace(B, S, K)
     ids = torch.empty((B, K), dtype=torch.int32, device=dev)
     sc = torch.empty((B, K), dtype=torch.float32, device=dev)
     keys = torch.empty((B, K), dtype=torch.int64, device=dev)
     gathered = torch.empty((world, B, K), dtype=torch.int64, device=dev)
     flush = torch.ones(64 << 20, dtype=torch.float32, device=dev)   # 256 MiB, READ between steps
     flush_out = torch.empty((), dtype=torch.float32, device=dev)
+    shard.workspace(B, S, K)
 
     def call():
         shard.query(emb, feat, x, K, ids, sc, stream, local_keys=keys, gathered=gathered)
 
     step = call
-    # --graph (1 GPU, latency path): replay a CUDA graph of the library call (the same cooperative
-    # kernel, enqueued without the per-call host work).  The batched path synchronises once per
-    # call (overflow check) and is always launched directly.
-    use_graph = (world == 1 and args.graph
-                 and idx.query_launches(B, S, K) == (B + 3) // 4)
+    # --graph (1 GPU): replay a CUDA graph of the library call (no host work per step)
+    use_graph = world == 1 and args.graph
     for _ in range(max(args.warmup, 3)):
         call()
     torch.cuda.synchronize()
@@ -286,10 +374,12 @@ def main():
         torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
-    hbm_peak, peak_kind = peaks()
+    pk = peaks_all()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    ebr.kernel_timer_read()                 # drop anything recorded so far
+    ebr.kernel_timer(not use_graph)         # events around the dominant kernel of each step
     with Clocks(local) as clk:
         t0 = time.perf_counter()
         for i in range(args.steps):
@@ -301,6 +391,8 @@ def main():
                 ev[i][1].record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
+    ebr.kernel_timer(False)
+    k_ms, k_n, k_name = ebr.kernel_timer_read()
     if world > 1:
         dist.barrier()
     per = np.array([a.elapsed_time(b) for a, b in ev])        # ms, device side
@@ -313,19 +405,40 @@ def main():
     users_s = B * args.steps / (tot_ms / 1e3)
 
     line = None
-    batched = idx.query_launches(B, S, K) != (B + 3) // 4
-    kernel_label = ("whole batched step per 128-user group: plan, span, wide_smem, gemm_kernel<0> (sample), "
-                    "theta, gemm_kernel<1> (tcgen05 + fused filter), final -- timed as one" if batched else
-                    "small_kernel (fused plan+decode+wide+GEMV+fuse+top-K, 1 launch per <=4 users)")
+    n_launch = idx.query_launches(B, S, K)
+    batched = n_launch != (B + 3) // 4
     if rank == 0:
-        emb_b, post_b, io_b = algorithmic_bytes(ebr, inv, users, st, lo, hi)
-        alg = emb_b + post_b + io_b + 8 * B * K
-        achieved = alg / (ms_step / 1e3) / 1e9   # GB/s (per GPU: shard bytes / step time)
+        wm = work_model(ebr, inv, users, st, lo, hi, K)
+        rs, rs_src = r_scatter()
+        # T_roof = max(bytes/BW, flops/TC, hits/R_scatter); the kernel runs inside a
+        # long back-to-back step, so the tensor bound takes the SUSTAINED bf16 rate
+        tc_peak = pk["tc_sustained"] if inv.dtype == "bf16" else None
+        t_hbm = wm["bytes"] / (pk["hbm"] * 1e9)
+        t_tc = wm["flops"] / (tc_peak * 1e12) if tc_peak else 0.0
+        t_hits = wm["hits"] / rs if rs else 0.0
+        bounds = {"hbm": t_hbm, "tensor": t_tc, "alu": t_hits}
+        bound = max(bounds, key=bounds.get)
+        # the dominant kernel, timed live (CUDA events on the launching stream, ebr_kernel_timer)
+        k_avg_s = (k_ms / k_n / 1e3) if k_n else None
+        launches_per_step = max(1, k_n // args.steps) if k_n else 1
+        frac_work = 1.0 / launches_per_step        # each launch handles its share of the step
+        if bound == "tensor":
+            unit, peak = "TFLOP/s", tc_peak
+            alg = wm["flops"] * frac_work
+            achieved = alg / k_avg_s / 1e12 if k_avg_s else None
+        elif bound == "hbm":
+            unit, peak = "GB/s", pk["hbm"]
+            alg = wm["bytes"] * frac_work
+            achieved = alg / k_avg_s / 1e9 if k_avg_s else None
+        else:
+            unit, peak = "hits/s", rs
+            alg = wm["hits"] * frac_work
+            achieved = alg / k_avg_s if k_avg_s else None
         traffic = None
         try:
             with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
                 tr = json.load(f).get(cfg.name)
-            if tr and tr.get("world", 1) == world and tr.get("batch") == B:
+            if tr and tr.get("world", 1) == world and tr.get("batch") == B and tr.get("k", K) == K:
                 traffic = tr["dram_bytes_per_launch"]
         except Exception:
             pass
@@ -340,16 +453,23 @@ def main():
             "latency_us": {"p50": float(np.percentile(per, 50) * 1e3),
                            "p99": float(np.percentile(per, 99) * 1e3),
                            "min": float(per.min() * 1e3)},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved / hbm_peak, "traffic": traffic,
-                         "peak_kind": peak_kind,
-                         "kernel": kernel_label,
-                         "alg_bytes_per_launch": alg,
-                         "alg_bytes_split": {"embeddings": emb_b, "postings": post_b, "io": io_b + 8 * B * K}},
+            "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "peak_kind": pk["kind"] + (" sustained bf16" if bound == "tensor" else ""),
+                         "kernel": k_name, "kernel_ms": (k_avg_s * 1e3) if k_avg_s else None,
+                         "kernel_launches_timed": k_n,
+                         "kernel_share_of_step": (k_ms / tot_ms) if k_n and not world > 1 else None,
+                         "alg_per_launch": alg,
+                         "step_bounds_us": {k2: v * 1e6 for k2, v in bounds.items()},
+                         "step_frac_of_bound": bounds[bound] / (ms_step / 1e3),
+                         "work": wm, "r_scatter_hits_per_s": rs, "r_scatter_source": rs_src},
             "index": {"build_ms": st["build_ms"], "index_bytes": st["index_bytes"],
-                      "nnz": st["nnz"], "chunks": st["chunks"]},
+                      "hot_bytes": st.get("hot_bytes", 0), "emb_bytes": st["emb_bytes"],
+                      "device_bytes": st["index_bytes"] + st.get("hot_bytes", 0) + st["emb_bytes"],
+                      "nnz": st["nnz"], "chunks": st["chunks"], "n_hot": st.get("n_hot", 0)},
             "clocks": clk.summary(),
-            "gpu_launches": args.steps * (idx.query_launches(B, S, K) + (1 if world > 1 else 0)),
+            "gpu_launches": args.steps * (n_launch + (2 if world > 1 else 0)),
+            "path": "batched tcgen05" if batched else "latency (fused cooperative kernel)",
             "launch": "cuda_graph replay of the C-ABI call" if use_graph else "direct C-ABI call per step",
             "wall_s_timed_region": wall,
         }

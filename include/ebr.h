@@ -229,6 +229,18 @@ ebr_status ebr_encode_host(const int32_t *ad_feat, int64_t n_ads, int32_t n_fiel
  * 1 memset plus 7 launches per group of 128 users).  Excludes the rare overflow fallback. */
 int32_t ebr_query_launches(const ebr_index *idx, int32_t batch, int32_t slots, int32_t k);
 
+/*
+ * Dominant-kernel timer (measurement support for bench.py's roofline; off by default).  While
+ * enabled, every query records a CUDA event pair on its stream around its dominant kernel: the
+ * batched path's full filter pass of the fused tensor-core kernel (score_kernel<1>), the latency
+ * path's fused cooperative kernel.  Calls on a stream that is being captured into a CUDA graph
+ * record nothing.  ebr_kernel_timer_read() synchronises on the recorded events, returns their
+ * summed elapsed milliseconds and the number of timed launches, copies the kernel's name into
+ * `name` (host, name_cap bytes, may be NULL) and clears the record.  Host-synchronous.
+ */
+ebr_status ebr_kernel_timer(int32_t enable);
+ebr_status ebr_kernel_timer_read(double *total_ms, int64_t *launches, char *name, int32_t name_cap);
+
 /* Thread-local message describing the last failure of any ebr_* call on this thread. */
 const char *ebr_last_error(void);
 

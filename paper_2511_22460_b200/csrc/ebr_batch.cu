@@ -1394,7 +1394,10 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
         theta_kernel<<<P, kThetaThreads, tsmem, q.stream>>>(ws, (int)L.n_samp, rank, (uint32_t)idx->ad_begin, P,
                                                            tscap_of(rank), 0, idx->n_pad);
         trace(q.stream, "theta");
-        e = launch_score(1, n_tiles, 1, 0);
+        {
+            KernelTimer kt(q.stream, "score_kernel<1> (fused tcgen05 deep + hot + cold wide + kappa + theta filter)");
+            e = launch_score(1, n_tiles, 1, 0);
+        }
         if (e != cudaSuccess) return cuda_check(e, "launch(score filter)");
         trace(q.stream, "score filter");
         if (diag & 4) {

@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -38,6 +39,42 @@ ebr_status set_error(ebr_status st, const char* fmt, ...) {
 ebr_status cuda_check(cudaError_t e, const char* what) {
     if (e == cudaSuccess) return EBR_OK;
     return set_error(EBR_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+// ------------------------------------------------------------------------------------------
+// dominant-kernel timer
+// ------------------------------------------------------------------------------------------
+struct TimerState {
+    std::mutex mu;
+    std::atomic<bool> on{false};
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+    std::string name;
+};
+static TimerState& timer_state() {
+    static TimerState t;
+    return t;
+}
+
+KernelTimer::KernelTimer(cudaStream_t stream, const char* name) {
+    TimerState& t = timer_state();
+    if (!t.on.load(std::memory_order_relaxed)) return;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
+    if (cudaEventCreate(&a) != cudaSuccess) { a = nullptr; return; }
+    s = stream;
+    cudaEventRecord(a, s);
+    std::lock_guard<std::mutex> lk(t.mu);
+    t.name = name;
+}
+
+KernelTimer::~KernelTimer() {
+    if (!a) return;
+    cudaEvent_t b = nullptr;
+    if (cudaEventCreate(&b) != cudaSuccess) { cudaEventDestroy(a); return; }
+    cudaEventRecord(b, s);
+    TimerState& t = timer_state();
+    std::lock_guard<std::mutex> lk(t.mu);
+    t.ev.emplace_back(a, b);
 }
 
 #define EBR_CUDA(call)                                              \
@@ -377,6 +414,36 @@ using namespace ebr;
 extern "C" {
 
 const char* ebr_last_error(void) { return g_last_error.c_str(); }
+
+ebr_status ebr_kernel_timer(int32_t enable) {
+    timer_state().on.store(enable != 0);
+    return EBR_OK;
+}
+
+ebr_status ebr_kernel_timer_read(double* total_ms, int64_t* launches, char* name, int32_t name_cap) {
+    if (!total_ms || !launches) return set_error(EBR_EINVAL, "ebr_kernel_timer_read: null output");
+    TimerState& t = timer_state();
+    std::lock_guard<std::mutex> lk(t.mu);
+    double tot = 0.0;
+    ebr_status st = EBR_OK;
+    for (auto& p : t.ev) {
+        float ms = 0.f;
+        cudaError_t e = cudaEventSynchronize(p.second);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, p.first, p.second);
+        if (e != cudaSuccess && st == EBR_OK) st = cuda_check(e, "kernel timer");
+        tot += ms;
+        cudaEventDestroy(p.first);
+        cudaEventDestroy(p.second);
+    }
+    *total_ms = tot;
+    *launches = (int64_t)t.ev.size();
+    t.ev.clear();
+    if (name && name_cap > 0) {
+        strncpy(name, t.name.c_str(), (size_t)name_cap - 1);
+        name[name_cap - 1] = 0;
+    }
+    return st;
+}
 
 int32_t ebr_query_launches(const ebr_index* idx, int32_t batch, int32_t slots, int32_t k) {
     if (!idx || batch < 1 || slots < 1 || k < 1) return 0;

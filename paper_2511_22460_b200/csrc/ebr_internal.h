@@ -73,6 +73,16 @@ ebr_status run_merge(const uint64_t* gathered, int32_t G, int32_t batch, int32_t
 ebr_status run_debug_decode(const ebr_index* idx, int64_t key, int32_t* dev_out, int64_t cap,
                             cudaStream_t stream);
 ebr_status set_error(ebr_status st, const char* fmt, ...);
+
+// Dominant-kernel timer (ebr_kernel_timer*, measurement support): while enabled, a KernelTimer
+// scope records a CUDA event pair on `stream` around the launch it encloses (skipped while the
+// stream is being captured into a graph).
+struct KernelTimer {
+    cudaEvent_t a = nullptr;
+    cudaStream_t s = nullptr;
+    KernelTimer(cudaStream_t stream, const char* name);
+    ~KernelTimer();
+};
 ebr_status cuda_check(cudaError_t e, const char* what);
 
 }  // namespace ebr

@@ -171,7 +171,10 @@ ebr_status run_small(const QueryArgs& q, int b0, int B) {
     }
     const int grid = std::max(1, std::min<int>(std::max(p.n_ranges, B), occ * sms));
     void* args[] = {&p};
-    e = cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(kThreads), args, smem, q.stream);
+    {
+        KernelTimer kt(q.stream, "small_kernel (fused plan + decode + wide + GEMV + fuse + top-K)");
+        e = cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(kThreads), args, smem, q.stream);
+    }
     if (e != cudaSuccess) return cuda_check(e, "launch(small)");
     return EBR_OK;
 }

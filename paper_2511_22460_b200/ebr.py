@@ -47,6 +47,9 @@ EXPORTS = {
     "ebr_encode_host": (ctypes.c_int, [_P, _I64, _I32, _P, _I64, _P, _P, _P, _I64, _P, _I64,
                                        ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     "ebr_query_launches": (_I32, [_P, _I32, _I32, _I32]),
+    "ebr_kernel_timer": (ctypes.c_int, [_I32]),
+    "ebr_kernel_timer_read": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64),
+                                             ctypes.c_char_p, _I32]),
     "ebr_last_error": (ctypes.c_char_p, []),
     "ebr_version": (ctypes.c_char_p, []),
 }
@@ -68,6 +71,19 @@ def last_error() -> str:
 
 def version() -> str:
     return _lib.ebr_version().decode()
+
+
+def kernel_timer(enable: bool) -> None:
+    """Start/stop recording CUDA events around each query's dominant kernel (ebr.h)."""
+    _check(_lib.ebr_kernel_timer(1 if enable else 0), "ebr_kernel_timer")
+
+
+def kernel_timer_read() -> tuple[float, int, str]:
+    """(summed ms, timed launches, kernel name) of the recorded launches; clears the record."""
+    ms, n = ctypes.c_double(0.0), ctypes.c_int64(0)
+    name = ctypes.create_string_buffer(256)
+    _check(_lib.ebr_kernel_timer_read(ctypes.byref(ms), ctypes.byref(n), name, 256), "ebr_kernel_timer_read")
+    return ms.value, n.value, name.value.decode()
 
 
 def _check(st: int, where: str):

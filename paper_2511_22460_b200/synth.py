@@ -22,6 +22,8 @@ Recipe, shaped by the paper's wide 
 from __future__ import annotations
 
 import dataclasses
+import os
+
 import numpy as np
 
 SEED_BASE = 2511_22460
@@ -191,6 +193,17 @@ def make_config(cfg: Config | str, mode: str = "real", n_ads: int | None = None,
     n = cfg.n_ads if n_ads is None else n_ads
     b = cfg.batch if batch is None else batch
     base = SEED_BASE + 100 * cfg.cfg_id + 10_000 * seed_offset
-    inv = make_inventory(n, cfg.d, cfg.n_fields, cfg.alpha, cfg.dtype, mode, seed=base + 0)
+    cache = os.environ.get("EBR_SYNTH_CACHE")     # optional directory: reuse a generated inventory
+    path = os.path.join(cache, f"{cfg.name}_{n}_{mode}_{base}.npz") if cache else None
+    if path and os.path.exists(path):
+        z = np.load(path)
+        inv = Inventory(n, cfg.d, cfg.dtype, z["emb"], z["feat"], z["cards"], z["w"], int(z["seed"]))
+    else:
+        inv = make_inventory(n, cfg.d, cfg.n_fields, cfg.alpha, cfg.dtype, mode, seed=base + 0)
+        if path:
+            os.makedirs(cache, exist_ok=True)
+            np.savez(path + ".tmp.npz", emb=inv.ad_emb, feat=inv.ad_feat, cards=inv.field_card,
+                     w=inv.cross_w, seed=inv.perm_seed)
+            os.replace(path + ".tmp.npz", path)
     users = make_users(inv, b, cfg.slots, cfg.alpha, mode, seed=base + 1)
     return inv, users

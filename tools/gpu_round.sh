@@ -5,6 +5,7 @@
 #   launches:CFG ncu launch list (gpu__time_duration + dram bytes) of a short bench run
 #   full:CFG:K   ncu --set full of kernel regex K in a short bench run
 OUT=gpurun_out
+export EBR_SYNTH_CACHE=/tmp/ebr_synth
 mkdir -p $OUT
 for w in "$@"; do
   IFS=: read -r what cfg kern <<< "$w"
