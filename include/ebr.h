@@ -180,6 +180,30 @@ ebr_status ebr_merge_topk(const uint64_t *gathered, int32_t G, int32_t batch, in
                           int32_t *out_ids, float *out_scores, void *workspace,
                           size_t workspace_bytes, void *stream);
 
+/*
+ * Threshold exchange for large batch x k (reading R24), three async
+ * calls around two small collectives that replace the all-gather of G*batch*k keys:
+ *   1. ebr_exchange_kth: out_kq[b] = local_keys[b][ceil(k/G) - 1] (device, [batch] uint64) -- this
+ *      rank's ceil(k/G)-th key; all-gather it into kq_gathered [G][batch].
+ *   2. ebr_exchange_pack: theta_b = min_r kq_gathered[r][b] is a lower bound of user b's global
+ *      k-th key (every rank holds >= ceil(k/G) keys >= theta_b), and every global top-k key is
+ *      >= theta_b and in its rank's local top k.  Writes out_count[b] = #{local keys >= theta_b}
+ *      (device, [batch] uint32), out_off[0..batch] = their exclusive scan (out_off[batch] = total)
+ *      and the packed keys out_packed[out_off[b] + j] = local_keys[b][j] (device, >= batch*k).
+ *      All-gather the counts ([G][batch]) and the packed lists, each padded to the largest total.
+ *   3. ebr_merge_topk_packed: packed [G][stride] (rank r's list at r*stride), counts [G][batch]:
+ *      the global top k per user, exactly the single-GPU answer (kappa is unique).
+ * local_keys: device, [batch][k] descending kappa, padding 0 (ebr_score_topk_keys).  G in 1..16.
+ */
+ebr_status ebr_exchange_kth(const uint64_t *local_keys, int32_t batch, int32_t k, int32_t G,
+                            uint64_t *out_kq, void *stream);
+ebr_status ebr_exchange_pack(const uint64_t *local_keys, int32_t batch, int32_t k,
+                             const uint64_t *kq_gathered, int32_t G, uint32_t *out_count,
+                             uint32_t *out_off, uint64_t *out_packed, void *stream);
+ebr_status ebr_merge_topk_packed(const uint64_t *packed, int64_t stride, const uint32_t *counts,
+                                 int32_t G, int32_t batch, int32_t k, int32_t *out_ids,
+                                 float *out_scores, void *stream);
+
 /* ------------------------------------------------------------------------------------------ */
 /* Parity / introspection                                                                       */
 /* ------------------------------------------------------------------------------------------ */

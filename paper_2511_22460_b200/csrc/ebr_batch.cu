@@ -50,10 +50,10 @@ constexpr int kMaxCluster = 2;       // CTAs (user groups) per cluster: <= 256 u
 constexpr int kTileM = 128;          // ads per tile (UMMA M)
 constexpr int kBlockK = 64;          // 16-bit elements per 128-byte swizzle row
 constexpr int kBlockBytes = kTileM * 128;   // one ring stage: 128 rows x 128 B
-constexpr int kSampleStride = 16;    // every 16th tile is sampled for theta
-constexpr int kAccPitch = kGroup + 4;   // int32 words per fixed-point row (16-B row reads conflict-free)
+constexpr int kSampleStride = 16;    // every 16th tile (at least) is sampled for theta
+constexpr int kSampleStrideMax = 64; // ... and every 64th on large inventories (sample_stride())
 #ifndef EBR_WIDE_WARPS
-#define EBR_WIDE_WARPS 16
+#define EBR_WIDE_WARPS 8
 #endif
 constexpr int kWideWarp0 = 4, kWideWarps = EBR_WIDE_WARPS, kWideThreads = 32 * kWideWarps;
 constexpr int kEpiWarp0 = kWideWarp0 + kWideWarps, kEpiWarps = 8;
@@ -61,20 +61,35 @@ constexpr int kGemmThreads = 32 * (kEpiWarp0 + kEpiWarps);   // TMA, MMA, 2 hot,
 constexpr int kMaxHotBlocks = 2;     // hot K blocks of 64 keys (the index keeps up to 128 hot keys)
 constexpr int kPairUBits = 7;        // cold pair = w~ 2^S (25-bit two's complement) << 7 | user in the group
 constexpr int kPairWMax = 24;        // |w~ 2^S| < 2^24
-constexpr int kMaxUnion = 1 << 15;   // union key slots per pass (15 bits in the level-1 bin entries)
-constexpr int kBinAdsMax = 1024;     // ads per entry bin (8 tiles; 10 bits of the bin entry)
+constexpr int kMaxUnion = 1 << 14;   // union key slots per pass (14 bits in the level-1 bin entries)
+constexpr int kBinAdShift = 14;      // level-1 bin entry = ad in bin << 14 | union slot
+constexpr int kBinAds = 1024;        // ads per entry bin (8 tiles)
+constexpr int kOrderStage = 16384;   // bin entries staged in shared memory by entry_order (64 KB)
+constexpr int kQuarters = 4;         // 32-ad quarters of a tile (the cold ring's unit in score_kernel)
+constexpr int kInlinePairs = 4;      // pairs of an entry scattered by its own thread; the rest of a
+                                     // heavy entry goes to a shared list scattered by whole warps
+constexpr int kHeavyCap = 1024;      // heavy entries per quarter (shared list; overflow -> inline)
+constexpr int kOrderThreads = 512;
 constexpr int kPlanThreads = 1024;
 constexpr uint32_t kFlagShort = 1u, kFlagOverflow = 2u, kFlagRaise = 4u;   // uflags; overflow users carry their dense slot << 8
 constexpr uint32_t kFlagAny = kFlagShort | kFlagOverflow | kFlagRaise;
 constexpr int kMaxFallback = 2;      // overflowed users per pass recomputed exactly (dense scores)
 
 constexpr int kMaxAccStages = 3;
-// shared memory of the fused kernel: the ad/hot ring, the fixed-point cold tile [users][ads],
-// barriers, per-user scalars and the byte -> one-hot table, then the group's slot -> pair offsets
-// and its pairs
-__host__ __device__ constexpr size_t score_smem_fixed(int stages) {
-    return (size_t)stages * kBlockBytes + (size_t)kGroup * kAccPitch * 4 +
-           (size_t)(2 * stages + 3 * kMaxAccStages + 1) * 8 + 16 + (size_t)kGroup * 20 + 256 * 16;
+constexpr int kMaxStages = 8;        // deep A ring stages (16 KB each; as many as the shared memory allows)
+constexpr int kPrefetchTiles = 4;    // tiles of A prefetched into L2 ahead of the ring's TMA loads
+constexpr int kHotStages = 2;        // ring of on-chip generated one-hot K blocks
+constexpr int kColdQuarter = 32 * kGroup;   // int32 words of a cold quarter buffer [32 ads][128 users]
+constexpr int kEntBuf = 2048;        // entries of a tile staged in shared memory (bulk copy; the rest from L2)
+constexpr int kEntHdr = 16;          // words of an entry buffer's header (quarter bounds, copied count)
+// shared memory of the fused kernel next to the A ring and the pairs: the hot ring, the cold
+// quarter buffers, 2 entry buffers, the byte -> one-hot table, the heavy list, barriers and
+// per-user scalars
+__host__ __device__ constexpr size_t score_smem_fixed() {
+    return (size_t)kHotStages * kBlockBytes + (size_t)kQuarters * kColdQuarter * 4 + 2 * (size_t)(kEntBuf + kEntHdr) * 4 +
+           256 * 16 + (size_t)kHeavyCap * 4 + 16 +
+           (size_t)(2 * kMaxStages + 2 * kHotStages + 2 * kMaxAccStages + 2 * kQuarters + 4 + 1) * 8 + 16 +
+           (size_t)kGroup * 20;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -97,15 +112,15 @@ struct Ws {
     uint32_t* uc0;        // [NU] first chunk of the key
     uint32_t* uc1;        // [NU] end chunk
     uint32_t* ukwb;       // [NU] payload word base
-    uint16_t* toff;       // [kMaxCluster][NU + 1] first pair of union slot s in group g's list (u16)
-    uint32_t* ucls;       // [NU] per group g, 3 bits at 3g: 0 = no user of g, else min(pairs, 7)
+    uint32_t* pinfo;      // [kMaxCluster][NU] group g's pairs of union slot s: first pair << 8 | count (0: none)
     uint32_t* pairs;      // [kMaxCluster][kGroup * F * S] each group's pairs, by union slot
     uint16_t* U;          // [P_pad][u_cols] deep bf16 | hot fp16 pieces
     uint32_t* uchunk;     // [NU + 1] exclusive scan of the union keys' chunk counts
     uint32_t* bin_cnt;    // [n_bins] entries in each ad-range bin (left zero by entry_sort)
-    uint32_t* tile_beg;   // [kMaxCluster][n_tiles] first entry of each tile in group g's stream
-    uint32_t* tile_end;   // [kMaxCluster][n_tiles]
-    uint32_t* gentries;   // [pool] the groups' entry streams (bins claim their ranges)
+    uint32_t* qbeg;       // [kMaxCluster][n_tiles * 4] first entry of each tile quarter in group g's stream
+    uint32_t* qend;       // [kMaxCluster][n_tiles * 4]
+    uint32_t* gentries;   // [pool] the groups' entry streams (bins claim their ranges):
+                          //   ad row << 24 | first pair << 8 | pairs, ordered by (tile, quarter, class)
     uint32_t* entries;    // [n_bins][bin_cap] level-1 bins (bin_cap = bin_ads * F: an ad has <= F keys)
     float* samp;          // [P][n_samp]
     uint64_t* theta;      // [P]
@@ -119,7 +134,7 @@ struct Ws {
 struct Layout {
     size_t total;
     size_t off[32];
-    int64_t TS, NU, P, n_samp, cap, n_bins, bin_ads, bin_cap, n_tiles, u_cols, gcap, pool;
+    int64_t TS, NU, P, n_samp, cap, n_bins, bin_ads, bin_cap, n_tiles, u_cols, gcap, pool, sstride;
 };
 
 static int64_t pow2ceil64(int64_t x) {
@@ -128,16 +143,25 @@ static int64_t pow2ceil64(int64_t x) {
     return p;
 }
 
-// users per pass: <= kGroup * kMaxCluster, the union slots must fit 15 bits and a group's pairs
-// the u16 offsets
+// users per pass: <= kGroup * kMaxCluster, the union slots must fit 14 bits and a group's pairs
+// the 16-bit first-pair field of an entry
 int pass_users(const ebr_index* idx, int32_t slots) {
     const int64_t fs = (int64_t)idx->n_fields * slots;
     int64_t p = std::min<int64_t>(kGroup * kMaxCluster, kMaxUnion / std::max<int64_t>(fs, 1));
     if ((int64_t)kGroup * fs > 65535) p = 0;
-    // shared memory of the fused kernel: slot offsets (2 B x P F S) + a group's pairs (4 B x 128 F S)
-    // next to the fixed part and >= 4 ring stages
-    while (p > 32 && 1024 + score_smem_fixed(4) + 2 * (p * fs + 2) + 4 * (int64_t)kGroup * fs > 232448) p -= 32;
+    // shared memory of the fused kernel: >= one tile's deep K blocks + 1 of the A ring, the fixed
+    // part and a group's worst-case pairs (4 B x 128 F S)
+    const int64_t n_kb = (idx->d_pad + kBlockK - 1) / kBlockK;
+    if (1024 + (n_kb + 1) * kBlockBytes + (int64_t)score_smem_fixed() + 4 * (int64_t)kGroup * fs > 232448) p = 0;
     return (int)(p / 32 * 32);
+}
+
+// the sample covers every sstride-th tile: the largest power of two <= kSampleStrideMax that keeps
+// >= 4 max(K, 128) sampled ads (batch_eligible guarantees it for kSampleStride)
+static int64_t sample_stride(const ebr_index* idx, int k) {
+    int64_t st = kSampleStrideMax;
+    while (st > kSampleStride && idx->n_ads < 4 * st * std::max(k, kTileM)) st >>= 1;
+    return st;
 }
 
 static int64_t cand_cap(int k) {
@@ -152,10 +176,11 @@ static Layout layout(const ebr_index* idx, int32_t slots, int32_t k) {
     L.gcap = (int64_t)kGroup * idx->n_fields * slots;
     L.TS = pow2ceil64(2 * L.NU);
     L.n_tiles = idx->n_pad / kTileM;
-    L.n_samp = ((L.n_tiles + kSampleStride - 1) / kSampleStride) * kTileM;
+    L.sstride = sample_stride(idx, k);
+    L.n_samp = ((L.n_tiles + L.sstride - 1) / L.sstride) * kTileM;
     L.cap = cand_cap(k);
-    // entry bins: as many ads as keep a bin's worst case (bin_ads * F entries) in 128 KB of smem
-    L.bin_ads = kBinAdsMax;
+    // entry bins of kBinAds ads; a bin's worst case is bin_ads * F entries (an ad has <= F keys)
+    L.bin_ads = kBinAds;
     L.bin_cap = L.bin_ads * idx->n_fields;
     L.n_bins = (idx->n_pad + L.bin_ads - 1) / L.bin_ads;
     // group streams: an (ad, key) entry appears once per group querying the key, so at most
@@ -170,12 +195,12 @@ static Layout layout(const ebr_index* idx, int32_t slots, int32_t k) {
         (size_t)Ppad * 128 * 4,                     // 7 hotw
         (size_t)P * 4, (size_t)P * 4, (size_t)P * 4, (size_t)P * 4,   // 8-11 per user
         (size_t)L.NU * 4, (size_t)L.NU * 4, (size_t)L.NU * 4, (size_t)L.NU * 4,   // 12-15 union
-        (((size_t)kMaxCluster * (L.NU + 1) * 2 + 15) & ~(size_t)15) + (size_t)L.NU * 4,   // 16 toff | ucls
+        (size_t)kMaxCluster * L.NU * 4,             // 16 pinfo
         (size_t)kMaxCluster * L.gcap * 4,           // 17 pairs
         (size_t)Ppad * L.u_cols * 2,                // 18 U
         (size_t)(L.NU + 1) * 4,                     // 19 uchunk
         (size_t)L.n_bins * 4,                       // 20 bin_cnt
-        (size_t)L.n_tiles * 4 * kMaxCluster, (size_t)L.n_tiles * 4 * kMaxCluster,   // 21-22 tile_beg / tile_end
+        (size_t)L.n_tiles * 16 * kMaxCluster, (size_t)L.n_tiles * 16 * kMaxCluster,   // 21-22 qbeg / qend
         (size_t)L.pool * 4,                         // 23 gentries
         (size_t)L.n_bins * L.bin_cap * 4,           // 24 entries
         (size_t)P * L.n_samp * 4,                   // 25 samp
@@ -203,12 +228,11 @@ static Ws carve(char* b, const Layout& L) {
     w.hotw = (float*)at(7);
     w.bound = (float*)at(8); w.emax = (uint32_t*)at(9); w.ushift = (int32_t*)at(10); w.uscale = (float*)at(11);
     w.ukey = (uint32_t*)at(12); w.uc0 = (uint32_t*)at(13); w.uc1 = (uint32_t*)at(14); w.ukwb = (uint32_t*)at(15);
-    w.toff = (uint16_t*)at(16); w.pairs = (uint32_t*)at(17);
-    w.ucls = reinterpret_cast<uint32_t*>(at(16) + (((size_t)kMaxCluster * (L.NU + 1) * 2 + 15) & ~(size_t)15));
+    w.pinfo = (uint32_t*)at(16); w.pairs = (uint32_t*)at(17);
     w.U = (uint16_t*)at(18);
     w.uchunk = (uint32_t*)at(19);
     w.bin_cnt = (uint32_t*)at(20);
-    w.tile_beg = (uint32_t*)at(21); w.tile_end = (uint32_t*)at(22);
+    w.qbeg = (uint32_t*)at(21); w.qend = (uint32_t*)at(22);
     w.gentries = (uint32_t*)at(23);
     w.entries = (uint32_t*)at(24);
     w.samp = (float*)at(25);
@@ -342,15 +366,12 @@ __global__ void __launch_bounds__(kPlanThreads) plan_b_kernel(PlanArgs a, Ws ws)
         ws.uc1[sl] = c1;
         ws.ukwb[sl] = a.key_word_off[key];
         ws.uchunk[sl] = base[1];
-        uint32_t cls = 0;
         for (int g = 0; g < kMaxCluster; ++g) {
-            const uint32_t c = ws.hcnt[t * kMaxCluster + g];
-            ws.toff[(size_t)g * (a.NU + 1) + sl] = (uint16_t)base[2 + g];
+            const uint32_t c = ws.hcnt[t * kMaxCluster + g];          // <= kGroup users
+            ws.pinfo[(size_t)g * a.NU + sl] = c ? (base[2 + g] << 8) | c : 0u;
             ws.hpair[t * kMaxCluster + g] = base[2 + g];
             base[2 + g] += c;
-            cls |= min(c, 7u) << (3 * g);
         }
-        ws.ucls[sl] = cls;
         base[0] += 1u;
         base[1] += c1 - c0;
         ws.hkey[t] = 0u;
@@ -361,10 +382,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_b_kernel(PlanArgs a, Ws ws)
         ws.header[0] = nu; ws.header[1] = 0; ws.header[2] = 0; ws.header[4] = 0; ws.header[6] = 0;
         ws.header[5] = sTot[1];                 // chunks of the union
         ws.uchunk[nu] = sTot[1];
-        for (int g = 0; g < kMaxCluster; ++g) {
-            ws.header[8 + g] = sTot[2 + g];     // pairs of group g
-            ws.toff[(size_t)g * (a.NU + 1) + nu] = (uint16_t)sTot[2 + g];
-        }
+        for (int g = 0; g < kMaxCluster; ++g) ws.header[8 + g] = sTot[2 + g];     // pairs of group g
     }
     for (int u = tid; u < a.P; u += kPlanThreads) {
         const float b = ws.bound[u], m = __uint_as_float(ws.emax[u]);
@@ -422,9 +440,10 @@ __global__ void __launch_bounds__(256) plan_c_kernel(PlanArgs a, Ws ws) {
 // ------------------------------------------------------------------------------------------
 // Level 1 (entry_bin): the union keys' chunks are decoded warp-cooperatively in key order (each
 // chunk once; Alg. 2 l.355-357 with the chunk codec), every posting appended to the bin of its
-// ad range; the lanes of a chunk that hit the same bin share one atomic (warp aggregation).
-// Level 2 (entry_sort): one CTA per bin sorts the bin by ad in shared memory (counting sort) and
-// writes it back with the per-tile bounds: entry = ad row << 24 | union slot.
+// 1024-ad range; the lanes of a chunk that hit the same bin share one atomic (warp aggregation).
+// Level 2 (entry_order): one CTA per bin orders the bin by (tile, quarter, pair-count class) with
+// a shared-memory counting sort and expands it into the stream of every user group that queries
+// the entry's key: entry = ad row << 24 | the group's first pair of the key << 8 | its pair count.
 struct EntryArgs {
     const uint2* hdr;
     const uint32_t* payload;
@@ -432,13 +451,12 @@ struct EntryArgs {
     int bin_ads, n_bins, n_tiles;
     int64_t bin_cap;
     int G;                  // user groups of the pass
-    int NU;                 // union slot capacity (toff row length - 1)
+    int NU;                 // union slot capacity (pinfo row length)
 };
 
 // Work item = 16 consecutive chunks of the union (in slot order); each key's part is decoded by
 // decode_unit16_warp (all headers, then all payload words in flight: two memory round trips per
-// item).  Bin entry = ad in bin << 21 | the slot's group classes << 15 | slot.
-constexpr int kBinEntryAdShift = 21;
+// item).  Bin entry = ad in bin << kBinAdShift | union slot.
 __global__ void __launch_bounds__(256) entry_bin_kernel(EntryArgs e, Ws ws) {
     const int lane = threadIdx.x & 31;
     const uint32_t nu = __ldcg(&ws.header[0]), total = __ldcg(&ws.header[5]);
@@ -463,7 +481,6 @@ __global__ void __launch_bounds__(256) entry_bin_kernel(EntryArgs e, Ws ws) {
             const uint32_t s_beg = __ldcg(&ws.uchunk[s]), s_end = __ldcg(&ws.uchunk[s + 1]);
             const uint32_t sub_end = min(gend, s_end);
             const uint32_t c0 = __ldcg(&ws.uc0[s]) + (g0 - s_beg);
-            const uint32_t tag = (__ldcg(&ws.ucls[s]) << 15) | s;
             decode_unit16_warp(e.hdr, e.payload, __ldcg(&ws.ukwb[s]), c0, c0 + (sub_end - g0), lane,
                                [&](uint32_t id, bool ok) {
                 const uint32_t r = ok ? id / R : 0xFFFFFFFFu;
@@ -475,7 +492,7 @@ __global__ void __launch_bounds__(256) entry_bin_kernel(EntryArgs e, Ws ws) {
                     if (lane == leader) base = atomicAdd(&ws.bin_cnt[r], (uint32_t)__popc(peers));
                     base = __shfl_sync(peers, base, leader);
                     const uint32_t pos = base + __popc(peers & ((1u << lane) - 1u));
-                    ws.entries[(size_t)r * e.bin_cap + pos] = ((id - r * R) << kBinEntryAdShift) | tag;
+                    ws.entries[(size_t)r * e.bin_cap + pos] = ((id - r * R) << kBinAdShift) | s;
                 }
             });
             g0 = sub_end;
@@ -483,75 +500,66 @@ __global__ void __launch_bounds__(256) entry_bin_kernel(EntryArgs e, Ws ws) {
     }
 }
 
-// Level 2: CTA = bin.  Every bin entry (ad, group classes, union slot) is expanded to the streams
-// of the groups whose users query the slot; each group's part of the bin is ordered by (tile,
-// pair-count class) so a warp's consecutive entries carry similar work in the fused kernel.  The
-// bin is staged in shared memory when it fits (the common case), else read twice from L2.
-constexpr int kCountClasses = 7;
-constexpr int kSortStage = 16384;    // bin entries staged in shared memory (64 KB)
-__global__ void __launch_bounds__(512) entry_sort_kernel(EntryArgs e, Ws ws) {
+// Level 2: CTA = bin (8 tiles).  The bin is staged in shared memory when it fits (the common
+// case), else read twice from L2: count per (group, tile quarter), scan, claim the groups' ranges
+// of the pool, scatter.
+constexpr int kOrderCells = (kBinAds / kTileM) * kQuarters;   // counters per group (= 32: one per lane)
+__global__ void __launch_bounds__(kOrderThreads) entry_order_kernel(EntryArgs e, Ws ws) {
     extern __shared__ uint32_t smem_u[];
-    uint32_t* off = smem_u;                               // [G][tiles_per_bin * kCountClasses]
-    uint32_t* buf = smem_u + kMaxCluster * (kBinAdsMax / kTileM) * kCountClasses;   // [kSortStage]
+    __shared__ uint32_t cnt[kMaxCluster * kOrderCells];
     __shared__ uint32_t sN, sBase[kMaxCluster];
-    const int r = blockIdx.x, tid = threadIdx.x;
-    const int tpb = e.bin_ads / kTileM, nb = tpb * kCountClasses, G = e.G;
+    uint32_t* buf = smem_u;                                 // [kOrderStage]
+    const int r = blockIdx.x, tid = threadIdx.x, G = e.G;
     if (tid == 0) { sN = ws.bin_cnt[r]; ws.bin_cnt[r] = 0u; }   // left zero for the next pass
-    for (int i = tid; i < G * nb; i += 512) off[i] = 0;
+    for (int i = tid; i < kMaxCluster * kOrderCells; i += kOrderThreads) cnt[i] = 0;
     __syncthreads();
     const uint32_t n = sN;
-    const bool staged = n <= (uint32_t)kSortStage;
+    const bool staged = n <= (uint32_t)kOrderStage;
     const uint32_t* ent = ws.entries + (size_t)r * e.bin_cap;
-    for (uint32_t i = tid; i < n; i += 512) {
-        const uint32_t v = __ldcg(&ent[i]);
+    const uint32_t* pinfo = ws.pinfo;
+    for (uint32_t i = tid; i < n; i += kOrderThreads) {
+        const uint32_t v = __ldcs(&ent[i]);
         if (staged) buf[i] = v;
-        const uint32_t b = ((v >> kBinEntryAdShift) / kTileM) * kCountClasses;
+        const uint32_t a = v >> kBinAdShift, sl = v & ((1u << kBinAdShift) - 1u);
         for (int g = 0; g < G; ++g) {
-            const uint32_t c = (v >> (15 + 3 * g)) & 7u;   // 0: no user of group g, else min(pairs, 7)
-            if (c) atomicAdd(&off[g * nb + b + c - 1], 1u);
+            const uint32_t c = __ldg(&pinfo[(size_t)g * e.NU + sl]) & 0xFFu;
+            if (c) atomicAdd(&cnt[g * kOrderCells + (a >> 5)], 1u);
         }
     }
     __syncthreads();
-    // per group: exclusive scan of the buckets (warp g), the group's range claimed from the pool
+    // warp g: exclusive scan of group g's counters (lane = tile quarter), its range claimed from
+    // the pool, the quarter bounds of the bin's tiles
     const int warp = tid >> 5, lane = tid & 31;
+    static_assert(kOrderCells == 32, "one counter per lane");
     if (warp < G) {
-        uint32_t* o = off + warp * nb;
-        uint32_t carry = 0;
-        for (int b0 = 0; b0 < nb; b0 += 32) {
-            const uint32_t x = (b0 + lane < nb) ? o[b0 + lane] : 0u;
-            uint32_t incl = x;
+        const uint32_t x = cnt[warp * kOrderCells + lane];
+        uint32_t incl = x;
 #pragma unroll
-            for (int k = 1; k < 32; k <<= 1) {
-                const uint32_t y = __shfl_up_sync(FULL, incl, k);
-                if (lane >= k) incl += y;
-            }
-            if (b0 + lane < nb) o[b0 + lane] = carry + incl - x;
-            carry += __shfl_sync(FULL, incl, 31);
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
         }
+        const uint32_t tot = __shfl_sync(FULL, incl, 31);
+        cnt[warp * kOrderCells + lane] = incl - x;
         uint32_t base = 0;
-        if (lane == 0) base = carry ? atomicAdd(&ws.header[6], carry) : 0u;
+        if (lane == 0) base = tot ? atomicAdd(&ws.header[6], tot) : 0u;
         base = __shfl_sync(FULL, base, 0);
         if (lane == 0) sBase[warp] = base;
-        // tile bounds of this group's stream
-        const int64_t t0 = (int64_t)r * tpb;
-        for (int tl = lane; tl < tpb; tl += 32) {
-            const int64_t t = t0 + tl;
-            if (t >= e.n_tiles) continue;
-            ws.tile_beg[(size_t)warp * e.n_tiles + t] = base + o[tl * kCountClasses];
-            ws.tile_end[(size_t)warp * e.n_tiles + t] = base + ((tl + 1 < tpb) ? o[(tl + 1) * kCountClasses] : carry);
+        const int64_t qi = (int64_t)r * kOrderCells + lane;      // global tile quarter
+        if (qi < (int64_t)e.n_tiles * kQuarters) {
+            ws.qbeg[(size_t)warp * e.n_tiles * kQuarters + qi] = base + incl - x;
+            ws.qend[(size_t)warp * e.n_tiles * kQuarters + qi] = base + incl;
         }
     }
     __syncthreads();
-    for (uint32_t i = tid; i < n; i += 512) {
-        const uint32_t v = staged ? buf[i] : __ldcg(&ent[i]);
-        const uint32_t a = v >> kBinEntryAdShift, sl = v & 0x7FFFu;
-        const uint32_t b = (a / kTileM) * kCountClasses;
-        const uint32_t out = ((a & (kTileM - 1)) << 24) | sl;
+    for (uint32_t i = tid; i < n; i += kOrderThreads) {
+        const uint32_t v = staged ? buf[i] : __ldcs(&ent[i]);
+        const uint32_t a = v >> kBinAdShift, sl = v & ((1u << kBinAdShift) - 1u);
         for (int g = 0; g < G; ++g) {
-            const uint32_t c = (v >> (15 + 3 * g)) & 7u;
-            if (c) {
-                const uint32_t pos = atomicAdd(&off[g * nb + b + c - 1], 1u);
-                ws.gentries[sBase[g] + pos] = out;
+            const uint32_t pi = __ldg(&pinfo[(size_t)g * e.NU + sl]);
+            if (pi & 0xFFu) {
+                const uint32_t pos = sBase[g] + atomicAdd(&cnt[g * kOrderCells + (a >> 5)], 1u);
+                ws.gentries[pos] = ((a & (kTileM - 1)) << 24) | pi;
             }
         }
     }
@@ -571,13 +579,15 @@ struct GemmParams {
     int P;                  // users in this pass
     int n_tiles, tile_stride;
     int n_samp;
-    int stages;             // ring stages (16 KB each)
+    int stages;             // max deep A ring stages (the kernel takes what the shared memory leaves)
+    int smem_bytes;         // dynamic shared memory of the launch
     int acc_stages;         // TMEM accumulator stages (128 columns each)
     int u_cols;             // 16-bit columns of the pass's user tile U
     int64_t cap;
     int rerun;              // filter rerun: only flagged users; gated on header[2] | header[4]
     int dense;              // sample-mode variant: every score of the overflowed users (gated on header[4])
     const uint4* hot_mask;
+    const void* A;          // the index's A [n_pad][d_pad] bf16 (L2 prefetch)
     Ws ws;
     uint32_t* err;
     int diag;               // A/B experiments (EBR_DIAG): 1 skip the cold scatter, 2 skip the epilogue work
@@ -610,47 +620,66 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
     const uint16_t mc_mask = (uint16_t)((1u << csize) - 1u);
     const int g = (int)rank;                         // this CTA's user group
     const int nu = min(kGroup, p.P - g * kGroup);    // valid users
-    const int nkt = p.n_kb + p.n_hb;
     const int a_cols = 32 * (p.n_kb + p.n_hb * p.pieces);   // TMEM columns of the users' A operand
     const int nst = p.acc_stages;
+    // deep A ring stages: what the shared memory leaves next to the fixed part and the largest
+    // group's pairs of the pass (the same in every CTA of the cluster: the multicast writes the
+    // ring stages at the same offsets)
+    uint32_t n_gp_max = 0;
+    for (uint32_t r = 0; r < csize; ++r) n_gp_max = max(n_gp_max, __ldcg(&p.ws.header[8 + r]));
+    const int nring = (int)min((size_t)kMaxStages,
+                               ((size_t)p.smem_bytes - 1024 - score_smem_fixed() - (size_t)n_gp_max * 4) / kBlockBytes);
 
-    unsigned char* sRing = smem;                                            // [stages][128 ads x 128 B]
-    int32_t* acc = reinterpret_cast<int32_t*>(sRing + (size_t)p.stages * kBlockBytes);   // [128 users][kAccPitch]
-    uint4* sLut = reinterpret_cast<uint4*>(acc + kGroup * kAccPitch);       // [256] byte -> 8 fp16 {0, 1} (16-B aligned)
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sLut + 256);
-    uint64_t* full = bars;
-    uint64_t* empty = full + p.stages;
-    uint64_t* tfull = empty + p.stages;
+    unsigned char* sRing = smem;                                            // [nring][128 ads x 128 B] deep blocks of A
+    unsigned char* sHot = sRing + (size_t)nring * kBlockBytes;              // [kHotStages][128 ads x 128 B] one-hot blocks
+    int32_t* sCold = reinterpret_cast<int32_t*>(sHot + (size_t)kHotStages * kBlockBytes);   // [4][32 ads][128 users]
+    uint32_t* sEnt = reinterpret_cast<uint32_t*>(sCold + kQuarters * kColdQuarter);   // [2][kEntHdr + kEntBuf]
+    uint4* sLut = reinterpret_cast<uint4*>(sEnt + 2 * (kEntHdr + kEntBuf));  // [256] byte -> 8 fp16 {0, 1}
+    uint32_t* sHeavy = reinterpret_cast<uint32_t*>(sLut + 256);              // [kHeavyCap] heavy entries' rest
+    uint32_t* sHeavyN = sHeavy + kHeavyCap;                                  // [2] counts by quarter parity
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sHeavyN + 4);
+    uint64_t* full = bars;                          // [kMaxStages] A ring
+    uint64_t* empty = full + kMaxStages;
+    uint64_t* hfull = empty + kMaxStages;           // [kHotStages] hot ring
+    uint64_t* hempty = hfull + kHotStages;
+    uint64_t* tfull = hempty + kHotStages;          // [kMaxAccStages] TMEM accumulator stages
     uint64_t* tempty = tfull + kMaxAccStages;
-    uint64_t* wready = tempty + kMaxAccStages;
-    uint64_t* aready = wready + kMaxAccStages;
+    uint64_t* cfull = tempty + kMaxAccStages;       // [4] cold quarter buffers
+    uint64_t* cempty = cfull + kQuarters;
+    uint64_t* efull = cempty + kQuarters;           // [2] entry buffers
+    uint64_t* eempty = efull + 2;
+    uint64_t* aready = eempty + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aready + 1);
     uint64_t* sTheta = reinterpret_cast<uint64_t*>(tmem_slot + 2);          // [kGroup]
     float* sThetaS = reinterpret_cast<float*>(sTheta + kGroup);             // [kGroup]
     float* sScale = sThetaS + kGroup;                                       // [kGroup]
     int* sDense = reinterpret_cast<int*>(sScale + kGroup);                  // [kGroup] dense slot or -1
-    uint16_t* sT = reinterpret_cast<uint16_t*>(sDense + kGroup);            // [n_union + 1] slot -> first pair
-    const uint32_t n_union = __ldcg(&p.ws.header[0]), n_gp = __ldcg(&p.ws.header[8 + g]);
-    uint32_t* sPairs = reinterpret_cast<uint32_t*>(sT + ((n_union + 2) & ~1u));   // [n_gp]
+    const uint32_t n_gp = __ldcg(&p.ws.header[8 + g]);
+    uint32_t* sPairs = reinterpret_cast<uint32_t*>(sDense + kGroup);        // [n_gp] the group's pairs
 
     if (tid == 0) {
-        for (int s = 0; s < p.stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], csize); }
+        for (int s = 0; s < nring; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], csize); }
+        for (int s = 0; s < 2; ++s) { mbar_init(&efull[s], 1); mbar_init(&eempty[s], 1); }
+        for (int s = 0; s < kHotStages; ++s) { mbar_init(&hfull[s], 1); mbar_init(&hempty[s], 1); }
         for (int s = 0; s < kMaxAccStages; ++s) {
             mbar_init(&tfull[s], 1);
             mbar_init(&tempty[s], kEpiWarps);
-            mbar_init(&wready[s], 1);
+        }
+        for (int q = 0; q < kQuarters; ++q) {
+            mbar_init(&cfull[q], 1);
+            mbar_init(&cempty[q], 4);                   // the 4 epilogue warps (user quadrants) of the quarter
         }
         mbar_init(aready, 4);
         fence_mbar_init();
     }
     if (warp == 2) tc::tmem_alloc(tmem_slot, 512);
-    for (int i = tid; i < kGroup * kAccPitch / 4; i += kGemmThreads)
-        reinterpret_cast<int4*>(acc)[i] = make_int4(0, 0, 0, 0);
+    if (tid == 0) { sHeavyN[0] = 0u; sHeavyN[1] = 0u; }
+    for (int i = tid; i < kQuarters * kColdQuarter / 4; i += kGemmThreads)
+        reinterpret_cast<int4*>(sCold)[i] = make_int4(0, 0, 0, 0);
     for (int b = tid; b < 256; b += kGemmThreads) {
         auto h2 = [b](int k) { return ((b >> k) & 1 ? 0x3C00u : 0u) | ((b >> (k + 1)) & 1 ? 0x3C000000u : 0u); };
         sLut[b] = make_uint4(h2(0), h2(2), h2(4), h2(6));
     }
-    for (uint32_t i = tid; i <= n_union; i += kGemmThreads) sT[i] = __ldcg(&p.ws.toff[(size_t)g * (p.NU + 1) + i]);
     for (uint32_t i = tid; i < n_gp; i += kGemmThreads) sPairs[i] = __ldcg(&p.ws.pairs[(size_t)g * p.gcap + i]);
     for (int i = tid; i < kGroup; i += kGemmThreads) {
         const int u = g * kGroup + i;
@@ -677,11 +706,62 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
             tc::tma_prefetch(&tmA);
             const uint64_t pol = tc::policy_evict_first();   // A is streamed once per pass
             uint32_t gb = 0;
-            for (int t = (int)cid; t < p.n_tiles; t += (int)ncl) {
+            int it = 0;
+            const size_t qrow = (size_t)g * p.n_tiles_all * kQuarters;
+            const uint32_t tile_bytes = (uint32_t)(kTileM * p.n_kb * 128);     // a tile's rows of A (contiguous)
+            const unsigned char* Abase = reinterpret_cast<const unsigned char*>(p.A);
+            // L2 prefetch kPrefetchTiles ahead of the TMA loads: the ring's loads then hit L2 (the
+            // HBM latency of a multicast stage exceeds what the ring's depth covers)
+            if (rank == 0)
+                for (int k = 0; k < kPrefetchTiles; ++k) {
+                    const int tp = (int)cid + k * (int)ncl;
+                    if (tp < p.n_tiles) tc::bulk_prefetch_l2(Abase + (size_t)tp * p.tile_stride * tile_bytes, tile_bytes);
+                }
+            // quarter bounds of the group stream, loaded two tiles ahead (never on the issue path)
+            auto load_qb = [&](int tt, uint32_t (&qb)[kQuarters + 1]) {
+                if (tt < p.n_tiles) {
+                    const size_t qi = qrow + (size_t)tt * p.tile_stride * kQuarters;
+#pragma unroll
+                    for (int q = 0; q < kQuarters; ++q) qb[q] = __ldcg(&p.ws.qbeg[qi + q]);
+                    qb[kQuarters] = __ldcg(&p.ws.qend[qi + kQuarters - 1]);
+                }
+            };
+            uint32_t qbA[kQuarters + 1] = {}, qbB[kQuarters + 1] = {};
+            load_qb((int)cid, qbA);
+            load_qb((int)cid + (int)ncl, qbB);
+            for (int t = (int)cid; t < p.n_tiles; t += (int)ncl, ++it) {
                 const int row0 = t * p.tile_stride * kTileM;
-                for (int kb = 0; kb < nkt; ++kb, ++gb) {
-                    if (kb >= p.n_kb) continue;             // hot block: expanded by the hot warps
-                    const uint32_t slot = gb % p.stages, round = gb / p.stages;
+                uint32_t qb[kQuarters + 1];
+#pragma unroll
+                for (int q = 0; q <= kQuarters; ++q) { qb[q] = qbA[q]; qbA[q] = qbB[q]; }
+                load_qb(t + 2 * (int)ncl, qbB);
+                if (rank == 0) {
+                    const int tp = t + kPrefetchTiles * (int)ncl;
+                    if (tp < p.n_tiles) tc::bulk_prefetch_l2(Abase + (size_t)tp * p.tile_stride * tile_bytes, tile_bytes);
+                }
+                {
+                    // this CTA's cold entries of the tile (contiguous in its group's stream) into
+                    // entry buffer it % 2 by one bulk copy; header = quarter bounds relative to the
+                    // copied base, and the number of entries copied
+                    const int eb = it & 1;
+                    if (it >= 2) mbar_wait_sleep(&eempty[eb], ((it >> 1) - 1) & 1);
+                    uint32_t* hdr = sEnt + eb * (kEntHdr + kEntBuf);
+                    if (p.diag & 1) qb[1] = qb[2] = qb[3] = qb[4] = qb[0];
+                    const uint32_t base = qb[0] & ~3u;                          // 16-byte aligned source
+                    const uint32_t ncopy = min((qb[kQuarters] - base + 3u) & ~3u, (uint32_t)kEntBuf);
+#pragma unroll
+                    for (int q = 0; q <= kQuarters; ++q) hdr[q] = qb[q] - base;
+                    hdr[kQuarters + 1] = base;
+                    hdr[kQuarters + 2] = ncopy;
+                    if (ncopy) {
+                        mbar_arrive_expect_tx(&efull[eb], ncopy * 4);
+                        bulk_g2s(hdr + kEntHdr, p.ws.gentries + base, ncopy * 4, &efull[eb]);
+                    } else {
+                        mbar_arrive(&efull[eb]);
+                    }
+                }
+                for (int kb = 0; kb < p.n_kb; ++kb, ++gb) {
+                    const uint32_t slot = gb % nring, round = gb / nring;
                     if (round > 0) { EBR_PROF_T0; mbar_wait_sleep(&empty[slot], (round - 1) & 1); EBR_PROF_ADD(0); }
                     mbar_arrive_expect_tx(&full[slot], (uint32_t)kBlockBytes);
                     if (csize == 1)
@@ -692,46 +772,50 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
                 }
             }
             // every remote arrival into this CTA's ring barriers has landed before it exits
-            for (uint32_t k = 0; k < (uint32_t)p.stages && k < gb; ++k) {
+            for (uint32_t k = 0; k < (uint32_t)nring && k < gb; ++k) {
                 const uint32_t q = gb - 1 - k;
-                mbar_wait_sleep(&empty[q % p.stages], (q / p.stages) & 1);
+                mbar_wait_sleep(&empty[q % nring], (q / nring) & 1);
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
             // ---------------- MMA issuer ----------------
-            // The accumulator stage already holds the tile's cold wide term (stored by the wide
-            // warps), so every MMA accumulates: D = cold + U A^T + U_hot (one-hot)^T.
+            // D = U A^T (deep, the first MMA of a tile overwrites the stage) + U_hot (one-hot)^T;
+            // the cold wide term is added by the epilogue from the shared-memory quarter ring.
             const uint32_t idb = tc::idesc_bf16_m128(kTileM), idh = tc::idesc_f16_m128(kTileM);
             mbar_wait_sleep(aready, 0);                   // users' A operand in TMEM
             tc::fence_after();
             int it = 0;
-            uint32_t gb = 0;
+            uint32_t gb = 0, hb = 0;
             for (int t = (int)cid; t < p.n_tiles; t += (int)ncl, ++it) {
                 const int st = it % nst;
-                { EBR_PROF_T0; mbar_wait_sleep(&wready[st], (it / nst) & 1); EBR_PROF_ADD(1); }
+                if (it >= nst) { EBR_PROF_T0; mbar_wait_sleep(&tempty[st], ((it / nst) - 1) & 1); EBR_PROF_ADD(1); }
                 tc::fence_after();
                 const uint32_t d_tmem = tmem_base + (uint32_t)(a_cols + st * kTileM);
-                for (int kb = 0; kb < nkt; ++kb, ++gb) {
-                    const uint32_t slot = gb % p.stages;
-                    { EBR_PROF_T0; mbar_wait_sleep(&full[slot], (gb / p.stages) & 1); EBR_PROF_ADD(2); }
+                for (int kb = 0; kb < p.n_kb; ++kb, ++gb) {
+                    const uint32_t slot = gb % nring;
+                    { EBR_PROF_T0; mbar_wait_sleep(&full[slot], (gb / nring) & 1); EBR_PROF_ADD(2); }
                     tc::fence_after();
                     const uint64_t db0 = tc::sdesc_sw128(sRing + (size_t)slot * kBlockBytes);
-                    if (kb < p.n_kb) {
 #pragma unroll
-                        for (int k = 0; k < kBlockK / 16; ++k)
-                            tc::umma_f16_ts(d_tmem, tmem_base + (uint32_t)(kb * 32 + k * 8), db0 + (uint64_t)(k * 2), idb, 1u);
-                    } else {
-                        const int h = kb - p.n_kb;
-                        for (int pc = 0; pc < p.pieces; ++pc) {
-                            const uint32_t ac = (uint32_t)(32 * (p.n_kb + h * p.pieces + pc));
-#pragma unroll
-                            for (int k = 0; k < kBlockK / 16; ++k)
-                                tc::umma_f16_ts(d_tmem, tmem_base + ac + (uint32_t)(k * 8), db0 + (uint64_t)(k * 2), idh, 1u);
-                        }
-                    }
+                    for (int k = 0; k < kBlockK / 16; ++k)
+                        tc::umma_f16_ts(d_tmem, tmem_base + (uint32_t)(kb * 32 + k * 8), db0 + (uint64_t)(k * 2), idb,
+                                        (kb | k) ? 1u : 0u);
                     if (csize == 1) tc::umma_commit(&empty[slot]);
                     else tc::umma_commit_mc(&empty[slot], mc_mask);
+                }
+                for (int h = 0; h < p.n_hb; ++h, ++hb) {
+                    const uint32_t hs = hb % kHotStages;
+                    { EBR_PROF_T0; mbar_wait_sleep(&hfull[hs], (hb / kHotStages) & 1); EBR_PROF_ADD(2); }
+                    tc::fence_after();
+                    const uint64_t db0 = tc::sdesc_sw128(sHot + (size_t)hs * kBlockBytes);
+                    for (int pc = 0; pc < p.pieces; ++pc) {
+                        const uint32_t ac = (uint32_t)(32 * (p.n_kb + h * p.pieces + pc));
+#pragma unroll
+                        for (int k = 0; k < kBlockK / 16; ++k)
+                            tc::umma_f16_ts(d_tmem, tmem_base + ac + (uint32_t)(k * 8), db0 + (uint64_t)(k * 2), idh, 1u);
+                    }
+                    tc::umma_commit(&hempty[hs]);
                 }
                 tc::umma_commit(&tfull[st]);
             }
@@ -752,21 +836,20 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
                 }
             };
             load((int)cid, hn);
-            uint32_t gb = 0;
+            uint32_t hb = 0;
             for (int t = (int)cid; t < p.n_tiles; t += (int)ncl) {
                 hm[0] = hn[0];
                 hm[1] = hn[1];
                 load(t + (int)ncl, hn);
-                for (int h = 0; h < p.n_hb; ++h) {
-                    const uint32_t pos = gb + p.n_kb + h;
-                    const uint32_t slot = pos % p.stages, round = pos / p.stages;
-                    if (round > 0) { EBR_PROF_T0; mbar_wait(&empty[slot], (round - 1) & 1); if (hw == 0) EBR_PROF_ADD(3); }
+                for (int h = 0; h < p.n_hb; ++h, ++hb) {
+                    const uint32_t hs = hb % kHotStages, round = hb / kHotStages;
+                    if (round > 0) { EBR_PROF_T0; mbar_wait_sleep(&hempty[hs], (round - 1) & 1); if (hw == 0) EBR_PROF_ADD(3); }
 #pragma unroll
                     for (int rr = 0; rr < 2; ++rr) {
                         const int row = hw + rr * 64;
                         const uint64_t bits = h == 0 ? ((uint64_t)hm[rr].y << 32 | hm[rr].x)
                                                      : ((uint64_t)hm[rr].w << 32 | hm[rr].z);
-                        unsigned char* rowp = sRing + (size_t)slot * kBlockBytes + (size_t)row * 128;
+                        unsigned char* rowp = sHot + (size_t)hs * kBlockBytes + (size_t)row * 128;
 #pragma unroll
                         for (int c = 0; c < 8; ++c) {                  // 16-byte chunk: keys 8c .. 8c+7
                             const uint32_t byte = (uint32_t)(bits >> (8 * c)) & 0xFFu;
@@ -775,19 +858,17 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
                     }
                     tc::fence_proxy_async_smem();
                     tc::named_bar_sync(2, 64);
-                    if (hw == 0) mbar_arrive(&full[slot]);
+                    if (hw == 0) mbar_arrive(&hfull[hs]);
                 }
-                gb += nkt;
             }
         }
     } else if (warp >= kWideWarp0 && warp < kEpiWarp0) {
-        // ---------------- wide warps: users' A operand once, then cold scatter + TMEM store ----------------
+        // ---------------- wide warps: users' A operand once, then the cold scatter ----------------
         const int wt = tid - kWideWarp0 * 32;
-        const int q = warp & 3;                          // TMEM lane quadrant = users 32q .. 32q + 31
-        const int cj = (warp - kWideWarp0) >> 2;         // this warp's 32-ad column chunk of a tile
-        const int urow = q * 32 + lane;                  // the user (TMEM lane) of this thread
         if (warp < kWideWarp0 + 4) {
             // U row of this user -> TMEM A columns (two 16-bit K elements per 32-bit column)
+            const int q = warp & 3;                      // TMEM lane quadrant = users 32q .. 32q + 31
+            const int urow = q * 32 + lane;
             const uint32_t* urow_p = reinterpret_cast<const uint32_t*>(p.ws.U) +
                                      (size_t)(g * kGroup + urow) * (p.u_cols / 2);
             for (int c0 = 0; c0 < a_cols; c0 += 32) {
@@ -801,103 +882,80 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
             __syncwarp();
             if (lane == 0) mbar_arrive(aready);
         }
+        // Per tile quarter (32 ads): its entries (ad row, the slot's first pair, pair count) of
+        // this CTA's group stream, staged in shared memory by the producer's bulk copy; each pair
+        // (user, w~ 2^S) is added to the quarter buffer [32 ads][128 users] with a native 32-bit
+        // shared atomic (exact, order-free; Alg. 2 l.358).  An entry's first kInlinePairs pairs are
+        // scattered by its thread, a heavy entry's rest by whole warps.
         const uint32_t* __restrict__ entries = p.ws.gentries;
-        constexpr int kE = kWideWarps >= 16 ? 4 : 8;   // entries per thread and batch (registers)
-        constexpr uint32_t kNoEntry = 0xFFFFFFFFu;     // (a real entry has bit 31 clear)
-        // software pipeline over tiles: the entry bounds two tiles ahead and the first entries one
-        // tile ahead are in flight while the current tile is processed
-        auto bounds = [&](int tt, uint32_t& b, uint32_t& e) {
-            b = e = 0u;
-            if (tt < p.n_tiles) {
-                const size_t ti = (size_t)g * p.n_tiles_all + (size_t)tt * p.tile_stride;
-                b = __ldcg(&p.ws.tile_beg[ti]);
-                e = __ldcg(&p.ws.tile_end[ti]);
-            }
-        };
-        uint32_t cur_beg, cur_end, nxt_beg, nxt_end, nent[kE];
-        bounds((int)cid, cur_beg, cur_end);
-        bounds((int)cid + (int)ncl, nxt_beg, nxt_end);
-#pragma unroll
-        for (int i = 0; i < kE; ++i) {
-            const uint32_t e = cur_beg + wt + i * kWideThreads;
-            nent[i] = e < cur_end ? __ldcs(&entries[e]) : kNoEntry;
-        }
-        const float uscale = sScale[urow];
         int it = 0;
         for (int t = (int)cid; t < p.n_tiles; t += (int)ncl, ++it) {
-            const int st = it % nst;
-            const long long _pc0 = (p.diag & 4) ? clock64() : 0;
-            // cold: the tile's entries (ad row, union slot) of this CTA's group stream; the slot's
-            // pairs (user, w~ 2^S) are in shared memory (sT: first pair per slot)
-            {
-                const uint32_t e0 = cur_beg, e1 = (p.diag & 1) ? cur_beg : cur_end;
-                const uint32_t nbatch = (e1 - e0 + kE * kWideThreads - 1) / (kE * kWideThreads);
-                for (uint32_t batch = 0, eb = e0 + wt; batch < nbatch; eb += kE * kWideThreads, ++batch) {
-                    uint32_t ent[kE];
+            const int eb = it & 1;
+            { EBR_PROF_T0; mbar_wait_sleep(&efull[eb], (it >> 1) & 1); if (wt == 0) EBR_PROF_ADD(11); }
+            const uint32_t* hdr = sEnt + eb * (kEntHdr + kEntBuf);
+            const uint32_t* ebuf = hdr + kEntHdr;
+            const uint32_t ebase = hdr[kQuarters + 1], ncopy = hdr[kQuarters + 2];
+            for (int q = 0; q < kQuarters; ++q) {
+                // the quarter buffer is free once the epilogue drained it (previous tile)
+                if (it > 0) { EBR_PROF_T0; mbar_wait_sleep(&cempty[q], (it - 1) & 1); if (wt == 0) EBR_PROF_ADD(5); }
+                const long long _pc0 = (p.diag & 4) ? clock64() : 0;
+                int32_t* buf = sCold + q * kColdQuarter;
+                const uint32_t e0 = hdr[q], e1 = hdr[q + 1];
+                for (uint32_t ei = e0 + wt; ei < e1; ei += kWideThreads) {
+                    const uint32_t en = ei < ncopy ? ebuf[ei] : __ldcs(&entries[ebase + ei]);
+                    const uint32_t a = (en >> 24) & 31u, lo = (en >> 8) & 0xFFFFu, c = en & 0xFFu;
 #pragma unroll
-                    for (int i = 0; i < kE; ++i) {
-                        const uint32_t e = eb + i * kWideThreads;
-                        ent[i] = batch == 0 ? nent[i] : (e < e1 ? __ldcs(&entries[e]) : kNoEntry);
+                    for (uint32_t qq = 0; qq < (uint32_t)kInlinePairs; ++qq) {
+                        if (qq < c) {
+                            const uint32_t pr = sPairs[lo + qq];
+                            atomicAdd(&buf[a * kGroup + (pr & (kGroup - 1))], (int32_t)pr >> kPairUBits);
+                        }
                     }
-#pragma unroll
-                    for (int i = 0; i < kE; ++i) {
-                        if (ent[i] == kNoEntry) continue;
-                        const uint32_t a = ent[i] >> 24, sl = ent[i] & 0xFFFFFFu;
-                        const uint32_t lo = sT[sl], hi = sT[sl + 1];
-                        for (uint32_t qq = lo; qq < hi; ++qq) {
-                            const uint32_t pr = sPairs[qq];
-                            atomicAdd(&acc[(pr & (kGroup - 1)) * kAccPitch + a], (int32_t)pr >> kPairUBits);
+                    if (c > (uint32_t)kInlinePairs) {
+                        const uint32_t hslot = atomicAdd(&sHeavyN[q & 1], 1u);
+                        const uint32_t rest = (a << 24) | ((lo + kInlinePairs) << 8) | (c - kInlinePairs);
+                        if (hslot < (uint32_t)kHeavyCap) {
+                            sHeavy[hslot] = rest;
+                        } else {
+                            for (uint32_t qq = kInlinePairs; qq < c; ++qq) {
+                                const uint32_t pr = sPairs[lo + qq];
+                                atomicAdd(&buf[a * kGroup + (pr & (kGroup - 1))], (int32_t)pr >> kPairUBits);
+                            }
                         }
                     }
                 }
-            }
-            // next tile's entries, in flight during the store phase
-            {
-                cur_beg = nxt_beg;
-                cur_end = nxt_end;
-#pragma unroll
-                for (int i = 0; i < kE; ++i) {
-                    const uint32_t e = cur_beg + wt + i * kWideThreads;
-                    nent[i] = e < cur_end ? __ldcs(&entries[e]) : kNoEntry;
+                tc::named_bar_sync(1, kWideThreads);
+                // the heavy entries' remaining pairs, a warp per entry (lanes over pairs)
+                const uint32_t nh = min(sHeavyN[q & 1], (uint32_t)kHeavyCap);
+                if (nh) {
+                    for (uint32_t h = (uint32_t)(wt >> 5); h < nh; h += kWideWarps) {
+                        const uint32_t hv = sHeavy[h];
+                        const uint32_t a = hv >> 24, lo = (hv >> 8) & 0xFFFFu, c = hv & 0xFFu;
+                        for (uint32_t qq = (uint32_t)lane; qq < c; qq += 32) {
+                            const uint32_t pr = sPairs[lo + qq];
+                            atomicAdd(&buf[a * kGroup + (pr & (kGroup - 1))], (int32_t)pr >> kPairUBits);
+                        }
+                    }
+                    tc::named_bar_sync(1, kWideThreads);
                 }
-                bounds(t + 2 * (int)ncl, nxt_beg, nxt_end);
-            }
-            tc::named_bar_sync(1, kWideThreads);
-            if ((p.diag & 4) && wt == 0) atomicAdd(&p.ws.prof[4], (unsigned long long)(clock64() - _pc0));
-            // the accumulator stage is free once the epilogue drained it (nst tiles ago)
-            if (it >= nst) { EBR_PROF_T0; mbar_wait(&tempty[st], ((it / nst) - 1) & 1); if (wt == 0) EBR_PROF_ADD(5); }
-            const long long _ps0 = (p.diag & 4) ? clock64() : 0;
-            tc::fence_after();
-            {
-                // this user's 32 ads of the tile: fixed point -> fp32 (the one rounding), zeroed
-                int4* src = reinterpret_cast<int4*>(acc + urow * kAccPitch + cj * 32);
-                uint32_t f[32];
-#pragma unroll
-                for (int v4 = 0; v4 < 8; ++v4) {
-                    const int4 v = src[v4];
-                    src[v4] = make_int4(0, 0, 0, 0);
-                    f[4 * v4 + 0] = __float_as_uint((float)v.x * uscale);
-                    f[4 * v4 + 1] = __float_as_uint((float)v.y * uscale);
-                    f[4 * v4 + 2] = __float_as_uint((float)v.z * uscale);
-                    f[4 * v4 + 3] = __float_as_uint((float)v.w * uscale);
+                if (wt == 0) {
+                    sHeavyN[q & 1] = 0u;      // (the other parity's counter is the next quarter's)
+                    mbar_arrive(&cfull[q]);
+                    if (q == kQuarters - 1) mbar_arrive(&eempty[eb]);   // entry buffer consumed
                 }
-                tc::tmem_st32_nowait(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a_cols + st * kTileM + cj * 32), f);
+                if ((p.diag & 4) && wt == 0) atomicAdd(&p.ws.prof[4], (unsigned long long)(clock64() - _pc0));
             }
-            tc::tmem_wait_st();
-            tc::fence_before();
-            tc::named_bar_sync(1, kWideThreads);
-            if (wt == 0) mbar_arrive(&wready[st]);
-            if ((p.diag & 4) && wt == 0) atomicAdd(&p.ws.prof[6], (unsigned long long)(clock64() - _ps0));
         }
     } else if (warp >= kEpiWarp0) {
-        // ---------------- epilogue: TMEM -> registers, kappa, sample store / filter ----------------
-        // thread = one user (TMEM lane) x half of the tile's ads (two 32-column chunks)
+        // ---------------- epilogue: TMEM + cold quarter -> s, kappa, sample store / filter ----------------
+        // thread = one user (TMEM lane) x half of the tile's ads (two 32-ad quarters)
         const int e = warp - kEpiWarp0;
         const int q = warp & 3;
         const int ul = q * 32 + lane;                    // CTA-local user
         const int u = g * kGroup + ul;                   // pass user
         const bool uok = ul < nu;
         const int hf = e >> 2;
+        const float uscale = sScale[ul];
         float thS = 0.f;
         uint64_t th = 0;
         int dslot = -1;
@@ -911,10 +969,23 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
             tc::fence_after();
             const long long _pe0 = (p.diag & 4) ? clock64() : 0;
 #pragma unroll 1
-            for (int ch = 0; ch < 2 && !(p.diag & 2); ++ch) {
-                const int c = hf * 64 + ch * 32;
+            for (int ch = 0; ch < 2; ++ch) {
+                const int qi = hf * 2 + ch;              // tile quarter = 32-column chunk
+                const int c = qi * 32;
                 uint32_t r[32];
                 tc::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a_cols + st * kTileM + c), r);
+                // the cold wide term of the quarter: fixed point -> fp32 (the one rounding), zeroed
+                { EBR_PROF_T0; mbar_wait_sleep(&cfull[qi], it & 1); if (warp == kEpiWarp0 && lane == 0) EBR_PROF_ADD(6); }
+                int32_t* cb = sCold + qi * kColdQuarter + ul;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const int32_t v = cb[j * kGroup];
+                    cb[j * kGroup] = 0;
+                    r[j] = __float_as_uint(__uint_as_float(r[j]) + (float)v * uscale);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&cempty[qi]);
+                if (p.diag & 2) continue;
                 const int64_t ac = a0 + c;
                 const int nval = (int)min((int64_t)32, max((int64_t)0, p.n_ads - ac));   // valid ads in the chunk
                 if (MODE == 0) {
@@ -1032,7 +1103,8 @@ __device__ __forceinline__ void theta_find_digit(const uint32_t* hist, uint32_t 
 // rerun = 1: only the users flagged by final_kernel, their lists reset: short users at rank K
 // of the sample; overflowed users at rank K of ALL their scores (dense), an exact threshold
 __global__ void __launch_bounds__(kThetaThreads, 1) theta_kernel(Ws ws, int n_samp, int rank, uint32_t ad_begin,
-                                                                int P, int scap, int rerun, int64_t n_pad) {
+                                                                int P, int scap, int rerun, int64_t n_pad,
+                                                                int64_t sstride) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint32_t sScalar[8];
     const int u = blockIdx.x;
@@ -1050,7 +1122,7 @@ __global__ void __launch_bounds__(kThetaThreads, 1) theta_kernel(Ws ws, int n_sa
     const float* sp = dense ? ws.dense + (size_t)(fl >> 8) * n_pad : ws.samp + (size_t)u * n_samp;
     const float4* sp4 = reinterpret_cast<const float4*>(sp);
     const int n4 = n_samp / 4;
-    const int64_t stride = dense ? 1 : kSampleStride;
+    const int64_t stride = dense ? 1 : sstride;
     auto ad_of = [stride](int64_t i) { return (i / kTileM) * stride * kTileM + (i % kTileM); };
     uint32_t prefix = 0, need = (uint32_t)rank;
     for (int pass = 0; pass < 2; ++pass) {
@@ -1220,7 +1292,7 @@ static Tuning tuning(const ebr_index* idx) {
 }
 
 static size_t gemm_smem(const Layout& L, int stages) {
-    return 1024 + score_smem_fixed(stages) + (size_t)(L.NU + 2) * 2 + (size_t)L.gcap * 4;
+    return 1024 + (size_t)stages * kBlockBytes + score_smem_fixed() + (size_t)L.gcap * 4;
 }
 
 }  // namespace batch
@@ -1265,15 +1337,13 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
     // >= 2 accumulator stages of 128 columns; hot blocks are dropped until both fit
     int stages = 0, acc_stages = 0;
     for (; tu.n_hb >= 0; --tu.n_hb) {
-        const int nkt = n_kb + tu.n_hb;
         acc_stages = std::min(kMaxAccStages, (512 - 32 * (n_kb + tu.n_hb * tu.pieces)) / kTileM);
         if (acc_stages < 2) continue;
-        stages = 6;
-        while (stages > nkt + 1 && gemm_smem(L, stages) > (size_t)max_smem) --stages;
+        stages = n_kb + 1;          // the minimum with the worst-case pairs; the kernel takes more
         if (gemm_smem(L, stages) <= (size_t)max_smem) break;
     }
     if (tu.n_hb < 0) return set_error(EBR_EUNSUPPORTED, "batched path: d=%d does not fit shared memory / TMEM", idx->d);
-    const size_t smem = gemm_smem(L, stages);
+    const size_t smem = (size_t)max_smem;
     CUtensorMap tmA;
     if (!encode_2d_16(&tmA, idx->A, (uint64_t)idx->d_pad, (uint64_t)idx->n_pad, kBlockK, kTileM))
         return set_error(EBR_ECUDA, "cuTensorMapEncodeTiled(A) failed");
@@ -1290,7 +1360,7 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
         set((const void*)score_kernel<1>, big);
         set((const void*)theta_kernel, 200 * 1024);
         set((const void*)final_kernel, 200 * 1024);
-        set((const void*)entry_sort_kernel, (int)(((size_t)(kBinAdsMax / kTileM) * kCountClasses * kMaxCluster + kSortStage) * 4));
+        set((const void*)entry_order_kernel, kOrderStage * 4);
         for (const void* f : {(const void*)score_kernel<0>, (const void*)score_kernel<1>}) {
             cudaError_t x = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
             (void)x;
@@ -1301,7 +1371,7 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
     const size_t tsmem = 200 * 1024;
     const size_t fsmem = 200 * 1024;
     const int64_t fscap = (int64_t)(fsmem - (size_t)pow2ceil_i(q.k) * 8 - kSelBins * 4) / 8;
-    const double ks = (double)q.k / kSampleStride;
+    const double ks = (double)q.k / (double)L.sstride;
     int rank = (int)std::ceil(ks + 5.0 * std::sqrt(ks) + 8.0);
     if (const char* r = getenv("EBR_THETA_RANK")) rank = atoi(r);   // test hook
     rank = std::max(1, std::min(rank, q.k));
@@ -1313,7 +1383,6 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
     ea.hdr = idx->chunk_hdr; ea.payload = idx->payload;
     ea.n_ads = idx->n_ads; ea.n_pad = idx->n_pad; ea.bin_ads = (int)L.bin_ads;
     ea.n_bins = (int)L.n_bins; ea.n_tiles = n_tiles; ea.bin_cap = L.bin_cap;
-    const size_t ssmem = ((size_t)(kBinAdsMax / kTileM) * kCountClasses * kMaxCluster + kSortStage) * 4;
     ea.NU = (int)L.NU;
 
     for (int b0 = 0; b0 < q.batch; b0 += (int)L.P) {
@@ -1338,16 +1407,16 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
         trace(q.stream, "plan_c");
         entry_bin_kernel<<<8 * idx->sm_count, 256, 0, q.stream>>>(ea, ws);
         trace(q.stream, "entry_bin");
-        entry_sort_kernel<<<(unsigned)L.n_bins, 512, ssmem, q.stream>>>(ea, ws);
-        trace(q.stream, "entry_sort");
+        entry_order_kernel<<<(unsigned)L.n_bins, kOrderThreads, kOrderStage * 4, q.stream>>>(ea, ws);
+        trace(q.stream, "entry_order");
         e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_check(e, "launch(plan/entries)");
 
         GemmParams gp;
         gp.n_ads = idx->n_ads; gp.n_pad = idx->n_pad; gp.dense = 0; gp.ad_begin = (uint32_t)idx->ad_begin;
         gp.n_kb = n_kb; gp.n_hb = tu.n_hb; gp.pieces = tu.pieces; gp.acc_stages = acc_stages; gp.u_cols = u_cols;
-        gp.P = P; gp.n_samp = (int)L.n_samp; gp.stages = stages; gp.cap = cap; gp.rerun = 0;
-        gp.hot_mask = reinterpret_cast<const uint4*>(idx->hot_mask); gp.ws = ws; gp.err = err_word;
+        gp.P = P; gp.n_samp = (int)L.n_samp; gp.stages = stages; gp.smem_bytes = (int)smem; gp.cap = cap; gp.rerun = 0;
+        gp.hot_mask = reinterpret_cast<const uint4*>(idx->hot_mask); gp.A = idx->A; gp.ws = ws; gp.err = err_word;
         static const int diag = getenv("EBR_DIAG") ? atoi(getenv("EBR_DIAG")) : 0;
         gp.diag = diag;
         gp.NU = (int)L.NU; gp.gcap = (int)L.gcap; gp.n_tiles_all = n_tiles;
@@ -1388,11 +1457,11 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
         int32_t* oi = q.out_ids ? q.out_ids + (size_t)b0 * q.k : nullptr;
         float* os = q.out_scores ? q.out_scores + (size_t)b0 * q.k : nullptr;
         uint64_t* ok = q.out_keys ? q.out_keys + (size_t)b0 * q.k : nullptr;
-        e = launch_score(0, n_samp_tiles, kSampleStride, 0);
+        e = launch_score(0, n_samp_tiles, (int)L.sstride, 0);
         if (e != cudaSuccess) return cuda_check(e, "launch(score sample)");
         trace(q.stream, "score sample");
         theta_kernel<<<P, kThetaThreads, tsmem, q.stream>>>(ws, (int)L.n_samp, rank, (uint32_t)idx->ad_begin, P,
-                                                           tscap_of(rank), 0, idx->n_pad);
+                                                           tscap_of(rank), 0, idx->n_pad, L.sstride);
         trace(q.stream, "theta");
         {
             KernelTimer kt(q.stream, "score_kernel<1> (fused tcgen05 deep + hot + cold wide + kappa + theta filter)");
@@ -1405,11 +1474,11 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
             cudaMemcpyAsync(h, ws.prof, sizeof h, cudaMemcpyDeviceToHost, q.stream);
             cudaStreamSynchronize(q.stream);
             const double c = h[9] ? (double)h[9] : 1.0;
-            fprintf(stderr, "[ebr prof] per CTA Mcycles (sample+filter): total %.2f tma_wait_empty %.2f mma_wait_wready %.2f "
-                            "mma_wait_full %.2f hot_wait_empty %.2f wide_cold %.2f wide_wait_tempty %.2f wide_store %.2f "
-                            "epi_wait_tfull %.2f epi_work %.2f (CTAs %llu)\n",
+            fprintf(stderr, "[ebr prof] per CTA Mcycles (sample+filter): total %.2f tma_wait_empty %.2f mma_wait_tempty %.2f "
+                            "mma_wait_full %.2f hot_wait_empty %.2f wide_cold %.2f wide_wait_cempty %.2f epi_wait_cfull %.2f "
+                            "epi_wait_tfull %.2f epi_work %.2f wide_wait_efull %.2f (CTAs %llu)\n",
                     h[10] / c / 1e6, h[0] / c / 1e6, h[1] / c / 1e6, h[2] / c / 1e6, h[3] / c / 1e6, h[4] / c / 1e6,
-                    h[5] / c / 1e6, h[6] / c / 1e6, h[7] / c / 1e6, h[8] / c / 1e6, h[9]);
+                    h[5] / c / 1e6, h[6] / c / 1e6, h[7] / c / 1e6, h[8] / c / 1e6, h[11] / c / 1e6, h[9]);
             cudaMemsetAsync(ws.prof, 0, sizeof h, q.stream);
         }
         final_kernel<<<P, 512, fsmem, q.stream>>>(ws, cap, q.k, P, oi, os, ok, fscap, 0, rank, err_word);
@@ -1420,7 +1489,7 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
         if (e != cudaSuccess) return cuda_check(e, "launch(score dense)");
         trace(q.stream, "score dense");
         theta_kernel<<<P, kThetaThreads, tsmem, q.stream>>>(ws, (int)L.n_samp, q.k, (uint32_t)idx->ad_begin, P,
-                                                           tscap_of(q.k), 1, idx->n_pad);
+                                                           tscap_of(q.k), 1, idx->n_pad, L.sstride);
         trace(q.stream, "theta rerun");
         e = launch_score(1, n_tiles, 1, 1);
         if (e != cudaSuccess) return cuda_check(e, "launch(score rerun)");

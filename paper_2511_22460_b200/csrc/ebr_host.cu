@@ -345,6 +345,98 @@ __global__ void __launch_bounds__(kThreads) merge_kernel(const uint64_t* __restr
     cta_write_topk(sbuf, nsel, K, out_ids + (size_t)b * K, out_scores + (size_t)b * K, nullptr);
 }
 
+// Threshold exchange (reading R24): with G shards, theta_u = min over ranks of
+// each rank's ceil(K/G)-th local key is a lower bound of the global K-th key (every rank holds
+// >= ceil(K/G) keys >= theta_u, so >= K keys overall), and every global top-K key is >= theta_u and
+// inside its rank's local top K -- each rank only needs to send its local keys >= theta_u.
+__global__ void kth_key_kernel(const uint64_t* __restrict__ keys, int B, int K, int kk, uint64_t* out) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < B) out[b] = keys[(size_t)b * K + (kk - 1)];
+}
+
+// one CTA: theta_u, the count of local keys >= theta_u (keys are descending, padding 0), the
+// exclusive scan of the counts (out_off[B] = total) and the packed keys
+__global__ void __launch_bounds__(1024) exchange_pack_kernel(const uint64_t* __restrict__ keys, int B, int K,
+                                                             const uint64_t* __restrict__ kq, int G,
+                                                             uint32_t* out_count, uint32_t* out_off,
+                                                             uint64_t* out_packed) {
+    __shared__ uint32_t scratch[40];
+    __shared__ uint32_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int b0 = 0; b0 < B; b0 += blockDim.x) {
+        const int b = b0 + threadIdx.x;
+        uint32_t c = 0;
+        if (b < B) {
+            uint64_t th = ~0ull;
+            for (int r = 0; r < G; ++r) th = min(th, kq[(size_t)r * B + b]);
+            const uint64_t* kb = keys + (size_t)b * K;
+            // first index with key < theta (or key == 0): binary search on the descending list
+            int lo = 0, hi = K;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                const uint64_t x = kb[mid];
+                if (x != 0 && x >= th) lo = mid + 1;
+                else hi = mid;
+            }
+            c = (uint32_t)lo;
+            out_count[b] = c;
+        }
+        uint32_t tot;
+        const uint32_t pre = block_exclusive_scan(c, scratch, &tot) + carry;
+        if (b < B) out_off[b] = pre;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out_off[B] = carry;
+    __syncthreads();
+    // pack: user b's first count[b] keys to out_packed[off[b] ...] (one warp per user)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int b = warp; b < B; b += nw) {
+        const uint32_t c = out_count[b], o = out_off[b];
+        for (uint32_t j = lane; j < c; j += 32) out_packed[o + j] = keys[(size_t)b * K + j];
+    }
+}
+
+// merge of packed per-rank lists: user b's candidates are, for every rank r, packed[r][off_r(b) ..
+// off_r(b) + count_r(b)) with off_r the exclusive scan of count_r (counts [G][B])
+__global__ void __launch_bounds__(kThreads) merge_packed_kernel(const uint64_t* __restrict__ packed, int64_t stride,
+                                                                const uint32_t* __restrict__ counts, int G, int B,
+                                                                int K, int32_t* out_ids, float* out_scores) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint32_t sScalar[8];
+    __shared__ int64_t sOff[16], sBeg[17];
+    const int P = pow2ceil_i(K);
+    uint64_t* sbuf = reinterpret_cast<uint64_t*>(smem);
+    uint32_t* shist = reinterpret_cast<uint32_t*>(sbuf + P);
+    const int b = blockIdx.x;
+    // offsets of user b in every rank's packed list (warp r sums count_r[0..b))
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp < G) {
+        uint64_t s = 0;
+        for (int u = lane; u < b; u += 32) s += counts[(size_t)warp * B + u];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+        if (lane == 0) sOff[warp] = (int64_t)s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int64_t t = 0;
+        for (int r = 0; r < G; ++r) { sBeg[r] = t; t += counts[(size_t)r * B + b]; }
+        sBeg[G] = t;
+    }
+    __syncthreads();
+    const int64_t n = sBeg[G];
+    auto get = [=](int64_t i) {
+        int r = 0;
+        while (i >= sBeg[r + 1]) ++r;
+        return __ldg(&packed[(size_t)r * stride + sOff[r] + (i - sBeg[r])]);
+    };
+    const int nsel = cta_select_topk(get, n, K, sbuf, nullptr, 0, shist, sScalar);
+    cta_write_topk(sbuf, nsel, K, out_ids + (size_t)b * K, out_scores + (size_t)b * K, nullptr);
+}
+
 __global__ void decode_key_kernel(const uint2* __restrict__ hdr, const uint32_t* __restrict__ payload,
                                   uint32_t c0, uint32_t c1, uint32_t kwb, int32_t* out, int64_t cap) {
     const int lane = threadIdx.x & 31;
@@ -744,6 +836,37 @@ ebr_status ebr_score_topk_host(const ebr_index* idx, const void* user_emb_host, 
     }
     if (prev >= 0 && prev != idx->device) cudaSetDevice(prev);
     return EBR_OK;
+}
+
+ebr_status ebr_exchange_kth(const uint64_t* local_keys, int32_t batch, int32_t k, int32_t G, uint64_t* out_kq,
+                            void* stream) {
+    if (!local_keys || !out_kq) return set_error(EBR_EINVAL, "null pointer");
+    if (G < 1 || G > 16 || batch < 1 || k < 1 || k > EBR_MAX_K) return set_error(EBR_EINVAL, "bad G/batch/k");
+    const int kk = (k + G - 1) / G;
+    kth_key_kernel<<<(batch + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(local_keys, batch, k, kk, out_kq);
+    return cuda_check(cudaGetLastError(), "launch(kth)");
+}
+
+ebr_status ebr_exchange_pack(const uint64_t* local_keys, int32_t batch, int32_t k, const uint64_t* kq_gathered,
+                             int32_t G, uint32_t* out_count, uint32_t* out_off, uint64_t* out_packed, void* stream) {
+    if (!local_keys || !kq_gathered || !out_count || !out_off || !out_packed)
+        return set_error(EBR_EINVAL, "null pointer");
+    if (G < 1 || G > 16 || batch < 1 || k < 1 || k > EBR_MAX_K) return set_error(EBR_EINVAL, "bad G/batch/k");
+    exchange_pack_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(local_keys, batch, k, kq_gathered, G,
+                                                                          out_count, out_off, out_packed);
+    return cuda_check(cudaGetLastError(), "launch(exchange pack)");
+}
+
+ebr_status ebr_merge_topk_packed(const uint64_t* packed, int64_t stride, const uint32_t* counts, int32_t G,
+                                 int32_t batch, int32_t k, int32_t* out_ids, float* out_scores, void* stream) {
+    if (!packed || !counts || !out_ids || !out_scores) return set_error(EBR_EINVAL, "null pointer");
+    if (G < 1 || G > 16 || batch < 1 || k < 1 || k > EBR_MAX_K || stride < 0)
+        return set_error(EBR_EINVAL, "bad G/batch/k/stride");
+    const size_t smem = (size_t)pow2ceil_i(k) * 8 + kSelBins * 4 + 64;
+    EBR_CUDA(cudaFuncSetAttribute(merge_packed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    merge_packed_kernel<<<batch, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(packed, stride, counts, G,
+                                                                                     batch, k, out_ids, out_scores);
+    return cuda_check(cudaGetLastError(), "launch(merge packed)");
 }
 
 size_t ebr_merge_workspace_bytes(int32_t G, int32_t batch, int32_t k) {

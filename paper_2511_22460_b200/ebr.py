@@ -47,6 +47,9 @@ EXPORTS = {
     "ebr_encode_host": (ctypes.c_int, [_P, _I64, _I32, _P, _I64, _P, _P, _P, _I64, _P, _I64,
                                        ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     "ebr_query_launches": (_I32, [_P, _I32, _I32, _I32]),
+    "ebr_exchange_kth": (ctypes.c_int, [_P, _I32, _I32, _I32, _P, _P]),
+    "ebr_exchange_pack": (ctypes.c_int, [_P, _I32, _I32, _P, _I32, _P, _P, _P, _P]),
+    "ebr_merge_topk_packed": (ctypes.c_int, [_P, _I64, _P, _I32, _I32, _I32, _P, _P, _P]),
     "ebr_kernel_timer": (ctypes.c_int, [_I32]),
     "ebr_kernel_timer_read": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64),
                                              ctypes.c_char_p, _I32]),
@@ -253,6 +256,26 @@ def merge_topk(gathered, G: int, batch: int, k: int, out_ids, out_scores, stream
     _check(_lib.ebr_merge_topk(_t_ptr(gathered), G, batch, k, _t_ptr(out_ids), _t_ptr(out_scores),
                                None, 0, _stream_ptr(stream)),
            "ebr_merge_topk")
+
+
+def exchange_kth(local_keys, G: int, out_kq, stream=None):
+    B, k = local_keys.shape
+    _check(_lib.ebr_exchange_kth(_t_ptr(local_keys), B, k, G, _t_ptr(out_kq), _stream_ptr(stream)),
+           "ebr_exchange_kth")
+
+
+def exchange_pack(local_keys, kq_gathered, G: int, out_count, out_off, out_packed, stream=None):
+    B, k = local_keys.shape
+    _check(_lib.ebr_exchange_pack(_t_ptr(local_keys), B, k, _t_ptr(kq_gathered), G, _t_ptr(out_count),
+                                  _t_ptr(out_off), _t_ptr(out_packed), _stream_ptr(stream)),
+           "ebr_exchange_pack")
+
+
+def merge_topk_packed(packed, counts, G: int, batch: int, k: int, out_ids, out_scores, stream=None):
+    """packed: [G][stride] int64 (kappa bits), counts: [G][batch] int32 (uint32 bits)."""
+    _check(_lib.ebr_merge_topk_packed(_t_ptr(packed), packed.shape[1], _t_ptr(counts), G, batch, k,
+                                      _t_ptr(out_ids), _t_ptr(out_scores), _stream_ptr(stream)),
+           "ebr_merge_topk_packed")
 
 
 def encode_host(ad_feat: np.ndarray, field_card: np.ndarray):

@@ -86,9 +86,18 @@ def field_cards(n_ads: int, n_fields: int) -> np.ndarray:
 
 def f32_to_bf16_bits(x: np.ndarray) -> np.ndarray:
     """Round-to-nearest-even fp32 -> bf16 bit pattern (finite inputs)."""
-    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
-    r = (u + 0x7FFF + ((u >> 16) & 1)) >> 16
-    return r.astype(np.uint16)
+    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32)
+    out = np.empty(u.shape, dtype=np.uint16)
+    fo, fu = out.reshape(-1), u.reshape(-1)
+    step = 1 << 24
+    for lo in range(0, fu.size, step):       # uint32 is enough: finite inputs stay below 2^32
+        c = fu[lo:lo + step]
+        r = (c >> 16) & np.uint32(1)
+        r += c
+        r += np.uint32(0x7FFF)
+        r >>= 16
+        fo[lo:lo + step] = r
+    return out
 
 
 def bf16_bits_to_f32(b: np.ndarray) -> np.ndarray:

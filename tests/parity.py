@@ -19,11 +19,38 @@ def oracle_full(o, users, b):
     return o.scores(users.user_emb[b], users.user_feat[b], users.user_x[b])
 
 
+def topk_order(r, kk):
+    """The first kk ads of the (score desc, id asc) order of r."""
+    n = r.shape[0]
+    if n > 4 * kk + 1024:
+        # O(n): every ad at or above the kk-th largest score (ties included), then the exact
+        # order of that subset -- the same prefix as the full lexsort
+        s_k = np.partition(r, n - kk)[n - kk]
+        sub = np.nonzero(r >= s_k)[0]
+        return sub[np.lexsort((sub, -r[sub]))][:kk]
+    return np.lexsort((np.arange(n), -r))[:kk]
+
+
+def check_many(o, users, ids, sc, k, mode, sel=None, threads=None, id_base=0):
+    """check_user for the users `sel` (default all), oracle scoring in a thread pool (the ctypes
+    oracle call and numpy's partition release the GIL).  Returns the summed id mismatches."""
+    import concurrent.futures as cf
+    import os
+    sel = list(range(users.batch)) if sel is None else list(sel)
+    threads = threads or min(len(sel), os.cpu_count() or 1)
+
+    def one(b):
+        r, s = o.scores(users.user_emb[b], users.user_feat[b], users.user_x[b])
+        return check_user(ids[b], sc[b], r, s, k, mode, id_base=id_base)
+    with cf.ThreadPoolExecutor(max_workers=threads) as ex:
+        return sum(ex.map(one, sel))
+
+
 def check_user(ids, scores, r, sigma, k, mode, tol=TOL_F32, id_base=0):
     """ids/scores: one user's GPU output (k,); r/sigma: oracle fp64 arrays over the inventory."""
     n = r.shape[0]
-    order = np.lexsort((np.arange(n), -r))[:k]
     kk = min(k, n)
+    order = topk_order(r, kk)
     ids = np.asarray(ids)
     scores = np.asarray(scores)
     # padding

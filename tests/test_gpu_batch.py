@@ -61,7 +61,7 @@ def test_batch_equals_latency_path(ebr):
 def test_batch_overflow_falls_back_exactly(ebr):
     inv, users = synth.make_config("C3", mode="exact", n_ads=40_000, batch=20)
     idx = ebr.Index.of(inv)
-    os.environ["EBR_TEST_CAND_CAP"] = "300"       # < 16 K: every user overflows
+    os.environ["EBR_TEST_CAND_CAP"] = "700"       # below the ~1 K candidates of a user: every user overflows
     try:
         (ids, sc), _ = run(ebr, idx, users, 100)
     finally:
