@@ -84,6 +84,22 @@ ebr_status ebr_build_index(const void *ad_emb, ebr_dtype dtype, int64_t ad_begin
                            const int32_t *field_card, const float *cross_w, int64_t n_keys,
                            int device, void *stream, ebr_index **out);
 
+/*
+ * Same contract and result as ebr_build_index, with the inverted list built on the DEVICE
+ * (Alg. 1, whose loops are data-parallel): ad_feat is uploaded,
+ * (key, ad) pairs are radix-sorted by key on the GPU (stable: lists stay ascending), chunked,
+ * delta-coded and bit-packed by GPU kernels -- the arrays are bit-identical to the host encoder's
+ * (ebr_index_export).  Bounds errors in ad_feat are detected on the device (EBR_EINVAL).  Needs
+ * ~20 B of temporary device memory per (ad, field) slot during the build.  Host-synchronous;
+ * queries on other streams with other indexes keep running meanwhile (double-buffered refresh:
+ * build the new index, swap the handle, free the old one once its queries completed).
+ */
+ebr_status ebr_build_index_device(const void *ad_emb, ebr_dtype dtype, int64_t ad_begin,
+                                  int64_t ad_end, int32_t d, const int32_t *ad_feat,
+                                  int32_t n_fields, const int32_t *field_card,
+                                  const float *cross_w, int64_t n_keys, int device, void *stream,
+                                  ebr_index **out);
+
 void ebr_free_index(ebr_index *idx);
 
 /* ------------------------------------------------------------------------------------------ */
@@ -234,6 +250,15 @@ typedef struct {
     int64_t hot_bytes;    /* device bytes of the one-hot columns H             */
 } ebr_stats;
 ebr_status ebr_index_stats(const ebr_index *idx, ebr_stats *out);
+
+/*
+ * Host-synchronous copy of one device array of the index to out_host (cap_bytes); *bytes
+ * receives its size (out_host = NULL: size only).  which: 0 key_chunk_off [M+1] u32, 1
+ * key_word_off [M] u32, 2 chunk_hdr [C] u32x2, 3 chunk_last [C] u32, 4 payload [W+2] u32,
+ * 5 hot_mask [n_pad] u32x4 (0 bytes without hot columns).  Parity support (host vs device build).
+ */
+ebr_status ebr_index_export(const ebr_index *idx, int32_t which, void *out_host, int64_t cap_bytes,
+                            int64_t *bytes);
 
 /*
  * Host-only encoder (no device needed; used to pin the wire format on CPU).  Encodes the

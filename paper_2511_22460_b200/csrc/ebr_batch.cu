@@ -53,7 +53,7 @@ constexpr int kBlockBytes = kTileM * 128;   // one ring stage: 128 rows x 128 B
 constexpr int kSampleStride = 16;    // every 16th tile (at least) is sampled for theta
 constexpr int kSampleStrideMax = 64; // ... and every 64th on large inventories (sample_stride())
 #ifndef EBR_WIDE_WARPS
-#define EBR_WIDE_WARPS 8
+#define EBR_WIDE_WARPS 16
 #endif
 constexpr int kWideWarp0 = 4, kWideWarps = EBR_WIDE_WARPS, kWideThreads = 32 * kWideWarps;
 constexpr int kEpiWarp0 = kWideWarp0 + kWideWarps, kEpiWarps = 8;
@@ -66,7 +66,10 @@ constexpr int kBinAdShift = 14;      // level-1 bin entry = ad in bin << 14 | un
 constexpr int kBinAds = 1024;        // ads per entry bin (8 tiles)
 constexpr int kOrderStage = 16384;   // bin entries staged in shared memory by entry_order (64 KB)
 constexpr int kQuarters = 4;         // 32-ad quarters of a tile (the cold ring's unit in score_kernel)
-constexpr int kInlinePairs = 4;      // pairs of an entry scattered by its own thread; the rest of a
+#ifndef EBR_INLINE_PAIRS
+#define EBR_INLINE_PAIRS 16
+#endif
+constexpr int kInlinePairs = EBR_INLINE_PAIRS;   // pairs of an entry scattered by its own thread; the rest of a
                                      // heavy entry goes to a shared list scattered by whole warps
 constexpr int kHeavyCap = 1024;      // heavy entries per quarter (shared list; overflow -> inline)
 constexpr int kOrderThreads = 512;
@@ -79,16 +82,16 @@ constexpr int kMaxAccStages = 3;
 constexpr int kMaxStages = 8;        // deep A ring stages (16 KB each; as many as the shared memory allows)
 constexpr int kPrefetchTiles = 4;    // tiles of A prefetched into L2 ahead of the ring's TMA loads
 constexpr int kHotStages = 2;        // ring of on-chip generated one-hot K blocks
-constexpr int kColdQuarter = 32 * kGroup;   // int32 words of a cold quarter buffer [32 ads][128 users]
+constexpr int kAccPitch = kGroup + 4; // int32 words per fixed-point row of the cold tile [users][ads]
 constexpr int kEntBuf = 2048;        // entries of a tile staged in shared memory (bulk copy; the rest from L2)
 constexpr int kEntHdr = 16;          // words of an entry buffer's header (quarter bounds, copied count)
 // shared memory of the fused kernel next to the A ring and the pairs: the hot ring, the cold
 // quarter buffers, 2 entry buffers, the byte -> one-hot table, the heavy list, barriers and
 // per-user scalars
 __host__ __device__ constexpr size_t score_smem_fixed() {
-    return (size_t)kHotStages * kBlockBytes + (size_t)kQuarters * kColdQuarter * 4 + 2 * (size_t)(kEntBuf + kEntHdr) * 4 +
+    return (size_t)kHotStages * kBlockBytes + (size_t)kGroup * kAccPitch * 4 + 2 * (size_t)(kEntBuf + kEntHdr) * 4 +
            256 * 16 + (size_t)kHeavyCap * 4 + 16 +
-           (size_t)(2 * kMaxStages + 2 * kHotStages + 2 * kMaxAccStages + 2 * kQuarters + 4 + 1) * 8 + 16 +
+           (size_t)(2 * kMaxStages + 2 * kHotStages + 3 * kMaxAccStages + 4 + 1) * 8 + 16 +
            (size_t)kGroup * 20;
 }
 
@@ -632,8 +635,8 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
 
     unsigned char* sRing = smem;                                            // [nring][128 ads x 128 B] deep blocks of A
     unsigned char* sHot = sRing + (size_t)nring * kBlockBytes;              // [kHotStages][128 ads x 128 B] one-hot blocks
-    int32_t* sCold = reinterpret_cast<int32_t*>(sHot + (size_t)kHotStages * kBlockBytes);   // [4][32 ads][128 users]
-    uint32_t* sEnt = reinterpret_cast<uint32_t*>(sCold + kQuarters * kColdQuarter);   // [2][kEntHdr + kEntBuf]
+    int32_t* sAcc = reinterpret_cast<int32_t*>(sHot + (size_t)kHotStages * kBlockBytes);   // [128 users][kAccPitch]
+    uint32_t* sEnt = reinterpret_cast<uint32_t*>(sAcc + kGroup * kAccPitch);  // [2][kEntHdr + kEntBuf]
     uint4* sLut = reinterpret_cast<uint4*>(sEnt + 2 * (kEntHdr + kEntBuf));  // [256] byte -> 8 fp16 {0, 1}
     uint32_t* sHeavy = reinterpret_cast<uint32_t*>(sLut + 256);              // [kHeavyCap] heavy entries' rest
     uint32_t* sHeavyN = sHeavy + kHeavyCap;                                  // [2] counts by quarter parity
@@ -644,9 +647,8 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
     uint64_t* hempty = hfull + kHotStages;
     uint64_t* tfull = hempty + kHotStages;          // [kMaxAccStages] TMEM accumulator stages
     uint64_t* tempty = tfull + kMaxAccStages;
-    uint64_t* cfull = tempty + kMaxAccStages;       // [4] cold quarter buffers
-    uint64_t* cempty = cfull + kQuarters;
-    uint64_t* efull = cempty + kQuarters;           // [2] entry buffers
+    uint64_t* wready = tempty + kMaxAccStages;      // [kMaxAccStages] cold tile stored into the stage
+    uint64_t* efull = wready + kMaxAccStages;       // [2] entry buffers
     uint64_t* eempty = efull + 2;
     uint64_t* aready = eempty + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aready + 1);
@@ -665,17 +667,14 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
             mbar_init(&tfull[s], 1);
             mbar_init(&tempty[s], kEpiWarps);
         }
-        for (int q = 0; q < kQuarters; ++q) {
-            mbar_init(&cfull[q], 1);
-            mbar_init(&cempty[q], 4);                   // the 4 epilogue warps (user quadrants) of the quarter
-        }
+        for (int s = 0; s < kMaxAccStages; ++s) mbar_init(&wready[s], 1);
         mbar_init(aready, 4);
         fence_mbar_init();
     }
     if (warp == 2) tc::tmem_alloc(tmem_slot, 512);
     if (tid == 0) { sHeavyN[0] = 0u; sHeavyN[1] = 0u; }
-    for (int i = tid; i < kQuarters * kColdQuarter / 4; i += kGemmThreads)
-        reinterpret_cast<int4*>(sCold)[i] = make_int4(0, 0, 0, 0);
+    for (int i = tid; i < kGroup * kAccPitch / 4; i += kGemmThreads)
+        reinterpret_cast<int4*>(sAcc)[i] = make_int4(0, 0, 0, 0);
     for (int b = tid; b < 256; b += kGemmThreads) {
         auto h2 = [b](int k) { return ((b >> k) & 1 ? 0x3C00u : 0u) | ((b >> (k + 1)) & 1 ? 0x3C000000u : 0u); };
         sLut[b] = make_uint4(h2(0), h2(2), h2(4), h2(6));
@@ -780,8 +779,8 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
     } else if (warp == 1) {
         if (lane == 0) {
             // ---------------- MMA issuer ----------------
-            // D = U A^T (deep, the first MMA of a tile overwrites the stage) + U_hot (one-hot)^T;
-            // the cold wide term is added by the epilogue from the shared-memory quarter ring.
+            // The accumulator stage already holds the tile's cold wide term (stored by the wide
+            // warps), so every MMA accumulates: D = cold + U A^T + U_hot (one-hot)^T.
             const uint32_t idb = tc::idesc_bf16_m128(kTileM), idh = tc::idesc_f16_m128(kTileM);
             mbar_wait_sleep(aready, 0);                   // users' A operand in TMEM
             tc::fence_after();
@@ -789,7 +788,7 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
             uint32_t gb = 0, hb = 0;
             for (int t = (int)cid; t < p.n_tiles; t += (int)ncl, ++it) {
                 const int st = it % nst;
-                if (it >= nst) { EBR_PROF_T0; mbar_wait_sleep(&tempty[st], ((it / nst) - 1) & 1); EBR_PROF_ADD(1); }
+                { EBR_PROF_T0; mbar_wait_sleep(&wready[st], (it / nst) & 1); EBR_PROF_ADD(1); }
                 tc::fence_after();
                 const uint32_t d_tmem = tmem_base + (uint32_t)(a_cols + st * kTileM);
                 for (int kb = 0; kb < p.n_kb; ++kb, ++gb) {
@@ -799,8 +798,7 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
                     const uint64_t db0 = tc::sdesc_sw128(sRing + (size_t)slot * kBlockBytes);
 #pragma unroll
                     for (int k = 0; k < kBlockK / 16; ++k)
-                        tc::umma_f16_ts(d_tmem, tmem_base + (uint32_t)(kb * 32 + k * 8), db0 + (uint64_t)(k * 2), idb,
-                                        (kb | k) ? 1u : 0u);
+                        tc::umma_f16_ts(d_tmem, tmem_base + (uint32_t)(kb * 32 + k * 8), db0 + (uint64_t)(k * 2), idb, 1u);
                     if (csize == 1) tc::umma_commit(&empty[slot]);
                     else tc::umma_commit_mc(&empty[slot], mc_mask);
                 }
@@ -882,80 +880,103 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
             __syncwarp();
             if (lane == 0) mbar_arrive(aready);
         }
-        // Per tile quarter (32 ads): its entries (ad row, the slot's first pair, pair count) of
-        // this CTA's group stream, staged in shared memory by the producer's bulk copy; each pair
-        // (user, w~ 2^S) is added to the quarter buffer [32 ads][128 users] with a native 32-bit
-        // shared atomic (exact, order-free; Alg. 2 l.358).  An entry's first kInlinePairs pairs are
-        // scattered by its thread, a heavy entry's rest by whole warps.
+        // Per tile: its entries (ad row, the slot's first pair, pair count) of this CTA's group
+        // stream, staged in shared memory by the producer's bulk copy; each pair (user, w~ 2^S) is
+        // added to the tile [128 users][128 ads] with a native 32-bit shared atomic (exact,
+        // order-free; Alg. 2 l.358).  Then the tile is converted once to fp32 and stored into the
+        // TMEM accumulator stage, which the tensor core accumulates onto.
         const uint32_t* __restrict__ entries = p.ws.gentries;
+        const int q = warp & 3;                          // TMEM lane quadrant = users 32q .. 32q + 31
+        const int cj = (warp - kWideWarp0) >> 2;         // this warp's 32-ad column chunk (store phase)
+        const int urow = q * 32 + lane;
+        const float uscale = sScale[urow];
         int it = 0;
         for (int t = (int)cid; t < p.n_tiles; t += (int)ncl, ++it) {
+            const int st = it % nst;
             const int eb = it & 1;
             { EBR_PROF_T0; mbar_wait_sleep(&efull[eb], (it >> 1) & 1); if (wt == 0) EBR_PROF_ADD(11); }
+            const long long _pc0 = (p.diag & 4) ? clock64() : 0;
             const uint32_t* hdr = sEnt + eb * (kEntHdr + kEntBuf);
             const uint32_t* ebuf = hdr + kEntHdr;
             const uint32_t ebase = hdr[kQuarters + 1], ncopy = hdr[kQuarters + 2];
-            for (int q = 0; q < kQuarters; ++q) {
-                // the quarter buffer is free once the epilogue drained it (previous tile)
-                if (it > 0) { EBR_PROF_T0; mbar_wait_sleep(&cempty[q], (it - 1) & 1); if (wt == 0) EBR_PROF_ADD(5); }
-                const long long _pc0 = (p.diag & 4) ? clock64() : 0;
-                int32_t* buf = sCold + q * kColdQuarter;
-                const uint32_t e0 = hdr[q], e1 = hdr[q + 1];
-                for (uint32_t ei = e0 + wt; ei < e1; ei += kWideThreads) {
-                    const uint32_t en = ei < ncopy ? ebuf[ei] : __ldcs(&entries[ebase + ei]);
-                    const uint32_t a = (en >> 24) & 31u, lo = (en >> 8) & 0xFFFFu, c = en & 0xFFu;
+            const uint32_t e0 = hdr[0], e1 = hdr[kQuarters];
+            for (uint32_t ei = e0 + wt; ei < e1; ei += kWideThreads) {
+                const uint32_t en = ei < ncopy ? ebuf[ei] : __ldcs(&entries[ebase + ei]);
+                const uint32_t a = en >> 24, lo = (en >> 8) & 0xFFFFu, c = en & 0xFFu;
 #pragma unroll
-                    for (uint32_t qq = 0; qq < (uint32_t)kInlinePairs; ++qq) {
-                        if (qq < c) {
+                for (uint32_t qq = 0; qq < (uint32_t)kInlinePairs; ++qq) {
+                    if (qq < c) {
+                        const uint32_t pr = sPairs[lo + qq];
+                        atomicAdd(&sAcc[(pr & (kGroup - 1)) * kAccPitch + a], (int32_t)pr >> kPairUBits);
+                    }
+                }
+                if (c > (uint32_t)kInlinePairs) {
+                    const uint32_t hslot = atomicAdd(&sHeavyN[it & 1], 1u);
+                    const uint32_t rest = (a << 24) | ((lo + kInlinePairs) << 8) | (c - kInlinePairs);
+                    if (hslot < (uint32_t)kHeavyCap) {
+                        sHeavy[hslot] = rest;
+                    } else {
+                        for (uint32_t qq = kInlinePairs; qq < c; ++qq) {
                             const uint32_t pr = sPairs[lo + qq];
-                            atomicAdd(&buf[a * kGroup + (pr & (kGroup - 1))], (int32_t)pr >> kPairUBits);
+                            atomicAdd(&sAcc[(pr & (kGroup - 1)) * kAccPitch + a], (int32_t)pr >> kPairUBits);
                         }
                     }
-                    if (c > (uint32_t)kInlinePairs) {
-                        const uint32_t hslot = atomicAdd(&sHeavyN[q & 1], 1u);
-                        const uint32_t rest = (a << 24) | ((lo + kInlinePairs) << 8) | (c - kInlinePairs);
-                        if (hslot < (uint32_t)kHeavyCap) {
-                            sHeavy[hslot] = rest;
-                        } else {
-                            for (uint32_t qq = kInlinePairs; qq < c; ++qq) {
-                                const uint32_t pr = sPairs[lo + qq];
-                                atomicAdd(&buf[a * kGroup + (pr & (kGroup - 1))], (int32_t)pr >> kPairUBits);
-                            }
-                        }
+                }
+            }
+            tc::named_bar_sync(1, kWideThreads);
+            // heavy entries' remaining pairs (keys queried by > kInlinePairs users of the group),
+            // a warp per entry with the lanes over its pairs
+            const uint32_t nh = min(sHeavyN[it & 1], (uint32_t)kHeavyCap);
+            if (nh) {
+                for (uint32_t h = (uint32_t)(wt >> 5); h < nh; h += kWideWarps) {
+                    const uint32_t hv = sHeavy[h];
+                    const uint32_t a = hv >> 24, lo = (hv >> 8) & 0xFFFFu, c = hv & 0xFFu;
+                    for (uint32_t qq = (uint32_t)lane; qq < c; qq += 32) {
+                        const uint32_t pr = sPairs[lo + qq];
+                        atomicAdd(&sAcc[(pr & (kGroup - 1)) * kAccPitch + a], (int32_t)pr >> kPairUBits);
                     }
                 }
                 tc::named_bar_sync(1, kWideThreads);
-                // the heavy entries' remaining pairs, a warp per entry (lanes over pairs)
-                const uint32_t nh = min(sHeavyN[q & 1], (uint32_t)kHeavyCap);
-                if (nh) {
-                    for (uint32_t h = (uint32_t)(wt >> 5); h < nh; h += kWideWarps) {
-                        const uint32_t hv = sHeavy[h];
-                        const uint32_t a = hv >> 24, lo = (hv >> 8) & 0xFFFFu, c = hv & 0xFFu;
-                        for (uint32_t qq = (uint32_t)lane; qq < c; qq += 32) {
-                            const uint32_t pr = sPairs[lo + qq];
-                            atomicAdd(&buf[a * kGroup + (pr & (kGroup - 1))], (int32_t)pr >> kPairUBits);
-                        }
-                    }
-                    tc::named_bar_sync(1, kWideThreads);
-                }
-                if (wt == 0) {
-                    sHeavyN[q & 1] = 0u;      // (the other parity's counter is the next quarter's)
-                    mbar_arrive(&cfull[q]);
-                    if (q == kQuarters - 1) mbar_arrive(&eempty[eb]);   // entry buffer consumed
-                }
-                if ((p.diag & 4) && wt == 0) atomicAdd(&p.ws.prof[4], (unsigned long long)(clock64() - _pc0));
             }
+            if (wt == 0) {
+                sHeavyN[it & 1] = 0u;          // (the other parity's counter is the next tile's)
+                mbar_arrive(&eempty[eb]);      // entry buffer consumed
+            }
+            if ((p.diag & 4) && wt == 0) atomicAdd(&p.ws.prof[4], (unsigned long long)(clock64() - _pc0));
+            // the accumulator stage is free once the epilogue drained it (nst tiles ago)
+            if (it >= nst) { EBR_PROF_T0; mbar_wait_sleep(&tempty[st], ((it / nst) - 1) & 1); if (wt == 0) EBR_PROF_ADD(5); }
+            const long long _ps0 = (p.diag & 4) ? clock64() : 0;
+            tc::fence_after();
+            {
+                // this user's 32 ads of the tile: fixed point -> fp32 (the one rounding), zeroed
+                int4* src = reinterpret_cast<int4*>(sAcc + urow * kAccPitch + cj * 32);
+                uint32_t f[32];
+#pragma unroll
+                for (int v4 = 0; v4 < 8; ++v4) {
+                    const int4 v = src[v4];
+                    src[v4] = make_int4(0, 0, 0, 0);
+                    f[4 * v4 + 0] = __float_as_uint((float)v.x * uscale);
+                    f[4 * v4 + 1] = __float_as_uint((float)v.y * uscale);
+                    f[4 * v4 + 2] = __float_as_uint((float)v.z * uscale);
+                    f[4 * v4 + 3] = __float_as_uint((float)v.w * uscale);
+                }
+                tc::tmem_st32_nowait(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a_cols + st * kTileM + cj * 32), f);
+            }
+            tc::tmem_wait_st();
+            tc::fence_before();
+            tc::named_bar_sync(1, kWideThreads);
+            if (wt == 0) mbar_arrive(&wready[st]);
+            if ((p.diag & 4) && wt == 0) atomicAdd(&p.ws.prof[6], (unsigned long long)(clock64() - _ps0));
         }
     } else if (warp >= kEpiWarp0) {
-        // ---------------- epilogue: TMEM + cold quarter -> s, kappa, sample store / filter ----------------
-        // thread = one user (TMEM lane) x half of the tile's ads (two 32-ad quarters)
+        // ---------------- epilogue: TMEM -> s, kappa, sample store / filter ----------------
+        // thread = one user (TMEM lane) x half of the tile's ads (two 32-column chunks)
         const int e = warp - kEpiWarp0;
         const int q = warp & 3;
         const int ul = q * 32 + lane;                    // CTA-local user
         const int u = g * kGroup + ul;                   // pass user
         const bool uok = ul < nu;
         const int hf = e >> 2;
-        const float uscale = sScale[ul];
         float thS = 0.f;
         uint64_t th = 0;
         int dslot = -1;
@@ -974,17 +995,6 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
                 const int c = qi * 32;
                 uint32_t r[32];
                 tc::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a_cols + st * kTileM + c), r);
-                // the cold wide term of the quarter: fixed point -> fp32 (the one rounding), zeroed
-                { EBR_PROF_T0; mbar_wait_sleep(&cfull[qi], it & 1); if (warp == kEpiWarp0 && lane == 0) EBR_PROF_ADD(6); }
-                int32_t* cb = sCold + qi * kColdQuarter + ul;
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const int32_t v = cb[j * kGroup];
-                    cb[j * kGroup] = 0;
-                    r[j] = __float_as_uint(__uint_as_float(r[j]) + (float)v * uscale);
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&cempty[qi]);
                 if (p.diag & 2) continue;
                 const int64_t ac = a0 + c;
                 const int nval = (int)min((int64_t)32, max((int64_t)0, p.n_ads - ac));   // valid ads in the chunk
@@ -1474,8 +1484,8 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
             cudaMemcpyAsync(h, ws.prof, sizeof h, cudaMemcpyDeviceToHost, q.stream);
             cudaStreamSynchronize(q.stream);
             const double c = h[9] ? (double)h[9] : 1.0;
-            fprintf(stderr, "[ebr prof] per CTA Mcycles (sample+filter): total %.2f tma_wait_empty %.2f mma_wait_tempty %.2f "
-                            "mma_wait_full %.2f hot_wait_empty %.2f wide_cold %.2f wide_wait_cempty %.2f epi_wait_cfull %.2f "
+            fprintf(stderr, "[ebr prof] per CTA Mcycles (sample+filter): total %.2f tma_wait_empty %.2f mma_wait_wready %.2f "
+                            "mma_wait_full %.2f hot_wait_empty %.2f wide_cold %.2f wide_wait_tempty %.2f wide_store %.2f "
                             "epi_wait_tfull %.2f epi_work %.2f wide_wait_efull %.2f (CTAs %llu)\n",
                     h[10] / c / 1e6, h[0] / c / 1e6, h[1] / c / 1e6, h[2] / c / 1e6, h[3] / c / 1e6, h[4] / c / 1e6,
                     h[5] / c / 1e6, h[6] / c / 1e6, h[7] / c / 1e6, h[8] / c / 1e6, h[11] / c / 1e6, h[9]);

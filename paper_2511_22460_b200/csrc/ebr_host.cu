@@ -84,6 +84,8 @@ KernelTimer::~KernelTimer() {
     } while (0)
 
 ebr_status run_small(const QueryArgs& q, int b0, int B);
+ebr_status device_encode(ebr_index* idx, const int32_t* d_feat, const int32_t* d_card, const int32_t* d_base,
+                         cudaStream_t st, std::vector<int64_t>& key_count);
 uint32_t workspace_magic(const ebr_index* idx);
 bool batch_eligible(const ebr_index* idx, int32_t batch, int32_t slots, int32_t k);
 int32_t batch_launches(const ebr_index* idx, int32_t batch, int32_t slots);
@@ -272,16 +274,17 @@ __global__ void hot_mask_kernel(const int32_t* __restrict__ feat, int64_t n, int
     mask[a] = make_uint4(m[0], m[1], m[2], m[3]);
 }
 
-static ebr_status build_hot(ebr_index* idx, const Encoded& enc, const int32_t* ad_feat, cudaStream_t stream) {
+static ebr_status build_hot(ebr_index* idx, const std::vector<int64_t>& key_count, const int32_t* ad_feat,
+                            const int32_t* d_feat_all, cudaStream_t stream) {
     int cap = kMaxHot;
     if (const char* e = getenv("EBR_HOT_KEYS")) cap = std::max(0, std::min(kMaxHot, atoi(e)));
     const int64_t M = idx->n_keys, n = idx->n_ads;
     const int64_t min_count = std::max<int64_t>(64, n / 512);
     std::vector<int32_t> cand;
     for (int64_t k = 0; k < M; ++k)
-        if (enc.key_count[k] >= min_count) cand.push_back((int32_t)k);
+        if (key_count[k] >= min_count) cand.push_back((int32_t)k);
     std::sort(cand.begin(), cand.end(), [&](int32_t x, int32_t y) {
-        return enc.key_count[x] != enc.key_count[y] ? enc.key_count[x] > enc.key_count[y] : x < y;
+        return key_count[x] != key_count[y] ? key_count[x] > key_count[y] : x < y;
     });
     if ((int64_t)cand.size() > cap) cand.resize(cap);
     const int n_hot = (int)((cand.size() + 63) / 64 * 64);
@@ -291,7 +294,7 @@ static ebr_status build_hot(ebr_index* idx, const Encoded& enc, const int32_t* a
     for (size_t h = 0; h < cand.size(); ++h) {
         slot[cand[h]] = (int32_t)h;
         key[h] = cand[h];
-        idx->hot_nnz += enc.key_count[cand[h]];
+        idx->hot_nnz += key_count[cand[h]];
     }
     EBR_CUDA(cudaMalloc(&idx->hot_slot, (size_t)M * 4));
     EBR_CUDA(cudaMemcpyAsync(idx->hot_slot, slot.data(), (size_t)M * 4, cudaMemcpyHostToDevice, stream));
@@ -301,6 +304,11 @@ static ebr_status build_hot(ebr_index* idx, const Encoded& enc, const int32_t* a
     EBR_CUDA(cudaMalloc(&idx->hot_mask, mbytes));
     EBR_CUDA(cudaMemsetAsync(idx->hot_mask, 0, mbytes, stream));
     const int F = idx->n_fields;
+    if (d_feat_all) {           // device build: the values are already on the device
+        hot_mask_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(d_feat_all, n, F, idx->field_base, idx->hot_slot,
+                                                                        static_cast<uint4*>(idx->hot_mask));
+        return cuda_check(cudaGetLastError(), "hot masks");
+    }
     const int64_t chunk = std::max<int64_t>(1, (int64_t)(256 << 20) / (4 * std::max(F, 1)));   // 256 MB of values
     int32_t* dfeat = nullptr;
     EBR_CUDA(cudaMalloc(&dfeat, (size_t)std::min(chunk, n) * F * 4));
@@ -668,7 +676,7 @@ ebr_status ebr_build_index(const void* ad_emb, ebr_dtype dtype, int64_t ad_begin
         EBR_TRY(upload((void**)&idx->field_card, field_card, (size_t)n_fields * 4));
         EBR_TRY(upload((void**)&idx->field_base, fb.data(), (size_t)n_fields * 4));
         if (dtype == EBR_BF16) {
-            st = build_hot(idx, enc, ad_feat, stream);
+            st = build_hot(idx, enc.key_count, ad_feat, nullptr, stream);
             if (st) return fail(st);
         }
         EBR_TRY(cudaStreamSynchronize(stream));
@@ -680,6 +688,126 @@ ebr_status ebr_build_index(const void* ad_emb, ebr_dtype dtype, int64_t ad_begin
     } catch (const std::bad_alloc&) {
         return set_error(EBR_ENOMEM, "host allocation failed");
     }
+}
+
+ebr_status ebr_build_index_device(const void* ad_emb, ebr_dtype dtype, int64_t ad_begin, int64_t ad_end,
+                                  int32_t d, const int32_t* ad_feat, int32_t n_fields,
+                                  const int32_t* field_card, const float* cross_w, int64_t n_keys,
+                                  int device, void* stream_v, ebr_index** out) {
+    auto t0 = std::chrono::steady_clock::now();
+    if (!out) return set_error(EBR_EINVAL, "out is null");
+    *out = nullptr;
+    if (d < 1) return set_error(EBR_EINVAL, "d < 1");
+    if ((int64_t)d * (dtype == EBR_BF16 ? 2 : 4) > 2048)
+        return set_error(EBR_EUNSUPPORTED, "embedding rows above 2 KB (d=%d) are not supported", d);
+    if (dtype != EBR_F32 && dtype != EBR_BF16) return set_error(EBR_EINVAL, "bad dtype");
+    if (ad_begin < 0 || ad_begin >= ad_end) return set_error(EBR_EINVAL, "need 0 <= ad_begin < ad_end");
+    if (ad_end > 0x7FFFFFFFll) return set_error(EBR_EINVAL, "ad_end > 2^31-1");
+    if (!ad_emb || !ad_feat || !field_card || (!cross_w && n_keys > 0))
+        return set_error(EBR_EINVAL, "null input");
+    if (n_fields < 0) return set_error(EBR_EINVAL, "n_fields < 0");
+    int64_t m = 0;
+    for (int f = 0; f < n_fields; ++f) {
+        if (field_card[f] < 1) return set_error(EBR_EINVAL, "field_card[%d] = %d < 1", f, field_card[f]);
+        m += field_card[f];
+    }
+    if (m != n_keys) return set_error(EBR_EINVAL, "n_keys %lld != sum(field_card) %lld", (long long)n_keys, (long long)m);
+    if (n_keys >= (int64_t)1 << 31) return set_error(EBR_EINVAL, "n_keys >= 2^31");
+    const int64_t n = ad_end - ad_begin;
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+    try {
+        int prev = -1;
+        cudaGetDevice(&prev);
+        EBR_CUDA(cudaSetDevice(device));
+        cudaDeviceProp prop;
+        EBR_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10) {
+            if (prev >= 0) cudaSetDevice(prev);
+            return set_error(EBR_EUNSUPPORTED, "device %d is sm_%d%d, this library is built for sm_100a",
+                             device, prop.major, prop.minor);
+        }
+        ebr_index* idx = new ebr_index();
+        memset(idx, 0, sizeof(*idx));
+        idx->device = device;
+        idx->dtype = dtype;
+        idx->d = d;
+        const int esz = dtype == EBR_BF16 ? 2 : 4;
+        idx->d_pad = padded_width(d, esz);
+        idx->n_ads = n;
+        idx->n_pad = (n + 127) / 128 * 128;
+        idx->ad_begin = ad_begin;
+        idx->n_fields = n_fields;
+        idx->n_keys = n_keys;
+        idx->sm_count = prop.multiProcessorCount;
+        int32_t* d_feat = nullptr;
+        auto fail = [&](ebr_status s) {
+            if (d_feat) cudaFree(d_feat);
+            ebr_free_index(idx);
+            if (prev >= 0) cudaSetDevice(prev);
+            return s;
+        };
+#define EBR_TRY(call) do { cudaError_t e__ = (call); if (e__ != cudaSuccess) return fail(cuda_check(e__, #call)); } while (0)
+        const size_t abytes = (size_t)idx->n_pad * idx->d_pad * esz;
+        EBR_TRY(cudaMalloc(&idx->A, abytes));
+        EBR_TRY(cudaMemsetAsync(idx->A, 0, abytes, stream));
+        EBR_TRY(cudaMemcpy2DAsync(idx->A, (size_t)idx->d_pad * esz, ad_emb, (size_t)d * esz, (size_t)d * esz, n,
+                                  cudaMemcpyHostToDevice, stream));
+        auto upload = [&](void** dst, const void* src, size_t bytes) -> cudaError_t {
+            cudaError_t e = cudaMalloc(dst, bytes ? bytes : 4);
+            if (e != cudaSuccess || !bytes) return e;
+            return cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, stream);
+        };
+        EBR_TRY(upload((void**)&d_feat, ad_feat, (size_t)n * n_fields * 4));
+        EBR_TRY(upload((void**)&idx->cross_w, cross_w, (size_t)n_keys * 4));
+        std::vector<int32_t> fb(n_fields);
+        int64_t acc = 0;
+        for (int f = 0; f < n_fields; ++f) { fb[f] = (int32_t)acc; acc += field_card[f]; }
+        EBR_TRY(upload((void**)&idx->field_card, field_card, (size_t)n_fields * 4));
+        EBR_TRY(upload((void**)&idx->field_base, fb.data(), (size_t)n_fields * 4));
+        std::vector<int64_t> key_count;
+        ebr_status st = device_encode(idx, d_feat, idx->field_card, idx->field_base, stream, key_count);
+        if (st) return fail(st);
+        if (dtype == EBR_BF16) {
+            st = build_hot(idx, key_count, ad_feat, d_feat, stream);
+            if (st) return fail(st);
+        }
+        EBR_TRY(cudaStreamSynchronize(stream));
+        cudaFree(d_feat);
+        d_feat = nullptr;
+#undef EBR_TRY
+        idx->build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        if (prev >= 0) cudaSetDevice(prev);
+        *out = idx;
+        return EBR_OK;
+    } catch (const std::bad_alloc&) {
+        return set_error(EBR_ENOMEM, "host allocation failed");
+    }
+}
+
+ebr_status ebr_index_export(const ebr_index* idx, int32_t which, void* out_host, int64_t cap_bytes, int64_t* bytes) {
+    if (!idx || !bytes) return set_error(EBR_EINVAL, "null argument");
+    const void* src = nullptr;
+    int64_t nb = 0;
+    switch (which) {
+        case 0: src = idx->key_chunk_off; nb = (idx->n_keys + 1) * 4; break;
+        case 1: src = idx->key_word_off; nb = idx->n_keys * 4; break;
+        case 2: src = idx->chunk_hdr; nb = idx->n_chunks * 8; break;
+        case 3: src = idx->chunk_last; nb = idx->n_chunks * 4; break;
+        case 4: src = idx->payload; nb = (idx->n_words + 2) * 4; break;
+        case 5: src = idx->hot_mask; nb = idx->hot_mask ? idx->n_pad * 16 : 0; break;
+        default: return set_error(EBR_EINVAL, "which must be 0..5");
+    }
+    *bytes = nb;
+    if (!out_host || cap_bytes < nb) return out_host ? set_error(EBR_EINVAL, "capacity %lld < %lld", (long long)cap_bytes, (long long)nb) : EBR_OK;
+    if (nb) {
+        int prev = -1;
+        cudaGetDevice(&prev);
+        if (prev != idx->device) cudaSetDevice(idx->device);
+        cudaError_t e = cudaMemcpy(out_host, src, (size_t)nb, cudaMemcpyDeviceToHost);
+        if (prev >= 0 && prev != idx->device) cudaSetDevice(prev);
+        if (e != cudaSuccess) return cuda_check(e, "export");
+    }
+    return EBR_OK;
 }
 
 size_t ebr_workspace_bytes(const ebr_index* idx, int32_t batch, int32_t slots, int32_t k) {

@@ -32,6 +32,9 @@ EXPORTS = {
     # name: (restype, argtypes)
     "ebr_build_index": (ctypes.c_int, [_P, ctypes.c_int, _I64, _I64, _I32, _P, _I32, _P, _P, _I64,
                                        ctypes.c_int, _P, ctypes.POINTER(_P)]),
+    "ebr_build_index_device": (ctypes.c_int, [_P, ctypes.c_int, _I64, _I64, _I32, _P, _I32, _P, _P, _I64,
+                                              ctypes.c_int, _P, ctypes.POINTER(_P)]),
+    "ebr_index_export": (ctypes.c_int, [_P, _I32, _P, _I64, ctypes.POINTER(_I64)]),
     "ebr_free_index": (None, [_P]),
     "ebr_workspace_bytes": (_SZ, [_P, _I32, _I32, _I32]),
     "ebr_score_topk": (ctypes.c_int, [_P, _P, _I32, _P, _P, _I32, _I32, _P, _P, _P, _SZ, _P]),
@@ -120,7 +123,7 @@ class Index:
     """An inventory shard resident on one GPU (ebr_build_index / ebr_free_index)."""
 
     def __init__(self, ad_emb, ad_feat, field_card, cross_w, ad_begin: int = 0, device: int = 0,
-                 stream=None):
+                 stream=None, device_build: bool = False):
         ad_emb = np.ascontiguousarray(ad_emb)
         if ad_emb.dtype == np.uint16:
             self.dtype = BF16
@@ -138,19 +141,21 @@ class Index:
         self.n_ads = int(n)
         self.device = device
         h = ctypes.c_void_p()
-        st = _lib.ebr_build_index(_np_ptr(ad_emb), self.dtype, self.ad_begin, self.ad_begin + n,
+        fn = _lib.ebr_build_index_device if device_build else _lib.ebr_build_index
+        st = fn(_np_ptr(ad_emb), self.dtype, self.ad_begin, self.ad_begin + n,
                                   self.d, _np_ptr(ad_feat), self.n_fields, _np_ptr(field_card),
                                   _np_ptr(cross_w), self.n_keys, device, _stream_ptr(stream),
                                   ctypes.byref(h))
-        _check(st, "ebr_build_index")
+        _check(st, "ebr_build_index_device" if device_build else "ebr_build_index")
         self._h = h
 
     @classmethod
-    def of(cls, inv, ad_begin: int = 0, device: int = 0, lo: int | None = None, hi: int | None = None):
+    def of(cls, inv, ad_begin: int = 0, device: int = 0, lo: int | None = None, hi: int | None = None,
+           device_build: bool = False):
         lo = 0 if lo is None else lo
         hi = inv.n_ads if hi is None else hi
         return cls(inv.ad_emb[lo:hi], inv.ad_feat[lo:hi], inv.field_card, inv.cross_w,
-                   ad_begin=ad_begin + lo, device=device)
+                   ad_begin=ad_begin + lo, device=device, device_build=device_build)
 
     @property
     def handle(self):
@@ -186,6 +191,17 @@ class Index:
 
     def query_launches(self, batch: int, slots: int, k: int) -> int:
         return int(_lib.ebr_query_launches(self._h, batch, slots, k))
+
+    def export(self, which: int) -> np.ndarray:
+        """One device array of the index as uint32 (ebr_index_export; 0 key_chunk_off, 1
+        key_word_off, 2 chunk_hdr, 3 chunk_last, 4 payload, 5 hot_mask)."""
+        nb = ctypes.c_int64(0)
+        _check(_lib.ebr_index_export(self.handle, which, None, 0, ctypes.byref(nb)), "ebr_index_export")
+        out = np.zeros(nb.value // 4, np.uint32)
+        if nb.value:
+            _check(_lib.ebr_index_export(self.handle, which, _np_ptr(out), nb.value, ctypes.byref(nb)),
+                   "ebr_index_export")
+        return out
 
     def debug_decode(self, key: int) -> np.ndarray:
         n = _I64()

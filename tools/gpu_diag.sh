@@ -17,7 +17,8 @@ for v in "${@:-base}"; do
     *) env=($v) ;;
   esac
   echo "== $v"
-  env "${env[@]}" timeout 600 python bench.py --config $CFG --steps 10 --warmup 3 --no-cpu-baseline --profile > $OUT/diag_$v.log 2>&1
-  grep "ebr prof" $OUT/diag_$v.log | tail -1
-  tail -1 $OUT/diag_$v.log | python -c "import json,sys; l=json.loads(sys.stdin.read()); print('ms', l['ms_per_step'], 'kernel_ms', l['roofline']['kernel_ms'])" 2>/dev/null || tail -3 $OUT/diag_$v.log
+  tag=$(echo "$v" | tr '/= ' '___')
+  env "${env[@]}" timeout 600 python bench.py --config $CFG --steps 10 --warmup 3 --no-cpu-baseline --profile > $OUT/diag_$tag.log 2>&1
+  grep "ebr prof" $OUT/diag_$tag.log | tail -1
+  tail -1 $OUT/diag_$tag.log | python -c "import json,sys; l=json.loads(sys.stdin.read()); print('ms', l['ms_per_step'], 'kernel_ms', l['roofline']['kernel_ms'])" 2>/dev/null || tail -3 $OUT/diag_$v.log
 done
