@@ -62,16 +62,11 @@ constexpr int kMaxHotBlocks = 2;     // hot K blocks of 64 keys (the index keeps
 constexpr int kPairUBits = 7;        // cold pair = w~ 2^S (25-bit two's complement) << 7 | user in the group
 constexpr int kPairWMax = 24;        // |w~ 2^S| < 2^24
 constexpr int kMaxUnion = 1 << 14;   // union key slots per pass (14 bits in the level-1 bin entries)
-constexpr int kBinAdShift = 14;      // level-1 bin entry = ad in bin << 14 | union slot
 constexpr int kBinAds = 1024;        // ads per entry bin (8 tiles)
+constexpr int kMaxBinCounters = 50 * 1024;   // bins per shard (entry_bin's shared counters): <= 51 M ads
 constexpr int kOrderStage = 16384;   // bin entries staged in shared memory by entry_order (64 KB)
-constexpr int kQuarters = 4;         // 32-ad quarters of a tile (the cold ring's unit in score_kernel)
-#ifndef EBR_INLINE_PAIRS
-#define EBR_INLINE_PAIRS 16
-#endif
-constexpr int kInlinePairs = EBR_INLINE_PAIRS;   // pairs of an entry scattered by its own thread; the rest of a
-                                     // heavy entry goes to a shared list scattered by whole warps
-constexpr int kHeavyCap = 1024;      // heavy entries per quarter (shared list; overflow -> inline)
+constexpr int kClasses = 4;          // pair-count classes of an entry (1, 2, 3-4, 5+ pairs): a tile's
+                                     // entries are ordered by class so a warp's entries carry similar work
 constexpr int kOrderThreads = 512;
 constexpr int kPlanThreads = 1024;
 constexpr uint32_t kFlagShort = 1u, kFlagOverflow = 2u, kFlagRaise = 4u;   // uflags; overflow users carry their dense slot << 8
@@ -90,7 +85,7 @@ constexpr int kEntHdr = 16;          // words of an entry buffer's header (quart
 // per-user scalars
 __host__ __device__ constexpr size_t score_smem_fixed() {
     return (size_t)kHotStages * kBlockBytes + (size_t)kGroup * kAccPitch * 4 + 2 * (size_t)(kEntBuf + kEntHdr) * 4 +
-           256 * 16 + (size_t)kHeavyCap * 4 + 16 +
+           256 * 16 +
            (size_t)(2 * kMaxStages + 2 * kHotStages + 3 * kMaxAccStages + 4 + 1) * 8 + 16 +
            (size_t)kGroup * 20;
 }
@@ -116,14 +111,15 @@ struct Ws {
     uint32_t* uc1;        // [NU] end chunk
     uint32_t* ukwb;       // [NU] payload word base
     uint32_t* pinfo;      // [kMaxCluster][NU] group g's pairs of union slot s: first pair << 8 | count (0: none)
+    uint32_t* ucls;       // [NU] 3 bits per group g at 3g: 0 = no user of g, else 1 + pair-count class
     uint32_t* pairs;      // [kMaxCluster][kGroup * F * S] each group's pairs, by union slot
     uint16_t* U;          // [P_pad][u_cols] deep bf16 | hot fp16 pieces
     uint32_t* uchunk;     // [NU + 1] exclusive scan of the union keys' chunk counts
     uint32_t* bin_cnt;    // [n_bins] entries in each ad-range bin (left zero by entry_sort)
-    uint32_t* qbeg;       // [kMaxCluster][n_tiles * 4] first entry of each tile quarter in group g's stream
-    uint32_t* qend;       // [kMaxCluster][n_tiles * 4]
+    uint32_t* tbeg;       // [kMaxCluster][n_tiles] first entry of each tile in group g's stream
+    uint32_t* tend;       // [kMaxCluster][n_tiles]
     uint32_t* gentries;   // [pool] the groups' entry streams (bins claim their ranges):
-                          //   ad row << 24 | first pair << 8 | pairs, ordered by (tile, quarter, class)
+                          //   ad row << 24 | first pair << 8 | pairs, ordered by (tile, pair-count class)
     uint32_t* entries;    // [n_bins][bin_cap] level-1 bins (bin_cap = bin_ads * F: an ad has <= F keys)
     float* samp;          // [P][n_samp]
     uint64_t* theta;      // [P]
@@ -198,12 +194,12 @@ static Layout layout(const ebr_index* idx, int32_t slots, int32_t k) {
         (size_t)Ppad * 128 * 4,                     // 7 hotw
         (size_t)P * 4, (size_t)P * 4, (size_t)P * 4, (size_t)P * 4,   // 8-11 per user
         (size_t)L.NU * 4, (size_t)L.NU * 4, (size_t)L.NU * 4, (size_t)L.NU * 4,   // 12-15 union
-        (size_t)kMaxCluster * L.NU * 4,             // 16 pinfo
+        (size_t)kMaxCluster * L.NU * 4 + (size_t)L.NU * 4 + 1024,   // 16 pinfo | ucls
         (size_t)kMaxCluster * L.gcap * 4,           // 17 pairs
         (size_t)Ppad * L.u_cols * 2,                // 18 U
         (size_t)(L.NU + 1) * 4,                     // 19 uchunk
         (size_t)L.n_bins * 4,                       // 20 bin_cnt
-        (size_t)L.n_tiles * 16 * kMaxCluster, (size_t)L.n_tiles * 16 * kMaxCluster,   // 21-22 qbeg / qend
+        (size_t)L.n_tiles * 4 * kMaxCluster, (size_t)L.n_tiles * 4 * kMaxCluster,   // 21-22 tbeg / tend
         (size_t)L.pool * 4,                         // 23 gentries
         (size_t)L.n_bins * L.bin_cap * 4,           // 24 entries
         (size_t)P * L.n_samp * 4,                   // 25 samp
@@ -232,10 +228,11 @@ static Ws carve(char* b, const Layout& L) {
     w.bound = (float*)at(8); w.emax = (uint32_t*)at(9); w.ushift = (int32_t*)at(10); w.uscale = (float*)at(11);
     w.ukey = (uint32_t*)at(12); w.uc0 = (uint32_t*)at(13); w.uc1 = (uint32_t*)at(14); w.ukwb = (uint32_t*)at(15);
     w.pinfo = (uint32_t*)at(16); w.pairs = (uint32_t*)at(17);
+    w.ucls = (uint32_t*)(at(16) + (((size_t)kMaxCluster * L.NU * 4 + 1023) & ~(size_t)1023));
     w.U = (uint16_t*)at(18);
     w.uchunk = (uint32_t*)at(19);
     w.bin_cnt = (uint32_t*)at(20);
-    w.qbeg = (uint32_t*)at(21); w.qend = (uint32_t*)at(22);
+    w.tbeg = (uint32_t*)at(21); w.tend = (uint32_t*)at(22);
     w.gentries = (uint32_t*)at(23);
     w.entries = (uint32_t*)at(24);
     w.samp = (float*)at(25);
@@ -268,6 +265,10 @@ struct PlanArgs {
 __device__ __forceinline__ uint32_t hash_key(uint32_t k) {
     k ^= k >> 16; k *= 0x7feb352dU; k ^= k >> 15; k *= 0x846ca68bU; k ^= k >> 16;
     return k;
+}
+
+__device__ __forceinline__ uint32_t pair_class(uint32_t c) {   // c >= 1 pairs -> 0..kClasses-1
+    return c <= 2u ? c - 1u : c <= 4u ? 2u : 3u;
 }
 
 // plan_a: every slot of the pass.  Hot slot -> its w~ is summed into hotw[u][h]; cold slot with
@@ -369,12 +370,15 @@ __global__ void __launch_bounds__(kPlanThreads) plan_b_kernel(PlanArgs a, Ws ws)
         ws.uc1[sl] = c1;
         ws.ukwb[sl] = a.key_word_off[key];
         ws.uchunk[sl] = base[1];
+        uint32_t cls = 0;
         for (int g = 0; g < kMaxCluster; ++g) {
             const uint32_t c = ws.hcnt[t * kMaxCluster + g];          // <= kGroup users
             ws.pinfo[(size_t)g * a.NU + sl] = c ? (base[2 + g] << 8) | c : 0u;
             ws.hpair[t * kMaxCluster + g] = base[2 + g];
             base[2 + g] += c;
+            if (c) cls |= (1u + pair_class(c)) << (3 * g);
         }
+        ws.ucls[sl] = cls;
         base[0] += 1u;
         base[1] += c1 - c0;
         ws.hkey[t] = 0u;
@@ -444,7 +448,7 @@ __global__ void __launch_bounds__(256) plan_c_kernel(PlanArgs a, Ws ws) {
 // Level 1 (entry_bin): the union keys' chunks are decoded warp-cooperatively in key order (each
 // chunk once; Alg. 2 l.355-357 with the chunk codec), every posting appended to the bin of its
 // 1024-ad range; the lanes of a chunk that hit the same bin share one atomic (warp aggregation).
-// Level 2 (entry_order): one CTA per bin orders the bin by (tile, quarter, pair-count class) with
+// Level 2 (entry_order): one CTA per bin orders the bin by (tile, pair-count class) with
 // a shared-memory counting sort and expands it into the stream of every user group that queries
 // the entry's key: entry = ad row << 24 | the group's first pair of the key << 8 | its pair count.
 struct EntryArgs {
@@ -457,56 +461,82 @@ struct EntryArgs {
     int NU;                 // union slot capacity (pinfo row length)
 };
 
-// Work item = 16 consecutive chunks of the union (in slot order); each key's part is decoded by
-// decode_unit16_warp (all headers, then all payload words in flight: two memory round trips per
-// item).  Bin entry = ad in bin << kBinAdShift | union slot.
-__global__ void __launch_bounds__(256) entry_bin_kernel(EntryArgs e, Ws ws) {
-    const int lane = threadIdx.x & 31;
+// CTA = a contiguous range of the union's chunks, decoded twice: pass 1 counts the postings per
+// bin in shared memory, one global atomic per (CTA, bin) reserves the CTA's segment of every bin,
+// pass 2 writes the entries into it (shared-memory cursors) -- no per-posting global atomic.
+// Work unit = 16 consecutive chunks (in slot order) of one or more keys, decoded by
+// decode_unit16_warp (all headers, then all payload words in flight).
+// Bin entry = ad in bin << 20 | the slot's group class codes << 14 | union slot.
+constexpr int kBinThreads = 512;
+constexpr int kBinAdShift2 = 20, kBinClsShift = 14;
+__global__ void __launch_bounds__(kBinThreads) entry_bin_kernel(EntryArgs e, Ws ws) {
+    extern __shared__ uint32_t cur[];                 // [n_bins] counts, then cursors
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t nu = __ldcg(&ws.header[0]), total = __ldcg(&ws.header[5]);
     const uint32_t n_items = (total + 15) / 16;
-    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t i0 = (uint32_t)(((uint64_t)n_items * blockIdx.x) / gridDim.x);
+    const uint32_t i1 = (uint32_t)(((uint64_t)n_items * (blockIdx.x + 1)) / gridDim.x);
     const uint32_t R = (uint32_t)e.bin_ads;
-    for (uint32_t item = gw; item < n_items; item += nw) {
-        uint32_t g0 = item * 16;
-        const uint32_t gend = min(total, g0 + 16);
-        // the key holding chunk g0: last s with uchunk[s] <= g0 (warp 32-ary search)
-        uint32_t lo = 0, hi = nu;
-        while (hi - lo > 1) {
-            const uint32_t step = (hi - lo + 31) / 32;
-            const uint32_t pidx = lo + lane * step;
-            const bool le = pidx < hi && __ldcg(&ws.uchunk[pidx]) <= g0;
-            const uint32_t cntle = __popc(__ballot_sync(FULL, le));
-            const uint32_t nlo = lo + (cntle - 1) * step;
-            hi = min(hi, nlo + step);
-            lo = nlo;
+    for (int i = threadIdx.x; i < e.n_bins; i += kBinThreads) cur[i] = 0;
+    __syncthreads();
+    for (int pass = 0; pass < 2; ++pass) {
+        for (uint32_t item = i0 + (uint32_t)warp; item < i1; item += kBinThreads / 32) {
+            uint32_t g0 = item * 16;
+            const uint32_t gend = min(total, g0 + 16);
+            // the key holding chunk g0: last s with uchunk[s] <= g0 (warp 32-ary search)
+            uint32_t lo = 0, hi = nu;
+            while (hi - lo > 1) {
+                const uint32_t step = (hi - lo + 31) / 32;
+                const uint32_t pidx = lo + lane * step;
+                const bool le = pidx < hi && __ldcg(&ws.uchunk[pidx]) <= g0;
+                const uint32_t cntle = __popc(__ballot_sync(FULL, le));
+                const uint32_t nlo = lo + (cntle - 1) * step;
+                hi = min(hi, nlo + step);
+                lo = nlo;
+            }
+            for (uint32_t s = lo; g0 < gend; ++s) {
+                const uint32_t s_beg = __ldcg(&ws.uchunk[s]), s_end = __ldcg(&ws.uchunk[s + 1]);
+                const uint32_t sub_end = min(gend, s_end);
+                const uint32_t c0 = __ldcg(&ws.uc0[s]) + (g0 - s_beg);
+                const uint32_t tag = (__ldcg(&ws.ucls[s]) << kBinClsShift) | s;
+                decode_unit16_warp(e.hdr, e.payload, __ldcg(&ws.ukwb[s]), c0, c0 + (sub_end - g0), lane,
+                                   [&](uint32_t id, bool ok) {
+                    const uint32_t r = ok ? id / R : 0xFFFFFFFFu;
+                    const unsigned act = __ballot_sync(FULL, ok);
+                    if (ok) {
+                        const unsigned peers = __match_any_sync(act, r);
+                        const int leader = __ffs(peers) - 1;
+                        if (pass == 0) {
+                            if (lane == leader) atomicAdd(&cur[r], (uint32_t)__popc(peers));
+                        } else {
+                            uint32_t base = 0;
+                            if (lane == leader) base = atomicAdd(&cur[r], (uint32_t)__popc(peers));
+                            base = __shfl_sync(peers, base, leader);
+                            const uint32_t pos = base + __popc(peers & ((1u << lane) - 1u));
+                            ws.entries[(size_t)r * e.bin_cap + pos] = ((id - r * R) << kBinAdShift2) | tag;
+                        }
+                    }
+                });
+                g0 = sub_end;
+            }
         }
-        for (uint32_t s = lo; g0 < gend; ++s) {
-            const uint32_t s_beg = __ldcg(&ws.uchunk[s]), s_end = __ldcg(&ws.uchunk[s + 1]);
-            const uint32_t sub_end = min(gend, s_end);
-            const uint32_t c0 = __ldcg(&ws.uc0[s]) + (g0 - s_beg);
-            decode_unit16_warp(e.hdr, e.payload, __ldcg(&ws.ukwb[s]), c0, c0 + (sub_end - g0), lane,
-                               [&](uint32_t id, bool ok) {
-                const uint32_t r = ok ? id / R : 0xFFFFFFFFu;
-                const unsigned act = __ballot_sync(FULL, ok);
-                if (ok) {
-                    const unsigned peers = __match_any_sync(act, r);
-                    const int leader = __ffs(peers) - 1;
-                    uint32_t base = 0;
-                    if (lane == leader) base = atomicAdd(&ws.bin_cnt[r], (uint32_t)__popc(peers));
-                    base = __shfl_sync(peers, base, leader);
-                    const uint32_t pos = base + __popc(peers & ((1u << lane) - 1u));
-                    ws.entries[(size_t)r * e.bin_cap + pos] = ((id - r * R) << kBinAdShift) | s;
-                }
-            });
-            g0 = sub_end;
+        __syncthreads();
+        if (pass == 0) {
+            // this CTA's segment of every bin it touches
+            for (int i = threadIdx.x; i < e.n_bins; i += kBinThreads) {
+                const uint32_t c = cur[i];
+                cur[i] = c ? atomicAdd(&ws.bin_cnt[i], c) : 0u;
+            }
+            __syncthreads();
         }
     }
 }
 
 // Level 2: CTA = bin (8 tiles).  The bin is staged in shared memory when it fits (the common
-// case), else read twice from L2: count per (group, tile quarter), scan, claim the groups' ranges
+// case), else read twice from L2: count per (group, tile, class), scan, claim the groups' ranges
 // of the pool, scatter.
-constexpr int kOrderCells = (kBinAds / kTileM) * kQuarters;   // counters per group (= 32: one per lane)
+constexpr int kOrderCells = (kBinAds / kTileM) * kClasses;   // counters per group (= 32: one per lane)
+
 __global__ void __launch_bounds__(kOrderThreads) entry_order_kernel(EntryArgs e, Ws ws) {
     extern __shared__ uint32_t smem_u[];
     __shared__ uint32_t cnt[kMaxCluster * kOrderCells];
@@ -523,15 +553,15 @@ __global__ void __launch_bounds__(kOrderThreads) entry_order_kernel(EntryArgs e,
     for (uint32_t i = tid; i < n; i += kOrderThreads) {
         const uint32_t v = __ldcs(&ent[i]);
         if (staged) buf[i] = v;
-        const uint32_t a = v >> kBinAdShift, sl = v & ((1u << kBinAdShift) - 1u);
+        const uint32_t a = v >> kBinAdShift2, cls = (v >> kBinClsShift) & 63u;
         for (int g = 0; g < G; ++g) {
-            const uint32_t c = __ldg(&pinfo[(size_t)g * e.NU + sl]) & 0xFFu;
-            if (c) atomicAdd(&cnt[g * kOrderCells + (a >> 5)], 1u);
+            const uint32_t cc = (cls >> (3 * g)) & 7u;           // 0: no user of g, else 1 + class
+            if (cc) atomicAdd(&cnt[g * kOrderCells + (a >> 7) * kClasses + cc - 1u], 1u);
         }
     }
     __syncthreads();
-    // warp g: exclusive scan of group g's counters (lane = tile quarter), its range claimed from
-    // the pool, the quarter bounds of the bin's tiles
+    // warp g: exclusive scan of group g's counters (lane = tile * kClasses + class), its range
+    // claimed from the pool, the bounds of the bin's tiles
     const int warp = tid >> 5, lane = tid & 31;
     static_assert(kOrderCells == 32, "one counter per lane");
     if (warp < G) {
@@ -548,20 +578,25 @@ __global__ void __launch_bounds__(kOrderThreads) entry_order_kernel(EntryArgs e,
         if (lane == 0) base = tot ? atomicAdd(&ws.header[6], tot) : 0u;
         base = __shfl_sync(FULL, base, 0);
         if (lane == 0) sBase[warp] = base;
-        const int64_t qi = (int64_t)r * kOrderCells + lane;      // global tile quarter
-        if (qi < (int64_t)e.n_tiles * kQuarters) {
-            ws.qbeg[(size_t)warp * e.n_tiles * kQuarters + qi] = base + incl - x;
-            ws.qend[(size_t)warp * e.n_tiles * kQuarters + qi] = base + incl;
+        const int tl = lane / kClasses;                           // the bin's tile of this lane's cell
+        const int64_t ti = (int64_t)r * (kBinAds / kTileM) + tl;  // global tile
+        const uint32_t tb = __shfl_sync(FULL, incl - x, tl * kClasses);
+        const uint32_t te = __shfl_sync(FULL, incl, tl * kClasses + kClasses - 1);
+        if (lane % kClasses == 0 && ti < (int64_t)e.n_tiles) {
+            ws.tbeg[(size_t)warp * e.n_tiles + ti] = base + tb;
+            ws.tend[(size_t)warp * e.n_tiles + ti] = base + te;
         }
     }
     __syncthreads();
     for (uint32_t i = tid; i < n; i += kOrderThreads) {
         const uint32_t v = staged ? buf[i] : __ldcs(&ent[i]);
-        const uint32_t a = v >> kBinAdShift, sl = v & ((1u << kBinAdShift) - 1u);
+        const uint32_t a = v >> kBinAdShift2, cls = (v >> kBinClsShift) & 63u;
+        const uint32_t sl = v & ((1u << kBinClsShift) - 1u);
         for (int g = 0; g < G; ++g) {
-            const uint32_t pi = __ldg(&pinfo[(size_t)g * e.NU + sl]);
-            if (pi & 0xFFu) {
-                const uint32_t pos = sBase[g] + atomicAdd(&cnt[g * kOrderCells + (a >> 5)], 1u);
+            const uint32_t cc = (cls >> (3 * g)) & 7u;
+            if (cc) {
+                const uint32_t pi = __ldg(&pinfo[(size_t)g * e.NU + sl]);
+                const uint32_t pos = sBase[g] + atomicAdd(&cnt[g * kOrderCells + (a >> 7) * kClasses + cc - 1u], 1u);
                 ws.gentries[pos] = ((a & (kTileM - 1)) << 24) | pi;
             }
         }
@@ -638,9 +673,7 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
     int32_t* sAcc = reinterpret_cast<int32_t*>(sHot + (size_t)kHotStages * kBlockBytes);   // [128 users][kAccPitch]
     uint32_t* sEnt = reinterpret_cast<uint32_t*>(sAcc + kGroup * kAccPitch);  // [2][kEntHdr + kEntBuf]
     uint4* sLut = reinterpret_cast<uint4*>(sEnt + 2 * (kEntHdr + kEntBuf));  // [256] byte -> 8 fp16 {0, 1}
-    uint32_t* sHeavy = reinterpret_cast<uint32_t*>(sLut + 256);              // [kHeavyCap] heavy entries' rest
-    uint32_t* sHeavyN = sHeavy + kHeavyCap;                                  // [2] counts by quarter parity
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sHeavyN + 4);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sLut + 256);
     uint64_t* full = bars;                          // [kMaxStages] A ring
     uint64_t* empty = full + kMaxStages;
     uint64_t* hfull = empty + kMaxStages;           // [kHotStages] hot ring
@@ -672,7 +705,6 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
         fence_mbar_init();
     }
     if (warp == 2) tc::tmem_alloc(tmem_slot, 512);
-    if (tid == 0) { sHeavyN[0] = 0u; sHeavyN[1] = 0u; }
     for (int i = tid; i < kGroup * kAccPitch / 4; i += kGemmThreads)
         reinterpret_cast<int4*>(sAcc)[i] = make_int4(0, 0, 0, 0);
     for (int b = tid; b < 256; b += kGemmThreads) {
@@ -706,7 +738,7 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
             const uint64_t pol = tc::policy_evict_first();   // A is streamed once per pass
             uint32_t gb = 0;
             int it = 0;
-            const size_t qrow = (size_t)g * p.n_tiles_all * kQuarters;
+            const size_t trow = (size_t)g * p.n_tiles_all;
             const uint32_t tile_bytes = (uint32_t)(kTileM * p.n_kb * 128);     // a tile's rows of A (contiguous)
             const unsigned char* Abase = reinterpret_cast<const unsigned char*>(p.A);
             // L2 prefetch kPrefetchTiles ahead of the TMA loads: the ring's loads then hit L2 (the
@@ -716,23 +748,22 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
                     const int tp = (int)cid + k * (int)ncl;
                     if (tp < p.n_tiles) tc::bulk_prefetch_l2(Abase + (size_t)tp * p.tile_stride * tile_bytes, tile_bytes);
                 }
-            // quarter bounds of the group stream, loaded two tiles ahead (never on the issue path)
-            auto load_qb = [&](int tt, uint32_t (&qb)[kQuarters + 1]) {
+            // tile bounds of the group stream, loaded two tiles ahead (never on the issue path)
+            auto load_qb = [&](int tt, uint32_t (&qb)[2]) {
                 if (tt < p.n_tiles) {
-                    const size_t qi = qrow + (size_t)tt * p.tile_stride * kQuarters;
-#pragma unroll
-                    for (int q = 0; q < kQuarters; ++q) qb[q] = __ldcg(&p.ws.qbeg[qi + q]);
-                    qb[kQuarters] = __ldcg(&p.ws.qend[qi + kQuarters - 1]);
+                    const size_t ti = trow + (size_t)tt * p.tile_stride;
+                    qb[0] = __ldcg(&p.ws.tbeg[ti]);
+                    qb[1] = __ldcg(&p.ws.tend[ti]);
                 }
             };
-            uint32_t qbA[kQuarters + 1] = {}, qbB[kQuarters + 1] = {};
+            uint32_t qbA[2] = {}, qbB[2] = {};
             load_qb((int)cid, qbA);
             load_qb((int)cid + (int)ncl, qbB);
             for (int t = (int)cid; t < p.n_tiles; t += (int)ncl, ++it) {
                 const int row0 = t * p.tile_stride * kTileM;
-                uint32_t qb[kQuarters + 1];
+                uint32_t qb[2];
 #pragma unroll
-                for (int q = 0; q <= kQuarters; ++q) { qb[q] = qbA[q]; qbA[q] = qbB[q]; }
+                for (int q = 0; q < 2; ++q) { qb[q] = qbA[q]; qbA[q] = qbB[q]; }
                 load_qb(t + 2 * (int)ncl, qbB);
                 if (rank == 0) {
                     const int tp = t + kPrefetchTiles * (int)ncl;
@@ -745,13 +776,13 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
                     const int eb = it & 1;
                     if (it >= 2) mbar_wait_sleep(&eempty[eb], ((it >> 1) - 1) & 1);
                     uint32_t* hdr = sEnt + eb * (kEntHdr + kEntBuf);
-                    if (p.diag & 1) qb[1] = qb[2] = qb[3] = qb[4] = qb[0];
+                    if (p.diag & 1) qb[1] = qb[0];
                     const uint32_t base = qb[0] & ~3u;                          // 16-byte aligned source
-                    const uint32_t ncopy = min((qb[kQuarters] - base + 3u) & ~3u, (uint32_t)kEntBuf);
-#pragma unroll
-                    for (int q = 0; q <= kQuarters; ++q) hdr[q] = qb[q] - base;
-                    hdr[kQuarters + 1] = base;
-                    hdr[kQuarters + 2] = ncopy;
+                    const uint32_t ncopy = min((qb[1] - base + 3u) & ~3u, (uint32_t)kEntBuf);
+                    hdr[0] = qb[0] - base;
+                    hdr[1] = qb[1] - base;
+                    hdr[2] = base;
+                    hdr[3] = ncopy;
                     if (ncopy) {
                         mbar_arrive_expect_tx(&efull[eb], ncopy * 4);
                         bulk_g2s(hdr + kEntHdr, p.ws.gentries + base, ncopy * 4, &efull[eb]);
@@ -881,7 +912,8 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
             if (lane == 0) mbar_arrive(aready);
         }
         // Per tile: its entries (ad row, the slot's first pair, pair count) of this CTA's group
-        // stream, staged in shared memory by the producer's bulk copy; each pair (user, w~ 2^S) is
+        // stream (ordered by pair-count class), staged in shared memory by the producer's bulk
+        // copy; each pair (user, w~ 2^S) is
         // added to the tile [128 users][128 ads] with a native 32-bit shared atomic (exact,
         // order-free; Alg. 2 l.358).  Then the tile is converted once to fp32 and stored into the
         // TMEM accumulator stage, which the tensor core accumulates onto.
@@ -898,50 +930,20 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
             const long long _pc0 = (p.diag & 4) ? clock64() : 0;
             const uint32_t* hdr = sEnt + eb * (kEntHdr + kEntBuf);
             const uint32_t* ebuf = hdr + kEntHdr;
-            const uint32_t ebase = hdr[kQuarters + 1], ncopy = hdr[kQuarters + 2];
-            const uint32_t e0 = hdr[0], e1 = hdr[kQuarters];
+            const uint32_t ebase = hdr[2], ncopy = hdr[3];
+            const uint32_t e0 = hdr[0], e1 = hdr[1];
             for (uint32_t ei = e0 + wt; ei < e1; ei += kWideThreads) {
                 const uint32_t en = ei < ncopy ? ebuf[ei] : __ldcs(&entries[ebase + ei]);
                 const uint32_t a = en >> 24, lo = (en >> 8) & 0xFFFFu, c = en & 0xFFu;
-#pragma unroll
-                for (uint32_t qq = 0; qq < (uint32_t)kInlinePairs; ++qq) {
-                    if (qq < c) {
-                        const uint32_t pr = sPairs[lo + qq];
-                        atomicAdd(&sAcc[(pr & (kGroup - 1)) * kAccPitch + a], (int32_t)pr >> kPairUBits);
-                    }
-                }
-                if (c > (uint32_t)kInlinePairs) {
-                    const uint32_t hslot = atomicAdd(&sHeavyN[it & 1], 1u);
-                    const uint32_t rest = (a << 24) | ((lo + kInlinePairs) << 8) | (c - kInlinePairs);
-                    if (hslot < (uint32_t)kHeavyCap) {
-                        sHeavy[hslot] = rest;
-                    } else {
-                        for (uint32_t qq = kInlinePairs; qq < c; ++qq) {
-                            const uint32_t pr = sPairs[lo + qq];
-                            atomicAdd(&sAcc[(pr & (kGroup - 1)) * kAccPitch + a], (int32_t)pr >> kPairUBits);
-                        }
-                    }
+                // (a warp's entries share a pair-count class: little divergence in this loop)
+#pragma unroll 2
+                for (uint32_t qq = lo; qq < lo + c; ++qq) {
+                    const uint32_t pr = sPairs[qq];
+                    atomicAdd(&sAcc[(pr & (kGroup - 1)) * kAccPitch + a], (int32_t)pr >> kPairUBits);
                 }
             }
             tc::named_bar_sync(1, kWideThreads);
-            // heavy entries' remaining pairs (keys queried by > kInlinePairs users of the group),
-            // a warp per entry with the lanes over its pairs
-            const uint32_t nh = min(sHeavyN[it & 1], (uint32_t)kHeavyCap);
-            if (nh) {
-                for (uint32_t h = (uint32_t)(wt >> 5); h < nh; h += kWideWarps) {
-                    const uint32_t hv = sHeavy[h];
-                    const uint32_t a = hv >> 24, lo = (hv >> 8) & 0xFFFFu, c = hv & 0xFFu;
-                    for (uint32_t qq = (uint32_t)lane; qq < c; qq += 32) {
-                        const uint32_t pr = sPairs[lo + qq];
-                        atomicAdd(&sAcc[(pr & (kGroup - 1)) * kAccPitch + a], (int32_t)pr >> kPairUBits);
-                    }
-                }
-                tc::named_bar_sync(1, kWideThreads);
-            }
-            if (wt == 0) {
-                sHeavyN[it & 1] = 0u;          // (the other parity's counter is the next tile's)
-                mbar_arrive(&eempty[eb]);      // entry buffer consumed
-            }
+            if (wt == 0) mbar_arrive(&eempty[eb]);      // entry buffer consumed
             if ((p.diag & 4) && wt == 0) atomicAdd(&p.ws.prof[4], (unsigned long long)(clock64() - _pc0));
             // the accumulator stage is free once the epilogue drained it (nst tiles ago)
             if (it >= nst) { EBR_PROF_T0; mbar_wait_sleep(&tempty[st], ((it / nst) - 1) & 1); if (wt == 0) EBR_PROF_ADD(5); }
@@ -1315,6 +1317,7 @@ bool batch_eligible(const ebr_index* idx, int32_t batch, int32_t slots, int32_t 
     // per-user wide scratch no longer fits L2 (C5 sweep: B=4 at 20 M ads 3.9 ms latency path)
     const bool big = idx->n_ads >= ((int64_t)1 << 21);
     return idx->dtype == EBR_BF16 && (batch >= 16 || (big && batch >= 4)) && idx->d_pad <= 256 &&
+           idx->n_pad <= (int64_t)kMaxBinCounters * kBinAds &&
            idx->n_fields <= 255 && pass_users(idx, slots) >= 32 &&
            idx->n_ads >= (int64_t)4 * kSampleStride * std::max(k, kTileM) && get_encode() != nullptr;
 }
@@ -1371,6 +1374,7 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
         set((const void*)theta_kernel, 200 * 1024);
         set((const void*)final_kernel, 200 * 1024);
         set((const void*)entry_order_kernel, kOrderStage * 4);
+        set((const void*)entry_bin_kernel, kMaxBinCounters * 4);
         for (const void* f : {(const void*)score_kernel<0>, (const void*)score_kernel<1>}) {
             cudaError_t x = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
             (void)x;
@@ -1415,7 +1419,7 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
         trace(q.stream, "plan_b");
         plan_c_kernel<<<std::max(pgrid, 2 * idx->sm_count), 256, 0, q.stream>>>(pa, ws);
         trace(q.stream, "plan_c");
-        entry_bin_kernel<<<8 * idx->sm_count, 256, 0, q.stream>>>(ea, ws);
+        entry_bin_kernel<<<2 * idx->sm_count, kBinThreads, (size_t)L.n_bins * 4, q.stream>>>(ea, ws);
         trace(q.stream, "entry_bin");
         entry_order_kernel<<<(unsigned)L.n_bins, kOrderThreads, kOrderStage * 4, q.stream>>>(ea, ws);
         trace(q.stream, "entry_order");
