@@ -63,7 +63,6 @@ constexpr int kPairUBits = 7;        // cold pair = w~ 2^S (25-bit two's complem
 constexpr int kPairWMax = 24;        // |w~ 2^S| < 2^24
 constexpr int kMaxUnion = 1 << 14;   // union key slots per pass (14 bits in the level-1 bin entries)
 constexpr int kBinAds = 1024;        // ads per entry bin (8 tiles)
-constexpr int kMaxBinCounters = 50 * 1024;   // bins per shard (entry_bin's shared counters): <= 51 M ads
 constexpr int kOrderStage = 16384;   // bin entries staged in shared memory by entry_order (64 KB)
 constexpr int kClasses = 4;          // pair-count classes of an entry (1, 2, 3-4, 5+ pairs): a tile's
                                      // entries are ordered by class so a warp's entries carry similar work
@@ -461,73 +460,54 @@ struct EntryArgs {
     int NU;                 // union slot capacity (pinfo row length)
 };
 
-// CTA = a contiguous range of the union's chunks, decoded twice: pass 1 counts the postings per
-// bin in shared memory, one global atomic per (CTA, bin) reserves the CTA's segment of every bin,
-// pass 2 writes the entries into it (shared-memory cursors) -- no per-posting global atomic.
-// Work unit = 16 consecutive chunks (in slot order) of one or more keys, decoded by
-// decode_unit16_warp (all headers, then all payload words in flight).
+// Work item = 16 consecutive chunks of the union (in slot order); each key's part is decoded by
+// decode_unit16_warp (all headers, then all payload words in flight: two memory round trips per
+// item); every posting is appended to its bin (lanes of a chunk hitting the same bin share one
+// atomic).  (A two-pass variant with per-CTA bin segments measured 2.4x slower: its many small
+// segments defeat write combining.)
 // Bin entry = ad in bin << 20 | the slot's group class codes << 14 | union slot.
-constexpr int kBinThreads = 512;
+constexpr int kBinThreads = 256;
 constexpr int kBinAdShift2 = 20, kBinClsShift = 14;
 __global__ void __launch_bounds__(kBinThreads) entry_bin_kernel(EntryArgs e, Ws ws) {
-    extern __shared__ uint32_t cur[];                 // [n_bins] counts, then cursors
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
     const uint32_t nu = __ldcg(&ws.header[0]), total = __ldcg(&ws.header[5]);
     const uint32_t n_items = (total + 15) / 16;
-    const uint32_t i0 = (uint32_t)(((uint64_t)n_items * blockIdx.x) / gridDim.x);
-    const uint32_t i1 = (uint32_t)(((uint64_t)n_items * (blockIdx.x + 1)) / gridDim.x);
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
     const uint32_t R = (uint32_t)e.bin_ads;
-    for (int i = threadIdx.x; i < e.n_bins; i += kBinThreads) cur[i] = 0;
-    __syncthreads();
-    for (int pass = 0; pass < 2; ++pass) {
-        for (uint32_t item = i0 + (uint32_t)warp; item < i1; item += kBinThreads / 32) {
-            uint32_t g0 = item * 16;
-            const uint32_t gend = min(total, g0 + 16);
-            // the key holding chunk g0: last s with uchunk[s] <= g0 (warp 32-ary search)
-            uint32_t lo = 0, hi = nu;
-            while (hi - lo > 1) {
-                const uint32_t step = (hi - lo + 31) / 32;
-                const uint32_t pidx = lo + lane * step;
-                const bool le = pidx < hi && __ldcg(&ws.uchunk[pidx]) <= g0;
-                const uint32_t cntle = __popc(__ballot_sync(FULL, le));
-                const uint32_t nlo = lo + (cntle - 1) * step;
-                hi = min(hi, nlo + step);
-                lo = nlo;
-            }
-            for (uint32_t s = lo; g0 < gend; ++s) {
-                const uint32_t s_beg = __ldcg(&ws.uchunk[s]), s_end = __ldcg(&ws.uchunk[s + 1]);
-                const uint32_t sub_end = min(gend, s_end);
-                const uint32_t c0 = __ldcg(&ws.uc0[s]) + (g0 - s_beg);
-                const uint32_t tag = (__ldcg(&ws.ucls[s]) << kBinClsShift) | s;
-                decode_unit16_warp(e.hdr, e.payload, __ldcg(&ws.ukwb[s]), c0, c0 + (sub_end - g0), lane,
-                                   [&](uint32_t id, bool ok) {
-                    const uint32_t r = ok ? id / R : 0xFFFFFFFFu;
-                    const unsigned act = __ballot_sync(FULL, ok);
-                    if (ok) {
-                        const unsigned peers = __match_any_sync(act, r);
-                        const int leader = __ffs(peers) - 1;
-                        if (pass == 0) {
-                            if (lane == leader) atomicAdd(&cur[r], (uint32_t)__popc(peers));
-                        } else {
-                            uint32_t base = 0;
-                            if (lane == leader) base = atomicAdd(&cur[r], (uint32_t)__popc(peers));
-                            base = __shfl_sync(peers, base, leader);
-                            const uint32_t pos = base + __popc(peers & ((1u << lane) - 1u));
-                            ws.entries[(size_t)r * e.bin_cap + pos] = ((id - r * R) << kBinAdShift2) | tag;
-                        }
-                    }
-                });
-                g0 = sub_end;
-            }
+    for (uint32_t item = gw; item < n_items; item += nw) {
+        uint32_t g0 = item * 16;
+        const uint32_t gend = min(total, g0 + 16);
+        // the key holding chunk g0: last s with uchunk[s] <= g0 (warp 32-ary search)
+        uint32_t lo = 0, hi = nu;
+        while (hi - lo > 1) {
+            const uint32_t step = (hi - lo + 31) / 32;
+            const uint32_t pidx = lo + lane * step;
+            const bool le = pidx < hi && __ldcg(&ws.uchunk[pidx]) <= g0;
+            const uint32_t cntle = __popc(__ballot_sync(FULL, le));
+            const uint32_t nlo = lo + (cntle - 1) * step;
+            hi = min(hi, nlo + step);
+            lo = nlo;
         }
-        __syncthreads();
-        if (pass == 0) {
-            // this CTA's segment of every bin it touches
-            for (int i = threadIdx.x; i < e.n_bins; i += kBinThreads) {
-                const uint32_t c = cur[i];
-                cur[i] = c ? atomicAdd(&ws.bin_cnt[i], c) : 0u;
-            }
-            __syncthreads();
+        for (uint32_t s = lo; g0 < gend; ++s) {
+            const uint32_t s_beg = __ldcg(&ws.uchunk[s]), s_end = __ldcg(&ws.uchunk[s + 1]);
+            const uint32_t sub_end = min(gend, s_end);
+            const uint32_t c0 = __ldcg(&ws.uc0[s]) + (g0 - s_beg);
+            const uint32_t tag = (__ldcg(&ws.ucls[s]) << kBinClsShift) | s;
+            decode_unit16_warp(e.hdr, e.payload, __ldcg(&ws.ukwb[s]), c0, c0 + (sub_end - g0), lane,
+                               [&](uint32_t id, bool ok) {
+                const uint32_t r = ok ? id / R : 0xFFFFFFFFu;
+                const unsigned act = __ballot_sync(FULL, ok);
+                if (ok) {
+                    const unsigned peers = __match_any_sync(act, r);
+                    const int leader = __ffs(peers) - 1;
+                    uint32_t base = 0;
+                    if (lane == leader) base = atomicAdd(&ws.bin_cnt[r], (uint32_t)__popc(peers));
+                    base = __shfl_sync(peers, base, leader);
+                    const uint32_t pos = base + __popc(peers & ((1u << lane) - 1u));
+                    ws.entries[(size_t)r * e.bin_cap + pos] = ((id - r * R) << kBinAdShift2) | tag;
+                }
+            });
+            g0 = sub_end;
         }
     }
 }
@@ -634,6 +614,13 @@ struct GemmParams {
     int n_tiles_all;        // tiles of the inventory (row length of the group streams' tile bounds)
 };
 
+// the producer's and the MMA issuer's waits: sleeping (default) or spinning (EBR_DIAG & 16)
+__device__ __forceinline__ void crit_wait(uint64_t* bar, uint32_t parity, int diag) {
+    if (diag & 256) mbar_wait_poll(bar, parity);
+    else if (diag & 16) mbar_wait(bar, parity);
+    else mbar_wait_sleep(bar, parity);
+}
+
 // role cycle accounting (EBR_DIAG & 4): prof[slot] += clock64 delta, from one thread per role
 #define EBR_PROF_T0 const long long _pt0 = (p.diag & 4) ? clock64() : 0
 #define EBR_PROF_ADD(slot) do { if ((p.diag & 4)) atomicAdd(&p.ws.prof[slot], (unsigned long long)(clock64() - _pt0)); } while (0)
@@ -693,7 +680,7 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
     uint32_t* sPairs = reinterpret_cast<uint32_t*>(sDense + kGroup);        // [n_gp] the group's pairs
 
     if (tid == 0) {
-        for (int s = 0; s < nring; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], csize); }
+        for (int s = 0; s < nring; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], (p.diag & 8) ? 1u : csize); }
         for (int s = 0; s < 2; ++s) { mbar_init(&efull[s], 1); mbar_init(&eempty[s], 1); }
         for (int s = 0; s < kHotStages; ++s) { mbar_init(&hfull[s], 1); mbar_init(&hempty[s], 1); }
         for (int s = 0; s < kMaxAccStages; ++s) {
@@ -774,7 +761,7 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
                     // entry buffer it % 2 by one bulk copy; header = quarter bounds relative to the
                     // copied base, and the number of entries copied
                     const int eb = it & 1;
-                    if (it >= 2) mbar_wait_sleep(&eempty[eb], ((it >> 1) - 1) & 1);
+                    if (it >= 2) crit_wait(&eempty[eb], ((it >> 1) - 1) & 1, p.diag);
                     uint32_t* hdr = sEnt + eb * (kEntHdr + kEntBuf);
                     if (p.diag & 1) qb[1] = qb[0];
                     const uint32_t base = qb[0] & ~3u;                          // 16-byte aligned source
@@ -792,9 +779,9 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
                 }
                 for (int kb = 0; kb < p.n_kb; ++kb, ++gb) {
                     const uint32_t slot = gb % nring, round = gb / nring;
-                    if (round > 0) { EBR_PROF_T0; mbar_wait_sleep(&empty[slot], (round - 1) & 1); EBR_PROF_ADD(0); }
+                    if (round > 0) { EBR_PROF_T0; crit_wait(&empty[slot], (round - 1) & 1, p.diag); EBR_PROF_ADD(0); }
                     mbar_arrive_expect_tx(&full[slot], (uint32_t)kBlockBytes);
-                    if (csize == 1)
+                    if (csize == 1 || (p.diag & 8))
                         tc::tma_load_2d_hint(sRing + (size_t)slot * kBlockBytes, &tmA, kb * kBlockK, row0, &full[slot], pol);
                     else if (rank == 0)
                         tc::tma_load_2d_mc(sRing + (size_t)slot * kBlockBytes, &tmA, kb * kBlockK, row0, &full[slot],
@@ -804,7 +791,7 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
             // every remote arrival into this CTA's ring barriers has landed before it exits
             for (uint32_t k = 0; k < (uint32_t)nring && k < gb; ++k) {
                 const uint32_t q = gb - 1 - k;
-                mbar_wait_sleep(&empty[q % nring], (q / nring) & 1);
+                crit_wait(&empty[q % nring], (q / nring) & 1, p.diag);
             }
         }
     } else if (warp == 1) {
@@ -813,29 +800,29 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
             // The accumulator stage already holds the tile's cold wide term (stored by the wide
             // warps), so every MMA accumulates: D = cold + U A^T + U_hot (one-hot)^T.
             const uint32_t idb = tc::idesc_bf16_m128(kTileM), idh = tc::idesc_f16_m128(kTileM);
-            mbar_wait_sleep(aready, 0);                   // users' A operand in TMEM
+            crit_wait(aready, 0, p.diag);                   // users' A operand in TMEM
             tc::fence_after();
             int it = 0;
             uint32_t gb = 0, hb = 0;
             for (int t = (int)cid; t < p.n_tiles; t += (int)ncl, ++it) {
                 const int st = it % nst;
-                { EBR_PROF_T0; mbar_wait_sleep(&wready[st], (it / nst) & 1); EBR_PROF_ADD(1); }
+                { EBR_PROF_T0; crit_wait(&wready[st], (it / nst) & 1, p.diag); EBR_PROF_ADD(1); }
                 tc::fence_after();
                 const uint32_t d_tmem = tmem_base + (uint32_t)(a_cols + st * kTileM);
                 for (int kb = 0; kb < p.n_kb; ++kb, ++gb) {
                     const uint32_t slot = gb % nring;
-                    { EBR_PROF_T0; mbar_wait_sleep(&full[slot], (gb / nring) & 1); EBR_PROF_ADD(2); }
+                    if (!(p.diag & 128)) { EBR_PROF_T0; crit_wait(&full[slot], (gb / nring) & 1, p.diag); EBR_PROF_ADD(2); }
                     tc::fence_after();
                     const uint64_t db0 = tc::sdesc_sw128(sRing + (size_t)slot * kBlockBytes);
 #pragma unroll
                     for (int k = 0; k < kBlockK / 16; ++k)
                         tc::umma_f16_ts(d_tmem, tmem_base + (uint32_t)(kb * 32 + k * 8), db0 + (uint64_t)(k * 2), idb, 1u);
-                    if (csize == 1) tc::umma_commit(&empty[slot]);
+                    if (csize == 1 || (p.diag & 8)) tc::umma_commit(&empty[slot]);
                     else tc::umma_commit_mc(&empty[slot], mc_mask);
                 }
                 for (int h = 0; h < p.n_hb; ++h, ++hb) {
                     const uint32_t hs = hb % kHotStages;
-                    { EBR_PROF_T0; mbar_wait_sleep(&hfull[hs], (hb / kHotStages) & 1); EBR_PROF_ADD(2); }
+                    { EBR_PROF_T0; crit_wait(&hfull[hs], (hb / kHotStages) & 1, p.diag); EBR_PROF_ADD(2); }
                     tc::fence_after();
                     const uint64_t db0 = tc::sdesc_sw128(sHot + (size_t)hs * kBlockBytes);
                     for (int pc = 0; pc < p.pieces; ++pc) {
@@ -872,7 +859,7 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
                 load(t + (int)ncl, hn);
                 for (int h = 0; h < p.n_hb; ++h, ++hb) {
                     const uint32_t hs = hb % kHotStages, round = hb / kHotStages;
-                    if (round > 0) { EBR_PROF_T0; mbar_wait_sleep(&hempty[hs], (round - 1) & 1); if (hw == 0) EBR_PROF_ADD(3); }
+                    if (round > 0) { EBR_PROF_T0; crit_wait(&hempty[hs], (round - 1) & 1, p.diag); if (hw == 0) EBR_PROF_ADD(3); }
 #pragma unroll
                     for (int rr = 0; rr < 2; ++rr) {
                         const int row = hw + rr * 64;
@@ -926,7 +913,7 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
         for (int t = (int)cid; t < p.n_tiles; t += (int)ncl, ++it) {
             const int st = it % nst;
             const int eb = it & 1;
-            { EBR_PROF_T0; mbar_wait_sleep(&efull[eb], (it >> 1) & 1); if (wt == 0) EBR_PROF_ADD(11); }
+            { EBR_PROF_T0; crit_wait(&efull[eb], (it >> 1) & 1, p.diag); if (wt == 0) EBR_PROF_ADD(11); }
             const long long _pc0 = (p.diag & 4) ? clock64() : 0;
             const uint32_t* hdr = sEnt + eb * (kEntHdr + kEntBuf);
             const uint32_t* ebuf = hdr + kEntHdr;
@@ -946,7 +933,7 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
             if (wt == 0) mbar_arrive(&eempty[eb]);      // entry buffer consumed
             if ((p.diag & 4) && wt == 0) atomicAdd(&p.ws.prof[4], (unsigned long long)(clock64() - _pc0));
             // the accumulator stage is free once the epilogue drained it (nst tiles ago)
-            if (it >= nst) { EBR_PROF_T0; mbar_wait_sleep(&tempty[st], ((it / nst) - 1) & 1); if (wt == 0) EBR_PROF_ADD(5); }
+            if (it >= nst) { EBR_PROF_T0; crit_wait(&tempty[st], ((it / nst) - 1) & 1, p.diag); if (wt == 0) EBR_PROF_ADD(5); }
             const long long _ps0 = (p.diag & 4) ? clock64() : 0;
             tc::fence_after();
             {
@@ -962,7 +949,8 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
                     f[4 * v4 + 2] = __float_as_uint((float)v.z * uscale);
                     f[4 * v4 + 3] = __float_as_uint((float)v.w * uscale);
                 }
-                tc::tmem_st32_nowait(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a_cols + st * kTileM + cj * 32), f);
+                if (!(p.diag & 64))                            // (A/B: no TMEM store)
+                    tc::tmem_st32_nowait(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a_cols + st * kTileM + cj * 32), f);
             }
             tc::tmem_wait_st();
             tc::fence_before();
@@ -988,7 +976,7 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
         for (int t = (int)cid; t < p.n_tiles; t += (int)ncl, ++it) {
             const int st = it % nst;
             const int64_t a0 = (int64_t)t * p.tile_stride * kTileM;   // shard-local first ad of the tile
-            { EBR_PROF_T0; mbar_wait_sleep(&tfull[st], (it / nst) & 1); if (warp == kEpiWarp0 && lane == 0) EBR_PROF_ADD(7); }
+            { EBR_PROF_T0; crit_wait(&tfull[st], (it / nst) & 1, p.diag); if (warp == kEpiWarp0 && lane == 0) EBR_PROF_ADD(7); }
             tc::fence_after();
             const long long _pe0 = (p.diag & 4) ? clock64() : 0;
 #pragma unroll 1
@@ -996,6 +984,7 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
                 const int qi = hf * 2 + ch;              // tile quarter = 32-column chunk
                 const int c = qi * 32;
                 uint32_t r[32];
+                if (p.diag & 32) continue;                     // (A/B: no TMEM read)
                 tc::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a_cols + st * kTileM + c), r);
                 if (p.diag & 2) continue;
                 const int64_t ac = a0 + c;
@@ -1317,7 +1306,6 @@ bool batch_eligible(const ebr_index* idx, int32_t batch, int32_t slots, int32_t 
     // per-user wide scratch no longer fits L2 (C5 sweep: B=4 at 20 M ads 3.9 ms latency path)
     const bool big = idx->n_ads >= ((int64_t)1 << 21);
     return idx->dtype == EBR_BF16 && (batch >= 16 || (big && batch >= 4)) && idx->d_pad <= 256 &&
-           idx->n_pad <= (int64_t)kMaxBinCounters * kBinAds &&
            idx->n_fields <= 255 && pass_users(idx, slots) >= 32 &&
            idx->n_ads >= (int64_t)4 * kSampleStride * std::max(k, kTileM) && get_encode() != nullptr;
 }
@@ -1374,7 +1362,6 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
         set((const void*)theta_kernel, 200 * 1024);
         set((const void*)final_kernel, 200 * 1024);
         set((const void*)entry_order_kernel, kOrderStage * 4);
-        set((const void*)entry_bin_kernel, kMaxBinCounters * 4);
         for (const void* f : {(const void*)score_kernel<0>, (const void*)score_kernel<1>}) {
             cudaError_t x = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
             (void)x;
@@ -1419,7 +1406,7 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
         trace(q.stream, "plan_b");
         plan_c_kernel<<<std::max(pgrid, 2 * idx->sm_count), 256, 0, q.stream>>>(pa, ws);
         trace(q.stream, "plan_c");
-        entry_bin_kernel<<<2 * idx->sm_count, kBinThreads, (size_t)L.n_bins * 4, q.stream>>>(ea, ws);
+        entry_bin_kernel<<<8 * idx->sm_count, kBinThreads, 0, q.stream>>>(ea, ws);
         trace(q.stream, "entry_bin");
         entry_order_kernel<<<(unsigned)L.n_bins, kOrderThreads, kOrderStage * 4, q.stream>>>(ea, ws);
         trace(q.stream, "entry_order");
