@@ -76,7 +76,9 @@ constexpr int kMaxAccStages = 3;
 constexpr int kMaxStages = 8;        // deep A ring stages (16 KB each; as many as the shared memory allows)
 constexpr int kPrefetchTiles = 4;    // tiles of A prefetched into L2 ahead of the ring's TMA loads
 constexpr int kHotStages = 2;        // ring of on-chip generated one-hot K blocks
-constexpr int kAccPitch = kGroup + 4; // int32 words per fixed-point row of the cold tile [users][ads]
+// int32 words per fixed-point row of the cold tile [users][ads]: an even pitch of 2 mod 32 words
+// keeps the store phase's 64-bit read-and-clear exchanges conflict-free (lane = user)
+constexpr int kAccPitch = kGroup + 2;
 constexpr int kEntBuf = 2048;        // entries of a tile staged in shared memory (bulk copy; the rest from L2)
 constexpr int kEntHdr = 16;          // words of an entry buffer's header (quarter bounds, copied count)
 // shared memory of the fused kernel next to the A ring and the pairs: the hot ring, the cold
@@ -155,15 +157,18 @@ int pass_users(const ebr_index* idx, int32_t slots) {
 }
 
 // the sample covers every sstride-th tile: the largest power of two <= kSampleStrideMax that keeps
-// >= 4 max(K, 128) sampled ads (batch_eligible guarantees it for kSampleStride)
+// >= 4 max(K, 128) sampled ads (batch_eligible guarantees it for kSampleStride) and stride x K
+// <= 160 k (a rank-K rerun then yields ~stride x K candidates per user: the list capacity)
 static int64_t sample_stride(const ebr_index* idx, int k) {
     int64_t st = kSampleStrideMax;
-    while (st > kSampleStride && idx->n_ads < 4 * st * std::max(k, kTileM)) st >>= 1;
+    while (st > kSampleStride && (idx->n_ads < 4 * st * std::max(k, kTileM) || st * k > 160000)) st >>= 1;
     return st;
 }
 
-static int64_t cand_cap(int k) {
-    return std::max<int64_t>(65536, 4 * ((int64_t)k + (int64_t)(100.0 * std::sqrt((double)k)) + 256));
+// candidate list capacity per user: the rank-K rerun's ~stride x K candidates with a 1.5x margin
+static int64_t cand_cap(const ebr_index* idx, int k) {
+    const int64_t st = sample_stride(idx, k);
+    return std::max<int64_t>(65536, (3 * st * (int64_t)k) / 2 + 4096);
 }
 
 static Layout layout(const ebr_index* idx, int32_t slots, int32_t k) {
@@ -176,7 +181,7 @@ static Layout layout(const ebr_index* idx, int32_t slots, int32_t k) {
     L.n_tiles = idx->n_pad / kTileM;
     L.sstride = sample_stride(idx, k);
     L.n_samp = ((L.n_tiles + L.sstride - 1) / L.sstride) * kTileM;
-    L.cap = cand_cap(k);
+    L.cap = cand_cap(idx, k);
     // entry bins of kBinAds ads; a bin's worst case is bin_ads * F entries (an ad has <= F keys)
     L.bin_ads = kBinAds;
     L.bin_cap = L.bin_ads * idx->n_fields;
@@ -938,16 +943,15 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
             tc::fence_after();
             {
                 // this user's 32 ads of the tile: fixed point -> fp32 (the one rounding), zeroed
-                int4* src = reinterpret_cast<int4*>(sAcc + urow * kAccPitch + cj * 32);
+                // read-and-clear in one shared-memory pass: 64-bit atomic exchanges (half the
+                // traffic of a load + a zero store)
+                unsigned long long* src = reinterpret_cast<unsigned long long*>(sAcc + urow * kAccPitch + cj * 32);
                 uint32_t f[32];
 #pragma unroll
-                for (int v4 = 0; v4 < 8; ++v4) {
-                    const int4 v = src[v4];
-                    src[v4] = make_int4(0, 0, 0, 0);
-                    f[4 * v4 + 0] = __float_as_uint((float)v.x * uscale);
-                    f[4 * v4 + 1] = __float_as_uint((float)v.y * uscale);
-                    f[4 * v4 + 2] = __float_as_uint((float)v.z * uscale);
-                    f[4 * v4 + 3] = __float_as_uint((float)v.w * uscale);
+                for (int v2 = 0; v2 < 16; ++v2) {
+                    const unsigned long long v = atomicExch(&src[v2], 0ull);
+                    f[2 * v2 + 0] = __float_as_uint((float)(int32_t)(uint32_t)v * uscale);
+                    f[2 * v2 + 1] = __float_as_uint((float)(int32_t)(uint32_t)(v >> 32) * uscale);
                 }
                 if (!(p.diag & 64))                            // (A/B: no TMEM store)
                     tc::tmem_st32_nowait(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a_cols + st * kTileM + cj * 32), f);

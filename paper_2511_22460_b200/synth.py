@@ -211,8 +211,9 @@ def make_config(cfg: Config | str, mode: str = "real", n_ads: int | None = None,
         inv = make_inventory(n, cfg.d, cfg.n_fields, cfg.alpha, cfg.dtype, mode, seed=base + 0)
         if path:
             os.makedirs(cache, exist_ok=True)
-            np.savez(path + ".tmp.npz", emb=inv.ad_emb, feat=inv.ad_feat, cards=inv.field_card,
-                     w=inv.cross_w, seed=inv.perm_seed)
-            os.replace(path + ".tmp.npz", path)
+            tmp = f"{path}.{os.getpid()}.tmp.npz"          # (concurrent writers: one file each)
+            np.savez(tmp, emb=inv.ad_emb, feat=inv.ad_feat, cards=inv.field_card, w=inv.cross_w,
+                     seed=inv.perm_seed)
+            os.replace(tmp, path)
     users = make_users(inv, b, cfg.slots, cfg.alpha, mode, seed=base + 1)
     return inv, users

@@ -1,0 +1,19 @@
+"""Index build time (A0 / SURVEY NEXT-1): host encoder vs device encoder on the same inventory,
+with the arrays checked bit-identical.  Prints one JSON line per config."""
+import json, os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+from paper_2511_22460_b200 import ebr, synth
+
+for cfg in sys.argv[1:] or ["C3"]:
+    inv, _ = synth.make_config(cfg, mode="real", batch=1)
+    t = time.perf_counter(); h = ebr.Index.of(inv); th = time.perf_counter() - t
+    ebr.Index.of(inv, device_build=True).close()          # warm-up (CUDA context, CUB)
+    t = time.perf_counter(); d = ebr.Index.of(inv, device_build=True); td = time.perf_counter() - t
+    same = all((h.export(w) == d.export(w)).all() for w in range(6))
+    st = d.stats()
+    print(json.dumps({"config": cfg, "n_ads": inv.n_ads, "nnz": st["nnz"], "chunks": st["chunks"],
+                      "host_build_ms": th * 1e3, "device_build_ms": td * 1e3,
+                      "host_reported_ms": h.stats()["build_ms"], "device_reported_ms": st["build_ms"],
+                      "bit_identical": bool(same)}), flush=True)
+    h.close(); d.close()
