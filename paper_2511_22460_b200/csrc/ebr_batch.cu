@@ -523,49 +523,34 @@ __global__ void __launch_bounds__(kBinThreads) entry_bin_kernel(EntryArgs e, Ws 
 constexpr int kOrderCells = (kBinAds / kTileM) * kClasses;   // counters per group (= 32: one per lane)
 
 __global__ void __launch_bounds__(kOrderThreads) entry_order_kernel(EntryArgs e, Ws ws) {
-    // Warp-private counters (no contended shared atomics on the bin's 64 cells): pass 1 counts per
-    // (warp, group, cell) with one add per run of equal cells in a warp (match_any); the scan gives
-    // every (warp, group, cell) its own base; pass 2 -- the same warps over the same entries --
-    // ranks each entry among its warp's equal cells.
-    constexpr int kOW = kOrderThreads / 32;
     extern __shared__ uint32_t smem_u[];
-    __shared__ uint32_t wcnt[kOW][kMaxCluster * kOrderCells];
-    __shared__ uint32_t cellbase[kMaxCluster * kOrderCells];
+    __shared__ uint32_t cnt[kMaxCluster * kOrderCells];
     __shared__ uint32_t sN, sBase[kMaxCluster];
     uint32_t* buf = smem_u;                                 // [kOrderStage]
     const int r = blockIdx.x, tid = threadIdx.x, G = e.G;
-    const int warp = tid >> 5, lane = tid & 31;
     if (tid == 0) { sN = ws.bin_cnt[r]; ws.bin_cnt[r] = 0u; }   // left zero for the next pass
-    for (int i = tid; i < kOW * kMaxCluster * kOrderCells; i += kOrderThreads) (&wcnt[0][0])[i] = 0;
+    for (int i = tid; i < kMaxCluster * kOrderCells; i += kOrderThreads) cnt[i] = 0;
     __syncthreads();
     const uint32_t n = sN;
     const bool staged = n <= (uint32_t)kOrderStage;
     const uint32_t* ent = ws.entries + (size_t)r * e.bin_cap;
     const uint32_t* pinfo = ws.pinfo;
-    const uint32_t n_up = (n + 31u) & ~31u;                 // whole warps iterate (match_any)
-    for (uint32_t i = tid; i < n_up; i += kOrderThreads) {
-        const bool ok = i < n;
-        uint32_t v = 0;
-        if (ok) {
-            v = __ldcs(&ent[i]);
-            if (staged) buf[i] = v;
-        }
+    for (uint32_t i = tid; i < n; i += kOrderThreads) {
+        const uint32_t v = __ldcs(&ent[i]);
+        if (staged) buf[i] = v;
         const uint32_t a = v >> kBinAdShift2, cls = (v >> kBinClsShift) & 63u;
         for (int g = 0; g < G; ++g) {
-            const uint32_t cc = ok ? (cls >> (3 * g)) & 7u : 0u;   // 0: no user of g, else 1 + class
-            const uint32_t cell = cc ? (a >> 7) * kClasses + cc - 1u : 0xFFFFFFFFu;
-            const unsigned peers = __match_any_sync(FULL, cell);
-            if (cc && lane == __ffs(peers) - 1) wcnt[warp][g * kOrderCells + cell] += __popc(peers);
-            __syncwarp();
+            const uint32_t cc = (cls >> (3 * g)) & 7u;           // 0: no user of g, else 1 + class
+            if (cc) atomicAdd(&cnt[g * kOrderCells + (a >> 7) * kClasses + cc - 1u], 1u);
         }
     }
     __syncthreads();
-    // per (group, cell): total over warps, exclusive scan over cells (warp g), the group's range of
-    // the pool, the bin's tile bounds; then each warp's base within the cell
+    // warp g: exclusive scan of group g's counters (lane = tile * kClasses + class), its range
+    // claimed from the pool, the bounds of the bin's tiles
+    const int warp = tid >> 5, lane = tid & 31;
     static_assert(kOrderCells == 32, "one counter per lane");
     if (warp < G) {
-        uint32_t x = 0;
-        for (int w = 0; w < kOW; ++w) x += wcnt[w][warp * kOrderCells + lane];
+        const uint32_t x = cnt[warp * kOrderCells + lane];
         uint32_t incl = x;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -573,7 +558,7 @@ __global__ void __launch_bounds__(kOrderThreads) entry_order_kernel(EntryArgs e,
             if (lane >= o) incl += y;
         }
         const uint32_t tot = __shfl_sync(FULL, incl, 31);
-        cellbase[warp * kOrderCells + lane] = incl - x;
+        cnt[warp * kOrderCells + lane] = incl - x;
         uint32_t base = 0;
         if (lane == 0) base = tot ? atomicAdd(&ws.header[6], tot) : 0u;
         base = __shfl_sync(FULL, base, 0);
@@ -588,33 +573,17 @@ __global__ void __launch_bounds__(kOrderThreads) entry_order_kernel(EntryArgs e,
         }
     }
     __syncthreads();
-    for (int c = tid; c < G * kOrderCells; c += kOrderThreads) {
-        uint32_t acc = sBase[c / kOrderCells] + cellbase[c];
-        for (int w = 0; w < kOW; ++w) {
-            const uint32_t x = wcnt[w][c];
-            wcnt[w][c] = acc;
-            acc += x;
-        }
-    }
-    __syncthreads();
-    for (uint32_t i = tid; i < n_up; i += kOrderThreads) {
-        const bool ok = i < n;
-        const uint32_t v = ok ? (staged ? buf[i] : __ldcs(&ent[i])) : 0u;
+    for (uint32_t i = tid; i < n; i += kOrderThreads) {
+        const uint32_t v = staged ? buf[i] : __ldcs(&ent[i]);
         const uint32_t a = v >> kBinAdShift2, cls = (v >> kBinClsShift) & 63u;
         const uint32_t sl = v & ((1u << kBinClsShift) - 1u);
         for (int g = 0; g < G; ++g) {
-            const uint32_t cc = ok ? (cls >> (3 * g)) & 7u : 0u;
-            const uint32_t cell = cc ? (a >> 7) * kClasses + cc - 1u : 0xFFFFFFFFu;
-            const unsigned peers = __match_any_sync(FULL, cell);
+            const uint32_t cc = (cls >> (3 * g)) & 7u;
             if (cc) {
-                uint32_t* wb = &wcnt[warp][g * kOrderCells + cell];
-                const uint32_t pos = *wb + __popc(peers & ((1u << lane) - 1u));
                 const uint32_t pi = __ldg(&pinfo[(size_t)g * e.NU + sl]);
+                const uint32_t pos = sBase[g] + atomicAdd(&cnt[g * kOrderCells + (a >> 7) * kClasses + cc - 1u], 1u);
                 ws.gentries[pos] = ((a & (kTileM - 1)) << 24) | pi;
-                __syncwarp(peers);
-                if (lane == __ffs(peers) - 1) *wb += __popc(peers);
             }
-            __syncwarp();
         }
     }
 }
