@@ -247,7 +247,9 @@ typedef struct {
     int32_t n_hot;        /* dense hot-key columns of L (bf16 indexes; 0 = none) */
     int32_t pad0;
     int64_t hot_nnz;      /* postings covered by the hot columns               */
-    int64_t hot_bytes;    /* device bytes of the one-hot columns H             */
+    int64_t hot_bytes;    /* device bytes of the hot-key bit masks             */
+    double encode_ms;     /* the inverted-list part of build_ms: host encode, or (device build)
+                             ad_feat upload + GPU sort/encode + hot masks; excludes A's upload */
 } ebr_stats;
 ebr_status ebr_index_stats(const ebr_index *idx, ebr_stats *out);
 

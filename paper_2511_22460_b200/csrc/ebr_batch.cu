@@ -73,7 +73,7 @@ constexpr uint32_t kFlagAny = kFlagShort | kFlagOverflow | kFlagRaise;
 constexpr int kMaxFallback = 2;      // overflowed users per pass recomputed exactly (dense scores)
 
 constexpr int kMaxAccStages = 3;
-constexpr int kMaxStages = 8;        // deep A ring stages (16 KB each; as many as the shared memory allows)
+constexpr int kMaxStages = 12;       // deep A ring stages (16 KB, or 8 KB per CTA of a pair; as many as fit)
 constexpr int kPrefetchTiles = 4;    // tiles of A prefetched into L2 ahead of the ring's TMA loads
 constexpr int kHotStages = 2;        // ring of on-chip generated one-hot K blocks
 // int32 words per fixed-point row of the cold tile [users][ads]: an even pitch of 2 mod 32 words
@@ -617,6 +617,10 @@ struct GemmParams {
     int NU;                 // union slot capacity of the pass (toff row length - 1)
     int gcap;               // pair capacity of a group's list
     int n_tiles_all;        // tiles of the inventory (row length of the group streams' tile bounds)
+    int deep_smem;          // the users' deep operand in shared memory (SS MMA), freeing TMEM for a third
+                            // accumulator stage; else in TMEM with the hot pieces (TS MMA)
+    int pair;               // 2-group pass as a CTA pair: tcgen05.mma.cta_group::2 (M = 256 users), each
+                            // CTA staging half of every ad tile and one-hot block
 };
 
 // the producer's and the MMA issuer's waits: sleeping (default) or spinning (EBR_DIAG & 16)
@@ -630,9 +634,10 @@ __device__ __forceinline__ void crit_wait(uint64_t* bar, uint32_t parity, int di
 #define EBR_PROF_T0 const long long _pt0 = (p.diag & 4) ? clock64() : 0
 #define EBR_PROF_ADD(slot) do { if ((p.diag & 4)) atomicAdd(&p.ws.prof[slot], (unsigned long long)(clock64() - _pt0)); } while (0)
 
-template <int MODE>   // 0: sample (store s; dense: all scores of overflowed users), 1: filter (append keys >= theta)
+template <int MODE, bool PAIR>   // MODE 0: sample (store s; dense: all scores of overflowed users), 1: filter
+                                 // (append keys >= theta); PAIR: the 2-group CTA pair (cta_group::2)
 __global__ void __launch_bounds__(kGemmThreads, 1)
-score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
+score_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmA64, const GemmParams p) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // gated launches (uniform over the grid): nothing to redo
     if (MODE == 1 && p.rerun && (*(volatile uint32_t*)&p.ws.header[2] | *(volatile uint32_t*)&p.ws.header[4]) == 0u)
@@ -650,18 +655,27 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
     const uint16_t mc_mask = (uint16_t)((1u << csize) - 1u);
     const int g = (int)rank;                         // this CTA's user group
     const int nu = min(kGroup, p.P - g * kGroup);    // valid users
-    const int a_cols = 32 * (p.n_kb + p.n_hb * p.pieces);   // TMEM columns of the users' A operand
+    // TMEM columns of the users' A operand: the hot pieces, and the deep part unless it is in smem
+    const int a_cols = 32 * ((p.deep_smem ? 0 : p.n_kb) + p.n_hb * p.pieces);
+    const int hot_col0 = p.deep_smem ? 0 : 32 * p.n_kb;     // TMEM column of the first hot piece
     const int nst = p.acc_stages;
     // deep A ring stages: what the shared memory leaves next to the fixed part and the largest
     // group's pairs of the pass (the same in every CTA of the cluster: the multicast writes the
     // ring stages at the same offsets)
     uint32_t n_gp_max = 0;
     for (uint32_t r = 0; r < csize; ++r) n_gp_max = max(n_gp_max, __ldcg(&p.ws.header[8 + r]));
-    const int nring = (int)min((size_t)kMaxStages,
-                               ((size_t)p.smem_bytes - 1024 - score_smem_fixed() - (size_t)n_gp_max * 4) / kBlockBytes);
+    constexpr bool pair = PAIR;                     // CTA pair: this CTA stages ads 64 rank .. 64 rank + 63 of a tile
+    const uint32_t sb = pair ? kBlockBytes / 2 : kBlockBytes;               // ring stage bytes of this CTA
+    const size_t user_bytes = p.deep_smem ? (size_t)p.n_kb * kBlockBytes : 0;   // [n_kb][128 users x 128 B]
+    // the group's pairs live in shared memory when they fit next to a minimal ring (one tile's deep
+    // blocks + 1), else the scatter reads them from L2 (the same in both CTAs of a cluster)
+    const size_t avail = (size_t)p.smem_bytes - 1024 - score_smem_fixed() - user_bytes;
+    const bool pairs_smem = avail >= (size_t)(p.n_kb + 1) * sb + (size_t)n_gp_max * 4;
+    const int nring = (int)min((size_t)kMaxStages, (avail - (pairs_smem ? (size_t)n_gp_max * 4 : 0)) / sb);
 
-    unsigned char* sRing = smem;                                            // [nring][128 ads x 128 B] deep blocks of A
-    unsigned char* sHot = sRing + (size_t)nring * kBlockBytes;              // [kHotStages][128 ads x 128 B] one-hot blocks
+    unsigned char* sUser = smem;                                            // users' deep operand (deep_smem)
+    unsigned char* sRing = smem + user_bytes;                                            // [nring][128 (pair: 64) ads x 128 B] deep blocks of A
+    unsigned char* sHot = sRing + (size_t)nring * sb;                       // [kHotStages][128 (64) ads x 128 B] one-hot blocks
     int32_t* sAcc = reinterpret_cast<int32_t*>(sHot + (size_t)kHotStages * kBlockBytes);   // [128 users][kAccPitch]
     uint32_t* sEnt = reinterpret_cast<uint32_t*>(sAcc + kGroup * kAccPitch);  // [2][kEntHdr + kEntBuf]
     uint4* sLut = reinterpret_cast<uint4*>(sEnt + 2 * (kEntHdr + kEntBuf));  // [256] byte -> 8 fp16 {0, 1}
@@ -685,25 +699,30 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
     uint32_t* sPairs = reinterpret_cast<uint32_t*>(sDense + kGroup);        // [n_gp] the group's pairs
 
     if (tid == 0) {
-        for (int s = 0; s < nring; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], (p.diag & 8) ? 1u : csize); }
+        for (int s = 0; s < nring; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], (pair || (p.diag & 8)) ? 1u : csize); }
         for (int s = 0; s < 2; ++s) { mbar_init(&efull[s], 1); mbar_init(&eempty[s], 1); }
-        for (int s = 0; s < kHotStages; ++s) { mbar_init(&hfull[s], 1); mbar_init(&hempty[s], 1); }
+        for (int s = 0; s < kHotStages; ++s) { mbar_init(&hfull[s], pair ? 2u : 1u); mbar_init(&hempty[s], 1); }
         for (int s = 0; s < kMaxAccStages; ++s) {
             mbar_init(&tfull[s], 1);
             mbar_init(&tempty[s], kEpiWarps);
         }
-        for (int s = 0; s < kMaxAccStages; ++s) mbar_init(&wready[s], 1);
-        mbar_init(aready, 4);
+        for (int s = 0; s < kMaxAccStages; ++s) mbar_init(&wready[s], pair ? 2u : 1u);
+        mbar_init(aready, pair ? 8u : 4u);
         fence_mbar_init();
     }
-    if (warp == 2) tc::tmem_alloc(tmem_slot, 512);
+    if (warp == 2) {
+        if (pair) tc::tmem_alloc2(tmem_slot, 512);
+        else tc::tmem_alloc(tmem_slot, 512);
+    }
     for (int i = tid; i < kGroup * kAccPitch / 4; i += kGemmThreads)
         reinterpret_cast<int4*>(sAcc)[i] = make_int4(0, 0, 0, 0);
     for (int b = tid; b < 256; b += kGemmThreads) {
         auto h2 = [b](int k) { return ((b >> k) & 1 ? 0x3C00u : 0u) | ((b >> (k + 1)) & 1 ? 0x3C000000u : 0u); };
         sLut[b] = make_uint4(h2(0), h2(2), h2(4), h2(6));
     }
-    for (uint32_t i = tid; i < n_gp; i += kGemmThreads) sPairs[i] = __ldcg(&p.ws.pairs[(size_t)g * p.gcap + i]);
+    if (pairs_smem)
+        for (uint32_t i = tid; i < n_gp; i += kGemmThreads) sPairs[i] = __ldcg(&p.ws.pairs[(size_t)g * p.gcap + i]);
+    const uint32_t* __restrict__ gPairs = p.ws.pairs + (size_t)g * p.gcap;
     for (int i = tid; i < kGroup; i += kGemmThreads) {
         const int u = g * kGroup + i;
         const bool ok = i < nu;
@@ -785,6 +804,13 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
                 for (int kb = 0; kb < p.n_kb; ++kb, ++gb) {
                     const uint32_t slot = gb % nring, round = gb / nring;
                     if (round > 0) { EBR_PROF_T0; crit_wait(&empty[slot], (round - 1) & 1, p.diag); EBR_PROF_ADD(0); }
+                    if (pair) {
+                        // each CTA its 64 rows; both halves' bytes complete on the leader's barrier
+                        if (rank == 0) mbar_arrive_expect_tx(&full[slot], (uint32_t)kBlockBytes);
+                        tc::tma_load_2d_pair(sRing + (size_t)slot * sb, &tmA64, kb * kBlockK, row0 + 64 * (int)rank,
+                                             tc::cluster_addr(&full[slot], 0), pol);
+                        continue;
+                    }
                     mbar_arrive_expect_tx(&full[slot], (uint32_t)kBlockBytes);
                     if (csize == 1 || (p.diag & 8))
                         tc::tma_load_2d_hint(sRing + (size_t)slot * kBlockBytes, &tmA, kb * kBlockK, row0, &full[slot], pol);
@@ -800,45 +826,69 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        if (lane == 0 && (!pair || rank == 0)) {   // (pair: the leader issues for both CTAs)
             // ---------------- MMA issuer ----------------
             // The accumulator stage already holds the tile's cold wide term (stored by the wide
             // warps), so every MMA accumulates: D = cold + U A^T + U_hot (one-hot)^T.
-            const uint32_t idb = tc::idesc_bf16_m128(kTileM), idh = tc::idesc_f16_m128(kTileM);
-            crit_wait(aready, 0, p.diag);                   // users' A operand in TMEM
+            const uint32_t idb = pair ? tc::idesc_bf16_m256(kTileM) : tc::idesc_bf16_m128(kTileM);
+            const uint32_t idh = pair ? tc::idesc_f16_m256(kTileM) : tc::idesc_f16_m128(kTileM);
+            // waits on barriers that receive the peer's arrivals take cluster-scope acquire
+            auto pwait = [&](uint64_t* bar, uint32_t parity) {
+                if (pair) tc::mbar_wait_cluster(bar, parity);
+                else crit_wait(bar, parity, p.diag);
+            };
+            auto mma = [&](uint32_t d, uint32_t a, uint64_t b, uint32_t id) {
+                if (pair) tc::umma2_f16_ts(d, a, b, id, 1u);
+                else tc::umma_f16_ts(d, a, b, id, 1u);
+            };
+            auto commit_all = [&](uint64_t* bar) {       // the arrival every consumer of the stage waits for
+                if (pair) tc::umma2_commit_mc(bar, (uint16_t)3);
+                else tc::umma_commit(bar);
+            };
+            pwait(aready, 0);                               // users' A operand in TMEM (both CTAs)
             tc::fence_after();
             int it = 0;
             uint32_t gb = 0, hb = 0;
             for (int t = (int)cid; t < p.n_tiles; t += (int)ncl, ++it) {
                 const int st = it % nst;
-                { EBR_PROF_T0; crit_wait(&wready[st], (it / nst) & 1, p.diag); EBR_PROF_ADD(1); }
+                { EBR_PROF_T0; pwait(&wready[st], (it / nst) & 1); EBR_PROF_ADD(1); }
                 tc::fence_after();
                 const uint32_t d_tmem = tmem_base + (uint32_t)(a_cols + st * kTileM);
                 for (int kb = 0; kb < p.n_kb; ++kb, ++gb) {
                     const uint32_t slot = gb % nring;
                     if (!(p.diag & 128)) { EBR_PROF_T0; crit_wait(&full[slot], (gb / nring) & 1, p.diag); EBR_PROF_ADD(2); }
                     tc::fence_after();
-                    const uint64_t db0 = tc::sdesc_sw128(sRing + (size_t)slot * kBlockBytes);
+                    const uint64_t db0 = tc::sdesc_sw128(sRing + (size_t)slot * sb);
+                    if (p.deep_smem) {
+                        const uint64_t da0 = tc::sdesc_sw128(sUser + (size_t)kb * kBlockBytes);
 #pragma unroll
-                    for (int k = 0; k < kBlockK / 16; ++k)
-                        tc::umma_f16_ts(d_tmem, tmem_base + (uint32_t)(kb * 32 + k * 8), db0 + (uint64_t)(k * 2), idb, 1u);
-                    if (csize == 1 || (p.diag & 8)) tc::umma_commit(&empty[slot]);
+                        for (int k = 0; k < kBlockK / 16; ++k) {
+                            if (pair) tc::umma2_f16_ss(d_tmem, da0 + (uint64_t)(k * 2), db0 + (uint64_t)(k * 2), idb, 1u);
+                            else tc::umma_f16(d_tmem, da0 + (uint64_t)(k * 2), db0 + (uint64_t)(k * 2), idb, 1u);
+                        }
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < kBlockK / 16; ++k)
+                            mma(d_tmem, tmem_base + (uint32_t)(kb * 32 + k * 8), db0 + (uint64_t)(k * 2), idb);
+                    }
+                    if (pair) tc::umma2_commit_mc(&empty[slot], (uint16_t)3);
+                    else if (csize == 1 || (p.diag & 8)) tc::umma_commit(&empty[slot]);
                     else tc::umma_commit_mc(&empty[slot], mc_mask);
                 }
                 for (int h = 0; h < p.n_hb; ++h, ++hb) {
                     const uint32_t hs = hb % kHotStages;
-                    { EBR_PROF_T0; crit_wait(&hfull[hs], (hb / kHotStages) & 1, p.diag); EBR_PROF_ADD(2); }
+                    { EBR_PROF_T0; pwait(&hfull[hs], (hb / kHotStages) & 1); EBR_PROF_ADD(2); }
                     tc::fence_after();
-                    const uint64_t db0 = tc::sdesc_sw128(sHot + (size_t)hs * kBlockBytes);
+                    const uint64_t db0 = tc::sdesc_sw128(sHot + (size_t)hs * sb);
                     for (int pc = 0; pc < p.pieces; ++pc) {
-                        const uint32_t ac = (uint32_t)(32 * (p.n_kb + h * p.pieces + pc));
+                        const uint32_t ac = (uint32_t)(hot_col0 + 32 * (h * p.pieces + pc));
 #pragma unroll
                         for (int k = 0; k < kBlockK / 16; ++k)
-                            tc::umma_f16_ts(d_tmem, tmem_base + ac + (uint32_t)(k * 8), db0 + (uint64_t)(k * 2), idh, 1u);
+                            mma(d_tmem, tmem_base + ac + (uint32_t)(k * 8), db0 + (uint64_t)(k * 2), idh);
                     }
-                    tc::umma_commit(&hempty[hs]);
+                    commit_all(&hempty[hs]);
                 }
-                tc::umma_commit(&tfull[st]);
+                commit_all(&tfull[st]);
             }
         }
     } else if (warp == 2 || warp == 3) {
@@ -847,13 +897,17 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
         // in the TMA 128B-swizzle layout (chunk c of row r at (c ^ (r & 7)) * 16).  The masks of
         // the next tile are loaded while this one is written.
         if (p.n_hb) {
+            // (pair: this CTA's 64 ad rows of the tile, rows 64 rank ..; thread hw owns row hw)
             const int hw = tid - 64;
-            uint4 hm[2], hn[2];
+            const int nrows = pair ? 1 : 2;
+            const int rbase = pair ? 64 * (int)rank : 0;
+            const uint32_t hfull_leader = pair ? tc::cluster_addr(&hfull[0], 0) : 0u;
+            uint4 hm[2] = {}, hn[2] = {};
             auto load = [&](int tt, uint4 (&m)[2]) {
                 if (tt < p.n_tiles) {
                     const int64_t tw = (int64_t)tt * p.tile_stride;
-                    m[0] = __ldg(&p.hot_mask[tw * kTileM + hw]);
-                    m[1] = __ldg(&p.hot_mask[tw * kTileM + hw + 64]);
+                    m[0] = __ldg(&p.hot_mask[tw * kTileM + rbase + hw]);
+                    if (!pair) m[1] = __ldg(&p.hot_mask[tw * kTileM + hw + 64]);
                 }
             };
             load((int)cid, hn);
@@ -865,12 +919,11 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
                 for (int h = 0; h < p.n_hb; ++h, ++hb) {
                     const uint32_t hs = hb % kHotStages, round = hb / kHotStages;
                     if (round > 0) { EBR_PROF_T0; crit_wait(&hempty[hs], (round - 1) & 1, p.diag); if (hw == 0) EBR_PROF_ADD(3); }
-#pragma unroll
-                    for (int rr = 0; rr < 2; ++rr) {
+                    for (int rr = 0; rr < nrows; ++rr) {
                         const int row = hw + rr * 64;
                         const uint64_t bits = h == 0 ? ((uint64_t)hm[rr].y << 32 | hm[rr].x)
                                                      : ((uint64_t)hm[rr].w << 32 | hm[rr].z);
-                        unsigned char* rowp = sHot + (size_t)hs * kBlockBytes + (size_t)row * 128;
+                        unsigned char* rowp = sHot + (size_t)hs * sb + (size_t)row * 128;
 #pragma unroll
                         for (int c = 0; c < 8; ++c) {                  // 16-byte chunk: keys 8c .. 8c+7
                             const uint32_t byte = (uint32_t)(bits >> (8 * c)) & 0xFFu;
@@ -879,7 +932,10 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
                     }
                     tc::fence_proxy_async_smem();
                     tc::named_bar_sync(2, 64);
-                    if (hw == 0) mbar_arrive(&hfull[hs]);
+                    if (hw == 0) {
+                        if (pair) tc::mbar_arrive_remote(hfull_leader + (uint32_t)(hs * 8));
+                        else mbar_arrive(&hfull[hs]);
+                    }
                 }
             }
         }
@@ -892,16 +948,32 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
             const int urow = q * 32 + lane;
             const uint32_t* urow_p = reinterpret_cast<const uint32_t*>(p.ws.U) +
                                      (size_t)(g * kGroup + urow) * (p.u_cols / 2);
+            const int src0 = p.deep_smem ? 32 * p.n_kb : 0;   // U columns (32-bit) going to TMEM
+            if (p.deep_smem) {
+                // deep K blocks -> shared memory in the 128B-swizzle K-major layout (row urow, 16-byte
+                // chunk c of a block at (c ^ (urow & 7)) * 16)
+                for (int kb = 0; kb < p.n_kb; ++kb)
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const uint4 v = *reinterpret_cast<const uint4*>(urow_p + kb * 32 + 4 * c);
+                        *reinterpret_cast<uint4*>(sUser + (size_t)kb * kBlockBytes + (size_t)urow * 128 +
+                                                  ((c ^ (urow & 7)) << 4)) = v;
+                    }
+                tc::fence_proxy_async_smem();
+            }
             for (int c0 = 0; c0 < a_cols; c0 += 32) {
                 uint32_t v[32];
 #pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = __ldcg(&urow_p[c0 + j]);
+                for (int j = 0; j < 32; ++j) v[j] = __ldcg(&urow_p[src0 + c0 + j]);
                 tc::tmem_st32_nowait(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
             }
             tc::tmem_wait_st();
             tc::fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(aready);
+            if (lane == 0) {
+                if (pair) tc::mbar_arrive_remote(tc::cluster_addr(aready, 0));
+                else mbar_arrive(aready);
+            }
         }
         // Per tile: its entries (ad row, the slot's first pair, pair count) of this CTA's group
         // stream (ordered by pair-count class), staged in shared memory by the producer's bulk
@@ -930,7 +1002,7 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
                 // (a warp's entries share a pair-count class: little divergence in this loop)
 #pragma unroll 2
                 for (uint32_t qq = lo; qq < lo + c; ++qq) {
-                    const uint32_t pr = sPairs[qq];
+                    const uint32_t pr = pairs_smem ? sPairs[qq] : __ldg(&gPairs[qq]);
                     atomicAdd(&sAcc[(pr & (kGroup - 1)) * kAccPitch + a], (int32_t)pr >> kPairUBits);
                 }
             }
@@ -959,7 +1031,10 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
             tc::tmem_wait_st();
             tc::fence_before();
             tc::named_bar_sync(1, kWideThreads);
-            if (wt == 0) mbar_arrive(&wready[st]);
+            if (wt == 0) {
+                if (pair) tc::mbar_arrive_remote(tc::cluster_addr(&wready[st], 0));
+                else mbar_arrive(&wready[st]);
+            }
             if ((p.diag & 4) && wt == 0) atomicAdd(&p.ws.prof[6], (unsigned long long)(clock64() - _ps0));
         }
     } else if (warp >= kEpiWarp0) {
@@ -988,9 +1063,16 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
                 const int qi = hf * 2 + ch;              // tile quarter = 32-column chunk
                 const int c = qi * 32;
                 uint32_t r[32];
-                if (p.diag & 32) continue;                     // (A/B: no TMEM read)
-                tc::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a_cols + st * kTileM + c), r);
-                if (p.diag & 2) continue;
+                if (!(p.diag & 32))                            // (A/B: no TMEM read)
+                    tc::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a_cols + st * kTileM + c), r);
+                if (ch == 1) {
+                    // the stage's last columns of this warp are in registers: hand the stage back
+                    // now (the MMA of tile it + nst can start while this chunk is filtered)
+                    tc::fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[st]);
+                }
+                if (p.diag & (2 | 32)) continue;
                 const int64_t ac = a0 + c;
                 const int nval = (int)min((int64_t)32, max((int64_t)0, p.n_ads - ac));   // valid ads in the chunk
                 if (MODE == 0) {
@@ -1051,9 +1133,6 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
                 }
             }
             if ((p.diag & 4) && warp == kEpiWarp0 && lane == 0) atomicAdd(&p.ws.prof[8], (unsigned long long)(clock64() - _pe0));
-            tc::fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[st]);
         }
     }
     __syncwarp();
@@ -1064,7 +1143,10 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
         atomicAdd(&p.ws.prof[9], 1ull);
         atomicAdd(&p.ws.prof[10], (unsigned long long)(clock64() - _pk0));
     }
-    if (warp == 2) tc::tmem_dealloc(tmem_base, 512);
+    if (warp == 2) {
+        if (pair) tc::tmem_dealloc2(tmem_base, 512);
+        else tc::tmem_dealloc(tmem_base, 512);
+    }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1296,8 +1378,8 @@ static Tuning tuning(const ebr_index* idx) {
     return t;
 }
 
-static size_t gemm_smem(const Layout& L, int stages) {
-    return 1024 + (size_t)stages * kBlockBytes + score_smem_fixed() + (size_t)L.gcap * 4;
+static size_t gemm_smem(const Layout& L, int stages, int user_blocks = 0) {
+    return 1024 + (size_t)(stages + user_blocks) * kBlockBytes + score_smem_fixed() + (size_t)L.gcap * 4;
 }
 
 }  // namespace batch
@@ -1341,17 +1423,23 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
     // score_kernel) plus one of lookahead; TMEM: the users' A operand (32 columns per 64 K) and
     // >= 2 accumulator stages of 128 columns; hot blocks are dropped until both fit
     int stages = 0, acc_stages = 0;
+    // the users' deep operand in shared memory (SS MMA, a third TMEM accumulator stage): opt-in
+    // (EBR_DEEP_SMEM=1); measured no faster (the ring loses two stages), DESIGN.md §6.2
+    static const bool deep_smem = getenv("EBR_DEEP_SMEM") != nullptr && atoi(getenv("EBR_DEEP_SMEM")) != 0;
     for (; tu.n_hb >= 0; --tu.n_hb) {
-        acc_stages = std::min(kMaxAccStages, (512 - 32 * (n_kb + tu.n_hb * tu.pieces)) / kTileM);
+        acc_stages = std::min(kMaxAccStages, (512 - 32 * ((deep_smem ? 0 : n_kb) + tu.n_hb * tu.pieces)) / kTileM);
         if (acc_stages < 2) continue;
         stages = n_kb + 1;          // the minimum with the worst-case pairs; the kernel takes more
-        if (gemm_smem(L, stages) <= (size_t)max_smem) break;
+        if (gemm_smem(L, stages, deep_smem ? n_kb : 0) - (size_t)L.gcap * 4 <= (size_t)max_smem) break;
     }
     if (tu.n_hb < 0) return set_error(EBR_EUNSUPPORTED, "batched path: d=%d does not fit shared memory / TMEM", idx->d);
     const size_t smem = (size_t)max_smem;
-    CUtensorMap tmA;
-    if (!encode_2d_16(&tmA, idx->A, (uint64_t)idx->d_pad, (uint64_t)idx->n_pad, kBlockK, kTileM))
+    CUtensorMap tmA, tmA64;
+    if (!encode_2d_16(&tmA, idx->A, (uint64_t)idx->d_pad, (uint64_t)idx->n_pad, kBlockK, kTileM) ||
+        !encode_2d_16(&tmA64, idx->A, (uint64_t)idx->d_pad, (uint64_t)idx->n_pad, kBlockK, kTileM / 2))
         return set_error(EBR_ECUDA, "cuTensorMapEncodeTiled(A) failed");
+    // CTA-pair MMA for 2-group passes: opt-in (EBR_PAIR=1) until it measures faster
+    static const bool use_pair = getenv("EBR_PAIR") != nullptr && atoi(getenv("EBR_PAIR")) != 0;
     // kernel attributes: set once per process (values fixed by the build)
     static std::once_flag attr_once;
     static cudaError_t attr_err = cudaSuccess;
@@ -1361,12 +1449,14 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
             if (x != cudaSuccess && attr_err == cudaSuccess) attr_err = x;
         };
         const int big = 227 * 1024;
-        set((const void*)score_kernel<0>, big);
-        set((const void*)score_kernel<1>, big);
+        for (const void* f : {(const void*)score_kernel<0, false>, (const void*)score_kernel<1, false>,
+                              (const void*)score_kernel<0, true>, (const void*)score_kernel<1, true>})
+            set(f, big);
         set((const void*)theta_kernel, 200 * 1024);
         set((const void*)final_kernel, 200 * 1024);
         set((const void*)entry_order_kernel, kOrderStage * 4);
-        for (const void* f : {(const void*)score_kernel<0>, (const void*)score_kernel<1>}) {
+        for (const void* f : {(const void*)score_kernel<0, false>, (const void*)score_kernel<1, false>,
+                              (const void*)score_kernel<0, true>, (const void*)score_kernel<1, true>}) {
             cudaError_t x = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
             (void)x;
         }
@@ -1425,6 +1515,8 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
         static const int diag = getenv("EBR_DIAG") ? atoi(getenv("EBR_DIAG")) : 0;
         gp.diag = diag;
         gp.NU = (int)L.NU; gp.gcap = (int)L.gcap; gp.n_tiles_all = n_tiles;
+        gp.pair = (G == 2 && use_pair) ? 1 : 0;
+        gp.deep_smem = deep_smem ? 1 : 0;
         // the U tensor map covers the whole pass tile: each CTA loads its group's 128 rows
         auto launch_score = [&](int mode, int tiles, int stride, int rerun, int dense = 0) -> cudaError_t {
             gp.n_tiles = tiles; gp.tile_stride = stride; gp.rerun = rerun; gp.dense = dense;
@@ -1448,16 +1540,20 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
                 if (!c) {
                     cfg.gridDim = dim3((unsigned)(G * ncl));
                     int n = 0;
-                    cudaError_t x = cudaOccupancyMaxActiveClusters(
-                        &n, mode ? (const void*)score_kernel<1> : (const void*)score_kernel<0>, &cfg);
+                    const void* kf = gp.pair ? (mode ? (const void*)score_kernel<1, true> : (const void*)score_kernel<0, true>)
+                                             : (mode ? (const void*)score_kernel<1, false> : (const void*)score_kernel<0, false>);
+                    cudaError_t x = cudaOccupancyMaxActiveClusters(&n, kf, &cfg);
                     c = (x == cudaSuccess && n > 0) ? n : ncl;
                 }
                 ncl = std::min(ncl, c);
             }
             ncl = std::max(1, std::min(ncl, tiles));
             cfg.gridDim = dim3((unsigned)(G * ncl));
-            return mode ? cudaLaunchKernelEx(&cfg, score_kernel<1>, tmA, gp)
-                        : cudaLaunchKernelEx(&cfg, score_kernel<0>, tmA, gp);
+            if (gp.pair)
+                return mode ? cudaLaunchKernelEx(&cfg, score_kernel<1, true>, tmA, tmA64, gp)
+                            : cudaLaunchKernelEx(&cfg, score_kernel<0, true>, tmA, tmA64, gp);
+            return mode ? cudaLaunchKernelEx(&cfg, score_kernel<1, false>, tmA, tmA64, gp)
+                        : cudaLaunchKernelEx(&cfg, score_kernel<0, false>, tmA, tmA64, gp);
         };
         int32_t* oi = q.out_ids ? q.out_ids + (size_t)b0 * q.k : nullptr;
         float* os = q.out_scores ? q.out_scores + (size_t)b0 * q.k : nullptr;

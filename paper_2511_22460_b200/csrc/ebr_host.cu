@@ -634,8 +634,10 @@ ebr_status ebr_build_index(const void* ad_emb, ebr_dtype dtype, int64_t ad_begin
                              device, prop.major, prop.minor);
         }
         Encoded enc;
+        const auto te0 = std::chrono::steady_clock::now();
         st = encode(ad_feat, n, n_fields, field_card, n_keys, enc);
         if (st) return st;
+        const double enc_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - te0).count();
         ebr_index* idx = new ebr_index();
         memset(idx, 0, sizeof(*idx));
         idx->device = device;
@@ -652,6 +654,7 @@ ebr_status ebr_build_index(const void* ad_emb, ebr_dtype dtype, int64_t ad_begin
         idx->n_chunks = (int64_t)enc.hdr.size() / 2;
         idx->n_words = (int64_t)enc.payload.size() - 2;
         idx->sm_count = prop.multiProcessorCount;
+        idx->encode_ms = enc_ms;
         auto fail = [&](ebr_status s) { ebr_free_index(idx); if (prev >= 0) cudaSetDevice(prev); return s; };
 #define EBR_TRY(call) do { cudaError_t e__ = (call); if (e__ != cudaSuccess) return fail(cuda_check(e__, #call)); } while (0)
         const size_t abytes = (size_t)idx->n_pad * idx->d_pad * esz;
@@ -757,6 +760,8 @@ ebr_status ebr_build_index_device(const void* ad_emb, ebr_dtype dtype, int64_t a
             if (e != cudaSuccess || !bytes) return e;
             return cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, stream);
         };
+        EBR_TRY(cudaStreamSynchronize(stream));        // (A's upload is not part of encode_ms)
+        const auto te0 = std::chrono::steady_clock::now();
         EBR_TRY(upload((void**)&d_feat, ad_feat, (size_t)n * n_fields * 4));
         EBR_TRY(upload((void**)&idx->cross_w, cross_w, (size_t)n_keys * 4));
         std::vector<int32_t> fb(n_fields);
@@ -772,6 +777,7 @@ ebr_status ebr_build_index_device(const void* ad_emb, ebr_dtype dtype, int64_t a
             if (st) return fail(st);
         }
         EBR_TRY(cudaStreamSynchronize(stream));
+        idx->encode_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - te0).count();
         cudaFree(d_feat);
         d_feat = nullptr;
 #undef EBR_TRY
@@ -1061,6 +1067,7 @@ ebr_status ebr_index_stats(const ebr_index* idx, ebr_stats* o) {
     o->n_hot = idx->n_hot;
     o->hot_nnz = idx->hot_nnz;
     o->hot_bytes = idx->hot_mask ? (int64_t)idx->n_pad * 16 : 0;
+    o->encode_ms = idx->encode_ms;
     return EBR_OK;
 }
 

@@ -37,6 +37,7 @@ struct ebr_index {
     void* hot_mask;                 // [n_pad] uint4: 128 bits per ad
     int64_t hot_nnz;                // postings covered by the hot columns
     double build_ms;
+    double encode_ms;               // the inverted-list part of build_ms (ebr_stats)
     int sm_count;
     void* tmap_A;                   // CUtensorMap (host copy) for the tcgen05 path, or null
 };

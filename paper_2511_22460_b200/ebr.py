@@ -102,7 +102,7 @@ class Stats(ctypes.Structure):
                 ("dtype", _I32), ("n_fields", _I32), ("n_keys", _I64), ("nnz", _I64),
                 ("chunks", _I64), ("payload_words", _I64), ("index_bytes", _I64),
                 ("emb_bytes", _I64), ("build_ms", ctypes.c_double), ("n_hot", _I32),
-                ("pad0", _I32), ("hot_nnz", _I64), ("hot_bytes", _I64)]
+                ("pad0", _I32), ("hot_nnz", _I64), ("hot_bytes", _I64), ("encode_ms", ctypes.c_double)]
 
 
 def _np_ptr(a: np.ndarray):

@@ -15,5 +15,6 @@ for cfg in sys.argv[1:] or ["C3"]:
     print(json.dumps({"config": cfg, "n_ads": inv.n_ads, "nnz": st["nnz"], "chunks": st["chunks"],
                       "host_build_ms": th * 1e3, "device_build_ms": td * 1e3,
                       "host_reported_ms": h.stats()["build_ms"], "device_reported_ms": st["build_ms"],
+                      "host_encode_ms": h.stats()["encode_ms"], "device_encode_ms": st["encode_ms"],
                       "bit_identical": bool(same)}), flush=True)
     h.close(); d.close()
