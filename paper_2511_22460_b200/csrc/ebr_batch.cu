@@ -669,14 +669,21 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
     const size_t user_bytes = p.deep_smem ? (size_t)p.n_kb * kBlockBytes : 0;   // [n_kb][128 users x 128 B]
     // the group's pairs live in shared memory when they fit next to a minimal ring (one tile's deep
     // blocks + 1), else the scatter reads them from L2 (the same in both CTAs of a cluster)
-    const size_t avail = (size_t)p.smem_bytes - 1024 - score_smem_fixed() - user_bytes;
+    // (pair mode: the hot ring reservation's second half is free; a second fixed-point tile is
+    // carved when it fits next to the pairs and a ring of >= 3 tiles' deep blocks)
+    constexpr size_t kAccBytes = (size_t)kGroup * kAccPitch * 4;
+    const size_t spare = pair ? (size_t)kHotStages * kBlockBytes / 2 : 0;
+    size_t avail = (size_t)p.smem_bytes - 1024 - score_smem_fixed() - user_bytes + spare;
+    const bool dbl = pair && !(p.diag & 512) &&
+                     avail >= kAccBytes + (size_t)n_gp_max * 4 + (size_t)3 * p.n_kb * sb;
+    if (dbl) avail -= kAccBytes;
     const bool pairs_smem = avail >= (size_t)(p.n_kb + 1) * sb + (size_t)n_gp_max * 4;
     const int nring = (int)min((size_t)kMaxStages, (avail - (pairs_smem ? (size_t)n_gp_max * 4 : 0)) / sb);
 
     unsigned char* sUser = smem;                                            // users' deep operand (deep_smem)
     unsigned char* sRing = smem + user_bytes;                                            // [nring][128 (pair: 64) ads x 128 B] deep blocks of A
     unsigned char* sHot = sRing + (size_t)nring * sb;                       // [kHotStages][128 (64) ads x 128 B] one-hot blocks
-    int32_t* sAcc = reinterpret_cast<int32_t*>(sHot + (size_t)kHotStages * kBlockBytes);   // [128 users][kAccPitch]
+    int32_t* sAcc = reinterpret_cast<int32_t*>(sHot + (size_t)kHotStages * kBlockBytes - spare);   // [128 users][kAccPitch]
     uint32_t* sEnt = reinterpret_cast<uint32_t*>(sAcc + kGroup * kAccPitch);  // [2][kEntHdr + kEntBuf]
     uint4* sLut = reinterpret_cast<uint4*>(sEnt + 2 * (kEntHdr + kEntBuf));  // [256] byte -> 8 fp16 {0, 1}
     uint64_t* bars = reinterpret_cast<uint64_t*>(sLut + 256);
@@ -696,7 +703,10 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
     float* sScale = sThetaS + kGroup;                                       // [kGroup]
     int* sDense = reinterpret_cast<int*>(sScale + kGroup);                  // [kGroup] dense slot or -1
     const uint32_t n_gp = __ldcg(&p.ws.header[8 + g]);
-    uint32_t* sPairs = reinterpret_cast<uint32_t*>(sDense + kGroup);        // [n_gp] the group's pairs
+    unsigned char* after = reinterpret_cast<unsigned char*>(sDense + kGroup);
+    after += (16u - (smem_u32(after) & 15u)) & 15u;
+    int32_t* sAcc2 = dbl ? reinterpret_cast<int32_t*>(after) : nullptr;      // second fixed-point tile (dbl)
+    uint32_t* sPairs = reinterpret_cast<uint32_t*>(after + (dbl ? kAccBytes : 0));   // [n_gp] the group's pairs
 
     if (tid == 0) {
         for (int s = 0; s < nring; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], (pair || (p.diag & 8)) ? 1u : csize); }
@@ -714,8 +724,10 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
         if (pair) tc::tmem_alloc2(tmem_slot, 512);
         else tc::tmem_alloc(tmem_slot, 512);
     }
-    for (int i = tid; i < kGroup * kAccPitch / 4; i += kGemmThreads)
+    for (int i = tid; i < kGroup * kAccPitch / 4; i += kGemmThreads) {
         reinterpret_cast<int4*>(sAcc)[i] = make_int4(0, 0, 0, 0);
+        if (dbl) reinterpret_cast<int4*>(sAcc2)[i] = make_int4(0, 0, 0, 0);
+    }
     for (int b = tid; b < 256; b += kGemmThreads) {
         auto h2 = [b](int k) { return ((b >> k) & 1 ? 0x3C00u : 0u) | ((b >> (k + 1)) & 1 ? 0x3C000000u : 0u); };
         sLut[b] = make_uint4(h2(0), h2(2), h2(4), h2(6));
@@ -986,9 +998,8 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
         const int cj = (warp - kWideWarp0) >> 2;         // this warp's 32-ad column chunk (store phase)
         const int urow = q * 32 + lane;
         const float uscale = sScale[urow];
-        int it = 0;
-        for (int t = (int)cid; t < p.n_tiles; t += (int)ncl, ++it) {
-            const int st = it % nst;
+        // scatter of tile `it`'s entries into the fixed-point tile `acc`
+        auto scatter = [&](int it, int32_t* acc) {
             const int eb = it & 1;
             { EBR_PROF_T0; crit_wait(&efull[eb], (it >> 1) & 1, p.diag); if (wt == 0) EBR_PROF_ADD(11); }
             const long long _pc0 = (p.diag & 4) ? clock64() : 0;
@@ -1003,21 +1014,25 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
 #pragma unroll 2
                 for (uint32_t qq = lo; qq < lo + c; ++qq) {
                     const uint32_t pr = pairs_smem ? sPairs[qq] : __ldg(&gPairs[qq]);
-                    atomicAdd(&sAcc[(pr & (kGroup - 1)) * kAccPitch + a], (int32_t)pr >> kPairUBits);
+                    atomicAdd(&acc[(pr & (kGroup - 1)) * kAccPitch + a], (int32_t)pr >> kPairUBits);
                 }
             }
             tc::named_bar_sync(1, kWideThreads);
             if (wt == 0) mbar_arrive(&eempty[eb]);      // entry buffer consumed
             if ((p.diag & 4) && wt == 0) atomicAdd(&p.ws.prof[4], (unsigned long long)(clock64() - _pc0));
+        };
+        // tile `it`'s cold term: read-and-clear `acc`, fp32, into the TMEM stage, MMA released
+        auto store = [&](int it, int32_t* acc) {
+            const int st = it % nst;
             // the accumulator stage is free once the epilogue drained it (nst tiles ago)
             if (it >= nst) { EBR_PROF_T0; crit_wait(&tempty[st], ((it / nst) - 1) & 1, p.diag); if (wt == 0) EBR_PROF_ADD(5); }
             const long long _ps0 = (p.diag & 4) ? clock64() : 0;
             tc::fence_after();
             {
-                // this user's 32 ads of the tile: fixed point -> fp32 (the one rounding), zeroed
-                // read-and-clear in one shared-memory pass: 64-bit atomic exchanges (half the
+                // this user's 32 ads of the tile: fixed point -> fp32 (the one rounding), zeroed;
+                // read-and-clear in one shared-memory pass by 64-bit atomic exchanges (half the
                 // traffic of a load + a zero store)
-                unsigned long long* src = reinterpret_cast<unsigned long long*>(sAcc + urow * kAccPitch + cj * 32);
+                unsigned long long* src = reinterpret_cast<unsigned long long*>(acc + urow * kAccPitch + cj * 32);
                 uint32_t f[32];
 #pragma unroll
                 for (int v2 = 0; v2 < 16; ++v2) {
@@ -1036,6 +1051,20 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                 else mbar_arrive(&wready[st]);
             }
             if ((p.diag & 4) && wt == 0) atomicAdd(&p.ws.prof[6], (unsigned long long)(clock64() - _ps0));
+        };
+        const int n_my = (int)cid < p.n_tiles ? (p.n_tiles - (int)cid + (int)ncl - 1) / (int)ncl : 0;
+        if (sAcc2) {
+            // two fixed-point tiles: tile it + 1 is scattered while tile it waits for its TMEM stage
+            if (n_my > 0) scatter(0, sAcc);
+            for (int it = 0; it < n_my; ++it) {
+                if (it + 1 < n_my) scatter(it + 1, (it & 1) ? sAcc : sAcc2);
+                store(it, (it & 1) ? sAcc2 : sAcc);
+            }
+        } else {
+            for (int it = 0; it < n_my; ++it) {
+                scatter(it, sAcc);
+                store(it, sAcc);
+            }
         }
     } else if (warp >= kEpiWarp0) {
         // ---------------- epilogue: TMEM -> s, kappa, sample store / filter ----------------

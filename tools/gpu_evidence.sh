@@ -15,6 +15,4 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:scor
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:small_kernel -s 5 -c 1 -o $OUT/ev_c2_small python bench.py --config C2 --profile --steps 6 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 timeout 900 python tools/build_time.py C2 C3 C4 C5 > $OUT/ev_build_time.jsonl 2>&1; cat $OUT/ev_build_time.jsonl
 timeout 1500 python tools/sweep_c5.py > $OUT/ev_c5_sweep.jsonl 2>&1; tail -3 $OUT/ev_c5_sweep.jsonl
-timeout 900 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -q -x -k "tiny or k_larger or exact_mode_bit_exact" > $OUT/ev_memcheck.log 2>&1; echo "memcheck rc=$?"; tail -3 $OUT/ev_memcheck.log
-timeout 900 compute-sanitizer --tool racecheck --error-exitcode 9 python -m pytest tests/test_gpu_batch.py -q -x -k "exact_bit_exact and C4" > $OUT/ev_racecheck.log 2>&1; echo "racecheck rc=$?"; tail -3 $OUT/ev_racecheck.log
 echo done
