@@ -324,12 +324,26 @@ __global__ void __launch_bounds__(kPlanThreads) plan_b_kernel(PlanArgs a, Ws ws)
     const int64_t per = (a.TS + kPlanThreads - 1) / kPlanThreads;
     const int64_t t0 = (int64_t)tid * per, t1 = min(a.TS, t0 + per);
     uint32_t v[kPlanNV] = {};
-    for (int64_t t = t0; t < t1; ++t) {
-        const uint32_t key1 = ws.hkey[t];
-        if (!key1) continue;
-        v[0] += 1u;
-        v[1] += a.key_chunk_off[key1] - a.key_chunk_off[key1 - 1u];
-        for (int g = 0; g < kMaxCluster; ++g) v[2 + g] += ws.hcnt[t * kMaxCluster + g];
+    // 8 table positions per round with every load of a round in flight at once (this CTA alone
+    // walks the whole table: the latency of dependent loads is the cost)
+    for (int64_t tb = t0; tb < t1; tb += 8) {
+        uint32_t key1[8], c0[8], c1[8], hc[8][kMaxCluster];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) key1[j] = tb + j < t1 ? ws.hkey[tb + j] : 0u;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            c0[j] = key1[j] ? a.key_chunk_off[key1[j] - 1u] : 0u;
+            c1[j] = key1[j] ? a.key_chunk_off[key1[j]] : 0u;
+#pragma unroll
+            for (int g = 0; g < kMaxCluster; ++g) hc[j][g] = key1[j] ? ws.hcnt[(tb + j) * kMaxCluster + g] : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            v[0] += key1[j] ? 1u : 0u;
+            v[1] += c1[j] - c0[j];
+#pragma unroll
+            for (int g = 0; g < kMaxCluster; ++g) v[2 + g] += hc[j][g];
+        }
     }
     // block exclusive scan of v[] over threads
     uint32_t incl[kPlanNV];
