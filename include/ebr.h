@@ -275,6 +275,36 @@ ebr_status ebr_encode_host(const int32_t *ad_feat, int64_t n_ads, int32_t n_fiel
                            uint32_t *payload, int64_t payload_cap, int64_t *n_chunks,
                            int64_t *n_words);
 
+/* ------------------------------------------------------------------------------------------ */
+/* NEXT-3 ablation: the paper's own inverted list (Alg. 1-2) on the same B200          */
+/* ------------------------------------------------------------------------------------------ */
+/*
+ * Not a path of ebr_score_topk: an ablation that builds the paper's index -- blocks of the ads
+ * sharing the high 24 bits of their id, grouped by ceil(log2 n) and padded to 2^g one-byte
+ * residuals, per-group SoA with per-key offsets (Alg. 1; readings R5-R7 of DESIGN.md:
+ * the valid count rides in the header word, keys are a CSR) -- and runs Alg. 2 for one
+ * user: scores[a] = sum over the query items (key, w) of w * L[a, key], by fp32 AtomicAdd into a
+ * global score array (zeroed first, Alg. 2 l.350).  ebr_chunk_hitmatch runs the same algorithm on
+ * this library's chunk codec, for an equal-terms comparison of the two layouts.
+ *
+ *  ad_feat etc.   host, as ebr_build_index (shard-local ids 0..n_ads-1); host-synchronous build.
+ *  keys, w        device, [n_items] int32 keys (out-of-range keys ignored) and fp32 weights w~.
+ *  scores         device, [n_ads] fp32, overwritten.  n_items <= 1024.  Async on `stream`.
+ * Errors: EBR_EINVAL (bad arguments / values), EBR_ECUDA.
+ */
+typedef struct ebr_paper_index ebr_paper_index;
+ebr_status ebr_paper_index_build(const int32_t *ad_feat, int64_t n_ads, int32_t n_fields,
+                                 const int32_t *field_card, int64_t n_keys, int device,
+                                 void *stream, ebr_paper_index **out);
+void ebr_paper_index_free(ebr_paper_index *pidx);
+/* blocks per group (host, [9]), device bytes and host build time of the paper index */
+ebr_status ebr_paper_index_info(const ebr_paper_index *pidx, int64_t *blocks9, int64_t *bytes,
+                                double *build_ms);
+ebr_status ebr_paper_hitmatch(const ebr_paper_index *pidx, const int32_t *keys, const float *w,
+                              int32_t n_items, float *scores, void *stream);
+ebr_status ebr_chunk_hitmatch(const ebr_index *idx, const int32_t *keys, const float *w,
+                              int32_t n_items, float *scores, void *stream);
+
 /* Number of CUDA kernels (and memsets) one ebr_score_topk* call with these arguments enqueues on
  * its stream (the latency path: one cooperative launch per 4 users; the batched tensor-core path:
  * 1 memset plus 7 launches per group of 128 users).  Excludes the rare overflow fallback. */

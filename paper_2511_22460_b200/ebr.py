@@ -53,6 +53,11 @@ EXPORTS = {
     "ebr_exchange_kth": (ctypes.c_int, [_P, _I32, _I32, _I32, _P, _P]),
     "ebr_exchange_pack": (ctypes.c_int, [_P, _I32, _I32, _P, _I32, _P, _P, _P, _P]),
     "ebr_merge_topk_packed": (ctypes.c_int, [_P, _I64, _P, _I32, _I32, _I32, _P, _P, _P]),
+    "ebr_paper_index_build": (ctypes.c_int, [_P, _I64, _I32, _P, _I64, ctypes.c_int, _P, ctypes.POINTER(_P)]),
+    "ebr_paper_index_free": (None, [_P]),
+    "ebr_paper_index_info": (ctypes.c_int, [_P, _P, ctypes.POINTER(_I64), ctypes.POINTER(ctypes.c_double)]),
+    "ebr_paper_hitmatch": (ctypes.c_int, [_P, _P, _P, _I32, _P, _P]),
+    "ebr_chunk_hitmatch": (ctypes.c_int, [_P, _P, _P, _I32, _P, _P]),
     "ebr_kernel_timer": (ctypes.c_int, [_I32]),
     "ebr_kernel_timer_read": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64),
                                              ctypes.c_char_p, _I32]),
@@ -77,6 +82,51 @@ def last_error() -> str:
 
 def version() -> str:
     return _lib.ebr_version().decode()
+
+
+class PaperIndex:
+    """NEXT-3 ablation: the paper's own inverted list (Alg. 1) on the GPU (ebr_paper_index_build)."""
+
+    def __init__(self, ad_feat, field_card, device: int = 0, stream=None):
+        ad_feat = np.ascontiguousarray(ad_feat, np.int32)
+        field_card = np.ascontiguousarray(field_card, np.int32)
+        self.n_ads, self.n_fields = ad_feat.shape
+        self.n_keys = int(field_card.astype(np.int64).sum())
+        h = ctypes.c_void_p()
+        _check(_lib.ebr_paper_index_build(_np_ptr(ad_feat), self.n_ads, self.n_fields, _np_ptr(field_card),
+                                          self.n_keys, device, _stream_ptr(stream), ctypes.byref(h)),
+               "ebr_paper_index_build")
+        self._h = h
+
+    def info(self) -> dict:
+        blocks = np.zeros(9, np.int64)
+        nb, ms = ctypes.c_int64(0), ctypes.c_double(0.0)
+        _check(_lib.ebr_paper_index_info(self._h, _np_ptr(blocks), ctypes.byref(nb), ctypes.byref(ms)),
+               "ebr_paper_index_info")
+        return {"blocks_per_group": blocks.tolist(), "bytes": nb.value, "build_ms": ms.value}
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.ebr_paper_index_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def paper_hitmatch(pidx: PaperIndex, keys, w, scores, stream=None):
+    """Alg. 2 on the paper's layout: scores[a] = sum_i w[i] L[a, keys[i]] (device tensors)."""
+    _check(_lib.ebr_paper_hitmatch(pidx._h, _t_ptr(keys), _t_ptr(w), keys.shape[0], _t_ptr(scores),
+                                   _stream_ptr(stream)), "ebr_paper_hitmatch")
+
+
+def chunk_hitmatch(idx: Index, keys, w, scores, stream=None):
+    """The same algorithm on this library's chunk codec (ebr_chunk_hitmatch)."""
+    _check(_lib.ebr_chunk_hitmatch(idx.handle, _t_ptr(keys), _t_ptr(w), keys.shape[0], _t_ptr(scores),
+                                   _stream_ptr(stream)), "ebr_chunk_hitmatch")
 
 
 def kernel_timer(enable: bool) -> None:
