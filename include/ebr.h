@@ -305,6 +305,18 @@ ebr_status ebr_paper_hitmatch(const ebr_paper_index *pidx, const int32_t *keys, 
 ebr_status ebr_chunk_hitmatch(const ebr_index *idx, const int32_t *keys, const float *w,
                               int32_t n_items, float *scores, void *stream);
 
+/*
+ * NEXT-4, in-query IPNN (Eq. 7-8): async.  For rows b in [0, rows):
+ *   out[b] = [h[b], W u[b]]  (length d0 + d1), the W u part accumulated in fp32 (fma over i in
+ *   order) and rounded once to `dtype` (bf16: round-to-nearest-even).
+ * h: device [rows][d0] in `dtype` (the dual tower's output h_u or h_a); u: device [rows][n] fp32
+ * (the pooled user / ad features); W: device [d1][n] fp32 row-major (W^(u) or W^(v)); out: device
+ * [rows][d0 + d1] in `dtype` -- the h~ that ebr_build_index (ads) and ebr_score_topk (users) take.
+ * Errors: EBR_EINVAL (null pointers, negative sizes, n > 12288, bad dtype), EBR_ECUDA.
+ */
+ebr_status ebr_ipnn_extend(const void *h, const float *u, const float *W, int64_t rows, int32_t d0,
+                           int32_t n, int32_t d1, ebr_dtype dtype, void *out, void *stream);
+
 /* Number of CUDA kernels (and memsets) one ebr_score_topk* call with these arguments enqueues on
  * its stream (the latency path: one cooperative launch per 4 users; the batched tensor-core path:
  * 1 memset plus 7 launches per group of 128 users).  Excludes the rare overflow fallback. */

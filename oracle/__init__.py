@@ -43,8 +43,9 @@ def lib():
                                      _I, _I64, _I, _P, _P, _P]
         _lib.oracle_postings.argtypes = [_I64, _I, _P, _P, _I64, _P, _P]
         _lib.oracle_decode_chunks.argtypes = [_I64, _P, _P, _P, _P, _I64, _P, _P, _I64]
+        _lib.oracle_ipnn_extend.argtypes = [_I64, _I, _I, _I, _I, _P, _P, _P, _P]
         for f in ("oracle_scores_user", "oracle_wide_pairs_user", "oracle_topk",
-                  "oracle_postings", "oracle_decode_chunks"):
+                  "oracle_postings", "oracle_decode_chunks", "oracle_ipnn_extend"):
             getattr(_lib, f).restype = _I
     return _lib
 
@@ -153,3 +154,22 @@ def decode_chunks(key_chunk_off, key_word_off, chunk_hdr, payload, cap: int):
     if rc:
         raise ValueError(f"oracle_decode_chunks rc={rc}")
     return off, ads[: int(off[-1])]
+
+
+def ipnn_extend(h, u, W):
+    """IPNN extension (Eq. 7-8): [h, W u] per row in fp64.  h: [rows][d0] fp32 or bf16
+    bits (uint16); u: [rows][n] fp32; W: [d1][n] fp32."""
+    h = np.ascontiguousarray(h)
+    is_bf16 = 1 if h.dtype == np.uint16 else 0
+    if not is_bf16:
+        h = np.ascontiguousarray(h, np.float32)
+    u = np.ascontiguousarray(u, np.float32)
+    W = np.ascontiguousarray(W, np.float32)
+    rows, d0 = h.shape
+    d1, n = W.shape
+    out = np.empty((rows, d0 + d1), np.float64)
+    rc = lib().oracle_ipnn_extend(rows, d0, n, d1, is_bf16, h.ctypes.data, u.ctypes.data, W.ctypes.data,
+                                  out.ctypes.data)
+    if rc:
+        raise ValueError(f"oracle_ipnn_extend rc={rc}")
+    return out

@@ -334,3 +334,24 @@ int oracle_decode_chunks(int64_t n_keys, const uint32_t *key_chunk_off,
     }
     return 0;
 }
+
+/*
+ * oracle_ipnn_extend (NEXT-4, Eq. 7-8): the IPNN extension of a tower output,
+ *   h~ = [h, W u],  W in R^{d1 x n} row-major, u in R^n,
+ * written out in fp64 (W u accumulated over i in order); out is fp64 [rows][d0 + d1].  h is read as
+ * fp32 or bf16 bits (widened exactly).
+ */
+int oracle_ipnn_extend(int64_t rows, int d0, int n, int d1, int h_is_bf16, const void *h, const float *u,
+                       const float *W, double *out) {
+    if (rows < 0 || d0 < 0 || n < 0 || d1 < 0) return 1;
+    for (int64_t b = 0; b < rows; ++b) {
+        double *o = out + b * (int64_t)(d0 + d1);
+        for (int j = 0; j < d0; ++j) o[j] = emb_at(h, h_is_bf16, b, d0, j);
+        for (int j = 0; j < d1; ++j) {
+            double s = 0.0;
+            for (int i = 0; i < n; ++i) s += (double)W[(int64_t)j * n + i] * (double)u[b * (int64_t)n + i];
+            o[d0 + j] = s;
+        }
+    }
+    return 0;
+}

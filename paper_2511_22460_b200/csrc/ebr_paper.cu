@@ -262,3 +262,48 @@ ebr_status ebr_chunk_hitmatch(const ebr_index* idx, const int32_t* keys, const f
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------------------------------
+// NEXT-4: the IPNN extension of a tower output (Eq. 7-8): h~ = [h, W u] per row, the
+// W u part accumulated in fp32 and rounded once to the index dtype.  Rows = users (per query,
+// before ebr_score_topk) or ads (before ebr_build_index).
+// ------------------------------------------------------------------------------------------
+namespace ebr {
+template <typename T>
+__global__ void __launch_bounds__(256) ipnn_kernel(const T* __restrict__ h, const float* __restrict__ u,
+                                                   const float* __restrict__ W, int64_t rows, int d0, int n, int d1,
+                                                   T* __restrict__ out) {
+    extern __shared__ float su[];                    // [n] this row's u
+    for (int64_t b = blockIdx.x; b < rows; b += gridDim.x) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < n; i += blockDim.x) su[i] = u[b * n + i];
+        __syncthreads();
+        T* o = out + b * (int64_t)(d0 + d1);
+        for (int j = threadIdx.x; j < d0; j += blockDim.x) o[j] = h[b * d0 + j];
+        for (int j = threadIdx.x; j < d1; j += blockDim.x) {
+            const float* wr = W + (int64_t)j * n;
+            float s = 0.f;
+            for (int i = 0; i < n; ++i) s = fmaf(__ldg(&wr[i]), su[i], s);
+            if constexpr (sizeof(T) == 2) o[d0 + j] = __float2bfloat16_rn(s);
+            else o[d0 + j] = s;
+        }
+    }
+}
+}  // namespace ebr
+
+extern "C" ebr_status ebr_ipnn_extend(const void* h, const float* u, const float* W, int64_t rows, int32_t d0,
+                                      int32_t n, int32_t d1, ebr_dtype dtype, void* out, void* stream_v) {
+    if (!out || (d0 > 0 && !h) || (n > 0 && (!u || !W))) return set_error(EBR_EINVAL, "null pointer");
+    if (rows < 0 || d0 < 0 || n < 0 || d1 < 0 || n > 12 * 1024) return set_error(EBR_EINVAL, "bad sizes");
+    if (dtype != EBR_F32 && dtype != EBR_BF16) return set_error(EBR_EINVAL, "bad dtype");
+    if (rows == 0) return EBR_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream_v);
+    const unsigned grid = (unsigned)std::min<int64_t>(rows, 148 * 16);
+    if (dtype == EBR_BF16)
+        ipnn_kernel<__nv_bfloat16><<<grid, 256, (size_t)n * 4, st>>>(static_cast<const __nv_bfloat16*>(h), u, W, rows,
+                                                                    d0, n, d1, static_cast<__nv_bfloat16*>(out));
+    else
+        ipnn_kernel<float><<<grid, 256, (size_t)n * 4, st>>>(static_cast<const float*>(h), u, W, rows, d0, n, d1,
+                                                            static_cast<float*>(out));
+    return cuda_check(cudaGetLastError(), "launch(ipnn)");
+}

@@ -58,6 +58,7 @@ EXPORTS = {
     "ebr_paper_index_info": (ctypes.c_int, [_P, _P, ctypes.POINTER(_I64), ctypes.POINTER(ctypes.c_double)]),
     "ebr_paper_hitmatch": (ctypes.c_int, [_P, _P, _P, _I32, _P, _P]),
     "ebr_chunk_hitmatch": (ctypes.c_int, [_P, _P, _P, _I32, _P, _P]),
+    "ebr_ipnn_extend": (ctypes.c_int, [_P, _P, _P, _I64, _I32, _I32, _I32, ctypes.c_int, _P, _P]),
     "ebr_kernel_timer": (ctypes.c_int, [_I32]),
     "ebr_kernel_timer_read": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64),
                                              ctypes.c_char_p, _I32]),
@@ -127,6 +128,16 @@ def chunk_hitmatch(idx: Index, keys, w, scores, stream=None):
     """The same algorithm on this library's chunk codec (ebr_chunk_hitmatch)."""
     _check(_lib.ebr_chunk_hitmatch(idx.handle, _t_ptr(keys), _t_ptr(w), keys.shape[0], _t_ptr(scores),
                                    _stream_ptr(stream)), "ebr_chunk_hitmatch")
+
+
+def ipnn_extend(h, u, W, out, stream=None):
+    """h~ = [h, W u] per row (Eq. 7-8) on the device: h [rows][d0] float32 or int16 (bf16 bits),
+    u [rows][n] float32, W [d1][n] float32, out [rows][d0 + d1] in h's dtype."""
+    rows, d0 = h.shape
+    d1, n = W.shape
+    dtype = BF16 if h.element_size() == 2 else F32
+    _check(_lib.ebr_ipnn_extend(_t_ptr(h), _t_ptr(u), _t_ptr(W), rows, d0, n, d1, dtype, _t_ptr(out),
+                                _stream_ptr(stream)), "ebr_ipnn_extend")
 
 
 def kernel_timer(enable: bool) -> None:

@@ -252,3 +252,24 @@ def test_decoder_special_chunks():
     off, ads = oracle.decode_chunks(kco, kwo, hdr, payload, cap=64)
     assert off.tolist() == [0, 1, 36]
     assert ads.tolist() == [7] + list(range(10, 42)) + [50, 53, 69]
+
+
+# ---- NEXT-4: the IPNN extension h~ = [h, W u] (Eq. 7-8)
+
+def test_ipnn_extend_hand_example_and_numpy():
+    W = np.array([[1, 2], [3, 4]], np.float32)
+    u = np.array([[1, 1], [0.5, -2]], np.float32)
+    h = np.array([[0.5], [-1.0]], np.float32)
+    out = oracle.ipnn_extend(h, u, W)
+    assert (out == np.array([[0.5, 3, 7], [-1.0, -3.5, -6.5]])).all()      # worked by hand
+    rng = np.random.default_rng(7)
+    h = rng.standard_normal((5, 9)).astype(np.float32)
+    u = rng.standard_normal((5, 33)).astype(np.float32)
+    W = rng.standard_normal((12, 33)).astype(np.float32)
+    out = oracle.ipnn_extend(h, u, W)
+    assert (out[:, :9] == h.astype(np.float64)).all()
+    assert np.allclose(out[:, 9:], u.astype(np.float64) @ W.astype(np.float64).T, rtol=1e-13, atol=1e-12)
+    # bf16 tower outputs are widened exactly
+    hb = np.array([[0x3F80, 0xC000]], np.uint16)                     # 1.0, -2.0
+    assert (oracle.ipnn_extend(hb, np.zeros((1, 1), np.float32), np.zeros((1, 1), np.float32))[0, :2]
+            == [1.0, -2.0]).all()
