@@ -100,6 +100,20 @@ ebr_status ebr_build_index_device(const void *ad_emb, ebr_dtype dtype, int64_t a
                                   const float *cross_w, int64_t n_keys, int device, void *stream,
                                   ebr_index **out);
 
+/*
+ * NEXT-4, multi-valued ad fields (tags): the same index (device build) from L given ad by
+ * ad as key lists -- ad a (shard-local) holds the global keys ad_keys[ad_key_off[a] ..
+ * ad_key_off[a+1]), any number per field (key = base_f + v as for ad_feat; <= 1024 keys per ad).
+ * L is binary: a key listed twice for one ad is EBR_EINVAL; keys outside [0, n_keys) are EBR_EINVAL.
+ *  ad_key_off host [n + 1] int64 (ad_key_off[0] = 0, ascending), ad_keys host [ad_key_off[n]] int32.
+ * Every other argument and the result as ebr_build_index_device.  The query calls are unchanged.
+ */
+ebr_status ebr_build_index_lists(const void *ad_emb, ebr_dtype dtype, int64_t ad_begin,
+                                 int64_t ad_end, int32_t d, const int64_t *ad_key_off,
+                                 const int32_t *ad_keys, int32_t n_fields, const int32_t *field_card,
+                                 const float *cross_w, int64_t n_keys, int device, void *stream,
+                                 ebr_index **out);
+
 void ebr_free_index(ebr_index *idx);
 
 /* ------------------------------------------------------------------------------------------ */

@@ -44,8 +44,11 @@ def lib():
         _lib.oracle_postings.argtypes = [_I64, _I, _P, _P, _I64, _P, _P]
         _lib.oracle_decode_chunks.argtypes = [_I64, _P, _P, _P, _P, _I64, _P, _P, _I64]
         _lib.oracle_ipnn_extend.argtypes = [_I64, _I, _I, _I, _I, _P, _P, _P, _P]
+        _lib.oracle_scores_user_pairs.argtypes = [_I64, _I, _I, _P, _P, _P, _I, _P, _P, _I64, _P, _I, _P, _P,
+                                                  _P, _P]
         for f in ("oracle_scores_user", "oracle_wide_pairs_user", "oracle_topk",
-                  "oracle_postings", "oracle_decode_chunks", "oracle_ipnn_extend"):
+                  "oracle_postings", "oracle_decode_chunks", "oracle_ipnn_extend",
+                  "oracle_scores_user_pairs"):
             getattr(_lib, f).restype = _I
     return _lib
 
@@ -173,3 +176,34 @@ def ipnn_extend(h, u, W):
     if rc:
         raise ValueError(f"oracle_ipnn_extend rc={rc}")
     return out
+
+
+class OraclePairs:
+    """Scorer A for an inventory whose L is given ad by ad as key lists (multi-valued fields):
+    ad_key_off [N+1] int64, ad_keys [nnz] int32 (global keys base_f + v)."""
+
+    def __init__(self, ad_emb, ad_key_off, ad_keys, field_card, cross_w):
+        self.ad_emb, self.is_bf16 = _emb(ad_emb)
+        self.off = np.ascontiguousarray(ad_key_off, np.int64)
+        self.keys = np.ascontiguousarray(ad_keys, np.int32)
+        self.field_card = np.ascontiguousarray(field_card, np.int32)
+        self.cross_w = np.ascontiguousarray(cross_w, np.float32)
+        self.n_ads, self.d = self.ad_emb.shape
+        self.n_keys = int(self.field_card.astype(np.int64).sum())
+
+    def scores(self, user_emb, user_feat, user_x):
+        ue, ub = _emb(np.asarray(user_emb).reshape(1, -1))
+        assert ub == self.is_bf16
+        uf = np.ascontiguousarray(user_feat, np.int32)
+        ux = np.ascontiguousarray(user_x, np.float32)
+        r = np.empty(self.n_ads, np.float64)
+        s = np.empty(self.n_ads, np.float64)
+        rc = lib().oracle_scores_user_pairs(self.n_ads, self.d, self.is_bf16, self.ad_emb.ctypes.data,
+                                            self.off.ctypes.data, self.keys.ctypes.data,
+                                            self.field_card.shape[0], self.field_card.ctypes.data,
+                                            self.cross_w.ctypes.data, self.n_keys, ue.ctypes.data,
+                                            uf.shape[-1], uf.ctypes.data, ux.ctypes.data, r.ctypes.data,
+                                            s.ctypes.data)
+        if rc:
+            raise ValueError(f"oracle_scores_user_pairs rc={rc}")
+        return r, s

@@ -355,3 +355,46 @@ int oracle_ipnn_extend(int64_t rows, int d0, int n, int d1, int h_is_bf16, const
     }
     return 0;
 }
+
+/*
+ * oracle_scores_user_pairs (NEXT-4, multi-valued ad fields -- tags): scorer A with L given
+ * as its nonzeros, ad by ad: ad a holds the keys ad_keys[ad_key_off[a] .. ad_key_off[a+1]); L is
+ * binary (L_{a,i} in {0,1}), so a key listed twice for one ad counts once.  Otherwise the
+ * same definition as oracle_scores_user: r(a) = <h_u, h_a> + sum_{i: L_{a,i}=1} T_u[i], with
+ * T_u[i] = sum over the user's slots carrying key i of w_i x_i (Eq. 9).
+ */
+int oracle_scores_user_pairs(int64_t n_ads, int d, int emb_is_bf16, const void *ad_emb,
+                             const int64_t *ad_key_off, const int32_t *ad_keys, int n_fields,
+                             const int32_t *field_card, const float *cross_w, int64_t n_keys,
+                             const void *user_emb, int slots, const int32_t *user_feat,
+                             const float *user_x, double *r, double *sigma) {
+    inventory_t iv = {n_ads, d, emb_is_bf16, n_fields, slots, ad_emb, NULL, field_card, cross_w, n_keys};
+    int64_t m = 0;
+    for (int f = 0; f < n_fields; ++f) m += field_card[f];
+    if (m != n_keys) return 1;
+    double *T = (double *)calloc((size_t)(n_keys > 0 ? n_keys : 1), sizeof(double));
+    if (!T) return 3;
+    if (fill_table(&iv, user_feat, user_x, T)) { free(T); return 2; }
+    for (int64_t a = 0; a < n_ads; ++a) {
+        double deep = 0.0, sg = 0.0;
+        for (int j = 0; j < d; ++j) {
+            double p = emb_at(user_emb, emb_is_bf16, 0, d, j) * emb_at(ad_emb, emb_is_bf16, a, d, j);
+            deep += p;
+            sg += fabs(p);
+        }
+        double wide = 0.0;
+        for (int64_t q = ad_key_off[a]; q < ad_key_off[a + 1]; ++q) {
+            int32_t k = ad_keys[q];
+            if (k < 0 || k >= n_keys) { free(T); return 1; }
+            int seen = 0;                            /* L is binary: each key of the ad once */
+            for (int64_t q2 = ad_key_off[a]; q2 < q; ++q2) seen |= ad_keys[q2] == k;
+            if (seen) continue;
+            wide += T[k];
+            sg += fabs(T[k]);
+        }
+        r[a] = deep + wide;
+        if (sigma) sigma[a] = sg;
+    }
+    free(T);
+    return 0;
+}

@@ -121,7 +121,7 @@ struct Ws {
     uint32_t* tend;       // [kMaxCluster][n_tiles]
     uint32_t* gentries;   // [pool] the groups' entry streams (bins claim their ranges):
                           //   ad row << 24 | first pair << 8 | pairs, ordered by (tile, pair-count class)
-    uint32_t* entries;    // [n_bins][bin_cap] level-1 bins (bin_cap = bin_ads * F: an ad has <= F keys)
+    uint32_t* entries;    // [n_bins][bin_cap] level-1 bins (bin_cap = bin_ads * max keys of an ad)
     float* samp;          // [P][n_samp]
     uint64_t* theta;      // [P]
     uint32_t* cand_count; // [P]
@@ -184,11 +184,12 @@ static Layout layout(const ebr_index* idx, int32_t slots, int32_t k) {
     L.cap = cand_cap(idx, k);
     // entry bins of kBinAds ads; a bin's worst case is bin_ads * F entries (an ad has <= F keys)
     L.bin_ads = kBinAds;
-    L.bin_cap = L.bin_ads * idx->n_fields;
+    L.bin_cap = L.bin_ads * std::max<int64_t>(1, idx->max_ad_keys);
     L.n_bins = (idx->n_pad + L.bin_ads - 1) / L.bin_ads;
     // group streams: an (ad, key) entry appears once per group querying the key, so at most
     // min(groups, ...) x F entries per ad; sized for the pass's largest group count
-    L.pool = (int64_t)std::min<int64_t>(kMaxCluster, (P + kGroup - 1) / kGroup) * idx->n_pad * idx->n_fields;
+    L.pool = (int64_t)std::min<int64_t>(kMaxCluster, (P + kGroup - 1) / kGroup) * idx->n_pad *
+             std::max<int64_t>(1, idx->max_ad_keys);
     L.u_cols = idx->d_pad + (int64_t)kMaxHotBlocks * 64 * 2;
     const int64_t Ppad = (int64_t)((P + kGroup - 1) / kGroup) * kGroup;
     const size_t sizes[] = {

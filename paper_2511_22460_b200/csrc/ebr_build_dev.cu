@@ -39,6 +39,28 @@ __global__ void pairs_kernel(const int32_t* __restrict__ feat, int64_t n, int F,
     }
 }
 
+// pairs given ad by ad (multi-valued fields): thread = ad, its keys in order (ads ascending in the
+// pair order, so the stable key sort keeps each list ascending); keys outside [0, M) flagged
+__global__ void pairs_from_lists_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ ad_keys,
+                                        int64_t n, uint32_t M, uint32_t* __restrict__ keys, int32_t* __restrict__ ads,
+                                        uint32_t* err) {
+    for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < n; a += (int64_t)gridDim.x * blockDim.x)
+        for (int64_t q = off[a]; q < off[a + 1]; ++q) {
+            const int32_t k = ad_keys[q];
+            const bool ok = k >= 0 && (uint32_t)k < M;
+            if (!ok) atomicOr(err, 1u);
+            keys[q] = ok ? (uint32_t)k : M;
+            ads[q] = (int32_t)a;
+        }
+}
+
+// after the sort: a (key, ad) pair listed twice for one ad is an error (L is binary)
+__global__ void duplicate_check_kernel(const uint32_t* __restrict__ keys, const int32_t* __restrict__ ads, int64_t N,
+                                       uint32_t M, uint32_t* err) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x + 1; i < N; i += (int64_t)gridDim.x * blockDim.x)
+        if (keys[i] < M && keys[i] == keys[i - 1] && ads[i] == ads[i - 1]) atomicOr(err, 4u);
+}
+
 // postings per key over the sorted keys (equal keys are adjacent: one atomic per run per warp)
 __global__ void count_kernel(const uint32_t* __restrict__ keys, int64_t N, uint32_t M, uint32_t* __restrict__ count) {
     const int lane = threadIdx.x & 31;
@@ -124,12 +146,14 @@ struct Max {
 // Device encoder: d_feat [n][F] on the device; fills idx's posting arrays (and n_chunks, n_words,
 // nnz) and returns the postings per key on the host (hot-key selection).  Host-synchronous.
 ebr_status device_encode(ebr_index* idx, const int32_t* d_feat, const int32_t* d_card, const int32_t* d_base,
-                         cudaStream_t st, std::vector<int64_t>& key_count) {
+                         cudaStream_t st, std::vector<int64_t>& key_count, const int64_t* d_off,
+                         const int32_t* d_keys, int64_t nnz) {
     using namespace build;
     const int64_t n = idx->n_ads;
     const int F = idx->n_fields;
     const uint32_t M = (uint32_t)idx->n_keys;
-    const int64_t N = n * F;
+    const bool lists = d_off != nullptr;                 // (ad, key) pairs given ad by ad
+    const int64_t N = lists ? nnz : n * F;
     std::vector<void*> tmp;
     auto dalloc = [&](size_t bytes) -> void* {
         void* p = nullptr;
@@ -148,7 +172,8 @@ ebr_status device_encode(ebr_index* idx, const int32_t* d_feat, const int32_t* d
     EBR_DALLOC(keys2, uint32_t, N);
     EBR_DALLOC(ads2, int32_t, N);
     const int grid = 4 * idx->sm_count;
-    pairs_kernel<<<grid, 256, 0, st>>>(d_feat, n, F, d_card, d_base, M, keys, ads, err);
+    if (lists) pairs_from_lists_kernel<<<grid, 256, 0, st>>>(d_off, d_keys, n, M, keys, ads, err);
+    else pairs_kernel<<<grid, 256, 0, st>>>(d_feat, n, F, d_card, d_base, M, keys, ads, err);
     EBR_DTRY(cudaGetLastError());
     int bits = 1;
     while (bits < 32 && ((uint64_t)1 << bits) <= (uint64_t)M) ++bits;     // key M (empty) included
@@ -161,6 +186,7 @@ ebr_status device_encode(ebr_index* idx, const int32_t* d_feat, const int32_t* d
     EBR_DTRY(cub::DeviceRadixSort::SortPairs(tsort, tbytes, kb, vb, N, 0, bits, st));
     const uint32_t* skeys = kb.Current();
     const int32_t* sads = vb.Current();
+    if (lists) duplicate_check_kernel<<<grid, 256, 0, st>>>(skeys, sads, N, M, err);
     EBR_DALLOC(count, uint32_t, M + 1);
     EBR_DTRY(cudaMemsetAsync(count, 0, (size_t)(M + 1) * 4, st));
     count_kernel<<<grid, 256, 0, st>>>(skeys, N, M, count);
@@ -230,7 +256,8 @@ ebr_status device_encode(ebr_index* idx, const int32_t* d_feat, const int32_t* d
     release();
 #undef EBR_DTRY
 #undef EBR_DALLOC
-    if (herr & 1u) return set_error(EBR_EINVAL, "ad_feat value outside [-1, V_f)");
+    if (herr & 1u) return set_error(EBR_EINVAL, lists ? "ad key outside [0, n_keys)" : "ad_feat value outside [-1, V_f)");
+    if (herr & 4u) return set_error(EBR_EINVAL, "a key listed twice for one ad (L is binary)");
     if (herr & 2u) return set_error(EBR_EUNSUPPORTED, "a posting list exceeds 2^22 payload words");
     return EBR_OK;
 }

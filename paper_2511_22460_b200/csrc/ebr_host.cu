@@ -85,7 +85,8 @@ KernelTimer::~KernelTimer() {
 
 ebr_status run_small(const QueryArgs& q, int b0, int B);
 ebr_status device_encode(ebr_index* idx, const int32_t* d_feat, const int32_t* d_card, const int32_t* d_base,
-                         cudaStream_t st, std::vector<int64_t>& key_count);
+                         cudaStream_t st, std::vector<int64_t>& key_count, const int64_t* d_off = nullptr,
+                         const int32_t* d_keys = nullptr, int64_t nnz = 0);
 uint32_t workspace_magic(const ebr_index* idx);
 bool batch_eligible(const ebr_index* idx, int32_t batch, int32_t slots, int32_t k);
 int32_t batch_launches(const ebr_index* idx, int32_t batch, int32_t slots);
@@ -274,8 +275,21 @@ __global__ void hot_mask_kernel(const int32_t* __restrict__ feat, int64_t n, int
     mask[a] = make_uint4(m[0], m[1], m[2], m[3]);
 }
 
+__global__ void hot_mask_lists_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ keys, int64_t n,
+                                      const int32_t* __restrict__ hot_slot, uint4* __restrict__ mask) {
+    const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= n) return;
+    uint32_t m[4] = {0u, 0u, 0u, 0u};
+    for (int64_t q = off[a]; q < off[a + 1]; ++q) {
+        const int32_t h = hot_slot[keys[q]];
+        if (h >= 0) m[h >> 5] |= 1u << (h & 31);
+    }
+    mask[a] = make_uint4(m[0], m[1], m[2], m[3]);
+}
+
 static ebr_status build_hot(ebr_index* idx, const std::vector<int64_t>& key_count, const int32_t* ad_feat,
-                            const int32_t* d_feat_all, cudaStream_t stream) {
+                            const int32_t* d_feat_all, cudaStream_t stream, const int64_t* d_off = nullptr,
+                            const int32_t* d_keys = nullptr) {
     int cap = kMaxHot;
     if (const char* e = getenv("EBR_HOT_KEYS")) cap = std::max(0, std::min(kMaxHot, atoi(e)));
     const int64_t M = idx->n_keys, n = idx->n_ads;
@@ -304,6 +318,11 @@ static ebr_status build_hot(ebr_index* idx, const std::vector<int64_t>& key_coun
     EBR_CUDA(cudaMalloc(&idx->hot_mask, mbytes));
     EBR_CUDA(cudaMemsetAsync(idx->hot_mask, 0, mbytes, stream));
     const int F = idx->n_fields;
+    if (d_off) {                // device build from per-ad key lists
+        hot_mask_lists_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(d_off, d_keys, n, idx->hot_slot,
+                                                                              static_cast<uint4*>(idx->hot_mask));
+        return cuda_check(cudaGetLastError(), "hot masks");
+    }
     if (d_feat_all) {           // device build: the values are already on the device
         hot_mask_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(d_feat_all, n, F, idx->field_base, idx->hot_slot,
                                                                         static_cast<uint4*>(idx->hot_mask));
@@ -654,6 +673,7 @@ ebr_status ebr_build_index(const void* ad_emb, ebr_dtype dtype, int64_t ad_begin
         idx->n_chunks = (int64_t)enc.hdr.size() / 2;
         idx->n_words = (int64_t)enc.payload.size() - 2;
         idx->sm_count = prop.multiProcessorCount;
+        idx->max_ad_keys = n_fields;
         idx->encode_ms = enc_ms;
         auto fail = [&](ebr_status s) { ebr_free_index(idx); if (prev >= 0) cudaSetDevice(prev); return s; };
 #define EBR_TRY(call) do { cudaError_t e__ = (call); if (e__ != cudaSuccess) return fail(cuda_check(e__, #call)); } while (0)
@@ -693,10 +713,11 @@ ebr_status ebr_build_index(const void* ad_emb, ebr_dtype dtype, int64_t ad_begin
     }
 }
 
-ebr_status ebr_build_index_device(const void* ad_emb, ebr_dtype dtype, int64_t ad_begin, int64_t ad_end,
-                                  int32_t d, const int32_t* ad_feat, int32_t n_fields,
-                                  const int32_t* field_card, const float* cross_w, int64_t n_keys,
-                                  int device, void* stream_v, ebr_index** out) {
+// device build from ad_feat (one value per field) or from per-ad key lists (ad_key_off/ad_keys)
+static ebr_status build_device(const void* ad_emb, ebr_dtype dtype, int64_t ad_begin, int64_t ad_end, int32_t d,
+                               const int32_t* ad_feat, const int64_t* ad_key_off, const int32_t* ad_keys,
+                               int32_t n_fields, const int32_t* field_card, const float* cross_w, int64_t n_keys,
+                               int device, void* stream_v, ebr_index** out) {
     auto t0 = std::chrono::steady_clock::now();
     if (!out) return set_error(EBR_EINVAL, "out is null");
     *out = nullptr;
@@ -706,7 +727,8 @@ ebr_status ebr_build_index_device(const void* ad_emb, ebr_dtype dtype, int64_t a
     if (dtype != EBR_F32 && dtype != EBR_BF16) return set_error(EBR_EINVAL, "bad dtype");
     if (ad_begin < 0 || ad_begin >= ad_end) return set_error(EBR_EINVAL, "need 0 <= ad_begin < ad_end");
     if (ad_end > 0x7FFFFFFFll) return set_error(EBR_EINVAL, "ad_end > 2^31-1");
-    if (!ad_emb || !ad_feat || !field_card || (!cross_w && n_keys > 0))
+    const bool lists = ad_feat == nullptr;
+    if (!ad_emb || (!ad_feat && (!ad_key_off || !ad_keys)) || !field_card || (!cross_w && n_keys > 0))
         return set_error(EBR_EINVAL, "null input");
     if (n_fields < 0) return set_error(EBR_EINVAL, "n_fields < 0");
     int64_t m = 0;
@@ -742,9 +764,27 @@ ebr_status ebr_build_index_device(const void* ad_emb, ebr_dtype dtype, int64_t a
         idx->n_fields = n_fields;
         idx->n_keys = n_keys;
         idx->sm_count = prop.multiProcessorCount;
+        idx->max_ad_keys = n_fields;
+        int64_t nnz = 0;
+        if (lists) {
+            if (ad_key_off[0] != 0) return set_error(EBR_EINVAL, "ad_key_off[0] != 0");
+            int64_t mx = 0;
+            for (int64_t a = 0; a < n; ++a) {
+                const int64_t c = ad_key_off[a + 1] - ad_key_off[a];
+                if (c < 0) return set_error(EBR_EINVAL, "ad_key_off not ascending");
+                mx = std::max(mx, c);
+            }
+            if (mx > 1024) return set_error(EBR_EUNSUPPORTED, "an ad with more than 1024 keys");
+            nnz = ad_key_off[n];
+            idx->max_ad_keys = (int32_t)std::max<int64_t>(mx, 1);
+        }
         int32_t* d_feat = nullptr;
+        int64_t* d_off = nullptr;
+        int32_t* d_keys = nullptr;
         auto fail = [&](ebr_status s) {
             if (d_feat) cudaFree(d_feat);
+            if (d_off) cudaFree(d_off);
+            if (d_keys) cudaFree(d_keys);
             ebr_free_index(idx);
             if (prev >= 0) cudaSetDevice(prev);
             return s;
@@ -762,7 +802,12 @@ ebr_status ebr_build_index_device(const void* ad_emb, ebr_dtype dtype, int64_t a
         };
         EBR_TRY(cudaStreamSynchronize(stream));        // (A's upload is not part of encode_ms)
         const auto te0 = std::chrono::steady_clock::now();
-        EBR_TRY(upload((void**)&d_feat, ad_feat, (size_t)n * n_fields * 4));
+        if (lists) {
+            EBR_TRY(upload((void**)&d_off, ad_key_off, (size_t)(n + 1) * 8));
+            EBR_TRY(upload((void**)&d_keys, ad_keys, (size_t)std::max<int64_t>(nnz, 1) * 4));
+        } else {
+            EBR_TRY(upload((void**)&d_feat, ad_feat, (size_t)n * n_fields * 4));
+        }
         EBR_TRY(upload((void**)&idx->cross_w, cross_w, (size_t)n_keys * 4));
         std::vector<int32_t> fb(n_fields);
         int64_t acc = 0;
@@ -770,16 +815,21 @@ ebr_status ebr_build_index_device(const void* ad_emb, ebr_dtype dtype, int64_t a
         EBR_TRY(upload((void**)&idx->field_card, field_card, (size_t)n_fields * 4));
         EBR_TRY(upload((void**)&idx->field_base, fb.data(), (size_t)n_fields * 4));
         std::vector<int64_t> key_count;
-        ebr_status st = device_encode(idx, d_feat, idx->field_card, idx->field_base, stream, key_count);
+        ebr_status st = device_encode(idx, d_feat, idx->field_card, idx->field_base, stream, key_count, d_off, d_keys,
+                                      nnz);
         if (st) return fail(st);
         if (dtype == EBR_BF16) {
-            st = build_hot(idx, key_count, ad_feat, d_feat, stream);
+            st = build_hot(idx, key_count, ad_feat, d_feat, stream, d_off, d_keys);
             if (st) return fail(st);
         }
         EBR_TRY(cudaStreamSynchronize(stream));
         idx->encode_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - te0).count();
         cudaFree(d_feat);
+        cudaFree(d_off);
+        cudaFree(d_keys);
         d_feat = nullptr;
+        d_off = nullptr;
+        d_keys = nullptr;
 #undef EBR_TRY
         idx->build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         if (prev >= 0) cudaSetDevice(prev);
@@ -788,6 +838,24 @@ ebr_status ebr_build_index_device(const void* ad_emb, ebr_dtype dtype, int64_t a
     } catch (const std::bad_alloc&) {
         return set_error(EBR_ENOMEM, "host allocation failed");
     }
+}
+
+ebr_status ebr_build_index_device(const void* ad_emb, ebr_dtype dtype, int64_t ad_begin, int64_t ad_end,
+                                  int32_t d, const int32_t* ad_feat, int32_t n_fields,
+                                  const int32_t* field_card, const float* cross_w, int64_t n_keys,
+                                  int device, void* stream_v, ebr_index** out) {
+    if (!ad_feat) return set_error(EBR_EINVAL, "null input");
+    return build_device(ad_emb, dtype, ad_begin, ad_end, d, ad_feat, nullptr, nullptr, n_fields, field_card, cross_w,
+                        n_keys, device, stream_v, out);
+}
+
+ebr_status ebr_build_index_lists(const void* ad_emb, ebr_dtype dtype, int64_t ad_begin, int64_t ad_end, int32_t d,
+                                 const int64_t* ad_key_off, const int32_t* ad_keys, int32_t n_fields,
+                                 const int32_t* field_card, const float* cross_w, int64_t n_keys, int device,
+                                 void* stream_v, ebr_index** out) {
+    if (!ad_key_off || !ad_keys) return set_error(EBR_EINVAL, "null input");
+    return build_device(ad_emb, dtype, ad_begin, ad_end, d, nullptr, ad_key_off, ad_keys, n_fields, field_card,
+                        cross_w, n_keys, device, stream_v, out);
 }
 
 ebr_status ebr_index_export(const ebr_index* idx, int32_t which, void* out_host, int64_t cap_bytes, int64_t* bytes) {

@@ -39,6 +39,7 @@ struct ebr_index {
     double build_ms;
     double encode_ms;               // the inverted-list part of build_ms (ebr_stats)
     int sm_count;
+    int32_t max_ad_keys;            // most keys of one ad (= n_fields for ad_feat builds; key lists: the max)
     void* tmap_A;                   // CUtensorMap (host copy) for the tcgen05 path, or null
 };
 

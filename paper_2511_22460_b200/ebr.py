@@ -34,6 +34,8 @@ EXPORTS = {
                                        ctypes.c_int, _P, ctypes.POINTER(_P)]),
     "ebr_build_index_device": (ctypes.c_int, [_P, ctypes.c_int, _I64, _I64, _I32, _P, _I32, _P, _P, _I64,
                                               ctypes.c_int, _P, ctypes.POINTER(_P)]),
+    "ebr_build_index_lists": (ctypes.c_int, [_P, ctypes.c_int, _I64, _I64, _I32, _P, _P, _I32, _P, _P, _I64,
+                                             ctypes.c_int, _P, ctypes.POINTER(_P)]),
     "ebr_index_export": (ctypes.c_int, [_P, _I32, _P, _I64, ctypes.POINTER(_I64)]),
     "ebr_free_index": (None, [_P]),
     "ebr_workspace_bytes": (_SZ, [_P, _I32, _I32, _I32]),
@@ -209,6 +211,31 @@ class Index:
                                   ctypes.byref(h))
         _check(st, "ebr_build_index_device" if device_build else "ebr_build_index")
         self._h = h
+
+    @classmethod
+    def from_lists(cls, ad_emb, ad_key_off, ad_keys, field_card, cross_w, ad_begin: int = 0, device: int = 0,
+                   stream=None):
+        """Multi-valued ad fields: L given ad by ad as global key lists (ebr_build_index_lists)."""
+        self = cls.__new__(cls)
+        ad_emb = np.ascontiguousarray(ad_emb)
+        self.dtype = BF16 if ad_emb.dtype == np.uint16 else F32
+        if self.dtype == F32:
+            ad_emb = np.ascontiguousarray(ad_emb, np.float32)
+        off = np.ascontiguousarray(ad_key_off, np.int64)
+        keys = np.ascontiguousarray(ad_keys, np.int32)
+        field_card = np.ascontiguousarray(field_card, np.int32)
+        cross_w = np.ascontiguousarray(cross_w, np.float32)
+        n, self.d = ad_emb.shape
+        self.n_fields = field_card.shape[0]
+        self.n_keys = int(field_card.astype(np.int64).sum())
+        self.ad_begin, self.n_ads, self.device = int(ad_begin), int(n), device
+        h = ctypes.c_void_p()
+        _check(_lib.ebr_build_index_lists(_np_ptr(ad_emb), self.dtype, self.ad_begin, self.ad_begin + n, self.d,
+                                          _np_ptr(off), _np_ptr(keys), self.n_fields, _np_ptr(field_card),
+                                          _np_ptr(cross_w), self.n_keys, device, _stream_ptr(stream),
+                                          ctypes.byref(h)), "ebr_build_index_lists")
+        self._h = h
+        return self
 
     @classmethod
     def of(cls, inv, ad_begin: int = 0, device: int = 0, lo: int | None = None, hi: int | None = None,

@@ -273,3 +273,28 @@ def test_ipnn_extend_hand_example_and_numpy():
     hb = np.array([[0x3F80, 0xC000]], np.uint16)                     # 1.0, -2.0
     assert (oracle.ipnn_extend(hb, np.zeros((1, 1), np.float32), np.zeros((1, 1), np.float32))[0, :2]
             == [1.0, -2.0]).all()
+
+
+# ---- NEXT-4: multi-valued ad fields (L given ad by ad as key lists)
+
+def test_pairs_scorer_equals_single_valued_and_hand_example():
+    inv, users = synth.make_config("C1", mode="exact", n_ads=500, batch=2)
+    base = np.concatenate([[0], np.cumsum(inv.field_card)[:-1]]).astype(np.int64)
+    keys = [[int(base[f] + v) for f, v in enumerate(row) if v >= 0] for row in inv.ad_feat]
+    off = np.concatenate([[0], np.cumsum([len(k) for k in keys])]).astype(np.int64)
+    flat = np.array([k for ks in keys for k in ks], np.int32)
+    a, p = oracle.Oracle.of(inv), oracle.OraclePairs(inv.ad_emb, off, flat, inv.field_card, inv.cross_w)
+    for b in range(2):
+        ra, sa = a.scores(users.user_emb[b], users.user_feat[b], users.user_x[b])
+        rp, sp = p.scores(users.user_emb[b], users.user_feat[b], users.user_x[b])
+        assert (ra == rp).all() and (sa == sp).all()
+    # hand example: 2 fields (V = 2, 3), ad 0 holds keys {0, 2, 3} (a tag field with two values),
+    # ad 1 holds key 3 twice (binary L: once); user: field 1 values 0 and 1 -> keys 2, 3
+    cards = np.array([2, 3], np.int32)
+    w = np.array([1, 1, 0.5, 0.25, 9], np.float32)
+    po = oracle.OraclePairs(np.zeros((2, 4), np.float32), np.array([0, 3, 5]), np.array([0, 2, 3, 3, 3], np.int32),
+                            cards, w)
+    uf = np.array([[-1, -1], [0, 1]], np.int32)
+    ux = np.array([[0, 0], [2, 4]], np.float32)
+    r, _ = po.scores(np.zeros(4, np.float32), uf, ux)
+    assert (r == [0.5 * 2 + 0.25 * 4, 0.25 * 4]).all()
