@@ -62,11 +62,23 @@ constexpr int kMaxHotBlocks = 2;     // hot K blocks of 64 keys (the index keeps
 constexpr int kPairUBits = 7;        // cold pair = w~ 2^S (25-bit two's complement) << 7 | user in the group
 constexpr int kPairWMax = 24;        // |w~ 2^S| < 2^24
 constexpr int kMaxUnion = 1 << 14;   // union key slots per pass (14 bits in the level-1 bin entries)
-constexpr int kBinAds = 1024;        // ads per entry bin (8 tiles)
-constexpr int kOrderStage = 16384;   // bin entries staged in shared memory by entry_order (64 KB)
+#ifndef EBR_BIN_ADS
+#define EBR_BIN_ADS 1024
+#endif
+constexpr int kBinAds = EBR_BIN_ADS;  // ads per entry bin (8 tiles at 1024)
+#ifndef EBR_ORDER_STAGE
+#define EBR_ORDER_STAGE 16384
+#endif
+constexpr int kOrderStage = EBR_ORDER_STAGE;   // bin entries staged in shared memory by entry_order
 constexpr int kClasses = 4;          // pair-count classes of an entry (1, 2, 3-4, 5+ pairs): a tile's
                                      // entries are ordered by class so a warp's entries carry similar work
-constexpr int kOrderThreads = 512;
+#ifndef EBR_ORDER_THREADS
+#define EBR_ORDER_THREADS 1024
+#endif
+#ifndef EBR_BIN_GRID
+#define EBR_BIN_GRID 8
+#endif
+constexpr int kOrderThreads = EBR_ORDER_THREADS;
 constexpr int kPlanThreads = 1024;
 constexpr uint32_t kFlagShort = 1u, kFlagOverflow = 2u, kFlagRaise = 4u;   // uflags; overflow users carry their dense slot << 8
 constexpr uint32_t kFlagAny = kFlagShort | kFlagOverflow | kFlagRaise;
@@ -378,29 +390,45 @@ __global__ void __launch_bounds__(kPlanThreads) plan_b_kernel(PlanArgs a, Ws ws)
     uint32_t base[kPlanNV];
 #pragma unroll
     for (int i = 0; i < kPlanNV; ++i) base[i] = sW[warp][i] + incl[i] - v[i];
-    for (int64_t t = t0; t < t1; ++t) {
-        const uint32_t key1 = ws.hkey[t];
-        if (!key1) continue;
-        const uint32_t key = key1 - 1u, sl = base[0];
-        const uint32_t c0 = a.key_chunk_off[key], c1 = a.key_chunk_off[key + 1];
-        ws.hslot[t] = sl;
-        ws.ukey[sl] = key;
-        ws.uc0[sl] = c0;
-        ws.uc1[sl] = c1;
-        ws.ukwb[sl] = a.key_word_off[key];
-        ws.uchunk[sl] = base[1];
-        uint32_t cls = 0;
-        for (int g = 0; g < kMaxCluster; ++g) {
-            const uint32_t c = ws.hcnt[t * kMaxCluster + g];          // <= kGroup users
-            ws.pinfo[(size_t)g * a.NU + sl] = c ? (base[2 + g] << 8) | c : 0u;
-            ws.hpair[t * kMaxCluster + g] = base[2 + g];
-            base[2 + g] += c;
-            if (c) cls |= (1u + pair_class(c)) << (3 * g);
+    // (8 positions per round, their loads in flight together, as in the counting pass)
+    for (int64_t tb = t0; tb < t1; tb += 8) {
+        uint32_t key1[8], c0[8], c1[8], kw[8], hc[8][kMaxCluster];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) key1[j] = tb + j < t1 ? ws.hkey[tb + j] : 0u;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint32_t key = key1[j] ? key1[j] - 1u : 0u;
+            c0[j] = key1[j] ? a.key_chunk_off[key] : 0u;
+            c1[j] = key1[j] ? a.key_chunk_off[key + 1] : 0u;
+            kw[j] = key1[j] ? a.key_word_off[key] : 0u;
+#pragma unroll
+            for (int g = 0; g < kMaxCluster; ++g) hc[j][g] = key1[j] ? ws.hcnt[(tb + j) * kMaxCluster + g] : 0u;
         }
-        ws.ucls[sl] = cls;
-        base[0] += 1u;
-        base[1] += c1 - c0;
-        ws.hkey[t] = 0u;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (!key1[j]) continue;
+            const int64_t t = tb + j;
+            const uint32_t sl = base[0];
+            ws.hslot[t] = sl;
+            ws.ukey[sl] = key1[j] - 1u;
+            ws.uc0[sl] = c0[j];
+            ws.uc1[sl] = c1[j];
+            ws.ukwb[sl] = kw[j];
+            ws.uchunk[sl] = base[1];
+            uint32_t cls = 0;
+#pragma unroll
+            for (int g = 0; g < kMaxCluster; ++g) {
+                const uint32_t c = hc[j][g];          // <= kGroup users
+                ws.pinfo[(size_t)g * a.NU + sl] = c ? (base[2 + g] << 8) | c : 0u;
+                ws.hpair[t * kMaxCluster + g] = base[2 + g];
+                base[2 + g] += c;
+                if (c) cls |= (1u + pair_class(c)) << (3 * g);
+            }
+            ws.ucls[sl] = cls;
+            base[0] += 1u;
+            base[1] += c1[j] - c0[j];
+            ws.hkey[t] = 0u;
+        }
     }
     __syncthreads();
     if (tid == 0) {
@@ -535,7 +563,7 @@ __global__ void __launch_bounds__(kBinThreads) entry_bin_kernel(EntryArgs e, Ws 
 // Level 2: CTA = bin (8 tiles).  The bin is staged in shared memory when it fits (the common
 // case), else read twice from L2: count per (group, tile, class), scan, claim the groups' ranges
 // of the pool, scatter.
-constexpr int kOrderCells = (kBinAds / kTileM) * kClasses;   // counters per group (= 32: one per lane)
+constexpr int kOrderCells = (kBinAds / kTileM) * kClasses;   // counters per group
 
 __global__ void __launch_bounds__(kOrderThreads) entry_order_kernel(EntryArgs e, Ws ws) {
     extern __shared__ uint32_t smem_u[];
@@ -563,26 +591,34 @@ __global__ void __launch_bounds__(kOrderThreads) entry_order_kernel(EntryArgs e,
     // warp g: exclusive scan of group g's counters (lane = tile * kClasses + class), its range
     // claimed from the pool, the bounds of the bin's tiles
     const int warp = tid >> 5, lane = tid & 31;
-    static_assert(kOrderCells == 32, "one counter per lane");
+    constexpr int kCPL = kOrderCells / 32;                      // cells per lane
+    static_assert(kOrderCells % 32 == 0, "whole cells per lane");
     if (warp < G) {
-        const uint32_t x = cnt[warp * kOrderCells + lane];
-        uint32_t incl = x;
+        uint32_t* c = cnt + warp * kOrderCells;
+        uint32_t x[kCPL], run = 0;
+#pragma unroll
+        for (int k = 0; k < kCPL; ++k) { x[k] = c[lane * kCPL + k]; run += x[k]; }
+        uint32_t incl = run;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(FULL, incl, o);
             if (lane >= o) incl += y;
         }
         const uint32_t tot = __shfl_sync(FULL, incl, 31);
-        cnt[warp * kOrderCells + lane] = incl - x;
+        uint32_t acc = incl - run;
+#pragma unroll
+        for (int k = 0; k < kCPL; ++k) { c[lane * kCPL + k] = acc; acc += x[k]; }
         uint32_t base = 0;
         if (lane == 0) base = tot ? atomicAdd(&ws.header[6], tot) : 0u;
         base = __shfl_sync(FULL, base, 0);
         if (lane == 0) sBase[warp] = base;
-        const int tl = lane / kClasses;                           // the bin's tile of this lane's cell
-        const int64_t ti = (int64_t)r * (kBinAds / kTileM) + tl;  // global tile
-        const uint32_t tb = __shfl_sync(FULL, incl - x, tl * kClasses);
-        const uint32_t te = __shfl_sync(FULL, incl, tl * kClasses + kClasses - 1);
-        if (lane % kClasses == 0 && ti < (int64_t)e.n_tiles) {
+        __syncwarp();
+        constexpr int tpb = kBinAds / kTileM;                      // tiles per bin
+        for (int tl = lane; tl < tpb; tl += 32) {
+            const int64_t ti = (int64_t)r * tpb + tl;               // global tile
+            if (ti >= (int64_t)e.n_tiles) break;
+            const uint32_t tb = c[tl * kClasses];
+            const uint32_t te = tl + 1 < tpb ? c[(tl + 1) * kClasses] : tot;
             ws.tbeg[(size_t)warp * e.n_tiles + ti] = base + tb;
             ws.tend[(size_t)warp * e.n_tiles + ti] = base + te;
         }
@@ -1544,7 +1580,7 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
         trace(q.stream, "plan_b");
         plan_c_kernel<<<std::max(pgrid, 2 * idx->sm_count), 256, 0, q.stream>>>(pa, ws);
         trace(q.stream, "plan_c");
-        entry_bin_kernel<<<8 * idx->sm_count, kBinThreads, 0, q.stream>>>(ea, ws);
+        entry_bin_kernel<<<EBR_BIN_GRID * idx->sm_count, kBinThreads, 0, q.stream>>>(ea, ws);
         trace(q.stream, "entry_bin");
         entry_order_kernel<<<(unsigned)L.n_bins, kOrderThreads, kOrderStage * 4, q.stream>>>(ea, ws);
         trace(q.stream, "entry_order");
