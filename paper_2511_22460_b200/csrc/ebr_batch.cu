@@ -664,7 +664,9 @@ struct GemmParams {
     const void* A;          // the index's A [n_pad][d_pad] bf16 (L2 prefetch)
     Ws ws;
     uint32_t* err;
-    int diag;               // A/B experiments (EBR_DIAG): 1 skip the cold scatter, 2 skip the epilogue work
+    int diag;               // A/B experiments (EBR_DIAG): 1 skip the cold scatter, 2 skip the epilogue work,
+                            // 32 / 64 no TMEM load / store, 1024 no MMA issued, 2048 no one-hot writes,
+                            // 32768 no A loads (results are wrong under any of these)
     int NU;                 // union slot capacity of the pass (toff row length - 1)
     int gcap;               // pair capacity of a group's list
     int n_tiles_all;        // tiles of the inventory (row length of the group streams' tile bounds)
@@ -874,6 +876,7 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                                              tc::cluster_addr(&full[slot], 0), pol);
                         continue;
                     }
+                    if (p.diag & 32768) { mbar_arrive(&full[slot]); continue; }   // (A/B: no A loads)
                     mbar_arrive_expect_tx(&full[slot], (uint32_t)kBlockBytes);
                     if (csize == 1 || (p.diag & 8))
                         tc::tma_load_2d_hint(sRing + (size_t)slot * kBlockBytes, &tmA, kb * kBlockK, row0, &full[slot], pol);
@@ -929,7 +932,7 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                             if (pair) tc::umma2_f16_ss(d_tmem, da0 + (uint64_t)(k * 2), db0 + (uint64_t)(k * 2), idb, 1u);
                             else tc::umma_f16(d_tmem, da0 + (uint64_t)(k * 2), db0 + (uint64_t)(k * 2), idb, 1u);
                         }
-                    } else {
+                    } else if (!(p.diag & 1024)) {                // (A/B: no MMA issued)
 #pragma unroll
                         for (int k = 0; k < kBlockK / 16; ++k)
                             mma(d_tmem, tmem_base + (uint32_t)(kb * 32 + k * 8), db0 + (uint64_t)(k * 2), idb);
@@ -943,7 +946,7 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                     { EBR_PROF_T0; pwait(&hfull[hs], (hb / kHotStages) & 1); EBR_PROF_ADD(2); }
                     tc::fence_after();
                     const uint64_t db0 = tc::sdesc_sw128(sHot + (size_t)hs * sb);
-                    for (int pc = 0; pc < p.pieces; ++pc) {
+                    for (int pc = 0; pc < ((p.diag & 1024) ? 0 : p.pieces); ++pc) {
                         const uint32_t ac = (uint32_t)(hot_col0 + 32 * (h * p.pieces + pc));
 #pragma unroll
                         for (int k = 0; k < kBlockK / 16; ++k)
@@ -982,7 +985,7 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                 for (int h = 0; h < p.n_hb; ++h, ++hb) {
                     const uint32_t hs = hb % kHotStages, round = hb / kHotStages;
                     if (round > 0) { EBR_PROF_T0; crit_wait(&hempty[hs], (round - 1) & 1, p.diag); if (hw == 0) EBR_PROF_ADD(3); }
-                    for (int rr = 0; rr < nrows; ++rr) {
+                    for (int rr = 0; rr < ((p.diag & 2048) ? 0 : nrows); ++rr) {   // (A/B: no one-hot writes)
                         const int row = hw + rr * 64;
                         const uint64_t bits = h == 0 ? ((uint64_t)hm[rr].y << 32 | hm[rr].x)
                                                      : ((uint64_t)hm[rr].w << 32 | hm[rr].z);
@@ -1181,11 +1184,16 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                         }
                     }
                 } else {
-                    uint32_t pass = 0;
+                    // early out on the chunk's maximum (almost every chunk has no candidate)
+                    float mx = __uint_as_float(r[0]);
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) pass |= (__uint_as_float(r[j]) >= thS ? 1u : 0u) << j;
-                    pass &= nval >= 32 ? 0xFFFFFFFFu : ((1u << nval) - 1u);
-                    if (!uok) pass = 0u;
+                    for (int j = 1; j < 32; ++j) mx = fmaxf(mx, __uint_as_float(r[j]));
+                    uint32_t pass = 0;
+                    if (mx >= thS && uok) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) pass |= (__uint_as_float(r[j]) >= thS ? 1u : 0u) << j;
+                        pass &= nval >= 32 ? 0xFFFFFFFFu : ((1u << nval) - 1u);
+                    }
                     // exact key compare, then this user's appends (one atomic per thread and chunk)
                     uint32_t take = 0;
                     if (pass) {
