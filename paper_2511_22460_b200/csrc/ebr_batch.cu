@@ -1526,8 +1526,10 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
     if (!encode_2d_16(&tmA, idx->A, (uint64_t)idx->d_pad, (uint64_t)idx->n_pad, kBlockK, kTileM) ||
         !encode_2d_16(&tmA64, idx->A, (uint64_t)idx->d_pad, (uint64_t)idx->n_pad, kBlockK, kTileM / 2))
         return set_error(EBR_ECUDA, "cuTensorMapEncodeTiled(A) failed");
-    // CTA-pair MMA for 2-group passes: opt-in (EBR_PAIR=1) until it measures faster
-    static const bool use_pair = getenv("EBR_PAIR") != nullptr && atoi(getenv("EBR_PAIR")) != 0;
+    // CTA-pair MMA for 2-group passes (3.00 vs 3.14 ms on C3); EBR_PAIR=0 selects the
+    // single-CTA kernel (read per call, so a test can exercise both)
+    const char* pair_env = getenv("EBR_PAIR");
+    const bool use_pair = pair_env == nullptr || atoi(pair_env) != 0;
     // kernel attributes: set once per process (values fixed by the build)
     static std::once_flag attr_once;
     static cudaError_t attr_err = cudaSuccess;
