@@ -9,12 +9,23 @@ for cfg in sys.argv[1:] or ["C3"]:
     inv, _ = synth.make_config(cfg, mode="real", batch=1)
     t = time.perf_counter(); h = ebr.Index.of(inv); th = time.perf_counter() - t
     ebr.Index.of(inv, device_build=True).close()          # warm-up (CUDA context, CUB)
-    t = time.perf_counter(); d = ebr.Index.of(inv, device_build=True); td = time.perf_counter() - t
+    # three timed device builds (the wall time includes cudaMalloc of the GB-sized temporaries and
+    # the pageable upload of ad_feat, both of which vary run to run): min and median reported
+    runs = []
+    for r in range(3):
+        t = time.perf_counter(); d = ebr.Index.of(inv, device_build=True); td = time.perf_counter() - t
+        runs.append((td, d.stats()["encode_ms"]))
+        if r < 2:
+            d.close()
+    walls = sorted(x[0] for x in runs)
+    encs = sorted(x[1] for x in runs)
     same = all((h.export(w) == d.export(w)).all() for w in range(6))
     st = d.stats()
     print(json.dumps({"config": cfg, "n_ads": inv.n_ads, "nnz": st["nnz"], "chunks": st["chunks"],
-                      "host_build_ms": th * 1e3, "device_build_ms": td * 1e3,
+                      "host_build_ms": th * 1e3, "device_build_ms": walls[1] * 1e3,
+                      "device_build_ms_min": walls[0] * 1e3,
                       "host_reported_ms": h.stats()["build_ms"], "device_reported_ms": st["build_ms"],
-                      "host_encode_ms": h.stats()["encode_ms"], "device_encode_ms": st["encode_ms"],
+                      "host_encode_ms": h.stats()["encode_ms"], "device_encode_ms": encs[1],
+                      "device_encode_ms_min": encs[0],
                       "bit_identical": bool(same)}), flush=True)
     h.close(); d.close()
