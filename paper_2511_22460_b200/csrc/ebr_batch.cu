@@ -892,7 +892,7 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
             }
         }
     } else if (warp == 1) {
-        if (lane == 0 && (!pair || rank == 0)) {   // (pair: the leader issues for both CTAs)
+        if (!pair || rank == 0) {   // (pair: the leader issues for both CTAs; the whole warp, one elected lane issues)
             // ---------------- MMA issuer ----------------
             // The accumulator stage already holds the tile's cold wide term (stored by the wide
             // warps), so every MMA accumulates: D = cold + U A^T + U_hot (one-hot)^T.
@@ -903,13 +903,13 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                 if (pair) tc::mbar_wait_cluster(bar, parity);
                 else crit_wait(bar, parity, p.diag);
             };
-            auto mma = [&](uint32_t d, uint32_t a, uint64_t b, uint32_t id) {
-                if (pair) tc::umma2_f16_ts(d, a, b, id, 1u);
-                else tc::umma_f16_ts(d, a, b, id, 1u);
+            auto mma4 = [&](uint32_t d, uint32_t a, uint64_t b, uint32_t id) {   // one 64-wide K block
+                if (pair) tc::umma2_f16_ts_x4_e(d, a, b, id, 1u);
+                else tc::umma_f16_ts_x4_e(d, a, b, id, 1u);
             };
             auto commit_all = [&](uint64_t* bar) {       // the arrival every consumer of the stage waits for
-                if (pair) tc::umma2_commit_mc(bar, (uint16_t)3);
-                else tc::umma_commit(bar);
+                if (pair) tc::umma2_commit_mc_e(bar, (uint16_t)3);
+                else tc::umma_commit_e(bar);
             };
             pwait(aready, 0);                               // users' A operand in TMEM (both CTAs)
             tc::fence_after();
@@ -917,40 +917,37 @@ score_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
             uint32_t gb = 0, hb = 0;
             for (int t = (int)cid; t < p.n_tiles; t += (int)ncl, ++it) {
                 const int st = it % nst;
-                { EBR_PROF_T0; pwait(&wready[st], (it / nst) & 1); EBR_PROF_ADD(1); }
+                { EBR_PROF_T0; pwait(&wready[st], (it / nst) & 1); if (lane == 0) EBR_PROF_ADD(1); }
                 tc::fence_after();
                 const uint32_t d_tmem = tmem_base + (uint32_t)(a_cols + st * kTileM);
                 for (int kb = 0; kb < p.n_kb; ++kb, ++gb) {
                     const uint32_t slot = gb % nring;
-                    if (!(p.diag & 128)) { EBR_PROF_T0; crit_wait(&full[slot], (gb / nring) & 1, p.diag); EBR_PROF_ADD(2); }
+                    if (!(p.diag & 128)) { EBR_PROF_T0; crit_wait(&full[slot], (gb / nring) & 1, p.diag); if (lane == 0) EBR_PROF_ADD(2); }
                     tc::fence_after();
                     const uint64_t db0 = tc::sdesc_sw128(sRing + (size_t)slot * sb);
                     if (p.deep_smem) {
                         const uint64_t da0 = tc::sdesc_sw128(sUser + (size_t)kb * kBlockBytes);
 #pragma unroll
                         for (int k = 0; k < kBlockK / 16; ++k) {
-                            if (pair) tc::umma2_f16_ss(d_tmem, da0 + (uint64_t)(k * 2), db0 + (uint64_t)(k * 2), idb, 1u);
-                            else tc::umma_f16(d_tmem, da0 + (uint64_t)(k * 2), db0 + (uint64_t)(k * 2), idb, 1u);
+                            if (pair) tc::umma2_f16_ss_e(d_tmem, da0 + (uint64_t)(k * 2), db0 + (uint64_t)(k * 2), idb, 1u);
+                            else tc::umma_f16_e(d_tmem, da0 + (uint64_t)(k * 2), db0 + (uint64_t)(k * 2), idb, 1u);
                         }
                     } else if (!(p.diag & 1024)) {                // (A/B: no MMA issued)
-#pragma unroll
-                        for (int k = 0; k < kBlockK / 16; ++k)
-                            mma(d_tmem, tmem_base + (uint32_t)(kb * 32 + k * 8), db0 + (uint64_t)(k * 2), idb);
+                        static_assert(kBlockK == 64, "mma4 issues four K=16 steps");
+                        mma4(d_tmem, tmem_base + (uint32_t)(kb * 32), db0, idb);
                     }
-                    if (pair) tc::umma2_commit_mc(&empty[slot], (uint16_t)3);
-                    else if (csize == 1 || (p.diag & 8)) tc::umma_commit(&empty[slot]);
-                    else tc::umma_commit_mc(&empty[slot], mc_mask);
+                    if (pair) tc::umma2_commit_mc_e(&empty[slot], (uint16_t)3);
+                    else if (csize == 1 || (p.diag & 8)) tc::umma_commit_e(&empty[slot]);
+                    else tc::umma_commit_mc_e(&empty[slot], mc_mask);
                 }
                 for (int h = 0; h < p.n_hb; ++h, ++hb) {
                     const uint32_t hs = hb % kHotStages;
-                    { EBR_PROF_T0; pwait(&hfull[hs], (hb / kHotStages) & 1); EBR_PROF_ADD(2); }
+                    { EBR_PROF_T0; pwait(&hfull[hs], (hb / kHotStages) & 1); if (lane == 0) EBR_PROF_ADD(2); }
                     tc::fence_after();
                     const uint64_t db0 = tc::sdesc_sw128(sHot + (size_t)hs * sb);
                     for (int pc = 0; pc < ((p.diag & 1024) ? 0 : p.pieces); ++pc) {
                         const uint32_t ac = (uint32_t)(hot_col0 + 32 * (h * p.pieces + pc));
-#pragma unroll
-                        for (int k = 0; k < kBlockK / 16; ++k)
-                            mma(d_tmem, tmem_base + ac + (uint32_t)(k * 8), db0 + (uint64_t)(k * 2), idh);
+                        mma4(d_tmem, tmem_base + ac, db0, idh);
                     }
                     commit_all(&hempty[hs]);
                 }

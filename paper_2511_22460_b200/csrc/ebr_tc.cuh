@@ -258,6 +258,73 @@ __device__ __forceinline__ void umma2_commit_mc(uint64_t* bar, uint16_t mask) {
         "h"(mask)
         : "memory");
 }
+// ---- warp-wide issue: the whole (converged) warp executes these, one elected lane issues.  The
+// operands are warp-uniform, so the compiler keeps them in uniform registers (no per-instruction
+// loop over the lanes' values, as a single-lane branch needs) ----
+#define EBR_ELECT_MMA(shape_ops)                                                    \
+    "{\n\t.reg .pred pa, pe;\n\t"                                              \
+    "elect.sync _|pe, 0xffffffff;\n\t"                                          \
+    "setp.ne.b32 pa, %4, 0;\n\t"                                                \
+    "@pe " shape_ops ";\n\t}"
+__device__ __forceinline__ void umma_f16_e(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(EBR_ELECT_MMA("tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, pa")
+                 ::"r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_f16_ts_e(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
+                                              uint32_t acc) {
+    asm volatile(EBR_ELECT_MMA("tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, pa")
+                 ::"r"(tmem_d), "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma2_f16_ts_e(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
+                                               uint32_t acc) {
+    asm volatile(EBR_ELECT_MMA("tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, pa")
+                 ::"r"(tmem_d), "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc), "r"(0u));
+}
+__device__ __forceinline__ void umma2_f16_ss_e(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(EBR_ELECT_MMA("tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, pa")
+                 ::"r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+#undef EBR_ELECT_MMA
+// one 64-wide K block = four K=16 MMAs (A columns +8, B descriptor +2 per step: 32 bytes of the
+// 128B-swizzled K-major tile) under ONE election: the per-MMA issue cost of the single issuing
+// lane is what bounds the fused kernel
+#define EBR_ELECT_MMA_X4(op, dis)                                                                \
+    "{\n\t.reg .pred pa, pe;\n\t.reg .b32 a1, a2, a3;\n\t.reg .b64 b1, b2, b3;\n\t"        \
+    "elect.sync _|pe, 0xffffffff;\n\t"                                                     \
+    "setp.ne.b32 pa, %4, 0;\n\t"                                                           \
+    "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t"                   \
+    "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"                      \
+    "@pe " op " [%0], [%1], %2, %3," dis " pa;\n\t"                                        \
+    "@pe " op " [%0], [a1], b1, %3," dis " 1;\n\t"                                         \
+    "@pe " op " [%0], [a2], b2, %3," dis " 1;\n\t"                                         \
+    "@pe " op " [%0], [a3], b3, %3," dis " 1;\n\t}"
+__device__ __forceinline__ void umma_f16_ts_x4_e(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
+                                                 uint32_t acc) {
+    asm volatile(EBR_ELECT_MMA_X4("tcgen05.mma.cta_group::1.kind::f16", "")
+                 ::"r"(tmem_d), "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma2_f16_ts_x4_e(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
+                                                  uint32_t acc) {
+    asm volatile(EBR_ELECT_MMA_X4("tcgen05.mma.cta_group::2.kind::f16", " {%5, %5, %5, %5, %5, %5, %5, %5},")
+                 ::"r"(tmem_d), "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc), "r"(0u));
+}
+#undef EBR_ELECT_MMA_X4
+
+__device__ __forceinline__ void umma_commit_e(uint64_t* bar) {
+    asm volatile("{\n\t.reg .pred pe;\n\telect.sync _|pe, 0xffffffff;\n\t"
+                 "@pe tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}"
+                 ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void umma_commit_mc_e(uint64_t* bar, uint16_t mask) {
+    asm volatile("{\n\t.reg .pred pe;\n\telect.sync _|pe, 0xffffffff;\n\t"
+                 "@pe tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
+                 ::"r"(smem_u32(bar)), "h"(mask) : "memory");
+}
+__device__ __forceinline__ void umma2_commit_mc_e(uint64_t* bar, uint16_t mask) {
+    asm volatile("{\n\t.reg .pred pe;\n\telect.sync _|pe, 0xffffffff;\n\t"
+                 "@pe tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
+                 ::"r"(smem_u32(bar)), "h"(mask) : "memory");
+}
 // the shared::cluster address of this CTA's shared variable `p` in CTA `rank` of the cluster
 __device__ __forceinline__ uint32_t cluster_addr(const void* p, uint32_t rank) {
     uint32_t r;
