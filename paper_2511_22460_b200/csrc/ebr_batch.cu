@@ -1509,8 +1509,10 @@ ebr_status run_batch(const QueryArgs& q, void* region, uint32_t* err_word) {
     // >= 2 accumulator stages of 128 columns; hot blocks are dropped until both fit
     int stages = 0, acc_stages = 0;
     // the users' deep operand in shared memory (SS MMA, a third TMEM accumulator stage): opt-in
-    // (EBR_DEEP_SMEM=1); measured no faster (the ring loses two stages), DESIGN.md §6.2
-    static const bool deep_smem = getenv("EBR_DEEP_SMEM") != nullptr && atoi(getenv("EBR_DEEP_SMEM")) != 0;
+    // (EBR_DEEP_SMEM=1, read per call so a test can exercise it); measured no faster (the ring loses
+    // two stages), DESIGN.md §6.2
+    const char* ds_env = getenv("EBR_DEEP_SMEM");
+    const bool deep_smem = ds_env != nullptr && atoi(ds_env) != 0;
     for (; tu.n_hb >= 0; --tu.n_hb) {
         acc_stages = std::min(kMaxAccStages, (512 - 32 * ((deep_smem ? 0 : n_kb) + tu.n_hb * tu.pieces)) / kTileM);
         if (acc_stages < 2) continue;

@@ -58,19 +58,23 @@ def test_batch_equals_latency_path(ebr):
     assert (ids_b == ids_s).all() and (sc_b == sc_s).all()
 
 
-@pytest.mark.parametrize("b", [200, 256])
-def test_single_cta_kernel_equals_pair(ebr, b):
+@pytest.mark.parametrize("b,env", [(200, {"EBR_PAIR": "0"}), (256, {"EBR_PAIR": "0"}),
+                                   (256, {"EBR_DEEP_SMEM": "1"}), (96, {"EBR_DEEP_SMEM": "1"}),
+                                   (256, {"EBR_PAIR": "0", "EBR_DEEP_SMEM": "1"})])
+def test_kernel_variants_equal_default(ebr, b, env):
     """Two-group passes run the CTA-pair kernel (tcgen05.mma.cta_group::2, M = 256 users) by default;
-    EBR_PAIR=0 selects the single-CTA kernel (two clustered CTAs, one M = 128 MMA each).  Both equal
-    the oracle bit for bit in exact mode, hence each other."""
+    EBR_PAIR=0 selects the single-CTA kernel (two clustered CTAs, one M = 128 MMA each) and
+    EBR_DEEP_SMEM=1 the users' deep operand in shared memory (SS MMA, three TMEM stages).  Every
+    variant equals the oracle bit for bit in exact mode, hence the default."""
     inv, users = synth.make_config("C3", mode="exact", n_ads=70_000, batch=b)
     idx = ebr.Index.of(inv)
     (ids_p, sc_p), _ = run(ebr, idx, users, 150)
-    os.environ["EBR_PAIR"] = "0"
+    os.environ.update(env)
     try:
         (ids_s, sc_s), ws = run(ebr, idx, users, 150)
     finally:
-        del os.environ["EBR_PAIR"]
+        for k_ in env:
+            del os.environ[k_]
     assert (ids_p == ids_s).all() and (sc_p == sc_s).all()
     assert check_all(oracle.Oracle.of(inv), users, ids_s, sc_s, 150, "exact") == 0
     assert ebr.query_error(ws) == 0
